@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Q-ARVD hot path (driver contract: one JSON line on rank 0).
+
+Headline workload (BASELINE.json configs[1]): the FFN of one Wan-1.3B block on
+one 3-latent-frame chunk, M = 4680 tokens: ffn.0 1536->8960 (dual-scale, K_o=32,
+GELU fused in the epilogue) then ffn.2 8960->1536 (dual-scale, K_o=192),
+each = K1 per-token INT8 quantize (+ permutation) -> K2 tcgen05 kind::i8
+dual-accumulator GEMM with the fused dequant epilogue.  One step = one FFN
+forward over one chunk.  Metric: dual-scale INT8 linear TOPS (2*M*N*K per GEMM).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_TOKENS = 4680
+DIM = 1536
+FFN = 8960
+METRIC = "dual-scale INT8 linear TOPS (% INT8 TC peak); calibration layers/sec at 1-8 GPU"
+WORKLOAD = "ffn_up_down_1536x8960x1536_M4680"
+INT8_DATASHEET_TOPS = 4500.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_ffn_layers(torch, seed=1):
+    """Synthetic Wan-shaped ffn.0 / ffn.2 with detected outliers (K3) and prepared weights (K5)."""
+    import paper_2605_21072_b200 as qb
+    from paper_2605_21072_b200 import engine, synth
+
+    specs = [s for s in synth.wan_registry(blocks=1) if s.name.startswith("block0.ffn")]
+    layers = []
+    for spec in specs:
+        w = synth.synth_weight(spec, seed=seed)
+        rep = qb.analyze_layer(spec.name, w)
+        plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+        layers.append((spec, w, engine.prepare_weights(spec.name, w, plan), rep))
+    return layers
+
+
+def int8_peak_cublas(torch):
+    """Measured INT8 tensor throughput of cuBLASLt (torch._int_mm), for the roofline denominator."""
+    try:
+        n = 8192
+        a = torch.randint(-127, 127, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 127, (n, n), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def cublas_bf16_ffn_ms(torch, x, w0, w2, iters=10):
+    """Same-shape cuBLAS bf16 GEMMs (x @ w0^T, gelu, @ w2^T): the north-star comparison."""
+    import torch.nn.functional as F
+
+    for _ in range(3):
+        F.linear(F.gelu(F.linear(x, w0)), w2)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ts = []
+    gemm_ts = []
+    for _ in range(iters):
+        flush.fill_(1)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record()
+        u = F.linear(x, w0)
+        e[1].record()
+        u = F.gelu(u)
+        e[2].record()
+        F.linear(u, w2)
+        e[3].record()
+        e[3].synchronize()
+        ts.append(e[0].elapsed_time(e[3]))
+        gemm_ts.append(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]))
+    return float(np.median(ts)), float(np.median(gemm_ts))
+
+
+def reference_ffn_sample(layers_host, x64, u64, threads, rows):
+    """Time the reference CPU path (oracle/_ref = compiled reference sources) for `rows` rows
+    of both FFN linears: permute -> kernel A -> kernel B (engine.cpp:137-139)."""
+    import oracle
+
+    r = oracle.ref()
+    r.ref_set_threads(threads)
+    total = 0.0
+    ops = 0.0
+    for (spec, wq32, perm, n_o, so, sn, s_x), xin in zip(layers_host, (x64, u64)):
+        xs = np.ascontiguousarray(xin[:rows])
+        secs = r.ref_time_linear(oracle._p(xs), rows, spec.in_dim, oracle._p(wq32), spec.out_dim,
+                                 oracle._p(perm), n_o, 1, oracle._p(so), oracle._p(sn), s_x,
+                                 max(1, rows // (threads * 4)), None)
+        if secs < 0:
+            raise RuntimeError(r.ref_last_error().decode())
+        total += secs
+        ops += 2.0 * rows * spec.out_dim * spec.in_dim
+    return total, ops
+
+
+def host_reference_layers(torch, layers):
+    """Reference-format (int32 codes in the reference's permuted order, f64 scales) copies."""
+    out = []
+    for spec, w, layer, rep in layers:
+        plan = layer.plan
+        wq = layer.wq.cpu().numpy()
+        # reference layout has no pad columns: drop gather == -1 positions
+        keep = plan.gather >= 0
+        wq32 = np.ascontiguousarray(wq[:, keep].astype(np.int32))
+        out.append((spec, wq32, plan.permutation.astype(np.uint32), plan.outlier_count(),
+                    layer.scale_outlier64.cpu().numpy(), layer.scale_normal64.cpu().numpy(), 0.05))
+    return out
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import torch
+
+    threads = os.cpu_count() or 1
+    line = {"impl": "reference", "metric": METRIC, "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8 codes, f64 epilogue (reference)",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "M": M_TOKENS, "parallelism": "cpu threads"}}
+    if not oracle.ref_available():
+        line["unavailable"] = "oracle/_ref/libqarvd_ref.so was not built (reference sources absent at build time)"
+        print(json.dumps(line))
+        return
+    # inputs: same synthetic layers as our arm, generated on the GPU when present, else numpy
+    if torch.cuda.is_available():
+        layers = build_ffn_layers(torch)
+        host = host_reference_layers(torch, layers)
+        from paper_2605_21072_b200 import synth
+        x = synth.synth_activation(M_TOKENS, DIM, seed=7).float().cpu().numpy().astype(np.float64)
+    else:
+        raise SystemExit("reference arm: input generation needs the GPU box")
+    r = np.random.default_rng(0)
+    u = np.abs(r.standard_normal((M_TOKENS, FFN))) * 0.5
+    # size the per-step sample to ~4 s of CPU work
+    t_probe, ops_probe = reference_ffn_sample(host, x, u, threads, 32)
+    rows = int(min(M_TOKENS, max(32, 32 * 4.0 / max(t_probe, 1e-3))))
+    for _ in range(args.warmup):
+        reference_ffn_sample(host, x, u, threads, min(rows, 64))
+    tot_t, tot_ops = 0.0, 0.0
+    for _ in range(args.steps):
+        t, ops = reference_ffn_sample(host, x, u, threads, rows)
+        tot_t += t
+        tot_ops += ops
+    v = tot_ops / tot_t / 1e12
+    line.update({"value": v, "ms_per_step": 1e3 * tot_t / args.steps,
+                 "cpu_baseline": {"value": v, "unit": "TOPS", "cores": threads, "kind": "reference",
+                                  "sample": f"{rows} of {M_TOKENS} rows of ffn.0 + ffn.2 per step (reference parallel_for row shards)"},
+                 "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args.gpus)
+
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2605_21072_b200 as qb
+    from paper_2605_21072_b200 import engine, synth, _lib
+
+    peaks, peaks_src = load_peaks()
+    layers = build_ffn_layers(torch)
+    (s0, w0, L0, r0), (s2, w2, L2, r2) = layers
+    x = synth.synth_activation(M_TOKENS, DIM, seed=7 + rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    from paper_2605_21072_b200.pipeline import QuantizedChain
+
+    chain = QuantizedChain([L0, L2], M_TOKENS, epilogues=[qb.EPI_GELU, qb.EPI_NONE])
+    chain.x.copy_(x)
+    chain.capture()
+    ops_per_step = chain.int_ops()
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            chain.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches0 = _lib.launch_count()
+        evs = []
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush (256 MiB write), outside the timed events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            chain.replay()
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    # graph replays do not go through the host API: count the kernels the graph holds
+    launches = chain.kernels_per_step() + (_lib.launch_count() - launches0) // max(1, args.steps)
+    my_ms = float(np.mean(step_ms))
+    t = torch.tensor([my_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * ops_per_step / (ms * 1e-3) / 1e12
+
+    # per-kernel device times (cold L2, CUDA events on the launching stream)
+    def kernel_ms(fn, reps=20):
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    st = torch.cuda.current_stream().cuda_stream
+
+    def gemm_fn(i):
+        L = chain.layers[i]
+        return lambda: _lib.call("qarvd_dual_gemm", chain.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
+                                 L.k_pad, M_TOKENS, L.out_dim, L.k_pad, L.k_outlier,
+                                 chain.sx[i].data_ptr(), L.scale_outlier32.data_ptr(),
+                                 L.scale_normal32.data_ptr(), None, chain.epilogues[i], qb.BF16,
+                                 chain.y[i].data_ptr(), L.out_dim, None, None, st)
+
+    def quant_fn(i):
+        L = chain.layers[i]
+        src = chain._src(i)
+        return lambda: _lib.call("qarvd_quantize_act", src.data_ptr(), qb.BF16, M_TOKENS, L.in_dim,
+                                 L.in_dim, L.gather_dev.data_ptr(), L.k_pad, qb.ACT_PER_TOKEN, 0.0, 8,
+                                 chain.xq[i].data_ptr(), L.k_pad, chain.sx[i].data_ptr(), None, None, st)
+
+    k_gemm = [kernel_ms(gemm_fn(i)) for i in range(2)]
+    k_quant = [kernel_ms(quant_fn(i)) for i in range(2)]
+    gemm_ms = [sum(k_gemm)]
+
+    # end to end through the C-ABI host-buffer entry (pinned host in/out, copies timed)
+    h0, h2 = engine.LinearHandle(L0, qb.EPI_GELU), engine.LinearHandle(L2)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((M_TOKENS, DIM), dtype=torch.bfloat16).pin_memory()
+    for _ in range(3):
+        engine.chain_forward_host([h0, h2], xh, yh)
+    e2e_ms = []
+    for _ in range(max(5, args.steps // 2)):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        engine.chain_forward_host([h0, h2], xh, yh)  # synchronous: H2D, 2x(K1+K2), D2H
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e = float(np.median(e2e_ms))
+    tt = torch.tensor([e2e], device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e = float(tt.item())
+
+    if rank == 0:
+        gemm = float(np.mean(gemm_ms))
+        achieved = ops_per_step / (gemm * 1e-3) / 1e12
+        quant_bytes = [M_TOKENS * (L.in_dim * 2 + L.k_pad + 4) for L in chain.layers]
+        peak_bf16 = peaks.get("bf16_tflops", 1590.0)
+        peak = 2.0 * peak_bf16  # int8 dense rate = 2x bf16 on sm_100 (4.5 vs 2.25 PF datasheet)
+        int8_cublas = int8_peak_cublas(torch)
+        cub_ms, cub_gemm_ms = cublas_bf16_ffn_ms(torch, x, w0, w2)
+        line = {
+            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8 (s8 x s8 -> s32 tcgen05), bf16 in/out",
+            "data": "synthetic (Wan-1.3B-shaped bf16 weights, 2.1% outlier input channels x8; bf16 N(0,1) activations with heavy channels)",
+            "config": {"workload": WORKLOAD, "M": M_TOKENS, "ffn0": [FFN, DIM, L0.k_outlier],
+                       "ffn2": [DIM, FFN, L2.k_outlier], "activation_quant": "per-token dynamic",
+                       "l2": "flushed (256 MiB write) before every timed step; step timed with CUDA events",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "dual_gemm_kernel (K2), both FFN GEMMs",
+                         "peak_source": f"2 x measured bf16 burst {peak_bf16} TF/s ({peaks_src})",
+                         "frac_of_int8_datasheet_4500": achieved / INT8_DATASHEET_TOPS,
+                         "int8_cublas_measured_tops": int8_cublas},
+            "cublas_bf16": {"ffn_ms": cub_ms, "gemm_ms": cub_gemm_ms,
+                            "speedup_ours_gemm_vs_cublas_gemm": cub_gemm_ms / gemm,
+                            "speedup_ours_step_vs_cublas_ffn": cub_ms / ms},
+            "graph": "whole FFN step (2x K1 + 2x K2) replayed as one CUDA graph",
+            "kernel_ms": {"gemm_ffn0": k_gemm[0], "gemm_ffn2": k_gemm[1], "quant_x": k_quant[0],
+                          "quant_u": k_quant[1], "note": "each kernel alone, cold L2, CUDA events"},
+            "kernel_tops": {"gemm_ffn0": 2.0 * M_TOKENS * FFN * DIM / (k_gemm[0] * 1e-3) / 1e12,
+                            "gemm_ffn2": 2.0 * M_TOKENS * FFN * DIM / (k_gemm[1] * 1e-3) / 1e12},
+            "quantize_roofline": {"bound": "hbm", "unit": "GB/s", "peak": peaks.get("hbm_gbs", 6650.0),
+                                  "achieved_x": quant_bytes[0] / (k_quant[0] * 1e-3) / 1e9,
+                                  "achieved_u": quant_bytes[1] / (k_quant[1] * 1e-3) / 1e9,
+                                  "bytes_per_launch": quant_bytes},
+            "e2e": {"value": world * ops_per_step / (e2e * 1e-3) / 1e12, "unit": "TOPS",
+                    "h2d_bytes_per_step": M_TOKENS * DIM * 2, "d2h_bytes_per_step": M_TOKENS * DIM * 2,
+                    "ms_per_step": e2e, "path": "qarvd_linear_chain_forward_host (C-ABI, pinned host buffers)"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            try:
+                import oracle
+                if oracle.ref_available():
+                    host = host_reference_layers(torch, layers)
+                    x64 = x.float().cpu().numpy().astype(np.float64)
+                    u64 = engine.kernel_b_gemm_dequant(*engine.kernel_a_quantize_activation(x, L0)[:2], L0,
+                                                       epilogue=qb.EPI_GELU).float().cpu().numpy().astype(np.float64)
+                    threads = os.cpu_count() or 1
+                    tp, _ = reference_ffn_sample(host, x64, u64, threads, 16)
+                    rows = int(min(M_TOKENS, max(16, 16 * 10.0 / max(tp, 1e-3))))
+                    tcpu, ops = reference_ffn_sample(host, x64, u64, threads, rows)
+                    line["cpu_baseline"] = {"value": ops / tcpu / 1e12, "unit": "TOPS", "cores": threads,
+                                            "kind": "reference",
+                                            "sample": f"{rows} of {M_TOKENS} rows through ffn.0 + ffn.2 (permute -> kernel A -> kernel B), reference parallel_for"}
+            except Exception as ex:  # reported, never fatal
+                line["cpu_baseline"] = {"error": str(ex)}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

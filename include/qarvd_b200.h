@@ -1,0 +1,224 @@
+/*
+ * qarvd_b200.h — C-ABI of the B200-native Q-ARVD quantized-inference and
+ * calibration hot path (libqarvd_b200.so).
+ *
+ * Every entry point replaces one operator of the reference C++ core
+ * (/root/reference/proj/core); the citation above each declaration names the
+ * reference interface it stands in for.  The reference works on host f64
+ * std::vector tensors and throws C++ exceptions; this ABI works on DEVICE
+ * pointers + sizes + a cudaStream_t (passed as void*) and returns an int
+ * status plus a thread-local message (qarvd_last_error).  The C++ adapter in
+ * paper_2605_21072_b200/adapter/ maps statuses back onto the reference's
+ * exception types (std::invalid_argument, std::out_of_range, std::logic_error,
+ * std::runtime_error) with the reference's message prefixes.
+ *
+ * Layout conventions (identical to the reference, tensor.hpp:67-70):
+ *   activations X  row-major [m x k]   (ld = elements between rows)
+ *   weights     W  row-major [n x k]   (both GEMM operands are K-major)
+ *   permuted / padded K axis: `gather[c]` = source column of output column c,
+ *   or -1 for a zero pad column.  A dual-scale plan's permutation
+ *   [outlier | normal] (dual_scale.cpp:81-83) becomes
+ *   gather = [outliers..., (-1 pad to a multiple of 32)..., normals..., (-1 pad)]
+ *   and k_outlier is the padded outlier-slab width (a multiple of 32).
+ *
+ * No torch types cross this boundary.  No CPU fallback exists behind it: when
+ * no CUDA device is present every compute entry point returns
+ * QARVD_ERR_CUDA.
+ */
+#ifndef QARVD_B200_H
+#define QARVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QARVD_B200_ABI_VERSION 1
+
+/* ---- status codes (mapped to the reference's exception types) ---------- */
+enum {
+  QARVD_OK = 0,
+  QARVD_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (quant.cpp:59-80, engine.cpp:47-50) */
+  QARVD_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range (engine.cpp:29, dual_scale.cpp:63-64)  */
+  QARVD_ERR_LOGIC = 3,            /* std::logic_error (engine.cpp:54-55)                      */
+  QARVD_ERR_RUNTIME = 4,          /* std::runtime_error                                      */
+  QARVD_ERR_CUDA = 5,             /* CUDA / driver failure, or no device                     */
+  QARVD_ERR_UNSUPPORTED = 6       /* valid for the reference, outside this build's envelope  */
+};
+
+/* element types for X / W inputs and GEMM outputs */
+enum { QARVD_BF16 = 0, QARVD_F32 = 1, QARVD_F64 = 2 };
+
+/* activation quantizer granularity */
+enum {
+  QARVD_ACT_PER_TOKEN = 0,  /* init_scale_minmax(x, b, per_channel, axis 0) (quant.cpp:170-182) */
+  QARVD_ACT_PER_TENSOR = 1  /* QuantParams::per_tensor_symmetric(b, s), static (engine.cpp:57)   */
+};
+
+/* GEMM epilogue options (bit flags) */
+enum {
+  QARVD_EPI_NONE = 0,
+  QARVD_EPI_GELU = 1 /* y = gelu_erf(y) after dequant + bias (toy_model.cpp:62-66 uses the erf form) */
+};
+
+int qarvd_abi_version(void);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* qarvd_last_error(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). Never fails. */
+int qarvd_device_count(void);
+/* Kernel launches issued by this library since load (all threads). */
+uint64_t qarvd_launch_count(void);
+
+/* ---- K1: activation quantization fused with the dual-scale permutation --
+ * Replaces  kernel_a_quantize_activation(permute_activations(x, plan), p)
+ *           engine.hpp:43 / engine.cpp:32-44, numeric contract quant.cpp:113-138.
+ * x       : device [m x k] (ldx), dtype QARVD_BF16 | QARVD_F32 | QARVD_F64.
+ * gather  : device int32 [k_out] source column per output column (-1 = zero);
+ *           NULL = identity (k_out must equal k).
+ * granularity: QARVD_ACT_PER_TOKEN (scale = rowmax|x| / qmax, computed here)
+ *           or QARVD_ACT_PER_TENSOR (scale = static_scale, validated > 0 finite).
+ * bits    : 2..8, symmetric range +-(2^(bits-1)-1) (quant.hpp:36).
+ * xq      : device int8 [m x k_out] (ldq), codes in gathered order.
+ * scale_f32 / scale_f64 : device [m] per-row scale (per-tensor: replicated);
+ *           either may be NULL.  All-zero rows get DBL_MIN / 0.0f (quant.cpp:164).
+ * err_index: device int64[1] or NULL.  Receives the smallest flat index
+ *           (row*k_out + c, gathered coordinates) holding a non-finite input,
+ *           or INT64_MAX.  The reference throws
+ *           "quantize: non-finite input at flat index N" (quant.cpp:128-129);
+ *           the adapter reproduces that from this value.
+ * Codes are bit-identical to round_half_even(v / s) in f64 (quant.hpp:14-20).
+ */
+int qarvd_quantize_act(const void* x, int x_dtype, int64_t m, int64_t k, int64_t ldx,
+                       const int32_t* gather, int64_t k_out, int granularity,
+                       double static_scale, int bits, int8_t* xq, int64_t ldq,
+                       float* scale_f32, double* scale_f64, int64_t* err_index,
+                       void* stream);
+
+/* ---- K5: dual-scale weight preparation ----------------------------------
+ * Replaces  build_plan scales (dual_scale.cpp:13-24, :58-90) +
+ *           nearest-rounding codes of fake_quant_dual (dual_scale.cpp:92-114) +
+ *           the pre-permute of calibrate.cpp:474-480.
+ * w       : device [n x k] (ldw), dtype as above.
+ * gather  : device int32 [k_pad] (see header comment); NULL = identity.
+ * k_outlier: outlier-slab width in gathered coordinates (0 = single-scale plan,
+ *           build_single_scale_plan dual_scale.cpp:44-56).
+ * wq      : device int8 [n x k_pad] (ldq) pre-permuted codes.
+ * scale_*_f64 / _f32 : device [n] per-row group scales (absmax/qmax, DBL_MIN
+ *           when the group is all zero); any may be NULL.  For k_outlier == 0
+ *           the outlier scales equal the normal ones (dual_scale.cpp:55).
+ * err_index: as for qarvd_quantize_act (reference: "fake_quant_dual: non-finite
+ *           weight element").
+ */
+int qarvd_prepare_weights(const void* w, int w_dtype, int64_t n, int64_t k, int64_t ldw,
+                          const int32_t* gather, int64_t k_pad, int64_t k_outlier, int bits,
+                          int8_t* wq, int64_t ldq, double* scale_outlier_f64,
+                          double* scale_normal_f64, float* scale_outlier_f32,
+                          float* scale_normal_f32, int64_t* err_index, void* stream);
+
+/* ---- K2: dual-scale W8A8 GEMM + dequant + bias epilogue ------------------
+ * Replaces  kernel_b_gemm_dequant(xq, layer)  engine.hpp:48 / engine.cpp:46-105
+ * (symmetric activations; the reference's zero-point correction, engine.cpp:95-100,
+ * is returned as QARVD_ERR_UNSUPPORTED by the adapter).
+ * xq [m x k] (ldq), wq [n x k] (ldw): int8 codes, both already in
+ *           [outlier | normal] order.  k % 32 == 0, k_outlier % 32 == 0,
+ *           0 <= k_outlier < k, ldq/ldw multiples of 16, pointers 16-B aligned.
+ *           k <= 132104 keeps the int32 accumulators exact (127*127*k < 2^31).
+ * Two int32 tensor-memory accumulators per tile:
+ *           acc_o = sum_{c <  k_outlier} xq[i,c]*wq[j,c]
+ *           acc_n = sum_{c >= k_outlier} xq[i,c]*wq[j,c]
+ * Epilogue (fp32, this exact op order):
+ *           t = s_wo[j]*float(acc_o);  t = fmaf(s_wn[j], float(acc_n), t);
+ *           y = bias ? fmaf(s_x[i], t, bias[j]) : s_x[i]*t;  [gelu]; round to out dtype (RNE).
+ * scale_x : device f32 [m];  scale_w_outlier / scale_w_normal : device f32 [n].
+ * bias    : device f32 [n] or NULL (reference parity: NULL).
+ * y       : device [m x n] (ldy), out_dtype QARVD_BF16 or QARVD_F32.
+ * acc_outlier / acc_normal : device int32 [m x n] debug dumps or NULL.
+ */
+int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                    int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                    const float* scale_w_outlier, const float* scale_w_normal, const float* bias,
+                    int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
+                    int32_t* acc_normal, void* stream);
+
+/* ---- K1+K2: one quantized linear, host buffers (end-to-end entry) --------
+ * Replaces  quantized_layer_forward(layer, x, Engine::int_kernels)
+ *           engine.hpp:60 / engine.cpp:134-142 (per-token or static activations).
+ * Host x (bf16 bits [m x k]) -> H2D -> K1 -> K2 -> D2H -> host y (bf16 [m x n]).
+ * The device-resident layer (codes, scales, gather) comes from
+ * qarvd_linear_create; workspace for activations is owned by the handle.
+ */
+typedef struct qarvd_linear* qarvd_linear_t;
+int qarvd_linear_create(const int8_t* wq_dev, int64_t n, int64_t k_pad, int64_t k_outlier,
+                        const int32_t* gather_dev, int64_t k_in, const float* scale_w_outlier_dev,
+                        const float* scale_w_normal_dev, const float* bias_dev, int granularity,
+                        double static_scale, int epilogue, qarvd_linear_t* out);
+int qarvd_linear_destroy(qarvd_linear_t layer);
+/* device-pointer forward (x bf16 [m x k_in] -> y bf16 [m x n]) */
+int qarvd_linear_forward(qarvd_linear_t layer, const uint16_t* x_dev, int64_t m, uint16_t* y_dev,
+                         void* stream);
+/* host-buffer forward: copies in, runs K1+K2, copies out, synchronizes */
+int qarvd_linear_forward_host(qarvd_linear_t layer, const uint16_t* x_host, int64_t m,
+                              uint16_t* y_host, void* stream);
+
+/* chained host-buffer forward through several linears (e.g. FFN up -> down):
+ * one H2D of x, K1+K2 per layer on the device, one D2H of the last output.
+ * layers[i].n must equal layers[i+1].k_in. */
+int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers,
+                                    const uint16_t* x_host, int64_t m, uint16_t* y_host,
+                                    void* stream);
+
+/* ---- K3: per-layer outlier detection (batched over layers) ---------------
+ * Replaces  analyze_layer(name, W, tau, alpha_min, align)  outlier.hpp:59-61,
+ *           i.e. channel_l2_norms(W, 1) (tensor.cpp:132-150) -> mad (outlier.cpp:30-38)
+ *           -> detect_outliers (outlier.cpp:40-52) -> align_outliers (outlier.cpp:54-78).
+ * All outputs are device pointers; bit-exact with the reference's f64 results.
+ */
+typedef struct qarvd_outlier_job {
+  const void* w;       /* device [n x k] (ldw) weight, dtype given to the call   */
+  int64_t n, k, ldw;
+  double* norms;       /* out [k]  channel L2 norms                              */
+  double* stats;       /* out [3]  median, mad, threshold                        */
+  int32_t* counts;     /* out [2]  |raw|, |aligned|                              */
+  int32_t* raw_idx;    /* out [k]  raw outlier indices, ascending                */
+  int32_t* aligned_idx;/* out [k]  aligned outlier indices, ascending            */
+} qarvd_outlier_job;
+int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs, int w_dtype, double tau,
+                         double alpha_min, int64_t align, void* stream);
+
+/* ---- K4: frame-weighted calibration scale search (batched over layers) ---
+ * Replaces  init_scale_percentile_search(samples, bits)  quant.hpp:78-82 /
+ *           quant.cpp:190-226, generalised with frame weights from
+ *           weighting_strategy (sensitivity.cpp:86-112):
+ *   L(c) = sum_f w_f * mse_f(c) / sum_f w_f,  mse_f(c) = ||X_f - FQ_{s_c}(X_f)||^2 / |X_f|
+ *   (all w_f equal reduces to, and is evaluated as, (1/S) sum_f mse_f = quant.cpp:216).
+ * X of one layer is `frames` consecutive row blocks of `rows` rows, [frames*rows x k] bf16.
+ * Candidate thresholds are exact order statistics of the pooled |x| (quant.cpp:20-28),
+ * argmin with ties to the larger percentile (quant.cpp:219).
+ */
+#define QARVD_MAX_CANDIDATES 16
+#define QARVD_MAX_FRAMES 64
+typedef struct qarvd_search_job {
+  const uint16_t* x;   /* device bf16 [frames*rows x k] (ldx)                     */
+  int64_t frames, rows, k, ldx;
+  double* result;      /* out device f64 [3*num_cand + 2]:
+                          thresholds[c], scales[c], losses[c], best_index, best_scale */
+} qarvd_search_job;
+int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs, const double* percentiles,
+                       int num_cand, const double* frame_weights, int bits, void* stream);
+
+/* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
+ * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)
+ * weights with a seeded set of input columns scaled by gamma.  Values are
+ * generated directly as bf16.  outlier_cols: device int32 [num_outliers] or NULL.
+ */
+int qarvd_synth_bf16(uint16_t* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                     double stddev, const int32_t* outlier_cols, int64_t num_outliers,
+                     double gamma, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QARVD_B200_H */

@@ -1,0 +1,289 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrappers around the UNMODIFIED reference functions of
+// /root/reference/proj/core (compiled from those sources by oracle/Makefile
+// into oracle/_ref/libqarvd_ref.so).  Used to pin the C restatement
+// (oracle/qarvd_oracle.c), to generate tests/golden fixtures, and as the
+// reference CPU arm of bench.py (`--impl reference`).  Never linked into the
+// product library.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qarvd/dual_scale.hpp"
+#include "qarvd/engine.hpp"
+#include "qarvd/outlier.hpp"
+#include "qarvd/quant.hpp"
+#include "qarvd/sensitivity.hpp"
+#include "qarvd/tensor.hpp"
+#include "qarvd/threading.hpp"
+#include "qarvd/toy_model.hpp"
+
+using namespace qarvd;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = std::string("out_of_range: ") + e.what();
+    return 2;
+  } catch (const std::logic_error& e) {
+    g_err = std::string("logic_error: ") + e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = std::string("runtime_error: ") + e.what();
+    return 4;
+  }
+}
+
+Tensor make_tensor(const double* x, int64_t r, int64_t c) {
+  return Tensor({static_cast<size_t>(r), static_cast<size_t>(c)},
+                std::vector<double>(x, x + r * c));
+}
+
+// A QuantizedLayer whose plan reproduces a permutation with `n_outlier` leading entries.
+QuantizedLayer make_layer(const int32_t* wq, int64_t n, int64_t k, const uint32_t* perm,
+                          int64_t n_outlier, int enabled, const double* s_o, const double* s_n,
+                          double s_x) {
+  QuantizedLayer l;
+  l.name = "shim";
+  l.out_dim = static_cast<size_t>(n);
+  l.in_dim = static_cast<size_t>(k);
+  l.preserved = false;
+  l.wq.shape = {static_cast<size_t>(n), static_cast<size_t>(k)};
+  l.wq.bits = 8;
+  l.wq.data.assign(wq, wq + n * k);
+  l.plan.layer_name = "shim";
+  l.plan.enabled = enabled != 0;
+  l.plan.d_in = static_cast<size_t>(k);
+  l.plan.permutation.assign(perm, perm + k);
+  if (enabled) {
+    l.plan.outlier_indices.assign(perm, perm + n_outlier);
+    l.plan.normal_indices.assign(perm + n_outlier, perm + k);
+  } else {
+    l.plan.normal_indices.assign(perm, perm + k);
+  }
+  l.plan.params_normal =
+      QuantParams::per_channel_symmetric(8, 0, std::vector<double>(s_n, s_n + n));
+  l.plan.params_outlier =
+      enabled ? QuantParams::per_channel_symmetric(8, 0, std::vector<double>(s_o, s_o + n))
+              : l.plan.params_normal;
+  l.act = QuantParams::per_tensor_symmetric(8, s_x);
+  return l;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+void ref_set_threads(unsigned n) { set_num_threads(n); }
+unsigned ref_num_threads(void) { return num_threads(); }
+
+// quantize(x, p): per_token -> p = init_scale_minmax(x, bits, per_channel, 0); else static s.
+int ref_quantize(const double* x, int64_t m, int64_t k, int per_token, double s, int bits,
+                 int32_t* codes, double* scales) {
+  return guarded([&] {
+    const Tensor t = make_tensor(x, m, k);
+    const QuantParams p = per_token ? init_scale_minmax(t, bits, Granularity::per_channel, 0)
+                                    : QuantParams::per_tensor_symmetric(bits, s);
+    const IntTensor q = kernel_a_quantize_activation(t, p);
+    std::memcpy(codes, q.data.data(), sizeof(int32_t) * q.data.size());
+    if (scales)
+      for (int64_t i = 0; i < m; ++i) scales[i] = p.scale_for(per_token ? i : 0);
+  });
+}
+
+// permute_activations(x, plan) for a plan with the given permutation
+int ref_permute(const double* x, int64_t m, int64_t k, const uint32_t* perm, int enabled,
+                double* out) {
+  return guarded([&] {
+    DualScalePlan plan;
+    plan.enabled = enabled != 0;
+    plan.d_in = static_cast<size_t>(k);
+    plan.permutation.assign(perm, perm + k);
+    const Tensor o = permute_activations(make_tensor(x, m, k), plan);
+    std::memcpy(out, o.data(), sizeof(double) * o.size());
+  });
+}
+
+// kernel_b_gemm_dequant with a per-row activation scale (rows are independent,
+// engine.cpp:86, so the per-token result is kernel B applied row block by row block).
+int ref_kernel_b(const int32_t* xq, int64_t m, int64_t k, const int32_t* wq, int64_t n,
+                 const uint32_t* perm, int64_t n_outlier, int enabled, const double* s_x,
+                 int per_row, const double* s_o, const double* s_n, double* out) {
+  return guarded([&] {
+    QuantizedLayer base = make_layer(wq, n, k, perm, n_outlier, enabled, s_o, s_n, s_x[0]);
+    if (!per_row) {
+      IntTensor q;
+      q.shape = {static_cast<size_t>(m), static_cast<size_t>(k)};
+      q.data.assign(xq, xq + m * k);
+      const Tensor y = kernel_b_gemm_dequant(q, base);
+      std::memcpy(out, y.data(), sizeof(double) * y.size());
+      return;
+    }
+    parallel_for(static_cast<size_t>(m), [&](size_t i) {
+      QuantizedLayer l = base;  // per-row activation scale
+      l.act = QuantParams::per_tensor_symmetric(8, s_x[i]);
+      IntTensor q;
+      q.shape = {1, static_cast<size_t>(k)};
+      q.data.assign(xq + i * k, xq + (i + 1) * k);
+      const Tensor y = kernel_b_gemm_dequant(q, l);
+      std::memcpy(out + i * n, y.data(), sizeof(double) * n);
+    });
+  });
+}
+
+// analyze_layer(name, W, tau, alpha_min, align)
+int ref_analyze_layer(const double* w, int64_t n, int64_t k, double tau, double alpha_min,
+                      int64_t align, double* norms, double* stats, int64_t* counts, int64_t* raw,
+                      int64_t* aligned) {
+  return guarded([&] {
+    const OutlierReport r =
+        analyze_layer("shim", make_tensor(w, n, k), tau, alpha_min, static_cast<size_t>(align));
+    std::memcpy(norms, r.norms.data(), sizeof(double) * r.norms.size());
+    stats[0] = r.median;
+    stats[1] = r.mad;
+    stats[2] = r.threshold;
+    counts[0] = static_cast<int64_t>(r.raw_outliers.size());
+    counts[1] = static_cast<int64_t>(r.aligned_outliers.size());
+    for (size_t i = 0; i < r.raw_outliers.size(); ++i) raw[i] = static_cast<int64_t>(r.raw_outliers[i]);
+    for (size_t i = 0; i < r.aligned_outliers.size(); ++i)
+      aligned[i] = static_cast<int64_t>(r.aligned_outliers[i]);
+  });
+}
+
+// detect_outliers / align_outliers / mad on a norm vector
+int ref_analyze_norms(const double* v, int64_t k, double tau, double alpha_min, int64_t align,
+                      double* stats, int64_t* counts, int64_t* raw, int64_t* aligned) {
+  return guarded([&] {
+    const OutlierReport r = analyze_norms("shim", std::vector<double>(v, v + k), tau, alpha_min,
+                                          static_cast<size_t>(align));
+    stats[0] = r.median;
+    stats[1] = r.mad;
+    stats[2] = r.threshold;
+    counts[0] = static_cast<int64_t>(r.raw_outliers.size());
+    counts[1] = static_cast<int64_t>(r.aligned_outliers.size());
+    for (size_t i = 0; i < r.raw_outliers.size(); ++i) raw[i] = static_cast<int64_t>(r.raw_outliers[i]);
+    for (size_t i = 0; i < r.aligned_outliers.size(); ++i)
+      aligned[i] = static_cast<int64_t>(r.aligned_outliers[i]);
+  });
+}
+
+// build_plan(W, report with the given aligned outliers) + nearest codes per group,
+// pre-permuted [outlier | normal] (calibrate.cpp:474-480).  Codes are produced by
+// the reference quantize() on each column group with the plan's per-row params.
+int ref_build_plan_codes(const double* w, int64_t n, int64_t k, const int64_t* outliers,
+                         int64_t n_out, int bits, double* s_o, double* s_n, uint32_t* perm,
+                         int32_t* wq_perm, int* enabled) {
+  return guarded([&] {
+    const Tensor W = make_tensor(w, n, k);
+    OutlierReport rep;
+    rep.layer_name = "shim";
+    rep.aligned_outliers.assign(outliers, outliers + n_out);
+    const DualScalePlan plan = build_plan(W, rep, bits);
+    *enabled = plan.enabled ? 1 : 0;
+    for (int64_t r = 0; r < n; ++r) {
+      s_o[r] = plan.params_outlier.scale[r];
+      s_n[r] = plan.params_normal.scale[r];
+    }
+    std::memcpy(perm, plan.permutation.data(), sizeof(uint32_t) * k);
+    const size_t n_o = plan.enabled ? plan.outlier_count() : 0;
+    auto group_codes = [&](const std::vector<size_t>& cols, const QuantParams& p, size_t pos0) {
+      if (cols.empty()) return;
+      Tensor g({static_cast<size_t>(n), cols.size()});
+      for (int64_t r = 0; r < n; ++r)
+        for (size_t c = 0; c < cols.size(); ++c) g.at(r, c) = W.at(r, cols[c]);
+      const IntTensor q = quantize(g, p);
+      for (int64_t r = 0; r < n; ++r)
+        for (size_t c = 0; c < cols.size(); ++c) wq_perm[r * k + pos0 + c] = q.at(r, c);
+    };
+    if (plan.enabled) group_codes(plan.outlier_indices, plan.params_outlier, 0);
+    group_codes(plan.normal_indices, plan.params_normal, n_o);
+  });
+}
+
+// init_scale_percentile_search over `frames` samples of [rows x k]
+int ref_percentile_search(const double* x, int64_t frames, int64_t rows, int64_t k, int bits,
+                          double* best_pct, double* scale, double* cand_mse) {
+  return guarded([&] {
+    std::vector<Tensor> samples;
+    for (int64_t f = 0; f < frames; ++f) samples.push_back(make_tensor(x + f * rows * k, rows, k));
+    const PercentileSearchResult r = init_scale_percentile_search(samples, bits);
+    *best_pct = r.best_percentile;
+    *scale = r.params.scale[0];
+    for (size_t c = 0; c < r.candidate_mse.size(); ++c) cand_mse[c] = r.candidate_mse[c];
+  });
+}
+
+// weighting_strategy(profile, kind) with a profile whose normalized alpha is given
+int ref_weighting(int kind, const double* alpha_raw, int64_t n, double* out) {
+  return guarded([&] {
+    SensitivityProfile prof;
+    prof.alpha_raw.assign(alpha_raw, alpha_raw + n);
+    prof.alpha_normalized = normalize_alpha(prof.alpha_raw);
+    const std::vector<double> w = weighting_strategy(prof, static_cast<WeightingKind>(kind));
+    std::memcpy(out, w.data(), sizeof(double) * n);
+  });
+}
+
+// ToyModel::build (toy_model.cpp:126-170): weight of `layer` with one injection rule
+int ref_toy_weight(int64_t blocks, int64_t hidden, uint64_t seed, const char* pattern,
+                   double fraction, double gamma, const char* layer, double* out, int64_t* rows,
+                   int64_t* cols) {
+  return guarded([&] {
+    ToyModelConfig cfg;
+    cfg.blocks = static_cast<size_t>(blocks);
+    cfg.hidden = static_cast<size_t>(hidden);
+    cfg.seed = seed;
+    if (pattern && pattern[0]) cfg.injections.push_back({pattern, fraction, gamma});
+    const ToyModel m = ToyModel::build(cfg);
+    const Tensor& w = m.weight(layer);
+    *rows = static_cast<int64_t>(w.rows());
+    *cols = static_cast<int64_t>(w.cols());
+    if (out) std::memcpy(out, w.data(), sizeof(double) * w.size());
+  });
+}
+
+// round_half_even (quant.hpp:14-20)
+double ref_round_half_even(double v) { return round_half_even(v); }
+
+// Timed reference CPU path for one quantized linear:
+// permute_activations -> kernel_a_quantize_activation -> kernel_b_gemm_dequant
+// (engine.cpp:137-139), row-sharded with the reference parallel_for (rows are
+// independent).  Returns seconds; y receives the f64 output.
+double ref_time_linear(const double* x, int64_t m, int64_t k, const int32_t* wq, int64_t n,
+                       const uint32_t* perm, int64_t n_outlier, int enabled, const double* s_o,
+                       const double* s_n, double s_x, int64_t rows_per_task, double* y) {
+  double secs = -1.0;
+  guarded([&] {
+    const QuantizedLayer layer = make_layer(wq, n, k, perm, n_outlier, enabled, s_o, s_n, s_x);
+    const Tensor X = make_tensor(x, m, k);
+    const size_t tasks = static_cast<size_t>((m + rows_per_task - 1) / rows_per_task);
+    const auto t0 = std::chrono::steady_clock::now();
+    parallel_for(tasks, [&](size_t t) {
+      const int64_t r0 = static_cast<int64_t>(t) * rows_per_task;
+      const int64_t r1 = std::min<int64_t>(m, r0 + rows_per_task);
+      Tensor xs({static_cast<size_t>(r1 - r0), static_cast<size_t>(k)});
+      std::memcpy(xs.data(), X.data() + r0 * k, sizeof(double) * (r1 - r0) * k);
+      const Tensor xp = permute_activations(xs, layer.plan);
+      const IntTensor xq = kernel_a_quantize_activation(xp, layer.act);
+      const Tensor out = kernel_b_gemm_dequant(xq, layer);
+      if (y) std::memcpy(y + r0 * n, out.data(), sizeof(double) * out.size());
+    });
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  return secs;
+}
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+"""Frame-weighted calibration scale search and its layer-sharded driver.
+
+Reference pieces (``/root/reference/proj/core``):
+
+* ``weighting_strategy`` / ``normalize_alpha``   sensitivity.cpp:16-27, :86-112
+* ``init_scale_percentile_search``               quant.cpp:185-226
+* ``calibrate_model``'s per-layer loop           calibrate.cpp:398-487
+  (``parallel_for`` over quantized layers, slot-indexed results, :432-484)
+
+The per-layer unit of ``calibrate_model`` becomes: K3 outlier detection ->
+K5 dual-scale weight prep -> K4 frame-weighted activation-scale search, all on
+the device.  Across GPUs the layers are split by a deterministic LPT
+assignment on algorithmic bytes; each rank runs its layers independently and
+one all-gather of packed per-layer records gives every rank the full,
+rank-count-invariant result (the reference's thread-count invariance,
+threading.hpp:13-14, lifted to GPU count).
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass
+from typing import Callable, Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import _stream
+
+PERCENTILES = (0.999, 0.9999, 0.99999)  # quant.cpp:185-188
+WEIGHTING_KINDS = ("uniform", "heuristic_exp", "reverse", "final_quality")  # sensitivity.hpp:37
+
+
+def normalize_alpha(raw: Sequence[float]) -> np.ndarray:
+    """sensitivity.cpp:16-27 (same f64 op order)."""
+    total = 0.0
+    for a in raw:
+        total += float(a)
+    if total <= 0.0:
+        return np.full(len(raw), 1.0 / len(raw))
+    return np.asarray([float(a) / total for a in raw])
+
+
+def weighting_strategy(kind: str, n: int, alpha_raw: Optional[Sequence[float]] = None) -> np.ndarray:
+    """weighting_strategy (sensitivity.cpp:86-112) for an N-entry profile."""
+    if n <= 0:
+        raise _lib.InvalidArgument("weighting_strategy: empty profile")
+    if kind == "uniform":
+        return np.full(n, 1.0 / n)
+    if kind == "heuristic_exp":
+        w = [2.0 ** -(i + 1) for i in range(n)]
+        total = 0.0
+        for v in w:
+            total += v
+        return np.asarray([v / total for v in w])
+    if alpha_raw is None or len(alpha_raw) != n:
+        raise _lib.InvalidArgument("weighting_strategy: profile required for " + kind)
+    a = normalize_alpha(alpha_raw)
+    if kind == "reverse":
+        return a[::-1].copy()
+    if kind == "final_quality":
+        return a
+    raise _lib.InvalidArgument("unknown weighting kind: " + kind)
+
+
+@dataclass
+class SearchResult:
+    """PercentileSearchResult (quant.hpp:72-77) + thresholds and the frame-weighted losses."""
+
+    thresholds: np.ndarray
+    scales: np.ndarray
+    losses: np.ndarray
+    best_index: int
+    scale: float
+    percentiles: tuple
+
+    @property
+    def best_percentile(self) -> float:
+        return self.percentiles[self.best_index]
+
+
+def scale_search_async(xs: Sequence[torch.Tensor], frames: int, frame_weights=None,
+                       percentiles=PERCENTILES, bits: int = 8) -> torch.Tensor:
+    """K4 over a batch of layers.  xs[i]: bf16 [frames*rows x k].  Returns the device result
+    matrix [len(xs), 3*nc+2] (thresholds, scales, losses, best index, best scale)."""
+    nc = len(percentiles)
+    res = torch.empty((len(xs), 3 * nc + 2), dtype=torch.float64, device=xs[0].device)
+    jobs = (_lib.SearchJob * len(xs))()
+    for i, x in enumerate(xs):
+        if x.dtype != torch.bfloat16:
+            raise _lib.InvalidArgument("scale_search: activations must be bf16")
+        if x.shape[0] % frames:
+            raise _lib.InvalidArgument("scale_search: rows not divisible by the frame count")
+        jobs[i].x = x.data_ptr()
+        jobs[i].frames = frames
+        jobs[i].rows = x.shape[0] // frames
+        jobs[i].k = x.shape[1]
+        jobs[i].ldx = x.stride(0)
+        jobs[i].result = res[i].data_ptr()
+    pct = (_lib.ctypes.c_double * nc)(*percentiles)
+    w = None
+    if frame_weights is not None:
+        if len(frame_weights) != frames:
+            raise _lib.InvalidArgument("calibrate_model: weight vector length must equal chunk count")
+        w = (_lib.ctypes.c_double * frames)(*[float(v) for v in frame_weights])
+    _lib.call("qarvd_scale_search", jobs, len(xs), pct, nc, w, bits, _stream())
+    return res
+
+
+def unpack_search(row: np.ndarray, percentiles=PERCENTILES) -> SearchResult:
+    nc = len(percentiles)
+    return SearchResult(row[:nc].copy(), row[nc:2 * nc].copy(), row[2 * nc:3 * nc].copy(),
+                        int(row[3 * nc]), float(row[3 * nc + 1]), tuple(percentiles))
+
+
+def init_scale_percentile_search(frames: Sequence[torch.Tensor], bits: int = 8,
+                                 frame_weights=None) -> SearchResult:
+    """init_scale_percentile_search(samples, bits) (quant.cpp:190-226); with ``frame_weights``
+    the per-sample MSEs are weighted (Eq. 5 frame weights)."""
+    if len(frames) == 0:
+        raise _lib.InvalidArgument("percentile search: empty calibration sample list")
+    shapes = {tuple(f.shape) for f in frames}
+    if len(shapes) != 1:
+        raise _lib.Unsupported("scale_search: samples of different shapes")
+    x = torch.cat([f.reshape(-1, f.shape[-1]) for f in frames], 0)
+    res = scale_search_async([x], len(frames), frame_weights, PERCENTILES, bits)
+    return unpack_search(res[0].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# layer sharding (calibrate.cpp:440-484 -> G GPUs)
+
+def lpt_assign(costs: Sequence[float], world: int) -> List[List[int]]:
+    """Deterministic longest-processing-time assignment: layers sorted by cost desc
+    (ties -> lower index), each to the least-loaded rank (ties -> lower rank).
+    Each rank's list is returned in ascending layer order."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    heap = [(0.0, r) for r in range(world)]
+    heapq.heapify(heap)
+    out: List[List[int]] = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    return [sorted(v) for v in out]
+
+
+@dataclass
+class LayerRecord:
+    """Everything the quantized deployment needs from calibration for one layer."""
+
+    index: int
+    k_outlier: int            # aligned outlier count (reference K_o)
+    outliers: np.ndarray      # aligned outlier indices (ascending)
+    act_scale: float          # selected per-tensor activation scale
+    best_index: int
+    losses: np.ndarray
+    scale_outlier: np.ndarray  # f64 [out_dim]
+    scale_normal: np.ndarray   # f64 [out_dim]
+
+    def pack(self) -> np.ndarray:
+        n = len(self.scale_normal)
+        head = [float(self.index), float(n), float(len(self.outliers)), float(len(self.losses)),
+                self.act_scale, float(self.best_index)]
+        return np.concatenate([np.asarray(head), self.losses, self.scale_outlier,
+                               self.scale_normal, self.outliers.astype(np.float64)])
+
+    @staticmethod
+    def unpack(buf: np.ndarray, pos: int):
+        idx, n, no, nl, act, best = buf[pos:pos + 6]
+        n, no, nl = int(n), int(no), int(nl)
+        p = pos + 6
+        losses = buf[p:p + nl].copy(); p += nl
+        so = buf[p:p + n].copy(); p += n
+        sn = buf[p:p + n].copy(); p += n
+        outl = buf[p:p + no].astype(np.int64); p += no
+        return LayerRecord(int(idx), no, outl, float(act), int(best), losses, so, sn), p
+
+
+def pack_records(records: Sequence[LayerRecord]) -> np.ndarray:
+    if not records:
+        return np.zeros(0, dtype=np.float64)
+    return np.concatenate([r.pack() for r in records])
+
+
+def unpack_records(buf: np.ndarray) -> List[LayerRecord]:
+    out, pos = [], 0
+    while pos < len(buf):
+        r, pos = LayerRecord.unpack(buf, pos)
+        out.append(r)
+    return out
+
+
+def allgather_records(local: Sequence[LayerRecord], group=None, device=None) -> List[LayerRecord]:
+    """One all-gather of the packed per-layer records (NCCL on GPU, gloo on CPU).
+    Payloads are padded to the largest rank's size; the result is sorted by layer index."""
+    import torch.distributed as dist
+
+    payload = pack_records(local)
+    dev = device if device is not None else torch.device("cpu")
+    world = dist.get_world_size(group)
+    size = torch.tensor([payload.size], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, size, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(max(sizes), 1)
+    buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+    buf[:payload.size] = torch.from_numpy(payload).to(dev)
+    gathered = torch.empty(world * cap, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(gathered, buf, group=group)
+    g = gathered.cpu().numpy()
+    recs: List[LayerRecord] = []
+    for r in range(world):
+        recs.extend(unpack_records(g[r * cap: r * cap + sizes[r]]))
+    recs.sort(key=lambda r: r.index)
+    return recs

@@ -1,0 +1,289 @@
+// C-ABI plumbing: error state, device checks, launch accounting, the
+// device-resident quantized linear handle (K1 + K2 behind one call, with a
+// host-buffer entry for end-to-end use) and the synthetic data generator.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <mutex>
+#include <new>
+
+#include "common.cuh"
+
+namespace qarvd_b200 {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> counter{0};
+  return counter;
+}
+
+int require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    QARVD_FAIL(QARVD_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+  }
+  return QARVD_OK;
+}
+
+int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                     int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                     const float* scale_wo, const float* scale_wn, const float* bias,
+                     int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
+                     int32_t* acc_n, cudaStream_t stream);
+
+// ---- synthetic data ---------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64_dev(uint64_t z) {
+  // one splitmix64 output for counter state z (rng.hpp:11-16 constants)
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void synth_bf16_kernel(uint16_t* out, int64_t rows, int64_t cols, int64_t ld,
+                                  uint64_t seed, float stddev) {
+  const int64_t total = rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const uint64_t h = splitmix64_dev(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ULL));
+    // Box-Muller on two 24-bit uniforms in (0, 1]
+    const float u1 = (static_cast<float>(h >> 40) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = static_cast<float>((h >> 16) & 0xffffffu) * (1.0f / 16777216.0f);
+    const float g = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+    const __nv_bfloat16 b = __float2bfloat16_rn(g * stddev);
+    out[r * ld + c] = *reinterpret_cast<const uint16_t*>(&b);
+  }
+}
+
+__global__ void scale_cols_bf16_kernel(uint16_t* out, int64_t rows, int64_t ld,
+                                       const int32_t* cols, int64_t ncols, float gamma) {
+  const int64_t total = rows * ncols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / ncols, j = i - r * ncols;
+    uint16_t* p = out + r * ld + cols[j];
+    const __nv_bfloat16 b = __float2bfloat16_rn(bf16_bits_to_float(*p) * gamma);
+    *p = *reinterpret_cast<const uint16_t*>(&b);
+  }
+}
+
+}  // namespace
+}  // namespace qarvd_b200
+
+using namespace qarvd_b200;
+
+// ---- the quantized linear handle ---------------------------------------------
+struct qarvd_linear {
+  const int8_t* wq;
+  int64_t n, k_pad, k_o, k_in;
+  const int32_t* gather;
+  const float* s_wo;
+  const float* s_wn;
+  const float* bias;
+  int granularity;
+  double static_scale;
+  int epilogue;
+  // workspace (grown on demand)
+  int64_t cap_m = 0;
+  int8_t* xq = nullptr;
+  float* sx = nullptr;
+  uint16_t* x_dev = nullptr;
+  uint16_t* y_dev = nullptr;
+  std::mutex mu;  // forward() is re-entrant per handle (reference providers are shared const)
+};
+
+namespace {
+int ensure_workspace(qarvd_linear* L, int64_t m, bool host_io) {
+  if (m <= L->cap_m && (!host_io || L->x_dev)) return QARVD_OK;
+  const int64_t cap = m > L->cap_m ? m : L->cap_m;
+  cudaFree(L->xq);
+  cudaFree(L->sx);
+  cudaFree(L->x_dev);
+  cudaFree(L->y_dev);
+  L->xq = nullptr;
+  L->sx = nullptr;
+  L->x_dev = nullptr;
+  L->y_dev = nullptr;
+  QARVD_CUDA_TRY(cudaMalloc(&L->xq, static_cast<size_t>(cap) * L->k_pad));
+  QARVD_CUDA_TRY(cudaMalloc(&L->sx, static_cast<size_t>(cap) * sizeof(float)));
+  if (host_io) {
+    QARVD_CUDA_TRY(cudaMalloc(&L->x_dev, static_cast<size_t>(cap) * L->k_in * 2));
+    QARVD_CUDA_TRY(cudaMalloc(&L->y_dev, static_cast<size_t>(cap) * L->n * 2));
+  }
+  L->cap_m = cap;
+  return QARVD_OK;
+}
+
+int linear_forward_dev(qarvd_linear* L, const uint16_t* x, int64_t m, uint16_t* y,
+                       cudaStream_t s) {
+  int st = qarvd_quantize_act(x, QARVD_BF16, m, L->k_in, L->k_in, L->gather, L->k_pad,
+                              L->granularity, L->static_scale, 8, L->xq, L->k_pad, L->sx, nullptr,
+                              nullptr, s);
+  if (st) return st;
+  return qarvd_dual_gemm(L->xq, L->k_pad, L->wq, L->k_pad, m, L->n, L->k_pad, L->k_o, L->sx,
+                         L->s_wo, L->s_wn, L->bias, L->epilogue, QARVD_BF16, y, L->n, nullptr,
+                         nullptr, s);
+}
+}  // namespace
+
+extern "C" {
+
+int qarvd_abi_version(void) { return QARVD_B200_ABI_VERSION; }
+const char* qarvd_last_error(void) { return qarvd_b200::last_error_cstr(); }
+
+int qarvd_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+uint64_t qarvd_launch_count(void) { return launch_counter().load(); }
+
+int qarvd_linear_create(const int8_t* wq_dev, int64_t n, int64_t k_pad, int64_t k_outlier,
+                        const int32_t* gather_dev, int64_t k_in, const float* scale_w_outlier_dev,
+                        const float* scale_w_normal_dev, const float* bias_dev, int granularity,
+                        double static_scale, int epilogue, qarvd_linear_t* out) {
+  clear_error();
+  if (!out || !wq_dev || !scale_w_normal_dev || n <= 0 || k_pad <= 0 || k_in <= 0)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_create: invalid argument");
+  if (!gather_dev && k_in != k_pad)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_create: identity layout needs k_in == k_pad");
+  if (k_pad % 32 || k_outlier % 32 || k_outlier < 0 || k_outlier >= k_pad)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_create: k_pad / k_outlier must be multiples of 32");
+  if (granularity == QARVD_ACT_PER_TENSOR && !(static_scale > 0.0 && static_scale <= DBL_MAX))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quant params: scale must be positive and finite");
+  auto* L = new (std::nothrow) qarvd_linear();
+  if (!L) QARVD_FAIL(QARVD_ERR_RUNTIME, "out of host memory");
+  L->wq = wq_dev;
+  L->n = n;
+  L->k_pad = k_pad;
+  L->k_o = k_outlier;
+  L->k_in = k_in;
+  L->gather = gather_dev;
+  L->s_wo = k_outlier > 0 ? scale_w_outlier_dev : scale_w_normal_dev;
+  L->s_wn = scale_w_normal_dev;
+  L->bias = bias_dev;
+  L->granularity = granularity;
+  L->static_scale = static_scale;
+  L->epilogue = epilogue;
+  *out = L;
+  return QARVD_OK;
+}
+
+int qarvd_linear_destroy(qarvd_linear_t L) {
+  clear_error();
+  if (!L) return QARVD_OK;
+  cudaFree(L->xq);
+  cudaFree(L->sx);
+  cudaFree(L->x_dev);
+  cudaFree(L->y_dev);
+  delete L;
+  return QARVD_OK;
+}
+
+int qarvd_linear_forward(qarvd_linear_t L, const uint16_t* x_dev, int64_t m, uint16_t* y_dev,
+                         void* stream) {
+  clear_error();
+  if (!L || !x_dev || !y_dev || m <= 0)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_forward: invalid argument");
+  if (int st = require_device()) return st;
+  std::lock_guard<std::mutex> lock(L->mu);
+  if (int st = ensure_workspace(L, m, false)) return st;
+  return linear_forward_dev(L, x_dev, m, y_dev, as_stream(stream));
+}
+
+int qarvd_linear_forward_host(qarvd_linear_t L, const uint16_t* x_host, int64_t m,
+                              uint16_t* y_host, void* stream) {
+  clear_error();
+  if (!L || !x_host || !y_host || m <= 0)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_forward_host: invalid argument");
+  if (int st = require_device()) return st;
+  std::lock_guard<std::mutex> lock(L->mu);
+  if (int st = ensure_workspace(L, m, true)) return st;
+  cudaStream_t s = as_stream(stream);
+  QARVD_CUDA_TRY(cudaMemcpyAsync(L->x_dev, x_host, static_cast<size_t>(m) * L->k_in * 2,
+                                 cudaMemcpyHostToDevice, s));
+  if (int st = linear_forward_dev(L, L->x_dev, m, L->y_dev, s)) return st;
+  QARVD_CUDA_TRY(cudaMemcpyAsync(y_host, L->y_dev, static_cast<size_t>(m) * L->n * 2,
+                                 cudaMemcpyDeviceToHost, s));
+  QARVD_CUDA_TRY(cudaStreamSynchronize(s));
+  return QARVD_OK;
+}
+
+int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers,
+                                    const uint16_t* x_host, int64_t m, uint16_t* y_host,
+                                    void* stream) {
+  clear_error();
+  if (!layers || num_layers <= 0 || !x_host || !y_host || m <= 0)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_chain_forward_host: invalid argument");
+  for (int i = 0; i + 1 < num_layers; ++i)
+    if (!layers[i] || !layers[i + 1] || layers[i]->n != layers[i + 1]->k_in)
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_chain_forward_host: layer widths do not chain");
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  for (int i = 0; i < num_layers; ++i) {
+    layers[i]->mu.lock();
+    const int st = ensure_workspace(layers[i], m, true);
+    if (st) {
+      for (int j = 0; j <= i; ++j) layers[j]->mu.unlock();
+      return st;
+    }
+  }
+  int st = QARVD_OK;
+  cudaError_t e = cudaMemcpyAsync(layers[0]->x_dev, x_host,
+                                  static_cast<size_t>(m) * layers[0]->k_in * 2,
+                                  cudaMemcpyHostToDevice, s);
+  const uint16_t* in = layers[0]->x_dev;
+  for (int i = 0; i < num_layers && e == cudaSuccess && st == QARVD_OK; ++i) {
+    st = linear_forward_dev(layers[i], in, m, layers[i]->y_dev, s);
+    in = layers[i]->y_dev;
+  }
+  if (e == cudaSuccess && st == QARVD_OK)
+    e = cudaMemcpyAsync(y_host, in, static_cast<size_t>(m) * layers[num_layers - 1]->n * 2,
+                        cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && st == QARVD_OK) e = cudaStreamSynchronize(s);
+  for (int i = 0; i < num_layers; ++i) layers[i]->mu.unlock();
+  if (st) return st;
+  QARVD_CUDA_TRY(e);
+  return QARVD_OK;
+}
+
+int qarvd_synth_bf16(uint16_t* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                     double stddev, const int32_t* outlier_cols, int64_t num_outliers,
+                     double gamma, void* stream) {
+  clear_error();
+  if (!out || rows < 0 || cols <= 0 || ld < cols || num_outliers < 0 ||
+      (num_outliers > 0 && !outlier_cols))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_synth_bf16: invalid argument");
+  if (int st = require_device()) return st;
+  if (rows == 0) return QARVD_OK;
+  cudaStream_t s = as_stream(stream);
+  synth_bf16_kernel<<<kNumSMs * 8, 256, 0, s>>>(out, rows, cols, ld, seed,
+                                                static_cast<float>(stddev));
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  if (num_outliers > 0) {
+    scale_cols_bf16_kernel<<<kNumSMs * 4, 256, 0, s>>>(out, rows, ld, outlier_cols, num_outliers,
+                                                       static_cast<float>(gamma));
+    count_launch();
+    QARVD_LAUNCH_CHECK();
+  }
+  return QARVD_OK;
+}
+
+}  // extern "C"

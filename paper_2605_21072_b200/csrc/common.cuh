@@ -1,0 +1,108 @@
+// Shared host/device helpers for libqarvd_b200.so (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cfloat>
+#include <cstdio>
+#include <string>
+
+#include "../../include/qarvd_b200.h"
+
+namespace qarvd_b200 {
+
+// ---- error plumbing (C-ABI: int status + thread-local message) ----------
+void set_error(const std::string& msg);
+const char* last_error_cstr();
+void clear_error();
+std::atomic<uint64_t>& launch_counter();
+inline void count_launch(uint64_t n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Returns QARVD_ERR_CUDA with a message when no device is usable.
+int require_device();
+
+#define QARVD_FAIL(code, msg)              \
+  do {                                     \
+    ::qarvd_b200::set_error(msg);          \
+    return (code);                         \
+  } while (0)
+
+#define QARVD_CUDA_TRY(expr)                                                             \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      ::qarvd_b200::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) +     \
+                              " at " + __FILE__ + ":" + std::to_string(__LINE__));       \
+      return QARVD_ERR_CUDA;                                                             \
+    }                                                                                    \
+  } while (0)
+
+#define QARVD_LAUNCH_CHECK() QARVD_CUDA_TRY(cudaGetLastError())
+
+constexpr int kNumSMs = 148;
+
+// ---- bf16 helpers (bit patterns; RNE as bytes.hpp:40-45) -----------------
+__device__ __forceinline__ float bf16_bits_to_float(uint16_t h) {
+  return __uint_as_float(static_cast<uint32_t>(h) << 16);
+}
+
+// ---- the bit-exact quantizer ---------------------------------------------
+// Reference contract (quant.cpp:132-135): code = clamp(round_half_even(v / s)).
+// round_half_even (quant.hpp:14-20) equals IEEE rint in the default rounding
+// mode, and v / s is an IEEE f64 division.  Fast path: t = v * r32 in fp32
+// with r32 ~= qmax/absmax (or 1/s).  |t - v/s| <= |t| * 2^-22 < 3.1e-5 for
+// |t| <= 254, so whenever frac(t) is >= 1e-4 away from 0.5 the f64 result
+// rounds to the same integer; otherwise recompute exactly with __ddiv_rn.
+__device__ __forceinline__ int quant_code_fast(float v, float r32, double s64, int qmax) {
+  const float t = __fmul_rn(v, r32);
+  const float at = fabsf(t);
+  if (at > 2.0f * qmax + 2.0f) return t > 0.f ? qmax : -qmax;  // far outside: clamps either way
+  const float fl = floorf(t);
+  const float fr = __fsub_rn(t, fl);  // exact for |t| < 2^23
+  int q;
+  if (fabsf(__fsub_rn(fr, 0.5f)) < 1e-4f) {
+    q = static_cast<int>(rint(__ddiv_rn(static_cast<double>(v), s64)));
+  } else {
+    q = static_cast<int>(rintf(t));
+  }
+  return q > qmax ? qmax : (q < -qmax ? -qmax : q);
+}
+
+// Exact path for any input precision (used when r32 is not a normal float,
+// and for f64 inputs): rint(v / s) in f64, then clamp.
+__device__ __forceinline__ int quant_code_exact(double v, double s64, int qmax) {
+  const double q = rint(__ddiv_rn(v, s64));
+  if (q > static_cast<double>(qmax)) return qmax;
+  if (q < -static_cast<double>(qmax)) return -qmax;
+  return static_cast<int>(q);
+}
+
+template <typename T>
+struct InType;
+template <>
+struct InType<uint16_t> {
+  static constexpr int code = QARVD_BF16;
+  __device__ static __forceinline__ double to_double(uint16_t v) {
+    return static_cast<double>(bf16_bits_to_float(v));
+  }
+  __device__ static __forceinline__ bool finite(uint16_t v) { return (v & 0x7f80u) != 0x7f80u; }
+};
+template <>
+struct InType<float> {
+  static constexpr int code = QARVD_F32;
+  __device__ static __forceinline__ double to_double(float v) { return static_cast<double>(v); }
+  __device__ static __forceinline__ bool finite(float v) { return isfinite(v); }
+};
+template <>
+struct InType<double> {
+  static constexpr int code = QARVD_F64;
+  __device__ static __forceinline__ double to_double(double v) { return v; }
+  __device__ static __forceinline__ bool finite(double v) { return isfinite(v); }
+};
+
+}  // namespace qarvd_b200

@@ -1,0 +1,340 @@
+// K3 — per-layer outlier detection, batched over layers.
+//
+// Reference: analyze_layer (outlier.cpp:98-102) =
+//   channel_l2_norms(W, 1)            tensor.cpp:132-150  (f64, rows summed in order i = 0..n-1)
+//   mad / sorted_median               outlier.cpp:13-18, :30-38
+//   threshold = max(med + (tau/0.6745)*MAD, alpha*med)   outlier.cpp:46-47 / :91-92
+//   raw = {j : v_j > threshold}       outlier.cpp:48-51
+//   align_outliers                    outlier.cpp:54-78
+// Every floating operation below is the reference's operation with explicit
+// round-to-nearest intrinsics (no FMA contraction), so norms, median, MAD,
+// threshold and both index sets are bit-identical to the f64 CPU code.
+//
+// Kernel 1 (HBM-bound): one thread owns 8 adjacent columns (one 16-byte bf16
+// load per row, a warp covers 512 contiguous bytes of a row) and accumulates
+// the 8 column sums sequentially over the rows, exactly the reference order.
+// For bf16/f32 inputs w*w is exact in f64, so the sum is the only rounding.
+// Kernel 2 (tiny): one 1024-thread CTA per layer sorts the K norms (bitonic,
+// shared memory) for the medians and runs the selection / alignment.
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qarvd_b200 {
+namespace {
+
+constexpr int kNormThreads = 256;
+constexpr int kSelThreads = 1024;
+constexpr int kMaxSelK = 16384;
+
+struct NormJobDev {
+  const void* w;
+  int64_t n, k, ldw;
+  double* norms;
+  int64_t col_groups;   // ceil(k / 8)
+  int64_t group_begin;  // prefix over jobs
+};
+
+template <typename T>
+__device__ __forceinline__ double sq(T v) {
+  const double d = InType<T>::to_double(v);
+  return __dmul_rn(d, d);
+}
+
+// grid-stride over the concatenated 8-column groups of all jobs
+template <typename T>
+__global__ void __launch_bounds__(kNormThreads)
+    column_norms_kernel(const NormJobDev* __restrict__ jobs, int num_jobs, int64_t total_groups) {
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total_groups;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // locate the job (few jobs; linear scan over prefix offsets)
+    int j = 0;
+    while (j + 1 < num_jobs && jobs[j + 1].group_begin <= g) ++j;
+    const NormJobDev job = jobs[j];
+    const int64_t c0 = (g - job.group_begin) * 8;
+    const T* w = static_cast<const T*>(job.w);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool full = (c0 + 8 <= job.k);
+    const bool vec = full && sizeof(T) == 2 && ((job.ldw & 7) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    if (vec) {
+      const uint16_t* base = reinterpret_cast<const uint16_t*>(w) + c0;
+      int64_t i = 0;
+      for (; i + 4 <= job.n; i += 4) {
+        uint4 d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          d[u] = __ldg(reinterpret_cast<const uint4*>(base + (i + u) * job.ldw));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t wd[4] = {d[u].x, d[u].y, d[u].z, d[u].w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            acc[2 * h] = __dadd_rn(acc[2 * h], sq<uint16_t>(static_cast<uint16_t>(wd[h] & 0xffffu)));
+            acc[2 * h + 1] = __dadd_rn(acc[2 * h + 1], sq<uint16_t>(static_cast<uint16_t>(wd[h] >> 16)));
+          }
+        }
+      }
+      for (; i < job.n; ++i) {
+        const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + i * job.ldw));
+        const uint32_t wd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          acc[2 * h] = __dadd_rn(acc[2 * h], sq<uint16_t>(static_cast<uint16_t>(wd[h] & 0xffffu)));
+          acc[2 * h + 1] = __dadd_rn(acc[2 * h + 1], sq<uint16_t>(static_cast<uint16_t>(wd[h] >> 16)));
+        }
+      }
+    } else {
+      const int cols = full ? 8 : static_cast<int>(job.k - c0);
+      for (int64_t i = 0; i < job.n; ++i) {
+        const T* row = w + i * job.ldw + c0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e < cols) acc[e] = __dadd_rn(acc[e], sq<T>(row[e]));
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (c0 + e < job.k) job.norms[c0 + e] = __dsqrt_rn(acc[e]);
+  }
+}
+
+// ---- selection -------------------------------------------------------------
+__device__ __forceinline__ void bitonic_sort_u64(unsigned long long* s, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = ((lo & size) == 0);
+        const unsigned long long a = s[lo], b = s[hi];
+        if ((a > b) == asc) {
+          s[lo] = b;
+          s[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// sorted_median (outlier.cpp:13-18) over an ascending array of non-negative doubles
+__device__ __forceinline__ double median_sorted(const unsigned long long* s, int n) {
+  if (n & 1) return __longlong_as_double(static_cast<long long>(s[n / 2]));
+  const double a = __longlong_as_double(static_cast<long long>(s[n / 2 - 1]));
+  const double b = __longlong_as_double(static_cast<long long>(s[n / 2]));
+  return __dmul_rn(0.5, __dadd_rn(a, b));
+}
+
+// block-wide ordered compaction: writes indices i (ascending) with pred(i) true
+template <typename Pred>
+__device__ int compact_indices(int k, Pred pred, int32_t* out, int* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int base = 0;
+  for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool f = (i < k) && pred(i);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) off += warp_tot[w];
+      tot += warp_tot[w];
+    }
+    if (f) out[base + off + __popc(bal & ((1u << lane) - 1u))] = i;
+    base += tot;
+    __syncthreads();
+  }
+  return base;
+}
+
+struct SelJobDev {
+  int64_t k;
+  const double* norms;
+  double* stats;
+  int32_t* counts;
+  int32_t* raw_idx;
+  int32_t* aligned_idx;
+};
+
+__global__ void __launch_bounds__(kSelThreads)
+    select_outliers_kernel(const SelJobDev* __restrict__ jobs, double tau, double alpha_min,
+                           int64_t align) {
+  extern __shared__ unsigned long long sbuf[];
+  __shared__ int warp_tot[32];
+  __shared__ double s_val[4];
+  const SelJobDev job = jobs[blockIdx.x];
+  const int k = static_cast<int>(job.k);
+  int P = 1;
+  while (P < k) P <<= 1;
+  const double* v = job.norms;
+
+  // median of norms
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(v[i])) : ~0ull;
+  __syncthreads();
+  bitonic_sort_u64(sbuf, P);
+  if (threadIdx.x == 0) s_val[0] = median_sorted(sbuf, k);
+  __syncthreads();
+  const double med = s_val[0];
+
+  // MAD = median |v - med|   (outlier.cpp:35-36)
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(v[i], med))))
+                    : ~0ull;
+  __syncthreads();
+  bitonic_sort_u64(sbuf, P);
+  if (threadIdx.x == 0) {
+    const double mad = median_sorted(sbuf, k);
+    const double zc = __ddiv_rn(tau, 0.6745);  // kModifiedZScoreFactor (outlier.hpp:13)
+    const double a = __dadd_rn(med, __dmul_rn(zc, mad));
+    const double b = __dmul_rn(alpha_min, med);
+    s_val[1] = mad;
+    s_val[2] = (a < b) ? b : a;  // std::max
+  }
+  __syncthreads();
+  const double thr = s_val[2];
+
+  // raw outliers, ascending (outlier.cpp:48-51)
+  const int R = compact_indices(k, [&](int i) { return v[i] > thr; }, job.raw_idx, warp_tot);
+
+  // align_outliers (outlier.cpp:54-78)
+  int A;
+  const int64_t al = align;
+  bool use_raw = (R == 0) || (k < 2 * al);
+  int64_t target = ((R + al - 1) / al) * al;
+  if (!use_raw) {
+    const int64_t cap = k - al;
+    if (target > cap) {
+      target = (cap / al) * al;
+      if (target < R) use_raw = true;
+    }
+  }
+  if (R == 0) {
+    A = 0;
+  } else if (use_raw) {
+    for (int i = threadIdx.x; i < R; i += blockDim.x) job.aligned_idx[i] = job.raw_idx[i];
+    A = R;
+  } else {
+    // the `target` largest norms, ties -> lower index: pivot value = target-th largest
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+      sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(v[i])) : ~0ull;
+    __syncthreads();
+    bitonic_sort_u64(sbuf, P);
+    const unsigned long long pivot = sbuf[k - target];
+    __syncthreads();
+    // count strictly greater, then take equal ones in index order
+    const double pv = __longlong_as_double(static_cast<long long>(pivot));
+    // number of values > pivot = k - (index of first element > pivot in sorted order)
+    if (threadIdx.x == 0) {
+      int lo = k - static_cast<int>(target), hi = k;  // first index with value > pivot in [lo, k]
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sbuf[mid] > pivot) hi = mid;
+        else lo = mid + 1;
+      }
+      warp_tot[0] = static_cast<int>(target) - (k - lo);  // equal ones to take
+    }
+    __syncthreads();
+    const int need_eq = warp_tot[0];
+    __syncthreads();
+    // rank of each equal element among equals (index order) via compaction into sbuf scratch
+    int32_t* eq_idx = reinterpret_cast<int32_t*>(sbuf);
+    const int n_eq = compact_indices(k, [&](int i) { return v[i] == pv; }, eq_idx, warp_tot);
+    (void)n_eq;
+    // mark: greater, or one of the first need_eq equals
+    // (eq_idx is ascending; membership test by binary search)
+    A = compact_indices(
+        k,
+        [&](int i) {
+          const double x = v[i];
+          if (x > pv) return true;
+          if (x != pv) return false;
+          int lo = 0, hi = need_eq;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (eq_idx[mid] < i) lo = mid + 1;
+            else hi = mid;
+          }
+          return lo < need_eq && eq_idx[lo] == i;
+        },
+        job.aligned_idx, warp_tot);
+  }
+  if (threadIdx.x == 0) {
+    job.stats[0] = med;
+    job.stats[1] = s_val[1];
+    job.stats[2] = thr;
+    job.counts[0] = R;
+    job.counts[1] = A;
+  }
+}
+
+}  // namespace
+}  // namespace qarvd_b200
+
+using namespace qarvd_b200;
+
+extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs, int w_dtype,
+                                    double tau, double alpha_min, int64_t align, void* stream) {
+  clear_error();
+  if (num_jobs < 0 || (num_jobs > 0 && !jobs))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "analyze_layers: invalid job list");
+  if (!(tau > 0.0)) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "detect_outliers: tau must be positive");
+  if (!(alpha_min > 1.0))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "detect_outliers: alpha_min must exceed 1");
+  if (align == 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "align_outliers: align must be >= 1");
+  if (w_dtype != QARVD_BF16 && w_dtype != QARVD_F32 && w_dtype != QARVD_F64)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "analyze_layers: unknown dtype");
+  if (num_jobs == 0) return QARVD_OK;
+  std::vector<NormJobDev> nj(num_jobs);
+  std::vector<SelJobDev> sj(num_jobs);
+  int64_t groups = 0;
+  int64_t max_k = 0;
+  for (int i = 0; i < num_jobs; ++i) {
+    const qarvd_outlier_job& J = jobs[i];
+    if (J.k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "mad: empty vector");
+    if (J.n <= 0 || J.ldw < J.k || !J.w || !J.norms || !J.stats || !J.counts || !J.raw_idx ||
+        !J.aligned_idx)
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "analyze_layers: invalid job " + std::to_string(i));
+    if (J.k > kMaxSelK)
+      QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "analyze_layers: d_in above 16384 is not supported");
+    nj[i] = NormJobDev{J.w, J.n, J.k, J.ldw, J.norms, (J.k + 7) / 8, groups};
+    groups += (J.k + 7) / 8;
+    sj[i] = SelJobDev{J.k, J.norms, J.stats, J.counts, J.raw_idx, J.aligned_idx};
+    if (J.k > max_k) max_k = J.k;
+  }
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  void* dev = nullptr;
+  const size_t bytes = num_jobs * (sizeof(NormJobDev) + sizeof(SelJobDev));
+  QARVD_CUDA_TRY(cudaMallocAsync(&dev, bytes, s));
+  NormJobDev* d_nj = static_cast<NormJobDev*>(dev);
+  SelJobDev* d_sj = reinterpret_cast<SelJobDev*>(d_nj + num_jobs);
+  QARVD_CUDA_TRY(cudaMemcpyAsync(d_nj, nj.data(), num_jobs * sizeof(NormJobDev),
+                                 cudaMemcpyHostToDevice, s));
+  QARVD_CUDA_TRY(cudaMemcpyAsync(d_sj, sj.data(), num_jobs * sizeof(SelJobDev),
+                                 cudaMemcpyHostToDevice, s));
+  const int64_t blocks_needed = (groups + kNormThreads - 1) / kNormThreads;
+  const int grid = static_cast<int>(blocks_needed < kNumSMs * 8 ? blocks_needed : kNumSMs * 8);
+  if (w_dtype == QARVD_BF16)
+    column_norms_kernel<uint16_t><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
+  else if (w_dtype == QARVD_F32)
+    column_norms_kernel<float><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
+  else
+    column_norms_kernel<double><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  int P = 1;
+  while (P < max_k) P <<= 1;
+  const size_t smem = static_cast<size_t>(P) * sizeof(unsigned long long);
+  QARVD_CUDA_TRY(cudaFuncSetAttribute(select_outliers_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMaxSelK * static_cast<int>(sizeof(unsigned long long))));
+  select_outliers_kernel<<<num_jobs, kSelThreads, smem, s>>>(d_sj, tau, alpha_min, align);
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  QARVD_CUDA_TRY(cudaFreeAsync(dev, s));
+  return QARVD_OK;
+}

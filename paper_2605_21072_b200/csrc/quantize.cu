@@ -1,0 +1,393 @@
+// K1 (activation quantization fused with the dual-scale permutation) and
+// K5 (dual-scale weight preparation): both are one HBM-bound pass of
+// "row absmax -> scale -> round-half-even codes in gathered order".
+//
+// Reference semantics:
+//   K1 = quantize(permute_activations(x, plan), p)   engine.cpp:32-44, quant.cpp:113-138
+//        with p per-token = init_scale_minmax(x, b, per_channel, 0) (quant.cpp:170-182)
+//        or per-tensor static p (engine.cpp:57).
+//   K5 = row_scales_over_columns over the outlier and normal column groups
+//        (dual_scale.cpp:13-24, :58-90) + nearest codes as in fake_quant_dual
+//        (dual_scale.cpp:92-114), stored pre-permuted (calibrate.cpp:474-480).
+//
+// Layout: bf16 rows are staged once into shared memory with 16-byte coalesced
+// loads (one warp per row), the row absmax is a warp-shuffle reduction, and
+// each lane then emits 16 consecutive output codes (one 16-byte store) by
+// gathering through `gather` from the shared-memory copy.
+#include <cuda_bf16.h>
+
+#include <climits>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace qarvd_b200 {
+namespace {
+
+enum Mode { kActPerToken = 0, kActStatic = 1, kWeightDual = 2 };
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kMaxSmemK = 16384;  // bf16 elements staged per warp (32 KB)
+
+__device__ __forceinline__ void record_error(unsigned long long* err, int64_t flat) {
+  if (err) atomicMin(err, static_cast<unsigned long long>(flat));
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Scale of one group from its absmax a (exact bf16 value as float):
+// s64 = a / qmax in f64 (quant.cpp:168/181), DBL_MIN for a == 0 (quant.cpp:164);
+// r32 = qmax / a in fp32 for the fast path; exact = r32 unusable (not normal).
+struct GroupScale {
+  double s64;
+  float s32;
+  float r32;
+  bool exact;
+};
+__device__ __forceinline__ GroupScale scale_from_absmax(float a, int qmax) {
+  GroupScale g;
+  if (a > 0.f) {
+    g.s64 = __ddiv_rn(static_cast<double>(a), static_cast<double>(qmax));
+    g.s32 = __double2float_rn(g.s64);
+    g.r32 = __fdiv_rn(static_cast<float>(qmax), a);
+    g.exact = !(g.r32 <= FLT_MAX && g.r32 >= FLT_MIN);
+  } else {
+    g.s64 = DBL_MIN;
+    g.s32 = 0.f;  // all codes are 0; the epilogue product is 0 either way
+    g.r32 = 0.f;
+    g.exact = false;
+  }
+  return g;
+}
+__device__ __forceinline__ GroupScale scale_static(double s64) {
+  GroupScale g;
+  g.s64 = s64;
+  g.s32 = __double2float_rn(s64);
+  const double r = 1.0 / s64;
+  g.r32 = __double2float_rn(r);
+  g.exact = !(r <= static_cast<double>(FLT_MAX) && r >= static_cast<double>(FLT_MIN));
+  return g;
+}
+
+__device__ __forceinline__ int code_of(float v, const GroupScale& g, int qmax) {
+  if (g.exact) return quant_code_exact(static_cast<double>(v), g.s64, qmax);
+  return quant_code_fast(v, g.r32, g.s64, qmax);
+}
+
+// ---------------------------------------------------------------------------
+// bf16 fast kernel: one warp per row, row staged in shared memory.
+template <int MODE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    quant_rows_bf16_kernel(const uint16_t* __restrict__ x, int64_t m, int64_t k, int64_t ldx,
+                           const int32_t* __restrict__ gather, int64_t k_out, int64_t k_o,
+                           double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
+                           float* __restrict__ s32_o, double* __restrict__ s64_o,
+                           float* __restrict__ s32_n, double* __restrict__ s64_n,
+                           unsigned long long* err) {
+  extern __shared__ uint4 smem_rows[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t kstride = (k + 7) & ~int64_t(7);
+  uint16_t* row_s = reinterpret_cast<uint16_t*>(smem_rows) + warp * kstride;
+  const bool vec_in = ((ldx & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool vec_out = ((ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(q) & 15) == 0) &&
+                       (gather == nullptr || (reinterpret_cast<uintptr_t>(gather) & 15) == 0);
+
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp; row < m;
+       row += static_cast<int64_t>(gridDim.x) * kWarpsPerCta) {
+    const uint16_t* xr = x + row * ldx;
+    float amax = 0.f;
+    bool bad = false;
+    // ---- stage the row (16-byte coalesced loads) and take |x| max ----
+    if (vec_in) {
+      const int64_t nvec = k >> 3;
+      for (int64_t v = lane; v < nvec; v += 32) {
+        const uint4 d = __ldg(reinterpret_cast<const uint4*>(xr) + v);
+        reinterpret_cast<uint4*>(row_s)[v] = d;
+        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint16_t lo = static_cast<uint16_t>(w[h] & 0xffffu);
+          const uint16_t hi = static_cast<uint16_t>(w[h] >> 16);
+          bad |= !InType<uint16_t>::finite(lo) || !InType<uint16_t>::finite(hi);
+          amax = fmaxf(amax, fabsf(bf16_bits_to_float(lo)));
+          amax = fmaxf(amax, fabsf(bf16_bits_to_float(hi)));
+        }
+      }
+      for (int64_t c = (nvec << 3) + lane; c < k; c += 32) {
+        const uint16_t h = xr[c];
+        row_s[c] = h;
+        bad |= !InType<uint16_t>::finite(h);
+        amax = fmaxf(amax, fabsf(bf16_bits_to_float(h)));
+      }
+    } else {
+      for (int64_t c = lane; c < k; c += 32) {
+        const uint16_t h = xr[c];
+        row_s[c] = h;
+        bad |= !InType<uint16_t>::finite(h);
+        amax = fmaxf(amax, fabsf(bf16_bits_to_float(h)));
+      }
+    }
+    __syncwarp();
+
+    // ---- scales ----
+    GroupScale g_o, g_n;
+    if (MODE == kActPerToken) {
+      g_n = scale_from_absmax(warp_max(amax), qmax);
+      g_o = g_n;
+      if (lane == 0) {
+        if (s32_n) s32_n[row] = g_n.s32;
+        if (s64_n) s64_n[row] = g_n.s64;
+      }
+    } else if (MODE == kActStatic) {
+      g_n = scale_static(static_scale);
+      g_o = g_n;
+      if (lane == 0) {
+        if (s32_n) s32_n[row] = g_n.s32;
+        if (s64_n) s64_n[row] = g_n.s64;
+      }
+    } else {
+      // group absmax over the gathered columns: [0, k_o) outlier, [k_o, k_out) normal
+      float ao = 0.f, an = 0.f;
+      for (int64_t c = lane; c < k_out; c += 32) {
+        const int32_t src = gather ? __ldg(gather + c) : static_cast<int32_t>(c);
+        if (src < 0) continue;
+        const float v = fabsf(bf16_bits_to_float(row_s[src]));
+        if (c < k_o) ao = fmaxf(ao, v);
+        else an = fmaxf(an, v);
+      }
+      g_n = scale_from_absmax(warp_max(an), qmax);
+      g_o = k_o > 0 ? scale_from_absmax(warp_max(ao), qmax) : g_n;
+      if (lane == 0) {
+        if (s32_n) s32_n[row] = g_n.s32;
+        if (s64_n) s64_n[row] = g_n.s64;
+        if (s32_o) s32_o[row] = g_o.s32;
+        if (s64_o) s64_o[row] = g_o.s64;
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+
+    // ---- codes, 16 per lane per iteration ----
+    int8_t* qr = q + row * ldq;
+    for (int64_t c0 = static_cast<int64_t>(lane) * 16; c0 < k_out; c0 += 32 * 16) {
+      int32_t src[16];
+      if (gather && vec_out && c0 + 16 <= k_out) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int4 gi = __ldg(reinterpret_cast<const int4*>(gather + c0) + v);
+          src[4 * v] = gi.x;
+          src[4 * v + 1] = gi.y;
+          src[4 * v + 2] = gi.z;
+          src[4 * v + 3] = gi.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int64_t c = c0 + e;
+          src[e] = c < k_out ? (gather ? __ldg(gather + c) : static_cast<int32_t>(c)) : -1;
+        }
+      }
+      uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        int code = 0;
+        if (src[e] >= 0) {
+          const uint16_t h = row_s[src[e]];
+          if (bad && !InType<uint16_t>::finite(h)) record_error(err, row * k_out + c0 + e);
+          const bool outl = (MODE == kWeightDual) && (c0 + e < k_o);
+          code = code_of(bf16_bits_to_float(h), outl ? g_o : g_n, qmax);
+        }
+        packed[e >> 2] |= (static_cast<uint32_t>(code) & 0xffu) << (8 * (e & 3));
+      }
+      if (vec_out && c0 + 16 <= k_out) {
+        *reinterpret_cast<uint4*>(qr + c0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        for (int e = 0; e < 16 && c0 + e < k_out; ++e)
+          qr[c0 + e] = static_cast<int8_t>((packed[e >> 2] >> (8 * (e & 3))) & 0xffu);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic kernel (f32 / f64 inputs, or rows too wide for shared memory):
+// one warp per row, reads straight from global memory; f64 inputs always take
+// the exact division (reference f64 semantics, no bf16 assumption).
+template <int MODE, typename T>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    quant_rows_generic_kernel(const T* __restrict__ x, int64_t m, int64_t k, int64_t ldx,
+                              const int32_t* __restrict__ gather, int64_t k_out, int64_t k_o,
+                              double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
+                              float* __restrict__ s32_o, double* __restrict__ s64_o,
+                              float* __restrict__ s32_n, double* __restrict__ s64_n,
+                              unsigned long long* err) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp; row < m;
+       row += static_cast<int64_t>(gridDim.x) * kWarpsPerCta) {
+    const T* xr = x + row * ldx;
+    double s_o64, s_n64;
+    if (MODE == kActStatic) {
+      s_o64 = s_n64 = static_scale;
+    } else {
+      double ao = 0.0, an = 0.0;
+      for (int64_t c = lane; c < k_out; c += 32) {
+        const int32_t src = gather ? __ldg(gather + c) : static_cast<int32_t>(c);
+        if (src < 0) continue;
+        const double v = fabs(InType<T>::to_double(xr[src]));
+        if (!(v <= DBL_MAX)) continue;  // non-finite: reported below
+        if (MODE == kWeightDual && c < k_o) ao = fmax(ao, v);
+        else an = fmax(an, v);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ao = fmax(ao, __shfl_xor_sync(0xffffffffu, ao, o));
+        an = fmax(an, __shfl_xor_sync(0xffffffffu, an, o));
+      }
+      s_n64 = an > 0.0 ? __ddiv_rn(an, static_cast<double>(qmax)) : DBL_MIN;
+      s_o64 = (MODE == kWeightDual && k_o > 0)
+                  ? (ao > 0.0 ? __ddiv_rn(ao, static_cast<double>(qmax)) : DBL_MIN)
+                  : s_n64;
+    }
+    if (lane == 0) {
+      if (s32_n) s32_n[row] = s_n64 == DBL_MIN ? 0.f : __double2float_rn(s_n64);
+      if (s64_n) s64_n[row] = s_n64;
+      if (MODE == kWeightDual) {
+        if (s32_o) s32_o[row] = s_o64 == DBL_MIN ? 0.f : __double2float_rn(s_o64);
+        if (s64_o) s64_o[row] = s_o64;
+      }
+    }
+    int8_t* qr = q + row * ldq;
+    for (int64_t c = lane; c < k_out; c += 32) {
+      const int32_t src = gather ? __ldg(gather + c) : static_cast<int32_t>(c);
+      int code = 0;
+      if (src >= 0) {
+        const T v = xr[src];
+        if (!InType<T>::finite(v)) {
+          record_error(err, row * k_out + c);
+        } else {
+          const double s = (MODE == kWeightDual && c < k_o) ? s_o64 : s_n64;
+          code = quant_code_exact(InType<T>::to_double(v), s, qmax);
+        }
+      }
+      qr[c] = static_cast<int8_t>(code);
+    }
+  }
+}
+
+__global__ void init_err_kernel(unsigned long long* err) { *err = 0x7fffffffffffffffull; }
+
+int grid_for_rows(int64_t m) {
+  const int64_t ctas = (m + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t cap = static_cast<int64_t>(kNumSMs) * 16;
+  return static_cast<int>(ctas < cap ? ctas : cap);
+}
+
+template <int MODE>
+int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, const int32_t* gather,
+                int64_t k_out, int64_t k_o, double static_scale, int bits, int8_t* q, int64_t ldq,
+                float* s32_o, double* s64_o, float* s32_n, double* s64_n, int64_t* err_index,
+                cudaStream_t stream) {
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, stream>>>(err);
+    count_launch();
+  }
+  if (m == 0) return QARVD_OK;
+  const int grid = grid_for_rows(m);
+  if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
+    const size_t smem = static_cast<size_t>(kWarpsPerCta) * (((k + 7) & ~int64_t(7)) * 2);
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+      attr = cudaFuncSetAttribute(quant_rows_bf16_kernel<MODE>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kWarpsPerCta * kMaxSmemK * 2);
+    });
+    QARVD_CUDA_TRY(attr);
+    quant_rows_bf16_kernel<MODE><<<grid, kWarpsPerCta * 32, smem, stream>>>(
+        static_cast<const uint16_t*>(x), m, k, ldx, gather, k_out, k_o, static_scale, qmax, q,
+        ldq, s32_o, s64_o, s32_n, s64_n, err);
+  } else if (dtype == QARVD_BF16) {
+    quant_rows_generic_kernel<MODE, uint16_t><<<grid, kWarpsPerCta * 32, 0, stream>>>(
+        static_cast<const uint16_t*>(x), m, k, ldx, gather, k_out, k_o, static_scale, qmax, q,
+        ldq, s32_o, s64_o, s32_n, s64_n, err);
+  } else if (dtype == QARVD_F32) {
+    quant_rows_generic_kernel<MODE, float><<<grid, kWarpsPerCta * 32, 0, stream>>>(
+        static_cast<const float*>(x), m, k, ldx, gather, k_out, k_o, static_scale, qmax, q, ldq,
+        s32_o, s64_o, s32_n, s64_n, err);
+  } else {
+    quant_rows_generic_kernel<MODE, double><<<grid, kWarpsPerCta * 32, 0, stream>>>(
+        static_cast<const double*>(x), m, k, ldx, gather, k_out, k_o, static_scale, qmax, q, ldq,
+        s32_o, s64_o, s32_n, s64_n, err);
+  }
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  return QARVD_OK;
+}
+
+int check_common(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, int64_t k_out,
+                 int bits, const int8_t* q, int64_t ldq, const int32_t* gather) {
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED,
+               "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (dtype != QARVD_BF16 && dtype != QARVD_F32 && dtype != QARVD_F64)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "unknown input dtype");
+  if (m < 0 || k <= 0 || k_out <= 0 || ldx < k || ldq < k_out)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "invalid shape or leading dimension");
+  if (!gather && k_out != k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "permute_activations: plan does not match activation width");
+  if ((m > 0) && (!x || !q)) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "null pointer argument");
+  return QARVD_OK;
+}
+
+}  // namespace
+}  // namespace qarvd_b200
+
+using namespace qarvd_b200;
+
+extern "C" int qarvd_quantize_act(const void* x, int x_dtype, int64_t m, int64_t k, int64_t ldx,
+                                  const int32_t* gather, int64_t k_out, int granularity,
+                                  double static_scale, int bits, int8_t* xq, int64_t ldq,
+                                  float* scale_f32, double* scale_f64, int64_t* err_index,
+                                  void* stream) {
+  clear_error();
+  if (int st = check_common(x, x_dtype, m, k, ldx, k_out, bits, xq, ldq, gather)) return st;
+  if (granularity == QARVD_ACT_PER_TENSOR) {
+    if (!(static_scale > 0.0) || !(static_scale <= DBL_MAX))
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quant params: scale must be positive and finite");
+  } else if (granularity != QARVD_ACT_PER_TOKEN) {
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "unknown activation granularity");
+  }
+  if (int st = require_device()) return st;
+  if (granularity == QARVD_ACT_PER_TOKEN)
+    return launch_rows<kActPerToken>(x, x_dtype, m, k, ldx, gather, k_out, 0, 0.0, bits, xq, ldq,
+                                     nullptr, nullptr, scale_f32, scale_f64, err_index,
+                                     as_stream(stream));
+  return launch_rows<kActStatic>(x, x_dtype, m, k, ldx, gather, k_out, 0, static_scale, bits, xq,
+                                 ldq, nullptr, nullptr, scale_f32, scale_f64, err_index,
+                                 as_stream(stream));
+}
+
+extern "C" int qarvd_prepare_weights(const void* w, int w_dtype, int64_t n, int64_t k, int64_t ldw,
+                                     const int32_t* gather, int64_t k_pad, int64_t k_outlier,
+                                     int bits, int8_t* wq, int64_t ldq, double* scale_outlier_f64,
+                                     double* scale_normal_f64, float* scale_outlier_f32,
+                                     float* scale_normal_f32, int64_t* err_index, void* stream) {
+  clear_error();
+  if (int st = check_common(w, w_dtype, n, k, ldw, k_pad, bits, wq, ldq, gather)) return st;
+  if (k_outlier < 0 || k_outlier >= k_pad)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "build_plan: outlier set would leave no normal channels");
+  if (int st = require_device()) return st;
+  return launch_rows<kWeightDual>(w, w_dtype, n, k, ldw, gather, k_pad, k_outlier, 0.0, bits, wq,
+                                  ldq, scale_outlier_f32, scale_outlier_f64, scale_normal_f32,
+                                  scale_normal_f64, err_index, as_stream(stream));
+}

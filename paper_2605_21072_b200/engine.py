@@ -1,0 +1,273 @@
+"""Host-side mirror of the reference's quantized-linear operator API.
+
+Reference interface (``/root/reference/proj/core/include/qarvd/engine.hpp``):
+
+* ``kernel_a_quantize_activation(x, p)``   engine.hpp:43  -> :func:`kernel_a_quantize_activation`
+* ``kernel_b_gemm_dequant(xq, layer)``      engine.hpp:48  -> :func:`kernel_b_gemm_dequant`
+* ``permute_activations(x, plan)``          engine.hpp:51  -> folded into K1 via ``plan.gather``
+* ``quantized_layer_forward(layer, x, e)``  engine.hpp:60  -> :func:`quantized_layer_forward`
+* ``QuantizedLayer``                        engine.hpp:18-30 -> :class:`QuantizedLayer`
+* ``DualScalePlan`` / ``build_plan``         dual_scale.hpp:18-41 -> :class:`DualScalePlan`, :func:`build_plan`
+
+Tensors are device-resident torch tensors (torch is the allocator / stream
+provider only); every computation runs in libqarvd_b200.so through the C-ABI.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+QMAX8 = 127
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.BF16
+    if t.dtype == torch.float32:
+        return _lib.F32
+    if t.dtype == torch.float64:
+        return _lib.F64
+    raise _lib.InvalidArgument(f"unsupported input dtype {t.dtype}")
+
+
+def _round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+@dataclass
+class DualScalePlan:
+    """Split of a layer's input channels (dual_scale.hpp:18-31).
+
+    ``permutation`` is [sorted outliers | sorted normals] over original column
+    ids (dual_scale.cpp:81-83).  ``gather`` is the padded device layout the
+    kernels consume: [outliers, -1 pad to a multiple of 32, normals, -1 pad to a
+    multiple of 32]; ``k_outlier`` is the padded outlier-slab width and
+    ``k_pad`` the padded K.  Zero-code pad columns leave every dot product
+    unchanged, so unaligned outlier sets (outlier.cpp:59, :63-66) stay exact.
+    """
+
+    layer_name: str
+    enabled: bool
+    d_in: int
+    outlier_indices: np.ndarray
+    normal_indices: np.ndarray
+    permutation: np.ndarray
+    gather: np.ndarray = field(repr=False, default=None)
+    k_outlier: int = 0
+    k_pad: int = 0
+
+    def outlier_count(self) -> int:
+        return int(len(self.outlier_indices))
+
+    def inverse_permutation(self) -> np.ndarray:
+        inv = np.empty_like(self.permutation)
+        inv[self.permutation] = np.arange(len(self.permutation), dtype=self.permutation.dtype)
+        return inv
+
+
+def build_plan(layer_name: str, d_in: int, aligned_outliers: Sequence[int]) -> DualScalePlan:
+    """Column split of build_plan / build_single_scale_plan (dual_scale.cpp:44-90).
+
+    The per-row group scales are computed on the device by
+    :func:`prepare_weights` (row_scales_over_columns, dual_scale.cpp:13-24).
+    """
+    outl = np.asarray(sorted(int(i) for i in aligned_outliers), dtype=np.int64)
+    if outl.size and (outl.min() < 0 or outl.max() >= d_in):
+        raise _lib.OutOfRange("build_plan: outlier index out of range")
+    if outl.size == 0:
+        perm = np.arange(d_in, dtype=np.uint32)
+        k_pad = _round_up(d_in, 32)
+        gather = np.full(k_pad, -1, dtype=np.int32)
+        gather[:d_in] = np.arange(d_in, dtype=np.int32)
+        return DualScalePlan(layer_name, False, d_in, outl, np.arange(d_in, dtype=np.int64),
+                             perm, gather, 0, k_pad)
+    mask = np.zeros(d_in, dtype=bool)
+    mask[outl] = True
+    normals = np.nonzero(~mask)[0].astype(np.int64)
+    if normals.size == 0:
+        raise _lib.InvalidArgument("build_plan: outlier set would leave no normal channels")
+    perm = np.concatenate([outl, normals]).astype(np.uint32)
+    k_o = _round_up(outl.size, 32)
+    k_pad = k_o + _round_up(normals.size, 32)
+    gather = np.full(k_pad, -1, dtype=np.int32)
+    gather[: outl.size] = outl
+    gather[k_o: k_o + normals.size] = normals
+    return DualScalePlan(layer_name, True, d_in, outl, normals, perm, gather, k_o, k_pad)
+
+
+@dataclass
+class QuantizedLayer:
+    """Device-resident deployed layer (engine.hpp:18-30).
+
+    ``wq`` holds the pre-permuted int8 codes [out_dim x k_pad]; group scales are
+    kept in f64 (the reference's in-memory precision) and f32 (the QARQ on-disk
+    precision, engine.cpp:225-233, which the GEMM epilogue uses).
+    """
+
+    name: str
+    out_dim: int
+    in_dim: int
+    plan: DualScalePlan
+    wq: torch.Tensor
+    scale_outlier64: torch.Tensor
+    scale_normal64: torch.Tensor
+    scale_outlier32: torch.Tensor
+    scale_normal32: torch.Tensor
+    gather_dev: torch.Tensor
+    act_granularity: int = _lib.ACT_PER_TOKEN
+    act_scale: float = 0.0
+    bias: Optional[torch.Tensor] = None
+
+    @property
+    def k_pad(self) -> int:
+        return self.plan.k_pad
+
+    @property
+    def k_outlier(self) -> int:
+        return self.plan.k_outlier
+
+
+def _check_err(err: torch.Tensor, what: str) -> None:
+    v = int(err.item())
+    if v != 0x7FFFFFFFFFFFFFFF:
+        raise _lib.InvalidArgument(f"{what}: non-finite input at flat index {v}")
+
+
+def prepare_weights(name: str, w: torch.Tensor, plan: DualScalePlan, bits: int = 8,
+                    check_finite: bool = True) -> QuantizedLayer:
+    """K5: group scales + nearest codes, pre-permuted (dual_scale.cpp:13-114, calibrate.cpp:474-480)."""
+    n, k = w.shape
+    if k != plan.d_in:
+        raise _lib.InvalidArgument("build_plan: report does not match the weight's input width")
+    dev = w.device
+    gather = torch.from_numpy(plan.gather).to(dev)
+    wq = torch.empty((n, plan.k_pad), dtype=torch.int8, device=dev)
+    so64 = torch.empty(n, dtype=torch.float64, device=dev)
+    sn64 = torch.empty(n, dtype=torch.float64, device=dev)
+    so32 = torch.empty(n, dtype=torch.float32, device=dev)
+    sn32 = torch.empty(n, dtype=torch.float32, device=dev)
+    err = torch.empty(1, dtype=torch.int64, device=dev) if check_finite else None
+    _lib.call("qarvd_prepare_weights", w.data_ptr(), _dtype_code(w), n, k, w.stride(0),
+              gather.data_ptr(), plan.k_pad, plan.k_outlier, bits, wq.data_ptr(), plan.k_pad,
+              so64.data_ptr(), sn64.data_ptr(), so32.data_ptr(), sn32.data_ptr(), _ptr(err),
+              _stream())
+    if err is not None:
+        v = int(err.item())
+        if v != 0x7FFFFFFFFFFFFFFF:
+            raise _lib.InvalidArgument("fake_quant_dual: non-finite weight element")
+    return QuantizedLayer(name, n, k, plan, wq, so64, sn64, so32, sn32, gather)
+
+
+def kernel_a_quantize_activation(x: torch.Tensor, layer_or_plan, granularity: int = _lib.ACT_PER_TOKEN,
+                                 static_scale: float = 0.0, bits: int = 8,
+                                 check_finite: bool = False):
+    """K1 = quantize(permute_activations(x, plan), p) (engine.cpp:32-44, quant.cpp:113-138).
+
+    Returns (xq int8 [m x k_pad], scale_f32 [m], scale_f64 [m]).
+    """
+    plan = layer_or_plan.plan if isinstance(layer_or_plan, QuantizedLayer) else layer_or_plan
+    gather_dev = (layer_or_plan.gather_dev if isinstance(layer_or_plan, QuantizedLayer)
+                  else torch.from_numpy(plan.gather).to(x.device))
+    m, k = x.shape
+    if k != plan.d_in:
+        raise _lib.InvalidArgument("permute_activations: plan does not match activation width")
+    xq = torch.empty((m, plan.k_pad), dtype=torch.int8, device=x.device)
+    s32 = torch.empty(m, dtype=torch.float32, device=x.device)
+    s64 = torch.empty(m, dtype=torch.float64, device=x.device)
+    err = torch.empty(1, dtype=torch.int64, device=x.device) if check_finite else None
+    _lib.call("qarvd_quantize_act", x.data_ptr(), _dtype_code(x), m, k, x.stride(0),
+              gather_dev.data_ptr(), plan.k_pad, granularity, float(static_scale), bits,
+              xq.data_ptr(), plan.k_pad, s32.data_ptr(), s64.data_ptr(), _ptr(err), _stream())
+    if err is not None:
+        _check_err(err, "quantize")
+    return xq, s32, s64
+
+
+def kernel_b_gemm_dequant(xq: torch.Tensor, scale_x: torch.Tensor, layer: QuantizedLayer,
+                          out_dtype=torch.bfloat16, epilogue: int = _lib.EPI_NONE,
+                          bias: Optional[torch.Tensor] = None, dump_acc: bool = False):
+    """K2 (engine.cpp:46-105): dual-slab int8 tensor-core GEMM + fused dequant / bias epilogue.
+
+    Returns y, or (y, acc_outlier, acc_normal) with ``dump_acc``.
+    """
+    m = xq.shape[0]
+    n = layer.out_dim
+    y = torch.empty((m, n), dtype=out_dtype, device=xq.device)
+    acc_o = torch.zeros((m, n), dtype=torch.int32, device=xq.device) if dump_acc else None
+    acc_n = torch.zeros((m, n), dtype=torch.int32, device=xq.device) if dump_acc else None
+    b = bias if bias is not None else layer.bias
+    _lib.call("qarvd_dual_gemm", xq.data_ptr(), xq.stride(0), layer.wq.data_ptr(),
+              layer.wq.stride(0), m, n, layer.k_pad, layer.k_outlier, scale_x.data_ptr(),
+              layer.scale_outlier32.data_ptr(), layer.scale_normal32.data_ptr(), _ptr(b), epilogue,
+              _lib.BF16 if out_dtype == torch.bfloat16 else _lib.F32, y.data_ptr(), y.stride(0),
+              _ptr(acc_o), _ptr(acc_n), _stream())
+    if dump_acc:
+        return y, acc_o, acc_n
+    return y
+
+
+def quantized_layer_forward(layer: QuantizedLayer, x: torch.Tensor, out_dtype=torch.bfloat16,
+                            epilogue: int = _lib.EPI_NONE) -> torch.Tensor:
+    """quantized_layer_forward(layer, x, Engine::int_kernels) (engine.cpp:134-142): K1 -> K2."""
+    xq, s32, _ = kernel_a_quantize_activation(x, layer, layer.act_granularity, layer.act_scale)
+    return kernel_b_gemm_dequant(xq, s32, layer, out_dtype=out_dtype, epilogue=epilogue)
+
+
+class LinearHandle:
+    """qarvd_linear_t: K1 + K2 behind one C-ABI call, incl. the host-buffer entry."""
+
+    def __init__(self, layer: QuantizedLayer, epilogue: int = _lib.EPI_NONE):
+        self.layer = layer
+        h = _lib.ctypes.c_void_p()
+        _lib.call("qarvd_linear_create", layer.wq.data_ptr(), layer.out_dim, layer.k_pad,
+                  layer.k_outlier, layer.gather_dev.data_ptr(), layer.in_dim,
+                  layer.scale_outlier32.data_ptr(), layer.scale_normal32.data_ptr(),
+                  _ptr(layer.bias), layer.act_granularity, float(layer.act_scale), epilogue,
+                  _lib.ctypes.byref(h))
+        self.h = h
+
+    def forward(self, x: torch.Tensor, y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        m = x.shape[0]
+        if y is None:
+            y = torch.empty((m, self.layer.out_dim), dtype=torch.bfloat16, device=x.device)
+        _lib.call("qarvd_linear_forward", self.h, x.data_ptr(), m, y.data_ptr(), _stream())
+        return y
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """x_host / y_host: CPU bf16 tensors (pinned for full PCIe bandwidth)."""
+        _lib.call("qarvd_linear_forward_host", self.h, x_host.data_ptr(), x_host.shape[0],
+                  y_host.data_ptr(), _stream())
+        return y_host
+
+    def close(self):
+        if self.h:
+            _lib.call("qarvd_linear_destroy", self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def chain_forward_host(handles: Sequence[LinearHandle], x_host: torch.Tensor,
+                       y_host: torch.Tensor) -> torch.Tensor:
+    """qarvd_linear_chain_forward_host: one H2D, K1+K2 per layer, one D2H (synchronous)."""
+    arr = (_lib.ctypes.c_void_p * len(handles))(*[h.h for h in handles])
+    _lib.call("qarvd_linear_chain_forward_host", arr, len(handles), x_host.data_ptr(),
+              x_host.shape[0], y_host.data_ptr(), _stream())
+    return y_host

@@ -1,0 +1,79 @@
+"""Device-resident chains of quantized linears, replayed as one CUDA graph.
+
+``QuantizedChain`` is the deployment form of a sequence of
+``quantized_layer_forward`` calls (engine.cpp:134-142): for each layer K1
+(per-token quantize + permutation) then K2 (dual-slab tcgen05 GEMM + fused
+epilogue), with every intermediate buffer allocated once.  The whole forward
+is captured into a CUDA graph so a step costs one graph launch instead of 2L
+host-side kernel launches (the reference runs these as plain C++ calls,
+engine.cpp:155-165; on the GPU the launch latency would otherwise exceed the
+kernels themselves).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from .engine import QuantizedLayer, _ptr, _stream
+
+
+class QuantizedChain:
+    def __init__(self, layers: Sequence[QuantizedLayer], m: int,
+                 epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None):
+        """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1)."""
+        self.layers = list(layers)
+        self.m = m
+        self.epilogues = list(epilogues) if epilogues is not None else [_lib.EPI_NONE] * len(layers)
+        self.inputs = list(inputs) if inputs is not None else list(range(-1, len(layers) - 1))
+        dev = self.layers[0].wq.device
+        self.x = torch.empty((m, self.layers[0].in_dim), dtype=torch.bfloat16, device=dev)
+        self.xq = [torch.empty((m, L.k_pad), dtype=torch.int8, device=dev) for L in self.layers]
+        self.sx = [torch.empty(m, dtype=torch.float32, device=dev) for _ in self.layers]
+        self.y = [torch.empty((m, L.out_dim), dtype=torch.bfloat16, device=dev) for L in self.layers]
+        self.graph = None
+
+    def _src(self, i):
+        j = self.inputs[i]
+        return self.x if j < 0 else self.y[j]
+
+    def launch(self, stream: Optional[int] = None):
+        """Enqueue K1 + K2 for every layer (2 kernels per layer)."""
+        s = _stream() if stream is None else stream
+        for i, L in enumerate(self.layers):
+            src = self._src(i)
+            _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
+                      src.stride(0), L.gather_dev.data_ptr(), L.k_pad, L.act_granularity,
+                      float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
+                      None, None, s)
+            _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
+                      self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                      self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
+
+    def capture(self):
+        """Capture launch() into a CUDA graph (after one eager warm-up launch)."""
+        self.launch()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    @property
+    def output(self) -> torch.Tensor:
+        return self.y[-1]
+
+    def kernels_per_step(self) -> int:
+        return 2 * len(self.layers)
+
+    def int_ops(self) -> float:
+        return float(sum(2.0 * self.m * L.out_dim * L.in_dim for L in self.layers))

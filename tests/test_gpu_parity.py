@@ -1,0 +1,279 @@
+"""GPU parity tests: every kernel through the C-ABI vs the CPU oracle (and the compiled
+reference where it exists).  Integer outputs (codes, accumulators, indices, selected
+scales) are compared bit-exactly; floating outputs as stated per test."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2605_21072_b200 as qb
+from paper_2605_21072_b200 import engine, calibrate, synth
+from qarvd_testutil import bf16_values
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev_bf16(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def dev_bits(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def make_plan(k, n_out, seed=0, pad_unaligned=False):
+    r = np.random.default_rng(seed)
+    outl = np.sort(r.choice(k, size=n_out, replace=False)) if n_out else []
+    return engine.build_plan("t", k, outl)
+
+
+# ---------------------------------------------------------------- K1
+@pytest.mark.parametrize("m,k,n_out", [(4680, 1536, 32), (257, 1536, 0), (96, 8960, 192),
+                                       (33, 200, 5), (1, 64, 3)])
+def test_k1_per_token_bitexact(cuda, m, k, n_out):
+    plan = make_plan(k, n_out, seed=m)
+    heavy = plan.outlier_indices if n_out else None
+    bits, x64 = bf16_values((m, k), seed=k + m, heavy_cols=heavy)
+    xq, s32, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(bits), plan, check_finite=True)
+    q_ref, s_ref, bad = oracle.quantize_act(x64, plan.gather, per_token=True)
+    assert bad < 0
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    np.testing.assert_array_equal(s32.cpu().numpy(), s_ref.astype(np.float32))
+
+
+def test_k1_ties_and_edges(cuda):
+    # rows built so v/s hits exact .5 ties, zeros, max, and an all-zero row
+    k = 256
+    r = np.random.default_rng(7)
+    rows = []
+    for i in range(64):
+        a = float(2.0 ** r.integers(-6, 6))
+        base = np.arange(-k // 2, k // 2, dtype=np.float64) * (a / 127.0) * 0.5
+        base[0] = a
+        rows.append(base)
+    rows.append(np.zeros(k))
+    x = np.asarray(rows, dtype=np.float32)
+    bits = oracle.f32_to_bf16_bits(x)
+    x64 = oracle.bf16_bits_to_f64(bits)
+    xq, _, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(bits), engine.build_plan("t", k, []))
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy()[:, :k], q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    assert s_ref[-1] == np.finfo(np.float64).tiny
+
+
+def test_k1_static_scale_clamps(cuda):
+    bits, x64 = bf16_values((512, 1536), seed=3, scale=4.0)
+    plan = make_plan(1536, 32, seed=1)
+    s = 0.0123
+    xq, s32, _ = engine.kernel_a_quantize_activation(to_dev_bf16(bits), plan, qb.ACT_PER_TENSOR, s)
+    q_ref, _, _ = oracle.quantize_act(x64, plan.gather, per_token=False, static_scale=s)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    assert (np.abs(q_ref) == 127).any()
+
+
+def test_k1_f64_input_matches_reference(cuda, ref_lib):
+    r = np.random.default_rng(11)
+    x64 = r.standard_normal((64, 96)) * 3.0  # not bf16-representable: the f64 path
+    codes_ref, scales_ref = oracle.ref_quantize(x64, per_token=True)
+    plan = engine.build_plan("t", 96, [])
+    xq, _, s64 = engine.kernel_a_quantize_activation(torch.from_numpy(x64).cuda(), plan)
+    np.testing.assert_array_equal(xq.cpu().numpy()[:, :96], codes_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), scales_ref)
+
+
+def test_k1_nonfinite_reports_first_index(cuda):
+    bits, _ = bf16_values((8, 64), seed=5)
+    bits[3, 10] = 0x7FC0  # nan
+    bits[5, 2] = 0x7F80   # inf
+    plan = engine.build_plan("t", 64, [])
+    with pytest.raises(qb.InvalidArgument, match="flat index 202"):
+        engine.kernel_a_quantize_activation(to_dev_bf16(bits), plan, check_finite=True)
+
+
+# ---------------------------------------------------------------- K5
+@pytest.mark.parametrize("n,k,n_out", [(1536, 1536, 32), (384, 8960, 188), (64, 256, 0), (40, 100, 7)])
+def test_k5_weights_bitexact(cuda, n, k, n_out):
+    plan = make_plan(k, n_out, seed=n)
+    heavy = plan.outlier_indices if n_out else None
+    bits, w64 = bf16_values((n, k), seed=n + 1, scale=1.0 / np.sqrt(k), heavy_cols=heavy)
+    layer = engine.prepare_weights("t", to_dev_bf16(bits), plan)
+    wq_ref, so_ref, sn_ref, bad = oracle.prepare_weights(w64, plan.gather, plan.k_outlier)
+    assert bad < 0
+    np.testing.assert_array_equal(layer.wq.cpu().numpy(), wq_ref)
+    np.testing.assert_array_equal(layer.scale_outlier64.cpu().numpy(), so_ref)
+    np.testing.assert_array_equal(layer.scale_normal64.cpu().numpy(), sn_ref)
+
+
+def test_k5_matches_reference_build_plan(cuda, ref_lib):
+    n, k = 96, 256
+    plan = make_plan(k, 32, seed=2)
+    bits, w64 = bf16_values((n, k), seed=9, heavy_cols=plan.outlier_indices)
+    ref = oracle.ref_build_plan_codes(w64, plan.outlier_indices)
+    layer = engine.prepare_weights("t", to_dev_bf16(bits), plan)
+    np.testing.assert_array_equal(plan.permutation, ref["permutation"])
+    np.testing.assert_array_equal(layer.scale_outlier64.cpu().numpy(), ref["scale_outlier"])
+    np.testing.assert_array_equal(layer.scale_normal64.cpu().numpy(), ref["scale_normal"])
+    np.testing.assert_array_equal(layer.wq.cpu().numpy().astype(np.int32), ref["wq"])
+
+
+# ---------------------------------------------------------------- K2
+def _gemm_case(m, n, k, n_out, seed):
+    plan = make_plan(k, n_out, seed=seed)
+    heavy = plan.outlier_indices if n_out else None
+    wbits, w64 = bf16_values((n, k), seed=seed + 1, scale=1.0 / np.sqrt(k), heavy_cols=heavy)
+    xbits, x64 = bf16_values((m, k), seed=seed + 2, heavy_cols=heavy, gamma=4.0)
+    layer = engine.prepare_weights("t", to_dev_bf16(wbits), plan)
+    xq, s32, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(xbits), layer)
+    return plan, layer, xq, s32, s64, w64, x64
+
+
+@pytest.mark.parametrize("m,n,k,n_out", [
+    (4680, 1536, 1536, 32),     # config 1 (self-attn qkv shape)
+    (300, 8960, 1536, 32),      # ffn.0 shape, ragged M
+    (200, 1536, 8960, 192),     # ffn.2 shape (K_o = 192)
+    (130, 256, 256, 0),         # disabled plan: single accumulator
+    (77, 96, 160, 5),           # unaligned outliers padded to 32, ragged N
+])
+def test_k2_accumulators_and_epilogue_bitexact(cuda, m, n, k, n_out):
+    plan, layer, xq, s32, s64, _, _ = _gemm_case(m, n, k, n_out, seed=m + n)
+    y, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, layer, dump_acc=True)
+    xq_h, wq_h = xq.cpu().numpy(), layer.wq.cpu().numpy()
+    _, ao_ref, an_ref = oracle.kernel_b(xq_h, wq_h, plan.k_outlier, s64.cpu().numpy(),
+                                        layer.scale_outlier64.cpu().numpy(),
+                                        layer.scale_normal64.cpu().numpy(), with_acc=True)
+    np.testing.assert_array_equal(acc_o.cpu().numpy(), ao_ref)
+    np.testing.assert_array_equal(acc_n.cpu().numpy(), an_ref)
+    y_ref = oracle.epilogue_f32(ao_ref, an_ref, plan.k_outlier > 0, s32.cpu().numpy(),
+                                layer.scale_outlier32.cpu().numpy(),
+                                layer.scale_normal32.cpu().numpy())
+    np.testing.assert_array_equal(dev_bits(y), y_ref)
+
+
+def test_k2_vs_reference_kernel_b_tolerance(cuda, ref_lib):
+    """bf16 output vs the reference's own f64 kernel_b_gemm_dequant (per-token rows)."""
+    m, n, k = 64, 512, 1536
+    plan, layer, xq, s32, s64, w64, x64 = _gemm_case(m, n, k, 32, seed=21)
+    ref = oracle.ref_build_plan_codes(w64, plan.outlier_indices)
+    xp = oracle.ref_permute(x64, ref["permutation"])
+    codes, sx = oracle.ref_quantize(xp, per_token=True)
+    np.testing.assert_array_equal(codes, xq.cpu().numpy().astype(np.int32))  # k_pad == k here
+    y_ref = oracle.ref_kernel_b(codes, ref["wq"], ref["permutation"], len(plan.outlier_indices),
+                                True, sx, ref["scale_outlier"], ref["scale_normal"])
+    y, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, layer, dump_acc=True)
+    yd = y.float().cpu().numpy().astype(np.float64)
+    so, sn = ref["scale_outlier"], ref["scale_normal"]
+    mag = np.abs(sx[:, None] * so[None] * acc_o.cpu().numpy()) + np.abs(sx[:, None] * sn[None] * acc_n.cpu().numpy())
+    tol = 2.0 ** -8 * np.abs(y_ref) + 2.0 ** -22 * mag + 1e-30
+    assert np.all(np.abs(yd - y_ref) <= tol)
+
+
+def test_k2_bias_gelu_f32(cuda):
+    m, n, k = 256, 384, 512
+    plan, layer, xq, s32, s64, _, _ = _gemm_case(m, n, k, 32, seed=5)
+    bias = torch.linspace(-1, 1, n, device="cuda", dtype=torch.float32)
+    y32, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, layer, out_dtype=torch.float32,
+                                                     bias=bias, dump_acc=True)
+    ref32 = oracle.epilogue_f32(acc_o.cpu().numpy(), acc_n.cpu().numpy(), True, s32.cpu().numpy(),
+                                layer.scale_outlier32.cpu().numpy(),
+                                layer.scale_normal32.cpu().numpy(), bias.cpu().numpy(), out="f32")
+    np.testing.assert_array_equal(y32.cpu().numpy(), ref32)
+    yg = engine.kernel_b_gemm_dequant(xq, s32, layer, out_dtype=torch.float32, bias=bias,
+                                      epilogue=qb.EPI_GELU)
+    r = torch.from_numpy(ref32).double()
+    gelu = 0.5 * r * (1 + torch.erf(r / np.sqrt(2.0)))
+    torch.testing.assert_close(yg.cpu().double(), gelu, rtol=1e-5, atol=1e-6)
+
+
+def test_linear_handle_device_and_host(cuda):
+    m, n, k = 4680, 1536, 1536
+    plan, layer, xq, s32, _, _, _ = _gemm_case(m, n, k, 32, seed=3)
+    y_ref = engine.kernel_b_gemm_dequant(xq, s32, layer)
+    xbits, _ = bf16_values((m, k), seed=3 + 2, heavy_cols=plan.outlier_indices, gamma=4.0)
+    x = to_dev_bf16(xbits)
+    h = engine.LinearHandle(layer)
+    y = h.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((m, n), dtype=torch.bfloat16).pin_memory()
+    h.forward_host(xh, yh)
+    assert torch.equal(yh.view(torch.int16), y_ref.cpu().view(torch.int16))
+    h.close()
+
+
+# ---------------------------------------------------------------- K3
+@pytest.mark.parametrize("n,k,frac,gamma", [(1536, 1536, 0.021, 8.0), (1536, 8960, 0.021, 8.0),
+                                            (8960, 1536, 0.021, 8.0), (64, 256, 0.03, 10.0),
+                                            (96, 40, 0.1, 5.0), (128, 512, 0.0, 1.0)])
+def test_k3_detection_bitexact(cuda, n, k, frac, gamma):
+    r = np.random.default_rng(n + k)
+    heavy = r.choice(k, size=max(1, int(round(frac * k))), replace=False) if frac else None
+    bits, w64 = bf16_values((n, k), seed=k, scale=1.0 / np.sqrt(k), heavy_cols=heavy, gamma=gamma)
+    rep = qb.analyze_layer("t", to_dev_bf16(bits))
+    o = oracle.analyze_layer(w64)
+    np.testing.assert_array_equal(rep.norms.cpu().numpy(), o["norms"])
+    assert (rep.median, rep.mad, rep.threshold) == (o["median"], o["mad"], o["threshold"])
+    np.testing.assert_array_equal(rep.raw_outliers, o["raw"])
+    np.testing.assert_array_equal(rep.aligned_outliers, o["aligned"])
+
+
+def test_k3_batched_matches_reference(cuda, ref_lib):
+    ws, refs = [], []
+    for i, (n, k) in enumerate([(64, 256), (128, 96), (32, 1024)]):
+        heavy = np.arange(3 + i, k, 37)[: 2 + i]
+        bits, w64 = bf16_values((n, k), seed=100 + i, heavy_cols=heavy, gamma=6.0)
+        ws.append(to_dev_bf16(bits))
+        refs.append(oracle.ref_analyze_layer(w64))
+    reps = qb.analyze_layers(["a", "b", "c"], ws)
+    for rep, ref in zip(reps, refs):
+        np.testing.assert_array_equal(rep.norms.cpu().numpy(), ref["norms"])
+        assert (rep.median, rep.mad, rep.threshold) == (ref["median"], ref["mad"], ref["threshold"])
+        np.testing.assert_array_equal(rep.raw_outliers, ref["raw"])
+        np.testing.assert_array_equal(rep.aligned_outliers, ref["aligned"])
+
+
+# ---------------------------------------------------------------- K4
+@pytest.mark.parametrize("frames,rows,k,kind", [(21, 156, 1536, "heuristic_exp"), (21, 60, 512, "uniform"),
+                                                (7, 16, 64, "heuristic_exp"), (3, 5, 40, "uniform")])
+def test_k4_search_bitexact_vs_oracle(cuda, frames, rows, k, kind):
+    bits, _ = bf16_values((frames * rows, k), seed=frames * k, heavy_cols=np.arange(0, k, 97))
+    w = calibrate.weighting_strategy(kind, frames)
+    res = calibrate.scale_search_async([to_dev_bf16(bits)], frames, w).cpu().numpy()[0]
+    ref = oracle.scale_search_hist(bits, frames, rows, k, weights=w)
+    np.testing.assert_array_equal(res, ref)
+
+
+def test_k4_uniform_limit_equals_reference_percentile_search(cuda, ref_lib):
+    frames, rows, k = 21, 40, 1536
+    bits, x64 = bf16_values((frames * rows, k), seed=1234, heavy_cols=np.arange(0, k, 97))
+    res = calibrate.scale_search_async([to_dev_bf16(bits)], frames, None).cpu().numpy()[0]
+    best_pct, scale, mse = oracle.ref_percentile_search(x64, frames, rows, k)
+    assert calibrate.PERCENTILES[int(res[9])] == best_pct
+    assert res[10] == scale  # bit-identical selected scale
+    np.testing.assert_allclose(res[6:9], mse, rtol=1e-12)
+
+
+def test_k4_batched_layers(cuda):
+    frames = 21
+    xs, exp = [], []
+    w = calibrate.weighting_strategy("heuristic_exp", frames)
+    for i, (rows, k) in enumerate([(20, 1536), (20, 8960), (10, 256)]):
+        bits, _ = bf16_values((frames * rows, k), seed=i, heavy_cols=np.arange(i, k, 61))
+        xs.append(to_dev_bf16(bits))
+        exp.append(oracle.scale_search_hist(bits, frames, rows, k, weights=w))
+    res = calibrate.scale_search_async(xs, frames, w).cpu().numpy()
+    for r, e in zip(res, exp):
+        np.testing.assert_array_equal(r, e)
+
+
+# ---------------------------------------------------------------- synthetic data
+def test_synth_weights_outlier_columns_detected(cuda):
+    specs = synth.wan_registry(blocks=1)
+    spec = [s for s in specs if s.name.endswith("ffn.2")][0]
+    w = synth.synth_weight(spec, seed=1)
+    rep = qb.analyze_layer(spec.name, w)
+    cols = synth.pick_outlier_columns(1, spec.index, spec.in_dim, spec.outlier_fraction)
+    assert set(cols.tolist()) <= set(rep.aligned_outliers.tolist())
+    assert len(rep.aligned_outliers) == 192
