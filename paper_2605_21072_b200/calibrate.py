@@ -214,3 +214,17 @@ def allgather_records(local: Sequence[LayerRecord], group=None, device=None) -> 
         recs.extend(unpack_records(g[r * cap: r * cap + sizes[r]]))
     recs.sort(key=lambda r: r.index)
     return recs
+
+
+def calibrate_model_sharded(costs: Sequence[float], compute: Callable[[List[int]], List[LayerRecord]],
+                            rank: int = 0, world: int = 1, group=None, device=None) -> List[LayerRecord]:
+    """calibrate_model's layer loop (calibrate.cpp:440-484) over `world` ranks.
+
+    ``compute(layer_ids)`` runs this rank's layers (on its GPU) and returns their
+    records; one all-gather assembles the full result.  The output is identical
+    for every world size (slot-indexed by layer, as the reference's parallel_for)."""
+    assign = lpt_assign(costs, world)
+    local = compute(assign[rank]) if assign[rank] else []
+    if world == 1:
+        return sorted(local, key=lambda r: r.index)
+    return allgather_records(local, group=group, device=device)

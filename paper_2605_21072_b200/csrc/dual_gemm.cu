@@ -27,7 +27,8 @@ namespace {
 
 constexpr int BM = 128;  // rows of the activation tile (one TMEM lane per row)
 constexpr int BK = 128;  // bytes (= int8 elements) of K per pipeline stage: one swizzle row
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
 
 template <int BN>
 struct GemmCfg {
@@ -38,7 +39,8 @@ struct GemmCfg {
   static constexpr int kAccStages = 512 / (2 * BN);  // two accumulators per stage
   static constexpr uint32_t kTmemCols = 512;
   static constexpr size_t kSmemBytes =
-      static_cast<size_t>(kStages) * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/;
+      static_cast<size_t>(kStages) * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/ +
+      kEpiWarps * 96 * sizeof(float) /*epilogue scale staging*/;
 };
 
 struct GemmParams {
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
+  float* epi_scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < C::kAccStages; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      ptx::mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -161,10 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (4 warps = 128 TMEM lanes) =====================
+    // ===================== epilogue: 8 warps, 2 per TMEM lane quadrant =====================
+    // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quadrant
+    // split the tile's 32-column chunks (even / odd).
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
     const bool has_outlier = p.k_o > 0;
+    float* scr = epi_scratch + (warp - 4) * 96;  // per-warp staging of the chunk's column scales
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -179,31 +186,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_o = tmem_base + t_lane + static_cast<uint32_t>(acc * 2 * BN);
       const uint32_t t_n = t_o + BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
         if (col0 >= p.n) break;  // warp-uniform
+        const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
+        {
+          const int64_t jc = col0 + (lane < ncols ? lane : 0);
+          scr[lane] = __ldg(p.scale_wn + jc);
+          scr[32 + lane] = has_outlier ? __ldg(p.scale_wo + jc) : 0.f;
+          scr[64 + lane] = p.bias ? __ldg(p.bias + jc) : 0.f;
+        }
         uint32_t rn[32], ro[32];
         ptx::tmem_ld32(t_n + c * 32, rn);
         if (has_outlier) ptx::tmem_ld32(t_o + c * 32, ro);
         ptx::tmem_wait_ld();
+        __syncwarp();
         if (row_ok) {
-          const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
-          float y[32];
+          if (p.acc_n_dbg) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int64_t j = col0 + (e < ncols ? e : 0);
-            const float swn = __ldg(p.scale_wn + j);
-            const float an = __int2float_rn(static_cast<int>(rn[e]));
-            float tacc;
-            if (has_outlier) {
-              const float swo = __ldg(p.scale_wo + j);
-              tacc = __fmaf_rn(swn, an, __fmul_rn(swo, __int2float_rn(static_cast<int>(ro[e]))));
-            } else {
-              tacc = __fmul_rn(swn, an);
+            for (int e = 0; e < 32; ++e) {
+              if (e >= ncols) continue;
+              p.acc_n_dbg[row * p.n + col0 + e] = static_cast<int32_t>(rn[e]);
+              if (p.acc_o_dbg)
+                p.acc_o_dbg[row * p.n + col0 + e] = has_outlier ? static_cast<int32_t>(ro[e]) : 0;
             }
-            float v = p.bias ? __fmaf_rn(sx, tacc, __ldg(p.bias + j)) : __fmul_rn(sx, tacc);
-            if (p.epilogue & QARVD_EPI_GELU) v = gelu_erf(v);
-            y[e] = v;
+          }
+          // y overwrites rn (as float bits): t = s_wo*acc_o; t = fmaf(s_wn, acc_n, t); y = s_x*t (+bias)
+#pragma unroll
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 sn4 = reinterpret_cast<const float4*>(scr)[e4];
+            const float4 so4 = reinterpret_cast<const float4*>(scr + 32)[e4];
+            const float4 sb4 = reinterpret_cast<const float4*>(scr + 64)[e4];
+            const float sn[4] = {sn4.x, sn4.y, sn4.z, sn4.w};
+            const float so[4] = {so4.x, so4.y, so4.z, so4.w};
+            const float sb[4] = {sb4.x, sb4.y, sb4.z, sb4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int e = 4 * e4 + u;
+              const float an = __int2float_rn(static_cast<int>(rn[e]));
+              float tacc;
+              if (has_outlier)
+                tacc = __fmaf_rn(sn[u], an, __fmul_rn(so[u], __int2float_rn(static_cast<int>(ro[e]))));
+              else
+                tacc = __fmul_rn(sn[u], an);
+              float v = p.bias ? __fmaf_rn(sx, tacc, sb[u]) : __fmul_rn(sx, tacc);
+              if (p.epilogue & QARVD_EPI_GELU) v = gelu_erf(v);
+              rn[e] = __float_as_uint(v);
+            }
           }
           if (p.out_dtype == QARVD_BF16) {
             __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
@@ -211,7 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t pk[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(y[2 * e], y[2 * e + 1]);
+                const __nv_bfloat162 h2 =
+                    __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
                 pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
               }
               uint4* dst = reinterpret_cast<uint4*>(yr);
@@ -219,9 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int v4 = 0; v4 < 4; ++v4)
                 dst[v4] = make_uint4(pk[4 * v4], pk[4 * v4 + 1], pk[4 * v4 + 2], pk[4 * v4 + 3]);
             } else {
-              #pragma unroll
+#pragma unroll
               for (int e = 0; e < 32; ++e)
-                if (e < ncols) yr[e] = __float2bfloat16_rn(y[e]);
+                if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
             }
           } else {
             float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
@@ -229,22 +259,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               float4* dst = reinterpret_cast<float4*>(yr);
 #pragma unroll
               for (int v4 = 0; v4 < 8; ++v4)
-                dst[v4] = make_float4(y[4 * v4], y[4 * v4 + 1], y[4 * v4 + 2], y[4 * v4 + 3]);
+                dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
+                                      __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
             } else {
-              #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (e < ncols) yr[e] = y[e];
-            }
-          }
-          if (p.acc_n_dbg) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              if (e >= ncols) continue;
-              p.acc_n_dbg[row * p.n + col0 + e] = static_cast<int32_t>(rn[e]);
-              if (p.acc_o_dbg) p.acc_o_dbg[row * p.n + col0 + e] = has_outlier ? static_cast<int32_t>(ro[e]) : 0;
+              for (int e = 0; e < 32; ++e)
+                if (e < ncols) yr[e] = __uint_as_float(rn[e]);
             }
           }
         }
+        __syncwarp();  // scr is rewritten by the next chunk
       }
       ptx::tc_fence_before();
       __syncwarp();

@@ -215,6 +215,206 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 }
 
 // ---------------------------------------------------------------------------
+// Activation fast path (bf16, per-token or static): persistent CTAs stream row
+// groups through a 4-stage shared-memory ring filled by TMA bulk copies
+// (cp.async.bulk, one per row), so HBM reads overlap the rounding of earlier
+// rows.  A group is G rows (G*K*2 ~ 16-24 KB); each row is owned by 8/G warps
+// which split its columns, combine their |x| maxima through shared memory,
+// then emit 16 codes per lane per step through an int16 gather table.
+// Rounding: t = v * (qmax/absmax) in fp32, q = rint(t).  |t - v/s| < 3.1e-5
+// for |t| <= 254, so q is the f64 round_half_even(v/s) unless t lies within
+// 1e-4 of a half-integer; those (~0.04%) are recomputed with __ddiv_rn.
+constexpr int kActThreads = 256;
+constexpr int kActStages = 4;
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init_(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx_(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+template <bool kStatic>
+__device__ __forceinline__ int act_code(uint16_t h, float r32, double s64, bool exact, int qmax) {
+  const float v = bf16_bits_to_float(h);
+  if (exact) return quant_code_exact(static_cast<double>(v), s64, qmax);
+  const float t = __fmul_rn(v, r32);
+  float q = rintf(t);
+  if (fabsf(__fsub_rn(t, q)) > 0.4999f) {
+    if (!kStatic || fabsf(t) <= 254.0f) return quant_code_exact(static_cast<double>(v), s64, qmax);
+  }
+  if (kStatic) q = fminf(fmaxf(q, -static_cast<float>(qmax)), static_cast<float>(qmax));
+  return static_cast<int>(q);  // per-token: |t| <= qmax by construction
+}
+
+template <bool kStatic>
+__global__ void __launch_bounds__(kActThreads)
+    quant_act_tma_kernel(const uint16_t* __restrict__ x, int64_t m, int64_t k, int64_t ldx,
+                         const int32_t* __restrict__ gather, int64_t k_out, int G,
+                         double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
+                         float* __restrict__ s32_out, double* __restrict__ s64_out,
+                         unsigned long long* err) {
+  extern __shared__ __align__(128) uint8_t smem_act[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row_elems = (k + 7) & ~int64_t(7);
+  const int64_t stage_elems = row_elems * G;
+  uint16_t* rows = reinterpret_cast<uint16_t*>(smem_act);
+  int16_t* gidx = reinterpret_cast<int16_t*>(rows + kActStages * stage_elems);
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(gidx + ((k_out + 7) & ~int64_t(7))) + 15) & ~uintptr_t(15));
+  float* part = reinterpret_cast<float*>(full + kActStages);
+  uint32_t* badflag = reinterpret_cast<uint32_t*>(part + 8);  // per-warp non-finite flags
+
+  const int64_t num_groups = (m + G - 1) / G;
+  const int W = 8 / G;              // warps per row
+  const int my_row = warp / W;      // row inside the group
+  const int sub = warp % W;         // column share of this warp
+
+  for (int64_t c = tid; c < k_out; c += kActThreads)
+    gidx[c] = gather ? static_cast<int16_t>(__ldg(gather + c)) : static_cast<int16_t>(c);
+  if (tid == 0) {
+    for (int s = 0; s < kActStages; ++s) mbar_init_(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t it, int slot) {
+    const int64_t g = blockIdx.x + it * gridDim.x;
+    if (g >= num_groups) return;
+    const int64_t r0 = g * G;
+    const int nr = static_cast<int>((m - r0) < G ? (m - r0) : G);
+    const uint32_t bytes = static_cast<uint32_t>(k * 2);
+    mbar_expect_tx_(&full[slot], bytes * nr);
+    for (int r = 0; r < nr; ++r)
+      bulk_load(rows + slot * stage_elems + r * row_elems, x + (r0 + r) * ldx, bytes, &full[slot]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kActStages; ++s) issue(s, s);
+
+  GroupScale gs_static;
+  if (kStatic) gs_static = scale_static(static_scale);
+  const int64_t csz = ((k + W - 1) / W);            // source columns per warp (absmax)
+  const int64_t osz = (((k_out + W - 1) / W) + 15) & ~int64_t(15);  // output columns per warp
+
+  for (int64_t it = 0;; ++it) {
+    const int64_t g = blockIdx.x + it * gridDim.x;
+    if (g >= num_groups) break;
+    const int slot = static_cast<int>(it % kActStages);
+    mbar_wait_(&full[slot], static_cast<uint32_t>((it / kActStages) & 1));
+    const int64_t row = g * G + my_row;
+    const bool active = row < m;
+    const uint16_t* rs = rows + slot * stage_elems + my_row * row_elems;
+
+    GroupScale gsc;
+    bool row_bad = false;
+    if (!kStatic) {
+      float amax = 0.f;
+      bool bad = false;
+      if (active) {
+        const int64_t c0 = sub * csz, c1 = (c0 + csz) < k ? (c0 + csz) : k;
+        for (int64_t c = c0 + lane * 8; c < c1; c += 256) {
+          if (c + 8 <= c1 && (c & 7) == 0) {
+            const uint4 d = *reinterpret_cast<const uint4*>(rs + c);
+            const uint32_t w4[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const uint32_t lo = w4[h] & 0x7fffu, hi = (w4[h] >> 16) & 0x7fffu;
+              bad |= (lo >= 0x7f80u) | (hi >= 0x7f80u);
+              amax = fmaxf(amax, fmaxf(__uint_as_float(lo << 16), __uint_as_float(hi << 16)));
+            }
+          } else {
+            for (int64_t e = c; e < c + 8 && e < c1; ++e) {
+              const uint32_t b = rs[e] & 0x7fffu;
+              bad |= b >= 0x7f80u;
+              amax = fmaxf(amax, __uint_as_float(b << 16));
+            }
+          }
+        }
+      }
+      amax = warp_max(amax);
+      row_bad = __any_sync(0xffffffffu, bad);
+      if (W > 1) {
+        if (lane == 0) {
+          part[warp] = amax;
+          badflag[warp] = row_bad ? 1u : 0u;
+        }
+        __syncthreads();
+        for (int w = 0; w < W; ++w) {
+          amax = fmaxf(amax, part[my_row * W + w]);
+          row_bad |= badflag[my_row * W + w] != 0;
+        }
+      }
+      gsc = scale_from_absmax(amax, qmax);
+      if (active && sub == 0 && lane == 0) {
+        if (s32_out) s32_out[row] = gsc.s32;
+        if (s64_out) s64_out[row] = gsc.s64;
+      }
+    } else {
+      gsc = gs_static;
+      if (active && sub == 0 && lane == 0) {
+        if (s32_out) s32_out[row] = gsc.s32;
+        if (s64_out) s64_out[row] = gsc.s64;
+      }
+    }
+    const bool check_bad = kStatic || row_bad;
+
+    if (active) {
+      int8_t* qr = q + row * ldq;
+      const int64_t o0 = sub * osz, o1 = (o0 + osz) < k_out ? (o0 + osz) : k_out;
+      for (int64_t c0 = o0 + lane * 16; c0 < o1; c0 += 512) {
+        const uint4 ga = *reinterpret_cast<const uint4*>(gidx + c0);
+        const uint4 gb = *reinterpret_cast<const uint4*>(gidx + c0 + 8);
+        const uint32_t gw[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int src = static_cast<int16_t>((gw[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+          int code = 0;
+          if (src >= 0) {
+            const uint16_t h = rs[src];
+            if (check_bad && (h & 0x7f80u) == 0x7f80u) {
+              if (err) atomicMin(err, static_cast<unsigned long long>(row * k_out + c0 + e));
+            } else {
+              code = act_code<kStatic>(h, gsc.r32, gsc.s64, gsc.exact, qmax);
+            }
+          }
+          packed[e >> 2] |= (static_cast<uint32_t>(code) & 0xffu) << (8 * (e & 3));
+        }
+        *reinterpret_cast<uint4*>(qr + c0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      }
+    }
+    __syncthreads();  // every warp is done with this slot (and with part[] / badflag)
+    if (tid == 0) issue(it + kActStages, slot);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic kernel (f32 / f64 inputs, or rows too wide for shared memory):
 // one warp per row, reads straight from global memory; f64 inputs always take
 // the exact division (reference f64 semantics, no bf16 assumption).
@@ -301,7 +501,29 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
   }
   if (m == 0) return QARVD_OK;
   const int grid = grid_for_rows(m);
-  if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
+  const bool tma_ok = MODE != kWeightDual && dtype == QARVD_BF16 && k <= 16384 &&
+                      (k % 8) == 0 && (ldx % 8) == 0 && (k_out % 16) == 0 && (ldq % 16) == 0 &&
+                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  if (tma_ok) {
+    const int G = k <= 1536 ? 8 : (k <= 3072 ? 4 : (k <= 6144 ? 2 : 1));
+    const size_t smem = static_cast<size_t>(kActStages) * G * k * 2 + k_out * 2 + 64 +
+                        kActStages * 8 + 16 * 4 + 16;
+    auto kern = quant_act_tma_kernel<MODE == kActStatic>;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] {
+      attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    QARVD_CUDA_TRY(attr);
+    const int64_t groups = (m + G - 1) / G;
+    const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
+    const int64_t cap = static_cast<int64_t>(kNumSMs) * ctas_per_sm;
+    const int g = static_cast<int>(groups < cap ? groups : cap);
+    kern<<<g, kActThreads, smem, stream>>>(static_cast<const uint16_t*>(x), m, k, ldx, gather,
+                                           k_out, G, static_scale, qmax, q, ldq, s32_n, s64_n,
+                                           err);
+  } else if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
     const size_t smem = static_cast<size_t>(kWarpsPerCta) * (((k + 7) & ~int64_t(7)) * 2);
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
