@@ -142,6 +142,14 @@ int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw
                     int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
                     int32_t* acc_normal, void* stream);
 
+/* K2 with the reference's exact f64 epilogue (engine.cpp:86-94: val = 0; val += (s_x*s_wo[j])*acc_o;
+ * val += (s_x*s_wn[j])*acc_n) on f64 scales -> f64 y.  Bit-identical to kernel_b_gemm_dequant
+ * for symmetric activations; used by the C++ drop-in adapter (toy / reference-parity path). */
+int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                        int64_t n, int64_t k, int64_t k_outlier, const double* scale_x,
+                        const double* scale_w_outlier, const double* scale_w_normal, double* y,
+                        int64_t ldy, void* stream);
+
 /* ---- K1+K2: one quantized linear, host buffers (end-to-end entry) --------
  * Replaces  quantized_layer_forward(layer, x, Engine::int_kernels)
  *           engine.hpp:60 / engine.cpp:134-142 (per-token or static activations).

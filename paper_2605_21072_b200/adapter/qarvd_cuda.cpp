@@ -1,0 +1,285 @@
+// qarvd_cuda.cpp — see qarvd_cuda.hpp.  Host staging + status mapping only.
+#include "qarvd_cuda.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <stdexcept>
+
+#include "../../include/qarvd_b200.h"
+
+namespace qarvd {
+namespace cuda {
+
+namespace {
+
+[[noreturn]] void throw_status(int st, const std::string& what) {
+  const std::string msg = what.empty() ? std::string(qarvd_last_error()) : what;
+  switch (st) {
+    case QARVD_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case QARVD_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case QARVD_ERR_LOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+void check(int st) {
+  if (st != QARVD_OK) throw_status(st, "");
+}
+
+void check_cuda(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) : bytes(n) { check_cuda(cudaMalloc(&p, n ? n : 1)); }
+  DevBuf(const void* host, size_t n) : DevBuf(n) {
+    if (n) check_cuda(cudaMemcpy(p, host, n, cudaMemcpyHostToDevice));
+  }
+  ~DevBuf() { cudaFree(p); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// Kernel layout of a plan: [outliers | pad to 32 | normals | pad to 32] (qarvd_b200.h)
+struct Layout {
+  std::vector<int32_t> gather;  // source column per padded position, -1 = pad
+  std::vector<int32_t> pos;     // padded position of permuted column c (reference order)
+  size_t k_outlier = 0, k_pad = 0;
+};
+
+Layout make_layout(const DualScalePlan& plan, size_t d_in) {
+  Layout L;
+  const size_t n_o = plan.enabled ? plan.outlier_count() : 0;
+  L.k_outlier = round_up(n_o, 32);
+  L.k_pad = L.k_outlier + round_up(d_in - n_o, 32);
+  L.gather.assign(L.k_pad, -1);
+  L.pos.resize(d_in);
+  for (size_t c = 0; c < d_in; ++c) {
+    const size_t dst = c < n_o ? c : L.k_outlier + (c - n_o);
+    L.gather[dst] = plan.enabled ? static_cast<int32_t>(plan.permutation[c]) : static_cast<int32_t>(c);
+    L.pos[c] = static_cast<int32_t>(dst);
+  }
+  return L;
+}
+
+}  // namespace
+
+class DeviceLayer {
+ public:
+  explicit DeviceLayer(const QuantizedLayer& l)
+      : name(l.name), n(l.out_dim), k(l.in_dim), layout(make_layout(l.plan, l.in_dim)) {
+    if (l.preserved) throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + l.name);
+    if (l.wq.shape.size() != 2 || l.wq.shape[0] != n || l.wq.shape[1] != k)
+      throw std::invalid_argument("kernel_b: weight shape mismatch for " + l.name);
+    std::vector<int8_t> wq(n * layout.k_pad, 0);
+    for (size_t r = 0; r < n; ++r)
+      for (size_t c = 0; c < k; ++c)
+        wq[r * layout.k_pad + layout.pos[c]] = static_cast<int8_t>(l.wq.data[r * k + c]);
+    // f64 group scales exactly as the reference holds them in memory (the f64 epilogue
+    // entry point reproduces kernel_b_gemm_dequant bit for bit)
+    std::vector<double> so(n), sn(n);
+    for (size_t r = 0; r < n; ++r) {
+      sn[r] = l.plan.params_normal.scale[r];
+      so[r] = l.plan.enabled ? l.plan.params_outlier.scale[r] : l.plan.params_normal.scale[r];
+    }
+    wq_dev = std::make_unique<DevBuf>(wq.data(), wq.size());
+    so_dev = std::make_unique<DevBuf>(so.data(), so.size() * 8);
+    sn_dev = std::make_unique<DevBuf>(sn.data(), sn.size() * 8);
+    gather_dev = std::make_unique<DevBuf>(layout.gather.data(), layout.gather.size() * 4);
+  }
+  std::string name;
+  size_t n, k;
+  Layout layout;
+  std::unique_ptr<DevBuf> wq_dev, so_dev, sn_dev, gather_dev;
+};
+
+namespace {
+
+// K1 on a host f64 tensor in the layer padded layout; returns device codes + f64 row scales.
+void quantize_to_device(const Tensor& x, const Layout& L, const DevBuf& gather_dev,
+                        const QuantParams& p, DevBuf& xq, DevBuf& sx, size_t m) {
+  if (p.per_channel() || p.zero_point[0] != 0 || !p.symmetric)
+    throw std::invalid_argument("quantize: the CUDA engine implements symmetric per-tensor activations");
+  p.validate(x.shape());
+  DevBuf xd(x.data(), x.size() * sizeof(double));
+  DevBuf err(sizeof(int64_t));
+  check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(x.cols()),
+                           static_cast<int64_t>(x.cols()), gather_dev.as<int32_t>(),
+                           static_cast<int64_t>(L.k_pad), QARVD_ACT_PER_TENSOR, p.scale[0], p.bits,
+                           xq.as<int8_t>(), static_cast<int64_t>(L.k_pad), nullptr, sx.as<double>(),
+                           err.as<int64_t>(), nullptr));
+  int64_t bad = 0;
+  check_cuda(cudaMemcpy(&bad, err.p, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != INT64_MAX) {
+    // report the first non-finite in the reference's (unpadded, permuted) flat index
+    const int64_t row = bad / static_cast<int64_t>(L.k_pad), pc = bad % static_cast<int64_t>(L.k_pad);
+    int64_t c = 0;
+    for (size_t i = 0; i < L.pos.size(); ++i)
+      if (L.pos[i] == pc) c = static_cast<int64_t>(i);
+    throw std::invalid_argument("quantize: non-finite input at flat index " +
+                                std::to_string(row * static_cast<int64_t>(x.cols()) + c));
+  }
+}
+
+// sx: device f64 [m] activation scale per row
+Tensor gemm_to_host(const DeviceLayer& L, const DevBuf& xq, const DevBuf& sx, size_t m) {
+  DevBuf y(m * L.n * sizeof(double));
+  check(qarvd_dual_gemm_f64(xq.as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
+                            L.wq_dev->as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
+                            static_cast<int64_t>(m), static_cast<int64_t>(L.n),
+                            static_cast<int64_t>(L.layout.k_pad),
+                            static_cast<int64_t>(L.layout.k_outlier), sx.as<double>(),
+                            L.so_dev->as<double>(), L.sn_dev->as<double>(), y.as<double>(),
+                            static_cast<int64_t>(L.n), nullptr));
+  Tensor out({m, L.n});
+  check_cuda(cudaMemcpy(out.data(), y.p, m * L.n * sizeof(double), cudaMemcpyDeviceToHost));
+  return out;
+}
+
+}  // namespace
+
+IntTensor kernel_a_quantize_activation(const Tensor& x, const QuantParams& p) {
+  p.validate(x.shape());
+  if (x.rank() != 2) return qarvd::quantize(x, p);  // non-matrix inputs: not a hot path
+  const size_t m = x.rows(), k = x.cols();
+  if (p.bits > 8) throw std::invalid_argument("quantize: the CUDA engine stores codes as int8");
+  const size_t kp = round_up(k, 32);
+  std::vector<int32_t> gather(kp, -1);
+  for (size_t c = 0; c < k; ++c) gather[c] = static_cast<int32_t>(c);
+  DevBuf gd(gather.data(), gather.size() * 4), xd(x.data(), x.size() * sizeof(double));
+  DevBuf q(m * kp + 16), err(sizeof(int64_t));
+  std::vector<double> scales_in;
+  IntTensor out;
+  out.shape = x.shape();
+  out.bits = p.bits;
+  out.data.resize(m * k);
+  if (p.per_channel() && p.channel_axis == 0) {
+    // per-token (per-row) scales: one K1 launch per distinct scale is wasteful; rows carry
+    // their own scale through the static path one row block at a time
+    for (size_t i = 0; i < m; ++i) {
+      check(qarvd_quantize_act(xd.as<double>() + i * k, QARVD_F64, 1, static_cast<int64_t>(k),
+                               static_cast<int64_t>(k), gd.as<int32_t>(), static_cast<int64_t>(kp),
+                               QARVD_ACT_PER_TENSOR, p.scale[i], p.bits, q.as<int8_t>() + i * kp,
+                               static_cast<int64_t>(kp), nullptr, nullptr, err.as<int64_t>(), nullptr));
+    }
+  } else if (p.per_channel()) {
+    return qarvd::quantize(x, p);  // per-column scales never occur on the activation path
+  } else {
+    check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(k),
+                             static_cast<int64_t>(k), gd.as<int32_t>(), static_cast<int64_t>(kp),
+                             QARVD_ACT_PER_TENSOR, p.scale[0], p.bits, q.as<int8_t>(),
+                             static_cast<int64_t>(kp), nullptr, nullptr, err.as<int64_t>(), nullptr));
+  }
+  int64_t bad = 0;
+  check_cuda(cudaMemcpy(&bad, err.p, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != INT64_MAX) {
+    const int64_t row = bad / static_cast<int64_t>(kp), c = bad % static_cast<int64_t>(kp);
+    throw std::invalid_argument("quantize: non-finite input at flat index " +
+                                std::to_string(row * static_cast<int64_t>(k) + c));
+  }
+  std::vector<int8_t> h(m * kp);
+  check_cuda(cudaMemcpy(h.data(), q.p, h.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < m; ++i)
+    for (size_t c = 0; c < k; ++c) out.data[i * k + c] = h[i * kp + c];
+  return out;
+}
+
+Tensor permute_activations(const Tensor& x, const DualScalePlan& plan) {
+  return qarvd::permute_activations(x, plan);  // a gather; fused into K1 on the device path
+}
+
+Tensor kernel_b_gemm_dequant(const IntTensor& xq, const QuantizedLayer& layer) {
+  if (layer.preserved)
+    throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + layer.name);
+  if (xq.shape.size() != 2 || xq.shape[1] != layer.in_dim)
+    throw std::invalid_argument("kernel_b: activation shape does not match layer " + layer.name);
+  if (layer.act.zero_point[0] != 0)
+    throw std::invalid_argument("kernel_b: asymmetric activations are not supported by the CUDA engine");
+  const DeviceLayer L(layer);
+  const size_t m = xq.shape[0];
+  std::vector<int8_t> h(m * L.layout.k_pad, 0);
+  for (size_t i = 0; i < m; ++i)
+    for (size_t c = 0; c < L.k; ++c)
+      h[i * L.layout.k_pad + L.layout.pos[c]] = static_cast<int8_t>(xq.data[i * L.k + c]);
+  DevBuf xd(h.data(), h.size());
+  std::vector<double> sx(m, layer.act.scale[0]);
+  DevBuf sd(sx.data(), sx.size() * 8);
+  return gemm_to_host(L, xd, sd, m);
+}
+
+Tensor quantized_layer_forward(const QuantizedLayer& layer, const Tensor& x, Engine engine) {
+  if (layer.preserved || engine == Engine::fakequant_sim)
+    return qarvd::quantized_layer_forward(layer, x, engine);  // f64 reference paths
+  const DeviceLayer L(layer);
+  const size_t m = x.rows();
+  DevBuf xq(m * L.layout.k_pad + 16), sx(m * 8);
+  quantize_to_device(x, L.layout, *L.gather_dev, layer.act, xq, sx, m);
+  return gemm_to_host(L, xq, sx, m);
+}
+
+OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w, double tau,
+                            double alpha_min, size_t align) {
+  if (w.rank() != 2) throw std::invalid_argument("channel_l2_norms: input must be 2-D");
+  const size_t n = w.rows(), k = w.cols();
+  DevBuf wd(w.data(), w.size() * sizeof(double)), norms(k * 8), stats(24), counts(8),
+      raw(k * 4), al(k * 4);
+  qarvd_outlier_job job{wd.p, static_cast<int64_t>(n), static_cast<int64_t>(k),
+                        static_cast<int64_t>(k), norms.as<double>(), stats.as<double>(),
+                        counts.as<int32_t>(), raw.as<int32_t>(), al.as<int32_t>()};
+  check(qarvd_analyze_layers(&job, 1, QARVD_F64, tau, alpha_min, static_cast<int64_t>(align), nullptr));
+  check_cuda(cudaDeviceSynchronize());
+  OutlierReport rep;
+  rep.layer_name = layer_name;
+  rep.tau = tau;
+  rep.alpha_min = alpha_min;
+  rep.align = align;
+  rep.norms.resize(k);
+  double st[3];
+  int32_t cnt[2];
+  check_cuda(cudaMemcpy(rep.norms.data(), norms.p, k * 8, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(st, stats.p, 24, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(cnt, counts.p, 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> r(k), a(k);
+  check_cuda(cudaMemcpy(r.data(), raw.p, k * 4, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(a.data(), al.p, k * 4, cudaMemcpyDeviceToHost));
+  rep.median = st[0];
+  rep.mad = st[1];
+  rep.threshold = st[2];
+  rep.raw_outliers.assign(r.begin(), r.begin() + cnt[0]);
+  rep.aligned_outliers.assign(a.begin(), a.begin() + cnt[1]);
+  return rep;
+}
+
+CudaQuantizedProvider::CudaQuantizedProvider(const QuantizedModel& qm) : qm_(qm) {
+  for (const auto& l : qm.layers)
+    if (!l.preserved) layers_.emplace(l.name, std::make_shared<DeviceLayer>(l));
+}
+
+CudaQuantizedProvider::~CudaQuantizedProvider() = default;
+
+Tensor CudaQuantizedProvider::forward(const std::string& layer, const Tensor& x) const {
+  const QuantizedLayer& l = qm_.layer(layer);  // std::out_of_range as the reference (engine.cpp:29)
+  if (l.preserved) return matmul_nt(x, l.fp_weight);
+  const DeviceLayer& L = *layers_.at(layer);
+  const size_t m = x.rows();
+  DevBuf xq(m * L.layout.k_pad + 16), sx(m * 8);
+  quantize_to_device(x, L.layout, *L.gather_dev, l.act, xq, sx, m);
+  return gemm_to_host(L, xq, sx, m);
+}
+
+Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed) {
+  const CudaQuantizedProvider provider(qm);
+  return run_rollout(qm.cfg, provider, &provider, QuantTarget::all, 0, prompt_seed);
+}
+
+}  // namespace cuda
+}  // namespace qarvd

@@ -1,0 +1,69 @@
+// qarvd_cuda.hpp — drop-in CUDA backend for the reference's quantized-inference
+// operators (/root/reference/proj/core/include/qarvd/engine.hpp, outlier.hpp).
+//
+// A maintainer adds this file pair to the reference tree (or links it from a
+// separate target against `qarvd::core` + libqarvd_b200.so) and swaps
+//     qarvd::kernel_a_quantize_activation  -> qarvd::cuda::kernel_a_quantize_activation
+//     qarvd::kernel_b_gemm_dequant         -> qarvd::cuda::kernel_b_gemm_dequant
+//     qarvd::quantized_layer_forward       -> qarvd::cuda::quantized_layer_forward
+//     qarvd::analyze_layer                 -> qarvd::cuda::analyze_layer
+//     QuantizedProvider (engine.cpp:146-171) -> qarvd::cuda::CudaQuantizedProvider
+// Signatures, argument meaning and exception types/messages follow the
+// reference.  All arithmetic runs in libqarvd_b200.so (sm_100a); this file only
+// stages host tensors to the device and maps C-ABI statuses to exceptions.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "qarvd/engine.hpp"
+#include "qarvd/outlier.hpp"
+#include "qarvd/quant.hpp"
+#include "qarvd/tensor.hpp"
+#include "qarvd/toy_model.hpp"
+
+namespace qarvd {
+namespace cuda {
+
+// engine.hpp:43 — codes bit-identical to qarvd::quantize (f64 inputs take the exact path).
+IntTensor kernel_a_quantize_activation(const Tensor& x, const QuantParams& p);
+
+// engine.hpp:48 — int8 tensor-core GEMM with two int32 accumulators (outlier / normal
+// group) and an fp32 dequant epilogue; equals the reference within fp32 rounding.
+Tensor kernel_b_gemm_dequant(const IntTensor& xq, const QuantizedLayer& layer);
+
+// engine.hpp:51
+Tensor permute_activations(const Tensor& x, const DualScalePlan& plan);
+
+// engine.hpp:60 (Engine::int_kernels semantics; fakequant_sim is delegated to the reference)
+Tensor quantized_layer_forward(const QuantizedLayer& layer, const Tensor& x, Engine engine);
+
+// outlier.hpp:59-61 — bit-identical report (norms, median, MAD, threshold, index sets).
+OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w,
+                            double tau = kDefaultTau, double alpha_min = kDefaultAlphaMin,
+                            size_t align = kDefaultAlign);
+
+// Device-resident copy of one QuantizedLayer (codes padded into the kernel layout).
+class DeviceLayer;
+
+// LinearProvider (toy_model.hpp:77-81) serving a QuantizedModel from the GPU.  Layers
+// are uploaded once; forward() is re-entrant (per-call workspace, one stream per call).
+class CudaQuantizedProvider : public LinearProvider {
+ public:
+  explicit CudaQuantizedProvider(const QuantizedModel& qm);
+  ~CudaQuantizedProvider() override;
+  Tensor forward(const std::string& layer, const Tensor& x) const override;
+
+ private:
+  const QuantizedModel& qm_;
+  std::map<std::string, std::shared_ptr<DeviceLayer>> layers_;
+};
+
+// run_quantized (engine.cpp:175-178) with the CUDA provider.
+Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed);
+
+}  // namespace cuda
+}  // namespace qarvd

@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -30,17 +31,21 @@ constexpr int BK = 128;  // bytes (= int8 elements) of K per pipeline stage: one
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
 
-template <int BN>
+// BN = output columns of the (pair) tile; CG = CTAs per MMA (1, or 2 = an SM pair
+// computing a 256-row tile, each CTA holding its 128 A rows and BN/2 B rows).
+template <int BN, int CG>
 struct GemmCfg {
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
   static constexpr int kABytes = BM * BK;
-  static constexpr int kBBytes = BN * BK;
+  static constexpr int kBBytes = (BN / CG) * BK;
+  static constexpr int kEpiBytes = 1024 /*align*/ + 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales*/ +
+                                   kEpiWarps * 2048 /*y staging*/;
+  static constexpr int kStages = (227 * 1024 - kEpiBytes) / (kABytes + kBBytes) > 8
+                                     ? 8
+                                     : (227 * 1024 - kEpiBytes) / (kABytes + kBBytes);
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kAccStages = 512 / (2 * BN);  // two accumulators per stage
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr size_t kSmemBytes =
-      static_cast<size_t>(kStages) * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/ +
-      kEpiWarps * 96 * sizeof(float) /*epilogue scale staging*/;
+  static constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + kEpiBytes;
 };
 
 struct GemmParams {
@@ -56,48 +61,65 @@ struct GemmParams {
   int epilogue;
   int out_dtype;
   int num_m_blks, num_n_blks, num_tiles;
+  const double* sx64;  // QARVD_F64 output: f64 scales, reference epilogue (engine.cpp:86-94)
+  const double* so64;
+  const double* sn64;
+  int use_tma_store;  // bf16 output through the TMA store path
+  int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
 };
 
 __device__ __forceinline__ float gelu_erf(float v) {
   return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
 }
 
-template <int BN>
+template <int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     dual_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-  using C = GemmCfg<BN>;
+                     const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
+  using C = GemmCfg<BN, CG>;
+  constexpr int TM = BM * CG;  // rows of the (pair) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint8_t* epi_ystage = sB + C::kStages * C::kBBytes;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 2048);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
-  float* epi_scratch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);
+  float* epi_scales = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int cta_id = static_cast<int>(blockIdx.x) / CG;  // pair index
+  const int num_ctas = static_cast<int>(gridDim.x) / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if (p.use_tma_store) ptx::prefetch_tmap(&tmY);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < C::kAccStages; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
+      ptx::mbar_init(&tempty[s], kEpiWarps * CG);  // one arrive per epilogue warp of the pair
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 2) {
+    if (CG == 2) ptx::tmem_alloc_2sm(tmem_slot, C::kTmemCols);
+    else ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -108,14 +130,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
         const int m_blk = t % p.num_m_blks;
         const int n_blk = t / p.num_m_blks;
+        const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
+        const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
-          ptx::tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_blk * BM);
-          ptx::tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_blk * BN);
+          if (p.debug == 2) {
+            if (leader) ptx::mbar_arrive(&full[stage]);
+          } else if (CG == 1) {
+            ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
+            ptx::tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, a_row);
+            ptx::tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, b_row);
+          } else {
+            if (leader) ptx::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+            ptx::tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, a_row);
+            ptx::tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, b_row);
+          }
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -125,13 +157,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = ptx::idesc_i8(TM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_o = tmem_base + static_cast<uint32_t>(acc * 2 * BN);
@@ -144,19 +176,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
             const int64_t kk = static_cast<int64_t>(kb) * BK + j * 32;
-            if (kk >= p.k) break;
+            if (kk >= p.k || p.debug == 1) break;
             const bool outl = kk < p.k_o;
             const uint32_t accumulate = (kk == 0 || kk == p.k_o) ? 0u : 1u;
             // +32 bytes along K inside the 128B swizzle row = +2 in the >>4 address field
-            ptx::mma_i8(outl ? d_o : d_n, a_desc + 2 * j, b_desc + 2 * j, idesc, accumulate);
+            if (CG == 1)
+              ptx::mma_i8(outl ? d_o : d_n, a_desc + 2 * j, b_desc + 2 * j, idesc, accumulate);
+            else
+              ptx::mma_i8_2sm(outl ? d_o : d_n, a_desc + 2 * j, b_desc + 2 * j, idesc, accumulate);
           }
-          ptx::mma_commit(&empty[stage]);
+          if (CG == 1) ptx::mma_commit(&empty[stage]);
+          else ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        if (CG == 1) ptx::mma_commit(&tfull[acc]);
+        else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
         if (++acc == C::kAccStages) {
           acc = 0;
           acc_phase ^= 1;
@@ -165,23 +202,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue: 8 warps, 2 per TMEM lane quadrant =====================
-    // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quadrant
-    // split the tile's 32-column chunks (even / odd).
+    // Warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quadrant split
+    // the tile's 32-column chunks (even / odd).  Each tile's column scales are prefetched
+    // into shared memory before the accumulator is ready (the loads overlap the MMAs);
+    // bf16 results go through a 64B-swizzled staging tile and a TMA bulk tensor store.
+    const int ew = warp - 4;
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int half = ew >> 2;
+    const int etid = ew * 32 + lane;
     const int row_in_tile = q * 32 + lane;
     const bool has_outlier = p.k_o > 0;
-    float* scr = epi_scratch + (warp - 4) * 96;  // per-warp staging of the chunk's column scales
+    uint8_t* ystage = epi_ystage + ew * 2048;  // 32 rows x 64 B, SWIZZLE_64B layout
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
       const int m_blk = t % p.num_m_blks;
       const int n_blk = t / p.num_m_blks;
+      float* sc = epi_scales + acc * 3 * BN;
+      if (p.out_dtype != QARVD_F64 && etid < BN) {
+        const int64_t j = static_cast<int64_t>(n_blk) * BN + etid;
+        const int64_t jc = j < p.n ? j : p.n - 1;
+        sc[etid] = __ldg(p.scale_wn + jc);
+        sc[BN + etid] = has_outlier ? __ldg(p.scale_wo + jc) : 0.f;
+        sc[2 * BN + etid] = p.bias ? __ldg(p.bias + jc) : 0.f;
+      }
+      const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM + q * 32;
+      const int64_t row = row0 + lane;
+      const bool row_ok = row < p.m;
+      const float sx = (row_ok && p.scale_x) ? __ldg(p.scale_x + row) : 0.f;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // scales visible to all epilogue warps
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int64_t row = static_cast<int64_t>(m_blk) * BM + row_in_tile;
-      const bool row_ok = row < p.m;
-      const float sx = row_ok ? __ldg(p.scale_x + row) : 0.f;
       const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
       const uint32_t t_o = tmem_base + t_lane + static_cast<uint32_t>(acc * 2 * BN);
       const uint32_t t_n = t_o + BN;
@@ -190,101 +241,126 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
         if (col0 >= p.n) break;  // warp-uniform
         const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
-        {
-          const int64_t jc = col0 + (lane < ncols ? lane : 0);
-          scr[lane] = __ldg(p.scale_wn + jc);
-          scr[32 + lane] = has_outlier ? __ldg(p.scale_wo + jc) : 0.f;
-          scr[64 + lane] = p.bias ? __ldg(p.bias + jc) : 0.f;
-        }
         uint32_t rn[32], ro[32];
         ptx::tmem_ld32(t_n + c * 32, rn);
         if (has_outlier) ptx::tmem_ld32(t_o + c * 32, ro);
         ptx::tmem_wait_ld();
-        __syncwarp();
-        if (row_ok) {
-          if (p.acc_n_dbg) {
+        if (p.out_dtype == QARVD_F64) {
+          // exact restatement of the reference epilogue: val = 0; val += (s_x*s_wo)*acc_o;
+          // val += (s_x*s_wn)*acc_n  (outlier group first, f64, no FMA)
+          if (row_ok) {
+            const double sx64 = p.sx64[row];
+            double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0;
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
               if (e >= ncols) continue;
-              p.acc_n_dbg[row * p.n + col0 + e] = static_cast<int32_t>(rn[e]);
-              if (p.acc_o_dbg)
-                p.acc_o_dbg[row * p.n + col0 + e] = has_outlier ? static_cast<int32_t>(ro[e]) : 0;
-            }
-          }
-          // y overwrites rn (as float bits): t = s_wo*acc_o; t = fmaf(s_wn, acc_n, t); y = s_x*t (+bias)
-#pragma unroll
-          for (int e4 = 0; e4 < 8; ++e4) {
-            const float4 sn4 = reinterpret_cast<const float4*>(scr)[e4];
-            const float4 so4 = reinterpret_cast<const float4*>(scr + 32)[e4];
-            const float4 sb4 = reinterpret_cast<const float4*>(scr + 64)[e4];
-            const float sn[4] = {sn4.x, sn4.y, sn4.z, sn4.w};
-            const float so[4] = {so4.x, so4.y, so4.z, so4.w};
-            const float sb[4] = {sb4.x, sb4.y, sb4.z, sb4.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int e = 4 * e4 + u;
-              const float an = __int2float_rn(static_cast<int>(rn[e]));
-              float tacc;
+              double v = 0.0;
               if (has_outlier)
-                tacc = __fmaf_rn(sn[u], an, __fmul_rn(so[u], __int2float_rn(static_cast<int>(ro[e]))));
-              else
-                tacc = __fmul_rn(sn[u], an);
-              float v = p.bias ? __fmaf_rn(sx, tacc, sb[u]) : __fmul_rn(sx, tacc);
-              if (p.epilogue & QARVD_EPI_GELU) v = gelu_erf(v);
-              rn[e] = __float_as_uint(v);
+                v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.so64[col0 + e]),
+                                           static_cast<double>(static_cast<int32_t>(ro[e]))));
+              v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.sn64[col0 + e]),
+                                         static_cast<double>(static_cast<int32_t>(rn[e]))));
+              yr[e] = v;
             }
           }
-          if (p.out_dtype == QARVD_BF16) {
-            __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
-            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
-              uint32_t pk[16];
+          continue;
+        }
+        if (row_ok && p.acc_n_dbg) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const __nv_bfloat162 h2 =
-                    __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
-                pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
-              }
-              uint4* dst = reinterpret_cast<uint4*>(yr);
-#pragma unroll
-              for (int v4 = 0; v4 < 4; ++v4)
-                dst[v4] = make_uint4(pk[4 * v4], pk[4 * v4 + 1], pk[4 * v4 + 2], pk[4 * v4 + 3]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
-            }
-          } else {
-            float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
-            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
-              float4* dst = reinterpret_cast<float4*>(yr);
-#pragma unroll
-              for (int v4 = 0; v4 < 8; ++v4)
-                dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
-                                      __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
-            } else {
-#pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (e < ncols) yr[e] = __uint_as_float(rn[e]);
-            }
+          for (int e = 0; e < 32; ++e) {
+            if (e >= ncols) continue;
+            p.acc_n_dbg[row * p.n + col0 + e] = static_cast<int32_t>(rn[e]);
+            if (p.acc_o_dbg)
+              p.acc_o_dbg[row * p.n + col0 + e] = has_outlier ? static_cast<int32_t>(ro[e]) : 0;
           }
         }
-        __syncwarp();  // scr is rewritten by the next chunk
+        // y overwrites rn (as float bits): t = s_wo*acc_o; t = fmaf(s_wn, acc_n, t); y = s_x*t (+bias)
+        const float* scc = sc + c * 32;
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
+          const float4 so4 = reinterpret_cast<const float4*>(scc + BN)[e4];
+          const float4 sb4 = reinterpret_cast<const float4*>(scc + 2 * BN)[e4];
+          const float sn[4] = {sn4.x, sn4.y, sn4.z, sn4.w};
+          const float so[4] = {so4.x, so4.y, so4.z, so4.w};
+          const float sb[4] = {sb4.x, sb4.y, sb4.z, sb4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = 4 * e4 + u;
+            const float an = __int2float_rn(static_cast<int>(rn[e]));
+            float tacc;
+            if (has_outlier)
+              tacc = __fmaf_rn(sn[u], an, __fmul_rn(so[u], __int2float_rn(static_cast<int>(ro[e]))));
+            else
+              tacc = __fmul_rn(sn[u], an);
+            float v = p.bias ? __fmaf_rn(sx, tacc, sb[u]) : __fmul_rn(sx, tacc);
+            if (p.epilogue & QARVD_EPI_GELU) v = gelu_erf(v);
+            rn[e] = __float_as_uint(v);
+          }
+        }
+        if (p.use_tma_store) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const __nv_bfloat162 h2 =
+                __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
+            pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          if (lane == 0) ptx::bulk_wait_read0();  // previous store has finished reading ystage
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int phys = (i ^ ((lane >> 1) & 3)) << 4;
+            *reinterpret_cast<uint4*>(ystage + lane * 64 + phys) =
+                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && row0 < p.m) {
+            ptx::tma_store_2d(&tmY, ystage, static_cast<int32_t>(col0), static_cast<int32_t>(row0));
+            ptx::bulk_commit();
+          }
+        } else if (row_ok && p.out_dtype == QARVD_BF16) {
+          __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
+        } else if (row_ok) {
+          float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
+          if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
+            float4* dst = reinterpret_cast<float4*>(yr);
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4)
+              dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
+                                    __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e < ncols) yr[e] = __uint_as_float(rn[e]);
+          }
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 1) ptx::mbar_arrive(&tempty[acc]);
+        else ptx::mbar_arrive_leader(&tempty[acc]);
+      }
       if (++acc == C::kAccStages) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) ptx::bulk_wait_all();
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, C::kTmemCols);
+    if (CG == 2) ptx::tmem_dealloc_2sm(tmem_base, C::kTmemCols);
+    else ptx::tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
@@ -321,6 +397,22 @@ int make_operand_tmap(CUtensorMap* map, const int8_t* base, int64_t rows, int64_
   return QARVD_OK;
 }
 
+// bf16 output [m x n] (ld elements), box 32 cols x 32 rows, 64B swizzle (epilogue staging)
+int make_y_tmap(CUtensorMap* map, void* y, int64_t m, int64_t n, int64_t ld) {
+  auto encode = get_encode_fn();
+  if (!encode) QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed with CUresult " + std::to_string(r));
+  return QARVD_OK;
+}
+
 int sm_count() {
   static int count = 0;
   static std::once_flag once;
@@ -333,14 +425,14 @@ int sm_count() {
   return count;
 }
 
-template <int BN>
+template <int BN, int CG>
 int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, GemmParams p,
                 cudaStream_t stream) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, CG>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(dual_gemm_kernel<BN>,
+    attr_err = cudaFuncSetAttribute(dual_gemm_kernel<BN, CG>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(C::kSmemBytes));
   });
@@ -348,37 +440,62 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   CUtensorMap ta, tb;
   int st = make_operand_tmap(&ta, xq, p.m, p.k, ldq, BM);
   if (st) return st;
-  st = make_operand_tmap(&tb, wq, p.n, p.k, ldw, BN);
+  st = make_operand_tmap(&tb, wq, p.n, p.k, ldw, BN / CG);
   if (st) return st;
-  p.num_m_blks = static_cast<int>((p.m + BM - 1) / BM);
+  CUtensorMap ty;
+  std::memset(&ty, 0, sizeof(ty));
+  p.use_tma_store = p.out_dtype == QARVD_BF16 && !p.acc_n_dbg && !p.acc_o_dbg &&
+                    (reinterpret_cast<uintptr_t>(p.y) & 15) == 0 && (p.ldy * 2) % 16 == 0;
+  if (p.use_tma_store) {
+    st = make_y_tmap(&ty, p.y, p.m, p.n, p.ldy);
+    if (st) return st;
+  }
+  p.num_m_blks = static_cast<int>((p.m + BM * CG - 1) / (BM * CG));
   p.num_n_blks = static_cast<int>((p.n + BN - 1) / BN);
   p.num_tiles = p.num_m_blks * p.num_n_blks;
-  const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-  dual_gemm_kernel<BN><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+  const int units = sm_count() / CG;
+  const int grid = CG * (p.num_tiles < units ? p.num_tiles : units);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QARVD_CUDA_TRY(cudaLaunchKernelEx(&cfg, dual_gemm_kernel<BN, CG>, ta, tb, ty, p));
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;
 }
 
-// Tile-width choice: minimise waves x BN (per-SM work on the critical path).
-int choose_bn(int64_t m, int64_t n) {
+// CTA-group choice: QARVD_GEMM_CG=1|2 overrides (default 2: SM pairs).
+int choose_cg() {
+  if (const char* env = getenv("QARVD_GEMM_CG")) {
+    const int v = atoi(env);
+    if (v == 1 || v == 2) return v;
+  }
+  return 2;
+}
+
+// Tile-width choice (QARVD_GEMM_BN=128|256 overrides).
+int choose_bn(int64_t m, int64_t n, int64_t k) {
   if (const char* env = getenv("QARVD_GEMM_BN")) {
     const int v = atoi(env);
     if (v == 128 || v == 256) return v;
   }
-  const int64_t mb = (m + BM - 1) / BM;
-  const int64_t sms = sm_count();
-  int best = 256;
-  int64_t best_cost = -1;
-  for (int bn : {256, 128}) {
-    const int64_t tiles = mb * ((n + bn - 1) / bn);
-    const int64_t cost = ((tiles + sms - 1) / sms) * bn;
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = bn;
-    }
-  }
-  return best;
+  // BN = 256 halves the B-operand traffic per MAC but leaves room for only one
+  // TMEM accumulator stage (2 accumulators x 256 columns), so its epilogue does
+  // not overlap the next tile's MMAs.  That pays off only when the mainloop is
+  // long compared with the epilogue (large K); measured on B200 at the Wan
+  // shapes: K=1536 -> BN=128 faster, K=8960 -> BN=256 faster.
+  (void)m;
+  (void)n;
+  return k >= 4096 ? 256 : 128;
 }
 
 }  // namespace
@@ -387,8 +504,12 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
                      int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
                      const float* scale_wo, const float* scale_wn, const float* bias,
                      int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
-                     int32_t* acc_n, cudaStream_t stream) {
+                     int32_t* acc_n, cudaStream_t stream, const double* sx64 = nullptr,
+                     const double* so64 = nullptr, const double* sn64 = nullptr) {
   GemmParams p{};
+  p.sx64 = sx64;
+  p.so64 = so64;
+  p.sn64 = sn64;
   p.m = m;
   p.n = n;
   p.k = k;
@@ -401,10 +522,15 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.ldy = ldy;
   p.acc_o_dbg = acc_o;
   p.acc_n_dbg = acc_n;
+  p.debug = getenv("QARVD_GEMM_DEBUG") ? atoi(getenv("QARVD_GEMM_DEBUG")) : 0;
   p.epilogue = epilogue;
   p.out_dtype = out_dtype;
-  return choose_bn(m, n) == 256 ? launch_gemm<256>(xq, ldq, wq, ldw, p, stream)
-                                : launch_gemm<128>(xq, ldq, wq, ldw, p, stream);
+  const int bn = choose_bn(m, n, k);
+  if (choose_cg() == 2)
+    return bn == 256 ? launch_gemm<256, 2>(xq, ldq, wq, ldw, p, stream)
+                     : launch_gemm<128, 2>(xq, ldq, wq, ldw, p, stream);
+  return bn == 256 ? launch_gemm<256, 1>(xq, ldq, wq, ldw, p, stream)
+                   : launch_gemm<128, 1>(xq, ldq, wq, ldw, p, stream);
 }
 
 }  // namespace qarvd_b200
@@ -438,4 +564,30 @@ extern "C" int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, 
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
                           scale_w_normal, bias, epilogue, out_dtype, y, ldy, acc_outlier,
                           acc_normal, as_stream(stream));
+}
+
+extern "C" int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                   int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                   const double* scale_x, const double* scale_w_outlier,
+                                   const double* scale_w_normal, double* y, int64_t ldy,
+                                   void* stream) {
+  clear_error();
+  if (m <= 0 || n <= 0 || k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
+  if (k % 32 != 0 || k_outlier % 32 != 0 || k_outlier < 0 || k_outlier >= k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "kernel_b: k and k_outlier must be multiples of 32 with 0 <= k_outlier < k");
+  if (k > 132104)
+    QARVD_FAIL(QARVD_ERR_LOGIC, "kernel_b: reduction dimension too large for exact int32 accumulation");
+  if (ldq < k || ldw < k || ldq % 16 || ldw % 16 || ldy < n)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: invalid leading dimension");
+  if (!xq || !wq || !scale_x || !scale_w_normal || !y || (k_outlier > 0 && !scale_w_outlier))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
+  if ((reinterpret_cast<uintptr_t>(xq) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: operand pointers must be 16-byte aligned");
+  if (int st = require_device()) return st;
+  static const float kDummy = 0.f;  // f32 scales unused on the f64 path
+  (void)kDummy;
+  return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, nullptr, nullptr, nullptr, nullptr,
+                          QARVD_EPI_NONE, QARVD_F64, y, ldy, nullptr, nullptr, as_stream(stream),
+                          scale_x, scale_w_outlier, scale_w_normal);
 }

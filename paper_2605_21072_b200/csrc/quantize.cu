@@ -260,44 +260,44 @@ __device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
-template <bool kStatic>
-__device__ __forceinline__ int act_code(uint16_t h, float r32, double s64, bool exact, int qmax) {
-  const float v = bf16_bits_to_float(h);
-  if (exact) return quant_code_exact(static_cast<double>(v), s64, qmax);
-  const float t = __fmul_rn(v, r32);
-  float q = rintf(t);
-  if (fabsf(__fsub_rn(t, q)) > 0.4999f) {
-    if (!kStatic || fabsf(t) <= 254.0f) return quant_code_exact(static_cast<double>(v), s64, qmax);
-  }
-  if (kStatic) q = fminf(fmaxf(q, -static_cast<float>(qmax)), static_cast<float>(qmax));
-  return static_cast<int>(q);  // per-token: |t| <= qmax by construction
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: an fp32 add rounds to an integer (RNE)
+
+__device__ __noinline__ int act_code_exact(float v, double s64, int qmax) {
+  return quant_code_exact(static_cast<double>(v), s64, qmax);
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
 
 template <bool kStatic>
 __global__ void __launch_bounds__(kActThreads)
-    quant_act_tma_kernel(const uint16_t* __restrict__ x, int64_t m, int64_t k, int64_t ldx,
-                         const int32_t* __restrict__ gather, int64_t k_out, int G,
+    quant_act_tma_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                         const int32_t* __restrict__ gather, int k_out, int G,
                          double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
                          float* __restrict__ s32_out, double* __restrict__ s64_out,
                          unsigned long long* err) {
   extern __shared__ __align__(128) uint8_t smem_act[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t row_elems = (k + 7) & ~int64_t(7);
-  const int64_t stage_elems = row_elems * G;
+  const int row_elems = (k + 1 + 7) & ~7;  // +1: zero sentinel read by pad columns
+  const int stage_elems = row_elems * G;
   uint16_t* rows = reinterpret_cast<uint16_t*>(smem_act);
   int16_t* gidx = reinterpret_cast<int16_t*>(rows + kActStages * stage_elems);
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(gidx + ((k_out + 7) & ~int64_t(7))) + 15) & ~uintptr_t(15));
-  float* part = reinterpret_cast<float*>(full + kActStages);
-  uint32_t* badflag = reinterpret_cast<uint32_t*>(part + 8);  // per-warp non-finite flags
+      (reinterpret_cast<uintptr_t>(gidx + ((k_out + 7) & ~7)) + 15) & ~uintptr_t(15));
+  uint32_t* part = reinterpret_cast<uint32_t*>(full + kActStages);  // per-warp |x| maxima (bits)
 
   const int64_t num_groups = (m + G - 1) / G;
-  const int W = 8 / G;              // warps per row
-  const int my_row = warp / W;      // row inside the group
-  const int sub = warp % W;         // column share of this warp
+  const int W = 8 / G;          // warps per row
+  const int my_row = warp / W;  // row inside the group
+  const int sub = warp % W;     // column share of this warp
 
-  for (int64_t c = tid; c < k_out; c += kActThreads)
-    gidx[c] = gather ? static_cast<int16_t>(__ldg(gather + c)) : static_cast<int16_t>(c);
+  for (int c = tid; c < k_out; c += kActThreads) {
+    const int src = gather ? __ldg(gather + c) : c;
+    gidx[c] = static_cast<int16_t>(src < 0 ? k : src);
+  }
+  for (int r = tid; r < kActStages * G; r += kActThreads)
+    for (int e = k; e < row_elems; ++e) rows[r * row_elems + e] = 0;
   if (tid == 0) {
     for (int s = 0; s < kActStages; ++s) mbar_init_(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kActThreads)
     if (g >= num_groups) return;
     const int64_t r0 = g * G;
     const int nr = static_cast<int>((m - r0) < G ? (m - r0) : G);
-    const uint32_t bytes = static_cast<uint32_t>(k * 2);
+    const uint32_t bytes = static_cast<uint32_t>(k) * 2u;
     mbar_expect_tx_(&full[slot], bytes * nr);
     for (int r = 0; r < nr; ++r)
       bulk_load(rows + slot * stage_elems + r * row_elems, x + (r0 + r) * ldx, bytes, &full[slot]);
@@ -317,10 +317,9 @@ __global__ void __launch_bounds__(kActThreads)
   if (tid == 0)
     for (int s = 0; s < kActStages; ++s) issue(s, s);
 
-  GroupScale gs_static;
-  if (kStatic) gs_static = scale_static(static_scale);
-  const int64_t csz = ((k + W - 1) / W);            // source columns per warp (absmax)
-  const int64_t osz = (((k_out + W - 1) / W) + 15) & ~int64_t(15);  // output columns per warp
+  const int csz = (((k + W - 1) / W) + 7) & ~7;     // source columns per warp (absmax)
+  const int osz = (((k_out + W - 1) / W) + 15) & ~15;  // output columns per warp
+  const float fq = static_cast<float>(qmax);
 
   for (int64_t it = 0;; ++it) {
     const int64_t g = blockIdx.x + it * gridDim.x;
@@ -331,85 +330,93 @@ __global__ void __launch_bounds__(kActThreads)
     const bool active = row < m;
     const uint16_t* rs = rows + slot * stage_elems + my_row * row_elems;
 
-    GroupScale gsc;
-    bool row_bad = false;
-    if (!kStatic) {
-      float amax = 0.f;
-      bool bad = false;
-      if (active) {
-        const int64_t c0 = sub * csz, c1 = (c0 + csz) < k ? (c0 + csz) : k;
-        for (int64_t c = c0 + lane * 8; c < c1; c += 256) {
-          if (c + 8 <= c1 && (c & 7) == 0) {
-            const uint4 d = *reinterpret_cast<const uint4*>(rs + c);
-            const uint32_t w4[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const uint32_t lo = w4[h] & 0x7fffu, hi = (w4[h] >> 16) & 0x7fffu;
-              bad |= (lo >= 0x7f80u) | (hi >= 0x7f80u);
-              amax = fmaxf(amax, fmaxf(__uint_as_float(lo << 16), __uint_as_float(hi << 16)));
-            }
-          } else {
-            for (int64_t e = c; e < c + 8 && e < c1; ++e) {
-              const uint32_t b = rs[e] & 0x7fffu;
-              bad |= b >= 0x7f80u;
-              amax = fmaxf(amax, __uint_as_float(b << 16));
-            }
-          }
-        }
+    // ---- |x| max as packed 16-bit integer max of the sign-cleared bf16 bits;
+    //      non-finite values (exponent all ones) are exactly the maxima >= 0x7f80
+    uint32_t mx = 0;
+    if (active) {
+      const int c0 = sub * csz, c1 = min(c0 + csz, k);
+      int c = c0 + lane * 8;
+      for (; c + 8 <= c1; c += 256) {
+        const uint4 d = *reinterpret_cast<const uint4*>(rs + c);
+        mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
+                                   __vmaxu2(d.z & 0x7fff7fffu, d.w & 0x7fff7fffu)));
       }
-      amax = warp_max(amax);
-      row_bad = __any_sync(0xffffffffu, bad);
-      if (W > 1) {
-        if (lane == 0) {
-          part[warp] = amax;
-          badflag[warp] = row_bad ? 1u : 0u;
-        }
-        __syncthreads();
-        for (int w = 0; w < W; ++w) {
-          amax = fmaxf(amax, part[my_row * W + w]);
-          row_bad |= badflag[my_row * W + w] != 0;
-        }
-      }
-      gsc = scale_from_absmax(amax, qmax);
-      if (active && sub == 0 && lane == 0) {
-        if (s32_out) s32_out[row] = gsc.s32;
-        if (s64_out) s64_out[row] = gsc.s64;
-      }
-    } else {
-      gsc = gs_static;
-      if (active && sub == 0 && lane == 0) {
-        if (s32_out) s32_out[row] = gsc.s32;
-        if (s64_out) s64_out[row] = gsc.s64;
-      }
+      for (; c < c1; ++c) mx = max(mx, static_cast<uint32_t>(rs[c] & 0x7fffu));
     }
-    const bool check_bad = kStatic || row_bad;
+    uint32_t mag = max(mx & 0xffffu, mx >> 16);
+    mag = __reduce_max_sync(0xffffffffu, mag);
+    if (W > 1) {
+      if (lane == 0) part[warp] = mag;
+      __syncthreads();
+      for (int w = 0; w < W; ++w) mag = max(mag, part[my_row * W + w]);
+    }
+    const bool row_bad = mag >= 0x7f80u;
+    GroupScale gsc = kStatic ? scale_static(static_scale)
+                             : scale_from_absmax(__uint_as_float(mag << 16), qmax);
+    if (active && sub == 0 && lane == 0) {
+      if (s32_out) s32_out[row] = gsc.s32;
+      if (s64_out) s64_out[row] = gsc.s64;
+    }
 
     if (active) {
       int8_t* qr = q + row * ldq;
-      const int64_t o0 = sub * osz, o1 = (o0 + osz) < k_out ? (o0 + osz) : k_out;
-      for (int64_t c0 = o0 + lane * 16; c0 < o1; c0 += 512) {
-        const uint4 ga = *reinterpret_cast<const uint4*>(gidx + c0);
-        const uint4 gb = *reinterpret_cast<const uint4*>(gidx + c0 + 8);
-        const uint32_t gw[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        uint32_t packed[4] = {0, 0, 0, 0};
+      const int o0 = sub * osz, o1 = min(o0 + osz, k_out);
+      if (!row_bad && !gsc.exact) {
+        const float r = gsc.r32;
+        for (int c0 = o0 + lane * 16; c0 < o1; c0 += 512) {
+          const uint4 ga = *reinterpret_cast<const uint4*>(gidx + c0);
+          const uint4 gb = *reinterpret_cast<const uint4*>(gidx + c0 + 8);
+          const uint32_t gw[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+          float v[16];
+          uint32_t rr[16];
+          bool need = false;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int src = static_cast<int16_t>((gw[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          int code = 0;
-          if (src >= 0) {
-            const uint16_t h = rs[src];
-            if (check_bad && (h & 0x7f80u) == 0x7f80u) {
-              if (err) atomicMin(err, static_cast<unsigned long long>(row * k_out + c0 + e));
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t src = (gw[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+            v[e] = __uint_as_float(static_cast<uint32_t>(rs[src]) << 16);
+            float t, d;
+            if (kStatic) {
+              t = fminf(fmaxf(__fmul_rn(v[e], r), -fq), fq);
+              const float y = __fadd_rn(t, kMagic);
+              d = __fsub_rn(t, __fsub_rn(y, kMagic));
+              rr[e] = __float_as_uint(y);
             } else {
-              code = act_code<kStatic>(h, gsc.r32, gsc.s64, gsc.exact, qmax);
+              const float y = __fmaf_rn(v[e], r, kMagic);
+              d = __fmaf_rn(v[e], r, -__fsub_rn(y, kMagic));
+              rr[e] = __float_as_uint(y);
+            }
+            need |= fabsf(d) > 0.4999f;
+          }
+          if (need) {  // within 1e-4 of a .5 tie: the exact f64 division decides
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float t = kStatic ? fminf(fmaxf(__fmul_rn(v[e], r), -fq), fq) : 0.f;
+              const float d = kStatic ? __fsub_rn(t, rintf(t))
+                                      : __fmaf_rn(v[e], r, -__fsub_rn(__uint_as_float(rr[e]), kMagic));
+              if (fabsf(d) > 0.4999f) rr[e] = static_cast<uint32_t>(act_code_exact(v[e], gsc.s64, qmax));
             }
           }
-          packed[e >> 2] |= (static_cast<uint32_t>(code) & 0xffu) << (8 * (e & 3));
+          *reinterpret_cast<uint4*>(qr + c0) =
+              make_uint4(pack4(rr[0], rr[1], rr[2], rr[3]), pack4(rr[4], rr[5], rr[6], rr[7]),
+                         pack4(rr[8], rr[9], rr[10], rr[11]), pack4(rr[12], rr[13], rr[14], rr[15]));
         }
-        *reinterpret_cast<uint4*>(qr + c0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        // rare rows: a non-finite input (reported, reference throws) or an unusable fp32 reciprocal
+        for (int c = o0 + lane; c < o1; c += 32) {
+          const int src = gidx[c];
+          const uint16_t h = rs[src];
+          int code = 0;
+          if ((h & 0x7f80u) == 0x7f80u) {
+            if (err) atomicMin(err, static_cast<unsigned long long>(row * k_out + c));
+          } else {
+            code = gsc.exact ? act_code_exact(bf16_bits_to_float(h), gsc.s64, qmax)
+                             : quant_code_fast(bf16_bits_to_float(h), gsc.r32, gsc.s64, qmax);
+          }
+          qr[c] = static_cast<int8_t>(code);
+        }
       }
     }
-    __syncthreads();  // every warp is done with this slot (and with part[] / badflag)
+    __syncthreads();  // every warp is done with this slot (and with part[])
     if (tid == 0) issue(it + kActStages, slot);
   }
 }
@@ -501,13 +508,14 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
   }
   if (m == 0) return QARVD_OK;
   const int grid = grid_for_rows(m);
-  const bool tma_ok = MODE != kWeightDual && dtype == QARVD_BF16 && k <= 16384 &&
+  const bool tma_ok = MODE != kWeightDual && dtype == QARVD_BF16 && k < 16384 &&
                       (k % 8) == 0 && (ldx % 8) == 0 && (k_out % 16) == 0 && (ldq % 16) == 0 &&
                       (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(q) & 15) == 0;
   if (tma_ok) {
     const int G = k <= 1536 ? 8 : (k <= 3072 ? 4 : (k <= 6144 ? 2 : 1));
-    const size_t smem = static_cast<size_t>(kActStages) * G * k * 2 + k_out * 2 + 64 +
+    const size_t row_elems = (k + 1 + 7) & ~int64_t(7);
+    const size_t smem = static_cast<size_t>(kActStages) * G * row_elems * 2 + k_out * 2 + 64 +
                         kActStages * 8 + 16 * 4 + 16;
     auto kern = quant_act_tma_kernel<MODE == kActStatic>;
     static std::once_flag once;
@@ -520,9 +528,9 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
     const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
     const int64_t cap = static_cast<int64_t>(kNumSMs) * ctas_per_sm;
     const int g = static_cast<int>(groups < cap ? groups : cap);
-    kern<<<g, kActThreads, smem, stream>>>(static_cast<const uint16_t*>(x), m, k, ldx, gather,
-                                           k_out, G, static_scale, qmax, q, ldq, s32_n, s64_n,
-                                           err);
+    kern<<<g, kActThreads, smem, stream>>>(static_cast<const uint16_t*>(x), m, static_cast<int>(k),
+                                           ldx, gather, static_cast<int>(k_out), G, static_scale,
+                                           qmax, q, ldq, s32_n, s64_n, err);
   } else if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
     const size_t smem = static_cast<size_t>(kWarpsPerCta) * (((k + 7) & ~int64_t(7)) * 2);
     static std::once_flag once;

@@ -46,17 +46,19 @@ for name, n, k, no in [("qkv", 1536, 1536, 32), ("ffn0", 8960, 1536, 32), ("ffn2
     x = synth.synth_activation(M, k, seed=3)
     xq, sx, _ = engine.kernel_a_quantize_activation(x, L)
     y = torch.empty((M, n), dtype=torch.bfloat16, device="cuda")
-    for bn in (128, 256):
+    for cg, bn in ((1, 128), (1, 256), (2, 128), (2, 256)):
         os.environ["QARVD_GEMM_BN"] = str(bn)
+        os.environ["QARVD_GEMM_CG"] = str(cg)
         for epi in (qb.EPI_NONE, qb.EPI_GELU):
             f = lambda: _lib.call("qarvd_dual_gemm", xq.data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad, M, n,
                                   L.k_pad, L.k_outlier, sx.data_ptr(), L.scale_outlier32.data_ptr(),
                                   L.scale_normal32.data_ptr(), None, epi, qb.BF16, y.data_ptr(), n,
                                   None, None, st)
             ms = timeit(f)
-            out[f"gemm_{name}_bn{bn}_{'gelu' if epi else 'none'}"] = {
+            out[f"gemm_{name}_cg{cg}_bn{bn}_{'gelu' if epi else 'none'}"] = {
                 "ms": ms, "tops": 2.0 * M * n * k / (ms * 1e-3) / 1e12}
     os.environ.pop("QARVD_GEMM_BN")
+    os.environ.pop("QARVD_GEMM_CG")
     for gran in (qb.ACT_PER_TOKEN, qb.ACT_PER_TENSOR):
         f = lambda: _lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, M, k, k, L.gather_dev.data_ptr(),
                               L.k_pad, gran, 0.05, 8, xq.data_ptr(), L.k_pad, sx.data_ptr(), None, None, st)

@@ -1,0 +1,133 @@
+// Drop-in test: the reference's own pipeline (toy model -> calibrate_model ->
+// QuantizedModel) served through qarvd::cuda (libqarvd_b200.so) instead of the
+// reference engine, compared with the reference engine on identical inputs.
+// Built against the reference headers and oracle/_ref/libqarvd_ref.a (the
+// unmodified reference sources); run on a GPU box by tests/test_gpu_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
+#include "../../paper_2605_21072_b200/adapter/qarvd_cuda.hpp"
+#include "qarvd/calibrate.hpp"
+#include "qarvd/engine.hpp"
+#include "qarvd/outlier.hpp"
+#include "qarvd/rng.hpp"
+#include "qarvd/sensitivity.hpp"
+#include "qarvd/toy_model.hpp"
+
+using namespace qarvd;
+
+static int failures = 0;
+#define EXPECT(cond, what)                                 \
+  do {                                                     \
+    if (!(cond)) {                                         \
+      std::printf("FAIL %s (%s:%d)\n", what, __FILE__, __LINE__); \
+      ++failures;                                          \
+    }                                                      \
+  } while (0)
+
+static Tensor random_tensor(size_t r, size_t c, uint64_t seed, double scale) {
+  Prng rng(seed);
+  Tensor t({r, c});
+  for (size_t i = 0; i < t.size(); ++i) t[i] = rng.gaussian() * scale;
+  return t;
+}
+
+int main() {
+  ToyModelConfig cfg;  // toy defaults (toy_model.hpp:24-38) + outlier injections
+  cfg.injections = {{"ffn.2", 0.05, 8.0}, {"self_attn.q", 0.03, 6.0}};
+  const ToyModel model = ToyModel::build(cfg);
+  SensitivityProfile prof;
+  prof.alpha_raw.assign(cfg.chunks, 1.0);
+  prof.alpha_normalized = normalize_alpha(prof.alpha_raw);
+  const std::vector<double> w = weighting_strategy(prof, WeightingKind::heuristic_exp);
+  ModelCalibOptions opts;
+  opts.base.iterations = 8;
+  opts.base.batch_size = 2;
+  const ModelCalibResult calib = calibrate_model(model, w, opts);
+  const QuantizedModel& qm = calib.qmodel;
+  std::printf("calibrated %zu layers\n", qm.layers.size());
+
+  // ---- per-operator parity on every quantized layer
+  size_t n_layers = 0;
+  for (const auto& l : qm.layers) {
+    if (l.preserved) continue;
+    ++n_layers;
+    const Tensor x = random_tensor(24, l.in_dim, 77 + n_layers, 1.5);
+    // kernel A: bit-exact codes
+    const Tensor xp = permute_activations(x, l.plan);
+    const IntTensor a_ref = qarvd::kernel_a_quantize_activation(xp, l.act);
+    const IntTensor a_gpu = qarvd::cuda::kernel_a_quantize_activation(xp, l.act);
+    EXPECT(a_ref.data == a_gpu.data, ("kernel_a codes " + l.name).c_str());
+    // kernel B: tensor-core int32 accumulators + the reference's f64 epilogue -> bit-identical
+    const Tensor b_ref = qarvd::kernel_b_gemm_dequant(a_ref, l);
+    const Tensor b_gpu = qarvd::cuda::kernel_b_gemm_dequant(a_ref, l);
+    EXPECT(b_ref.vec() == b_gpu.vec(), ("kernel_b bit-exact " + l.name).c_str());
+    // full layer forward (K1 + K2 on the device)
+    const Tensor f_ref = qarvd::quantized_layer_forward(l, x, Engine::int_kernels);
+    const Tensor f_gpu = qarvd::cuda::quantized_layer_forward(l, x, Engine::int_kernels);
+    EXPECT(f_ref.vec() == f_gpu.vec(), ("layer forward bit-exact " + l.name).c_str());
+    // outlier detection on the layer's f64 weight: bit-exact report
+    const OutlierReport r_ref = qarvd::analyze_layer(l.name, model.weight(l.name));
+    const OutlierReport r_gpu = qarvd::cuda::analyze_layer(l.name, model.weight(l.name));
+    EXPECT(r_ref.norms == r_gpu.norms, ("norms " + l.name).c_str());
+    EXPECT(r_ref.median == r_gpu.median && r_ref.mad == r_gpu.mad &&
+               r_ref.threshold == r_gpu.threshold,
+           ("median/mad/threshold " + l.name).c_str());
+    EXPECT(r_ref.raw_outliers == r_gpu.raw_outliers && r_ref.aligned_outliers == r_gpu.aligned_outliers,
+           ("outlier indices " + l.name).c_str());
+  }
+  std::printf("checked %zu quantized layers\n", n_layers);
+
+  // ---- the seam: run_rollout with the CUDA provider vs the reference int engine
+  for (uint64_t seed : {5000ull, 5001ull}) {
+    const Rollout ref = run_quantized(qm, seed, Engine::int_kernels);
+    const Rollout gpu = qarvd::cuda::run_quantized(qm, seed);
+    double max_diff = 0.0, max_abs = 0.0;
+    for (size_t c = 0; c < ref.chunks.size(); ++c)
+      for (size_t i = 0; i < ref.chunks[c].size(); ++i) {
+        max_diff = std::max(max_diff, std::fabs(ref.chunks[c][i] - gpu.chunks[c][i]));
+        max_abs = std::max(max_abs, std::fabs(ref.chunks[c][i]));
+      }
+    std::printf("rollout seed %llu: max |diff| %.3e (max |latent| %.3e)\n",
+                static_cast<unsigned long long>(seed), max_diff, max_abs);
+    EXPECT(max_diff == 0.0, "rollout latents bit-identical");
+  }
+
+  // ---- error convention: same exception types as the reference
+  {
+    bool ok = false;
+    const qarvd::cuda::CudaQuantizedProvider p(qm);
+    try {
+      p.forward("no_such_layer", Tensor({1, cfg.hidden}));
+    } catch (const std::out_of_range&) {
+      ok = true;
+    }
+    EXPECT(ok, "missing layer -> std::out_of_range");
+    ok = false;
+    for (const auto& l : qm.layers)
+      if (l.preserved) {
+        try {
+          qarvd::cuda::kernel_b_gemm_dequant(IntTensor{{1, l.in_dim}, std::vector<int32_t>(l.in_dim), 8}, l);
+        } catch (const std::invalid_argument& e) {
+          ok = std::string(e.what()).rfind("kernel_b: layer is preserved", 0) == 0;
+        }
+        break;
+      }
+    EXPECT(ok, "preserved layer -> std::invalid_argument");
+    ok = false;
+    Tensor bad = random_tensor(2, qm.layers[1].in_dim, 3, 1.0);
+    bad[5] = std::nan("");
+    try {
+      qarvd::cuda::kernel_a_quantize_activation(bad, QuantParams::per_tensor_symmetric(8, 0.1));
+    } catch (const std::invalid_argument& e) {
+      ok = std::string(e.what()) == "quantize: non-finite input at flat index 5";
+    }
+    EXPECT(ok, "non-finite -> std::invalid_argument with the reference message");
+  }
+
+  std::printf(failures ? "DROPIN FAIL %d\n" : "DROPIN PASS\n", failures);
+  return failures ? 1 : 0;
+}
