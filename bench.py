@@ -248,6 +248,57 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line))
 
 
+def calibration_bench(torch, world, rank, steps, hbm_peak):
+    """Config 4: frame-weighted calibration over all 300 Wan-1.3B layers (21 frames x 1560
+    tokens, heuristic_exp frame weights), layers LPT-sharded over the ranks, one all-gather
+    of the per-layer records.  Timed: K3 detection + K5 weight prep + K4 search + gather."""
+    import torch.distributed as dist
+    from paper_2605_21072_b200 import calibrate, synth
+
+    specs = synth.wan_registry()
+    frames, rows = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME
+    rows_of = lambda s: rows if s.tokens != synth.WAN_TEXT_LEN else synth.WAN_TEXT_LEN
+    costs = [calibrate.layer_cost_bytes(s, frames, rows_of(s)) for s in specs]
+    assign = calibrate.lpt_assign(costs, world)
+    weights = calibrate.weighting_strategy("heuristic_exp", frames)
+    shard = calibrate.CalibrationShard(specs, assign[rank], frames, rows, frame_weights=weights)
+    shard.setup()
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def step():
+        recs = shard.run()
+        if world > 1:
+            recs = calibrate.allgather_records(recs, device=dev)
+        return recs
+
+    recs = step()  # warm-up
+    ts = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        recs = step()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([float(np.mean(ts))], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_bytes = sum(costs)
+    return {"layers": len(specs), "layers_per_s": len(specs) / (ms * 1e-3), "ms_per_calibration": ms,
+            "steps": steps, "frames": frames, "tokens_per_frame": rows, "weighting": "heuristic_exp",
+            "records_gathered": len(recs),
+            "roofline": {"bound": "hbm", "achieved": total_bytes / world / (ms * 1e-3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": total_bytes / world / (ms * 1e-3) / 1e9 / hbm_peak,
+                         "algorithmic_bytes_total": total_bytes,
+                         "note": "one read of X and W + int8 codes per layer, per rank share"},
+            "sharding": f"LPT over {world} rank(s), one all_gather of packed records"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,6 +306,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-calib", action="store_true")
+    ap.add_argument("--calib-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args.gpus)
@@ -367,6 +420,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e = float(tt.item())
 
+    calib = None
+    if not args.no_calib:
+        calib = calibration_bench(torch, world, rank, args.calib_steps, peaks.get("hbm_gbs", 6650.0))
+
     if rank == 0:
         gemm = float(np.mean(gemm_ms))
         achieved = ops_per_step / (gemm * 1e-3) / 1e12
@@ -406,6 +463,7 @@ def main():
                     "h2d_bytes_per_step": M_TOKENS * DIM * 2, "d2h_bytes_per_step": M_TOKENS * DIM * 2,
                     "ms_per_step": e2e, "path": "qarvd_linear_chain_forward_host (C-ABI, pinned host buffers)"},
             "gpu_launches": int(launches),
+            "calibration": calib,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

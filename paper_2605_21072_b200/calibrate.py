@@ -228,3 +228,78 @@ def calibrate_model_sharded(costs: Sequence[float], compute: Callable[[List[int]
     if world == 1:
         return sorted(local, key=lambda r: r.index)
     return allgather_records(local, group=group, device=device)
+
+
+# ---------------------------------------------------------------------------
+# config 4: the per-layer calibration unit on the device, for a shard of the Wan registry
+
+def layer_cost_bytes(spec, frames: int, rows: int) -> float:
+    """Algorithmic bytes of one layer's calibration unit: one read of X, one read of W,
+    one int8 code write."""
+    return float(frames * rows * spec.in_dim * 2 + spec.out_dim * spec.in_dim * 2 +
+                 spec.out_dim * spec.in_dim)
+
+
+class CalibrationShard:
+    """Device-resident calibration inputs of this rank's layers and the K3 -> K5 -> K4 unit.
+
+    ``setup()`` materialises W (bf16) and the per-frame activations X (bf16,
+    frames x rows tokens) with the counter-based generator, keyed only by
+    (seed, layer), so every rank produces the same data for a layer whatever
+    the world size.  ``run()`` is the timed calibration step."""
+
+    def __init__(self, specs, layer_ids, frames: int = 21, rows: int = 1560, seed: int = 1,
+                 frame_weights=None, device="cuda"):
+        self.specs = [specs[i] for i in layer_ids]
+        self.ids = list(layer_ids)
+        self.frames, self.rows, self.seed = frames, rows, seed
+        self.weights = frame_weights
+        self.device = device
+        self.w, self.x = [], []
+
+    def setup(self):
+        from . import synth
+        for spec in self.specs:
+            self.w.append(synth.synth_weight(spec, seed=self.seed, device=self.device))
+            # cross-attn k/v see the 512 text tokens, identical for every frame
+            rows = self.rows if spec.tokens != synth.WAN_TEXT_LEN else synth.WAN_TEXT_LEN
+            x = torch.empty((self.frames * rows, spec.in_dim), dtype=torch.bfloat16,
+                            device=self.device)
+            for f in range(self.frames):
+                synth.synth_activation(rows, spec.in_dim, seed=synth.mix_seed(self.seed, spec.index),
+                                       frame=f, device=self.device, out=x[f * rows:(f + 1) * rows])
+            self.x.append(x)
+        torch.cuda.synchronize()
+
+    def bytes(self) -> float:
+        return float(sum(x.numel() * 2 for x in self.x) + sum(w.numel() * 3 for w in self.w))
+
+    def run(self) -> List[LayerRecord]:
+        from . import engine, outlier
+        if not self.specs:
+            return []
+        # K3: batched outlier detection (one launch pair per weight dtype group)
+        dev_rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w)
+        # K4 over every layer's frames (independent of K3/K5; same stream)
+        groups = {}
+        for i, x in enumerate(self.x):
+            groups.setdefault(x.shape[0] // self.frames, []).append(i)
+        search = {}
+        for rows, idx in groups.items():
+            res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights)
+            for j, i in enumerate(idx):
+                search[i] = res[j]
+        reps = outlier.collect_reports(dev_rep)  # host sync: plans need the index sets
+        layers = []
+        for spec, w, rep in zip(self.specs, self.w, reps):
+            plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+            layers.append(engine.prepare_weights(spec.name, w, plan, check_finite=False))  # K5
+        out = []
+        for i, (spec, L, rep) in enumerate(zip(self.specs, layers, reps)):
+            r = search[i].cpu().numpy()
+            nc = len(PERCENTILES)
+            out.append(LayerRecord(spec.index, len(rep.aligned_outliers), rep.aligned_outliers,
+                                   float(r[3 * nc + 1]), int(r[3 * nc]), r[2 * nc:3 * nc].copy(),
+                                   L.scale_outlier64.cpu().numpy(), L.scale_normal64.cpu().numpy()))
+        self.layers = layers
+        return out

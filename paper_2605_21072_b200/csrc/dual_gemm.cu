@@ -37,8 +37,8 @@ template <int BN, int CG>
 struct GemmCfg {
   static constexpr int kABytes = BM * BK;
   static constexpr int kBBytes = (BN / CG) * BK;
-  static constexpr int kEpiBytes = 1024 /*align*/ + 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales*/ +
-                                   kEpiWarps * 2048 /*y staging*/;
+  static constexpr int kEpiBytes = 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales, 2 buffers*/ +
+                                   kEpiWarps * 4096 /*y staging, 2 buffers per warp*/;
   static constexpr int kStages = (227 * 1024 - kEpiBytes) / (kABytes + kBBytes) > 8
                                      ? 8
                                      : (227 * 1024 - kEpiBytes) / (kABytes + kBBytes);
@@ -65,11 +65,107 @@ struct GemmParams {
   const double* so64;
   const double* sn64;
   int use_tma_store;  // bf16 output through the TMA store path
+  int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
 };
 
-__device__ __forceinline__ float gelu_erf(float v) {
-  return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+// ---- packed fp32x2 helpers (sm_100a FFMA2 / FMUL2: one instruction per element pair,
+// each lane rounded exactly like the scalar fma.rn / mul.rn) -------------------------
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// gelu(v) = 0.5 v (1 + erf(v/sqrt 2)) on a pair (toy_model.cpp:62-66 uses the erf form).
+// erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the bf16 output
+// resolution): t = 1/(1 + p|z|), erf = 1 - t*P(t)*exp(-z^2).  One rcp + one ex2 per
+// element, the polynomial on packed FMAs; erff's two-range coefficient selection cost
+// more than the whole dequant epilogue.
+__device__ __forceinline__ uint64_t gelu2(uint64_t v) {
+  const uint64_t h = mul2(v, pk2(0.5f, 0.5f));
+  const uint64_t z = mul2(v, pk2(0.70710678118654752f, 0.70710678118654752f));
+  float z0, z1;
+  upk2(z, z0, z1);
+  const uint64_t a = pk2(fabsf(z0), fabsf(z1));
+  float d0, d1;
+  upk2(fma2(pk2(0.3275911f, 0.3275911f), a, pk2(1.0f, 1.0f)), d0, d1);
+  const uint64_t t = pk2(rcp_approx(d0), rcp_approx(d1));
+  // negated coefficients: q = -(t * P(t))
+  uint64_t q = fma2(pk2(-1.061405429f, -1.061405429f), t, pk2(1.453152027f, 1.453152027f));
+  q = fma2(q, t, pk2(-1.421413741f, -1.421413741f));
+  q = fma2(q, t, pk2(0.284496736f, 0.284496736f));
+  q = fma2(q, t, pk2(-0.254829592f, -0.254829592f));
+  q = mul2(q, t);
+  float s0, s1;
+  upk2(mul2(mul2(a, pk2(-1.4426950408889634f, -1.4426950408889634f)), a), s0, s1);
+  float r0, r1;
+  upk2(fma2(q, pk2(ex2_approx(s0), ex2_approx(s1)), pk2(1.0f, 1.0f)), r0, r1);
+  const uint64_t erfv = pk2(copysignf(r0, z0), copysignf(r1, z1));
+  return fma2(h, erfv, h);
+}
+
+// y = s_x * (s_wo*acc_o + s_wn*acc_n) (+ bias) [gelu], written back into rn as float bits.
+// Same per-element op order as the scalar form (oracle_epilogue_f32), on packed pairs;
+// specialised on (outlier slab?, bias?, gelu?) so every variant is straight-line code.
+template <bool HO, bool HB, bool GL>
+__device__ __forceinline__ void epi_math(uint32_t (&rn)[32], const uint32_t (&ro)[32],
+                                         const float* scc, int bn, float sx) {
+  const uint64_t sx2 = pk2(sx, sx);
+#pragma unroll
+  for (int e4 = 0; e4 < 8; ++e4) {
+    const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
+    float4 so4 = sn4, sb4 = sn4;
+    if (HO) so4 = reinterpret_cast<const float4*>(scc + bn)[e4];
+    if (HB) sb4 = reinterpret_cast<const float4*>(scc + 2 * bn)[e4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 4 * e4 + 2 * h;
+      const uint64_t sn = h ? pk2(sn4.z, sn4.w) : pk2(sn4.x, sn4.y);
+      const uint64_t an = pk2(__int2float_rn(static_cast<int>(rn[e])),
+                              __int2float_rn(static_cast<int>(rn[e + 1])));
+      uint64_t t;
+      if (HO) {
+        const uint64_t so = h ? pk2(so4.z, so4.w) : pk2(so4.x, so4.y);
+        const uint64_t ao = pk2(__int2float_rn(static_cast<int>(ro[e])),
+                                __int2float_rn(static_cast<int>(ro[e + 1])));
+        t = fma2(sn, an, mul2(so, ao));
+      } else {
+        t = mul2(sn, an);
+      }
+      uint64_t v;
+      if (HB) v = fma2(sx2, t, h ? pk2(sb4.z, sb4.w) : pk2(sb4.x, sb4.y));
+      else v = mul2(sx2, t);
+      if (GL) v = gelu2(v);
+      float y0, y1;
+      upk2(v, y0, y1);
+      rn[e] = __float_as_uint(y0);
+      rn[e + 1] = __float_as_uint(y1);
+    }
+  }
 }
 
 template <int BN, int CG>
@@ -79,13 +175,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
   using C = GemmCfg<BN, CG>;
   constexpr int TM = BM * CG;  // rows of the (pair) tile
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-B alignment (128B swizzle atoms) comes from the declaration, not from pointer
+  // rounding: integer rounding would hide the shared address space (generic LD/ST).
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
   uint8_t* epi_ystage = sB + C::kStages * C::kBBytes;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 2048);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 4096);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccStages;
@@ -164,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
+        const long long tr0 = clock64();
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        const long long tr1 = clock64();
         ptx::tc_fence_after();
         const uint32_t d_o = tmem_base + static_cast<uint32_t>(acc * 2 * BN);
         const uint32_t d_n = d_o + BN;
@@ -194,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (CG == 1) ptx::mma_commit(&tfull[acc]);
         else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+        if (p.trace && blockIdx.x == 0)
+          printf("MMA tile %d: wait_tempty %lld issue %lld (t=%lld)\n", t, tr1 - tr0, clock64() - tr1, tr0);
         if (++acc == C::kAccStages) {
           acc = 0;
           acc_phase ^= 1;
@@ -212,26 +313,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int etid = ew * 32 + lane;
     const int row_in_tile = q * 32 + lane;
     const bool has_outlier = p.k_o > 0;
-    uint8_t* ystage = epi_ystage + ew * 2048;  // 32 rows x 64 B, SWIZZLE_64B layout
+    const int epi_mode = (has_outlier ? 1 : 0) | (p.bias ? 2 : 0) | ((p.epilogue & QARVD_EPI_GELU) ? 4 : 0);
+    uint8_t* ystage0 = epi_ystage + ew * 4096;  // 2 x (32 rows x 64 B, SWIZZLE_64B layout)
+    int ybuf = 0, sbuf = 0;
+    // scales of the next tile are loaded into registers one tile ahead, so the global
+    // load latency hides behind the current tile's epilogue
+    float pf_n = 0.f, pf_o = 0.f, pf_b = 0.f, pf_x = 0.f;
+    auto prefetch = [&](int tt) {
+      if (tt >= p.num_tiles || p.out_dtype == QARVD_F64) return;
+      if (etid < BN) {
+        const int64_t j = static_cast<int64_t>(tt / p.num_m_blks) * BN + etid;
+        const int64_t jc = j < p.n ? j : p.n - 1;
+        pf_n = __ldg(p.scale_wn + jc);
+        if (has_outlier) pf_o = __ldg(p.scale_wo + jc);
+        if (p.bias) pf_b = __ldg(p.bias + jc);
+      }
+      const int64_t r = static_cast<int64_t>(tt % p.num_m_blks) * TM + rank * BM + q * 32 + lane;
+      pf_x = (r < p.m && p.scale_x) ? __ldg(p.scale_x + r) : 0.f;
+    };
+    prefetch(cta_id);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
       const int m_blk = t % p.num_m_blks;
       const int n_blk = t / p.num_m_blks;
-      float* sc = epi_scales + acc * 3 * BN;
-      if (p.out_dtype != QARVD_F64 && etid < BN) {
-        const int64_t j = static_cast<int64_t>(n_blk) * BN + etid;
-        const int64_t jc = j < p.n ? j : p.n - 1;
-        sc[etid] = __ldg(p.scale_wn + jc);
-        sc[BN + etid] = has_outlier ? __ldg(p.scale_wo + jc) : 0.f;
-        sc[2 * BN + etid] = p.bias ? __ldg(p.bias + jc) : 0.f;
+      float* sc = epi_scales + sbuf * 3 * BN;
+      if (etid < BN) {
+        sc[etid] = pf_n;
+        sc[BN + etid] = pf_o;
+        sc[2 * BN + etid] = pf_b;
       }
+      const float sx = pf_x;
+      prefetch(t + num_ctas);
+      sbuf ^= 1;
       const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM + q * 32;
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.m;
-      const float sx = (row_ok && p.scale_x) ? __ldg(p.scale_x + row) : 0.f;
       asm volatile("bar.sync 1, 256;" ::: "memory");  // scales visible to all epilogue warps
+      const long long te0 = clock64();
       ptx::mbar_wait(&tfull[acc], acc_phase);
+      const long long te1 = clock64();
       ptx::tc_fence_after();
       const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
       const uint32_t t_o = tmem_base + t_lane + static_cast<uint32_t>(acc * 2 * BN);
@@ -274,28 +395,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               p.acc_o_dbg[row * p.n + col0 + e] = has_outlier ? static_cast<int32_t>(ro[e]) : 0;
           }
         }
-        // y overwrites rn (as float bits): t = s_wo*acc_o; t = fmaf(s_wn, acc_n, t); y = s_x*t (+bias)
-        const float* scc = sc + c * 32;
-#pragma unroll
-        for (int e4 = 0; e4 < 8; ++e4) {
-          const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
-          const float4 so4 = reinterpret_cast<const float4*>(scc + BN)[e4];
-          const float4 sb4 = reinterpret_cast<const float4*>(scc + 2 * BN)[e4];
-          const float sn[4] = {sn4.x, sn4.y, sn4.z, sn4.w};
-          const float so[4] = {so4.x, so4.y, so4.z, so4.w};
-          const float sb[4] = {sb4.x, sb4.y, sb4.z, sb4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = 4 * e4 + u;
-            const float an = __int2float_rn(static_cast<int>(rn[e]));
-            float tacc;
-            if (has_outlier)
-              tacc = __fmaf_rn(sn[u], an, __fmul_rn(so[u], __int2float_rn(static_cast<int>(ro[e]))));
-            else
-              tacc = __fmul_rn(sn[u], an);
-            float v = p.bias ? __fmaf_rn(sx, tacc, sb[u]) : __fmul_rn(sx, tacc);
-            if (p.epilogue & QARVD_EPI_GELU) v = gelu_erf(v);
-            rn[e] = __float_as_uint(v);
+        {
+          const float* scc = sc + c * 32;
+          switch (epi_mode) {
+            case 0: epi_math<false, false, false>(rn, ro, scc, BN, sx); break;
+            case 1: epi_math<true, false, false>(rn, ro, scc, BN, sx); break;
+            case 2: epi_math<false, true, false>(rn, ro, scc, BN, sx); break;
+            case 3: epi_math<true, true, false>(rn, ro, scc, BN, sx); break;
+            case 4: epi_math<false, false, true>(rn, ro, scc, BN, sx); break;
+            case 5: epi_math<true, false, true>(rn, ro, scc, BN, sx); break;
+            case 6: epi_math<false, true, true>(rn, ro, scc, BN, sx); break;
+            default: epi_math<true, true, true>(rn, ro, scc, BN, sx); break;
           }
         }
         if (p.use_tma_store) {
@@ -306,7 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
             pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
           }
-          if (lane == 0) ptx::bulk_wait_read0();  // previous store has finished reading ystage
+          uint8_t* ystage = ystage0 + ybuf * 2048;
+          ybuf ^= 1;
+          if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -340,6 +452,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.trace && blockIdx.x == 0 && lane == 0 && (warp == 4 || warp == 11))
+        printf("EPI w%d tile %d: wait_tfull %lld body %lld (t=%lld)\n", warp, t, te1 - te0,
+               clock64() - te1, te0);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -473,29 +588,34 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   return QARVD_OK;
 }
 
-// CTA-group choice: QARVD_GEMM_CG=1|2 overrides (default 2: SM pairs).
-int choose_cg() {
-  if (const char* env = getenv("QARVD_GEMM_CG")) {
-    const int v = atoi(env);
-    if (v == 1 || v == 2) return v;
+// Tile configuration (BN, CG).  QARVD_GEMM_BN=128|192|256 and QARVD_GEMM_CG=1|2 override.
+// * BN = 256 halves the B traffic per MAC versus 128 but fits only one TMEM stage
+//   (2 accumulators x 256 columns), so its epilogue does not overlap the next tile.
+// * BN = 192 exists for N = 1536 (Wan qkv / ffn.2 outputs): 37 x 8 = 296 single-SM tiles
+//   at M = 4680 is exactly two waves on 148 SMs (BN = 256 gives 1.5 waves).
+struct TileCfg {
+  int bn, cg;
+};
+TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
+  (void)k;
+  TileCfg c{256, 2};
+  const int64_t sms = sm_count();
+  if (n % 192 == 0 && n <= 2048) {
+    const int64_t t192 = ((m + BM - 1) / BM) * (n / 192);
+    const int64_t t256 = ((m + 2 * BM - 1) / (2 * BM)) * ((n + 255) / 256);
+    const double eff192 = static_cast<double>(t192) / (((t192 + sms - 1) / sms) * sms);
+    const double eff256 = static_cast<double>(t256) / (((t256 + sms / 2 - 1) / (sms / 2)) * (sms / 2));
+    if (eff192 > eff256) c = TileCfg{192, 1};
   }
-  return 2;
-}
-
-// Tile-width choice (QARVD_GEMM_BN=128|256 overrides).
-int choose_bn(int64_t m, int64_t n, int64_t k) {
   if (const char* env = getenv("QARVD_GEMM_BN")) {
     const int v = atoi(env);
-    if (v == 128 || v == 256) return v;
+    if (v == 128 || v == 192 || v == 256) c.bn = v;
   }
-  // BN = 256 halves the B-operand traffic per MAC but leaves room for only one
-  // TMEM accumulator stage (2 accumulators x 256 columns), so its epilogue does
-  // not overlap the next tile's MMAs.  That pays off only when the mainloop is
-  // long compared with the epilogue (large K); measured on B200 at the Wan
-  // shapes: K=1536 -> BN=128 faster, K=8960 -> BN=256 faster.
-  (void)m;
-  (void)n;
-  return k >= 4096 ? 256 : 128;
+  if (const char* env = getenv("QARVD_GEMM_CG")) {
+    const int v = atoi(env);
+    if (v == 1 || v == 2) c.cg = v;
+  }
+  return c;
 }
 
 }  // namespace
@@ -523,14 +643,18 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.acc_o_dbg = acc_o;
   p.acc_n_dbg = acc_n;
   p.debug = getenv("QARVD_GEMM_DEBUG") ? atoi(getenv("QARVD_GEMM_DEBUG")) : 0;
+  p.trace = getenv("QARVD_GEMM_TRACE") ? 1 : 0;
   p.epilogue = epilogue;
   p.out_dtype = out_dtype;
-  const int bn = choose_bn(m, n, k);
-  if (choose_cg() == 2)
-    return bn == 256 ? launch_gemm<256, 2>(xq, ldq, wq, ldw, p, stream)
-                     : launch_gemm<128, 2>(xq, ldq, wq, ldw, p, stream);
-  return bn == 256 ? launch_gemm<256, 1>(xq, ldq, wq, ldw, p, stream)
-                   : launch_gemm<128, 1>(xq, ldq, wq, ldw, p, stream);
+  const TileCfg c = choose_cfg(m, n, k);
+  if (c.cg == 2) {
+    if (c.bn == 256) return launch_gemm<256, 2>(xq, ldq, wq, ldw, p, stream);
+    if (c.bn == 192) return launch_gemm<192, 2>(xq, ldq, wq, ldw, p, stream);
+    return launch_gemm<128, 2>(xq, ldq, wq, ldw, p, stream);
+  }
+  if (c.bn == 256) return launch_gemm<256, 1>(xq, ldq, wq, ldw, p, stream);
+  if (c.bn == 192) return launch_gemm<192, 1>(xq, ldq, wq, ldw, p, stream);
+  return launch_gemm<128, 1>(xq, ldq, wq, ldw, p, stream);
 }
 
 }  // namespace qarvd_b200
