@@ -27,18 +27,25 @@ namespace qarvd_b200 {
 namespace {
 
 constexpr int BM = 128;  // rows of the activation tile (one TMEM lane per row)
-constexpr int BK = 128;  // bytes (= int8 elements) of K per pipeline stage: one swizzle row
+constexpr int BK = 128;  // bytes (= int8 elements) of K per 128B-swizzle sub-tile (one TMA box)
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
 
 // BN = output columns of the (pair) tile; CG = CTAs per MMA (1, or 2 = an SM pair
 // computing a 256-row tile, each CTA holding its 128 A rows and BN/2 B rows).
-template <int BN, int CG>
+// KS = 128-byte K sub-tiles per pipeline stage.  Every stage costs the MMA issuer one
+// mbarrier wait (~110-250 clk that the tensor pipe does not overlap, measured by
+// scripts/mma_rate2.cu), so KS = 2 (8 MMAs per wait) halves that overhead per MAC.
+template <int BN, int CG, int KS>
 struct GemmCfg {
-  static constexpr int kABytes = BM * BK;
-  static constexpr int kBBytes = (BN / CG) * BK;
+  static constexpr int kASub = BM * BK;           // one 128 B K sub-tile of A
+  static constexpr int kBSub = (BN / CG) * BK;    // one 128 B K sub-tile of this CTA's B
+  static constexpr int kABytes = KS * kASub;
+  static constexpr int kBBytes = KS * kBSub;
+  // y staging: 2 KB per epilogue warp, double-buffered unless the operand stages need the room
+  static constexpr int kYBufs = KS == 2 ? 1 : 2;
   static constexpr int kEpiBytes = 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales, 2 buffers*/ +
-                                   kEpiWarps * 4096 /*y staging, 2 buffers per warp*/;
+                                   kEpiWarps * 2048 * kYBufs /*y staging*/;
   static constexpr int kStages = (227 * 1024 - kEpiBytes) / (kABytes + kBBytes) > 8
                                      ? 8
                                      : (227 * 1024 - kEpiBytes) / (kABytes + kBBytes);
@@ -168,13 +175,14 @@ __device__ __forceinline__ void epi_math(uint32_t (&rn)[32], const uint32_t (&ro
   }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int KS>
 __global__ void __launch_bounds__(kThreads, 1)
     dual_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, KS>;
   constexpr int TM = BM * CG;  // rows of the (pair) tile
+  constexpr int SK = BK * KS;  // K bytes per stage
   // 1024-B alignment (128B swizzle atoms) comes from the declaration, not from pointer
   // rounding: integer rounding would hide the shared address space (generic LD/ST).
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -182,15 +190,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
   uint8_t* epi_ystage = sB + C::kStages * C::kBBytes;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 4096);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 2048 * C::kYBufs);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
+  uint64_t* tofree = tempty + C::kAccStages;  // acc_o released (one-stage TMEM only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tofree + 1);
   float* epi_scales = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  __shared__ long long s_trace[5][32];  // QARVD_GEMM_TRACE: per-tile clocks of CTA 0
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int cta_id = static_cast<int>(blockIdx.x) / CG;  // pair index
@@ -208,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], kEpiWarps * CG);  // one arrive per epilogue warp of the pair
     }
+    ptx::mbar_init(tofree, kEpiWarps * CG);
     ptx::fence_mbar_init();
   }
   if (warp == 2) {
@@ -220,81 +231,137 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_kb = static_cast<int>((p.k + BK - 1) / BK);
+  const int num_kb = static_cast<int>((p.k + SK - 1) / SK);
+  // one-stage TMEM: k-blocks holding outlier steps are issued last (see the MMA issuer)
+  auto kblock_rotation = [&](int ko32_, int nkb) {
+    if (C::kAccStages != 1) return 0;
+    const int r = (ko32_ + SK / 32 - 1) / (SK / 32);
+    return (r > 0 && r < nkb) ? r : 0;
+  };
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
-        const int m_blk = t % p.num_m_blks;
-        const int n_blk = t / p.num_m_blks;
-        const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
-        const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+    // ===================== TMA producer (whole warp loops, lane 0 issues) ==============
+    int stage = 0;
+    uint32_t phase = 0;
+    const int rot = kblock_rotation(static_cast<int>(p.k_o / 32), num_kb);  // = the MMA issuer's
+    for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
+      const int m_blk = t % p.num_m_blks;
+      const int n_blk = t / p.num_m_blks;
+      const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
+      const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
+      for (int i = 0; i < num_kb; ++i) {
+        const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
           if (p.debug == 2) {
             if (leader) ptx::mbar_arrive(&full[stage]);
           } else if (CG == 1) {
             ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
-            ptx::tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, a_row);
-            ptx::tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, b_row);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              ptx::tma_load_2d(sA + stage * C::kABytes + ks * C::kASub, &tmA, &full[stage],
+                               kb * SK + ks * BK, a_row);
+              ptx::tma_load_2d(sB + stage * C::kBBytes + ks * C::kBSub, &tmB, &full[stage],
+                               kb * SK + ks * BK, b_row);
+            }
           } else {
             if (leader) ptx::mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
-            ptx::tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, a_row);
-            ptx::tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, b_row);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              ptx::tma_load_2d_2sm(sA + stage * C::kABytes + ks * C::kASub, &tmA, &full[stage],
+                                   kb * SK + ks * BK, a_row);
+              ptx::tma_load_2d_2sm(sB + stage * C::kBBytes + ks * C::kBSub, &tmB, &full[stage],
+                                   kb * SK + ks * BK, b_row);
+            }
           }
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0 && leader) {
+    // ===================== MMA issuer =====================
+    // The whole warp runs the (warp-uniform) loop so descriptors, accumulator addresses
+    // and slab routing live in uniform registers; lane 0 issues.
+    //
+    // TMEM: with two accumulator stages (BN <= 128) tile t+1 uses the other stage.  With
+    // one stage (BN >= 192: acc_o + acc_n fill the 512 columns) the k-blocks holding
+    // outlier steps run LAST, and the epilogue releases the accumulators in two steps:
+    // acc_n as soon as it has folded s_wn*acc_n + s_wo*acc_o into acc_o's columns, acc_o
+    // after the stores.  The next tile's acc_n MMAs wait only for the first step.
+    if (leader) {
       constexpr uint32_t idesc = ptx::idesc_i8(TM, BN);
+      const uint64_t a_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sA));
+      const uint64_t b_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sB));
+      const int k32 = static_cast<int>(p.k / 32), ko32 = static_cast<int>(p.k_o / 32);
+      constexpr int SPB = SK / 32;  // K=32 steps per k-block
+      // k-block rotation (outlier k-blocks last) and the first acc_n step in issue order
+      const int rot = kblock_rotation(ko32, num_kb);
+      const int first_n = rot > 0 ? rot * SPB : ko32;
+      const int kb_first_n = first_n / SPB;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
         const long long tr0 = clock64();
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (C::kAccStages == 2) ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         const long long tr1 = clock64();
         ptx::tc_fence_after();
         const uint32_t d_o = tmem_base + static_cast<uint32_t>(acc * 2 * BN);
         const uint32_t d_n = d_o + BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int i = 0; i < num_kb; ++i) {
+          const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
+          if (C::kAccStages == 1) {
+            if (kb == kb_first_n) ptx::mbar_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
+            if (ko32 > 0 && kb == 0) ptx::mbar_wait(&tofree[0], acc_phase ^ 1);  // acc_o free
+            ptx::tc_fence_after();
+          }
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t a_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(sA + stage * C::kABytes));
-          const uint64_t b_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(sB + stage * C::kBBytes));
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (C::kABytes >> 4));
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (C::kBBytes >> 4));
+          if (lane == 0 && p.debug != 1) {
 #pragma unroll
-          for (int j = 0; j < BK / 32; ++j) {
-            const int64_t kk = static_cast<int64_t>(kb) * BK + j * 32;
-            if (kk >= p.k || p.debug == 1) break;
-            const bool outl = kk < p.k_o;
-            const uint32_t accumulate = (kk == 0 || kk == p.k_o) ? 0u : 1u;
-            // +32 bytes along K inside the 128B swizzle row = +2 in the >>4 address field
-            if (CG == 1)
-              ptx::mma_i8(outl ? d_o : d_n, a_desc + 2 * j, b_desc + 2 * j, idesc, accumulate);
-            else
-              ptx::mma_i8_2sm(outl ? d_o : d_n, a_desc + 2 * j, b_desc + 2 * j, idesc, accumulate);
+            for (int j = 0; j < SPB; ++j) {
+              const int s32 = kb * SPB + j;  // K=32 step index
+              if (s32 < k32) {
+                const bool outl = s32 < ko32;
+                const uint32_t d = outl ? d_o : d_n;
+                const uint32_t accumulate = (outl ? s32 == 0 : s32 == first_n) ? 0u : 1u;
+                // sub-tile j/4; +32 bytes along K inside the 128B swizzle row = +2 in the
+                // >>4 address field
+                const uint64_t ao = static_cast<uint64_t>((j >> 2) * (C::kASub >> 4) + 2 * (j & 3));
+                const uint64_t bo = static_cast<uint64_t>((j >> 2) * (C::kBSub >> 4) + 2 * (j & 3));
+                if (CG == 1) ptx::mma_i8(d, ad + ao, bd + bo, idesc, accumulate);
+                else ptx::mma_i8_2sm(d, ad + ao, bd + bo, idesc, accumulate);
+              }
+            }
           }
-          if (CG == 1) ptx::mma_commit(&empty[stage]);
-          else ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 1) ptx::mma_commit(&empty[stage]);
+            else ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 1) ptx::mma_commit(&tfull[acc]);
-        else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
-        if (p.trace && blockIdx.x == 0)
-          printf("MMA tile %d: wait_tempty %lld issue %lld (t=%lld)\n", t, tr1 - tr0, clock64() - tr1, tr0);
+        if (lane == 0) {
+          if (CG == 1) ptx::mma_commit(&tfull[acc]);
+          else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+          const int ti = (t - cta_id) / num_ctas;
+          if (p.trace && blockIdx.x == 0 && ti < 32) {
+            s_trace[0][ti] = tr0;
+            s_trace[1][ti] = clock64();
+          }
+        }
+        __syncwarp();
         if (++acc == C::kAccStages) {
           acc = 0;
           acc_phase ^= 1;
@@ -305,19 +372,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue: 8 warps, 2 per TMEM lane quadrant =====================
     // Warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quadrant split
     // the tile's 32-column chunks (even / odd).  Each tile's column scales are prefetched
-    // into shared memory before the accumulator is ready (the loads overlap the MMAs);
-    // bf16 results go through a 64B-swizzled staging tile and a TMA bulk tensor store.
+    // one tile ahead; bf16 results go through a 64B-swizzled staging tile and a TMA bulk
+    // tensor store.
     const int ew = warp - 4;
     const int q = warp & 3;
     const int half = ew >> 2;
     const int etid = ew * 32 + lane;
-    const int row_in_tile = q * 32 + lane;
     const bool has_outlier = p.k_o > 0;
-    const int epi_mode = (has_outlier ? 1 : 0) | (p.bias ? 2 : 0) | ((p.epilogue & QARVD_EPI_GELU) ? 4 : 0);
-    uint8_t* ystage0 = epi_ystage + ew * 4096;  // 2 x (32 rows x 64 B, SWIZZLE_64B layout)
+    const bool gelu = (p.epilogue & QARVD_EPI_GELU) != 0;
+    // two-step release (see the MMA issuer) for bf16/f32 outputs without debug dumps
+    const bool two_step = C::kAccStages == 1 && p.out_dtype != QARVD_F64 && !p.acc_n_dbg &&
+                          !p.acc_o_dbg;
+    const int epi_mode = (has_outlier ? 1 : 0) | (p.bias ? 2 : 0) | (gelu && !two_step ? 4 : 0);
+    uint8_t* ystage0 = epi_ystage + ew * 2048 * C::kYBufs;  // kYBufs x (32 rows x 64 B, SWIZZLE_64B)
     int ybuf = 0, sbuf = 0;
-    // scales of the next tile are loaded into registers one tile ahead, so the global
-    // load latency hides behind the current tile's epilogue
     float pf_n = 0.f, pf_o = 0.f, pf_b = 0.f, pf_x = 0.f;
     auto prefetch = [&](int tt) {
       if (tt >= p.num_tiles || p.out_dtype == QARVD_F64) return;
@@ -330,6 +398,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int64_t r = static_cast<int64_t>(tt % p.num_m_blks) * TM + rank * BM + q * 32 + lane;
       pf_x = (r < p.m && p.scale_x) ? __ldg(p.scale_x + r) : 0.f;
+    };
+    auto release = [&](uint64_t* bar) {
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 1) ptx::mbar_arrive(bar);
+        else ptx::mbar_arrive_leader(bar);
+      }
+    };
+    // y (fp32 bits in rn) -> bf16 TMA store, or direct bf16 / f32 stores
+    auto store_chunk = [&](uint32_t (&rn)[32], int64_t row0, int64_t row, int64_t col0, int ncols) {
+      if (p.use_tma_store) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const __nv_bfloat162 h2 =
+              __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
+          pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        uint8_t* ystage = ystage0 + ybuf * 2048;
+        if (C::kYBufs == 2) {
+          ybuf ^= 1;
+          if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
+        } else if (lane == 0) {
+          ptx::bulk_wait_read0();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int phys = (i ^ ((lane >> 1) & 3)) << 4;
+          *reinterpret_cast<uint4*>(ystage + lane * 64 + phys) =
+              make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && row0 < p.m) {
+          ptx::tma_store_2d(&tmY, ystage, static_cast<int32_t>(col0), static_cast<int32_t>(row0));
+          ptx::bulk_commit();
+        }
+      } else if (row < p.m && p.out_dtype == QARVD_BF16) {
+        __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
+      } else if (row < p.m) {
+        float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
+        if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
+          float4* dst = reinterpret_cast<float4*>(yr);
+#pragma unroll
+          for (int v4 = 0; v4 < 8; ++v4)
+            dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
+                                  __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < ncols) yr[e] = __uint_as_float(rn[e]);
+        }
+      }
     };
     prefetch(cta_id);
     int acc = 0;
@@ -408,58 +534,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             default: epi_math<true, true, true>(rn, ro, scc, BN, sx); break;
           }
         }
-        if (p.use_tma_store) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const __nv_bfloat162 h2 =
-                __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
-            pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
-          uint8_t* ystage = ystage0 + ybuf * 2048;
-          ybuf ^= 1;
-          if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int phys = (i ^ ((lane >> 1) & 3)) << 4;
-            *reinterpret_cast<uint4*>(ystage + lane * 64 + phys) =
-                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-          }
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && row0 < p.m) {
-            ptx::tma_store_2d(&tmY, ystage, static_cast<int32_t>(col0), static_cast<int32_t>(row0));
-            ptx::bulk_commit();
-          }
-        } else if (row_ok && p.out_dtype == QARVD_BF16) {
-          __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
-        } else if (row_ok) {
-          float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
-          if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
-            float4* dst = reinterpret_cast<float4*>(yr);
-#pragma unroll
-            for (int v4 = 0; v4 < 8; ++v4)
-              dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
-                                    __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (e < ncols) yr[e] = __uint_as_float(rn[e]);
-          }
-        }
+        if (two_step) ptx::tmem_st32(t_o + c * 32, rn);  // fold y into acc_o's columns
+        else store_chunk(rn, row0, row, col0, ncols);
       }
-      if (p.trace && blockIdx.x == 0 && lane == 0 && (warp == 4 || warp == 11))
-        printf("EPI w%d tile %d: wait_tfull %lld body %lld (t=%lld)\n", warp, t, te1 - te0,
-               clock64() - te1, te0);
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 1) ptx::mbar_arrive(&tempty[acc]);
-        else ptx::mbar_arrive_leader(&tempty[acc]);
+      if (two_step) {
+        ptx::tmem_wait_st();
+        release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += 2) {
+          const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+          if (col0 >= p.n) break;
+          const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
+          uint32_t rn[32];
+          ptx::tmem_ld32(t_o + c * 32, rn);
+          ptx::tmem_wait_ld();
+          if (gelu) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float y0, y1;
+              upk2(gelu2(pk2(__uint_as_float(rn[e]), __uint_as_float(rn[e + 1]))), y0, y1);
+              rn[e] = __float_as_uint(y0);
+              rn[e + 1] = __float_as_uint(y1);
+            }
+          }
+          store_chunk(rn, row0, row, col0, ncols);
+        }
+        release(&tofree[0]);  // acc_o free
+      } else {
+        release(&tempty[acc]);
+        if (C::kAccStages == 1) release(&tofree[0]);
+      }
+      {
+        const int ti = (t - cta_id) / num_ctas;
+        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4 && ti < 32) {
+          s_trace[2][ti] = te0;
+          s_trace[3][ti] = te1;
+          s_trace[4][ti] = clock64();
+        }
       }
       if (++acc == C::kAccStages) {
         acc = 0;
@@ -471,6 +582,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int nt = (p.num_tiles - cta_id + num_ctas - 1) / num_ctas;
+    const long long t0 = s_trace[0][0];
+    for (int i = 0; i < nt && i < 32; ++i)
+      printf("tile %2d: mma %7lld..%7lld  epi wait %7lld tfull %7lld done %7lld\n", i,
+             s_trace[0][i] - t0, s_trace[1][i] - t0, s_trace[2][i] - t0, s_trace[3][i] - t0,
+             s_trace[4][i] - t0);
+  }
   if (CG == 2) ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
     ptx::tc_fence_after();
@@ -540,14 +659,14 @@ int sm_count() {
   return count;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int KS>
 int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, GemmParams p,
                 cudaStream_t stream) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, KS>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(dual_gemm_kernel<BN, CG>,
+    attr_err = cudaFuncSetAttribute(dual_gemm_kernel<BN, CG, KS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(C::kSmemBytes));
   });
@@ -582,7 +701,7 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  QARVD_CUDA_TRY(cudaLaunchKernelEx(&cfg, dual_gemm_kernel<BN, CG>, ta, tb, ty, p));
+  QARVD_CUDA_TRY(cudaLaunchKernelEx(&cfg, dual_gemm_kernel<BN, CG, KS>, ta, tb, ty, p));
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;
@@ -594,18 +713,18 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
 // * BN = 192 exists for N = 1536 (Wan qkv / ffn.2 outputs): 37 x 8 = 296 single-SM tiles
 //   at M = 4680 is exactly two waves on 148 SMs (BN = 256 gives 1.5 waves).
 struct TileCfg {
-  int bn, cg;
+  int bn, cg, ks;
 };
 TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
   (void)k;
-  TileCfg c{256, 2};
+  TileCfg c{256, 2, 2};
   const int64_t sms = sm_count();
   if (n % 192 == 0 && n <= 2048) {
     const int64_t t192 = ((m + BM - 1) / BM) * (n / 192);
     const int64_t t256 = ((m + 2 * BM - 1) / (2 * BM)) * ((n + 255) / 256);
     const double eff192 = static_cast<double>(t192) / (((t192 + sms - 1) / sms) * sms);
     const double eff256 = static_cast<double>(t256) / (((t256 + sms / 2 - 1) / (sms / 2)) * (sms / 2));
-    if (eff192 > eff256) c = TileCfg{192, 1};
+    if (eff192 > eff256) c = TileCfg{192, 1, 1};
   }
   if (const char* env = getenv("QARVD_GEMM_BN")) {
     const int v = atoi(env);
@@ -615,6 +734,11 @@ TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
     const int v = atoi(env);
     if (v == 1 || v == 2) c.cg = v;
   }
+  if (const char* env = getenv("QARVD_GEMM_KS")) {
+    const int v = atoi(env);
+    if (v == 1 || v == 2) c.ks = v;
+  }
+  if (c.bn == 192) c.ks = 1;  // 80 KB stages would leave two stages only
   return c;
 }
 
@@ -648,13 +772,17 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.out_dtype = out_dtype;
   const TileCfg c = choose_cfg(m, n, k);
   if (c.cg == 2) {
-    if (c.bn == 256) return launch_gemm<256, 2>(xq, ldq, wq, ldw, p, stream);
-    if (c.bn == 192) return launch_gemm<192, 2>(xq, ldq, wq, ldw, p, stream);
-    return launch_gemm<128, 2>(xq, ldq, wq, ldw, p, stream);
+    if (c.bn == 256) return c.ks == 2 ? launch_gemm<256, 2, 2>(xq, ldq, wq, ldw, p, stream)
+                                      : launch_gemm<256, 2, 1>(xq, ldq, wq, ldw, p, stream);
+    if (c.bn == 192) return launch_gemm<192, 2, 1>(xq, ldq, wq, ldw, p, stream);
+    return c.ks == 2 ? launch_gemm<128, 2, 2>(xq, ldq, wq, ldw, p, stream)
+                     : launch_gemm<128, 2, 1>(xq, ldq, wq, ldw, p, stream);
   }
-  if (c.bn == 256) return launch_gemm<256, 1>(xq, ldq, wq, ldw, p, stream);
-  if (c.bn == 192) return launch_gemm<192, 1>(xq, ldq, wq, ldw, p, stream);
-  return launch_gemm<128, 1>(xq, ldq, wq, ldw, p, stream);
+  if (c.bn == 256) return c.ks == 2 ? launch_gemm<256, 1, 2>(xq, ldq, wq, ldw, p, stream)
+                                    : launch_gemm<256, 1, 1>(xq, ldq, wq, ldw, p, stream);
+  if (c.bn == 192) return launch_gemm<192, 1, 1>(xq, ldq, wq, ldw, p, stream);
+  return c.ks == 2 ? launch_gemm<128, 1, 2>(xq, ldq, wq, ldw, p, stream)
+                   : launch_gemm<128, 1, 1>(xq, ldq, wq, ldw, p, stream);
 }
 
 }  // namespace qarvd_b200

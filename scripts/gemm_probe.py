@@ -45,14 +45,16 @@ for name, n, k, no in [("qkv", 1536, 1536, 32), ("ffn0", 8960, 1536, 32), ("ffn2
     f = lambda: _lib.call("qarvd_dual_gemm", xq.data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad, M, n,
                           L.k_pad, L.k_outlier, sx.data_ptr(), L.scale_outlier32.data_ptr(),
                           L.scale_normal32.data_ptr(), None, 0, qb.BF16, y.data_ptr(), n, None, None, st)
-    for cg, bn in ((1, 128), (1, 192), (1, 256), (2, 128), (2, 192), (2, 256)):
+    for cg, bn, ks in ((1, 128, 1), (1, 192, 1), (1, 128, 2), (2, 128, 1), (2, 256, 1), (2, 128, 2),
+                       (2, 256, 2)):
         os.environ["QARVD_GEMM_BN"] = str(bn)
         os.environ["QARVD_GEMM_CG"] = str(cg)
+        os.environ["QARVD_GEMM_KS"] = str(ks)
         for dbg, tag in ((0, "full"), (2, "mma_only")):
             os.environ["QARVD_GEMM_DEBUG"] = str(dbg)
             for warm in (False,):
                 ms = timeit(f, do_flush=not warm)
-                out[f"{name}_cg{cg}_bn{bn}_{tag}{'_warmL2' if warm else ''}"] = round(
+                out[f"{name}_cg{cg}_bn{bn}_ks{ks}_{tag}{'_warmL2' if warm else ''}"] = round(
                     2.0 * M * n * k / (ms * 1e-3) / 1e12, 1)
         os.environ.pop("QARVD_GEMM_DEBUG")
 print(json.dumps(out, indent=1))
