@@ -46,6 +46,17 @@ int require_device();
 
 constexpr int kNumSMs = 148;
 
+// Large-smem kernels all request the maximum shared-memory carveout, so consecutive
+// kernels of a pipeline never force an SM carveout reconfiguration between launches.
+template <typename Kernel>
+inline cudaError_t set_smem_attrs(Kernel kern, int dynamic_bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dynamic_bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              static_cast<int>(cudaSharedmemCarveoutMaxShared));
+}
+
 // ---- bf16 helpers (bit patterns; RNE as bytes.hpp:40-45) -----------------
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t h) {
   return __uint_as_float(static_cast<uint32_t>(h) << 16);

@@ -666,9 +666,7 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(dual_gemm_kernel<BN, CG, KS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(C::kSmemBytes));
+    attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS>, static_cast<int>(C::kSmemBytes));
   });
   QARVD_CUDA_TRY(attr_err);
   CUtensorMap ta, tb;

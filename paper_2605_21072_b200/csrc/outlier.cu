@@ -329,9 +329,7 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
   int P = 1;
   while (P < max_k) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * sizeof(unsigned long long);
-  QARVD_CUDA_TRY(cudaFuncSetAttribute(select_outliers_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMaxSelK * static_cast<int>(sizeof(unsigned long long))));
+  QARVD_CUDA_TRY(set_smem_attrs(select_outliers_kernel, kMaxSelK * static_cast<int>(sizeof(unsigned long long))));
   select_outliers_kernel<<<num_jobs, kSelThreads, smem, s>>>(d_sj, tau, alpha_min, align);
   count_launch();
   QARVD_LAUNCH_CHECK();

@@ -276,8 +276,12 @@ __global__ void __launch_bounds__(kActThreads)
                          const int32_t* __restrict__ gather, int k_out, int G,
                          double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
                          float* __restrict__ s32_out, double* __restrict__ s64_out,
-                         unsigned long long* err) {
+                         unsigned long long* err, int k1_debug) {
   extern __shared__ __align__(128) uint8_t smem_act[];
+  __shared__ long long ktrace[3][32];
+  const long long k_entry = clock64();
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row_elems = (k + 1 + 7) & ~7;  // +1: zero sentinel read by pad columns
   const int stage_elems = row_elems * G;
@@ -292,18 +296,6 @@ __global__ void __launch_bounds__(kActThreads)
   const int my_row = warp / W;  // row inside the group
   const int sub = warp % W;     // column share of this warp
 
-  for (int c = tid; c < k_out; c += kActThreads) {
-    const int src = gather ? __ldg(gather + c) : c;
-    gidx[c] = static_cast<int16_t>(src < 0 ? k : src);
-  }
-  for (int r = tid; r < kActStages * G; r += kActThreads)
-    for (int e = k; e < row_elems; ++e) rows[r * row_elems + e] = 0;
-  if (tid == 0) {
-    for (int s = 0; s < kActStages; ++s) mbar_init_(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
   auto issue = [&](int64_t it, int slot) {
     const int64_t g = blockIdx.x + it * gridDim.x;
     if (g >= num_groups) return;
@@ -314,8 +306,31 @@ __global__ void __launch_bounds__(kActThreads)
     for (int r = 0; r < nr; ++r)
       bulk_load(rows + slot * stage_elems + r * row_elems, x + (r0 + r) * ldx, bytes, &full[slot]);
   };
-  if (tid == 0)
+  // the first row groups are requested before anything else, so HBM latency overlaps
+  // the gather-table setup (the copies write [0, k) of each row, the sentinel column k
+  // and the table are disjoint)
+  if (tid == 0) {
+    for (int s = 0; s < kActStages; ++s) mbar_init_(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < kActStages; ++s) issue(s, s);
+  }
+  if (gather && (k_out & 3) == 0 && (reinterpret_cast<uintptr_t>(gather) & 15) == 0) {
+#pragma unroll 4
+    for (int c4 = tid; c4 < (k_out >> 2); c4 += kActThreads) {
+      const int4 gi = __ldg(reinterpret_cast<const int4*>(gather) + c4);
+      const int src[4] = {gi.x, gi.y, gi.z, gi.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) gidx[4 * c4 + e] = static_cast<int16_t>(src[e] < 0 ? k : src[e]);
+    }
+  } else {
+    for (int c = tid; c < k_out; c += kActThreads) {
+      const int src = gather ? __ldg(gather + c) : c;
+      gidx[c] = static_cast<int16_t>(src < 0 ? k : src);
+    }
+  }
+  for (int r = tid; r < kActStages * G; r += kActThreads)
+    for (int e = k; e < row_elems; ++e) rows[r * row_elems + e] = 0;
+  __syncthreads();
 
   const int csz = (((k + W - 1) / W) + 7) & ~7;     // source columns per warp (absmax)
   const int osz = (((k_out + W - 1) / W) + 15) & ~15;  // output columns per warp
@@ -325,7 +340,12 @@ __global__ void __launch_bounds__(kActThreads)
     const int64_t g = blockIdx.x + it * gridDim.x;
     if (g >= num_groups) break;
     const int slot = static_cast<int>(it % kActStages);
+    const long long tw0 = clock64();
     mbar_wait_(&full[slot], static_cast<uint32_t>((it / kActStages) & 1));
+    if (k1_debug == 2 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && tid == 0 && it < 32) {
+      ktrace[0][it] = tw0;
+      ktrace[1][it] = clock64();
+    }
     const int64_t row = g * G + my_row;
     const bool active = row < m;
     const uint16_t* rs = rows + slot * stage_elems + my_row * row_elems;
@@ -351,14 +371,31 @@ __global__ void __launch_bounds__(kActThreads)
       for (int w = 0; w < W; ++w) mag = max(mag, part[my_row * W + w]);
     }
     const bool row_bad = mag >= 0x7f80u;
-    GroupScale gsc = kStatic ? scale_static(static_scale)
-                             : scale_from_absmax(__uint_as_float(mag << 16), qmax);
-    if (active && sub == 0 && lane == 0) {
-      if (s32_out) s32_out[row] = gsc.s32;
-      if (s64_out) s64_out[row] = gsc.s64;
+    // fp32 reciprocal for the fast path; the f64 scale (a division) only where it is
+    // written or where the rare exact path needs it
+    const float amax = __uint_as_float(mag << 16);
+    GroupScale gsc;
+    if (kStatic) {
+      gsc = scale_static(static_scale);
+    } else {
+      gsc.r32 = amax > 0.f ? __fdiv_rn(static_cast<float>(qmax), amax) : 0.f;
+      gsc.exact = amax > 0.f && !(gsc.r32 <= FLT_MAX && gsc.r32 >= FLT_MIN);
+      gsc.s64 = 0.0;
+      gsc.s32 = 0.f;
     }
+    auto row_s64 = [&]() -> double {
+      return kStatic ? static_scale
+                     : (amax > 0.f ? __ddiv_rn(static_cast<double>(amax), static_cast<double>(qmax))
+                                   : DBL_MIN);
+    };
+    if (active && sub == 0 && lane == 0) {
+      const double s64 = row_s64();
+      if (s32_out) s32_out[row] = amax > 0.f || kStatic ? __double2float_rn(s64) : 0.f;
+      if (s64_out) s64_out[row] = s64;
+    }
+    if (!kStatic && (gsc.exact || row_bad)) gsc.s64 = row_s64();
 
-    if (active) {
+    if (active && k1_debug != 1) {
       int8_t* qr = q + row * ldq;
       const int o0 = sub * osz, o1 = min(o0 + osz, k_out);
       if (!row_bad && !gsc.exact) {
@@ -393,7 +430,7 @@ __global__ void __launch_bounds__(kActThreads)
               const float t = kStatic ? fminf(fmaxf(__fmul_rn(v[e], r), -fq), fq) : 0.f;
               const float d = kStatic ? __fsub_rn(t, rintf(t))
                                       : __fmaf_rn(v[e], r, -__fsub_rn(__uint_as_float(rr[e]), kMagic));
-              if (fabsf(d) > 0.4999f) rr[e] = static_cast<uint32_t>(act_code_exact(v[e], gsc.s64, qmax));
+              if (fabsf(d) > 0.4999f) rr[e] = static_cast<uint32_t>(act_code_exact(v[e], row_s64(), qmax));
             }
           }
           *reinterpret_cast<uint4*>(qr + c0) =
@@ -416,8 +453,21 @@ __global__ void __launch_bounds__(kActThreads)
         }
       }
     }
+    if (k1_debug == 2 && blockIdx.x == 0 && tid == 0 && it < 32) ktrace[2][it] = clock64();
     __syncthreads();  // every warp is done with this slot (and with part[])
     if (tid == 0) issue(it + kActStages, slot);
+  }
+  if (k1_debug == 2 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && tid == 0) {
+    unsigned long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    printf("cta %d: entry %lld clk before first wait; globaltimer entry %llu exit %llu (%llu ns)\n",
+           blockIdx.x, ktrace[0][0] - k_entry, g_entry, g_exit, g_exit - g_entry);
+  }
+  if (k1_debug == 2 && blockIdx.x == 0 && tid == 0) {
+    const long long t0 = ktrace[0][0];
+    for (int i = 0; i < 32 && blockIdx.x + static_cast<int64_t>(i) * gridDim.x < num_groups; ++i)
+      printf("group %2d: wait %7lld..%7lld done %7lld\n", i, ktrace[0][i] - t0, ktrace[1][i] - t0,
+             ktrace[2][i] - t0);
   }
 }
 
@@ -521,7 +571,7 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [&] {
-      attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = set_smem_attrs(kern, 200 * 1024);
     });
     QARVD_CUDA_TRY(attr);
     const int64_t groups = (m + G - 1) / G;
@@ -530,15 +580,14 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
     const int g = static_cast<int>(groups < cap ? groups : cap);
     kern<<<g, kActThreads, smem, stream>>>(static_cast<const uint16_t*>(x), m, static_cast<int>(k),
                                            ldx, gather, static_cast<int>(k_out), G, static_scale,
-                                           qmax, q, ldq, s32_n, s64_n, err);
+                                           qmax, q, ldq, s32_n, s64_n, err,
+                                           getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0);
   } else if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
     const size_t smem = static_cast<size_t>(kWarpsPerCta) * (((k + 7) & ~int64_t(7)) * 2);
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [] {
-      attr = cudaFuncSetAttribute(quant_rows_bf16_kernel<MODE>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kWarpsPerCta * kMaxSmemK * 2);
+      attr = set_smem_attrs(quant_rows_bf16_kernel<MODE>, kWarpsPerCta * kMaxSmemK * 2);
     });
     QARVD_CUDA_TRY(attr);
     quant_rows_bf16_kernel<MODE><<<grid, kWarpsPerCta * 32, smem, stream>>>(

@@ -328,7 +328,7 @@ extern "C" int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs,
 
   const int hist_smem = kBins * sizeof(uint32_t);
   QARVD_CUDA_TRY(
-      cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hist_smem));
+      set_smem_attrs(hist_kernel, hist_smem));
   // grid.x is limited to 2^31-1; units are far fewer
   hist_kernel<<<static_cast<unsigned>(units.size()), kHistThreads, hist_smem, s>>>(d_units);
   count_launch();
@@ -338,8 +338,7 @@ extern "C" int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs,
                            static_cast<size_t>(F) * num_cand * kNumBlocks * sizeof(double);
   if (eval_smem > 227 * 1024)
     QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "scale_search: frames x candidates too large for one CTA");
-  QARVD_CUDA_TRY(cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(eval_smem)));
+  QARVD_CUDA_TRY(set_smem_attrs(eval_kernel, static_cast<int>(eval_smem)));
   eval_kernel<<<num_jobs, kEvalThreads, eval_smem, s>>>(d_jobs, cst);
   count_launch();
   QARVD_LAUNCH_CHECK();

@@ -38,30 +38,47 @@ class QuantizedChain:
         j = self.inputs[i]
         return self.x if j < 0 else self.y[j]
 
-    def launch(self, stream: Optional[int] = None):
-        """Enqueue K1 + K2 for every layer (2 kernels per layer)."""
+    def launch(self, stream: Optional[int] = None, events: Optional[List] = None):
+        """Enqueue K1 + K2 for every layer (2 kernels per layer).  With ``events`` (a list of
+        2L+1 timing events) an event is recorded before, between and after the kernels;
+        recorded during capture they become graph nodes, so per-kernel device times come
+        from the replayed step itself."""
         s = _stream() if stream is None else stream
+        if events is not None:
+            events[0].record()
         for i, L in enumerate(self.layers):
             src = self._src(i)
             _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
                       src.stride(0), L.gather_dev.data_ptr(), L.k_pad, L.act_granularity,
                       float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
                       None, None, s)
+            if events is not None:
+                events[2 * i + 1].record()
             _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
                       self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
                       L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
                       self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
+            if events is not None:
+                events[2 * i + 2].record()
 
-    def capture(self):
-        """Capture launch() into a CUDA graph (after one eager warm-up launch)."""
+    def capture(self, timed: bool = False):
+        """Capture launch() into a CUDA graph (after one eager warm-up launch).  With
+        ``timed`` the graph also records per-kernel timing events (``self.events``)."""
         self.launch()
         torch.cuda.synchronize()
+        self.events = ([torch.cuda.Event(enable_timing=True) for _ in range(2 * len(self.layers) + 1)]
+                       if timed else None)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.launch()
+            self.launch(events=self.events)
         torch.cuda.synchronize()
         self.graph = g
         return g
+
+    def kernel_times_ms(self) -> List[float]:
+        """Per-kernel device times [K1, K2] * L of the last replay (timed graphs only)."""
+        e = self.events
+        return [e[i].elapsed_time(e[i + 1]) for i in range(len(e) - 1)]
 
     def replay(self):
         if self.graph is None:
