@@ -378,7 +378,7 @@ def main():
     gemm_ms = [sum(k_gemm)]
 
     # end to end through the C-ABI host-buffer entry (pinned host in/out, copies timed)
-    h0, h2 = engine.LinearHandle(L0, qb.EPI_GELU), engine.LinearHandle(L2)
+    h0, h2 = engine.LinearHandle(chain.layers[0], qb.EPI_GELU), engine.LinearHandle(chain.layers[1])
     xh = x.cpu().pin_memory()
     yh = torch.empty((M_TOKENS, DIM), dtype=torch.bfloat16).pin_memory()
     for _ in range(3):
@@ -415,6 +415,7 @@ def main():
             "data": "synthetic (Wan-1.3B-shaped bf16 weights, 2.1% outlier input channels x8; bf16 N(0,1) activations with heavy channels)",
             "config": {"workload": WORKLOAD, "M": M_TOKENS, "ffn0": [FFN, DIM, L0.k_outlier],
                        "ffn2": [DIM, FFN, L2.k_outlier], "activation_quant": "per-token dynamic",
+                       "chain": "ffn.0 output channels folded into ffn.2's plan order (no gather in K1 for U)",
                        "l2": "flushed (256 MiB write) before every timed step; step timed with CUDA events",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",

@@ -20,6 +20,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace qarvd_b200 {
 namespace {
@@ -215,51 +216,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 }
 
 // ---------------------------------------------------------------------------
-// Activation fast path (bf16, per-token or static): persistent CTAs stream row
-// groups through a 4-stage shared-memory ring filled by TMA bulk copies
-// (cp.async.bulk, one per row), so HBM reads overlap the rounding of earlier
-// rows.  A group is G rows (G*K*2 ~ 16-24 KB); each row is owned by 8/G warps
-// which split its columns, combine their |x| maxima through shared memory,
-// then emit 16 codes per lane per step through an int16 gather table.
-// Rounding: t = v * (qmax/absmax) in fp32, q = rint(t).  |t - v/s| < 3.1e-5
-// for |t| <= 254, so q is the f64 round_half_even(v/s) unless t lies within
-// 1e-4 of a half-integer; those (~0.04%) are recomputed with __ddiv_rn.
-constexpr int kActThreads = 256;
-constexpr int kActStages = 4;
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
-                                          uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_init_(uint64_t* bar, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
-               "r"(n));
-}
-__device__ __forceinline__ void mbar_expect_tx_(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
+// K1 fast path (bf16 activations, per-token or static scale).
+//
+// One team of T threads owns one row.  It loads the row with coalesced 16-byte
+// loads straight into registers (at most kK1Vec chunks of 8 values per thread),
+// reduces |x|max across the team and emits the codes:
+//   * no permutation (the producer already wrote the row in plan order, see
+//     pipeline.QuantizedChain): codes come from the registers, 8 per chunk,
+//     written back as one 8-byte store;
+//   * with a permutation: the row is also copied to a per-team shared-memory
+//     buffer (plus 8 zero sentinels that pad slots read) and every thread
+//     gathers 16 codes per step through the plan's index table.
+// Teams never wait on one another, so each SM keeps many rows in flight.
+//
+// Rounding: t = v * (qmax/absmax) in fp32 (packed f32x2 FMAs), q = t rounded by
+// the 1.5*2^23 magic add.  |t - v/s| < 3.1e-5 for |t| <= 254, so q equals the
+// reference's f64 round_half_even(v/s) (quant.cpp:123-131) unless t lies within
+// 1e-4 of a half-integer; the exact residual d = v*r - q (one fma) flags those
+// (~0.04% of chunks), which are recomputed with the f64 division.
+constexpr int kK1Vec = 8;
+// Residual above which the f64 division decides.  Per-token: t = v*r32 exactly (fma), so
+// |t - v/s64| <= |t| * 2^-24 <= 7.6e-6 for |t| <= 127: guard 3e-5.  Static: the product is
+// rounded as well and clamped, |t - v/s64| <= |t| * 2^-23 <= 3.1e-5: guard 1e-4.
+template <bool kStatic>
+__device__ __forceinline__ constexpr float tie_guard() { return kStatic ? 0.4999f : 0.49997f; }
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: an fp32 add rounds to an integer (RNE)
 
 __device__ __noinline__ int act_code_exact(float v, double s64, int qmax) {
@@ -269,205 +249,391 @@ __device__ __noinline__ int act_code_exact(float v, double s64, int qmax) {
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 
+struct ActScale {
+  float r;      // fp32 reciprocal qmax/absmax (or 1/s for a static scale)
+  float fq;     // qmax as float (static clamp)
+  bool exact;   // r is unusable: every code takes the f64 division
+  double s64;   // f64 scale, valid where exact/rare paths need it
+};
+
+// Fast codes of two bf16 values (packed in w); code words carry the code in their
+// low byte.  |residual| is folded into dmax (> 0.4999 => the chunk is redone exactly).
 template <bool kStatic>
-__global__ void __launch_bounds__(kActThreads)
-    quant_act_tma_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
-                         const int32_t* __restrict__ gather, int k_out, int G,
-                         double static_scale, int qmax, int8_t* __restrict__ q, int64_t ldq,
-                         float* __restrict__ s32_out, double* __restrict__ s64_out,
-                         unsigned long long* err, int k1_debug) {
-  extern __shared__ __align__(128) uint8_t smem_act[];
-  __shared__ long long ktrace[3][32];
-  const long long k_entry = clock64();
-  unsigned long long g_entry;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row_elems = (k + 1 + 7) & ~7;  // +1: zero sentinel read by pad columns
-  const int stage_elems = row_elems * G;
-  uint16_t* rows = reinterpret_cast<uint16_t*>(smem_act);
-  int16_t* gidx = reinterpret_cast<int16_t*>(rows + kActStages * stage_elems);
-  uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(gidx + ((k_out + 7) & ~7)) + 15) & ~uintptr_t(15));
-  uint32_t* part = reinterpret_cast<uint32_t*>(full + kActStages);  // per-warp |x| maxima (bits)
-
-  const int64_t num_groups = (m + G - 1) / G;
-  const int W = 8 / G;          // warps per row
-  const int my_row = warp / W;  // row inside the group
-  const int sub = warp % W;     // column share of this warp
-
-  auto issue = [&](int64_t it, int slot) {
-    const int64_t g = blockIdx.x + it * gridDim.x;
-    if (g >= num_groups) return;
-    const int64_t r0 = g * G;
-    const int nr = static_cast<int>((m - r0) < G ? (m - r0) : G);
-    const uint32_t bytes = static_cast<uint32_t>(k) * 2u;
-    mbar_expect_tx_(&full[slot], bytes * nr);
-    for (int r = 0; r < nr; ++r)
-      bulk_load(rows + slot * stage_elems + r * row_elems, x + (r0 + r) * ldx, bytes, &full[slot]);
-  };
-  // the first row groups are requested before anything else, so HBM latency overlaps
-  // the gather-table setup (the copies write [0, k) of each row, the sentinel column k
-  // and the table are disjoint)
-  if (tid == 0) {
-    for (int s = 0; s < kActStages; ++s) mbar_init_(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < kActStages; ++s) issue(s, s);
-  }
-  if (gather && (k_out & 3) == 0 && (reinterpret_cast<uintptr_t>(gather) & 15) == 0) {
-#pragma unroll 4
-    for (int c4 = tid; c4 < (k_out >> 2); c4 += kActThreads) {
-      const int4 gi = __ldg(reinterpret_cast<const int4*>(gather) + c4);
-      const int src[4] = {gi.x, gi.y, gi.z, gi.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) gidx[4 * c4 + e] = static_cast<int16_t>(src[e] < 0 ? k : src[e]);
-    }
+__device__ __forceinline__ void act_codes2(float lo, float hi, const ActScale& sc, uint32_t& c0,
+                                           uint32_t& c1, float& dmax) {
+  if (kStatic) {
+    const float t0 = fminf(fmaxf(__fmul_rn(lo, sc.r), -sc.fq), sc.fq);
+    const float t1 = fminf(fmaxf(__fmul_rn(hi, sc.r), -sc.fq), sc.fq);
+    const float y0 = __fadd_rn(t0, kMagic), y1 = __fadd_rn(t1, kMagic);
+    dmax = fmaxf(dmax, fmaxf(fabsf(__fsub_rn(t0, __fsub_rn(y0, kMagic))),
+                             fabsf(__fsub_rn(t1, __fsub_rn(y1, kMagic)))));
+    c0 = __float_as_uint(y0);
+    c1 = __float_as_uint(y1);
   } else {
-    for (int c = tid; c < k_out; c += kActThreads) {
-      const int src = gather ? __ldg(gather + c) : c;
-      gidx[c] = static_cast<int16_t>(src < 0 ? k : src);
+    const uint64_t v2 = pk2(lo, hi), r2 = pk2(sc.r, sc.r), m2 = pk2(kMagic, kMagic);
+    const uint64_t y2 = ffma2(v2, r2, m2);                // magic + rint(v*r)
+    const uint64_t n2 = ffma2(y2, pk2(-1.f, -1.f), m2);  // -rint(v*r), exact
+    const uint64_t d2 = ffma2(v2, r2, n2);                // v*r - rint(v*r), one rounding
+    float d0, d1, y0, y1;
+    upk2(d2, d0, d1);
+    upk2(y2, y0, y1);
+    dmax = fmaxf(dmax, fmaxf(fabsf(d0), fabsf(d1)));
+    c0 = __float_as_uint(y0);
+    c1 = __float_as_uint(y1);
+  }
+}
+
+// Slow code of one value: non-finite inputs are reported (the reference throws,
+// quant.cpp:113-121) and give 0; everything else takes the exact f64 division.
+__device__ __forceinline__ uint32_t act_code_slow(uint16_t h, double s64, int qmax,
+                                                  unsigned long long* err, int64_t flat) {
+  if ((h & 0x7f80u) == 0x7f80u) {
+    record_error(err, flat);
+    return 0u;
+  }
+  return static_cast<uint32_t>(act_code_exact(bf16_bits_to_float(h), s64, qmax));
+}
+
+// Exact code of a per-token value whose fp32 product t = v*r32 lies within the tie guard of
+// the half-integer hc (bf16 inputs make exact .5 ties common: a row whose |x|max mantissa
+// is a power of two turns every odd mantissa of one binade into a tie).  The reference
+// rounds fl64(v / s64) half-to-even (quant.cpp:123-131).  fl64(v / s64) == hc exactly iff
+// |v/s64 - hc| <= half an ulp of hc (a quarter on the small side of hc = +-0.5), i.e. iff
+// |r| <= s64 * ulp(hc)/2 with r = v - hc*s64 from one f64 fma; otherwise the quotient is a
+// neighbouring double on r's side.  A band of 2^-30 around the boundary takes the division.
+// Returns kTieUndecided for the band (the caller rescans those values with the division).
+constexpr uint32_t kTieUndecided = 0x100u;
+__device__ __forceinline__ uint32_t act_code_tie(float v, float t, double s64, int qmax) {
+  const float q = rintf(t);
+  const float lower = t > q ? q : q - 1.f;  // hc = lower + 0.5
+  const double hc = static_cast<double>(lower) + 0.5;
+  const double r = fma(-hc, s64, static_cast<double>(v));
+  const int e = static_cast<int>((__float_as_uint(fabsf(static_cast<float>(hc))) >> 23) & 0xffu) - 127;
+  double hu = s64 * __longlong_as_double(static_cast<long long>(1023 + e - 53) << 52);
+  if (e == -1 && ((r < 0.0) == (hc > 0.0))) hu *= 0.5;  // |hc| = 0.5: finer spacing below
+  const double ar = fabs(r);
+  int code;
+  if (ar < hu * (1.0 - 0x1p-30)) {
+    const int lo = static_cast<int>(lower);
+    code = (lo & 1) ? lo + 1 : lo;  // exact tie in f64: half to even
+  } else if (ar > hu * (1.0 + 0x1p-30)) {
+    code = static_cast<int>(lower) + (r > 0.0 ? 1 : 0);
+  } else {
+    return kTieUndecided;
+  }
+  code = code > qmax ? qmax : (code < -qmax ? -qmax : code);
+  return static_cast<uint32_t>(code);
+}
+
+// Patch the codes of one flagged chunk (N values, bf16 bits hv): per-token values within
+// the guard are decided exactly by act_code_tie.  Values that need the f64 division (the
+// undecided band, and static-scale near-ties) keep their fast code and set `rescan`; with
+// `exact` (the rescan pass) they take the division here.
+template <bool kStatic, int N, bool kExact>
+__device__ __forceinline__ void act_fix_chunk(const uint16_t* hv, uint32_t* c, const ActScale& sc,
+                                              double s64, int qmax, bool& rescan) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const float v = __uint_as_float(static_cast<uint32_t>(hv[e]) << 16);
+    bool divide = false;
+    if (kStatic) {
+      const float t = fminf(fmaxf(__fmul_rn(v, sc.r), -sc.fq), sc.fq);
+      divide = fabsf(__fsub_rn(t, rintf(t))) > tie_guard<true>();
+    } else {
+      const float t = __fmul_rn(v, sc.r);  // only its position relative to hc matters
+      const float d = __fmaf_rn(v, sc.r, -rintf(t));
+      if (fabsf(d) > tie_guard<false>()) {
+        const uint32_t code = act_code_tie(v, t, s64, qmax);
+        if (code == kTieUndecided) divide = true;
+        else c[e] = code;
+      }
+    }
+    if (divide) {
+      if (kExact) c[e] = static_cast<uint32_t>(act_code_exact(v, s64, qmax));
+      else rescan = true;
     }
   }
-  for (int r = tid; r < kActStages * G; r += kActThreads)
-    for (int e = k; e < row_elems; ++e) rows[r * row_elems + e] = 0;
-  __syncthreads();
+}
 
-  const int csz = (((k + W - 1) / W) + 7) & ~7;     // source columns per warp (absmax)
-  const int osz = (((k_out + W - 1) / W) + 15) & ~15;  // output columns per warp
-  const float fq = static_cast<float>(qmax);
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
-  for (int64_t it = 0;; ++it) {
-    const int64_t g = blockIdx.x + it * gridDim.x;
-    if (g >= num_groups) break;
-    const int slot = static_cast<int>(it % kActStages);
-    const long long tw0 = clock64();
-    mbar_wait_(&full[slot], static_cast<uint32_t>((it / kActStages) & 1));
-    if (k1_debug == 2 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && tid == 0 && it < 32) {
-      ktrace[0][it] = tw0;
-      ktrace[1][it] = clock64();
+// Persistent teams: team g of the grid quantizes rows g, g + G, g + 2G, ... (G teams in
+// total).  Each team keeps S row slots in shared memory filled by cp.async (16 bytes per
+// thread per copy, no registers held): rows j+1 .. j+S-1 stream in while row j is rounded.
+// Teams are either four independent warps per CTA (rows of <= 2048 values) or one CTA of
+// a multiple of 32 threads chosen so the row's 16-byte chunks split evenly.  A one-CTA team
+// combines its per-warp |x| maxima through mbarriers one row ahead -- each warp publishes
+// row j+1's partial maximum before rounding row j -- so no CTA-wide barrier sits on the
+// row loop (4 partial buffers: a warp runs at most three rows ahead of the slowest reader).
+// The permutation, when present, is staged once per CTA as an int16 table (pad -> k, the
+// zero sentinel column of every row slot).
+constexpr int kK1Parts = 4;
+
+template <int S, bool kStatic, bool kGather, bool kWarpTeams>
+__global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
+    quant_act_rows_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                          const int32_t* __restrict__ gather, int k_out, double static_scale,
+                          int qmax, int8_t* __restrict__ q, int64_t ldq,
+                          float* __restrict__ s32_out, double* __restrict__ s64_out,
+                          unsigned long long* __restrict__ err,
+                          unsigned long long* __restrict__ trace) {
+  constexpr int kTeams = kWarpTeams ? 4 : 1;
+  constexpr int kMaxWarps = kWarpTeams ? 1 : 8;
+  extern __shared__ __align__(16) uint16_t k1_smem[];
+  __shared__ uint32_t part[kK1Parts][kMaxWarps];
+  __shared__ __align__(8) uint64_t pbar[kK1Parts];
+  if (trace && threadIdx.x == 0) {  // diagnostics (QARVD_K1_TRACE): CTA start time and SM
+    unsigned long long t;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trace[3 * blockIdx.x] = t;
+    trace[3 * blockIdx.x + 2] = smid;
+  }
+  const int T = kWarpTeams ? 32 : static_cast<int>(blockDim.x);
+  const int team = kWarpTeams ? static_cast<int>(threadIdx.x >> 5) : 0;
+  const int tt = kWarpTeams ? static_cast<int>(threadIdx.x & 31) : static_cast<int>(threadIdx.x);
+  const int warp = tt >> 5, lane = threadIdx.x & 31, nwarps = T >> 5;
+  const int nvec = k >> 3;
+  const int row_stride = k + 8;  // + 8 zero sentinels read by pad slots
+  uint16_t* slots = k1_smem + team * S * row_stride;
+  int16_t* gidx = reinterpret_cast<int16_t*>(k1_smem + kTeams * S * row_stride);
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kTeams;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTeams + team;
+
+  auto issue = [&](int64_t r, int slot) {
+    if (r < m) {
+      const uint16_t* src = x + r * ldx;
+      uint16_t* dst = slots + slot * row_stride;
+      for (int vi = tt; vi < nvec; vi += T) cp_async16(dst + vi * 8, src + vi * 8);
     }
-    const int64_t row = g * G + my_row;
-    const bool active = row < m;
-    const uint16_t* rs = rows + slot * stage_elems + my_row * row_elems;
-
-    // ---- |x| max as packed 16-bit integer max of the sign-cleared bf16 bits;
-    //      non-finite values (exponent all ones) are exactly the maxima >= 0x7f80
+    cp_async_commit();
+  };
+  // |x| max of this thread's chunks as packed 16-bit max of the sign-cleared bf16 bits
+  // (non-finite values are exactly the magnitudes >= 0x7f80), reduced over the warp
+  auto warp_part_max = [&](int slot) -> uint32_t {
+    const uint16_t* srow = slots + slot * row_stride;
     uint32_t mx = 0;
-    if (active) {
-      const int c0 = sub * csz, c1 = min(c0 + csz, k);
-      int c = c0 + lane * 8;
-      for (; c + 8 <= c1; c += 256) {
-        const uint4 d = *reinterpret_cast<const uint4*>(rs + c);
-        mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
-                                   __vmaxu2(d.z & 0x7fff7fffu, d.w & 0x7fff7fffu)));
-      }
-      for (; c < c1; ++c) mx = max(mx, static_cast<uint32_t>(rs[c] & 0x7fffu));
+    for (int vi = tt; vi < nvec; vi += T) {
+      const uint4 d = *reinterpret_cast<const uint4*>(srow + vi * 8);
+      mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
+                                 __vmaxu2(d.z & 0x7fff7fffu, d.w & 0x7fff7fffu)));
     }
-    uint32_t mag = max(mx & 0xffffu, mx >> 16);
-    mag = __reduce_max_sync(0xffffffffu, mag);
-    if (W > 1) {
-      if (lane == 0) part[warp] = mag;
-      __syncthreads();
-      for (int w = 0; w < W; ++w) mag = max(mag, part[my_row * W + w]);
+    return __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+  };
+  auto publish = [&](int64_t j) {  // this warp's partial max of row j (its copies landed)
+    const uint32_t pm = warp_part_max(static_cast<int>(j % S));
+    if (lane == 0) part[j % kK1Parts][warp] = pm;
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&pbar[j % kK1Parts]);
+  };
+
+  if (!kWarpTeams && threadIdx.x == 0) {
+    for (int b = 0; b < kK1Parts; ++b) ptx::mbar_init(&pbar[b], nwarps);
+    ptx::fence_mbar_init();
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) issue(row0 + s * step, s);
+  if (kGather) {  // k_out % 16 == 0 and gather 16-byte aligned (launch_rows)
+#pragma unroll 4
+    for (int c4 = threadIdx.x; c4 < (k_out >> 2); c4 += blockDim.x) {
+      const int4 g = __ldg(reinterpret_cast<const int4*>(gather) + c4);
+      const uint32_t lo = static_cast<uint16_t>(g.x < 0 ? k : g.x) |
+                          (static_cast<uint32_t>(g.y < 0 ? k : g.y) << 16);
+      const uint32_t hi = static_cast<uint16_t>(g.z < 0 ? k : g.z) |
+                          (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16);
+      reinterpret_cast<uint2*>(gidx)[c4] = make_uint2(lo, hi);
     }
-    const bool row_bad = mag >= 0x7f80u;
-    // fp32 reciprocal for the fast path; the f64 scale (a division) only where it is
-    // written or where the rare exact path needs it
-    const float amax = __uint_as_float(mag << 16);
-    GroupScale gsc;
-    if (kStatic) {
-      gsc = scale_static(static_scale);
+  }
+  if (tt < 8) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) slots[s * row_stride + k + tt] = 0;
+  }
+  __syncthreads();
+  if (!kWarpTeams && row0 < m) {
+    cp_async_wait_group<S - 1>();  // row 0 landed
+    publish(0);
+  }
+
+  int64_t j = 0;
+  for (int64_t row = row0; row < m; ++j, row += step) {
+    const int slot = static_cast<int>(j % S);
+    const uint16_t* srow = slots + slot * row_stride;
+    uint32_t mag;
+    if (kWarpTeams) {
+      cp_async_wait_group<S - 1>();  // row j landed
+      __syncwarp();
+      mag = warp_part_max(slot);
     } else {
-      gsc.r32 = amax > 0.f ? __fdiv_rn(static_cast<float>(qmax), amax) : 0.f;
-      gsc.exact = amax > 0.f && !(gsc.r32 <= FLT_MAX && gsc.r32 >= FLT_MIN);
-      gsc.s64 = 0.0;
-      gsc.s32 = 0.f;
+      if (row + step < m) {
+        cp_async_wait_group<S - 2>();  // row j+1 landed
+        publish(j + 1);
+      }
+      ptx::mbar_wait(&pbar[j % kK1Parts], static_cast<uint32_t>((j / kK1Parts) & 1));
+      mag = 0;
+      for (int w = 0; w < nwarps; ++w) mag = max(mag, part[j % kK1Parts][w]);
+    }
+
+    const bool row_bad = mag >= 0x7f80u;
+    const float amax = __uint_as_float(mag << 16);
+    ActScale sc;
+    sc.fq = static_cast<float>(qmax);
+    if (kStatic) {
+      const GroupScale g = scale_static(static_scale);
+      sc.r = g.r32;
+      sc.exact = g.exact;
+      sc.s64 = static_scale;
+    } else {
+      sc.r = amax > 0.f ? __fdiv_rn(static_cast<float>(qmax), amax) : 0.f;
+      sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
+      sc.s64 = 0.0;
     }
     auto row_s64 = [&]() -> double {
       return kStatic ? static_scale
                      : (amax > 0.f ? __ddiv_rn(static_cast<double>(amax), static_cast<double>(qmax))
                                    : DBL_MIN);
     };
-    if (active && sub == 0 && lane == 0) {
-      const double s64 = row_s64();
-      if (s32_out) s32_out[row] = amax > 0.f || kStatic ? __double2float_rn(s64) : 0.f;
-      if (s64_out) s64_out[row] = s64;
+    // the scale outputs come from the team's last thread (the first runs the row-ahead
+    // publish on the critical path)
+    if (tt == T - 1) {
+      const double s = row_s64();
+      if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s) : 0.f;
+      if (s64_out) s64_out[row] = s;
     }
-    if (!kStatic && (gsc.exact || row_bad)) gsc.s64 = row_s64();
+    int8_t* qr = q + row * ldq;
+    auto src_of = [&](int c) -> int { return kGather ? gidx[c] : c; };
 
-    if (active && k1_debug != 1) {
-      int8_t* qr = q + row * ldq;
-      const int o0 = sub * osz, o1 = min(o0 + osz, k_out);
-      if (!row_bad && !gsc.exact) {
-        const float r = gsc.r32;
-        for (int c0 = o0 + lane * 16; c0 < o1; c0 += 512) {
-          const uint4 ga = *reinterpret_cast<const uint4*>(gidx + c0);
-          const uint4 gb = *reinterpret_cast<const uint4*>(gidx + c0 + 8);
-          const uint32_t gw[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-          float v[16];
-          uint32_t rr[16];
-          bool need = false;
+    if (row_bad || sc.exact) {
+      // rare rows: a non-finite input (reported; the reference throws) or an unusable
+      // fp32 reciprocal -- every code takes the exact path
+      const double s64 = row_s64();
+      for (int c = tt; c < k_out; c += T)
+        qr[c] = static_cast<int8_t>(act_code_slow(srow[src_of(c)], s64, qmax, err, row * k_out + c));
+    } else {
+      // Fast codes.  A chunk holding a value within the tie guard is patched in place
+      // (act_fix_chunk: one f64 fma per flagged value) before its store.
+      double s64 = 0.0;
+      bool have_s64 = false, rescan = false;
+      auto lazy_s64 = [&]() {
+        if (!have_s64) {
+          s64 = row_s64();
+          have_s64 = true;
+        }
+        return s64;
+      };
+      if (!kGather) {
+#pragma unroll 2
+        for (int vi = tt; vi < nvec; vi += T) {
+          const uint4 d = *reinterpret_cast<const uint4*>(srow + vi * 8);
+          const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+          uint32_t c[8];
+          float dmax = 0.f;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint32_t src = (gw[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-            v[e] = __uint_as_float(static_cast<uint32_t>(rs[src]) << 16);
-            float t, d;
-            if (kStatic) {
-              t = fminf(fmaxf(__fmul_rn(v[e], r), -fq), fq);
-              const float y = __fadd_rn(t, kMagic);
-              d = __fsub_rn(t, __fsub_rn(y, kMagic));
-              rr[e] = __float_as_uint(y);
-            } else {
-              const float y = __fmaf_rn(v[e], r, kMagic);
-              d = __fmaf_rn(v[e], r, -__fsub_rn(y, kMagic));
-              rr[e] = __float_as_uint(y);
-            }
-            need |= fabsf(d) > 0.4999f;
+          for (int h = 0; h < 4; ++h)
+            act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u),
+                                sc, c[2 * h], c[2 * h + 1], dmax);
+          if (dmax > tie_guard<kStatic>()) {
+            const uint16_t hv[8] = {static_cast<uint16_t>(w[0]), static_cast<uint16_t>(w[0] >> 16),
+                                    static_cast<uint16_t>(w[1]), static_cast<uint16_t>(w[1] >> 16),
+                                    static_cast<uint16_t>(w[2]), static_cast<uint16_t>(w[2] >> 16),
+                                    static_cast<uint16_t>(w[3]), static_cast<uint16_t>(w[3] >> 16)};
+            act_fix_chunk<kStatic, 8, false>(hv, c, sc, lazy_s64(), qmax, rescan);
           }
-          if (need) {  // within 1e-4 of a .5 tie: the exact f64 division decides
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float t = kStatic ? fminf(fmaxf(__fmul_rn(v[e], r), -fq), fq) : 0.f;
-              const float d = kStatic ? __fsub_rn(t, rintf(t))
-                                      : __fmaf_rn(v[e], r, -__fsub_rn(__uint_as_float(rr[e]), kMagic));
-              if (fabsf(d) > 0.4999f) rr[e] = static_cast<uint32_t>(act_code_exact(v[e], row_s64(), qmax));
-            }
-          }
-          *reinterpret_cast<uint4*>(qr + c0) =
-              make_uint4(pack4(rr[0], rr[1], rr[2], rr[3]), pack4(rr[4], rr[5], rr[6], rr[7]),
-                         pack4(rr[8], rr[9], rr[10], rr[11]), pack4(rr[12], rr[13], rr[14], rr[15]));
+          *reinterpret_cast<uint2*>(qr + vi * 8) =
+              make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
         }
       } else {
-        // rare rows: a non-finite input (reported, reference throws) or an unusable fp32 reciprocal
-        for (int c = o0 + lane; c < o1; c += 32) {
-          const int src = gidx[c];
-          const uint16_t h = rs[src];
-          int code = 0;
-          if ((h & 0x7f80u) == 0x7f80u) {
-            if (err) atomicMin(err, static_cast<unsigned long long>(row * k_out + c));
-          } else {
-            code = gsc.exact ? act_code_exact(bf16_bits_to_float(h), gsc.s64, qmax)
-                             : quant_code_fast(bf16_bits_to_float(h), gsc.r32, gsc.s64, qmax);
+        // 4 consecutive codes per lane per step: neighbouring lanes read shared memory
+        // 8 bytes apart (at most 2-way bank conflicts for a near-contiguous gather) and
+        // write one coalesced 4-byte word each
+#pragma unroll 4
+        for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
+          const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+          const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu],
+                                  srow[gp.y >> 16]};
+          uint32_t c[4];
+          float dmax = 0.f;
+          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                              __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
+          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                              __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
+          if (dmax > tie_guard<kStatic>())
+            act_fix_chunk<kStatic, 4, false>(hv, c, sc, lazy_s64(), qmax, rescan);
+          *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
+        }
+      }
+      if (rescan) {  // (very rare) values only the f64 division decides: redo this thread's codes
+        if (!kGather) {
+          for (int vi = tt; vi < nvec; vi += T) {
+            uint16_t hv[8];
+            uint32_t c[8];
+            for (int e = 0; e < 8; ++e) {
+              hv[e] = srow[vi * 8 + e];
+              c[e] = static_cast<uint32_t>(qr[vi * 8 + e]);
+            }
+            act_fix_chunk<kStatic, 8, true>(hv, c, sc, s64, qmax, rescan);
+            for (int e = 0; e < 8; ++e) qr[vi * 8 + e] = static_cast<int8_t>(c[e]);
           }
-          qr[c] = static_cast<int8_t>(code);
+        } else {
+          for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
+            uint16_t hv[4];
+            uint32_t c[4];
+            for (int e = 0; e < 4; ++e) {
+              hv[e] = srow[src_of(c0 + e)];
+              c[e] = static_cast<uint32_t>(qr[c0 + e]);
+            }
+            act_fix_chunk<kStatic, 4, true>(hv, c, sc, s64, qmax, rescan);
+            for (int e = 0; e < 4; ++e) qr[c0 + e] = static_cast<int8_t>(c[e]);
+          }
         }
       }
     }
-    if (k1_debug == 2 && blockIdx.x == 0 && tid == 0 && it < 32) ktrace[2][it] = clock64();
-    __syncthreads();  // every warp is done with this slot (and with part[])
-    if (tid == 0) issue(it + kActStages, slot);
+    // refill this slot with row j+S (a gathered row is read by the whole team first)
+    if (kGather) {
+      if (kWarpTeams) __syncwarp();
+      else __syncthreads();
+    }
+    issue(row + S * step, slot);
   }
-  if (k1_debug == 2 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && tid == 0) {
-    unsigned long long g_exit;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
-    printf("cta %d: entry %lld clk before first wait; globaltimer entry %llu exit %llu (%llu ns)\n",
-           blockIdx.x, ktrace[0][0] - k_entry, g_entry, g_exit, g_exit - g_entry);
-  }
-  if (k1_debug == 2 && blockIdx.x == 0 && tid == 0) {
-    const long long t0 = ktrace[0][0];
-    for (int i = 0; i < 32 && blockIdx.x + static_cast<int64_t>(i) * gridDim.x < num_groups; ++i)
-      printf("group %2d: wait %7lld..%7lld done %7lld\n", i, ktrace[0][i] - t0, ktrace[1][i] - t0,
-             ktrace[2][i] - t0);
+  if (trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[3 * blockIdx.x + 1] = t;
+    }
   }
 }
 
@@ -545,6 +711,76 @@ int grid_for_rows(int64_t m) {
   return static_cast<int>(ctas < cap ? ctas : cap);
 }
 
+template <int S, bool kStatic, bool kGather, bool kWarpTeams>
+int launch_act_rows_t(int threads, const uint16_t* x, int64_t m, int k, int64_t ldx,
+                      const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
+                      int64_t ldq, float* s32, double* s64, unsigned long long* err,
+                      cudaStream_t stream) {
+  constexpr int kTeams = kWarpTeams ? 4 : 1;
+  auto kern = quant_act_rows_kernel<S, kStatic, kGather, kWarpTeams>;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] { attr = set_smem_attrs(kern, 110 * 1024); });
+  QARVD_CUDA_TRY(attr);
+  const size_t smem = static_cast<size_t>(kTeams) * S * (k + 8) * 2 +
+                      (kGather ? static_cast<size_t>((k_out + 7) & ~7) * 2 : 0);
+  // persistent grid: as many CTAs as fit on the GPU (cached per launch shape)
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_threads = 0, cached_blocks = 0;
+  if (cached_smem != smem || cached_threads != threads) {
+    int nb = 0;
+    QARVD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
+    cached_smem = smem;
+    cached_threads = threads;
+    cached_blocks = nb > 0 ? nb : 1;
+  }
+  const int64_t need = (m + kTeams - 1) / kTeams;
+  const int64_t cap = static_cast<int64_t>(kNumSMs) * cached_blocks;
+  const int64_t grid = need < cap ? need : cap;
+  // QARVD_K1_TRACE=<device address>: per-CTA (start, end, smid) globaltimer trace (diagnostics)
+  static unsigned long long* trace = [] {
+    const char* e = getenv("QARVD_K1_TRACE");
+    return e ? reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0)) : nullptr;
+  }();
+  kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(x, m, k, ldx, gather, k_out, static_scale,
+                                                             qmax, q, ldq, s32, s64, err, trace);
+  return QARVD_OK;
+}
+
+// Team shape for a row of nvec 16-byte chunks: four one-warp teams per CTA for rows of up
+// to 256 chunks, else one CTA of 4..8 warps, the count that splits the chunks most evenly
+// (ties: more warps), e.g. 1120 chunks (K = 8960) -> 7 warps x 5 chunks per thread.
+inline int k1_team_threads(int nvec) {
+  if (nvec <= 256) return 32;
+  int best_w = 8, best_waste = 1 << 30;
+  for (int w = 8; w >= 4; --w) {
+    const int per = (nvec + 32 * w - 1) / (32 * w);
+    const int waste = per * 32 * w - nvec;
+    if (waste < best_waste) {
+      best_waste = waste;
+      best_w = w;
+    }
+  }
+  return 32 * best_w;
+}
+
+template <bool kStatic>
+int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t ldx,
+                    const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
+                    int64_t ldq, float* s32, double* s64, unsigned long long* err,
+                    cudaStream_t stream) {
+  const int threads = k1_team_threads(k / 8);
+  if (threads == 32)
+    return gathered ? launch_act_rows_t<2, kStatic, true, true>(128, x, m, k, ldx, gather, k_out, static_scale,
+                                                                qmax, q, ldq, s32, s64, err, stream)
+                    : launch_act_rows_t<2, kStatic, false, true>(128, x, m, k, ldx, gather, k_out, static_scale,
+                                                                 qmax, q, ldq, s32, s64, err, stream);
+  return gathered ? launch_act_rows_t<3, kStatic, true, false>(threads, x, m, k, ldx, gather, k_out,
+                                                               static_scale, qmax, q, ldq, s32, s64, err, stream)
+                  : launch_act_rows_t<3, kStatic, false, false>(threads, x, m, k, ldx, gather, k_out,
+                                                                static_scale, qmax, q, ldq, s32, s64, err, stream);
+}
+
 template <int MODE>
 int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, const int32_t* gather,
                 int64_t k_out, int64_t k_o, double static_scale, int bits, int8_t* q, int64_t ldq,
@@ -558,30 +794,21 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
   }
   if (m == 0) return QARVD_OK;
   const int grid = grid_for_rows(m);
-  const bool tma_ok = MODE != kWeightDual && dtype == QARVD_BF16 && k < 16384 &&
-                      (k % 8) == 0 && (ldx % 8) == 0 && (k_out % 16) == 0 && (ldq % 16) == 0 &&
-                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(q) & 15) == 0;
-  if (tma_ok) {
-    const int G = k <= 1536 ? 8 : (k <= 3072 ? 4 : (k <= 6144 ? 2 : 1));
-    const size_t row_elems = (k + 1 + 7) & ~int64_t(7);
-    const size_t smem = static_cast<size_t>(kActStages) * G * row_elems * 2 + k_out * 2 + 64 +
-                        kActStages * 8 + 16 * 4 + 16;
-    auto kern = quant_act_tma_kernel<MODE == kActStatic>;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [&] {
-      attr = set_smem_attrs(kern, 200 * 1024);
-    });
-    QARVD_CUDA_TRY(attr);
-    const int64_t groups = (m + G - 1) / G;
-    const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
-    const int64_t cap = static_cast<int64_t>(kNumSMs) * ctas_per_sm;
-    const int g = static_cast<int>(groups < cap ? groups : cap);
-    kern<<<g, kActThreads, smem, stream>>>(static_cast<const uint16_t*>(x), m, static_cast<int>(k),
-                                           ldx, gather, static_cast<int>(k_out), G, static_scale,
-                                           qmax, q, ldq, s32_n, s64_n, err,
-                                           getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0);
+  const bool fast_ok = MODE != kWeightDual && dtype == QARVD_BF16 && k <= 32 * kK1Vec * 8 * 8 &&
+                       (k % 8) == 0 && (ldx % 8) == 0 && (k_out % 16) == 0 && (ldq % 16) == 0 &&
+                       (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(gather) & 15) == 0;
+  // shared memory of the team slots (+ int16 permutation table) must fit the 110 KB opt-in
+  const int64_t k1_smem = fast_ok ? ((k / 8 <= 256 ? 4 * 2 : 3) * (k + 8) * 2 +
+                                     (gather ? ((k_out + 7) & ~int64_t(7)) * 2 : 0))
+                                  : 0;
+  if (fast_ok && k1_smem <= 110 * 1024) {
+    if (int st = launch_act_rows<MODE == kActStatic>(gather != nullptr, static_cast<const uint16_t*>(x), m,
+                                                     static_cast<int>(k), ldx, gather,
+                                                     static_cast<int>(k_out), static_scale, qmax, q,
+                                                     ldq, s32_n, s64_n, err, stream))
+      return st;
   } else if (dtype == QARVD_BF16 && k <= kMaxSmemK) {
     const size_t smem = static_cast<size_t>(kWarpsPerCta) * (((k + 7) & ~int64_t(7)) * 2);
     static std::once_flag once;

@@ -126,7 +126,7 @@ class QuantizedLayer:
     scale_normal64: torch.Tensor
     scale_outlier32: torch.Tensor
     scale_normal32: torch.Tensor
-    gather_dev: torch.Tensor
+    gather_dev: Optional[torch.Tensor]  # None: inputs already arrive in plan order (pipeline.fold_output_permutation)
     act_granularity: int = _lib.ACT_PER_TOKEN
     act_scale: float = 0.0
     bias: Optional[torch.Tensor] = None
@@ -182,14 +182,15 @@ def kernel_a_quantize_activation(x: torch.Tensor, layer_or_plan, granularity: in
     gather_dev = (layer_or_plan.gather_dev if isinstance(layer_or_plan, QuantizedLayer)
                   else torch.from_numpy(plan.gather).to(x.device))
     m, k = x.shape
-    if k != plan.d_in:
+    d_in = plan.d_in if gather_dev is not None else plan.k_pad  # folded layer: plan-order input
+    if k != d_in:
         raise _lib.InvalidArgument("permute_activations: plan does not match activation width")
     xq = torch.empty((m, plan.k_pad), dtype=torch.int8, device=x.device)
     s32 = torch.empty(m, dtype=torch.float32, device=x.device)
     s64 = torch.empty(m, dtype=torch.float64, device=x.device)
     err = torch.empty(1, dtype=torch.int64, device=x.device) if check_finite else None
     _lib.call("qarvd_quantize_act", x.data_ptr(), _dtype_code(x), m, k, x.stride(0),
-              gather_dev.data_ptr(), plan.k_pad, granularity, float(static_scale), bits,
+              _ptr(gather_dev), plan.k_pad, granularity, float(static_scale), bits,
               xq.data_ptr(), plan.k_pad, s32.data_ptr(), s64.data_ptr(), _ptr(err), _stream())
     if err is not None:
         _check_err(err, "quantize")
@@ -233,7 +234,7 @@ class LinearHandle:
         self.layer = layer
         h = _lib.ctypes.c_void_p()
         _lib.call("qarvd_linear_create", layer.wq.data_ptr(), layer.out_dim, layer.k_pad,
-                  layer.k_outlier, layer.gather_dev.data_ptr(), layer.in_dim,
+                  layer.k_outlier, _ptr(layer.gather_dev), layer.in_dim,
                   layer.scale_outlier32.data_ptr(), layer.scale_normal32.data_ptr(),
                   _ptr(layer.bias), layer.act_granularity, float(layer.act_scale), epilogue,
                   _lib.ctypes.byref(h))

@@ -11,7 +11,8 @@ kernels themselves).
 """
 from __future__ import annotations
 
-from typing import List, Optional, Sequence
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 
@@ -19,14 +20,64 @@ from . import _lib
 from .engine import QuantizedLayer, _ptr, _stream
 
 
+def fold_output_permutation(producer: QuantizedLayer,
+                            consumer: QuantizedLayer) -> Tuple[QuantizedLayer, QuantizedLayer]:
+    """Make ``producer`` emit its outputs directly in ``consumer``'s plan order.
+
+    The consumer's first step, permute_activations(y, plan) (engine.cpp:32-44), only
+    reorders y's columns.  Reordering the producer's output channels -- its code rows,
+    group scales and bias -- by the consumer's gather yields y already in plan order;
+    pad slots get all-zero rows (codes, scales and bias 0), which produce exact zeros
+    (GELU(0) = 0), the reference's zero pad columns.  The consumer's K1 then quantizes
+    contiguous rows: same codes, same per-token scale (zeros do not move |x|max), and
+    no gather.  Returns (producer', consumer'); the originals are left untouched.
+    """
+    g = consumer.gather_dev
+    if g is None:
+        return producer, consumer
+    if producer.out_dim != consumer.in_dim:
+        raise _lib.InvalidArgument("fold_output_permutation: producer width does not match the consumer")
+    gl = g.long()
+    valid = gl >= 0
+    src = gl[valid]
+    if src.numel() != consumer.in_dim or not torch.equal(
+            torch.sort(src).values, torch.arange(consumer.in_dim, device=src.device)):
+        raise _lib.InvalidArgument("fold_output_permutation: plan gather is not a permutation")
+    n = consumer.k_pad
+
+    def rows(t: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+        if t is None:
+            return None
+        out = torch.zeros((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        out[valid] = t[src]
+        return out
+
+    prod = dataclasses.replace(
+        producer, out_dim=n, wq=rows(producer.wq), scale_outlier64=rows(producer.scale_outlier64),
+        scale_normal64=rows(producer.scale_normal64), scale_outlier32=rows(producer.scale_outlier32),
+        scale_normal32=rows(producer.scale_normal32), bias=rows(producer.bias))
+    cons = dataclasses.replace(consumer, in_dim=n, gather_dev=None)
+    return prod, cons
+
+
 class QuantizedChain:
     def __init__(self, layers: Sequence[QuantizedLayer], m: int,
-                 epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None):
-        """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1)."""
+                 epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None,
+                 fold: bool = True):
+        """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1).
+
+        With ``fold`` every intermediate consumed by exactly one layer is produced in that
+        layer's plan order (fold_output_permutation), so its K1 runs without a gather.
+        ``self.source_ops`` keeps the unfolded shapes for op counting."""
         self.layers = list(layers)
         self.m = m
         self.epilogues = list(epilogues) if epilogues is not None else [_lib.EPI_NONE] * len(layers)
         self.inputs = list(inputs) if inputs is not None else list(range(-1, len(layers) - 1))
+        self.source_ops = float(sum(2.0 * m * L.out_dim * L.in_dim for L in self.layers))
+        if fold:
+            for j, i in enumerate(self.inputs):
+                if i >= 0 and self.inputs.count(i) == 1 and self.layers[j].gather_dev is not None:
+                    self.layers[i], self.layers[j] = fold_output_permutation(self.layers[i], self.layers[j])
         dev = self.layers[0].wq.device
         self.x = torch.empty((m, self.layers[0].in_dim), dtype=torch.bfloat16, device=dev)
         self.xq = [torch.empty((m, L.k_pad), dtype=torch.int8, device=dev) for L in self.layers]
@@ -49,7 +100,7 @@ class QuantizedChain:
         for i, L in enumerate(self.layers):
             src = self._src(i)
             _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
-                      src.stride(0), L.gather_dev.data_ptr(), L.k_pad, L.act_granularity,
+                      src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
                       float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
                       None, None, s)
             if events is not None:
@@ -66,7 +117,7 @@ class QuantizedChain:
         ``timed`` the graph also records per-kernel timing events (``self.events``)."""
         self.launch()
         torch.cuda.synchronize()
-        self.events = ([torch.cuda.Event(enable_timing=True) for _ in range(2 * len(self.layers) + 1)]
+        self.events = ([torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * len(self.layers) + 1)]
                        if timed else None)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -93,4 +144,5 @@ class QuantizedChain:
         return 2 * len(self.layers)
 
     def int_ops(self) -> float:
-        return float(sum(2.0 * self.m * L.out_dim * L.in_dim for L in self.layers))
+        """Algorithmic ops of the chain as specified (unfolded shapes, no pad rows)."""
+        return self.source_ops

@@ -277,3 +277,96 @@ def test_synth_weights_outlier_columns_detected(cuda):
     cols = synth.pick_outlier_columns(1, spec.index, spec.in_dim, spec.outlier_fraction)
     assert set(cols.tolist()) <= set(rep.aligned_outliers.tolist())
     assert len(rep.aligned_outliers) == 192
+
+
+# ---------------------------------------------------------------- K1 without a gather + chain fold
+@pytest.mark.parametrize("m,k", [(4680, 8960), (300, 1536), (33, 200), (7, 16384), (5, 2056)])
+def test_k1_contiguous_rows_bitexact(cuda, m, k):
+    """Identity layout (inputs already in plan order): the no-gather K1 path."""
+    bits, x64 = bf16_values((m, k), seed=k + 3 * m, heavy_cols=np.arange(0, k, 97))
+    x = to_dev_bf16(bits)
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    qb._lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, m, k, k, None, k, qb.ACT_PER_TOKEN,
+                 0.0, 8, xq.data_ptr(), k, None, s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+
+
+def test_k1_contiguous_nonfinite_and_static(cuda):
+    bits, x64 = bf16_values((16, 1024), seed=17, scale=4.0)
+    x = to_dev_bf16(bits)
+    xq = torch.empty((16, 1024), dtype=torch.int8, device="cuda")
+    s = 0.0123
+    qb._lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, 16, 1024, 1024, None, 1024,
+                 qb.ACT_PER_TENSOR, s, 8, xq.data_ptr(), 1024, None, None, None, None)
+    q_ref, _, _ = oracle.quantize_act(x64, None, per_token=False, static_scale=s)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    bits[9, 700] = 0x7F80
+    bits[12, 5] = 0xFFC0
+    err = torch.empty(1, dtype=torch.int64, device="cuda")
+    qb._lib.call("qarvd_quantize_act", to_dev_bf16(bits).data_ptr(), qb.BF16, 16, 1024, 1024, None,
+                 1024, qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), 1024, None, None, err.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 9 * 1024 + 700
+
+
+@pytest.mark.parametrize("d,f,m,n0,n2", [(256, 640, 300, 32, 13), (1536, 8960, 256, 32, 192),
+                                          (96, 200, 33, 5, 0)])
+def test_chain_fold_bitexact(cuda, d, f, m, n0, n2):
+    """Producing the intermediate in the consumer's plan order (pipeline.fold_output_permutation)
+    gives the same codes, scales and final output as permute-then-quantize."""
+    from paper_2605_21072_b200.pipeline import QuantizedChain
+    p0, p2 = make_plan(d, n0, seed=1), make_plan(f, n2, seed=2)
+    w0, _ = bf16_values((f, d), seed=4, scale=1.0 / np.sqrt(d), heavy_cols=p0.outlier_indices if n0 else None)
+    w2, _ = bf16_values((d, f), seed=5, scale=1.0 / np.sqrt(f), heavy_cols=p2.outlier_indices if n2 else None)
+    L0 = engine.prepare_weights("ffn.0", to_dev_bf16(w0), p0)
+    L2 = engine.prepare_weights("ffn.2", to_dev_bf16(w2), p2)
+    L0.bias = torch.linspace(-0.5, 0.5, f, device="cuda", dtype=torch.float32)
+    xb, _ = bf16_values((m, d), seed=6, heavy_cols=p0.outlier_indices if n0 else None, gamma=4.0)
+    outs = []
+    for fold in (False, True):
+        ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fold=fold)
+        assert (ch.layers[1].gather_dev is None) == fold
+        ch.x.copy_(to_dev_bf16(xb))
+        ch.launch()
+        torch.cuda.synchronize()
+        outs.append((ch.xq[1].clone(), ch.sx[1].clone(), ch.output.clone()))
+    (q_a, s_a, y_a), (q_b, s_b, y_b) = outs
+    assert torch.equal(q_a, q_b)
+    assert torch.equal(s_a, s_b)
+    assert torch.equal(y_a.view(torch.int16), y_b.view(torch.int16))
+    # and the C-ABI host chain over the folded layers agrees
+    ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fold=True)
+    hs = [engine.LinearHandle(ch.layers[0], qb.EPI_GELU), engine.LinearHandle(ch.layers[1])]
+    xh = torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).pin_memory()
+    yh = torch.empty((m, d), dtype=torch.bfloat16).pin_memory()
+    engine.chain_forward_host(hs, xh, yh)
+    assert torch.equal(yh.view(torch.int16), y_a.cpu().view(torch.int16))
+    for h in hs:
+        h.close()
+
+
+@pytest.mark.parametrize("k", [256, 8960])
+def test_k1_contiguous_ties(cuda, k):
+    """Rows built so v/s lands on exact .5 ties (and an all-zero row) on the no-gather path."""
+    r = np.random.default_rng(k)
+    rows = []
+    for i in range(48):
+        a = float(2.0 ** r.integers(-6, 6))
+        base = (np.arange(k, dtype=np.float64) % 255 - 127) * (a / 127.0) * 0.5
+        base[0] = a
+        rows.append(base)
+    rows.append(np.zeros(k))
+    bits = oracle.f32_to_bf16_bits(np.asarray(rows, dtype=np.float32))
+    x64 = oracle.bf16_bits_to_f64(bits)
+    m = len(rows)
+    x = to_dev_bf16(bits)
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    qb._lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, m, k, k, None, k, qb.ACT_PER_TOKEN,
+                 0.0, 8, xq.data_ptr(), k, None, s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
