@@ -96,6 +96,16 @@ int qarvd_quantize_act(const void* x, int x_dtype, int64_t m, int64_t k, int64_t
                        float* scale_f32, double* scale_f64, int64_t* err_index,
                        void* stream);
 
+/* K1 for bf16 rows already in plan order (identity gather, k_out = k) whose |x| max is
+ * known: per-token with row_absmax from the producer (qarvd_dual_gemm_rowmax), or a
+ * static per-tensor scale (row_absmax unused, may be NULL).  Same codes, scales and
+ * error reporting as qarvd_quantize_act(x, QARVD_BF16, m, k, ldx, NULL, k, ...);
+ * per-token rows reset their row_absmax entry to 0.  k, ldx, ldq multiples of 8. */
+int qarvd_quantize_act_rowmax(const uint16_t* x, int64_t m, int64_t k, int64_t ldx,
+                              uint32_t* row_absmax, int granularity, double static_scale,
+                              int bits, int8_t* xq, int64_t ldq, float* scale_f32,
+                              double* scale_f64, int64_t* err_index, void* stream);
+
 /* ---- K5: dual-scale weight preparation ----------------------------------
  * Replaces  build_plan scales (dual_scale.cpp:13-24, :58-90) +
  *           nearest-rounding codes of fake_quant_dual (dual_scale.cpp:92-114) +
@@ -141,6 +151,18 @@ int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw
                     const float* scale_w_outlier, const float* scale_w_normal, const float* bias,
                     int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
                     int32_t* acc_normal, void* stream);
+
+/* K2 for a chained producer: bf16 y as qarvd_dual_gemm, plus
+ *   row_absmax[i] = max(row_absmax[i], max_j (bf16 bits of y[i,j]) & 0x7fff)
+ * (the per-token |y| max the next layer's K1 needs, reduced in the epilogue instead of
+ * re-reading y).  row_absmax: device uint32 [m], zero before the first step; the
+ * consumer's qarvd_quantize_act_rowmax resets it.  No reference counterpart: the fusion
+ * of engine.cpp:134-142 (layer i output) with quant.cpp:170-182 (layer i+1 scales). */
+int qarvd_dual_gemm_rowmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                           int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                           const float* scale_w_outlier, const float* scale_w_normal,
+                           const float* bias, int epilogue, uint16_t* y, int64_t ldy,
+                           uint32_t* row_absmax, void* stream);
 
 /* K2 with the reference's exact f64 epilogue (engine.cpp:86-94: val = 0; val += (s_x*s_wo[j])*acc_o;
  * val += (s_x*s_wn[j])*acc_n) on f64 scales -> f64 y.  Bit-identical to kernel_b_gemm_dequant

@@ -57,6 +57,7 @@ def lib():
         _o.oracle_round_half_even.restype = c_double
         _o.oracle_round_half_even.argtypes = [c_double]
         _o.oracle_num_threads.restype = c_int
+        _o.oracle_row_scale_formula_mismatches.restype = c_int64
     return _o
 
 
@@ -326,3 +327,8 @@ def ref_toy_weight(layer, blocks=2, hidden=64, seed=1, pattern="", fraction=0.02
     _rc(ref().ref_toy_weight(blocks, hidden, seed, pattern.encode(), fraction, gamma,
                              layer.encode(), _p(out), ctypes.byref(rows), ctypes.byref(cols)))
     return out
+
+
+def row_scale_formula_mismatches() -> int:
+    """Mismatches of the device row-scale formula vs fl(amax/qmax) over all bf16 amax, 2..8 bits."""
+    return int(lib().oracle_row_scale_formula_mismatches())

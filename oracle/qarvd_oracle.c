@@ -420,3 +420,25 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Check of the device's row-scale formula (quantize.cu row_s64): for every positive
+ * finite bf16 amax and every qmax of 2..8 bits, y = amax * fl(1/qmax) corrected by one
+ * fma equals the correctly rounded fl(amax / qmax) of quant.cpp:168-181.  Returns the
+ * number of mismatches (0). */
+int64_t oracle_row_scale_formula_mismatches(void) {
+  int64_t bad = 0;
+  for (int b = 2; b <= 8; ++b) {
+    const double q = (double)((1 << (b - 1)) - 1);
+    const double rq = 1.0 / q;
+    for (uint32_t h = 1; h < 0x7f80u; ++h) {
+      const uint32_t u = h << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      const double a = (double)f;
+      const double y = a * rq;
+      const double y2 = fma(fma(-y, q, a), rq, y);
+      if (y2 != a / q) ++bad;
+    }
+  }
+  return bad;
+}

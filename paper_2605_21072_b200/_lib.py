@@ -110,6 +110,16 @@ SIGNATURES = {
          c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p,
          c_void_p],
     ),
+    "qarvd_dual_gemm_rowmax": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p],
+    ),
+    "qarvd_quantize_act_rowmax": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_double, c_int, c_void_p, c_int64,
+         c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
     "qarvd_dual_gemm_f64": (
         c_int,
         [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

@@ -102,6 +102,7 @@ struct qarvd_linear {
   float* sx = nullptr;
   uint16_t* x_dev = nullptr;
   uint16_t* y_dev = nullptr;
+  uint32_t* rowmax = nullptr;  // per-row |y| max for a chained consumer (zero between steps)
   std::mutex mu;  // forward() is re-entrant per handle (reference providers are shared const)
 };
 
@@ -113,12 +114,16 @@ int ensure_workspace(qarvd_linear* L, int64_t m, bool host_io) {
   cudaFree(L->sx);
   cudaFree(L->x_dev);
   cudaFree(L->y_dev);
+  cudaFree(L->rowmax);
   L->xq = nullptr;
   L->sx = nullptr;
   L->x_dev = nullptr;
   L->y_dev = nullptr;
+  L->rowmax = nullptr;
   QARVD_CUDA_TRY(cudaMalloc(&L->xq, static_cast<size_t>(cap) * L->k_pad));
   QARVD_CUDA_TRY(cudaMalloc(&L->sx, static_cast<size_t>(cap) * sizeof(float)));
+  QARVD_CUDA_TRY(cudaMalloc(&L->rowmax, static_cast<size_t>(cap) * sizeof(uint32_t)));
+  QARVD_CUDA_TRY(cudaMemset(L->rowmax, 0, static_cast<size_t>(cap) * sizeof(uint32_t)));
   if (host_io) {
     QARVD_CUDA_TRY(cudaMalloc(&L->x_dev, static_cast<size_t>(cap) * L->k_in * 2));
     QARVD_CUDA_TRY(cudaMalloc(&L->y_dev, static_cast<size_t>(cap) * L->n * 2));
@@ -193,6 +198,7 @@ int qarvd_linear_destroy(qarvd_linear_t L) {
   cudaFree(L->sx);
   cudaFree(L->x_dev);
   cudaFree(L->y_dev);
+  cudaFree(L->rowmax);
   delete L;
   return QARVD_OK;
 }
@@ -250,9 +256,34 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
                                   static_cast<size_t>(m) * layers[0]->k_in * 2,
                                   cudaMemcpyHostToDevice, s);
   const uint16_t* in = layers[0]->x_dev;
+  // A layer whose input already arrives in plan order (no gather: the producer's output
+  // channels were folded, pipeline.fold_output_permutation) takes the streaming K1; for
+  // per-token activations its producer reduces the row |y| max in the GEMM epilogue.
+  auto streams_from = [&](int i) {
+    return i + 1 < num_layers && !layers[i + 1]->gather && layers[i + 1]->k_in % 8 == 0;
+  };
   for (int i = 0; i < num_layers && e == cudaSuccess && st == QARVD_OK; ++i) {
-    st = linear_forward_dev(layers[i], in, m, layers[i]->y_dev, s);
-    in = layers[i]->y_dev;
+    qarvd_linear* L = layers[i];
+    if (i > 0 && streams_from(i - 1)) {
+      qarvd_linear* P = layers[i - 1];
+      st = qarvd_quantize_act_rowmax(in, m, L->k_in, L->k_in,
+                                     L->granularity == QARVD_ACT_PER_TOKEN ? P->rowmax : nullptr,
+                                     L->granularity, L->static_scale, 8, L->xq, L->k_pad, L->sx,
+                                     nullptr, nullptr, s);
+    } else {
+      st = qarvd_quantize_act(in, QARVD_BF16, m, L->k_in, L->k_in, L->gather, L->k_pad,
+                              L->granularity, L->static_scale, 8, L->xq, L->k_pad, L->sx, nullptr,
+                              nullptr, s);
+    }
+    if (st) break;
+    if (streams_from(i) && layers[i + 1]->granularity == QARVD_ACT_PER_TOKEN)
+      st = qarvd_dual_gemm_rowmax(L->xq, L->k_pad, L->wq, L->k_pad, m, L->n, L->k_pad, L->k_o, L->sx,
+                                  L->s_wo, L->s_wn, L->bias, L->epilogue, L->y_dev, L->n, L->rowmax, s);
+    else
+      st = qarvd_dual_gemm(L->xq, L->k_pad, L->wq, L->k_pad, m, L->n, L->k_pad, L->k_o, L->sx,
+                           L->s_wo, L->s_wn, L->bias, L->epilogue, QARVD_BF16, L->y_dev, L->n,
+                           nullptr, nullptr, s);
+    in = L->y_dev;
   }
   if (e == cudaSuccess && st == QARVD_OK)
     e = cudaMemcpyAsync(y_host, in, static_cast<size_t>(m) * layers[num_layers - 1]->n * 2,

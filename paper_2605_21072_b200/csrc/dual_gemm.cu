@@ -71,6 +71,7 @@ struct GemmParams {
   const double* sx64;  // QARVD_F64 output: f64 scales, reference epilogue (engine.cpp:86-94)
   const double* so64;
   const double* sn64;
+  uint32_t* row_absmax;  // optional: atomicMax per row of the sign-cleared bf16 output bits
   int use_tma_store;  // bf16 output through the TMA store path
   int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
@@ -407,6 +408,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         else ptx::mbar_arrive_leader(bar);
       }
     };
+    // |y| max of the row over this tile (sign-cleared bf16 bits, packed 16-bit lanes); the
+    // consumer's per-token K1 reads it instead of re-reducing the row (pipeline.QuantizedChain)
+    uint32_t tile_mx = 0;
     // y (fp32 bits in rn) -> bf16 TMA store, or direct bf16 / f32 stores
     auto store_chunk = [&](uint32_t (&rn)[32], int64_t row0, int64_t row, int64_t col0, int ncols) {
       if (p.use_tma_store) {
@@ -416,6 +420,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __nv_bfloat162 h2 =
               __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
           pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        if (p.row_absmax) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t keep = (2 * e + 1 < ncols ? 0x7fff7fffu : 0u) | (2 * e < ncols ? 0x7fffu : 0u);
+            tile_mx = __vmaxu2(tile_mx, pk[e] & keep);
+          }
         }
         uint8_t* ystage = ystage0 + ybuf * 2048;
         if (C::kYBufs == 2) {
@@ -441,7 +452,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          if (e < ncols) yr[e] = __float2bfloat16_rn(__uint_as_float(rn[e]));
+          if (e < ncols) {
+            const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(rn[e]));
+            yr[e] = h;
+            tile_mx = max(tile_mx, static_cast<uint32_t>(__bfloat16_as_ushort(h)) & 0x7fffu);
+          }
       } else if (row < p.m) {
         float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
         if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
@@ -475,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM + q * 32;
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.m;
+      tile_mx = 0;
       asm volatile("bar.sync 1, 256;" ::: "memory");  // scales visible to all epilogue warps
       const long long te0 = clock64();
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -564,6 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         release(&tempty[acc]);
         if (C::kAccStages == 1) release(&tofree[0]);
       }
+      if (p.row_absmax && row_ok)
+        atomicMax(p.row_absmax + row, max(tile_mx & 0xffffu, tile_mx >> 16));
       {
         const int ti = (t - cta_id) / num_ctas;
         if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4 && ti < 32) {
@@ -747,8 +765,10 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
                      const float* scale_wo, const float* scale_wn, const float* bias,
                      int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
                      int32_t* acc_n, cudaStream_t stream, const double* sx64 = nullptr,
-                     const double* so64 = nullptr, const double* sn64 = nullptr) {
+                     const double* so64 = nullptr, const double* sn64 = nullptr,
+                     uint32_t* row_absmax = nullptr) {
   GemmParams p{};
+  p.row_absmax = row_absmax;
   p.sx64 = sx64;
   p.so64 = so64;
   p.sn64 = sn64;
@@ -787,12 +807,12 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
 
 using namespace qarvd_b200;
 
-extern "C" int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
-                               int64_t m, int64_t n, int64_t k, int64_t k_outlier,
-                               const float* scale_x, const float* scale_w_outlier,
-                               const float* scale_w_normal, const float* bias, int epilogue,
-                               int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
-                               int32_t* acc_normal, void* stream) {
+namespace {
+int dual_gemm_checked(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                      int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                      const float* scale_w_outlier, const float* scale_w_normal, const float* bias,
+                      int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
+                      int32_t* acc_normal, uint32_t* row_absmax, void* stream) {
   clear_error();
   if (m <= 0 || n <= 0 || k <= 0)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
@@ -810,10 +830,38 @@ extern "C" int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, 
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
   if (out_dtype != QARVD_BF16 && out_dtype != QARVD_F32)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: output dtype must be bf16 or f32");
+  if (row_absmax && out_dtype != QARVD_BF16)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: row |y| max is defined for bf16 outputs");
   if (int st = require_device()) return st;
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
                           scale_w_normal, bias, epilogue, out_dtype, y, ldy, acc_outlier,
-                          acc_normal, as_stream(stream));
+                          acc_normal, as_stream(stream), nullptr, nullptr, nullptr, row_absmax);
+}
+}  // namespace
+
+extern "C" int qarvd_dual_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                               int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                               const float* scale_x, const float* scale_w_outlier,
+                               const float* scale_w_normal, const float* bias, int epilogue,
+                               int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
+                               int32_t* acc_normal, void* stream) {
+  return dual_gemm_checked(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
+                           scale_w_normal, bias, epilogue, out_dtype, y, ldy, acc_outlier,
+                           acc_normal, nullptr, stream);
+}
+
+extern "C" int qarvd_dual_gemm_rowmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                      int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                      const float* scale_x, const float* scale_w_outlier,
+                                      const float* scale_w_normal, const float* bias, int epilogue,
+                                      uint16_t* y, int64_t ldy, uint32_t* row_absmax, void* stream) {
+  if (!row_absmax) {
+    clear_error();
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null row |y| max buffer");
+  }
+  return dual_gemm_checked(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
+                           scale_w_normal, bias, epilogue, QARVD_BF16, y, ldy, nullptr, nullptr,
+                           row_absmax, stream);
 }
 
 extern "C" int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,

@@ -235,9 +235,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 // 1e-4 of a half-integer; the exact residual d = v*r - q (one fma) flags those
 // (~0.04% of chunks), which are recomputed with the f64 division.
 constexpr int kK1Vec = 8;
-// Residual above which the f64 division decides.  Per-token: t = v*r32 exactly (fma), so
-// |t - v/s64| <= |t| * 2^-24 <= 7.6e-6 for |t| <= 127: guard 3e-5.  Static: the product is
-// rounded as well and clamped, |t - v/s64| <= |t| * 2^-23 <= 3.1e-5: guard 1e-4.
+// Residual above which the f64 path decides.  Per-token: t = v*r32 with the product exact
+// (fma) and r32 = fl(fl(1/amax) * qmax) within 2^-23 of qmax/amax, so |t - v/s64| <= |t| *
+// 2^-23 <= 1.6e-5 for |t| <= 127: guard 3e-5.  Static: the product is rounded as well and
+// clamped, |t - v/s64| <= |t| * 2^-23 <= 3.1e-5 for |t| <= 254: guard 1e-4.
 template <bool kStatic>
 __device__ __forceinline__ constexpr float tie_guard() { return kStatic ? 0.4999f : 0.49997f; }
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: an fp32 add rounds to an integer (RNE)
@@ -376,44 +377,82 @@ __device__ __forceinline__ void act_fix_chunk(const uint16_t* hv, uint32_t* c, c
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-               "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // Persistent teams: team g of the grid quantizes rows g, g + G, g + 2G, ... (G teams in
-// total).  Each team keeps S row slots in shared memory filled by cp.async (16 bytes per
-// thread per copy, no registers held): rows j+1 .. j+S-1 stream in while row j is rounded.
-// Teams are either four independent warps per CTA (rows of <= 2048 values) or one CTA of
-// a multiple of 32 threads chosen so the row's 16-byte chunks split evenly.  A one-CTA team
-// combines its per-warp |x| maxima through mbarriers one row ahead -- each warp publishes
-// row j+1's partial maximum before rounding row j -- so no CTA-wide barrier sits on the
-// row loop (4 partial buffers: a warp runs at most three rows ahead of the slowest reader).
-// The permutation, when present, is staged once per CTA as an int16 table (pad -> k, the
-// zero sentinel column of every row slot).
+// total).  Each team keeps S row slots in shared memory filled by 1-D TMA bulk copies (one
+// instruction per row; per-thread loads through L1 cap the bytes in flight per SM and left
+// HBM at ~2 TB/s), so rows j+1 .. j+S-1 stream in while row j is rounded.  Teams are either
+// four independent warps per CTA (rows of <= 2048 values; lane 0 refills its own slots) or
+// one CTA of W consumer warps -- the count that splits the row's 16-byte chunks evenly --
+// plus a producer warp that refills slots as the consumers release them (full/empty
+// mbarriers).  A one-CTA team combines its per-warp |x| maxima through mbarriers one row
+// ahead: each warp publishes row j+1's partial maximum before rounding row j, so no
+// CTA-wide barrier sits on the row loop (4 partial buffers: a warp runs at most three rows
+// ahead of the slowest reader).  The permutation, when present, is staged once per CTA as an
+// int16 table (pad -> k, the zero sentinel column of every row slot).
 constexpr int kK1Parts = 4;
 
-template <int S, bool kStatic, bool kGather, bool kWarpTeams>
-__global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
+// Out-of-line repair of the chunks a thread flagged in its streaming loop (bit i = its
+// i-th chunk / step): recompute the fast codes, decide the values within the tie guard
+// exactly (act_fix_chunk), then values only the f64 division decides, and store again.
+// Kept out of the loop so the hot path stays a short straight-line body.
+template <bool kStatic, bool kGather>
+__device__ __noinline__ void act_fix_flagged(const uint16_t* srow, const int16_t* gidx,
+                                             int8_t* qr, int tt, int T, uint32_t flagged,
+                                             ActScale sc, double s64, int qmax) {
+  constexpr int N = kGather ? 4 : 8;
+  while (flagged) {
+    const int i = __ffs(flagged) - 1;
+    flagged &= flagged - 1;
+    const int c0 = (tt + i * T) * N;
+    uint16_t hv[N];
+    uint32_t c[N];
+    float dmax = 0.f;
+#pragma unroll
+    for (int e = 0; e < N; ++e) hv[e] = srow[kGather ? gidx[c0 + e] : c0 + e];
+#pragma unroll
+    for (int e = 0; e < N; e += 2)
+      act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[e]) << 16),
+                          __uint_as_float(static_cast<uint32_t>(hv[e + 1]) << 16), sc, c[e],
+                          c[e + 1], dmax);
+    bool rescan = false;
+    act_fix_chunk<kStatic, N, false>(hv, c, sc, s64, qmax, rescan);
+    if (rescan) act_fix_chunk<kStatic, N, true>(hv, c, sc, s64, qmax, rescan);
+#pragma unroll
+    for (int e = 0; e < N; ++e) qr[c0 + e] = static_cast<int8_t>(c[e]);
+  }
+}
+
+template <int S, int W, bool kWarpTeams>
+struct K1Shape {
+  static constexpr int kTeams = kWarpTeams ? 4 : 1;
+  static constexpr int kConsumers = kWarpTeams ? 32 : 32 * W;  // rounding threads per team
+  static constexpr int kThreads = kWarpTeams ? 128 : 32 * (W + 1);
+  static constexpr int kMinBlocks = kWarpTeams ? 8 : (1024 / kThreads > 0 ? 1024 / kThreads : 1);
+};
+
+// kRowMax (one-CTA teams, no gather): |x|max comes from row_absmax (written by the
+// producing GEMM's epilogue) instead of a reduction, so consumer warps never wait on one
+// another; the producer warp resets each row's entry once every consumer released it.
+template <int S, int W, bool kStatic, bool kGather, bool kWarpTeams, bool kRowMax = false>
+__global__ void __launch_bounds__(K1Shape<S, W, kWarpTeams>::kThreads,
+                                  K1Shape<S, W, kWarpTeams>::kMinBlocks)
     quant_act_rows_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
                           const int32_t* __restrict__ gather, int k_out, double static_scale,
-                          int qmax, int8_t* __restrict__ q, int64_t ldq,
+                          int qmax, double rqmax, int8_t* __restrict__ q, int64_t ldq,
                           float* __restrict__ s32_out, double* __restrict__ s64_out,
                           unsigned long long* __restrict__ err,
-                          unsigned long long* __restrict__ trace) {
-  constexpr int kTeams = kWarpTeams ? 4 : 1;
-  constexpr int kMaxWarps = kWarpTeams ? 1 : 8;
-  extern __shared__ __align__(16) uint16_t k1_smem[];
-  __shared__ uint32_t part[kK1Parts][kMaxWarps];
+                          unsigned long long* __restrict__ trace, int dbg,
+                          uint32_t* __restrict__ row_absmax) {
+  static_assert(!kRowMax || (!kWarpTeams && !kGather && !kStatic),
+                "row_absmax mode: per-token, one-CTA teams, no gather");
+  using Sh = K1Shape<S, W, kWarpTeams>;
+  constexpr int kTeams = Sh::kTeams;
+  constexpr int T = Sh::kConsumers;
+  extern __shared__ __align__(128) uint16_t k1_smem[];
+  __shared__ uint32_t part[kK1Parts][kWarpTeams ? 1 : W];
   __shared__ __align__(8) uint64_t pbar[kK1Parts];
+  __shared__ __align__(8) uint64_t full[kTeams][S];
+  __shared__ __align__(8) uint64_t empty[S];
   if (trace && threadIdx.x == 0) {  // diagnostics (QARVD_K1_TRACE): CTA start time and SM
     unsigned long long t;
     uint32_t smid;
@@ -422,30 +461,33 @@ __global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
     trace[3 * blockIdx.x] = t;
     trace[3 * blockIdx.x + 2] = smid;
   }
-  const int T = kWarpTeams ? 32 : static_cast<int>(blockDim.x);
   const int team = kWarpTeams ? static_cast<int>(threadIdx.x >> 5) : 0;
   const int tt = kWarpTeams ? static_cast<int>(threadIdx.x & 31) : static_cast<int>(threadIdx.x);
-  const int warp = tt >> 5, lane = threadIdx.x & 31, nwarps = T >> 5;
+  const int warp = tt >> 5, lane = threadIdx.x & 31;
   const int nvec = k >> 3;
-  const int row_stride = k + 8;  // + 8 zero sentinels read by pad slots
+  const int row_stride = (k + 8 + 63) & ~63;  // + 8 zero sentinels; 128-byte aligned slots
+  const uint32_t row_bytes = static_cast<uint32_t>(k) * 2u;
   uint16_t* slots = k1_smem + team * S * row_stride;
   int16_t* gidx = reinterpret_cast<int16_t*>(k1_smem + kTeams * S * row_stride);
   const int64_t step = static_cast<int64_t>(gridDim.x) * kTeams;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kTeams + team;
+  const int nrows = row0 < m ? static_cast<int>((m - 1 - row0) / step + 1) : 0;
 
-  auto issue = [&](int64_t r, int slot) {
-    if (r < m) {
-      const uint16_t* src = x + r * ldx;
-      uint16_t* dst = slots + slot * row_stride;
-      for (int vi = tt; vi < nvec; vi += T) cp_async16(dst + vi * 8, src + vi * 8);
-    }
-    cp_async_commit();
+  auto load_row = [&](int j) {  // one lane: stream row j of this team into its slot
+    const int s = j % S;
+    ptx::mbar_expect_tx(&full[team][s], row_bytes);
+    ptx::bulk_load_1d(slots + s * row_stride, x + (row0 + static_cast<int64_t>(j) * step) * ldx,
+                      row_bytes, &full[team][s]);
+  };
+  auto wait_full = [&](int j) {
+    ptx::mbar_wait_spin(&full[team][j % S], static_cast<uint32_t>((j / S) & 1));
   };
   // |x| max of this thread's chunks as packed 16-bit max of the sign-cleared bf16 bits
   // (non-finite values are exactly the magnitudes >= 0x7f80), reduced over the warp
   auto warp_part_max = [&](int slot) -> uint32_t {
     const uint16_t* srow = slots + slot * row_stride;
     uint32_t mx = 0;
+#pragma unroll 4
     for (int vi = tt; vi < nvec; vi += T) {
       const uint4 d = *reinterpret_cast<const uint4*>(srow + vi * 8);
       mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
@@ -453,19 +495,25 @@ __global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
     }
     return __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
   };
-  auto publish = [&](int64_t j) {  // this warp's partial max of row j (its copies landed)
-    const uint32_t pm = warp_part_max(static_cast<int>(j % S));
+  auto publish = [&](int j) {  // this warp's partial max of row j (landed)
+    const uint32_t pm = warp_part_max(j % S);
     if (lane == 0) part[j % kK1Parts][warp] = pm;
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&pbar[j % kK1Parts]);
   };
 
-  if (!kWarpTeams && threadIdx.x == 0) {
-    for (int b = 0; b < kK1Parts; ++b) ptx::mbar_init(&pbar[b], nwarps);
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < kTeams; ++t)
+      for (int s = 0; s < S; ++s) ptx::mbar_init(&full[t][s], 1);
+    for (int s = 0; s < S; ++s) ptx::mbar_init(&empty[s], W);
+    for (int b = 0; b < kK1Parts; ++b) ptx::mbar_init(&pbar[b], W);
     ptx::fence_mbar_init();
   }
-#pragma unroll
-  for (int s = 0; s < S; ++s) issue(row0 + s * step, s);
+  __syncthreads();
+  // the first rows stream in while the permutation table is staged
+  const bool producer = kWarpTeams ? lane == 0 : (warp == W && lane == 0);
+  if (producer)
+    for (int j = 0; j < S && j < nrows; ++j) load_row(j);
   if (kGather) {  // k_out % 16 == 0 and gather 16-byte aligned (launch_rows)
 #pragma unroll 4
     for (int c4 = threadIdx.x; c4 < (k_out >> 2); c4 += blockDim.x) {
@@ -482,30 +530,204 @@ __global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
     for (int s = 0; s < S; ++s) slots[s * row_stride + k + tt] = 0;
   }
   __syncthreads();
-  if (!kWarpTeams && row0 < m) {
-    cp_async_wait_group<S - 1>();  // row 0 landed
-    publish(0);
-  }
 
-  int64_t j = 0;
-  for (int64_t row = row0; row < m; ++j, row += step) {
-    const int slot = static_cast<int>(j % S);
-    const uint16_t* srow = slots + slot * row_stride;
-    uint32_t mag;
-    if (kWarpTeams) {
-      cp_async_wait_group<S - 1>();  // row j landed
-      __syncwarp();
-      mag = warp_part_max(slot);
-    } else {
-      if (row + step < m) {
-        cp_async_wait_group<S - 2>();  // row j+1 landed
-        publish(j + 1);
+  if (!kWarpTeams && warp == W) {
+    // producer warp: refill each slot once all consumer warps released it
+    if (lane == 0) {
+      for (int j = S; j < nrows; ++j) {
+        ptx::mbar_wait_spin(&empty[j % S], static_cast<uint32_t>((j / S - 1) & 1));
+        if (kRowMax) row_absmax[row0 + static_cast<int64_t>(j - S) * step] = 0u;
+        load_row(j);
       }
-      ptx::mbar_wait(&pbar[j % kK1Parts], static_cast<uint32_t>((j / kK1Parts) & 1));
-      mag = 0;
-      for (int w = 0; w < nwarps; ++w) mag = max(mag, part[j % kK1Parts][w]);
+      if (kRowMax)  // the last rows' entries, once their slots are released
+        for (int j = nrows > S ? nrows - S : 0; j < nrows; ++j) {
+          ptx::mbar_wait_spin(&empty[j % S], static_cast<uint32_t>((j / S) & 1));
+          row_absmax[row0 + static_cast<int64_t>(j) * step] = 0u;
+        }
     }
+  } else {
+    if (!kWarpTeams && !kRowMax && nrows > 0) {
+      wait_full(0);
+      publish(0);
+    }
+    for (int j = 0; j < nrows; ++j) {
+      const int64_t row = row0 + static_cast<int64_t>(j) * step;
+      const int slot = j % S;
+      const uint16_t* srow = slots + slot * row_stride;
+      uint32_t mag;
+      if (kWarpTeams) {
+        wait_full(j);
+        mag = warp_part_max(slot);
+      } else if (kRowMax) {
+        mag = kStatic ? 0u : __ldcg(row_absmax + row);
+        wait_full(j);
+      } else {
+        if (j + 1 < nrows) {
+          wait_full(j + 1);
+          publish(j + 1);
+        }
+        ptx::mbar_wait_spin(&pbar[j % kK1Parts], static_cast<uint32_t>((j / kK1Parts) & 1));
+        mag = 0;
+#pragma unroll
+        for (int w = 0; w < (kWarpTeams ? 1 : W); ++w) mag = max(mag, part[j % kK1Parts][w]);
+      }
 
+      const bool row_bad = mag >= 0x7f80u;
+      const float amax = __uint_as_float(mag << 16);
+      ActScale sc;
+      sc.fq = static_cast<float>(qmax);
+      if (kStatic) {
+        const GroupScale g = scale_static(static_scale);
+        sc.r = g.r32;
+        sc.exact = g.exact;
+        sc.s64 = static_scale;
+      } else {
+        // r = fl(fl(1/amax) * qmax): within 2^-23 of qmax/amax, inside the tie guard's margin
+        sc.r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+        sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
+        sc.s64 = 0.0;
+      }
+      // s64 = fl64(amax / qmax) (quant.cpp:168-181) as y = amax * fl64(1/qmax) plus one fma
+      // correction -- equal to the correctly rounded quotient for every bf16 amax and every
+      // qmax of 2..8 bits (checked exhaustively, tests/test_oracle.py)
+      auto row_s64 = [&]() -> double {
+        if (kStatic) return static_scale;
+        if (!(amax > 0.f)) return DBL_MIN;
+        const double a = static_cast<double>(amax), y = a * rqmax;
+        return fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
+      };
+      if (tt == T - 1) {
+        const double s = row_s64();
+        if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s) : 0.f;
+        if (s64_out) s64_out[row] = s;
+      }
+      int8_t* qr = q + row * ldq;
+      auto src_of = [&](int c) -> int { return kGather ? gidx[c] : c; };
+
+      if (dbg & 1) {
+        // diagnostics: no codes
+      } else if (row_bad || sc.exact) {
+        // rare rows: a non-finite input (reported; the reference throws) or an unusable
+        // fp32 reciprocal -- every code takes the exact path
+        const double s64 = row_s64();
+        for (int c = tt; c < k_out; c += T)
+          qr[c] = static_cast<int8_t>(act_code_slow(srow[src_of(c)], s64, qmax, err, row * k_out + c));
+      } else {
+        // Fast codes.  A chunk holding a value within the tie guard sets its bit in
+        // `flagged` and is repaired after the loop (act_fix_flagged).
+        const double s64 = row_s64();
+        uint32_t flagged = 0;
+        if (!kGather) {
+          int i = 0;
+#pragma unroll 2
+          for (int vi = tt; vi < nvec; vi += T, ++i) {
+            const uint4 d = *reinterpret_cast<const uint4*>(srow + vi * 8);
+            const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+            uint32_t c[8];
+            float dmax = 0.f;
+            if (dbg & 4) {  // diagnostics: trivial codes (isolates the rounding math)
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                c[2 * h] = w[h] >> 8;
+                c[2 * h + 1] = w[h] >> 24;
+              }
+            } else {
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u),
+                                  sc, c[2 * h], c[2 * h + 1], dmax);
+            }
+            flagged |= static_cast<uint32_t>(dmax > tie_guard<kStatic>()) << i;
+            const uint2 st = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+            if (!(dbg & 2) || st.x == 0x12345678u) *reinterpret_cast<uint2*>(qr + vi * 8) = st;
+          }
+        } else {
+          // 4 consecutive codes per lane per step: neighbouring lanes read shared memory
+          // 8 bytes apart (at most 2-way bank conflicts for a near-contiguous gather) and
+          // write one coalesced 4-byte word each
+          int i = 0;
+#pragma unroll 4
+          for (int c0 = tt * 4; c0 < k_out; c0 += T * 4, ++i) {
+            const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+            const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu],
+                                    srow[gp.y >> 16]};
+            uint32_t c[4];
+            float dmax = 0.f;
+            act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                                __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
+            act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                                __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
+            flagged |= static_cast<uint32_t>(dmax > tie_guard<kStatic>()) << i;
+            *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
+          }
+        }
+        if (flagged) act_fix_flagged<kStatic, kGather>(srow, gidx, qr, tt, T, flagged, sc, s64, qmax);
+      }
+      // release the slot: the team's lane 0 (warp teams) or the producer warp refills it
+      __syncwarp();
+      if (kWarpTeams) {
+        if (lane == 0 && j + S < nrows) load_row(j + S);
+      } else if (lane == 0) {
+        ptx::mbar_arrive(&empty[slot]);
+      }
+    }
+  }
+  if (trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[3 * blockIdx.x + 1] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming K1 for rows already in plan order whose |x|max is known: per-token rows whose
+// producer GEMM wrote row_absmax in its epilogue (qarvd_dual_gemm_rowmax; the chain folds
+// the permutation into that producer, pipeline.QuantizedChain), or a static scale.  Every
+// 16-byte chunk is then independent: one CTA per row (grid-stride), threads stride over the
+// row's chunks, no barrier between load and store.  A per-token row's row_absmax entry is
+// reset to 0 once the row is done, ready for the producer's next step.
+template <bool kStatic>
+__device__ __noinline__ void act_fix_flagged_global(const uint16_t* xr, int8_t* qr, int tid, int nthr,
+                                                    uint32_t flagged, ActScale sc, double s64,
+                                                    int qmax) {
+  while (flagged) {
+    const int i = __ffs(flagged) - 1;
+    flagged &= flagged - 1;
+    const int c0 = (tid + i * nthr) * 8;
+    uint16_t hv[8];
+    uint32_t c[8];
+    float dmax = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) hv[e] = xr[c0 + e];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2)
+      act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[e]) << 16),
+                          __uint_as_float(static_cast<uint32_t>(hv[e + 1]) << 16), sc, c[e],
+                          c[e + 1], dmax);
+    bool rescan = false;
+    act_fix_chunk<kStatic, 8, false>(hv, c, sc, s64, qmax, rescan);
+    if (rescan) act_fix_chunk<kStatic, 8, true>(hv, c, sc, s64, qmax, rescan);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qr[c0 + e] = static_cast<int8_t>(c[e]);
+  }
+}
+
+constexpr int kStreamThreads = 256;
+
+template <bool kStatic>
+__global__ void __launch_bounds__(kStreamThreads, 4)
+    quant_act_stream_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                            uint32_t* __restrict__ row_absmax, double static_scale, int qmax,
+                            double rqmax, int8_t* __restrict__ q, int64_t ldq,
+                            float* __restrict__ s32_out, double* __restrict__ s64_out,
+                            unsigned long long* __restrict__ err) {
+  const int nvec = k >> 3;
+  const int tid = threadIdx.x;
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const uint32_t mag = kStatic ? 0u : __ldcg(row_absmax + row);
     const bool row_bad = mag >= 0x7f80u;
     const float amax = __uint_as_float(mag << 16);
     ActScale sc;
@@ -516,123 +738,71 @@ __global__ void __launch_bounds__(kWarpTeams ? 128 : 256, kWarpTeams ? 8 : 4)
       sc.exact = g.exact;
       sc.s64 = static_scale;
     } else {
-      sc.r = amax > 0.f ? __fdiv_rn(static_cast<float>(qmax), amax) : 0.f;
+      sc.r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
       sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
       sc.s64 = 0.0;
     }
-    auto row_s64 = [&]() -> double {
-      return kStatic ? static_scale
-                     : (amax > 0.f ? __ddiv_rn(static_cast<double>(amax), static_cast<double>(qmax))
-                                   : DBL_MIN);
-    };
-    // the scale outputs come from the team's last thread (the first runs the row-ahead
-    // publish on the critical path)
-    if (tt == T - 1) {
-      const double s = row_s64();
-      if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s) : 0.f;
-      if (s64_out) s64_out[row] = s;
+    double s64;
+    if (kStatic) {
+      s64 = static_scale;
+    } else if (!(amax > 0.f)) {
+      s64 = DBL_MIN;
+    } else {  // fl64(amax / qmax), see quant_act_rows_kernel
+      const double a = static_cast<double>(amax), y = a * rqmax;
+      s64 = fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
     }
+    if (tid == 0) {
+      if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s64) : 0.f;
+      if (s64_out) s64_out[row] = s64;
+    }
+    const uint16_t* xr = x + row * ldx;
     int8_t* qr = q + row * ldq;
-    auto src_of = [&](int c) -> int { return kGather ? gidx[c] : c; };
-
     if (row_bad || sc.exact) {
-      // rare rows: a non-finite input (reported; the reference throws) or an unusable
-      // fp32 reciprocal -- every code takes the exact path
-      const double s64 = row_s64();
-      for (int c = tt; c < k_out; c += T)
-        qr[c] = static_cast<int8_t>(act_code_slow(srow[src_of(c)], s64, qmax, err, row * k_out + c));
-    } else {
-      // Fast codes.  A chunk holding a value within the tie guard is patched in place
-      // (act_fix_chunk: one f64 fma per flagged value) before its store.
-      double s64 = 0.0;
-      bool have_s64 = false, rescan = false;
-      auto lazy_s64 = [&]() {
-        if (!have_s64) {
-          s64 = row_s64();
-          have_s64 = true;
-        }
-        return s64;
-      };
-      if (!kGather) {
-#pragma unroll 2
-        for (int vi = tt; vi < nvec; vi += T) {
-          const uint4 d = *reinterpret_cast<const uint4*>(srow + vi * 8);
-          const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-          uint32_t c[8];
-          float dmax = 0.f;
-#pragma unroll
-          for (int h = 0; h < 4; ++h)
-            act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u),
-                                sc, c[2 * h], c[2 * h + 1], dmax);
-          if (dmax > tie_guard<kStatic>()) {
-            const uint16_t hv[8] = {static_cast<uint16_t>(w[0]), static_cast<uint16_t>(w[0] >> 16),
-                                    static_cast<uint16_t>(w[1]), static_cast<uint16_t>(w[1] >> 16),
-                                    static_cast<uint16_t>(w[2]), static_cast<uint16_t>(w[2] >> 16),
-                                    static_cast<uint16_t>(w[3]), static_cast<uint16_t>(w[3] >> 16)};
-            act_fix_chunk<kStatic, 8, false>(hv, c, sc, lazy_s64(), qmax, rescan);
-          }
-          *reinterpret_cast<uint2*>(qr + vi * 8) =
-              make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
-        }
-      } else {
-        // 4 consecutive codes per lane per step: neighbouring lanes read shared memory
-        // 8 bytes apart (at most 2-way bank conflicts for a near-contiguous gather) and
-        // write one coalesced 4-byte word each
-#pragma unroll 4
-        for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
-          const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
-          const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu],
-                                  srow[gp.y >> 16]};
-          uint32_t c[4];
-          float dmax = 0.f;
-          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
-                              __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
-          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
-                              __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
-          if (dmax > tie_guard<kStatic>())
-            act_fix_chunk<kStatic, 4, false>(hv, c, sc, lazy_s64(), qmax, rescan);
-          *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
-        }
+      // a non-finite input (reported; the reference throws) or an unusable fp32 reciprocal
+      for (int c = tid; c < k; c += kStreamThreads) {
+        const uint16_t h = xr[c];
+        // a static-scale row has no |x|max: its non-finite values surface here per value
+        qr[c] = static_cast<int8_t>(act_code_slow(h, s64, qmax, err, row * k + c));
       }
-      if (rescan) {  // (very rare) values only the f64 division decides: redo this thread's codes
-        if (!kGather) {
-          for (int vi = tt; vi < nvec; vi += T) {
-            uint16_t hv[8];
-            uint32_t c[8];
-            for (int e = 0; e < 8; ++e) {
-              hv[e] = srow[vi * 8 + e];
-              c[e] = static_cast<uint32_t>(qr[vi * 8 + e]);
-            }
-            act_fix_chunk<kStatic, 8, true>(hv, c, sc, s64, qmax, rescan);
-            for (int e = 0; e < 8; ++e) qr[vi * 8 + e] = static_cast<int8_t>(c[e]);
+    } else {
+      uint32_t flagged = 0;
+      int i = 0;
+#pragma unroll 4
+      for (int vi = tid; vi < nvec; vi += kStreamThreads, ++i) {
+        const uint4 d = ldg_stream(reinterpret_cast<const uint4*>(xr) + vi);
+        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+        uint32_t c[8];
+        float dmax = 0.f;
+        if (kStatic) {  // no |x|max: non-finite values are caught per chunk
+          const uint32_t mx = __vmaxu2(__vmaxu2(w[0] & 0x7fff7fffu, w[1] & 0x7fff7fffu),
+                                       __vmaxu2(w[2] & 0x7fff7fffu, w[3] & 0x7fff7fffu));
+          if (max(mx & 0xffffu, mx >> 16) >= 0x7f80u) dmax = 1.f;
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc,
+                              c[2 * h], c[2 * h + 1], dmax);
+        flagged |= static_cast<uint32_t>(dmax > tie_guard<kStatic>()) << i;
+        *reinterpret_cast<uint2*>(qr + vi * 8) =
+            make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+      }
+      if (flagged) {
+        if (kStatic) {  // flagged static chunks: exact per value (also reports non-finite ones)
+          while (flagged) {
+            const int b = __ffs(flagged) - 1;
+            flagged &= flagged - 1;
+            const int c0 = (tid + b * kStreamThreads) * 8;
+            for (int e = 0; e < 8; ++e)
+              qr[c0 + e] = static_cast<int8_t>(act_code_slow(xr[c0 + e], s64, qmax, err, row * k + c0 + e));
           }
         } else {
-          for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
-            uint16_t hv[4];
-            uint32_t c[4];
-            for (int e = 0; e < 4; ++e) {
-              hv[e] = srow[src_of(c0 + e)];
-              c[e] = static_cast<uint32_t>(qr[c0 + e]);
-            }
-            act_fix_chunk<kStatic, 4, true>(hv, c, sc, s64, qmax, rescan);
-            for (int e = 0; e < 4; ++e) qr[c0 + e] = static_cast<int8_t>(c[e]);
-          }
+          act_fix_flagged_global<kStatic>(xr, qr, tid, kStreamThreads, flagged, sc, s64, qmax);
         }
       }
     }
-    // refill this slot with row j+S (a gathered row is read by the whole team first)
-    if (kGather) {
-      if (kWarpTeams) __syncwarp();
-      else __syncthreads();
-    }
-    issue(row + S * step, slot);
-  }
-  if (trace) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[3 * blockIdx.x + 1] = t;
+    if (!kStatic) {
+      __syncthreads();  // every thread has read row_absmax[row]
+      if (tid == 0) row_absmax[row] = 0u;
     }
   }
 }
@@ -711,27 +881,26 @@ int grid_for_rows(int64_t m) {
   return static_cast<int>(ctas < cap ? ctas : cap);
 }
 
-template <int S, bool kStatic, bool kGather, bool kWarpTeams>
-int launch_act_rows_t(int threads, const uint16_t* x, int64_t m, int k, int64_t ldx,
-                      const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
-                      int64_t ldq, float* s32, double* s64, unsigned long long* err,
-                      cudaStream_t stream) {
-  constexpr int kTeams = kWarpTeams ? 4 : 1;
-  auto kern = quant_act_rows_kernel<S, kStatic, kGather, kWarpTeams>;
+template <int S, int W, bool kStatic, bool kGather, bool kWarpTeams>
+int launch_act_rows_t(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather,
+                      int k_out, double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32,
+                      double* s64, unsigned long long* err, cudaStream_t stream) {
+  constexpr int kTeams = K1Shape<S, W, kWarpTeams>::kTeams;
+  constexpr int kThreads = K1Shape<S, W, kWarpTeams>::kThreads;
+  auto kern = quant_act_rows_kernel<S, W, kStatic, kGather, kWarpTeams>;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [&] { attr = set_smem_attrs(kern, 110 * 1024); });
   QARVD_CUDA_TRY(attr);
-  const size_t smem = static_cast<size_t>(kTeams) * S * (k + 8) * 2 +
+  const size_t smem = static_cast<size_t>(kTeams) * S * ((k + 8 + 63) & ~63) * 2 +
                       (kGather ? static_cast<size_t>((k_out + 7) & ~7) * 2 : 0);
-  // persistent grid: as many CTAs as fit on the GPU (cached per launch shape)
+  // persistent grid: as many CTAs as fit on the GPU (cached per shared-memory size)
   static thread_local size_t cached_smem = 0;
-  static thread_local int cached_threads = 0, cached_blocks = 0;
-  if (cached_smem != smem || cached_threads != threads) {
+  static thread_local int cached_blocks = 0;
+  if (cached_smem != smem) {
     int nb = 0;
-    QARVD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
+    QARVD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
     cached_smem = smem;
-    cached_threads = threads;
     cached_blocks = nb > 0 ? nb : 1;
   }
   const int64_t need = (m + kTeams - 1) / kTeams;
@@ -742,16 +911,18 @@ int launch_act_rows_t(int threads, const uint16_t* x, int64_t m, int k, int64_t 
     const char* e = getenv("QARVD_K1_TRACE");
     return e ? reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0)) : nullptr;
   }();
-  kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(x, m, k, ldx, gather, k_out, static_scale,
-                                                             qmax, q, ldq, s32, s64, err, trace);
+  static const int dbg = getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
+      x, m, k, ldx, gather, k_out, static_scale, qmax, 1.0 / static_cast<double>(qmax), q, ldq, s32,
+      s64, err, trace, dbg, nullptr);
   return QARVD_OK;
 }
 
 // Team shape for a row of nvec 16-byte chunks: four one-warp teams per CTA for rows of up
 // to 256 chunks, else one CTA of 4..8 warps, the count that splits the chunks most evenly
 // (ties: more warps), e.g. 1120 chunks (K = 8960) -> 7 warps x 5 chunks per thread.
-inline int k1_team_threads(int nvec) {
-  if (nvec <= 256) return 32;
+inline int k1_team_warps(int nvec) {
+  if (nvec <= 256) return 1;
   int best_w = 8, best_waste = 1 << 30;
   for (int w = 8; w >= 4; --w) {
     const int per = (nvec + 32 * w - 1) / (32 * w);
@@ -761,7 +932,82 @@ inline int k1_team_threads(int nvec) {
       best_w = w;
     }
   }
-  return 32 * best_w;
+  return best_w;
+}
+
+template <int W>
+int launch_act_rowmax_ring(const uint16_t* x, int64_t m, int k, int64_t ldx, uint32_t* row_absmax,
+                           int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                           unsigned long long* err, cudaStream_t stream) {
+  constexpr int S = 4;
+  constexpr int kThreads = K1Shape<S, W, false>::kThreads;
+  auto kern = quant_act_rows_kernel<S, W, false, false, false, true>;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] { attr = set_smem_attrs(kern, 110 * 1024); });
+  QARVD_CUDA_TRY(attr);
+  const size_t smem = static_cast<size_t>(S) * ((k + 8 + 63) & ~63) * 2;
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_blocks = 0;
+  if (cached_smem != smem) {
+    int nb = 0;
+    QARVD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
+    cached_smem = smem;
+    cached_blocks = nb > 0 ? nb : 1;
+  }
+  const int64_t cap = static_cast<int64_t>(kNumSMs) * cached_blocks;
+  const int64_t grid = m < cap ? m : cap;
+  static const int dbg = getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
+      x, m, k, ldx, nullptr, k, 0.0, qmax, 1.0 / static_cast<double>(qmax), q, ldq, s32, s64, err,
+      nullptr, dbg, row_absmax);
+  return QARVD_OK;
+}
+
+int launch_act_rowmax(const uint16_t* x, int64_t m, int k, int64_t ldx, uint32_t* row_absmax,
+                      int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                      unsigned long long* err, cudaStream_t stream) {
+  switch (k1_team_warps(k / 8)) {
+    case 4: return launch_act_rowmax_ring<4>(x, m, k, ldx, row_absmax, qmax, q, ldq, s32, s64, err, stream);
+    case 5: return launch_act_rowmax_ring<5>(x, m, k, ldx, row_absmax, qmax, q, ldq, s32, s64, err, stream);
+    case 6: return launch_act_rowmax_ring<6>(x, m, k, ldx, row_absmax, qmax, q, ldq, s32, s64, err, stream);
+    case 7: return launch_act_rowmax_ring<7>(x, m, k, ldx, row_absmax, qmax, q, ldq, s32, s64, err, stream);
+    case 8: return launch_act_rowmax_ring<8>(x, m, k, ldx, row_absmax, qmax, q, ldq, s32, s64, err, stream);
+  }
+  QARVD_FAIL(QARVD_ERR_LOGIC, "unsupported K1 team size");
+}
+
+template <bool kStatic, bool kGather>
+int launch_act_rows_g(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather,
+                      int k_out, double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32,
+                      double* s64, unsigned long long* err, cudaStream_t stream) {
+  // warp teams: one slot (a 1-row-per-team grid keeps 8 CTAs per SM resident, so every row
+  // of a 4680-token step gets its own team in one wave); CTA teams: three
+  int w = k1_team_warps(k / 8), slots = w == 1 ? 1 : 3;
+  // diagnostics: QARVD_K1_SHAPE=<warps>x<slots> overrides the team shape of one-CTA teams
+  static const char* shape = getenv("QARVD_K1_SHAPE");
+  if (shape && w > 1) sscanf(shape, "%dx%d", &w, &slots);
+  const int key = w * 10 + slots;
+  switch (key) {
+#define QARVD_K1_CASE(WW, SS, TEAMS)                                                              \
+  case WW * 10 + SS:                                                                              \
+    return launch_act_rows_t<SS, WW, kStatic, kGather, TEAMS>(x, m, k, ldx, gather, k_out,       \
+                                                              static_scale, qmax, q, ldq, s32,   \
+                                                              s64, err, stream);
+    QARVD_K1_CASE(1, 1, true)
+    QARVD_K1_CASE(1, 2, true)
+    QARVD_K1_CASE(2, 2, false)
+    QARVD_K1_CASE(2, 3, false)
+    QARVD_K1_CASE(4, 2, false)
+    QARVD_K1_CASE(4, 3, false)
+    QARVD_K1_CASE(5, 3, false)
+    QARVD_K1_CASE(6, 3, false)
+    QARVD_K1_CASE(7, 2, false)
+    QARVD_K1_CASE(7, 3, false)
+    QARVD_K1_CASE(8, 3, false)
+#undef QARVD_K1_CASE
+  }
+  QARVD_FAIL(QARVD_ERR_LOGIC, "unsupported K1 team shape");
 }
 
 template <bool kStatic>
@@ -769,16 +1015,10 @@ int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t 
                     const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
                     int64_t ldq, float* s32, double* s64, unsigned long long* err,
                     cudaStream_t stream) {
-  const int threads = k1_team_threads(k / 8);
-  if (threads == 32)
-    return gathered ? launch_act_rows_t<2, kStatic, true, true>(128, x, m, k, ldx, gather, k_out, static_scale,
-                                                                qmax, q, ldq, s32, s64, err, stream)
-                    : launch_act_rows_t<2, kStatic, false, true>(128, x, m, k, ldx, gather, k_out, static_scale,
-                                                                 qmax, q, ldq, s32, s64, err, stream);
-  return gathered ? launch_act_rows_t<3, kStatic, true, false>(threads, x, m, k, ldx, gather, k_out,
-                                                               static_scale, qmax, q, ldq, s32, s64, err, stream)
-                  : launch_act_rows_t<3, kStatic, false, false>(threads, x, m, k, ldx, gather, k_out,
-                                                                static_scale, qmax, q, ldq, s32, s64, err, stream);
+  return gathered ? launch_act_rows_g<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
+                                                     ldq, s32, s64, err, stream)
+                  : launch_act_rows_g<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax,
+                                                      q, ldq, s32, s64, err, stream);
 }
 
 template <int MODE>
@@ -800,7 +1040,7 @@ int launch_rows(const void* x, int dtype, int64_t m, int64_t k, int64_t ldx, con
                        (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(gather) & 15) == 0;
   // shared memory of the team slots (+ int16 permutation table) must fit the 110 KB opt-in
-  const int64_t k1_smem = fast_ok ? ((k / 8 <= 256 ? 4 * 2 : 3) * (k + 8) * 2 +
+  const int64_t k1_smem = fast_ok ? ((k / 8 <= 256 ? 4 * 1 : 3) * ((k + 8 + 63) & ~int64_t(63)) * 2 +
                                      (gather ? ((k_out + 7) & ~int64_t(7)) * 2 : 0))
                                   : 0;
   if (fast_ok && k1_smem <= 110 * 1024) {
@@ -896,4 +1136,58 @@ extern "C" int qarvd_prepare_weights(const void* w, int w_dtype, int64_t n, int6
   return launch_rows<kWeightDual>(w, w_dtype, n, k, ldw, gather, k_pad, k_outlier, 0.0, bits, wq,
                                   ldq, scale_outlier_f32, scale_outlier_f64, scale_normal_f32,
                                   scale_normal_f64, err_index, as_stream(stream));
+}
+
+extern "C" int qarvd_quantize_act_rowmax(const uint16_t* x, int64_t m, int64_t k, int64_t ldx,
+                                         uint32_t* row_absmax, int granularity,
+                                         double static_scale, int bits, int8_t* xq, int64_t ldq,
+                                         float* scale_f32, double* scale_f64, int64_t* err_index,
+                                         void* stream) {
+  clear_error();
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (m < 0 || k <= 0 || ldx < k || ldq < k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "invalid shape or leading dimension");
+  if (k % 8 || ldx % 8 || ldq % 8 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(xq) & 7))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "quantize (rowmax): k, ldx, ldq must be multiples of 8 and x 16-byte aligned");
+  if (m > 0 && (!x || !xq)) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (granularity == QARVD_ACT_PER_TENSOR) {
+    if (!(static_scale > 0.0) || !(static_scale <= DBL_MAX))
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quant params: scale must be positive and finite");
+  } else if (granularity == QARVD_ACT_PER_TOKEN) {
+    if (!row_absmax) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize (rowmax): null row |x| max buffer");
+  } else {
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "unknown activation granularity");
+  }
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, s>>>(err);
+    count_launch();
+  }
+  if (m == 0) return QARVD_OK;
+  const int64_t cap = static_cast<int64_t>(kNumSMs) * 4;
+  const unsigned grid = static_cast<unsigned>(m < cap ? m : cap);
+  const bool ring = granularity == QARVD_ACT_PER_TOKEN && k / 8 > 256 &&
+                    4 * ((k + 8 + 63) & ~int64_t(63)) * 2 <= 110 * 1024 &&
+                    !getenv("QARVD_K1_STREAM");  // diagnostics: force the streaming kernel
+  if (ring) {
+    if (int st = launch_act_rowmax(x, m, static_cast<int>(k), ldx, row_absmax, qmax, xq, ldq,
+                                   scale_f32, scale_f64, err, s))
+      return st;
+  } else if (granularity == QARVD_ACT_PER_TOKEN)
+    quant_act_stream_kernel<false><<<grid, kStreamThreads, 0, s>>>(
+        x, m, static_cast<int>(k), ldx, row_absmax, 0.0, qmax, 1.0 / qmax, xq, ldq, scale_f32,
+        scale_f64, err);
+  else
+    quant_act_stream_kernel<true><<<grid, kStreamThreads, 0, s>>>(
+        x, m, static_cast<int>(k), ldx, nullptr, static_scale, qmax, 1.0 / qmax, xq, ldq,
+        scale_f32, scale_f64, err);
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  return QARVD_OK;
 }

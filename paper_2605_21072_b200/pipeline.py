@@ -63,11 +63,15 @@ def fold_output_permutation(producer: QuantizedLayer,
 class QuantizedChain:
     def __init__(self, layers: Sequence[QuantizedLayer], m: int,
                  epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None,
-                 fold: bool = True):
+                 fold: bool = True, fuse_rowmax: bool = False):
         """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1).
 
         With ``fold`` every intermediate consumed by exactly one layer is produced in that
         layer's plan order (fold_output_permutation), so its K1 runs without a gather.
+        With ``fuse_rowmax`` a folded consumer's per-token |x| max is reduced in the producer's
+        GEMM epilogue (qarvd_dual_gemm_rowmax) and its K1 streams (qarvd_quantize_act_rowmax);
+        off by default: on B200 the extra epilogue work costs the 1-TMEM-stage producer GEMM
+        more than the consumer saves (profiles/round1_k1.md).
         ``self.source_ops`` keeps the unfolded shapes for op counting."""
         self.layers = list(layers)
         self.m = m
@@ -79,6 +83,18 @@ class QuantizedChain:
                 if i >= 0 and self.inputs.count(i) == 1 and self.layers[j].gather_dev is not None:
                     self.layers[i], self.layers[j] = fold_output_permutation(self.layers[i], self.layers[j])
         dev = self.layers[0].wq.device
+        # A folded consumer of a single producer gets that producer's per-row |y| max from
+        # the producer's epilogue (qarvd_dual_gemm_rowmax) and quantizes with the streaming
+        # K1 (qarvd_quantize_act_rowmax), which also resets the buffer for the next step.
+        self.rowmax = [None] * len(self.layers)  # indexed by producer
+        self.stream_k1 = [False] * len(self.layers)  # indexed by consumer
+        if fold:
+            for j, i in enumerate(self.inputs):
+                L = self.layers[j]
+                if i >= 0 and L.gather_dev is None and self.inputs.count(i) == 1 and fuse_rowmax:
+                    self.stream_k1[j] = True
+                    if L.act_granularity == _lib.ACT_PER_TOKEN:
+                        self.rowmax[i] = torch.zeros(m, dtype=torch.int32, device=dev)
         self.x = torch.empty((m, self.layers[0].in_dim), dtype=torch.bfloat16, device=dev)
         self.xq = [torch.empty((m, L.k_pad), dtype=torch.int8, device=dev) for L in self.layers]
         self.sx = [torch.empty(m, dtype=torch.float32, device=dev) for _ in self.layers]
@@ -99,16 +115,28 @@ class QuantizedChain:
             events[0].record()
         for i, L in enumerate(self.layers):
             src = self._src(i)
-            _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
-                      src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
-                      float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
-                      None, None, s)
+            if self.stream_k1[i]:
+                rm = self.rowmax[self.inputs[i]]
+                _lib.call("qarvd_quantize_act_rowmax", src.data_ptr(), self.m, L.in_dim, src.stride(0),
+                          _ptr(rm), L.act_granularity, float(L.act_scale), 8, self.xq[i].data_ptr(),
+                          L.k_pad, self.sx[i].data_ptr(), None, None, s)
+            else:
+                _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
+                          src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
+                          float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
+                          None, None, s)
             if events is not None:
                 events[2 * i + 1].record()
-            _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
-                      self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
-                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
-                      self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
+            if self.rowmax[i] is not None:
+                _lib.call("qarvd_dual_gemm_rowmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
+                          L.k_pad, self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                          L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                          self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(), s)
+            else:
+                _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
+                          self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                          L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                          self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
             if events is not None:
                 events[2 * i + 2].record()
 

@@ -326,17 +326,19 @@ def test_chain_fold_bitexact(cuda, d, f, m, n0, n2):
     L0.bias = torch.linspace(-0.5, 0.5, f, device="cuda", dtype=torch.float32)
     xb, _ = bf16_values((m, d), seed=6, heavy_cols=p0.outlier_indices if n0 else None, gamma=4.0)
     outs = []
-    for fold in (False, True):
-        ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fold=fold)
+    for fold, fuse in ((False, False), (True, False), (True, True)):
+        ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fold=fold,
+                            fuse_rowmax=fuse)
         assert (ch.layers[1].gather_dev is None) == fold
         ch.x.copy_(to_dev_bf16(xb))
         ch.launch()
         torch.cuda.synchronize()
         outs.append((ch.xq[1].clone(), ch.sx[1].clone(), ch.output.clone()))
-    (q_a, s_a, y_a), (q_b, s_b, y_b) = outs
-    assert torch.equal(q_a, q_b)
-    assert torch.equal(s_a, s_b)
-    assert torch.equal(y_a.view(torch.int16), y_b.view(torch.int16))
+    (q_a, s_a, y_a) = outs[0]
+    for (q_b, s_b, y_b) in outs[1:]:
+        assert torch.equal(q_a, q_b)
+        assert torch.equal(s_a, s_b)
+        assert torch.equal(y_a.view(torch.int16), y_b.view(torch.int16))
     # and the C-ABI host chain over the folded layers agrees
     ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fold=True)
     hs = [engine.LinearHandle(ch.layers[0], qb.EPI_GELU), engine.LinearHandle(ch.layers[1])]
@@ -370,3 +372,81 @@ def test_k1_contiguous_ties(cuda, k):
     q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
     np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
     np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+
+
+# ---------------------------------------------------------------- chained producer / streaming K1
+def _rowmax_bits(y_bf16: torch.Tensor) -> np.ndarray:
+    return (dev_bits(y_bf16).astype(np.uint32) & 0x7FFF).max(axis=1)
+
+
+@pytest.mark.parametrize("m,n,k,n_out,epi", [(300, 8960, 1536, 32, qb.EPI_GELU), (77, 200, 160, 5, qb.EPI_NONE)])
+def test_k2_rowmax_matches_output(cuda, m, n, k, n_out, epi):
+    """qarvd_dual_gemm_rowmax: same y as qarvd_dual_gemm, plus the per-row max of |bf16 y| bits."""
+    plan, layer, xq, s32, s64, _, _ = _gemm_case(m, n, k, n_out, seed=m)
+    y_ref = engine.kernel_b_gemm_dequant(xq, s32, layer, epilogue=epi)
+    y = torch.empty_like(y_ref)
+    rm = torch.zeros(m, dtype=torch.int32, device="cuda")
+    for _ in range(2):  # accumulating twice over the same output leaves the max unchanged
+        qb._lib.call("qarvd_dual_gemm_rowmax", xq.data_ptr(), layer.k_pad, layer.wq.data_ptr(),
+                     layer.k_pad, m, n, layer.k_pad, layer.k_outlier, s32.data_ptr(),
+                     layer.scale_outlier32.data_ptr(), layer.scale_normal32.data_ptr(), None, epi,
+                     y.data_ptr(), n, rm.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
+    np.testing.assert_array_equal(rm.cpu().numpy().astype(np.uint32), _rowmax_bits(y_ref))
+
+
+@pytest.mark.parametrize("m,k", [(4680, 8960), (33, 200), (5, 1536)])
+def test_k1_stream_rowmax_bitexact(cuda, m, k):
+    """qarvd_quantize_act_rowmax == the gather-free qarvd_quantize_act; it resets row_absmax."""
+    bits, x64 = bf16_values((m, k), seed=m + k, heavy_cols=np.arange(3, k, 101))
+    x = to_dev_bf16(bits)
+    rm = torch.from_numpy((bits.astype(np.uint32) & 0x7FFF).max(axis=1).astype(np.int32)).cuda()
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    s32 = torch.empty(m, dtype=torch.float32, device="cuda")
+    qb._lib.call("qarvd_quantize_act_rowmax", x.data_ptr(), m, k, k, rm.data_ptr(), qb.ACT_PER_TOKEN,
+                 0.0, 8, xq.data_ptr(), k, s32.data_ptr(), s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    np.testing.assert_array_equal(s32.cpu().numpy(), s_ref.astype(np.float32))
+    assert int(rm.abs().sum().item()) == 0
+    # static scale (row_absmax unused)
+    s = 0.0123
+    qb._lib.call("qarvd_quantize_act_rowmax", x.data_ptr(), m, k, k, None, qb.ACT_PER_TENSOR, s, 8,
+                 xq.data_ptr(), k, None, None, None, None)
+    q_ref, _, _ = oracle.quantize_act(x64, None, per_token=False, static_scale=s)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+
+
+def test_k1_stream_rowmax_ties_and_nonfinite(cuda):
+    k = 256
+    r = np.random.default_rng(3)
+    rows = []
+    for i in range(40):
+        a = float(2.0 ** r.integers(-6, 6))
+        base = (np.arange(k, dtype=np.float64) % 255 - 127) * (a / 127.0) * 0.5
+        base[0] = a
+        rows.append(base)
+    rows.append(np.zeros(k))
+    bits = oracle.f32_to_bf16_bits(np.asarray(rows, dtype=np.float32))
+    x64 = oracle.bf16_bits_to_f64(bits)
+    m = len(rows)
+    rm = torch.from_numpy((bits.astype(np.uint32) & 0x7FFF).max(axis=1).astype(np.int32)).cuda()
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    x = to_dev_bf16(bits)
+    qb._lib.call("qarvd_quantize_act_rowmax", x.data_ptr(), m, k, k, rm.data_ptr(), qb.ACT_PER_TOKEN,
+                 0.0, 8, xq.data_ptr(), k, None, s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    bits[7, 30] = 0x7F80
+    bits[9, 3] = 0xFFC0
+    rm = torch.from_numpy((bits.astype(np.uint32) & 0x7FFF).max(axis=1).astype(np.int32)).cuda()
+    err = torch.empty(1, dtype=torch.int64, device="cuda")
+    qb._lib.call("qarvd_quantize_act_rowmax", to_dev_bf16(bits).data_ptr(), m, k, k, rm.data_ptr(),
+                 qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), k, None, None, err.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 7 * k + 30

@@ -239,3 +239,9 @@ def test_ref_toy_injection_columns_match_synth(ref_lib):
     cols = np.nonzero(np.isclose(ratio, 8.0).all(axis=0))[0]
     mine = np.sort(pick_outlier_columns(1, 10, w_base.shape[1], 0.05))
     np.testing.assert_array_equal(cols, mine)
+
+
+def test_device_row_scale_formula_is_correctly_rounded():
+    """K1 computes s = fl(amax/qmax) as amax*fl(1/qmax) + one fma correction (quantize.cu
+    row_s64); exhaustively equal to the division for every bf16 amax and bit width."""
+    assert oracle.row_scale_formula_mismatches() == 0
