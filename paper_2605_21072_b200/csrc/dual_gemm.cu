@@ -19,6 +19,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -28,8 +29,13 @@ namespace {
 
 constexpr int BM = 128;  // rows of the activation tile (one TMEM lane per row)
 constexpr int BK = 128;  // bytes (= int8 elements) of K per 128B-swizzle sub-tile (one TMA box)
-constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
-constexpr int kEpiWarps = 8;
+// 4 control warps + 16 epilogue warps (4 per TMEM lane quadrant).  The epilogue (dequant,
+// GELU, bf16 pack, stores) is latency-bound per warp, so it runs on as many warps as the
+// register file allows (96 registers x 640 threads) in 16-column chunks.
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int CW = 16;            // columns per epilogue chunk (one tcgen05.ld .32x32b.x16)
+constexpr int kYStageBytes = 32 * CW * 2;  // one warp's bf16 staging tile: 32 rows x 32 B
 
 // BN = output columns of the (pair) tile; CG = CTAs per MMA (1, or 2 = an SM pair
 // computing a 256-row tile, each CTA holding its 128 A rows and BN/2 B rows).
@@ -42,10 +48,11 @@ struct GemmCfg {
   static constexpr int kBSub = (BN / CG) * BK;    // one 128 B K sub-tile of this CTA's B
   static constexpr int kABytes = KS * kASub;
   static constexpr int kBBytes = KS * kBSub;
-  // y staging: 2 KB per epilogue warp, double-buffered unless the operand stages need the room
+  // y staging: one 32 x 16 bf16 tile per epilogue warp, double-buffered unless the operand
+  // stages need the room
   static constexpr int kYBufs = KS == 2 ? 1 : 2;
   static constexpr int kEpiBytes = 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales, 2 buffers*/ +
-                                   kEpiWarps * 2048 * kYBufs /*y staging*/;
+                                   kEpiWarps * kYStageBytes * kYBufs /*y staging*/;
   static constexpr int kStages = (227 * 1024 - kEpiBytes) / (kABytes + kBBytes) > 8
                                      ? 8
                                      : (227 * 1024 - kEpiBytes) / (kABytes + kBBytes);
@@ -140,11 +147,11 @@ __device__ __forceinline__ uint64_t gelu2(uint64_t v) {
 // Same per-element op order as the scalar form (oracle_epilogue_f32), on packed pairs;
 // specialised on (outlier slab?, bias?, gelu?) so every variant is straight-line code.
 template <bool HO, bool HB, bool GL>
-__device__ __forceinline__ void epi_math(uint32_t (&rn)[32], const uint32_t (&ro)[32],
+__device__ __forceinline__ void epi_math(uint32_t (&rn)[CW], const uint32_t (&ro)[CW],
                                          const float* scc, int bn, float sx) {
   const uint64_t sx2 = pk2(sx, sx);
 #pragma unroll
-  for (int e4 = 0; e4 < 8; ++e4) {
+  for (int e4 = 0; e4 < CW / 4; ++e4) {
     const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
     float4 so4 = sn4, sb4 = sn4;
     if (HO) so4 = reinterpret_cast<const float4*>(scc + bn)[e4];
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
   uint8_t* epi_ystage = sB + C::kStages * C::kBBytes;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * 2048 * C::kYBufs);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_ystage + kEpiWarps * kYStageBytes * C::kYBufs);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccStages;
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  __shared__ long long s_trace[5][32];  // QARVD_GEMM_TRACE: per-tile clocks of CTA 0
+  __shared__ long long s_trace[6][32];  // QARVD_GEMM_TRACE: per-tile clocks of CTA 0
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int cta_id = static_cast<int>(blockIdx.x) / CG;  // pair index
@@ -370,14 +377,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue: 8 warps, 2 per TMEM lane quadrant =====================
-    // Warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quadrant split
-    // the tile's 32-column chunks (even / odd).  Each tile's column scales are prefetched
-    // one tile ahead; bf16 results go through a 64B-swizzled staging tile and a TMA bulk
-    // tensor store.
+    // ===================== epilogue: 16 warps, 4 per TMEM lane quadrant =====================
+    // Warp w may only touch TMEM lanes 32*(w%4)..+31; the four warps of a quadrant take
+    // every fourth 16-column chunk.  Each tile's column scales are prefetched one tile
+    // ahead; bf16 results go through a 32B-swizzled staging tile and a TMA bulk tensor store.
+    constexpr int kSubs = kEpiWarps / 4;
     const int ew = warp - 4;
     const int q = warp & 3;
-    const int half = ew >> 2;
+    const int half = ew >> 2;  // this warp's chunk phase within its quadrant
     const int etid = ew * 32 + lane;
     const bool has_outlier = p.k_o > 0;
     const bool gelu = (p.epilogue & QARVD_EPI_GELU) != 0;
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool two_step = C::kAccStages == 1 && p.out_dtype != QARVD_F64 && !p.acc_n_dbg &&
                           !p.acc_o_dbg;
     const int epi_mode = (has_outlier ? 1 : 0) | (p.bias ? 2 : 0) | (gelu && !two_step ? 4 : 0);
-    uint8_t* ystage0 = epi_ystage + ew * 2048 * C::kYBufs;  // kYBufs x (32 rows x 64 B, SWIZZLE_64B)
+    uint8_t* ystage0 = epi_ystage + ew * kYStageBytes * C::kYBufs;  // kYBufs x (32 rows x 32 B, SWIZZLE_32B)
     int ybuf = 0, sbuf = 0;
     float pf_n = 0.f, pf_o = 0.f, pf_b = 0.f, pf_x = 0.f;
     auto prefetch = [&](int tt) {
@@ -412,23 +419,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // consumer's per-token K1 reads it instead of re-reducing the row (pipeline.QuantizedChain)
     uint32_t tile_mx = 0;
     // y (fp32 bits in rn) -> bf16 TMA store, or direct bf16 / f32 stores
-    auto store_chunk = [&](uint32_t (&rn)[32], int64_t row0, int64_t row, int64_t col0, int ncols) {
+    auto store_chunk = [&](uint32_t (&rn)[CW], int64_t row0, int64_t row, int64_t col0, int ncols) {
       if (p.use_tma_store) {
-        uint32_t pk[16];
+        uint32_t pk[CW / 2];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < CW / 2; ++e) {
           const __nv_bfloat162 h2 =
               __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
           pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
         }
         if (p.row_absmax) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < CW / 2; ++e) {
             const uint32_t keep = (2 * e + 1 < ncols ? 0x7fff7fffu : 0u) | (2 * e < ncols ? 0x7fffu : 0u);
             tile_mx = __vmaxu2(tile_mx, pk[e] & keep);
           }
         }
-        uint8_t* ystage = ystage0 + ybuf * 2048;
+        uint8_t* ystage = ystage0 + ybuf * kYStageBytes;
         if (C::kYBufs == 2) {
           ybuf ^= 1;
           if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
@@ -436,10 +443,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::bulk_wait_read0();
         }
         __syncwarp();
+        // SWIZZLE_32B: the 16-byte half index of row r is XORed with bit 7 of the row's
+        // byte offset (r >> 2 & 1), which also spreads a warp's 16-byte stores over all banks
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int phys = (i ^ ((lane >> 1) & 3)) << 4;
-          *reinterpret_cast<uint4*>(ystage + lane * 64 + phys) =
+        for (int i = 0; i < 2; ++i) {
+          const int phys = (i ^ ((lane >> 2) & 1)) << 4;
+          *reinterpret_cast<uint4*>(ystage + lane * 32 + phys) =
               make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
         ptx::fence_proxy_async_smem();
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (row < p.m && p.out_dtype == QARVD_BF16) {
         __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + col0;
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
+        for (int e = 0; e < CW; ++e)
           if (e < ncols) {
             const __nv_bfloat16 h = __float2bfloat16_rn(__uint_as_float(rn[e]));
             yr[e] = h;
@@ -459,15 +468,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       } else if (row < p.m) {
         float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy + col0;
-        if (ncols == 32 && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
+        if (ncols == CW && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0)) {
           float4* dst = reinterpret_cast<float4*>(yr);
 #pragma unroll
-          for (int v4 = 0; v4 < 8; ++v4)
+          for (int v4 = 0; v4 < CW / 4; ++v4)
             dst[v4] = make_float4(__uint_as_float(rn[4 * v4]), __uint_as_float(rn[4 * v4 + 1]),
                                   __uint_as_float(rn[4 * v4 + 2]), __uint_as_float(rn[4 * v4 + 3]));
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
+          for (int e = 0; e < CW; ++e)
             if (e < ncols) yr[e] = __uint_as_float(rn[e]);
         }
       }
@@ -491,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.m;
       tile_mx = 0;
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // scales visible to all epilogue warps
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // scales visible to all epilogue warps
       const long long te0 = clock64();
       ptx::mbar_wait(&tfull[acc], acc_phase);
       const long long te1 = clock64();
@@ -499,14 +508,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
       const uint32_t t_o = tmem_base + t_lane + static_cast<uint32_t>(acc * 2 * BN);
       const uint32_t t_n = t_o + BN;
+      // Fast path (the deployment case: two-step bf16 TMA stores, tile inside N, no debug
+      // outputs): compile-time chunk loops with the per-chunk checks hoisted to the tile.
+      const bool fast = two_step && p.use_tma_store && !p.row_absmax &&
+                        static_cast<int64_t>(n_blk + 1) * BN <= p.n;
+      if (fast) {
+        auto phase1 = [&](auto ho, auto hb) {
+          constexpr bool HO = decltype(ho)::value, HB = decltype(hb)::value;
+#pragma unroll
+          for (int i = 0; i < BN / CW / kSubs; ++i) {
+            const int c = half + i * kSubs;
+            uint32_t rn[CW], ro[CW];
+            ptx::tmem_ld16(t_n + c * CW, rn);
+            if (HO) ptx::tmem_ld16(t_o + c * CW, ro);
+            ptx::tmem_wait_ld();
+            epi_math<HO, HB, false>(rn, ro, sc + c * CW, BN, sx);
+            ptx::tmem_st16(t_o + c * CW, rn);  // fold y into acc_o's columns
+          }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if (has_outlier) {
+          if (p.bias) phase1(T_{}, T_{});
+          else phase1(T_{}, F_{});
+        } else {
+          if (p.bias) phase1(F_{}, T_{});
+          else phase1(F_{}, F_{});
+        }
+        ptx::tmem_wait_st();
+        release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
+        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
+          const int ti = (t - cta_id) / num_ctas;
+          if (ti < 32) s_trace[5][ti] = clock64();
+        }
+        auto phase2 = [&](auto gl) {
+          constexpr bool GL = decltype(gl)::value;
+#pragma unroll
+          for (int i = 0; i < BN / CW / kSubs; ++i) {
+            const int c = half + i * kSubs;
+            uint32_t rn[CW];
+            ptx::tmem_ld16(t_o + c * CW, rn);
+            ptx::tmem_wait_ld();
+            if (GL) {
+#pragma unroll
+              for (int e = 0; e < CW; e += 2) {
+                float y0, y1;
+                upk2(gelu2(pk2(__uint_as_float(rn[e]), __uint_as_float(rn[e + 1]))), y0, y1);
+                rn[e] = __float_as_uint(y0);
+                rn[e + 1] = __float_as_uint(y1);
+              }
+            }
+            store_chunk(rn, row0, row, static_cast<int64_t>(n_blk) * BN + c * CW, CW);
+          }
+        };
+        if (gelu) phase2(T_{});
+        else phase2(F_{});
+        release(&tofree[0]);  // acc_o free
+      } else {
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
-        const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+      for (int c = half; c < BN / CW; c += kSubs) {
+        const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * CW;
         if (col0 >= p.n) break;  // warp-uniform
-        const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
-        uint32_t rn[32], ro[32];
-        ptx::tmem_ld32(t_n + c * 32, rn);
-        if (has_outlier) ptx::tmem_ld32(t_o + c * 32, ro);
+        const int ncols = (p.n - col0) < CW ? static_cast<int>(p.n - col0) : CW;
+        uint32_t rn[CW], ro[CW];
+        ptx::tmem_ld16(t_n + c * CW, rn);
+        if (has_outlier) ptx::tmem_ld16(t_o + c * CW, ro);
         ptx::tmem_wait_ld();
         if (p.out_dtype == QARVD_F64) {
           // exact restatement of the reference epilogue: val = 0; val += (s_x*s_wo)*acc_o;
@@ -515,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const double sx64 = p.sx64[row];
             double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
+            for (int e = 0; e < CW; ++e) {
               if (e >= ncols) continue;
               double v = 0.0;
               if (has_outlier)
@@ -530,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (row_ok && p.acc_n_dbg) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
+          for (int e = 0; e < CW; ++e) {
             if (e >= ncols) continue;
             p.acc_n_dbg[row * p.n + col0 + e] = static_cast<int32_t>(rn[e]);
             if (p.acc_o_dbg)
@@ -538,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         {
-          const float* scc = sc + c * 32;
+          const float* scc = sc + c * CW;
           switch (epi_mode) {
             case 0: epi_math<false, false, false>(rn, ro, scc, BN, sx); break;
             case 1: epi_math<true, false, false>(rn, ro, scc, BN, sx); break;
@@ -550,23 +616,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             default: epi_math<true, true, true>(rn, ro, scc, BN, sx); break;
           }
         }
-        if (two_step) ptx::tmem_st32(t_o + c * 32, rn);  // fold y into acc_o's columns
+        if (two_step) ptx::tmem_st16(t_o + c * CW, rn);  // fold y into acc_o's columns
         else store_chunk(rn, row0, row, col0, ncols);
       }
       if (two_step) {
         ptx::tmem_wait_st();
         release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
+        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
+          const int ti = (t - cta_id) / num_ctas;
+          if (ti < 32) s_trace[5][ti] = clock64();
+        }
 #pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
-          const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+        for (int c = half; c < BN / CW; c += kSubs) {
+          const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * CW;
           if (col0 >= p.n) break;
-          const int ncols = (p.n - col0) < 32 ? static_cast<int>(p.n - col0) : 32;
-          uint32_t rn[32];
-          ptx::tmem_ld32(t_o + c * 32, rn);
+          const int ncols = (p.n - col0) < CW ? static_cast<int>(p.n - col0) : CW;
+          uint32_t rn[CW];
+          ptx::tmem_ld16(t_o + c * CW, rn);
           ptx::tmem_wait_ld();
           if (gelu) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
+            for (int e = 0; e < CW; e += 2) {
               float y0, y1;
               upk2(gelu2(pk2(__uint_as_float(rn[e]), __uint_as_float(rn[e + 1]))), y0, y1);
               rn[e] = __float_as_uint(y0);
@@ -580,6 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         release(&tempty[acc]);
         if (C::kAccStages == 1) release(&tofree[0]);
       }
+      }  // generic path
       if (p.row_absmax && row_ok)
         atomicMax(p.row_absmax + row, max(tile_mx & 0xffffu, tile_mx >> 16));
       {
@@ -604,9 +675,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nt = (p.num_tiles - cta_id + num_ctas - 1) / num_ctas;
     const long long t0 = s_trace[0][0];
     for (int i = 0; i < nt && i < 32; ++i)
-      printf("tile %2d: mma %7lld..%7lld  epi wait %7lld tfull %7lld done %7lld\n", i,
+      printf("tile %2d: mma %7lld..%7lld  epi wait %7lld tfull %7lld phase1 %7lld done %7lld\n", i,
              s_trace[0][i] - t0, s_trace[1][i] - t0, s_trace[2][i] - t0, s_trace[3][i] - t0,
-             s_trace[4][i] - t0);
+             s_trace[5][i] - t0, s_trace[4][i] - t0);
   }
   if (CG == 2) ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
@@ -649,16 +720,16 @@ int make_operand_tmap(CUtensorMap* map, const int8_t* base, int64_t rows, int64_
   return QARVD_OK;
 }
 
-// bf16 output [m x n] (ld elements), box 32 cols x 32 rows, 64B swizzle (epilogue staging)
+// bf16 output [m x n] (ld elements), box CW cols x 32 rows, 32B swizzle (epilogue staging)
 int make_y_tmap(CUtensorMap* map, void* y, int64_t m, int64_t n, int64_t ld) {
   auto encode = get_encode_fn();
   if (!encode) QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {CW, 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed with CUresult " + std::to_string(r));
@@ -723,25 +794,21 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   return QARVD_OK;
 }
 
-// Tile configuration (BN, CG).  QARVD_GEMM_BN=128|192|256 and QARVD_GEMM_CG=1|2 override.
+// Tile configuration (BN, CG, KS).  QARVD_GEMM_BN=128|192|256, QARVD_GEMM_CG=1|2 and
+// QARVD_GEMM_KS=1|2 override.  Default: SM-pair tiles of 256 x 256 with 256-byte K stages.
 // * BN = 256 halves the B traffic per MAC versus 128 but fits only one TMEM stage
-//   (2 accumulators x 256 columns), so its epilogue does not overlap the next tile.
-// * BN = 192 exists for N = 1536 (Wan qkv / ffn.2 outputs): 37 x 8 = 296 single-SM tiles
-//   at M = 4680 is exactly two waves on 148 SMs (BN = 256 gives 1.5 waves).
+//   (2 accumulators x 256 columns); the two-step release overlaps most of the epilogue.
+// * KS = 2 halves the MMA issuer's per-stage mbarrier waits, which the tensor pipe does not
+//   overlap: measured on the Wan FFN (M = 4680, bench.py), 256/2/2 beats the wave-exact
+//   192/1/1 on N = 1536 (57.5 vs 63.7 us) as well as on N = 8960.
 struct TileCfg {
   int bn, cg, ks;
 };
 TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
+  (void)m;
+  (void)n;
   (void)k;
   TileCfg c{256, 2, 2};
-  const int64_t sms = sm_count();
-  if (n % 192 == 0 && n <= 2048) {
-    const int64_t t192 = ((m + BM - 1) / BM) * (n / 192);
-    const int64_t t256 = ((m + 2 * BM - 1) / (2 * BM)) * ((n + 255) / 256);
-    const double eff192 = static_cast<double>(t192) / (((t192 + sms - 1) / sms) * sms);
-    const double eff256 = static_cast<double>(t256) / (((t256 + sms / 2 - 1) / (sms / 2)) * (sms / 2));
-    if (eff192 > eff256) c = TileCfg{192, 1, 1};
-  }
   if (const char* env = getenv("QARVD_GEMM_BN")) {
     const int v = atoi(env);
     if (v == 128 || v == 192 || v == 256) c.bn = v;

@@ -6,6 +6,7 @@ import paper_2605_21072_b200 as qb
 from paper_2605_21072_b200 import _lib, engine, synth
 M = 4680
 name, n, k, no = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+epi = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 spec = synth.LayerSpec(7, "l", n, k, M, no / k, 8.0)
 w = synth.synth_weight(spec, seed=1)
 plan = engine.build_plan("l", k, qb.analyze_layer("l", w).aligned_outliers)
@@ -16,7 +17,7 @@ y = torch.empty((M, n), dtype=torch.bfloat16, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 f = lambda: _lib.call("qarvd_dual_gemm", xq.data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad, M, n, L.k_pad,
                       L.k_outlier, sx.data_ptr(), L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(),
-                      None, 0, qb.BF16, y.data_ptr(), n, None, None, st)
+                      None, epi, qb.BF16, y.data_ptr(), n, None, None, st)
 f(); torch.cuda.synchronize()
 os.environ["QARVD_GEMM_TRACE"] = "1"
 print("=== trace", name, os.environ.get("QARVD_GEMM_CG"), os.environ.get("QARVD_GEMM_BN"), os.environ.get("QARVD_GEMM_DEBUG"))
