@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_double, c_int, c_int64, c_uint64, c_void_p, c_char_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqarvd_b200.so")
+LIB_PATH = os.environ.get("QARVD_B200_LIB") or os.path.join(_HERE, "libqarvd_b200.so")  # override: A/B builds
 
 # status codes (qarvd_b200.h)
 OK = 0

@@ -8,6 +8,8 @@
 #include <atomic>
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <string>
 
 #include "../../include/qarvd_b200.h"
@@ -48,6 +50,50 @@ constexpr int kNumSMs = 148;
 
 // Large-smem kernels all request the maximum shared-memory carveout, so consecutive
 // kernels of a pipeline never force an SM carveout reconfiguration between launches.
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic stream
+// serialisation attribute may start while its predecessor drains; it runs its prologue
+// (barrier init, TMEM allocation, tensor-map prefetch, table staging) and then waits in
+// pdl_wait() until the predecessor grid has completed and its writes are visible.
+// QARVD_PDL=0 launches without the attribute (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("QARVD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// cudaLaunchKernelEx with the PDL attribute (and an optional cluster dimension)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <typename Kernel>
 inline cudaError_t set_smem_attrs(Kernel kern, int dynamic_bytes) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

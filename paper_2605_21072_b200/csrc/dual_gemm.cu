@@ -209,6 +209,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   __shared__ long long s_trace[6][32];  // QARVD_GEMM_TRACE: per-tile clocks of CTA 0
+  __shared__ long long s_clk0;
+  __shared__ unsigned long long s_g0;
+  if (p.trace && threadIdx.x == 0) {
+    s_clk0 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_g0));
+  }
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int cta_id = static_cast<int>(blockIdx.x) / CG;  // pair index
@@ -238,6 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (CG == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: wait for the producer of xq / scale_x (PDL), then let the next kernel
+  // launch -- its CTAs only fit on SMs this grid has left
+  pdl_wait();
+  pdl_launch_dependents();
 
   const int num_kb = static_cast<int>((p.k + SK - 1) / SK);
   // one-stage TMEM: k-blocks holding outlier steps are issued last (see the MMA issuer)
@@ -323,32 +333,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d_n = d_o + BN;
         for (int i = 0; i < num_kb; ++i) {
           const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
+          // acc_o is needed only by the outlier steps: in the (last-issued) outlier block the
+          // normal steps go first and the wait for the epilogue's acc_o release sits right
+          // before the first outlier step
+          const bool wait_o = C::kAccStages == 1 && ko32 > 0 && kb == 0;
           if (C::kAccStages == 1) {
             if (kb == kb_first_n) ptx::mbar_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
-            if (ko32 > 0 && kb == 0) ptx::mbar_wait(&tofree[0], acc_phase ^ 1);  // acc_o free
             ptx::tc_fence_after();
           }
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (C::kABytes >> 4));
           const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (C::kBBytes >> 4));
-          if (lane == 0 && p.debug != 1) {
+          auto issue = [&](bool outlier_pass) {
+            if (lane == 0 && p.debug != 1) {
 #pragma unroll
-            for (int j = 0; j < SPB; ++j) {
-              const int s32 = kb * SPB + j;  // K=32 step index
-              if (s32 < k32) {
+              for (int j = 0; j < SPB; ++j) {
+                const int s32 = kb * SPB + j;  // K=32 step index
                 const bool outl = s32 < ko32;
-                const uint32_t d = outl ? d_o : d_n;
-                const uint32_t accumulate = (outl ? s32 == 0 : s32 == first_n) ? 0u : 1u;
-                // sub-tile j/4; +32 bytes along K inside the 128B swizzle row = +2 in the
-                // >>4 address field
-                const uint64_t ao = static_cast<uint64_t>((j >> 2) * (C::kASub >> 4) + 2 * (j & 3));
-                const uint64_t bo = static_cast<uint64_t>((j >> 2) * (C::kBSub >> 4) + 2 * (j & 3));
-                if (CG == 1) ptx::mma_i8(d, ad + ao, bd + bo, idesc, accumulate);
-                else ptx::mma_i8_2sm(d, ad + ao, bd + bo, idesc, accumulate);
+                if (s32 < k32 && outl == outlier_pass) {
+                  const uint32_t d = outl ? d_o : d_n;
+                  const uint32_t accumulate = (outl ? s32 == 0 : s32 == first_n) ? 0u : 1u;
+                  // sub-tile j/4; +32 bytes along K inside the 128B swizzle row = +2 in the
+                  // >>4 address field
+                  const uint64_t ao = static_cast<uint64_t>((j >> 2) * (C::kASub >> 4) + 2 * (j & 3));
+                  const uint64_t bo = static_cast<uint64_t>((j >> 2) * (C::kBSub >> 4) + 2 * (j & 3));
+                  if (CG == 1) ptx::mma_i8(d, ad + ao, bd + bo, idesc, accumulate);
+                  else ptx::mma_i8_2sm(d, ad + ao, bd + bo, idesc, accumulate);
+                }
               }
             }
+          };
+          issue(false);
+          if (wait_o) {
+            __syncwarp();
+            ptx::mbar_wait(&tofree[0], acc_phase ^ 1);  // acc_o free
+            ptx::tc_fence_after();
           }
+          issue(true);
           __syncwarp();
           if (lane == 0) {
             if (CG == 1) ptx::mma_commit(&empty[stage]);
@@ -672,6 +694,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    const long long c1 = clock64();
+    printf("effective SM clock over the kernel: %.0f MHz\n",
+           1e3 * static_cast<double>(c1 - s_clk0) / static_cast<double>(g1 - s_g0));
     const int nt = (p.num_tiles - cta_id + num_ctas - 1) / num_ctas;
     const long long t0 = s_trace[0][0];
     for (int i = 0; i < nt && i < 32; ++i)
@@ -776,19 +803,8 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   p.num_tiles = p.num_m_blks * p.num_n_blks;
   const int units = sm_count() / CG;
   const int grid = CG * (p.num_tiles < units ? p.num_tiles : units);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  QARVD_CUDA_TRY(cudaLaunchKernelEx(&cfg, dual_gemm_kernel<BN, CG, KS>, ta, tb, ty, p));
+  QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS>, dim3(grid), dim3(kThreads), C::kSmemBytes,
+                            stream, CG, ta, tb, ty, p));
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;

@@ -510,6 +510,8 @@ __global__ void __launch_bounds__(K1Shape<S, W, kWarpTeams>::kThreads,
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();  // x is written by the previous kernel of the chain
+  pdl_launch_dependents();
   // the first rows stream in while the permutation table is staged
   const bool producer = kWarpTeams ? lane == 0 : (warp == W && lane == 0);
   if (producer)
@@ -726,6 +728,8 @@ __global__ void __launch_bounds__(kStreamThreads, 4)
                             unsigned long long* __restrict__ err) {
   const int nvec = k >> 3;
   const int tid = threadIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
   for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
     const uint32_t mag = kStatic ? 0u : __ldcg(row_absmax + row);
     const bool row_bad = mag >= 0x7f80u;
@@ -912,9 +916,9 @@ int launch_act_rows_t(const uint16_t* x, int64_t m, int k, int64_t ldx, const in
     return e ? reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0)) : nullptr;
   }();
   static const int dbg = getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0;
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      x, m, k, ldx, gather, k_out, static_scale, qmax, 1.0 / static_cast<double>(qmax), q, ldq, s32,
-      s64, err, trace, dbg, nullptr);
+  QARVD_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, stream, 1, x, m,
+                            k, ldx, gather, k_out, static_scale, qmax, 1.0 / static_cast<double>(qmax), q,
+                            ldq, s32, s64, err, trace, dbg, static_cast<uint32_t*>(nullptr)));
   return QARVD_OK;
 }
 
@@ -958,9 +962,10 @@ int launch_act_rowmax_ring(const uint16_t* x, int64_t m, int k, int64_t ldx, uin
   const int64_t cap = static_cast<int64_t>(kNumSMs) * cached_blocks;
   const int64_t grid = m < cap ? m : cap;
   static const int dbg = getenv("QARVD_K1_DEBUG") ? atoi(getenv("QARVD_K1_DEBUG")) : 0;
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
-      x, m, k, ldx, nullptr, k, 0.0, qmax, 1.0 / static_cast<double>(qmax), q, ldq, s32, s64, err,
-      nullptr, dbg, row_absmax);
+  QARVD_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, stream, 1, x, m,
+                            k, ldx, static_cast<const int32_t*>(nullptr), k, 0.0, qmax,
+                            1.0 / static_cast<double>(qmax), q, ldq, s32, s64, err,
+                            static_cast<unsigned long long*>(nullptr), dbg, row_absmax));
   return QARVD_OK;
 }
 
@@ -1175,18 +1180,19 @@ extern "C" int qarvd_quantize_act_rowmax(const uint16_t* x, int64_t m, int64_t k
   const bool ring = granularity == QARVD_ACT_PER_TOKEN && k / 8 > 256 &&
                     4 * ((k + 8 + 63) & ~int64_t(63)) * 2 <= 110 * 1024 &&
                     !getenv("QARVD_K1_STREAM");  // diagnostics: force the streaming kernel
-  if (ring) {
+  if (ring) {  // (launches through launch_pdl)
     if (int st = launch_act_rowmax(x, m, static_cast<int>(k), ldx, row_absmax, qmax, xq, ldq,
                                    scale_f32, scale_f64, err, s))
       return st;
-  } else if (granularity == QARVD_ACT_PER_TOKEN)
-    quant_act_stream_kernel<false><<<grid, kStreamThreads, 0, s>>>(
-        x, m, static_cast<int>(k), ldx, row_absmax, 0.0, qmax, 1.0 / qmax, xq, ldq, scale_f32,
-        scale_f64, err);
-  else
-    quant_act_stream_kernel<true><<<grid, kStreamThreads, 0, s>>>(
-        x, m, static_cast<int>(k), ldx, nullptr, static_scale, qmax, 1.0 / qmax, xq, ldq,
-        scale_f32, scale_f64, err);
+  } else if (granularity == QARVD_ACT_PER_TOKEN) {
+    QARVD_CUDA_TRY(launch_pdl(quant_act_stream_kernel<false>, dim3(grid), dim3(kStreamThreads), 0, s, 1,
+                              x, m, static_cast<int>(k), ldx, row_absmax, 0.0, qmax, 1.0 / qmax, xq,
+                              ldq, scale_f32, scale_f64, err));
+  } else {
+    QARVD_CUDA_TRY(launch_pdl(quant_act_stream_kernel<true>, dim3(grid), dim3(kStreamThreads), 0, s, 1,
+                              x, m, static_cast<int>(k), ldx, static_cast<uint32_t*>(nullptr),
+                              static_scale, qmax, 1.0 / qmax, xq, ldq, scale_f32, scale_f64, err));
+  }
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;

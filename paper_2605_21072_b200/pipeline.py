@@ -146,7 +146,7 @@ class QuantizedChain:
         self.launch()
         torch.cuda.synchronize()
         self.events = ([torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * len(self.layers) + 1)]
-                       if timed else None)
+                       if timed else None)  # kept by the caller with the returned graph
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.launch(events=self.events)
