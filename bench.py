@@ -99,6 +99,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def k2_traffic_bytes():
+    """DRAM bytes (read + write) of the two K2 launches of one step, from the committed
+    ncu --set full capture summary (profiles/round1_traffic.json); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1_traffic.json")) as f:
+            t = json.load(f)
+        return sum(t[k]["dram_read_bytes"] + t[k]["dram_write_bytes"]
+                   for k in ("dual_gemm_ffn0", "dual_gemm_ffn2"))
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def dist_setup(gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -429,7 +441,7 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step; step timed with CUDA events",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": k2_traffic_bytes(),
                          "kernel": "dual_gemm_kernel (K2), both FFN GEMMs",
                          "peak_source": f"2 x measured bf16 burst {peak_bf16} TF/s ({peaks_src})",
                          "frac_of_int8_datasheet_4500": achieved / INT8_DATASHEET_TOPS,

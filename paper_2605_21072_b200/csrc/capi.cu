@@ -259,8 +259,10 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
   // A layer whose input already arrives in plan order (no gather: the producer's output
   // channels were folded, pipeline.fold_output_permutation) takes the streaming K1; for
   // per-token activations its producer reduces the row |y| max in the GEMM epilogue.
+  // (off by default, like pipeline.QuantizedChain(fuse_rowmax=False); QARVD_FUSE_ROWMAX=1)
+  static const bool fuse = getenv("QARVD_FUSE_ROWMAX") && getenv("QARVD_FUSE_ROWMAX")[0] == '1';
   auto streams_from = [&](int i) {
-    return i + 1 < num_layers && !layers[i + 1]->gather && layers[i + 1]->k_in % 8 == 0;
+    return fuse && i + 1 < num_layers && !layers[i + 1]->gather && layers[i + 1]->k_in % 8 == 0;
   };
   for (int i = 0; i < num_layers && e == cudaSuccess && st == QARVD_OK; ++i) {
     qarvd_linear* L = layers[i];
