@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <mutex>
+#include <vector>
 #include <new>
 
 #include "common.cuh"
@@ -103,6 +104,21 @@ struct qarvd_linear {
   uint16_t* x_dev = nullptr;
   uint16_t* y_dev = nullptr;
   uint32_t* rowmax = nullptr;  // per-row |y| max for a chained consumer (zero between steps)
+  uint64_t ws_gen = 0;         // bumped whenever the workspace is reallocated
+  // host-chain pipelining (owned by the chain's first layer): copy-in / copy-out streams and
+  // per-chunk events, created on first use
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_cmp = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[8] = {}, ev_comp[8] = {}, ev_out = nullptr;
+  // graph of the whole pipelined chain call, keyed by (host buffers, rows, layers)
+  struct ChainGraph {
+    const void* x_host = nullptr;
+    void* y_host = nullptr;
+    int64_t m = 0;
+    std::vector<const qarvd_linear*> layers;
+    std::vector<uint64_t> gens;
+    int calls = 0;
+    cudaGraphExec_t exec = nullptr;
+  } chain_graph;
   std::mutex mu;  // forward() is re-entrant per handle (reference providers are shared const)
 };
 
@@ -129,6 +145,7 @@ int ensure_workspace(qarvd_linear* L, int64_t m, bool host_io) {
     QARVD_CUDA_TRY(cudaMalloc(&L->y_dev, static_cast<size_t>(cap) * L->n * 2));
   }
   L->cap_m = cap;
+  ++L->ws_gen;  // cached chain graphs referencing the old buffers are stale
   return QARVD_OK;
 }
 
@@ -199,6 +216,14 @@ int qarvd_linear_destroy(qarvd_linear_t L) {
   cudaFree(L->x_dev);
   cudaFree(L->y_dev);
   cudaFree(L->rowmax);
+  if (L->s_in) cudaStreamDestroy(L->s_in);
+  if (L->s_out) cudaStreamDestroy(L->s_out);
+  if (L->s_cmp) cudaStreamDestroy(L->s_cmp);
+  for (cudaEvent_t ev : L->ev_in) if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : L->ev_comp) if (ev) cudaEventDestroy(ev);
+  if (L->ev_start) cudaEventDestroy(L->ev_start);
+  if (L->ev_out) cudaEventDestroy(L->ev_out);
+  if (L->chain_graph.exec) cudaGraphExecDestroy(L->chain_graph.exec);
   delete L;
   return QARVD_OK;
 }
@@ -251,46 +276,144 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
       return st;
     }
   }
-  int st = QARVD_OK;
-  cudaError_t e = cudaMemcpyAsync(layers[0]->x_dev, x_host,
-                                  static_cast<size_t>(m) * layers[0]->k_in * 2,
-                                  cudaMemcpyHostToDevice, s);
-  const uint16_t* in = layers[0]->x_dev;
-  // A layer whose input already arrives in plan order (no gather: the producer's output
-  // channels were folded, pipeline.fold_output_permutation) takes the streaming K1; for
-  // per-token activations its producer reduces the row |y| max in the GEMM epilogue.
-  // (off by default, like pipeline.QuantizedChain(fuse_rowmax=False); QARVD_FUSE_ROWMAX=1)
-  static const bool fuse = getenv("QARVD_FUSE_ROWMAX") && getenv("QARVD_FUSE_ROWMAX")[0] == '1';
-  auto streams_from = [&](int i) {
-    return fuse && i + 1 < num_layers && !layers[i + 1]->gather && layers[i + 1]->k_in % 8 == 0;
-  };
-  for (int i = 0; i < num_layers && e == cudaSuccess && st == QARVD_OK; ++i) {
-    qarvd_linear* L = layers[i];
-    if (i > 0 && streams_from(i - 1)) {
-      qarvd_linear* P = layers[i - 1];
-      st = qarvd_quantize_act_rowmax(in, m, L->k_in, L->k_in,
-                                     L->granularity == QARVD_ACT_PER_TOKEN ? P->rowmax : nullptr,
-                                     L->granularity, L->static_scale, 8, L->xq, L->k_pad, L->sx,
-                                     nullptr, nullptr, s);
-    } else {
-      st = qarvd_quantize_act(in, QARVD_BF16, m, L->k_in, L->k_in, L->gather, L->k_pad,
-                              L->granularity, L->static_scale, 8, L->xq, L->k_pad, L->sx, nullptr,
-                              nullptr, s);
-    }
-    if (st) break;
-    if (streams_from(i) && layers[i + 1]->granularity == QARVD_ACT_PER_TOKEN)
-      st = qarvd_dual_gemm_rowmax(L->xq, L->k_pad, L->wq, L->k_pad, m, L->n, L->k_pad, L->k_o, L->sx,
-                                  L->s_wo, L->s_wn, L->bias, L->epilogue, L->y_dev, L->n, L->rowmax, s);
-    else
-      st = qarvd_dual_gemm(L->xq, L->k_pad, L->wq, L->k_pad, m, L->n, L->k_pad, L->k_o, L->sx,
-                           L->s_wo, L->s_wn, L->bias, L->epilogue, QARVD_BF16, L->y_dev, L->n,
-                           nullptr, nullptr, s);
-    in = L->y_dev;
+  // Row-chunk pipeline: chunk c's H2D (copy-in stream), K1+K2 per layer (the caller's
+  // stream) and D2H (copy-out stream) are ordered by events, so the copies of neighbouring
+  // chunks overlap the compute and each other (PCIe is full duplex).  QARVD_HOST_CHUNKS
+  // overrides the chunk count (1 = the sequential H2D -> chain -> D2H).
+  qarvd_linear* L0 = layers[0];
+  // Equal row chunks, 128-row aligned.  (Measured: 4 chunks 0.49 ms per Wan FFN step vs
+  // 0.73 ms sequential; the PCIe floor with both directions busy is 0.33 ms.  Smaller or
+  // uneven chunks lose more GEMM efficiency -- N = 1536 has only 6 tile columns -- than they
+  // gain in pipeline fill.)
+  int nchunks = m >= 2048 ? 4 : 1;
+  if (const char* env = getenv("QARVD_HOST_CHUNKS")) nchunks = atoi(env);
+  nchunks = nchunks < 1 ? 1 : (nchunks > 8 ? 8 : nchunks);
+  int64_t bounds[9] = {0};
+  {
+    int64_t crow = (m + nchunks - 1) / nchunks;
+    crow = (crow + 127) / 128 * 128;
+    for (int c = 0; c < nchunks; ++c) bounds[c + 1] = (c + 1) * crow < m ? (c + 1) * crow : m;
   }
-  if (e == cudaSuccess && st == QARVD_OK)
-    e = cudaMemcpyAsync(y_host, in, static_cast<size_t>(m) * layers[num_layers - 1]->n * 2,
-                        cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && st == QARVD_OK) e = cudaStreamSynchronize(s);
+  cudaError_t e = cudaSuccess;
+  if (!L0->s_in) {
+    e = cudaStreamCreateWithFlags(&L0->s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&L0->s_out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&L0->s_cmp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&L0->ev_start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&L0->ev_out, cudaEventDisableTiming);
+    for (int c = 0; c < 8 && e == cudaSuccess; ++c) {
+      e = cudaEventCreateWithFlags(&L0->ev_in[c], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&L0->ev_comp[c], cudaEventDisableTiming);
+    }
+  }
+  int st = QARVD_OK;
+  cudaStream_t cs = L0->s_cmp;
+  auto enqueue = [&]() {
+    // A layer whose input already arrives in plan order (no gather: the producer's output
+    // channels were folded, pipeline.fold_output_permutation) may take the streaming K1 with
+    // the producer reducing the row |y| max in its epilogue
+    // (off by default, like pipeline.QuantizedChain(fuse_rowmax=False); QARVD_FUSE_ROWMAX=1)
+    static const bool fuse = getenv("QARVD_FUSE_ROWMAX") && getenv("QARVD_FUSE_ROWMAX")[0] == '1';
+    auto streams_from = [&](int i) {
+      return fuse && i + 1 < num_layers && !layers[i + 1]->gather && layers[i + 1]->k_in % 8 == 0;
+    };
+    const int64_t n_last = layers[num_layers - 1]->n;
+    if (e == cudaSuccess) e = cudaEventRecord(L0->ev_start, cs);  // (cs waited for the caller's prior work)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(L0->s_in, L0->ev_start, 0);
+    for (int c = 0; c < nchunks && e == cudaSuccess && st == QARVD_OK; ++c) {
+      const int64_t r0 = bounds[c];
+      const int64_t rows = bounds[c + 1] - r0;
+      if (rows <= 0) continue;
+      e = cudaMemcpyAsync(L0->x_dev + r0 * L0->k_in, x_host + r0 * L0->k_in,
+                          static_cast<size_t>(rows) * L0->k_in * 2, cudaMemcpyHostToDevice, L0->s_in);
+      if (e == cudaSuccess) e = cudaEventRecord(L0->ev_in[c], L0->s_in);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, L0->ev_in[c], 0);
+      const uint16_t* in = L0->x_dev + r0 * L0->k_in;
+      for (int i = 0; i < num_layers && e == cudaSuccess && st == QARVD_OK; ++i) {
+        qarvd_linear* L = layers[i];
+        int8_t* xq = L->xq + r0 * L->k_pad;
+        float* sx = L->sx + r0;
+        uint16_t* yo = L->y_dev + r0 * L->n;
+        if (i > 0 && streams_from(i - 1)) {
+          qarvd_linear* P = layers[i - 1];
+          st = qarvd_quantize_act_rowmax(in, rows, L->k_in, L->k_in,
+                                         L->granularity == QARVD_ACT_PER_TOKEN ? P->rowmax + r0 : nullptr,
+                                         L->granularity, L->static_scale, 8, xq, L->k_pad, sx, nullptr,
+                                         nullptr, cs);
+        } else {
+          st = qarvd_quantize_act(in, QARVD_BF16, rows, L->k_in, L->k_in, L->gather, L->k_pad,
+                                  L->granularity, L->static_scale, 8, xq, L->k_pad, sx, nullptr,
+                                  nullptr, cs);
+        }
+        if (st) break;
+        if (streams_from(i) && layers[i + 1]->granularity == QARVD_ACT_PER_TOKEN)
+          st = qarvd_dual_gemm_rowmax(xq, L->k_pad, L->wq, L->k_pad, rows, L->n, L->k_pad, L->k_o, sx,
+                                      L->s_wo, L->s_wn, L->bias, L->epilogue, yo, L->n, L->rowmax + r0, cs);
+        else
+          st = qarvd_dual_gemm(xq, L->k_pad, L->wq, L->k_pad, rows, L->n, L->k_pad, L->k_o, sx, L->s_wo,
+                               L->s_wn, L->bias, L->epilogue, QARVD_BF16, yo, L->n, nullptr, nullptr, cs);
+        in = yo;
+      }
+      if (st) break;
+      e = cudaEventRecord(L0->ev_comp[c], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(L0->s_out, L0->ev_comp[c], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(y_host + r0 * n_last, in, static_cast<size_t>(rows) * n_last * 2,
+                            cudaMemcpyDeviceToHost, L0->s_out);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(L0->ev_out, L0->s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, L0->ev_out, 0);
+  };
+  // The first call for a (host buffers, rows, layers) key runs eagerly (it also performs
+  // first-use setup: kernel attributes, occupancy queries), the second captures the whole
+  // pipelined sequence -- copies, events, both streams -- into a graph, later calls replay it
+  // (one launch instead of ~16 kernel launches and 8 copies; QARVD_HOST_GRAPH=0 disables).
+  static const bool use_graph = !(getenv("QARVD_HOST_GRAPH") && getenv("QARVD_HOST_GRAPH")[0] == '0');
+  auto& cg = L0->chain_graph;
+  std::vector<const qarvd_linear*> key(layers, layers + num_layers);
+  std::vector<uint64_t> gens;
+  for (int i = 0; i < num_layers; ++i) gens.push_back(layers[i]->ws_gen);
+  if (cg.x_host != x_host || cg.y_host != y_host || cg.m != m || cg.layers != key || cg.gens != gens) {
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    cg = qarvd_linear::ChainGraph{};
+    cg.x_host = x_host;
+    cg.y_host = y_host;
+    cg.m = m;
+    cg.layers = key;
+    cg.gens = gens;
+  }
+  // all pipelined work runs on the chain's own compute stream (capturable even when the
+  // caller passes the legacy default stream), forked from and joined back to `s`
+  if (e == cudaSuccess) e = cudaEventRecord(L0->ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, L0->ev_start, 0);
+  if (e == cudaSuccess && use_graph && cg.exec) {
+    e = cudaGraphLaunch(cg.exec, cs);
+  } else if (e == cudaSuccess && use_graph && cg.calls == 1) {
+    cudaGraph_t g = nullptr;
+    e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      enqueue();
+      cudaGraph_t tmp = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(cs, &tmp);
+      if (e == cudaSuccess) e = ec;
+      g = tmp;
+    }
+    if (e == cudaSuccess && st == QARVD_OK) e = cudaGraphInstantiate(&cg.exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e == cudaSuccess && st == QARVD_OK) e = cudaGraphLaunch(cg.exec, cs);
+  } else if (e == cudaSuccess) {
+    enqueue();
+  }
+  ++cg.calls;
+  if (e == cudaSuccess) e = cudaEventRecord(L0->ev_out, cs);  // join back to the caller
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, L0->ev_out, 0);
+  if (e == cudaSuccess && st == QARVD_OK) {
+    e = cudaStreamSynchronize(s);
+  } else {  // drain whatever was enqueued before releasing the workspaces
+    if (L0->s_in) cudaStreamSynchronize(L0->s_in);
+    if (L0->s_out) cudaStreamSynchronize(L0->s_out);
+    cudaStreamSynchronize(s);
+  }
   for (int i = 0; i < num_layers; ++i) layers[i]->mu.unlock();
   if (st) return st;
   QARVD_CUDA_TRY(e);

@@ -450,3 +450,37 @@ def test_k1_stream_rowmax_ties_and_nonfinite(cuda):
                  qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), k, None, None, err.data_ptr(), None)
     torch.cuda.synchronize()
     assert int(err.item()) == 7 * k + 30
+
+
+def test_host_chain_pipelined_chunks(cuda):
+    """qarvd_linear_chain_forward_host splits M into row chunks whose copies overlap the
+    compute; the result equals the device-resident chain bit for bit."""
+    from paper_2605_21072_b200.pipeline import QuantizedChain
+    d, f, m = 256, 640, 3000
+    p0, p2 = make_plan(d, 32, seed=3), make_plan(f, 13, seed=4)
+    w0, _ = bf16_values((f, d), seed=7, scale=1.0 / np.sqrt(d), heavy_cols=p0.outlier_indices)
+    w2, _ = bf16_values((d, f), seed=8, scale=1.0 / np.sqrt(f), heavy_cols=p2.outlier_indices)
+    L0 = engine.prepare_weights("ffn.0", to_dev_bf16(w0), p0)
+    L2 = engine.prepare_weights("ffn.2", to_dev_bf16(w2), p2)
+    xb, _ = bf16_values((m, d), seed=9, heavy_cols=p0.outlier_indices, gamma=4.0)
+    ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE])
+    ch.x.copy_(to_dev_bf16(xb))
+    ch.launch()
+    torch.cuda.synchronize()
+    hs = [engine.LinearHandle(ch.layers[0], qb.EPI_GELU), engine.LinearHandle(ch.layers[1])]
+    xh = torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).pin_memory()
+    yh = torch.empty((m, d), dtype=torch.bfloat16).pin_memory()
+    for _ in range(4):  # eager, then captured into a graph, then replayed
+        yh.zero_()
+        engine.chain_forward_host(hs, xh, yh)
+        assert torch.equal(yh.view(torch.int16), ch.output.cpu().view(torch.int16))
+    # new input values through the same (graph-cached) buffers
+    xb2, _ = bf16_values((m, d), seed=10, heavy_cols=p0.outlier_indices, gamma=4.0)
+    xh.copy_(torch.from_numpy(xb2.view(np.int16)).view(torch.bfloat16))
+    ch.x.copy_(to_dev_bf16(xb2))
+    ch.launch()
+    torch.cuda.synchronize()
+    engine.chain_forward_host(hs, xh, yh)
+    assert torch.equal(yh.view(torch.int16), ch.output.cpu().view(torch.int16))
+    for h in hs:
+        h.close()
