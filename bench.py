@@ -344,7 +344,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     from paper_2605_21072_b200.pipeline import QuantizedChain
 
-    chain = QuantizedChain([L0, L2], M_TOKENS, epilogues=[qb.EPI_GELU, qb.EPI_NONE])
+    fuse = os.environ.get("QARVD_BENCH_FUSE", "0") == "1"
+    chain = QuantizedChain([L0, L2], M_TOKENS, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fuse_rowmax=fuse)
     chain.x.copy_(x)
     # two graphs of the same step: one with CUDA event nodes between the kernels (per-kernel
     # device times) and a plain one for the headline timing -- event nodes would also cut the

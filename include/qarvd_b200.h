@@ -106,6 +106,16 @@ int qarvd_quantize_act_rowmax(const uint16_t* x, int64_t m, int64_t k, int64_t l
                               int bits, int8_t* xq, int64_t ldq, float* scale_f32,
                               double* scale_f64, int64_t* err_index, void* stream);
 
+/* K1 for bf16 rows in plan order (identity gather, k_out = k, k >= 512) whose |x| max
+ * comes from a producer's partial maxima: row_pmax [m x pm_count] as written by
+ * qarvd_dual_gemm_pmax (per-token), or a static per-tensor scale (row_pmax unused).  Same
+ * codes, scales and error reporting as qarvd_quantize_act(x, QARVD_BF16, m, k, ldx, NULL,
+ * k, ...); a flat streaming pass (no per-row synchronisation, nothing to reset). */
+int qarvd_quantize_act_pmax(const uint16_t* x, int64_t m, int64_t k, int64_t ldx,
+                            const uint32_t* row_pmax, int64_t pm_count, int granularity,
+                            double static_scale, int bits, int8_t* xq, int64_t ldq,
+                            float* scale_f32, double* scale_f64, int64_t* err_index, void* stream);
+
 /* ---- K5: dual-scale weight preparation ----------------------------------
  * Replaces  build_plan scales (dual_scale.cpp:13-24, :58-90) +
  *           nearest-rounding codes of fake_quant_dual (dual_scale.cpp:92-114) +
@@ -163,6 +173,17 @@ int qarvd_dual_gemm_rowmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int6
                            const float* scale_w_outlier, const float* scale_w_normal,
                            const float* bias, int epilogue, uint16_t* y, int64_t ldy,
                            uint32_t* row_absmax, void* stream);
+
+/* K2 for a chained producer, plain-store variant: bf16 y as qarvd_dual_gemm, plus
+ *   row_pmax[i * pm_count + p] = max over output columns of tile/epilogue-warp p of
+ *                                (bf16 bits of y[i, j]) & 0x7fff,
+ * pm_count = qarvd_dual_gemm_pmax_count(m, n, k) partials per row, rewritten every call. */
+int64_t qarvd_dual_gemm_pmax_count(int64_t m, int64_t n, int64_t k);
+int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                         int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                         const float* scale_w_outlier, const float* scale_w_normal,
+                         const float* bias, int epilogue, uint16_t* y, int64_t ldy,
+                         uint32_t* row_pmax, int64_t pm_count, void* stream);
 
 /* K2 with the reference's exact f64 epilogue (engine.cpp:86-94: val = 0; val += (s_x*s_wo[j])*acc_o;
  * val += (s_x*s_wn[j])*acc_n) on f64 scales -> f64 y.  Bit-identical to kernel_b_gemm_dequant

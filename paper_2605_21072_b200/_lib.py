@@ -120,6 +120,17 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_double, c_int, c_void_p, c_int64,
          c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "qarvd_dual_gemm_pmax_count": (c_int64, [c_int64, c_int64, c_int64]),
+    "qarvd_dual_gemm_pmax": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p],
+    ),
+    "qarvd_quantize_act_pmax": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int, c_double, c_int, c_void_p,
+         c_int64, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
     "qarvd_dual_gemm_f64": (
         c_int,
         [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

@@ -79,6 +79,8 @@ struct GemmParams {
   const double* so64;
   const double* sn64;
   uint32_t* row_absmax;  // optional: atomicMax per row of the sign-cleared bf16 output bits
+  uint32_t* row_pmax;    // optional: per-row partial maxima, [m][pm_count] (one per epilogue
+  int pm_count;          //   warp and tile: pm_count = num_n_blks * 4), plain stores
   int use_tma_store;  // bf16 output through the TMA store path
   int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
           pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        if (p.row_absmax) {
+        if (p.row_absmax || p.row_pmax) {
 #pragma unroll
           for (int e = 0; e < CW / 2; ++e) {
             const uint32_t keep = (2 * e + 1 < ncols ? 0x7fff7fffu : 0u) | (2 * e < ncols ? 0x7fffu : 0u);
@@ -675,6 +677,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }  // generic path
       if (p.row_absmax && row_ok)
         atomicMax(p.row_absmax + row, max(tile_mx & 0xffffu, tile_mx >> 16));
+      if (p.row_pmax && row_ok)
+        p.row_pmax[row * p.pm_count + n_blk * kSubs + half] = max(tile_mx & 0xffffu, tile_mx >> 16);
       {
         const int ti = (t - cta_id) / num_ctas;
         if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4 && ti < 32) {
@@ -800,6 +804,7 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   }
   p.num_m_blks = static_cast<int>((p.m + BM * CG - 1) / (BM * CG));
   p.num_n_blks = static_cast<int>((p.n + BN - 1) / BN);
+  p.pm_count = p.num_n_blks * (kEpiWarps / 4);
   p.num_tiles = p.num_m_blks * p.num_n_blks;
   const int units = sm_count() / CG;
   const int grid = CG * (p.num_tiles < units ? p.num_tiles : units);
@@ -849,9 +854,10 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
                      int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
                      int32_t* acc_n, cudaStream_t stream, const double* sx64 = nullptr,
                      const double* so64 = nullptr, const double* sn64 = nullptr,
-                     uint32_t* row_absmax = nullptr) {
+                     uint32_t* row_absmax = nullptr, uint32_t* row_pmax = nullptr) {
   GemmParams p{};
   p.row_absmax = row_absmax;
+  p.row_pmax = row_pmax;
   p.sx64 = sx64;
   p.so64 = so64;
   p.sn64 = sn64;
@@ -895,7 +901,8 @@ int dual_gemm_checked(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t l
                       int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
                       const float* scale_w_outlier, const float* scale_w_normal, const float* bias,
                       int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_outlier,
-                      int32_t* acc_normal, uint32_t* row_absmax, void* stream) {
+                      int32_t* acc_normal, uint32_t* row_absmax, void* stream,
+                      uint32_t* row_pmax = nullptr) {
   clear_error();
   if (m <= 0 || n <= 0 || k <= 0)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
@@ -913,12 +920,13 @@ int dual_gemm_checked(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t l
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
   if (out_dtype != QARVD_BF16 && out_dtype != QARVD_F32)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: output dtype must be bf16 or f32");
-  if (row_absmax && out_dtype != QARVD_BF16)
+  if ((row_absmax || row_pmax) && out_dtype != QARVD_BF16)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: row |y| max is defined for bf16 outputs");
   if (int st = require_device()) return st;
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
                           scale_w_normal, bias, epilogue, out_dtype, y, ldy, acc_outlier,
-                          acc_normal, as_stream(stream), nullptr, nullptr, nullptr, row_absmax);
+                          acc_normal, as_stream(stream), nullptr, nullptr, nullptr, row_absmax,
+                          row_pmax);
 }
 }  // namespace
 
@@ -971,4 +979,26 @@ extern "C" int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* 
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, nullptr, nullptr, nullptr, nullptr,
                           QARVD_EPI_NONE, QARVD_F64, y, ldy, nullptr, nullptr, as_stream(stream),
                           scale_x, scale_w_outlier, scale_w_normal);
+}
+
+extern "C" int64_t qarvd_dual_gemm_pmax_count(int64_t m, int64_t n, int64_t k) {
+  if (n <= 0) return 0;
+  const TileCfg c = choose_cfg(m, n, k);
+  return (n + c.bn - 1) / c.bn * (kEpiWarps / 4);
+}
+
+extern "C" int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                    int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                    const float* scale_x, const float* scale_w_outlier,
+                                    const float* scale_w_normal, const float* bias, int epilogue,
+                                    uint16_t* y, int64_t ldy, uint32_t* row_pmax, int64_t pm_count,
+                                    void* stream) {
+  if (!row_pmax || pm_count != qarvd_dual_gemm_pmax_count(m, n, k)) {
+    clear_error();
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "kernel_b: row partial-max buffer missing or pm_count != qarvd_dual_gemm_pmax_count");
+  }
+  return dual_gemm_checked(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
+                           scale_w_normal, bias, epilogue, QARVD_BF16, y, ldy, nullptr, nullptr,
+                           nullptr, stream, row_pmax);
 }

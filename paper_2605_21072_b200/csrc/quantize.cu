@@ -812,6 +812,182 @@ __global__ void __launch_bounds__(kStreamThreads, 4)
 }
 
 // ---------------------------------------------------------------------------
+// Flat K1 for rows already in plan order whose |x|max is known from the producer GEMM's
+// per-row partial maxima (qarvd_dual_gemm_pmax: one per epilogue warp and 256-column tile,
+// row-major [m][pm_count], rewritten every step -- nothing to reset), or a static scale.
+// The M x K/8 16-byte chunks are split into spans of 1024 consecutive chunks, one span per
+// CTA (256 threads x 4 chunks): every thread issues its four loads first, the CTA folds the
+// partial maxima of the <= 18 rows its span touches (k >= 512) in shared memory, then rounds
+// and stores.  No row-level synchronisation, so loads, rounding and stores of neighbouring
+// CTAs overlap like a plain elementwise kernel (the structure that reaches the HBM floor in
+// scripts/stream_probe.cu).
+constexpr int kFlatThreads = 256;
+constexpr int kFlatChunks = 4;
+constexpr int kFlatSpan = kFlatThreads * kFlatChunks;
+constexpr int kFlatMaxRows = 18;
+
+// repair of one flagged chunk (values within the tie guard / only the division decides)
+template <bool kStatic>
+__device__ __noinline__ void act_fix_one_chunk(const uint16_t* xs, int8_t* qs, ActScale sc,
+                                               double s64, int qmax, unsigned long long* err,
+                                               int64_t flat) {
+  uint16_t hv[8];
+  uint32_t c[8];
+  float dmax = 0.f;
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    hv[e] = xs[e];
+    bad |= (hv[e] & 0x7f80u) == 0x7f80u;
+  }
+  if (kStatic && bad) {  // a static scale has no |x|max: non-finite values surface per value
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qs[e] = static_cast<int8_t>(act_code_slow(hv[e], s64, qmax, err, flat + e));
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; e += 2)
+    act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[e]) << 16),
+                        __uint_as_float(static_cast<uint32_t>(hv[e + 1]) << 16), sc, c[e], c[e + 1], dmax);
+  bool rescan = false;
+  act_fix_chunk<kStatic, 8, false>(hv, c, sc, s64, qmax, rescan);
+  if (rescan) act_fix_chunk<kStatic, 8, true>(hv, c, sc, s64, qmax, rescan);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) qs[e] = static_cast<int8_t>(c[e]);
+}
+
+template <bool kStatic>
+__global__ void __launch_bounds__(kFlatThreads, 5)
+    quant_act_flat_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                          const uint32_t* __restrict__ row_pmax, int pm_count, double static_scale,
+                          int qmax, double rqmax, int8_t* __restrict__ q, int64_t ldq,
+                          float* __restrict__ s32_out, double* __restrict__ s64_out,
+                          unsigned long long* __restrict__ err) {
+  __shared__ uint32_t s_mag[kFlatMaxRows];
+  __shared__ float s_r[kFlatMaxRows];
+  __shared__ double s_s64[kFlatMaxRows];
+  __shared__ int s_slow[kFlatMaxRows];
+  const int nvec = k >> 3;
+  const int tid = threadIdx.x;
+  const int64_t total = m * nvec;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kFlatSpan;
+  const int64_t ra = c0 / nvec;                         // first row of the span
+  const int base0 = static_cast<int>(c0 - ra * nvec);  // its first chunk within that row
+  const int span = static_cast<int>(total - c0 < kFlatSpan ? total - c0 : kFlatSpan);
+  const int nr = (base0 + span - 1) / nvec + 1;        // rows touched (<= kFlatMaxRows)
+  if (tid < kFlatMaxRows) s_mag[tid] = 0u;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  // ---- issue the loads (row / column of each chunk by stepping, no per-chunk division)
+  uint4 d[kFlatChunks];
+  int rl[kFlatChunks], col[kFlatChunks];
+  {
+    int local = base0 + tid;
+    int r = local / nvec;
+    int cc = local - r * nvec;
+#pragma unroll
+    for (int i = 0; i < kFlatChunks; ++i) {
+      rl[i] = r;
+      col[i] = cc;
+      if (tid + i * kFlatThreads < span)
+        d[i] = ldg_stream(reinterpret_cast<const uint4*>(x + (ra + r) * ldx) + cc);
+      cc += kFlatThreads;
+      while (cc >= nvec) {
+        cc -= nvec;
+        ++r;
+      }
+    }
+  }
+  __syncthreads();  // s_mag cleared
+  if (!kStatic) {
+    for (int rr = 0; rr < nr; ++rr) {
+      const uint32_t* pr = row_pmax + (ra + rr) * pm_count;
+      uint32_t mx = 0;
+      for (int j = tid; j < pm_count; j += kFlatThreads) mx = max(mx, __ldcg(pr + j));
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if ((tid & 31) == 0 && mx) atomicMax(&s_mag[rr], mx);
+    }
+    __syncthreads();
+  }
+  if (tid < nr) {
+    const int64_t row = ra + tid;
+    const uint32_t mag = kStatic ? 0u : s_mag[tid];
+    const float amax = __uint_as_float(mag << 16);
+    double s64;
+    float r;
+    bool slow;
+    if (kStatic) {
+      const GroupScale g = scale_static(static_scale);
+      r = g.r32;
+      slow = g.exact;
+      s64 = static_scale;
+    } else {
+      r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+      slow = mag >= 0x7f80u || (amax > 0.f && !(r <= FLT_MAX && r >= FLT_MIN));
+      if (!(amax > 0.f)) {
+        s64 = DBL_MIN;
+      } else {  // fl64(amax / qmax), see quant_act_rows_kernel
+        const double a = static_cast<double>(amax), y = a * rqmax;
+        s64 = fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
+      }
+    }
+    s_r[tid] = r;
+    s_s64[tid] = s64;
+    s_slow[tid] = slow ? 1 : 0;
+    if (row * nvec >= c0) {  // this span holds the row's first chunk: it writes the scales
+      if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s64) : 0.f;
+      if (s64_out) s64_out[row] = s64;
+    }
+  }
+  __syncthreads();
+
+  ActScale sc;
+  sc.fq = static_cast<float>(qmax);
+  sc.exact = false;
+  sc.s64 = 0.0;
+  uint32_t flagged = 0;
+#pragma unroll
+  for (int i = 0; i < kFlatChunks; ++i) {
+    if (tid + i * kFlatThreads >= span) continue;
+    const int rr = rl[i];
+    const int64_t row = ra + rr;
+    int8_t* qs = q + row * ldq + col[i] * 8;
+    sc.r = s_r[rr];
+    const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
+    uint32_t c[8];
+    float dmax = 0.f;
+    if (kStatic) {  // no |x|max: non-finite values are caught per chunk
+      const uint32_t mx = __vmaxu2(__vmaxu2(w[0] & 0x7fff7fffu, w[1] & 0x7fff7fffu),
+                                   __vmaxu2(w[2] & 0x7fff7fffu, w[3] & 0x7fff7fffu));
+      if (max(mx & 0xffffu, mx >> 16) >= 0x7f80u) dmax = 1.f;
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc,
+                          c[2 * h], c[2 * h + 1], dmax);
+    if (s_slow[rr] || dmax > tie_guard<kStatic>()) flagged |= 1u << i;
+    *reinterpret_cast<uint2*>(qs) = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+  }
+  while (flagged) {  // (rare) out of line: ties, slow rows, non-finite values
+    const int i = __ffs(flagged) - 1;
+    flagged &= flagged - 1;
+    const int rr = rl[i];
+    const int64_t row = ra + rr;
+    const uint16_t* xs = x + row * ldx + col[i] * 8;
+    int8_t* qs = q + row * ldq + col[i] * 8;
+    if (s_slow[rr]) {
+      for (int e = 0; e < 8; ++e)
+        qs[e] = static_cast<int8_t>(act_code_slow(xs[e], s_s64[rr], qmax, err, row * k + col[i] * 8 + e));
+    } else {
+      ActScale sf = sc;
+      sf.r = s_r[rr];
+      act_fix_one_chunk<kStatic>(xs, qs, sf, s_s64[rr], qmax, err, row * k + col[i] * 8);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic kernel (f32 / f64 inputs, or rows too wide for shared memory):
 // one warp per row, reads straight from global memory; f64 inputs always take
 // the exact division (reference f64 semantics, no bf16 assumption).
@@ -1193,6 +1369,54 @@ extern "C" int qarvd_quantize_act_rowmax(const uint16_t* x, int64_t m, int64_t k
                               x, m, static_cast<int>(k), ldx, static_cast<uint32_t*>(nullptr),
                               static_scale, qmax, 1.0 / qmax, xq, ldq, scale_f32, scale_f64, err));
   }
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  return QARVD_OK;
+}
+
+extern "C" int qarvd_quantize_act_pmax(const uint16_t* x, int64_t m, int64_t k, int64_t ldx,
+                                       const uint32_t* row_pmax, int64_t pm_count, int granularity,
+                                       double static_scale, int bits, int8_t* xq, int64_t ldq,
+                                       float* scale_f32, double* scale_f64, int64_t* err_index,
+                                       void* stream) {
+  clear_error();
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (m < 0 || k <= 0 || ldx < k || ldq < k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "invalid shape or leading dimension");
+  if (k % 8 || k < 512 || ldx % 8 || ldq % 8 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(xq) & 7))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "quantize (pmax): k >= 512; k, ldx, ldq multiples of 8; x 16-byte aligned");
+  if (m > 0 && (!x || !xq)) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (granularity == QARVD_ACT_PER_TENSOR) {
+    if (!(static_scale > 0.0) || !(static_scale <= DBL_MAX))
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quant params: scale must be positive and finite");
+  } else if (granularity == QARVD_ACT_PER_TOKEN) {
+    if (!row_pmax || pm_count <= 0)
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize (pmax): missing row partial maxima");
+  } else {
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "unknown activation granularity");
+  }
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, s>>>(err);
+    count_launch();
+  }
+  if (m == 0) return QARVD_OK;
+  const int64_t chunks = m * (k / 8);
+  const unsigned grid = static_cast<unsigned>((chunks + kFlatSpan - 1) / kFlatSpan);
+  if (granularity == QARVD_ACT_PER_TOKEN)
+    QARVD_CUDA_TRY(launch_pdl(quant_act_flat_kernel<false>, dim3(grid), dim3(kFlatThreads), 0, s, 1, x,
+                              m, static_cast<int>(k), ldx, row_pmax, static_cast<int>(pm_count), 0.0,
+                              qmax, 1.0 / qmax, xq, ldq, scale_f32, scale_f64, err));
+  else
+    QARVD_CUDA_TRY(launch_pdl(quant_act_flat_kernel<true>, dim3(grid), dim3(kFlatThreads), 0, s, 1, x, m,
+                              static_cast<int>(k), ldx, static_cast<const uint32_t*>(nullptr), 0,
+                              static_scale, qmax, 1.0 / qmax, xq, ldq, scale_f32, scale_f64, err));
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;

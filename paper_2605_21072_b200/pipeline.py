@@ -68,10 +68,9 @@ class QuantizedChain:
 
         With ``fold`` every intermediate consumed by exactly one layer is produced in that
         layer's plan order (fold_output_permutation), so its K1 runs without a gather.
-        With ``fuse_rowmax`` a folded consumer's per-token |x| max is reduced in the producer's
-        GEMM epilogue (qarvd_dual_gemm_rowmax) and its K1 streams (qarvd_quantize_act_rowmax);
-        off by default: on B200 the extra epilogue work costs the 1-TMEM-stage producer GEMM
-        more than the consumer saves (profiles/round1_k1.md).
+        With ``fuse_rowmax`` a folded consumer's per-token |x| max comes from per-row partial
+        maxima the producer's GEMM epilogue stores (qarvd_dual_gemm_pmax) and its K1 is a flat
+        streaming pass (qarvd_quantize_act_pmax).
         ``self.source_ops`` keeps the unfolded shapes for op counting."""
         self.layers = list(layers)
         self.m = m
@@ -91,10 +90,13 @@ class QuantizedChain:
         if fold:
             for j, i in enumerate(self.inputs):
                 L = self.layers[j]
-                if i >= 0 and L.gather_dev is None and self.inputs.count(i) == 1 and fuse_rowmax:
+                if (i >= 0 and L.gather_dev is None and self.inputs.count(i) == 1 and fuse_rowmax
+                        and L.in_dim >= 512 and L.in_dim % 8 == 0):
                     self.stream_k1[j] = True
                     if L.act_granularity == _lib.ACT_PER_TOKEN:
-                        self.rowmax[i] = torch.zeros(m, dtype=torch.int32, device=dev)
+                        P = self.layers[i]
+                        pm = _lib.load().qarvd_dual_gemm_pmax_count(m, P.out_dim, P.k_pad)
+                        self.rowmax[i] = torch.zeros((m, pm), dtype=torch.int32, device=dev)
         self.x = torch.empty((m, self.layers[0].in_dim), dtype=torch.bfloat16, device=dev)
         self.xq = [torch.empty((m, L.k_pad), dtype=torch.int8, device=dev) for L in self.layers]
         self.sx = [torch.empty(m, dtype=torch.float32, device=dev) for _ in self.layers]
@@ -117,9 +119,10 @@ class QuantizedChain:
             src = self._src(i)
             if self.stream_k1[i]:
                 rm = self.rowmax[self.inputs[i]]
-                _lib.call("qarvd_quantize_act_rowmax", src.data_ptr(), self.m, L.in_dim, src.stride(0),
-                          _ptr(rm), L.act_granularity, float(L.act_scale), 8, self.xq[i].data_ptr(),
-                          L.k_pad, self.sx[i].data_ptr(), None, None, s)
+                _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), self.m, L.in_dim, src.stride(0),
+                          _ptr(rm), 0 if rm is None else rm.shape[1], L.act_granularity,
+                          float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
+                          None, None, s)
             else:
                 _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
                           src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
@@ -128,10 +131,11 @@ class QuantizedChain:
             if events is not None:
                 events[2 * i + 1].record()
             if self.rowmax[i] is not None:
-                _lib.call("qarvd_dual_gemm_rowmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
+                _lib.call("qarvd_dual_gemm_pmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
                           L.k_pad, self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
                           L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
-                          self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(), s)
+                          self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(),
+                          self.rowmax[i].shape[1], s)
             else:
                 _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
                           self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),

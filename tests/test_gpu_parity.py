@@ -484,3 +484,79 @@ def test_host_chain_pipelined_chunks(cuda):
     assert torch.equal(yh.view(torch.int16), ch.output.cpu().view(torch.int16))
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("m,k", [(4680, 8960), (33, 512), (300, 1536)])
+def test_k1_flat_pmax_bitexact(cuda, m, k):
+    """qarvd_quantize_act_pmax (row |x| max from partial maxima) == the gather-free K1."""
+    bits, x64 = bf16_values((m, k), seed=m + 2 * k, heavy_cols=np.arange(5, k, 89))
+    x = to_dev_bf16(bits)
+    mag = (bits.astype(np.uint32) & 0x7FFF)
+    pm = 7  # arbitrary partition of each row into partials
+    parts = np.zeros((m, pm), dtype=np.uint32)
+    for p_ in range(pm):
+        parts[:, p_] = mag[:, p_::pm].max(axis=1)
+    rp = torch.from_numpy(parts.astype(np.int32)).cuda()
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    s32 = torch.empty(m, dtype=torch.float32, device="cuda")
+    qb._lib.call("qarvd_quantize_act_pmax", x.data_ptr(), m, k, k, rp.data_ptr(), pm, qb.ACT_PER_TOKEN,
+                 0.0, 8, xq.data_ptr(), k, s32.data_ptr(), s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    np.testing.assert_array_equal(s32.cpu().numpy(), s_ref.astype(np.float32))
+    s = 0.0123
+    qb._lib.call("qarvd_quantize_act_pmax", x.data_ptr(), m, k, k, None, 0, qb.ACT_PER_TENSOR, s, 8,
+                 xq.data_ptr(), k, None, None, None, None)
+    q_ref, _, _ = oracle.quantize_act(x64, None, per_token=False, static_scale=s)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+
+
+def test_k1_flat_pmax_ties_and_nonfinite(cuda):
+    k = 1024
+    r = np.random.default_rng(5)
+    rows = []
+    for i in range(40):
+        a = float(2.0 ** r.integers(-6, 6))
+        base = (np.arange(k, dtype=np.float64) % 255 - 127) * (a / 127.0) * 0.5
+        base[0] = a
+        rows.append(base)
+    rows.append(np.zeros(k))
+    bits = oracle.f32_to_bf16_bits(np.asarray(rows, dtype=np.float32))
+    x64 = oracle.bf16_bits_to_f64(bits)
+    m = len(rows)
+    rp = torch.from_numpy((bits.astype(np.uint32) & 0x7FFF).max(axis=1, keepdims=True).astype(np.int32)).cuda()
+    xq = torch.empty((m, k), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    qb._lib.call("qarvd_quantize_act_pmax", to_dev_bf16(bits).data_ptr(), m, k, k, rp.data_ptr(), 1,
+                 qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), k, None, s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, None, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+    bits[7, 30] = 0x7F80
+    bits[9, 3] = 0xFFC0
+    rp = torch.from_numpy((bits.astype(np.uint32) & 0x7FFF).max(axis=1, keepdims=True).astype(np.int32)).cuda()
+    err = torch.empty(1, dtype=torch.int64, device="cuda")
+    qb._lib.call("qarvd_quantize_act_pmax", to_dev_bf16(bits).data_ptr(), m, k, k, rp.data_ptr(), 1,
+                 qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), k, None, None, err.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 7 * k + 30
+
+
+@pytest.mark.parametrize("m,n,k,n_out,epi", [(300, 8960, 1536, 32, qb.EPI_GELU), (77, 200, 160, 5, qb.EPI_NONE)])
+def test_k2_pmax_partials(cuda, m, n, k, n_out, epi):
+    """qarvd_dual_gemm_pmax: same y; the row max of its partials is the row max of |bf16 y|."""
+    plan, layer, xq, s32, s64, _, _ = _gemm_case(m, n, k, n_out, seed=m + 1)
+    y_ref = engine.kernel_b_gemm_dequant(xq, s32, layer, epilogue=epi)
+    pm = qb._lib.load().qarvd_dual_gemm_pmax_count(m, n, layer.k_pad)
+    y = torch.empty_like(y_ref)
+    rp = torch.full((m, pm), -1, dtype=torch.int32, device="cuda")
+    qb._lib.call("qarvd_dual_gemm_pmax", xq.data_ptr(), layer.k_pad, layer.wq.data_ptr(), layer.k_pad,
+                 m, n, layer.k_pad, layer.k_outlier, s32.data_ptr(), layer.scale_outlier32.data_ptr(),
+                 layer.scale_normal32.data_ptr(), None, epi, y.data_ptr(), n, rp.data_ptr(), pm, None)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
+    parts = rp.cpu().numpy().astype(np.uint32)
+    assert (parts != 0xFFFFFFFF).all()  # every partial written
+    np.testing.assert_array_equal(parts.max(axis=1), _rowmax_bits(y_ref))
