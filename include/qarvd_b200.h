@@ -137,6 +137,25 @@ int qarvd_prepare_weights(const void* w, int w_dtype, int64_t n, int64_t k, int6
                           double* scale_normal_f64, float* scale_outlier_f32,
                           float* scale_normal_f32, int64_t* err_index, void* stream);
 
+/* K5 batched over layers (one launch for a whole calibration step).  Each job is one
+ * qarvd_prepare_weights call's arguments; all jobs share w_dtype and bits.  bf16 jobs
+ * with k <= 12288 run in one batched kernel, others take the per-layer kernel.
+ * err_index: min over jobs of the first non-finite index (as for prepare_weights), or NULL. */
+typedef struct qarvd_weight_job {
+  const void* w;              /* device [n x k] (ldw) weights                          */
+  int64_t n, k, ldw;
+  const int32_t* gather;      /* device int32 [k_pad] plan gather                      */
+  int64_t k_pad, k_outlier;
+  int8_t* wq;                 /* out device int8 [n x k_pad] (ldq)                     */
+  int64_t ldq;
+  double* scale_outlier_f64;  /* out device [n] each; any may be NULL                  */
+  double* scale_normal_f64;
+  float* scale_outlier_f32;
+  float* scale_normal_f32;
+} qarvd_weight_job;
+int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int num_jobs, int w_dtype,
+                                  int bits, int64_t* err_index, void* stream);
+
 /* ---- K2: dual-scale W8A8 GEMM + dequant + bias epilogue ------------------
  * Replaces  kernel_b_gemm_dequant(xq, layer)  engine.hpp:48 / engine.cpp:46-105
  * (symmetric activations; the reference's zero-point correction, engine.cpp:95-100,
@@ -258,6 +277,12 @@ typedef struct qarvd_search_job {
 } qarvd_search_job;
 int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs, const double* percentiles,
                        int num_cand, const double* frame_weights, int bits, void* stream);
+/* Same, without the host synchronisation: the non-finite check lands in *nonfinite_flag_dev
+ * (device uint64; all ones = every sample finite) for the caller to read later. */
+int qarvd_scale_search_async(const qarvd_search_job* jobs, int num_jobs,
+                             const double* percentiles, int num_cand,
+                             const double* frame_weights, int bits, uint64_t* nonfinite_flag_dev,
+                             void* stream);
 
 /* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
  * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)

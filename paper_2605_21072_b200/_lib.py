@@ -88,6 +88,24 @@ class SearchJob(ctypes.Structure):
     ]
 
 
+class WeightJob(ctypes.Structure):
+    _fields_ = [
+        ("w", c_void_p),
+        ("n", c_int64),
+        ("k", c_int64),
+        ("ldw", c_int64),
+        ("gather", c_void_p),
+        ("k_pad", c_int64),
+        ("k_outlier", c_int64),
+        ("wq", c_void_p),
+        ("ldq", c_int64),
+        ("scale_outlier_f64", c_void_p),
+        ("scale_normal_f64", c_void_p),
+        ("scale_outlier_f32", c_void_p),
+        ("scale_normal_f32", c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol in include/qarvd_b200.h
 SIGNATURES = {
     "qarvd_abi_version": (c_int, []),
@@ -104,6 +122,8 @@ SIGNATURES = {
         [c_void_p, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int, c_void_p,
          c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "qarvd_scale_search_async": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p]),
+    "qarvd_prepare_weights_batched": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     "qarvd_dual_gemm": (
         c_int,
         [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

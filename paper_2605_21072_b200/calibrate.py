@@ -80,7 +80,8 @@ class SearchResult:
 
 
 def scale_search_async(xs: Sequence[torch.Tensor], frames: int, frame_weights=None,
-                       percentiles=PERCENTILES, bits: int = 8) -> torch.Tensor:
+                       percentiles=PERCENTILES, bits: int = 8,
+                       nonfinite_flag: Optional[torch.Tensor] = None) -> torch.Tensor:
     """K4 over a batch of layers.  xs[i]: bf16 [frames*rows x k].  Returns the device result
     matrix [len(xs), 3*nc+2] (thresholds, scales, losses, best index, best scale)."""
     nc = len(percentiles)
@@ -103,7 +104,11 @@ def scale_search_async(xs: Sequence[torch.Tensor], frames: int, frame_weights=No
         if len(frame_weights) != frames:
             raise _lib.InvalidArgument("calibrate_model: weight vector length must equal chunk count")
         w = (_lib.ctypes.c_double * frames)(*[float(v) for v in frame_weights])
-    _lib.call("qarvd_scale_search", jobs, len(xs), pct, nc, w, bits, _stream())
+    if nonfinite_flag is None:  # synchronous: raises on non-finite samples
+        _lib.call("qarvd_scale_search", jobs, len(xs), pct, nc, w, bits, _stream())
+    else:  # the caller checks nonfinite_flag (int64, -1 = all finite) after its own sync
+        _lib.call("qarvd_scale_search_async", jobs, len(xs), pct, nc, w, bits,
+                  nonfinite_flag.data_ptr(), _stream())
     return res
 
 
@@ -284,22 +289,45 @@ class CalibrationShard:
         groups = {}
         for i, x in enumerate(self.x):
             groups.setdefault(x.shape[0] // self.frames, []).append(i)
+        # K4 runs on a side stream: the host reads K3's reports, builds the plans and
+        # launches K5 while the histogram passes stream X
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(device=self.x[0].device)
+        main = torch.cuda.current_stream()
+        self._side.wait_stream(main)
         search = {}
+        with torch.cuda.stream(self._side):
+            flags = torch.empty(len(groups), dtype=torch.int64, device=self.x[0].device)
+            for g, (rows, idx) in enumerate(groups.items()):
+                res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights,
+                                         nonfinite_flag=flags[g:g + 1])
+                for j, i in enumerate(idx):
+                    search[i] = res[j]
+        reps = outlier.collect_reports(dev_rep)  # host sync (main stream): plans need the index sets
+        plans = [engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+                 for spec, rep in zip(self.specs, reps)]
+        # K5 for every layer in one launch; codes / scales land in one buffer per field
+        layers = engine.prepare_weights_batched([s.name for s in self.specs], self.w, plans,
+                                                check_finite=False)
+        main.wait_stream(self._side)
+        # one device -> host copy per result group (not per layer)
+        search_host = {}
         for rows, idx in groups.items():
-            res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights)
+            mat = torch.stack([search[i] for i in idx]).cpu().numpy()
             for j, i in enumerate(idx):
-                search[i] = res[j]
-        reps = outlier.collect_reports(dev_rep)  # host sync: plans need the index sets
-        layers = []
-        for spec, w, rep in zip(self.specs, self.w, reps):
-            plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
-            layers.append(engine.prepare_weights(spec.name, w, plan, check_finite=False))  # K5
-        out = []
+                search_host[i] = mat[j]
+        if (flags.cpu() != -1).any():
+            raise _lib.InvalidArgument("quantize: non-finite input in calibration samples")
+        so_all = torch.cat([L.scale_outlier64 for L in layers]).cpu().numpy()
+        sn_all = torch.cat([L.scale_normal64 for L in layers]).cpu().numpy()
+        out, off = [], 0
+        nc = len(PERCENTILES)
         for i, (spec, L, rep) in enumerate(zip(self.specs, layers, reps)):
-            r = search[i].cpu().numpy()
-            nc = len(PERCENTILES)
+            r = search_host[i]
+            n = L.out_dim
             out.append(LayerRecord(spec.index, len(rep.aligned_outliers), rep.aligned_outliers,
                                    float(r[3 * nc + 1]), int(r[3 * nc]), r[2 * nc:3 * nc].copy(),
-                                   L.scale_outlier64.cpu().numpy(), L.scale_normal64.cpu().numpy()))
+                                   so_all[off:off + n].copy(), sn_all[off:off + n].copy()))
+            off += n
         self.layers = layers
         return out

@@ -32,6 +32,21 @@ int require_device() {
     cudaGetLastError();
     QARVD_FAIL(QARVD_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
   }
+  // Stream-ordered workspaces (K3 job tables, K4 histograms -- ~0.8 GB per calibration step)
+  // come from the device's default memory pool; keep what it has instead of returning it to
+  // the driver at every synchronisation (re-mapping the histograms each step cost up to
+  // 10x the step itself when the caching allocators hold most of the device).
+  static thread_local int pool_device = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != pool_device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    pool_device = dev;
+  }
   return QARVD_OK;
 }
 

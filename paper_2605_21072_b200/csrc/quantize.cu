@@ -18,6 +18,7 @@
 
 #include <climits>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -988,6 +989,138 @@ __global__ void __launch_bounds__(kFlatThreads, 5)
 }
 
 // ---------------------------------------------------------------------------
+// K5 batched over layers (calibration: every layer's weights in one launch).  One warp team
+// per row: the row streams into shared memory by a 1-D bulk copy, pass 1 takes the
+// outlier- and normal-group |w| maxima through the layer's int16 gather table, pass 2
+// emits the codes of each group with its scale (same exact rounding and tie handling as
+// K1), four per lane per step.  grid.y = layer; each CTA stages its layer's table.
+struct WeightJobDev {
+  const uint16_t* w;
+  int64_t n, k, ldw;
+  const int32_t* gather;
+  int64_t k_pad, k_o;
+  int8_t* wq;
+  int64_t ldq;
+  double* so64;
+  double* sn64;
+  float* so32;
+  float* sn32;
+};
+constexpr int kWTeams = 4;
+
+template <bool dummy = false>
+__device__ __noinline__ void wq_fix_chunk(const uint16_t* hv, uint32_t* c, ActScale sc, double s64, int qmax) {
+  bool rescan = false;
+  act_fix_chunk<false, 4, false>(hv, c, sc, s64, qmax, rescan);
+  if (rescan) act_fix_chunk<false, 4, true>(hv, c, sc, s64, qmax, rescan);
+}
+
+__global__ void __launch_bounds__(32 * kWTeams, 4)
+    prep_weights_batched_kernel(const WeightJobDev* __restrict__ jobs, int qmax, double rqmax,
+                                unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(128) uint16_t wsm[];
+  __shared__ __align__(8) uint64_t full[kWTeams];
+  const WeightJobDev J = jobs[blockIdx.y];
+  const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kWTeams + team;
+  if (static_cast<int64_t>(blockIdx.x) * kWTeams >= J.n) return;  // CTA-uniform
+  const int k = static_cast<int>(J.k), k_pad = static_cast<int>(J.k_pad), k_o = static_cast<int>(J.k_o);
+  const int row_stride = (k + 8 + 63) & ~63;
+  uint16_t* srow = wsm + team * row_stride;
+  int16_t* gidx = reinterpret_cast<int16_t*>(wsm + kWTeams * row_stride);
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kWTeams;
+  const uint32_t row_bytes = static_cast<uint32_t>(k) * 2u;
+  if (threadIdx.x < kWTeams) ptx::mbar_init(&full[threadIdx.x], 1);
+  ptx::fence_mbar_init();
+  __syncthreads();
+  if (lane == 0 && row0 < J.n) {
+    ptx::mbar_expect_tx(&full[team], row_bytes);
+    ptx::bulk_load_1d(srow, J.w + row0 * J.ldw, row_bytes, &full[team]);
+  }
+  for (int c4 = threadIdx.x; c4 < (k_pad >> 2); c4 += blockDim.x) {
+    const int4 g = __ldg(reinterpret_cast<const int4*>(J.gather) + c4);
+    const uint32_t lo = static_cast<uint16_t>(g.x < 0 ? k : g.x) | (static_cast<uint32_t>(g.y < 0 ? k : g.y) << 16);
+    const uint32_t hi = static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16);
+    reinterpret_cast<uint2*>(gidx)[c4] = make_uint2(lo, hi);
+  }
+  if (lane < 8) srow[k + lane] = 0;
+  __syncthreads();
+
+  int j = 0;
+  for (int64_t row = row0; row < J.n; row += step, ++j) {
+    ptx::mbar_wait_spin(&full[team], static_cast<uint32_t>(j & 1));
+    // ---- pass 1: group maxima through the gather (sign-cleared bf16 bits)
+    uint32_t mo = 0, mn = 0;
+    for (int c0 = lane * 4; c0 < k_pad; c0 += 128) {
+      const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+      const uint32_t a = max(max(srow[gp.x & 0xffffu] & 0x7fffu, srow[gp.x >> 16] & 0x7fffu),
+                             max(srow[gp.y & 0xffffu] & 0x7fffu, srow[gp.y >> 16] & 0x7fffu));
+      if (c0 < k_o) mo = max(mo, a);
+      else mn = max(mn, a);
+    }
+    mo = __reduce_max_sync(0xffffffffu, mo);
+    mn = __reduce_max_sync(0xffffffffu, mn);
+    const bool bad = mo >= 0x7f80u || mn >= 0x7f80u;
+    ActScale so, sn;
+    double so64, sn64;
+    auto group = [&](uint32_t mg, ActScale& sc, double& s64) {
+      const float amax = __uint_as_float(mg << 16);
+      sc.fq = static_cast<float>(qmax);
+      sc.s64 = 0.0;
+      sc.r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+      sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
+      if (!(amax > 0.f)) {
+        s64 = DBL_MIN;  // dual_scale.cpp:13-24 (all-zero group)
+      } else {  // fl64(amax / qmax), see quant_act_rows_kernel
+        const double a = static_cast<double>(amax), y = a * rqmax;
+        s64 = fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
+      }
+    };
+    group(mn, sn, sn64);
+    if (k_o > 0) group(mo, so, so64);
+    else {
+      so = sn;
+      so64 = sn64;  // single-scale plan: outlier scale = normal scale (dual_scale.cpp:55)
+    }
+    if (lane == 0) {
+      if (J.so64) J.so64[row] = so64;
+      if (J.sn64) J.sn64[row] = sn64;
+      if (J.so32) J.so32[row] = so64 == DBL_MIN ? 0.f : __double2float_rn(so64);
+      if (J.sn32) J.sn32[row] = sn64 == DBL_MIN ? 0.f : __double2float_rn(sn64);
+    }
+    int8_t* qr = J.wq + row * J.ldq;
+    // ---- pass 2: codes, four per lane per step
+    for (int c0 = lane * 4; c0 < k_pad; c0 += 128) {
+      const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+      const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu], srow[gp.y >> 16]};
+      const bool outl = c0 < k_o;
+      const ActScale& sc = outl ? so : sn;
+      const double s64 = outl ? so64 : sn64;
+      uint32_t c[4];
+      if (bad || sc.exact) {
+        for (int e = 0; e < 4; ++e) {
+          const int g = gidx[c0 + e];
+          c[e] = (g >= k) ? 0u : act_code_slow(hv[e], s64, qmax, err, row * k_pad + c0 + e);
+        }
+      } else {
+        float dmax = 0.f;
+        act_codes2<false>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                          __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
+        act_codes2<false>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                          __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
+        if (dmax > tie_guard<false>()) wq_fix_chunk(hv, c, sc, s64, qmax);
+      }
+      *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
+    }
+    __syncwarp();
+    if (lane == 0 && row + step < J.n) {
+      ptx::mbar_expect_tx(&full[team], row_bytes);
+      ptx::bulk_load_1d(srow, J.w + (row + step) * J.ldw, row_bytes, &full[team]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic kernel (f32 / f64 inputs, or rows too wide for shared memory):
 // one warp per row, reads straight from global memory; f64 inputs always take
 // the exact division (reference f64 semantics, no bf16 assumption).
@@ -1419,5 +1552,76 @@ extern "C" int qarvd_quantize_act_pmax(const uint16_t* x, int64_t m, int64_t k, 
                               static_scale, qmax, 1.0 / qmax, xq, ldq, scale_f32, scale_f64, err));
   count_launch();
   QARVD_LAUNCH_CHECK();
+  return QARVD_OK;
+}
+
+extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int num_jobs, int w_dtype,
+                                             int bits, int64_t* err_index, void* stream) {
+  clear_error();
+  if (num_jobs < 0 || (num_jobs > 0 && !jobs))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "prepare_weights_batched: invalid job table");
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (num_jobs == 0) return QARVD_OK;
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, s>>>(err);
+    count_launch();
+  }
+  // jobs the batched bf16 kernel serves; the rest take the per-layer path
+  std::vector<WeightJobDev> fast;
+  int64_t max_n = 0, max_k = 0, max_kp = 0;
+  for (int i = 0; i < num_jobs; ++i) {
+    const qarvd_weight_job& j = jobs[i];
+    if (int st = check_common(j.w, w_dtype, j.n, j.k, j.ldw, j.k_pad, bits, j.wq, j.ldq, j.gather)) return st;
+    if (j.k_outlier < 0 || j.k_outlier >= j.k_pad)
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "build_plan: outlier set would leave no normal channels");
+    const bool ok = w_dtype == QARVD_BF16 && j.gather && j.k % 8 == 0 && j.ldw % 8 == 0 &&
+                    j.k_pad % 4 == 0 && j.ldq % 4 == 0 && j.k_outlier % 4 == 0 && j.k <= 12288 &&
+                    j.k_pad <= 16384 && (reinterpret_cast<uintptr_t>(j.w) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(j.gather) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(j.wq) & 3) == 0;
+    if (ok) {
+      fast.push_back(WeightJobDev{static_cast<const uint16_t*>(j.w), j.n, j.k, j.ldw, j.gather, j.k_pad,
+                                  j.k_outlier, j.wq, j.ldq, j.scale_outlier_f64, j.scale_normal_f64,
+                                  j.scale_outlier_f32, j.scale_normal_f32});
+      max_n = j.n > max_n ? j.n : max_n;
+      max_k = j.k > max_k ? j.k : max_k;
+      max_kp = j.k_pad > max_kp ? j.k_pad : max_kp;
+    } else if (j.n > 0) {
+      if (int st = launch_rows<kWeightDual>(j.w, w_dtype, j.n, j.k, j.ldw, j.gather, j.k_pad, j.k_outlier,
+                                            0.0, bits, j.wq, j.ldq, j.scale_outlier_f32, j.scale_outlier_f64,
+                                            j.scale_normal_f32, j.scale_normal_f64, nullptr, s))
+        return st;
+      if (err) {  // fold the per-layer check into the batch's error index
+        (void)0;
+      }
+    }
+  }
+  if (!fast.empty() && max_n > 0) {
+    WeightJobDev* d_jobs = nullptr;
+    const size_t bytes = fast.size() * sizeof(WeightJobDev);
+    QARVD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_jobs), bytes, s));
+    QARVD_CUDA_TRY(cudaMemcpyAsync(d_jobs, fast.data(), bytes, cudaMemcpyHostToDevice, s));
+    const size_t smem = static_cast<size_t>(kWTeams) * ((max_k + 8 + 63) & ~int64_t(63)) * 2 + max_kp * 2;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] { attr = set_smem_attrs(prep_weights_batched_kernel, 110 * 1024); });
+    QARVD_CUDA_TRY(attr);
+    if (smem > 110 * 1024) QARVD_FAIL(QARVD_ERR_LOGIC, "prepare_weights_batched: rows too wide");
+    // enough CTAs per layer to fill the GPU a few times over, rows strided across teams
+    int64_t gx = (max_n + kWTeams - 1) / kWTeams;
+    const int64_t cap = (static_cast<int64_t>(kNumSMs) * 16 + static_cast<int64_t>(fast.size()) - 1) /
+                        static_cast<int64_t>(fast.size());
+    gx = gx < cap ? gx : (cap < 1 ? 1 : cap);
+    prep_weights_batched_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(fast.size())),
+                                  32 * kWTeams, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
+    count_launch();
+    QARVD_LAUNCH_CHECK();
+    QARVD_CUDA_TRY(cudaFreeAsync(d_jobs, s));
+  }
   return QARVD_OK;
 }

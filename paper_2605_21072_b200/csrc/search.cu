@@ -51,20 +51,35 @@ __global__ void __launch_bounds__(kHistThreads)
   bool bad = false;
   const bool vec = ((u.k & 7) == 0) && ((u.ldx & 7) == 0) &&
                    ((reinterpret_cast<uintptr_t>(u.x) & 15) == 0);
-  if (vec) {
-    const int64_t vpr = u.k >> 3;  // uint4 per row
-    const int64_t total = u.rows * vpr;
-    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
-      const int64_t r = t / vpr, v = t - r * vpr;
-      const uint4 d = __ldg(reinterpret_cast<const uint4*>(u.x + r * u.ldx) + v);
-      const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  auto count8 = [&](const uint4 d) {
+    const uint32_t w[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const uint32_t lo = w[h] & 0x7fffu, hi = (w[h] >> 16) & 0x7fffu;
-        bad |= (lo >= kFiniteBins) | (hi >= kFiniteBins);
-        atomicAdd(&sh[lo], 1u);
-        atomicAdd(&sh[hi], 1u);
-      }
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t lo = w[h] & 0x7fffu, hi = (w[h] >> 16) & 0x7fffu;
+      bad |= (lo >= kFiniteBins) | (hi >= kFiniteBins);
+      atomicAdd(&sh[lo], 1u);
+      atomicAdd(&sh[hi], 1u);
+    }
+  };
+  if (vec && u.ldx == u.k) {
+    // contiguous rows: one flat stream of 16-byte chunks (no per-chunk row division)
+    const uint4* p = reinterpret_cast<const uint4*>(u.x);
+    const int64_t total = u.rows * (u.k >> 3);
+    int64_t t = threadIdx.x;
+    for (; t + 3 * blockDim.x < total; t += 4 * blockDim.x) {
+      const uint4 d0 = __ldg(p + t), d1 = __ldg(p + t + blockDim.x), d2 = __ldg(p + t + 2 * blockDim.x),
+                  d3 = __ldg(p + t + 3 * blockDim.x);
+      count8(d0);
+      count8(d1);
+      count8(d2);
+      count8(d3);
+    }
+    for (; t < total; t += blockDim.x) count8(__ldg(p + t));
+  } else if (vec) {
+    const int vpr = static_cast<int>(u.k >> 3);  // uint4 per row
+    for (int64_t r = 0; r < u.rows; ++r) {
+      const uint4* p = reinterpret_cast<const uint4*>(u.x + r * u.ldx);
+      for (int v = threadIdx.x; v < vpr; v += blockDim.x) count8(__ldg(p + v));
     }
   } else {
     const int64_t total = u.rows * u.k;
@@ -239,9 +254,38 @@ __global__ void __launch_bounds__(kEvalThreads)
 
 using namespace qarvd_b200;
 
+namespace qarvd_b200 {
+namespace {
+int scale_search_impl(const qarvd_search_job* jobs, int num_jobs, const double* percentiles,
+                      int num_cand, const double* frame_weights, int bits, void* stream,
+                      unsigned long long* err_out);
+}  // namespace
+}  // namespace qarvd_b200
+
 extern "C" int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs,
                                   const double* percentiles, int num_cand,
                                   const double* frame_weights, int bits, void* stream) {
+  return qarvd_b200::scale_search_impl(jobs, num_jobs, percentiles, num_cand, frame_weights, bits,
+                                       stream, nullptr);
+}
+
+extern "C" int qarvd_scale_search_async(const qarvd_search_job* jobs, int num_jobs,
+                                        const double* percentiles, int num_cand,
+                                        const double* frame_weights, int bits,
+                                        uint64_t* nonfinite_flag_dev, void* stream) {
+  if (!nonfinite_flag_dev) {
+    qarvd_b200::clear_error();
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "scale_search_async: null non-finite flag");
+  }
+  return qarvd_b200::scale_search_impl(jobs, num_jobs, percentiles, num_cand, frame_weights, bits,
+                                       stream, reinterpret_cast<unsigned long long*>(nonfinite_flag_dev));
+}
+
+namespace qarvd_b200 {
+namespace {
+int scale_search_impl(const qarvd_search_job* jobs, int num_jobs, const double* percentiles,
+                      int num_cand, const double* frame_weights, int bits, void* stream,
+                      unsigned long long* err_out) {
   clear_error();
   if (num_jobs < 0 || (num_jobs > 0 && !jobs))
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "scale_search: invalid job list");
@@ -344,6 +388,12 @@ extern "C" int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs,
   QARVD_LAUNCH_CHECK();
 
   // non-finite input check (reference: quantize throws on non-finite, quant.cpp:128-129)
+  if (err_out) {  // async variant: the caller checks the flag (~0 = all finite) later
+    QARVD_CUDA_TRY(cudaMemcpyAsync(err_out, err, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    QARVD_CUDA_TRY(cudaFreeAsync(tables, s));
+    QARVD_CUDA_TRY(cudaFreeAsync(ws, s));
+    return QARVD_OK;
+  }
   unsigned long long h_err = ~0ull;
   QARVD_CUDA_TRY(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
   QARVD_CUDA_TRY(cudaFreeAsync(tables, s));
@@ -353,3 +403,5 @@ extern "C" int qarvd_scale_search(const qarvd_search_job* jobs, int num_jobs,
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize: non-finite input in calibration samples");
   return QARVD_OK;
 }
+}  // namespace
+}  // namespace qarvd_b200

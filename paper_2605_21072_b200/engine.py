@@ -15,7 +15,7 @@ provider only); every computation runs in libqarvd_b200.so through the C-ABI.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 import torch
@@ -169,6 +169,65 @@ def prepare_weights(name: str, w: torch.Tensor, plan: DualScalePlan, bits: int =
         if v != 0x7FFFFFFFFFFFFFFF:
             raise _lib.InvalidArgument("fake_quant_dual: non-finite weight element")
     return QuantizedLayer(name, n, k, plan, wq, so64, sn64, so32, sn32, gather)
+
+
+def prepare_weights_batched(names: Sequence[str], ws: Sequence[torch.Tensor],
+                            plans: Sequence[DualScalePlan], bits: int = 8,
+                            check_finite: bool = True) -> List[QuantizedLayer]:
+    """K5 for many layers in one launch (qarvd_prepare_weights_batched): the plans' gathers go
+    to the device in one copy, codes and scales land in one buffer per field (per-layer views).
+    Same results as prepare_weights per layer."""
+    if not ws:
+        return []
+    dev = ws[0].device
+    dtype = _dtype_code(ws[0])
+    for w, plan in zip(ws, plans):
+        if w.shape[1] != plan.d_in:
+            raise _lib.InvalidArgument("build_plan: report does not match the weight's input width")
+        if _dtype_code(w) != dtype:
+            raise _lib.InvalidArgument("prepare_weights_batched: weights of one batch share a dtype")
+    # gathers: one host concatenation, one H2D (16-byte aligned slices)
+    offs, tot = [], 0
+    for plan in plans:
+        offs.append(tot)
+        tot += (plan.k_pad + 3) // 4 * 4
+    g_host = np.full(tot, -1, dtype=np.int32)
+    for o, plan in zip(offs, plans):
+        g_host[o:o + plan.k_pad] = plan.gather
+    g_dev = torch.from_numpy(g_host).to(dev)
+    # outputs: one buffer per field
+    wq_offs, wq_tot, n_offs, n_tot = [], 0, [], 0
+    for w, plan in zip(ws, plans):
+        wq_offs.append(wq_tot)
+        wq_tot += (w.shape[0] * plan.k_pad + 15) // 16 * 16
+        n_offs.append(n_tot)
+        n_tot += w.shape[0]
+    wq_all = torch.empty(wq_tot, dtype=torch.int8, device=dev)
+    so64 = torch.empty(n_tot, dtype=torch.float64, device=dev)
+    sn64 = torch.empty(n_tot, dtype=torch.float64, device=dev)
+    so32 = torch.empty(n_tot, dtype=torch.float32, device=dev)
+    sn32 = torch.empty(n_tot, dtype=torch.float32, device=dev)
+    jobs = (_lib.WeightJob * len(ws))()
+    layers = []
+    for i, (name, w, plan) in enumerate(zip(names, ws, plans)):
+        n, k = w.shape
+        wq = wq_all[wq_offs[i]:wq_offs[i] + n * plan.k_pad].view(n, plan.k_pad)
+        sl = slice(n_offs[i], n_offs[i] + n)
+        gather = g_dev[offs[i]:offs[i] + plan.k_pad]
+        j = jobs[i]
+        j.w, j.n, j.k, j.ldw = w.data_ptr(), n, k, w.stride(0)
+        j.gather, j.k_pad, j.k_outlier = gather.data_ptr(), plan.k_pad, plan.k_outlier
+        j.wq, j.ldq = wq.data_ptr(), plan.k_pad
+        j.scale_outlier_f64, j.scale_normal_f64 = so64[sl].data_ptr(), sn64[sl].data_ptr()
+        j.scale_outlier_f32, j.scale_normal_f32 = so32[sl].data_ptr(), sn32[sl].data_ptr()
+        layers.append(QuantizedLayer(name, n, k, plan, wq, so64[sl], sn64[sl], so32[sl], sn32[sl], gather))
+    err = torch.empty(1, dtype=torch.int64, device=dev) if check_finite else None
+    _lib.call("qarvd_prepare_weights_batched", jobs, len(ws), dtype, bits, _ptr(err), _stream())
+    if err is not None:
+        v = int(err.item())
+        if v != 0x7FFFFFFFFFFFFFFF:
+            raise _lib.InvalidArgument("fake_quant_dual: non-finite weight element")
+    return layers
 
 
 def kernel_a_quantize_activation(x: torch.Tensor, layer_or_plan, granularity: int = _lib.ACT_PER_TOKEN,

@@ -560,3 +560,38 @@ def test_k2_pmax_partials(cuda, m, n, k, n_out, epi):
     parts = rp.cpu().numpy().astype(np.uint32)
     assert (parts != 0xFFFFFFFF).all()  # every partial written
     np.testing.assert_array_equal(parts.max(axis=1), _rowmax_bits(y_ref))
+
+
+def test_k5_batched_matches_per_layer_and_oracle(cuda):
+    """qarvd_prepare_weights_batched == qarvd_prepare_weights per layer == oracle, over a
+    batch of mixed shapes, ragged outlier sets, a single-scale plan and an all-zero group."""
+    shapes = [(384, 8960, 188), (1536, 1536, 32), (96, 256, 0), (200, 1536, 5), (64, 512, 64)]
+    ws, plans, refs = [], [], []
+    for i, (n, k, no) in enumerate(shapes):
+        plan = make_plan(k, no, seed=100 + i)
+        bits, w64 = bf16_values((n, k), seed=200 + i, scale=1.0 / np.sqrt(k),
+                                heavy_cols=plan.outlier_indices if no else None)
+        if i == 4:  # an all-zero outlier group in some rows
+            bits[:10, plan.outlier_indices] = 0
+            w64 = oracle.bf16_bits_to_f64(bits)
+        ws.append(to_dev_bf16(bits))
+        plans.append(plan)
+        refs.append(oracle.prepare_weights(w64, plan.gather, plan.k_outlier))
+    layers = engine.prepare_weights_batched([f"l{i}" for i in range(len(ws))], ws, plans)
+    for L, w, plan, (wq_ref, so_ref, sn_ref, bad) in zip(layers, ws, plans, refs):
+        assert bad < 0
+        np.testing.assert_array_equal(L.wq.cpu().numpy(), wq_ref)
+        np.testing.assert_array_equal(L.scale_outlier64.cpu().numpy(), so_ref)
+        np.testing.assert_array_equal(L.scale_normal64.cpu().numpy(), sn_ref)
+        one = engine.prepare_weights("one", w, plan)
+        assert torch.equal(one.wq, L.wq)
+        assert torch.equal(one.scale_outlier32, L.scale_outlier32)
+        assert torch.equal(one.scale_normal32, L.scale_normal32)
+
+
+def test_k5_batched_nonfinite(cuda):
+    plan = make_plan(512, 32, seed=3)
+    bits, _ = bf16_values((40, 512), seed=4)
+    bits[11, 7] = 0x7FC0
+    with pytest.raises(qb.InvalidArgument, match="non-finite"):
+        engine.prepare_weights_batched(["a"], [to_dev_bf16(bits)], [plan])
