@@ -42,61 +42,88 @@ __device__ __forceinline__ double sq(T v) {
   return __dmul_rn(d, d);
 }
 
-// grid-stride over the concatenated 8-column groups of all jobs
+// grid-stride over the concatenated 2-column groups of all jobs.  Each column's sum stays
+// sequential over rows (tensor.cpp:138-140, bit-exact); parallelism comes from many threads
+// (two columns each) and from issuing 8 rows of loads before adding them in order.
+constexpr int kNormCols = 2;
+constexpr int kNormRows = 8;
+
+template <typename T>
+struct Pair;
+template <>
+struct Pair<uint16_t> {
+  using V = uint32_t;
+  __device__ static void split(V v, uint16_t& a, uint16_t& b) {
+    a = static_cast<uint16_t>(v & 0xffffu);
+    b = static_cast<uint16_t>(v >> 16);
+  }
+};
+template <>
+struct Pair<float> {
+  using V = float2;
+  __device__ static void split(V v, float& a, float& b) {
+    a = v.x;
+    b = v.y;
+  }
+};
+template <>
+struct Pair<double> {
+  using V = double2;
+  __device__ static void split(V v, double& a, double& b) {
+    a = v.x;
+    b = v.y;
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kNormThreads)
     column_norms_kernel(const NormJobDev* __restrict__ jobs, int num_jobs, int64_t total_groups) {
+  using PV = typename Pair<T>::V;
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total_groups;
        g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // locate the job (few jobs; linear scan over prefix offsets)
-    int j = 0;
-    while (j + 1 < num_jobs && jobs[j + 1].group_begin <= g) ++j;
-    const NormJobDev job = jobs[j];
-    const int64_t c0 = (g - job.group_begin) * 8;
+    int lo = 0, hi = num_jobs - 1;  // the last job whose first group is <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (jobs[mid].group_begin <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const NormJobDev job = jobs[lo];
+    const int64_t c0 = (g - job.group_begin) * kNormCols;
     const T* w = static_cast<const T*>(job.w);
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const bool full = (c0 + 8 <= job.k);
-    const bool vec = full && sizeof(T) == 2 && ((job.ldw & 7) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
-    if (vec) {
-      const uint16_t* base = reinterpret_cast<const uint16_t*>(w) + c0;
+    double a0 = 0.0, a1 = 0.0;
+    const bool pair = (c0 + 2 <= job.k) && ((job.ldw & 1) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(w) & (sizeof(PV) - 1)) == 0);
+    if (pair) {
+      const T* base = w + c0;
       int64_t i = 0;
-      for (; i + 4 <= job.n; i += 4) {
-        uint4 d[4];
+      for (; i + kNormRows <= job.n; i += kNormRows) {
+        PV d[kNormRows];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          d[u] = __ldg(reinterpret_cast<const uint4*>(base + (i + u) * job.ldw));
+        for (int u = 0; u < kNormRows; ++u) d[u] = __ldg(reinterpret_cast<const PV*>(base + (i + u) * job.ldw));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t wd[4] = {d[u].x, d[u].y, d[u].z, d[u].w};
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            acc[2 * h] = __dadd_rn(acc[2 * h], sq<uint16_t>(static_cast<uint16_t>(wd[h] & 0xffffu)));
-            acc[2 * h + 1] = __dadd_rn(acc[2 * h + 1], sq<uint16_t>(static_cast<uint16_t>(wd[h] >> 16)));
-          }
+        for (int u = 0; u < kNormRows; ++u) {
+          T e0, e1;
+          Pair<T>::split(d[u], e0, e1);
+          a0 = __dadd_rn(a0, sq<T>(e0));
+          a1 = __dadd_rn(a1, sq<T>(e1));
         }
       }
       for (; i < job.n; ++i) {
-        const uint4 d = __ldg(reinterpret_cast<const uint4*>(base + i * job.ldw));
-        const uint32_t wd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          acc[2 * h] = __dadd_rn(acc[2 * h], sq<uint16_t>(static_cast<uint16_t>(wd[h] & 0xffffu)));
-          acc[2 * h + 1] = __dadd_rn(acc[2 * h + 1], sq<uint16_t>(static_cast<uint16_t>(wd[h] >> 16)));
-        }
+        T e0, e1;
+        Pair<T>::split(__ldg(reinterpret_cast<const PV*>(base + i * job.ldw)), e0, e1);
+        a0 = __dadd_rn(a0, sq<T>(e0));
+        a1 = __dadd_rn(a1, sq<T>(e1));
       }
     } else {
-      const int cols = full ? 8 : static_cast<int>(job.k - c0);
+      const bool two = c0 + 1 < job.k;
       for (int64_t i = 0; i < job.n; ++i) {
         const T* row = w + i * job.ldw + c0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < cols) acc[e] = __dadd_rn(acc[e], sq<T>(row[e]));
+        a0 = __dadd_rn(a0, sq<T>(row[0]));
+        if (two) a1 = __dadd_rn(a1, sq<T>(row[1]));
       }
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (c0 + e < job.k) job.norms[c0 + e] = __dsqrt_rn(acc[e]);
+    job.norms[c0] = __dsqrt_rn(a0);
+    if (c0 + 1 < job.k) job.norms[c0 + 1] = __dsqrt_rn(a1);
   }
 }
 
@@ -300,8 +327,8 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
       QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "analyze_layers: invalid job " + std::to_string(i));
     if (J.k > kMaxSelK)
       QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "analyze_layers: d_in above 16384 is not supported");
-    nj[i] = NormJobDev{J.w, J.n, J.k, J.ldw, J.norms, (J.k + 7) / 8, groups};
-    groups += (J.k + 7) / 8;
+    nj[i] = NormJobDev{J.w, J.n, J.k, J.ldw, J.norms, (J.k + kNormCols - 1) / kNormCols, groups};
+    groups += (J.k + kNormCols - 1) / kNormCols;
     sj[i] = SelJobDev{J.k, J.norms, J.stats, J.counts, J.raw_idx, J.aligned_idx};
     if (J.k > max_k) max_k = J.k;
   }
@@ -317,7 +344,7 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
   QARVD_CUDA_TRY(cudaMemcpyAsync(d_sj, sj.data(), num_jobs * sizeof(SelJobDev),
                                  cudaMemcpyHostToDevice, s));
   const int64_t blocks_needed = (groups + kNormThreads - 1) / kNormThreads;
-  const int grid = static_cast<int>(blocks_needed < kNumSMs * 8 ? blocks_needed : kNumSMs * 8);
+  const int grid = static_cast<int>(blocks_needed < kNumSMs * 16 ? blocks_needed : kNumSMs * 16);
   if (w_dtype == QARVD_BF16)
     column_norms_kernel<uint16_t><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
   else if (w_dtype == QARVD_F32)
