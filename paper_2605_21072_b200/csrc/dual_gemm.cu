@@ -842,7 +842,7 @@ TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
     const int v = atoi(env);
     if (v == 1 || v == 2) c.ks = v;
   }
-  if (c.bn == 192) c.ks = 1;  // 80 KB stages would leave two stages only
+  if (c.bn == 192 && c.cg == 2) c.ks = 1;
   return c;
 }
 
@@ -887,7 +887,8 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   }
   if (c.bn == 256) return c.ks == 2 ? launch_gemm<256, 1, 2>(xq, ldq, wq, ldw, p, stream)
                                     : launch_gemm<256, 1, 1>(xq, ldq, wq, ldw, p, stream);
-  if (c.bn == 192) return launch_gemm<192, 1, 1>(xq, ldq, wq, ldw, p, stream);
+  if (c.bn == 192) return c.ks == 2 ? launch_gemm<192, 1, 2>(xq, ldq, wq, ldw, p, stream)
+                                    : launch_gemm<192, 1, 1>(xq, ldq, wq, ldw, p, stream);
   return c.ks == 2 ? launch_gemm<128, 1, 2>(xq, ldq, wq, ldw, p, stream)
                    : launch_gemm<128, 1, 1>(xq, ldq, wq, ldw, p, stream);
 }
