@@ -34,6 +34,8 @@ constexpr int BK = 128;  // bytes (= int8 elements) of K per 128B-swizzle sub-ti
 // register file allows (96 registers x 640 threads) in 16-column chunks.
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kCtrlRegs = 32;   // setmaxnreg split of 640 x 96 registers
+constexpr int kEpiRegs = 112;   //   (4 x 32 x 32 + 16 x 32 x 112 = 640 x 96)
 constexpr int CW = 16;            // columns per epilogue chunk (one tcgen05.ld .32x32b.x16)
 constexpr int kYStageBytes = 32 * CW * 2;  // one warp's bf16 staging tile: 32 rows x 32 B
 
@@ -51,7 +53,7 @@ struct GemmCfg {
   // y staging: one 32 x 16 bf16 tile per epilogue warp, double-buffered unless the operand
   // stages need the room
   static constexpr int kYBufs = KS == 2 ? 1 : 2;
-  static constexpr int kEpiBytes = 512 /*barriers*/ + 2 * 3 * 256 * 4 /*scales, 2 buffers*/ +
+  static constexpr int kEpiBytes = 512 /*barriers*/ + 3 * BN * 4 * 4 /*scales: 16 warps x 3 x BN/4*/ +
                                    kEpiWarps * kYStageBytes * kYBufs /*y staging*/;
   static constexpr int kStages = (227 * 1024 - kEpiBytes) / (kABytes + kBBytes) > 8
                                      ? 8
@@ -82,6 +84,8 @@ struct GemmParams {
   uint32_t* row_pmax;    // optional: per-row partial maxima, [m][pm_count] (one per epilogue
   int pm_count;          //   warp and tile: pm_count = num_n_blks * 4), plain stores
   int use_tma_store;  // bf16 output through the TMA store path
+  int direct_store;   // QARVD_GEMM_DIRECT=1: fast path stores bf16 rows from registers
+  int epi_regs;       // fast path holds acc_n in registers (QARVD_GEMM_EPIREG=0 disables)
   int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
 };
@@ -119,30 +123,32 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // gelu(v) = 0.5 v (1 + erf(v/sqrt 2)) on a pair (toy_model.cpp:62-66 uses the erf form).
 // erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the bf16 output
-// resolution): t = 1/(1 + p|z|), erf = 1 - t*P(t)*exp(-z^2).  One rcp + one ex2 per
-// element, the polynomial on packed FMAs; erff's two-range coefficient selection cost
-// more than the whole dequant epilogue.
+// resolution): one rcp + one ex2 per element, the rest on packed FMAs (erff's two-range
+// coefficient selection cost more than the whole dequant epilogue).  The epilogue is
+// issue-bound (scripts/epi_rate.cu), so the form below minimises instructions.
+// Non-finite v -> NaN (inputs are finite int32 accumulators times finite scales).
 __device__ __forceinline__ uint64_t gelu2(uint64_t v) {
-  const uint64_t h = mul2(v, pk2(0.5f, 0.5f));
-  const uint64_t z = mul2(v, pk2(0.70710678118654752f, 0.70710678118654752f));
-  float z0, z1;
-  upk2(z, z0, z1);
-  const uint64_t a = pk2(fabsf(z0), fabsf(z1));
+  // gelu(v) = h (1 + erf z), h = v/2, z = v/sqrt2.  With erf|z| = 1 - E (A&S 7.1.26:
+  // E = t P(t) exp(-z^2), t = 1/(1 + p|z|)) and sign z = sign h:  gelu = max(v, 0) - |h| E.
+  // In w = v sqrt(log2(e)/2): exp(-z^2) = 2^(-w^2), p|z| = p'|w|, and |h| P(t) = |w| Q(t)
+  // with Q = -P / (2 sqrt(log2(e)/2)) folded into the coefficients.  No cancellation for
+  // v < 0 (|error| <= 3.4e-7 absolute over [-10, 10], checked in f32 against scipy's erf).
+  const uint64_t w = mul2(v, pk2(0.8493218f, 0.8493218f));
+  float w0, w1, v0, v1;
+  upk2(w, w0, w1);
+  upk2(v, v0, v1);
+  const uint64_t aw = pk2(fabsf(w0), fabsf(w1));
   float d0, d1;
-  upk2(fma2(pk2(0.3275911f, 0.3275911f), a, pk2(1.0f, 1.0f)), d0, d1);
+  upk2(fma2(pk2(0.272737481f, 0.272737481f), aw, pk2(1.0f, 1.0f)), d0, d1);
   const uint64_t t = pk2(rcp_approx(d0), rcp_approx(d1));
-  // negated coefficients: q = -(t * P(t))
-  uint64_t q = fma2(pk2(-1.061405429f, -1.061405429f), t, pk2(1.453152027f, 1.453152027f));
-  q = fma2(q, t, pk2(-1.421413741f, -1.421413741f));
-  q = fma2(q, t, pk2(0.284496736f, 0.284496736f));
-  q = fma2(q, t, pk2(-0.254829592f, -0.254829592f));
-  q = mul2(q, t);
+  uint64_t q = fma2(pk2(-0.624854695f, -0.624854695f), t, pk2(0.85547788f, 0.85547788f));
+  q = fma2(q, t, pk2(-0.836793392f, -0.836793392f));
+  q = fma2(q, t, pk2(0.167484654f, 0.167484654f));
+  q = fma2(q, t, pk2(-0.150019458f, -0.150019458f));
+  const uint64_t g = mul2(mul2(aw, t), q);
   float s0, s1;
-  upk2(mul2(mul2(a, pk2(-1.4426950408889634f, -1.4426950408889634f)), a), s0, s1);
-  float r0, r1;
-  upk2(fma2(q, pk2(ex2_approx(s0), ex2_approx(s1)), pk2(1.0f, 1.0f)), r0, r1);
-  const uint64_t erfv = pk2(copysignf(r0, z0), copysignf(r1, z1));
-  return fma2(h, erfv, h);
+  upk2(mul2(w, w), s0, s1);
+  return fma2(g, pk2(ex2_approx(-s0), ex2_approx(-s1)), pk2(fmaxf(v0, 0.f), fmaxf(v1, 0.f)));
 }
 
 // y = s_x * (s_wo*acc_o + s_wn*acc_n) (+ bias) [gelu], written back into rn as float bits.
@@ -250,6 +256,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // launch -- its CTAs only fit on SMs this grid has left
   pdl_wait();
   pdl_launch_dependents();
+  // 640 threads x 96 registers: the control warpgroup (producer, MMA issuer, TMEM owner)
+  // needs few, the epilogue holds a warp's whole acc_n slice (64 registers) -> 32 / 112,
+  // set inside each role branch so ptxas sizes every branch by its own limit
 
   const int num_kb = static_cast<int>((p.k + SK - 1) / SK);
   // one-stage TMEM: k-blocks holding outlier steps are issued last (see the MMA issuer)
@@ -261,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ===================== TMA producer (whole warp loops, lane 0 issues) ==============
+    ptx::setmaxnreg_dec<kCtrlRegs>();
     int stage = 0;
     uint32_t phase = 0;
     const int rot = kblock_rotation(static_cast<int>(p.k_o / 32), num_kb);  // = the MMA issuer's
@@ -304,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
+    ptx::setmaxnreg_dec<kCtrlRegs>();
     // The whole warp runs the (warp-uniform) loop so descriptors, accumulator addresses
     // and slab routing live in uniform registers; lane 0 issues.
     //
@@ -402,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue: 16 warps, 4 per TMEM lane quadrant =====================
+    ptx::setmaxnreg_inc<kEpiRegs>();
     // Warp w may only touch TMEM lanes 32*(w%4)..+31; the four warps of a quadrant take
     // every fourth 16-column chunk.  Each tile's column scales are prefetched one tile
     // ahead; bf16 results go through a 32B-swizzled staging tile and a TMA bulk tensor store.
@@ -417,16 +429,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                           !p.acc_o_dbg;
     const int epi_mode = (has_outlier ? 1 : 0) | (p.bias ? 2 : 0) | (gelu && !two_step ? 4 : 0);
     uint8_t* ystage0 = epi_ystage + ew * kYStageBytes * C::kYBufs;  // kYBufs x (32 rows x 32 B, SWIZZLE_32B)
-    int ybuf = 0, sbuf = 0;
-    float pf_n = 0.f, pf_o = 0.f, pf_b = 0.f, pf_x = 0.f;
+    int ybuf = 0;
+    // Column scales: every warp stages the 64 (BN / kSubs) columns it owns in a private
+    // [3][WC] slot (s_wn, s_wo, bias), prefetched one tile ahead -- no cross-warp barrier, so
+    // the 16 warps drift freely between the TMEM handshakes.
+    constexpr int WC = BN / kSubs;
+    float* wsc = epi_scales + ew * 3 * WC;
+    auto scol = [&](int c) { return wsc + ((c - half) / kSubs) * CW; };  // chunk c's scales
+    float pf_n[WC / 32], pf_o[WC / 32], pf_b[WC / 32], pf_x = 0.f;
+#pragma unroll
+    for (int u = 0; u < WC / 32; ++u) pf_n[u] = pf_o[u] = pf_b[u] = 0.f;
     auto prefetch = [&](int tt) {
       if (tt >= p.num_tiles || p.out_dtype == QARVD_F64) return;
-      if (etid < BN) {
-        const int64_t j = static_cast<int64_t>(tt / p.num_m_blks) * BN + etid;
+#pragma unroll
+      for (int u = 0; u < WC / 32; ++u) {
+        const int jl = lane + 32 * u;
+        const int64_t j = static_cast<int64_t>(tt / p.num_m_blks) * BN +
+                          (half + (jl / CW) * kSubs) * CW + jl % CW;
         const int64_t jc = j < p.n ? j : p.n - 1;
-        pf_n = __ldg(p.scale_wn + jc);
-        if (has_outlier) pf_o = __ldg(p.scale_wo + jc);
-        if (p.bias) pf_b = __ldg(p.bias + jc);
+        pf_n[u] = __ldg(p.scale_wn + jc);
+        if (has_outlier) pf_o[u] = __ldg(p.scale_wo + jc);
+        if (p.bias) pf_b[u] = __ldg(p.bias + jc);
       }
       const int64_t r = static_cast<int64_t>(tt % p.num_m_blks) * TM + rank * BM + q * 32 + lane;
       pf_x = (r < p.m && p.scale_x) ? __ldg(p.scale_x + r) : 0.f;
@@ -511,20 +534,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
       const int m_blk = t % p.num_m_blks;
       const int n_blk = t / p.num_m_blks;
-      float* sc = epi_scales + sbuf * 3 * BN;
-      if (etid < BN) {
-        sc[etid] = pf_n;
-        sc[BN + etid] = pf_o;
-        sc[2 * BN + etid] = pf_b;
+#pragma unroll
+      for (int u = 0; u < WC / 32; ++u) {
+        wsc[lane + 32 * u] = pf_n[u];
+        wsc[WC + lane + 32 * u] = pf_o[u];
+        wsc[2 * WC + lane + 32 * u] = pf_b[u];
       }
       const float sx = pf_x;
       prefetch(t + num_ctas);
-      sbuf ^= 1;
       const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM + q * 32;
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.m;
       tile_mx = 0;
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // scales visible to all epilogue warps
+      __syncwarp();  // this warp's scales visible to its lanes
       const long long te0 = clock64();
       ptx::mbar_wait(&tfull[acc], acc_phase);
       const long long te1 = clock64();
@@ -536,9 +558,114 @@ __global__ void __launch_bounds__(kThreads, 1)
       // outputs): compile-time chunk loops with the per-chunk checks hoisted to the tile.
       const bool fast = two_step && p.use_tma_store && !p.row_absmax &&
                         static_cast<int64_t>(n_blk + 1) * BN <= p.n;
-      if (fast) {
-        auto phase1 = [&](auto ho, auto hb) {
-          constexpr bool HO = decltype(ho)::value, HB = decltype(hb)::value;
+      if (fast && p.epi_regs) {
+        // register-held variant: the warp's 4 acc_n chunks (64 columns) are read into
+        // registers and acc_n is released at once; the dequant/GELU/stores then overlap the
+        // next tile's normal-slab MMAs and only acc_o (read chunk by chunk) gates its outliers.
+        constexpr int NCH = BN / CW / kSubs;
+        uint32_t an[NCH][CW];
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) ptx::tmem_ld16(t_n + (half + i * kSubs) * CW, an[i]);
+        ptx::tmem_wait_ld();
+        release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
+        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
+          const int ti = (t - cta_id) / num_ctas;
+          if (ti < 32) s_trace[5][ti] = clock64();
+        }
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        // t = s_wn*acc_n (+ s_wo*acc_o) into the held registers, then acc_o is released too:
+        // the whole y = s_x*t (+ b) [gelu] -> bf16 tail overlaps the next tile's MMAs
+        auto fold = [&](auto ho) {
+          constexpr bool HO = decltype(ho)::value;
+#pragma unroll
+          for (int i = 0; i < NCH; ++i) {
+            const int c = half + i * kSubs;
+            uint32_t ro[CW];
+            if (HO) {
+              ptx::tmem_ld16(t_o + c * CW, ro);
+              ptx::tmem_wait_ld();
+            }
+            const float* scc = scol(c);
+#pragma unroll
+            for (int e4 = 0; e4 < CW / 4; ++e4) {
+              const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
+              float4 so4 = sn4;
+              if (HO) so4 = reinterpret_cast<const float4*>(scc + WC)[e4];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = 4 * e4 + 2 * h;
+                const uint64_t sn = h ? pk2(sn4.z, sn4.w) : pk2(sn4.x, sn4.y);
+                const uint64_t a2 = pk2(__int2float_rn(static_cast<int>(an[i][e])),
+                                        __int2float_rn(static_cast<int>(an[i][e + 1])));
+                uint64_t tt;
+                if (HO) {
+                  const uint64_t so = h ? pk2(so4.z, so4.w) : pk2(so4.x, so4.y);
+                  const uint64_t ao = pk2(__int2float_rn(static_cast<int>(ro[e])),
+                                          __int2float_rn(static_cast<int>(ro[e + 1])));
+                  tt = fma2(sn, a2, mul2(so, ao));
+                } else {
+                  tt = mul2(sn, a2);
+                }
+                float y0, y1;
+                upk2(tt, y0, y1);
+                an[i][e] = __float_as_uint(y0);
+                an[i][e + 1] = __float_as_uint(y1);
+              }
+            }
+          }
+        };
+        if (has_outlier) fold(T_{});
+        else fold(F_{});
+        release(&tofree[0]);  // acc_o free: the next tile's outlier steps may issue
+        const uint64_t sx2 = pk2(sx, sx);
+        auto tail = [&](auto hb, auto gl) {
+          constexpr bool HB = decltype(hb)::value, GL = decltype(gl)::value;
+#pragma unroll
+          for (int i = 0; i < NCH; ++i) {
+            const int c = half + i * kSubs;
+            const float* scb = scol(c) + 2 * WC;
+#pragma unroll
+            for (int e4 = 0; e4 < CW / 4; ++e4) {
+              float4 sb4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (HB) sb4 = reinterpret_cast<const float4*>(scb)[e4];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = 4 * e4 + 2 * h;
+                const uint64_t tt = pk2(__uint_as_float(an[i][e]), __uint_as_float(an[i][e + 1]));
+                uint64_t v;
+                if (HB) v = fma2(sx2, tt, h ? pk2(sb4.z, sb4.w) : pk2(sb4.x, sb4.y));
+                else v = mul2(sx2, tt);
+                if (GL) v = gelu2(v);
+                float y0, y1;
+                upk2(v, y0, y1);
+                an[i][e] = __float_as_uint(y0);
+                an[i][e + 1] = __float_as_uint(y1);
+              }
+            }
+            if (p.debug & 32) {  // diagnostic: math without stores
+#pragma unroll
+              for (int e = 0; e < CW; ++e) tile_mx ^= an[i][e];
+            } else {
+              store_chunk(an[i], row0, row, static_cast<int64_t>(n_blk) * BN + c * CW, CW);
+            }
+          }
+          if ((p.debug & 32) && tile_mx == 0x12345678u) p.acc_o_dbg[0] = 1;
+        };
+        if (p.debug & 16) {  // diagnostic: no tail (fold + releases only)
+        } else if (gelu) {
+          if (p.bias) tail(T_{}, T_{});
+          else tail(F_{}, T_{});
+        } else {
+          if (p.bias) tail(T_{}, F_{});
+          else tail(F_{}, F_{});
+        }
+      } else if (fast) {
+        // phase 1 (blocks the next tile's normal slab): t = s_wn*acc_n (+ s_wo*acc_o), folded
+        // into acc_o's columns as f32 bits; phase 2 (overlaps the next tile's MMAs):
+        // y = s_x*t (+ b) [gelu] -> bf16.  Same per-element op order as epi_math.
+        auto phase1 = [&](auto ho) {
+          constexpr bool HO = decltype(ho)::value;
 #pragma unroll
           for (int i = 0; i < BN / CW / kSubs; ++i) {
             const int c = half + i * kSubs;
@@ -546,47 +673,121 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_ld16(t_n + c * CW, rn);
             if (HO) ptx::tmem_ld16(t_o + c * CW, ro);
             ptx::tmem_wait_ld();
-            epi_math<HO, HB, false>(rn, ro, sc + c * CW, BN, sx);
-            ptx::tmem_st16(t_o + c * CW, rn);  // fold y into acc_o's columns
+            const float* scc = scol(c);
+#pragma unroll
+            for (int e4 = 0; e4 < CW / 4; ++e4) {
+              const float4 sn4 = reinterpret_cast<const float4*>(scc)[e4];
+              float4 so4 = sn4;
+              if (HO) so4 = reinterpret_cast<const float4*>(scc + WC)[e4];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = 4 * e4 + 2 * h;
+                const uint64_t sn = h ? pk2(sn4.z, sn4.w) : pk2(sn4.x, sn4.y);
+                const uint64_t an = pk2(__int2float_rn(static_cast<int>(rn[e])),
+                                        __int2float_rn(static_cast<int>(rn[e + 1])));
+                uint64_t tt;
+                if (HO) {
+                  const uint64_t so = h ? pk2(so4.z, so4.w) : pk2(so4.x, so4.y);
+                  const uint64_t ao = pk2(__int2float_rn(static_cast<int>(ro[e])),
+                                          __int2float_rn(static_cast<int>(ro[e + 1])));
+                  tt = fma2(sn, an, mul2(so, ao));
+                } else {
+                  tt = mul2(sn, an);
+                }
+                float y0, y1;
+                upk2(tt, y0, y1);
+                rn[e] = __float_as_uint(y0);
+                rn[e + 1] = __float_as_uint(y1);
+              }
+            }
+            ptx::tmem_st16(t_o + c * CW, rn);  // fold t into acc_o's columns
           }
         };
         using T_ = std::true_type;
         using F_ = std::false_type;
-        if (has_outlier) {
-          if (p.bias) phase1(T_{}, T_{});
-          else phase1(T_{}, F_{});
-        } else {
-          if (p.bias) phase1(F_{}, T_{});
-          else phase1(F_{}, F_{});
-        }
+        if (has_outlier) phase1(T_{});
+        else phase1(F_{});
         ptx::tmem_wait_st();
         release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
         if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
           const int ti = (t - cta_id) / num_ctas;
           if (ti < 32) s_trace[5][ti] = clock64();
         }
-        auto phase2 = [&](auto gl) {
-          constexpr bool GL = decltype(gl)::value;
+        const uint64_t sx2 = pk2(sx, sx);
+        auto phase2 = [&](auto gl, auto hb, auto direct) {
+          constexpr bool GL = decltype(gl)::value, HB = decltype(hb)::value;
+          constexpr bool DS = decltype(direct)::value;
 #pragma unroll
           for (int i = 0; i < BN / CW / kSubs; ++i) {
             const int c = half + i * kSubs;
             uint32_t rn[CW];
             ptx::tmem_ld16(t_o + c * CW, rn);
             ptx::tmem_wait_ld();
-            if (GL) {
+            const float* scb = scol(c) + 2 * WC;
 #pragma unroll
-              for (int e = 0; e < CW; e += 2) {
+            for (int e4 = 0; e4 < CW / 4; ++e4) {
+              float4 sb4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (HB) sb4 = reinterpret_cast<const float4*>(scb)[e4];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = 4 * e4 + 2 * h;
+                const uint64_t tt = pk2(__uint_as_float(rn[e]), __uint_as_float(rn[e + 1]));
+                uint64_t v;
+                if (HB) v = fma2(sx2, tt, h ? pk2(sb4.z, sb4.w) : pk2(sb4.x, sb4.y));
+                else v = mul2(sx2, tt);
+                if (GL) v = gelu2(v);
                 float y0, y1;
-                upk2(gelu2(pk2(__uint_as_float(rn[e]), __uint_as_float(rn[e + 1]))), y0, y1);
+                upk2(v, y0, y1);
                 rn[e] = __float_as_uint(y0);
                 rn[e + 1] = __float_as_uint(y1);
               }
             }
-            store_chunk(rn, row0, row, static_cast<int64_t>(n_blk) * BN + c * CW, CW);
+            const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * CW;
+            if (DS) {
+              uint32_t pk[CW / 2];
+#pragma unroll
+              for (int e = 0; e < CW / 2; ++e) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(rn[2 * e]),
+                                                                __uint_as_float(rn[2 * e + 1]));
+                pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                if (p.row_pmax) tile_mx = __vmaxu2(tile_mx, pk[e] & 0x7fff7fffu);
+              }
+              if (row_ok) {
+                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.y) +
+                                                      row * p.ldy + col0);
+                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              }
+            } else {
+              store_chunk(rn, row0, row, col0, CW);
+            }
           }
         };
-        if (gelu) phase2(T_{});
-        else phase2(F_{});
+        const bool direct = p.direct_store != 0;
+        auto phase2_b = [&](auto gl, auto hb) {
+          if (p.debug & 4) {  // diagnostic: phase 2 reads TMEM only (no math, no stores)
+#pragma unroll
+            for (int i = 0; i < BN / CW / kSubs; ++i) {
+              uint32_t rn[CW];
+              ptx::tmem_ld16(t_o + (half + i * kSubs) * CW, rn);
+              ptx::tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < CW; ++e) tile_mx ^= rn[e];
+            }
+            if (tile_mx == 0x12345678u) p.acc_o_dbg[0] = 1;
+            return;
+          }
+          if (p.debug & 8) phase2(F_{}, F_{}, F_{});  // diagnostic: stores without GELU
+          else if (direct) phase2(gl, hb, T_{});
+          else phase2(gl, hb, F_{});
+        };
+        if (gelu) {
+          if (p.bias) phase2_b(T_{}, T_{});
+          else phase2_b(T_{}, F_{});
+        } else {
+          if (p.bias) phase2_b(F_{}, T_{});
+          else phase2_b(F_{}, F_{});
+        }
         release(&tofree[0]);  // acc_o free
       } else {
 #pragma unroll 1
@@ -628,16 +829,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         {
-          const float* scc = sc + c * CW;
+          const float* scc = scol(c);
           switch (epi_mode) {
-            case 0: epi_math<false, false, false>(rn, ro, scc, BN, sx); break;
-            case 1: epi_math<true, false, false>(rn, ro, scc, BN, sx); break;
-            case 2: epi_math<false, true, false>(rn, ro, scc, BN, sx); break;
-            case 3: epi_math<true, true, false>(rn, ro, scc, BN, sx); break;
-            case 4: epi_math<false, false, true>(rn, ro, scc, BN, sx); break;
-            case 5: epi_math<true, false, true>(rn, ro, scc, BN, sx); break;
-            case 6: epi_math<false, true, true>(rn, ro, scc, BN, sx); break;
-            default: epi_math<true, true, true>(rn, ro, scc, BN, sx); break;
+            case 0: epi_math<false, false, false>(rn, ro, scc, WC, sx); break;
+            case 1: epi_math<true, false, false>(rn, ro, scc, WC, sx); break;
+            case 2: epi_math<false, true, false>(rn, ro, scc, WC, sx); break;
+            case 3: epi_math<true, true, false>(rn, ro, scc, WC, sx); break;
+            case 4: epi_math<false, false, true>(rn, ro, scc, WC, sx); break;
+            case 5: epi_math<true, false, true>(rn, ro, scc, WC, sx); break;
+            case 6: epi_math<false, true, true>(rn, ro, scc, WC, sx); break;
+            default: epi_math<true, true, true>(rn, ro, scc, WC, sx); break;
           }
         }
         if (two_step) ptx::tmem_st16(t_o + c * CW, rn);  // fold y into acc_o's columns
@@ -693,6 +894,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) ptx::bulk_wait_all();
+  } else {
+    ptx::setmaxnreg_dec<kCtrlRegs>();  // warps 2-3
   }
 
   ptx::tc_fence_before();
@@ -798,6 +1001,12 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   std::memset(&ty, 0, sizeof(ty));
   p.use_tma_store = p.out_dtype == QARVD_BF16 && !p.acc_n_dbg && !p.acc_o_dbg &&
                     (reinterpret_cast<uintptr_t>(p.y) & 15) == 0 && (p.ldy * 2) % 16 == 0;
+  {
+    const char* e = std::getenv("QARVD_GEMM_DIRECT");
+    p.direct_store = (e && e[0] == '1') ? 1 : 0;
+    const char* r = std::getenv("QARVD_GEMM_EPIREG");
+    p.epi_regs = (r && r[0] == '0') ? 0 : 1;
+  }
   if (p.use_tma_store) {
     st = make_y_tmap(&ty, p.y, p.m, p.n, p.ldy);
     if (st) return st;

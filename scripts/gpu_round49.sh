@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for d in 0 4 8; do
+QARVD_GEMM_DEBUG=$d timeout 300 python scripts/gemm_trace.py ffn0 8960 1536 32 1 > gpurun_out/tr49_$d.log 2>&1
+done
+timeout 300 python scripts/gemm_trace.py ffn0 8960 1536 32 0 > gpurun_out/tr49_nogelu.log 2>&1
