@@ -86,6 +86,7 @@ struct GemmParams {
   int use_tma_store;  // bf16 output through the TMA store path
   int direct_store;   // QARVD_GEMM_DIRECT=1: fast path stores bf16 rows from registers
   int epi_regs;       // fast path holds acc_n in registers (QARVD_GEMM_EPIREG=0 disables)
+  int spin;
   int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
 };
@@ -261,6 +262,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // set inside each role branch so ptxas sizes every branch by its own limit
 
   const int num_kb = static_cast<int>((p.k + SK - 1) / SK);
+  // producer / MMA-issuer waits (QARVD_GEMM_SPIN=1: retry without the suspend hint)
+  auto ctl_wait = [&](uint64_t* bar, uint32_t parity) {
+    if (p.spin) ptx::mbar_wait_spin(bar, parity);
+    else ptx::mbar_wait(bar, parity);
+  };
   // one-stage TMEM: k-blocks holding outlier steps are issued last (see the MMA issuer)
   auto kblock_rotation = [&](int ko32_, int nkb) {
     if (C::kAccStages != 1) return 0;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
       for (int i = 0; i < num_kb; ++i) {
         const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
-        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ctl_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           if (p.debug == 2) {
             if (leader) ptx::mbar_arrive(&full[stage]);
@@ -351,10 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // before the first outlier step
           const bool wait_o = C::kAccStages == 1 && ko32 > 0 && kb == 0;
           if (C::kAccStages == 1) {
-            if (kb == kb_first_n) ptx::mbar_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
+            if (kb == kb_first_n) ctl_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
             ptx::tc_fence_after();
           }
-          ptx::mbar_wait(&full[stage], phase);
+          ctl_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (C::kABytes >> 4));
           const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (C::kBBytes >> 4));
@@ -377,13 +383,29 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
+          // all SPB steps of this block are normal and inside K: straight-line issue
+          const bool plain = kb * SPB >= ko32 && (kb + 1) * SPB <= k32;
+          if (plain) {
+            if (p.debug != 1 && ptx::elect_one()) {
+              const uint32_t acc0 = kb * SPB == first_n ? 0u : 1u;
+#pragma unroll
+              for (int j = 0; j < SPB; ++j) {
+                constexpr uint64_t kA = C::kASub >> 4, kB = C::kBSub >> 4;
+                const uint64_t ao = static_cast<uint64_t>(j >> 2) * kA + 2 * (j & 3);
+                const uint64_t bo = static_cast<uint64_t>(j >> 2) * kB + 2 * (j & 3);
+                if (CG == 1) ptx::mma_i8(d_n, ad + ao, bd + bo, idesc, j == 0 ? acc0 : 1u);
+                else ptx::mma_i8_2sm(d_n, ad + ao, bd + bo, idesc, j == 0 ? acc0 : 1u);
+              }
+            }
+          } else {
           issue(false);
           if (wait_o) {
             __syncwarp();
-            ptx::mbar_wait(&tofree[0], acc_phase ^ 1);  // acc_o free
+            ctl_wait(&tofree[0], acc_phase ^ 1);  // acc_o free
             ptx::tc_fence_after();
           }
           issue(true);
+          }
           __syncwarp();
           if (lane == 0) {
             if (CG == 1) ptx::mma_commit(&empty[stage]);
@@ -1006,6 +1028,8 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
     p.direct_store = (e && e[0] == '1') ? 1 : 0;
     const char* r = std::getenv("QARVD_GEMM_EPIREG");
     p.epi_regs = (r && r[0] == '0') ? 0 : 1;
+    const char* sp = std::getenv("QARVD_GEMM_SPIN");
+    p.spin = (sp && sp[0] == '1') ? 1 : 0;
   }
   if (p.use_tma_store) {
     st = make_y_tmap(&ty, p.y, p.m, p.n, p.ldy);

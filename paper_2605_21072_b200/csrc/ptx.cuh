@@ -156,6 +156,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers
+// one elected lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // warpgroup register rebalancing (all 4 warps of a warpgroup execute the same one)
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {
