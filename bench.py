@@ -312,6 +312,86 @@ def calibration_bench(torch, world, rank, steps, hbm_peak):
             "sharding": f"LPT over {world} rank(s), one all_gather of packed records"}
 
 
+def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
+    """Config 3: all 300 quantized linears of the 30-block Wan-1.3B-shaped stack, one chunk
+    (M = 4680 tokens, cross k/v on 512 text tokens), K1 + K2 per layer, one CUDA graph.
+    With ``rollouts`` > 0 also config 5: that many independent 7-chunk x 4-step AR rollouts,
+    split over the ranks (8/G per GPU) and batched along M, each denoising step one stack
+    forward plus the z -= y/T update (the stack's attention / KV-cache glue is elided, §7)."""
+    import torch.distributed as dist
+    from paper_2605_21072_b200 import synth
+    from paper_2605_21072_b200.pipeline import QuantizedChain, wan_stack_chain
+
+    chain = wan_stack_chain()
+    chain.x.copy_(synth.synth_activation(chain.m, synth.WAN_DIM, seed=11 + rank))
+    chain.ctx.copy_(synth.synth_activation(synth.WAN_TEXT_LEN, synth.WAN_DIM, seed=13 + rank))
+    chain.capture()
+    for _ in range(3):
+        chain.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    for _ in range(steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        chain.replay()
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    t = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in evs]))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ops = chain.int_ops()
+    out = {"workload": "wan_stack_30blocks_300_linears_M4680_text512", "int_ops_per_forward": ops,
+           "ms_per_forward": ms, "value": world * ops / (ms * 1e-3) / 1e12, "unit": "TOPS",
+           "frac_of_peak": ops / (ms * 1e-3) / 1e12 / peak, "kernels_per_forward": chain.kernels_per_step(),
+           "steps": steps, "l2": "flushed before every forward (weights 1.4 GB > L2 anyway)"}
+    if rollouts > 0:
+        per = max(1, rollouts // world)
+        chunks, tsteps = 7, 4
+        rc = QuantizedChain(chain.layers, per * chain.m, epilogues=chain.epilogues, inputs=chain.inputs,
+                            ms=[per * mi for mi in chain.ms], ctx_rows=per * chain.ctx.shape[0])
+        del chain
+        rc.ctx.copy_(synth.synth_activation(rc.ctx.shape[0], synth.WAN_DIM, seed=17 + rank))
+        z = torch.empty_like(rc.x)
+
+        def denoise_step():  # one AR denoising step: f = stack(z); z -= f / T
+            rc.x.copy_(z)
+            rc.launch()
+            z.sub_(rc.output, alpha=1.0 / tsteps)
+
+        rc.launch()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(tsteps):
+                denoise_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for c in range(chunks):
+            z.copy_(synth.synth_activation(rc.x.shape[0], synth.WAN_DIM, seed=1000 + c, frame=rank))
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rms = float(t.item())
+        rops = rc.int_ops() * chunks * tsteps
+        out["rollouts"] = {"workload": f"{per * world} x 7-chunk x 4-step AR rollouts, {per} per GPU batched along M",
+                           "rollouts_per_gpu": per, "ms": rms, "int_ops_per_gpu": rops,
+                           "value": world * rops / (rms * 1e-3) / 1e12, "unit": "TOPS",
+                           "rollouts_per_s": per * world / (rms * 1e-3),
+                           "parallelism": f"data-parallel x{world}, no collective"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -321,6 +401,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-calib", action="store_true")
     ap.add_argument("--calib-steps", type=int, default=5)
+    ap.add_argument("--no-stack", action="store_true")
+    ap.add_argument("--stack-steps", type=int, default=10)
+    ap.add_argument("--rollouts", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args.gpus)
@@ -424,6 +507,12 @@ def main():
     if not args.no_calib:
         calib = calibration_bench(torch, world, rank, args.calib_steps, peaks.get("hbm_gbs", 6650.0))
 
+    stack = None
+    if not args.no_stack:
+        stack = stack_bench(torch, world, rank, args.stack_steps, 2.0 * peaks.get("bf16_tflops", 1590.0),
+                            flush, rollouts=args.rollouts)
+        torch.cuda.empty_cache()
+
     if rank == 0:
         gemm = float(np.mean(gemm_ms))
         achieved = ops_per_step / (gemm * 1e-3) / 1e12
@@ -466,6 +555,7 @@ def main():
                     "ms_per_step": e2e, "path": "qarvd_linear_chain_forward_host (C-ABI, pinned host buffers)"},
             "gpu_launches": int(launches),
             "calibration": calib,
+            "stack": stack,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

@@ -56,6 +56,11 @@ def lib():
         _o.oracle_weighting.argtypes = [c_int, c_void_p, c_int64, c_void_p]
         _o.oracle_round_half_even.restype = c_double
         _o.oracle_round_half_even.argtypes = [c_double]
+        _o.oracle_weighted_loss.restype = c_int
+        _o.oracle_weighted_loss.argtypes = [c_void_p, c_void_p, c_double, c_void_p, c_void_p,
+                                            c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                            c_int64, c_void_p, c_void_p, c_int64, c_void_p,
+                                            c_int64, c_void_p, c_void_p]
         _o.oracle_num_threads.restype = c_int
         _o.oracle_row_scale_formula_mismatches.restype = c_int64
     return _o
@@ -86,6 +91,9 @@ def ref():
         _r.ref_percentile_search.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p,
                                              c_void_p, c_void_p]
         _r.ref_weighting.argtypes = [c_int, c_void_p, c_int64, c_void_p]
+        _r.ref_weighted_loss.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
+                                         c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
         _r.ref_toy_weight.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
                                       ctypes.c_char_p, c_double, c_double, ctypes.c_char_p,
                                       c_void_p, c_void_p, c_void_p]
@@ -332,3 +340,50 @@ def ref_toy_weight(layer, blocks=2, hidden=64, seed=1, pattern="", fraction=0.02
 def row_scale_formula_mismatches() -> int:
     """Mismatches of the device row-scale formula vs fl(amax/qmax) over all bf16 amax, 2..8 bits."""
     return int(lib().oracle_row_scale_formula_mismatches())
+
+
+def weighted_loss(x64, xq, s_x, w64, codes, s_wo, s_wn, outlier_mask, row_off, chunks, chunk_w):
+    """oracle_weighted_loss: Eq. 5 over stacked samples (calibrate.cpp:201-224); all in
+    ORIGINAL column order.  Returns (loss, per-sample errors)."""
+    x64 = np.ascontiguousarray(x64, dtype=np.float64)
+    m, k = x64.shape
+    w64 = np.ascontiguousarray(w64, dtype=np.float64)
+    n = w64.shape[0]
+    xq = np.ascontiguousarray(xq, dtype=np.int32)
+    codes = np.ascontiguousarray(codes, dtype=np.int32)
+    ro = np.ascontiguousarray(row_off, dtype=np.int64)
+    ch = np.ascontiguousarray(chunks, dtype=np.int64)
+    cw = np.ascontiguousarray(chunk_w, dtype=np.float64)
+    err = np.empty(max(1, len(ch)))
+    loss = c_double()
+    st = lib().oracle_weighted_loss(_p(x64), _p(xq), float(s_x), _p(w64), _p(codes),
+                                    _p(np.ascontiguousarray(s_wo, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(s_wn, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(outlier_mask, dtype=np.uint8)), m, n, k,
+                                    _p(ro), _p(ch), len(ch), _p(cw), len(cw), _p(err),
+                                    ctypes.byref(loss))
+    if st == 1:
+        raise ValueError("weighted loss: empty batch")
+    if st == 2:
+        raise IndexError("weighted loss: sample chunk outside the weight vector")
+    return loss.value, err[:len(ch)]
+
+
+def ref_weighted_loss(w64, outliers, act_scale, x64, row_off, chunks, chunk_w):
+    """The reference weighted_loss on a LearnableQuantState::init state; returns the loss and
+    the state's deployable quantities (hard codes, group scales, act scale, outlier mask)."""
+    w64 = np.ascontiguousarray(w64, dtype=np.float64)
+    n, k = w64.shape
+    x64 = np.ascontiguousarray(x64, dtype=np.float64)
+    o = np.ascontiguousarray(outliers, dtype=np.int64)
+    ro = np.ascontiguousarray(row_off, dtype=np.int64)
+    ch = np.ascontiguousarray(chunks, dtype=np.int64)
+    cw = np.ascontiguousarray(chunk_w, dtype=np.float64)
+    loss, act = c_double(), c_double()
+    codes = np.empty((n, k), dtype=np.int32)
+    so, sn = np.empty(n), np.empty(n)
+    mask = np.empty(k, dtype=np.uint8)
+    _rc(ref().ref_weighted_loss(_p(w64), n, k, _p(o), len(o), float(act_scale), _p(x64), _p(ro),
+                                _p(ch), len(ch), _p(cw), len(cw), ctypes.byref(loss), _p(codes),
+                                _p(so), _p(sn), ctypes.byref(act), _p(mask)))
+    return dict(loss=loss.value, codes=codes, s_wo=so, s_wn=sn, act_scale=act.value, mask=mask)

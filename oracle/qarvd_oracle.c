@@ -442,3 +442,57 @@ int64_t oracle_row_scale_formula_mismatches(void) {
   }
   return bad;
 }
+
+/* ---- Eq. 5 frame-weighted reconstruction loss ------------------------------
+ * weighted_recon_loss (calibrate.cpp:201-216) with the deployable weights:
+ *   (1/B) sum_s w[chunk_s - 1] * || X_s W^T - FQ(X_s) What^T ||_F^2
+ * target = matmul_nt(X, W) (tensor.cpp:82-105: c(i,j) += a(i,k) * b(k,j), k ascending
+ * from 0.0); FQ(X) = (q - 0) * s_x (quant.cpp:140-159, per-tensor act params);
+ * What = s_g(row) * code (calibrate.cpp:128-147, hard rounding); the squared distance
+ * accumulates row-major (tensor.cpp:116-126).  x [m x k] stacks the samples (rows
+ * row_off[s] .. row_off[s+1]); codes / w are in ORIGINAL column order; xq are the
+ * activation codes (row-major [m x k], original order); s_wo / s_wn per output row,
+ * outlier_mask[c] = 1 for outlier columns.  err[s] receives each sample's distance.
+ * Returns 0, or 1 for an empty batch, 2 for a chunk outside [1, n_chunks]. */
+int oracle_weighted_loss(const double* x, const int32_t* xq, double s_x, const double* w,
+                         const int32_t* codes, const double* s_wo, const double* s_wn,
+                         const uint8_t* outlier_mask, int64_t m, int64_t n, int64_t k,
+                         const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
+                         const double* chunk_w, int64_t n_chunks, double* err, double* loss) {
+  if (n_samples <= 0) return 1;
+  (void)m;
+  double* what = (double*)malloc(sizeof(double) * (size_t)(n * k));
+  double* t = (double*)malloc(sizeof(double) * (size_t)n);
+  double* p = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t c = 0; c < k; ++c)
+      what[j * k + c] = (outlier_mask[c] ? s_wo[j] : s_wn[j]) * (double)codes[j * k + c];
+  double total = 0.0;
+  int st = 0;
+  for (int64_t s = 0; s < n_samples && !st; ++s) {
+    if (chunk[s] < 1 || chunk[s] > n_chunks) { st = 2; break; }
+    double acc = 0.0;
+    for (int64_t i = row_off[s]; i < row_off[s + 1]; ++i) {
+      for (int64_t j = 0; j < n; ++j) { t[j] = 0.0; p[j] = 0.0; }
+      for (int64_t c = 0; c < k; ++c) {
+        const double av = x[i * k + c];
+        const double fq = (double)xq[i * k + c] * s_x;
+        for (int64_t j = 0; j < n; ++j) {
+          t[j] += av * w[j * k + c];
+          p[j] += fq * what[j * k + c];
+        }
+      }
+      for (int64_t j = 0; j < n; ++j) {
+        const double d = t[j] - p[j];
+        acc += d * d;
+      }
+    }
+    err[s] = acc;
+    total += chunk_w[chunk[s] - 1] * acc;
+  }
+  if (!st) *loss = total / (double)n_samples;
+  free(what);
+  free(t);
+  free(p);
+  return st;
+}

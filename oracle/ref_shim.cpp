@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "qarvd/calibrate.hpp"
 #include "qarvd/dual_scale.hpp"
 #include "qarvd/engine.hpp"
 #include "qarvd/outlier.hpp"
@@ -287,3 +288,46 @@ double ref_time_linear(const double* x, int64_t m, int64_t k, const int32_t* wq,
 }
 
 }  // extern "C"
+
+// weighted_loss (calibrate.cpp:220-224) on a LearnableQuantState initialised by the reference
+// (LearnableQuantState::init with build_plan(W, aligned outliers) and a per-tensor act scale),
+// over samples x[row_off[s] .. row_off[s+1]) with 1-based chunks.  Also exports the state's
+// deployable quantities: hard codes (original column order), per-row group scales
+// weight_scale(r, g) and act_scale(), so the GPU objective can be run on the same state.
+extern "C" int ref_weighted_loss(const double* w, int64_t n, int64_t k, const int64_t* outliers,
+                                 int64_t n_out, double act_scale, const double* x,
+                                 const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
+                                 const double* chunk_w, int64_t n_chunks, double* loss,
+                                 int32_t* codes, double* s_wo, double* s_wn, double* act_out,
+                                 uint8_t* outlier_mask) {
+  return guarded([&] {
+    const Tensor W = make_tensor(w, n, k);
+    OutlierReport rep;
+    rep.layer_name = "shim";
+    rep.aligned_outliers.assign(outliers, outliers + n_out);
+    const DualScalePlan plan = build_plan(W, rep, 8);
+    CalibConfig cfg;
+    const LearnableQuantState st =
+        LearnableQuantState::init(W, plan, QuantParams::per_tensor_symmetric(8, act_scale), cfg);
+    std::vector<CalibSample> samples(static_cast<size_t>(n_samples));
+    std::vector<const CalibSample*> batch;
+    for (int64_t s = 0; s < n_samples; ++s) {
+      samples[s].layer = "shim";
+      samples[s].chunk = static_cast<size_t>(chunk[s]);
+      samples[s].x = make_tensor(x + row_off[s] * k, row_off[s + 1] - row_off[s], k);
+      batch.push_back(&samples[s]);
+    }
+    const std::vector<double> cw(chunk_w, chunk_w + n_chunks);
+    *loss = weighted_loss(batch, st, cw);
+    const IntTensor hc = st.hard_codes();
+    std::memcpy(codes, hc.data.data(), sizeof(int32_t) * n * k);
+    for (int64_t r = 0; r < n; ++r) {
+      s_wo[r] = st.weight_scale(static_cast<size_t>(r), true);
+      s_wn[r] = st.weight_scale(static_cast<size_t>(r), false);
+    }
+    *act_out = st.act_scale();
+    std::memset(outlier_mask, 0, static_cast<size_t>(k));
+    if (plan.enabled)
+      for (size_t c : plan.outlier_indices) outlier_mask[c] = 1;
+  });
+}

@@ -63,8 +63,12 @@ def fold_output_permutation(producer: QuantizedLayer,
 class QuantizedChain:
     def __init__(self, layers: Sequence[QuantizedLayer], m: int,
                  epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None,
-                 fold: bool = True, fuse_rowmax: bool = False):
-        """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1).
+                 fold: bool = True, fuse_rowmax: bool = False, ms: Optional[Sequence[int]] = None,
+                 ctx_rows: int = 0):
+        """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1;
+        -2 = the context input ``self.ctx`` of ``ctx_rows`` rows, e.g. the text tokens the
+        cross-attention k / v projections read).  ``ms[i]`` = rows layer i processes (default m;
+        a layer reading a producer must match its rows).
 
         With ``fold`` every intermediate consumed by exactly one layer is produced in that
         layer's plan order (fold_output_permutation), so its K1 runs without a gather.
@@ -73,10 +77,16 @@ class QuantizedChain:
         streaming pass (qarvd_quantize_act_pmax).
         ``self.source_ops`` keeps the unfolded shapes for op counting."""
         self.layers = list(layers)
+        self.source_layers = list(layers)  # as given (before any output-permutation fold)
         self.m = m
         self.epilogues = list(epilogues) if epilogues is not None else [_lib.EPI_NONE] * len(layers)
         self.inputs = list(inputs) if inputs is not None else list(range(-1, len(layers) - 1))
-        self.source_ops = float(sum(2.0 * m * L.out_dim * L.in_dim for L in self.layers))
+        self.ms = list(ms) if ms is not None else [m] * len(self.layers)
+        for i, j in enumerate(self.inputs):
+            want = m if j == -1 else (ctx_rows if j == -2 else self.ms[j])
+            if self.ms[i] != want:
+                raise _lib.InvalidArgument("QuantizedChain: layer rows do not match its input's rows")
+        self.source_ops = float(sum(2.0 * mi * L.out_dim * L.in_dim for mi, L in zip(self.ms, self.layers)))
         if fold:
             for j, i in enumerate(self.inputs):
                 if i >= 0 and self.inputs.count(i) == 1 and self.layers[j].gather_dev is not None:
@@ -95,17 +105,20 @@ class QuantizedChain:
                     self.stream_k1[j] = True
                     if L.act_granularity == _lib.ACT_PER_TOKEN:
                         P = self.layers[i]
-                        pm = _lib.load().qarvd_dual_gemm_pmax_count(m, P.out_dim, P.k_pad)
-                        self.rowmax[i] = torch.zeros((m, pm), dtype=torch.int32, device=dev)
-        self.x = torch.empty((m, self.layers[0].in_dim), dtype=torch.bfloat16, device=dev)
-        self.xq = [torch.empty((m, L.k_pad), dtype=torch.int8, device=dev) for L in self.layers]
-        self.sx = [torch.empty(m, dtype=torch.float32, device=dev) for _ in self.layers]
-        self.y = [torch.empty((m, L.out_dim), dtype=torch.bfloat16, device=dev) for L in self.layers]
+                        pm = _lib.load().qarvd_dual_gemm_pmax_count(self.ms[i], P.out_dim, P.k_pad)
+                        self.rowmax[i] = torch.zeros((self.ms[i], pm), dtype=torch.int32, device=dev)
+        first = {j: i for i, j in reversed(list(enumerate(self.inputs))) if j < 0}
+        self.x = torch.empty((m, self.layers[first.get(-1, 0)].in_dim), dtype=torch.bfloat16, device=dev)
+        self.ctx = (torch.empty((ctx_rows, self.layers[first[-2]].in_dim), dtype=torch.bfloat16, device=dev)
+                    if -2 in first else None)
+        self.xq = [torch.empty((mi, L.k_pad), dtype=torch.int8, device=dev) for mi, L in zip(self.ms, self.layers)]
+        self.sx = [torch.empty(mi, dtype=torch.float32, device=dev) for mi in self.ms]
+        self.y = [torch.empty((mi, L.out_dim), dtype=torch.bfloat16, device=dev) for mi, L in zip(self.ms, self.layers)]
         self.graph = None
 
     def _src(self, i):
         j = self.inputs[i]
-        return self.x if j < 0 else self.y[j]
+        return self.x if j == -1 else (self.ctx if j == -2 else self.y[j])
 
     def launch(self, stream: Optional[int] = None, events: Optional[List] = None):
         """Enqueue K1 + K2 for every layer (2 kernels per layer).  With ``events`` (a list of
@@ -117,14 +130,15 @@ class QuantizedChain:
             events[0].record()
         for i, L in enumerate(self.layers):
             src = self._src(i)
+            m = self.ms[i]
             if self.stream_k1[i]:
                 rm = self.rowmax[self.inputs[i]]
-                _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), self.m, L.in_dim, src.stride(0),
+                _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), m, L.in_dim, src.stride(0),
                           _ptr(rm), 0 if rm is None else rm.shape[1], L.act_granularity,
                           float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
                           None, None, s)
             else:
-                _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, self.m, L.in_dim,
+                _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, m, L.in_dim,
                           src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
                           float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
                           None, None, s)
@@ -132,13 +146,13 @@ class QuantizedChain:
                 events[2 * i + 1].record()
             if self.rowmax[i] is not None:
                 _lib.call("qarvd_dual_gemm_pmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
-                          L.k_pad, self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                          L.k_pad, m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
                           L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
                           self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(),
                           self.rowmax[i].shape[1], s)
             else:
                 _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
-                          self.m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                          m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
                           L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
                           self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
             if events is not None:
@@ -178,3 +192,45 @@ class QuantizedChain:
     def int_ops(self) -> float:
         """Algorithmic ops of the chain as specified (unfolded shapes, no pad rows)."""
         return self.source_ops
+
+
+def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
+                    text_len: Optional[int] = None, fuse_rowmax: bool = False) -> "QuantizedChain":
+    """BASELINE config 3: every quantized linear of a Wan-1.3B-shaped DiT stack for one chunk.
+
+    Per block (toy_model.cpp:25-27 layer types, Wan2.1 shapes): self_attn.{q,k,v} read the
+    block input; self_attn.o reads v's output; cross_attn.q reads o's; cross_attn.{k,v}
+    read the 512 text tokens; cross_attn.o reads cross q's; ffn.0 (GELU fused) reads
+    cross o's; ffn.2 reads ffn.0's and is the next block's input.  The attention, norm,
+    modulation and residual glue between the linears is not on the quantized path (the
+    reference's own f64 glue) and is elided: each linear still sees its real
+    shape, its own outlier plan (K3 on its synthetic weight) and a real per-token K1.
+    """
+    from . import engine, synth
+    from .outlier import analyze_layer
+
+    specs = synth.wan_registry(blocks=blocks)
+    m = synth.WAN_CHUNK_TOKENS if m is None else m
+    text_len = synth.WAN_TEXT_LEN if text_len is None else text_len
+    layers, inputs, epis, ms = [], [], [], []
+    block_in = -1
+    for b in range(blocks):
+        base = len(layers)
+        idx = {t: base + i for i, t in enumerate(synth.BLOCK_LAYER_TYPES)}
+        src = {"self_attn.q": block_in, "self_attn.k": block_in, "self_attn.v": block_in,
+               "self_attn.o": idx["self_attn.v"], "cross_attn.q": idx["self_attn.o"],
+               "cross_attn.k": -2, "cross_attn.v": -2, "cross_attn.o": idx["cross_attn.q"],
+               "ffn.0": idx["cross_attn.o"], "ffn.2": idx["ffn.0"]}
+        for t in synth.BLOCK_LAYER_TYPES:
+            spec = specs[idx[t]]
+            w = synth.synth_weight(spec, seed=seed)
+            rep = analyze_layer(spec.name, w)
+            plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+            layers.append(engine.prepare_weights(spec.name, w, plan))
+            del w
+            inputs.append(src[t])
+            epis.append(_lib.EPI_GELU if t == "ffn.0" else _lib.EPI_NONE)
+            ms.append(text_len if src[t] == -2 else m)
+        block_in = idx["ffn.2"]
+    return QuantizedChain(layers, m, epilogues=epis, inputs=inputs, ms=ms, ctx_rows=text_len,
+                          fuse_rowmax=fuse_rowmax)

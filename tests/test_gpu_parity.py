@@ -595,3 +595,31 @@ def test_k5_batched_nonfinite(cuda):
     bits[11, 7] = 0x7FC0
     with pytest.raises(qb.InvalidArgument, match="non-finite"):
         engine.prepare_weights_batched(["a"], [to_dev_bf16(bits)], [plan])
+
+
+@pytest.mark.gpu
+def test_wan_stack_chain_fold_invariant(cuda):
+    """Config 3's stack (multi-consumer block inputs, a context input for cross k/v, per-layer
+    rows, GELU on ffn.0) gives bit-identical outputs with and without the permutation folds."""
+    from paper_2605_21072_b200 import synth
+    from paper_2605_21072_b200.pipeline import QuantizedChain, wan_stack_chain
+    ch = wan_stack_chain(blocks=2, m=300, text_len=64)
+    assert len(ch.layers) == 20 and ch.ms[5] == 64 and ch.ms[6] == 64
+    ref = QuantizedChain(ch.source_layers, ch.m, epilogues=ch.epilogues, inputs=ch.inputs, ms=ch.ms,
+                         ctx_rows=64, fold=False)
+    x = synth.synth_activation(300, synth.WAN_DIM, seed=3)
+    c = synth.synth_activation(64, synth.WAN_DIM, seed=4)
+    for chain in (ch, ref):
+        chain.x.copy_(x)
+        chain.ctx.copy_(c)
+        chain.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(ch.output.view(torch.int16), ref.output.view(torch.int16))
+    for i in (0, 1, 5, 6):  # unfolded outputs (q, k of block 0; cross k, v)
+        assert torch.equal(ch.y[i].view(torch.int16), ref.y[i].view(torch.int16))
+    # graph replay reproduces the eager launch
+    ch.capture()
+    ch.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ch.output.view(torch.int16), ref.output.view(torch.int16))
+    assert ch.int_ops() == ref.int_ops()

@@ -245,3 +245,40 @@ def test_device_row_scale_formula_is_correctly_rounded():
     """K1 computes s = fl(amax/qmax) as amax*fl(1/qmax) + one fma correction (quantize.cu
     row_s64); exhaustively equal to the division for every bf16 amax and bit width."""
     assert oracle.row_scale_formula_mismatches() == 0
+
+
+def _loss_case(n, k, n_out, seed, samples=3, rows=5):
+    r = np.random.default_rng(seed)
+    outl = np.sort(r.choice(k, n_out, replace=False)) if n_out else np.zeros(0, np.int64)
+    wb, w = bf16_values((n, k), seed=seed, scale=1.0 / np.sqrt(k), heavy_cols=outl if n_out else None)
+    xb, x = bf16_values((samples * rows, k), seed=seed + 1, heavy_cols=outl if n_out else None, gamma=3.0)
+    row_off = np.arange(samples + 1) * rows
+    chunks = np.array([1, 3, 2][:samples])
+    cw = oracle.weighting(1, None, 3)  # heuristic_exp over 3 chunks
+    return w, x, outl, row_off, chunks, cw
+
+
+@pytest.mark.parametrize("n,k,n_out", [(24, 96, 32), (16, 64, 0), (8, 160, 33)])
+def test_ref_weighted_loss_equals_restatement(ref_lib, n, k, n_out):
+    """Eq. 5 (calibrate.cpp:201-224) on a reference-initialised LearnableQuantState: the plain-C
+    restatement reproduces the reference's weighted_loss bit-for-bit."""
+    w, x, outl, row_off, chunks, cw = _loss_case(n, k, n_out, seed=n + k)
+    act = np.abs(x).max() / 127.0
+    ref = oracle.ref_weighted_loss(w, outl, act, x, row_off, chunks, cw)
+    xq, _, _ = oracle.quantize_act(x, None, per_token=False, static_scale=ref["act_scale"])
+    loss, err = oracle.weighted_loss(x, xq, ref["act_scale"], w, ref["codes"], ref["s_wo"], ref["s_wn"],
+                                     ref["mask"], row_off, chunks, cw)
+    assert loss == ref["loss"]
+    assert loss > 0 and np.all(err > 0)
+    assert np.isclose(loss, sum(cw[c - 1] * e for c, e in zip(chunks, err)) / len(chunks), rtol=1e-15)
+
+
+def test_weighted_loss_errors(ref_lib):
+    w, x, outl, row_off, chunks, cw = _loss_case(8, 64, 0, seed=3)
+    with pytest.raises(oracle.RefError, match="outside the weight vector"):
+        oracle.ref_weighted_loss(w, outl, 0.01, x, row_off, np.array([1, 4, 2]), cw)
+    with pytest.raises(IndexError):
+        oracle.weighted_loss(x, np.zeros(x.shape, np.int32), 0.01, w, np.zeros(w.shape, np.int32),
+                             np.ones(8), np.ones(8), np.zeros(64, np.uint8), row_off, np.array([0, 1, 2]), cw)
+    with pytest.raises(oracle.RefError, match="empty batch"):
+        oracle.ref_weighted_loss(w, outl, 0.01, x, np.array([0]), np.zeros(0, np.int64), cw)
