@@ -284,6 +284,34 @@ int qarvd_scale_search_async(const qarvd_search_job* jobs, int num_jobs,
                              const double* frame_weights, int bits, uint64_t* nonfinite_flag_dev,
                              void* stream);
 
+/* ---- Eq. 5: frame-weighted output-space reconstruction loss ---------------
+ * Replaces  weighted_loss(batch, state, chunk_weights)  calibrate.hpp:80-82 /
+ *           calibrate.cpp:201-224:
+ *   loss = (1/B) sum_s chunk_weights[chunk_s - 1] * || X_s W^T - FQ(X_s) What^T ||_F^2
+ * One tcgen05 kernel per call: X W^T (bf16 x bf16 -> f32 TMEM) and the two int8 slabs of
+ * xq . wq^T (int32 TMEM) per 128 x 128 tile, squared difference reduced in the epilogue;
+ * neither product is written to memory.
+ *   x  device bf16 [m x k] (ldx): the B samples stacked, sample s = rows
+ *      sample_rows[s] .. sample_rows[s+1] (HOST int64 [B+1], sample_rows[B] = m)
+ *   w  device bf16 [n x k] (ldw): the FP weight, same column order as x
+ *   xq / wq  device int8 codes [m x k_pad] / [n x k_pad] in plan order (K1 / K5 outputs),
+ *      k_outlier leading outlier-slab columns; scale_x f32 [m], scale_w_* f32 [n]
+ *   sample_chunk  HOST int64 [B], 1-based; chunk_weights HOST f64 [n_chunks]
+ *   sample_err  out device f64 [B]; loss  out device f64 [1]
+ *   workspace   device, >= qarvd_weighted_loss_workspace(m, n, B) bytes, 8-byte aligned
+ * Errors as the reference: empty batch -> INVALID_ARGUMENT, a chunk outside [1, n_chunks]
+ * -> OUT_OF_RANGE ("sample chunk outside the weight vector", calibrate.cpp:207-208).
+ */
+int64_t qarvd_weighted_loss_workspace(int64_t m, int64_t n, int64_t n_samples);
+int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_t* w, int64_t ldw,
+                        const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldwq, int64_t m,
+                        int64_t n, int64_t k, int64_t k_pad, int64_t k_outlier,
+                        const float* scale_x, const float* scale_w_outlier,
+                        const float* scale_w_normal, const int64_t* sample_rows,
+                        const int64_t* sample_chunk, int64_t n_samples,
+                        const double* chunk_weights, int64_t n_chunks, double* sample_err,
+                        double* loss, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
  * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)
  * weights with a seeded set of input columns scaled by gamma.  Values are

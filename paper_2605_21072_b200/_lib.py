@@ -172,6 +172,11 @@ SIGNATURES = {
         c_int,
         [POINTER(SearchJob), c_int, POINTER(c_double), c_int, POINTER(c_double), c_int, c_void_p],
     ),
+    "qarvd_weighted_loss_workspace": (c_int64, [c_int64, c_int64, c_int64]),
+    "qarvd_weighted_loss": (
+        c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+                c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "qarvd_synth_bf16": (
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double, c_void_p, c_int64, c_double,

@@ -331,3 +331,42 @@ class CalibrationShard:
             off += n
         self.layers = layers
         return out
+
+
+def weighted_loss(batch: Sequence, layer, w: torch.Tensor, chunk_weights: Sequence[float],
+                  act_scale: float, return_errors: bool = False):
+    """Eq. 5 on the GPU: weighted_loss(batch, state, chunk_weights) (calibrate.cpp:201-224).
+
+    ``batch`` holds (x, chunk) pairs: a calibration sample's bf16 activations [rows x k] on the
+    device (CalibSample.x, calibrate.hpp:37-41) and its 1-based chunk.  The state is the
+    deployable layer (``layer``: plan-order int8 codes and f32 group scales; see
+    engine.layer_from_codes for learned codes), its FP weight ``w`` (bf16 [n x k], original
+    order) and the per-tensor activation scale (LearnableQuantState::act_params).
+    K1 quantizes the stacked samples with the static scale, then one qarvd_weighted_loss call
+    evaluates every sample's ||X W^T - FQ(X) What^T||_F^2 and the weighted mean.
+    """
+    from .engine import kernel_a_quantize_activation
+    if len(batch) == 0:
+        raise _lib.InvalidArgument("weighted loss: empty batch")
+    xs = [x for x, _ in batch]
+    chunks = np.asarray([int(c) for _, c in batch], dtype=np.int64)
+    rows = np.zeros(len(xs) + 1, dtype=np.int64)
+    rows[1:] = np.cumsum([x.shape[0] for x in xs])
+    x = xs[0] if len(xs) == 1 else torch.cat(xs, 0)
+    x = x.contiguous()
+    xq, s32, _ = kernel_a_quantize_activation(x, layer, _lib.ACT_PER_TENSOR, static_scale=float(act_scale))
+    m, k = x.shape
+    n = layer.out_dim
+    cw = np.ascontiguousarray(chunk_weights, dtype=np.float64)
+    ws_bytes = int(_lib.load().qarvd_weighted_loss_workspace(m, n, len(xs)))
+    ws = torch.empty(max(8, ws_bytes) // 8, dtype=torch.float64, device=x.device)
+    err = torch.empty(len(xs), dtype=torch.float64, device=x.device)
+    loss = torch.empty(1, dtype=torch.float64, device=x.device)
+    _lib.call("qarvd_weighted_loss", x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0),
+              xq.data_ptr(), xq.stride(0), layer.wq.data_ptr(), layer.wq.stride(0), m, n, k,
+              layer.k_pad, layer.k_outlier, s32.data_ptr(), layer.scale_outlier32.data_ptr(),
+              layer.scale_normal32.data_ptr(), rows.ctypes.data, chunks.ctypes.data, len(xs),
+              cw.ctypes.data, len(cw), err.data_ptr(), loss.data_ptr(), ws.data_ptr(), ws_bytes, _stream())
+    if return_errors:
+        return float(loss.item()), err.cpu().numpy()
+    return float(loss.item())

@@ -230,6 +230,29 @@ def prepare_weights_batched(names: Sequence[str], ws: Sequence[torch.Tensor],
     return layers
 
 
+def layer_from_codes(name: str, codes: np.ndarray, scale_outlier: Sequence[float],
+                     scale_normal: Sequence[float], plan: DualScalePlan, device="cuda") -> QuantizedLayer:
+    """Deploy given integer codes (ORIGINAL column order, e.g. LearnableQuantState::hard_codes,
+    calibrate.cpp:163-183) with their per-row group scales: the pre-permute of
+    calibrate.cpp:474-480 (wq[r, pos] = codes[r, perm[pos]], zero codes in pad slots)."""
+    codes = np.asarray(codes)
+    n, k = codes.shape
+    if k != plan.d_in:
+        raise _lib.InvalidArgument("layer_from_codes: codes do not match the plan's input width")
+    if codes.min(initial=0) < -127 or codes.max(initial=0) > 127:
+        raise _lib.InvalidArgument("layer_from_codes: codes outside the int8 range")
+    g = plan.gather
+    wq = np.zeros((n, plan.k_pad), dtype=np.int8)
+    valid = g >= 0
+    wq[:, valid] = codes[:, g[valid]].astype(np.int8)
+    so = np.asarray(scale_outlier if plan.enabled else scale_normal, dtype=np.float64)
+    sn = np.asarray(scale_normal, dtype=np.float64)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
+    return QuantizedLayer(name, n, k, plan, t(wq, torch.int8), t(so, torch.float64), t(sn, torch.float64),
+                          t(so.astype(np.float32), torch.float32), t(sn.astype(np.float32), torch.float32),
+                          t(g, torch.int32))
+
+
 def kernel_a_quantize_activation(x: torch.Tensor, layer_or_plan, granularity: int = _lib.ACT_PER_TOKEN,
                                  static_scale: float = 0.0, bits: int = 8,
                                  check_finite: bool = False):

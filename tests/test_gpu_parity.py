@@ -623,3 +623,81 @@ def test_wan_stack_chain_fold_invariant(cuda):
     torch.cuda.synchronize()
     assert torch.equal(ch.output.view(torch.int16), ref.output.view(torch.int16))
     assert ch.int_ops() == ref.int_ops()
+
+
+# ---------------------------------------------------------------- Eq. 5 weighted loss
+def _ref_loss_case(n, k, n_out, rows, seed):
+    r = np.random.default_rng(seed)
+    outl = np.sort(r.choice(k, n_out, replace=False)) if n_out else np.zeros(0, np.int64)
+    wb, w = bf16_values((n, k), seed=seed, scale=1.0 / np.sqrt(k), heavy_cols=outl if n_out else None)
+    xb, x = bf16_values((sum(rows), k), seed=seed + 1, heavy_cols=outl if n_out else None, gamma=3.0)
+    row_off = np.concatenate([[0], np.cumsum(rows)])
+    chunks = (np.arange(len(rows)) % 3) + 1
+    cw = calibrate.weighting_strategy("heuristic_exp", 3)
+    ref = oracle.ref_weighted_loss(w, outl, np.abs(x).max() / 127.0, x, row_off, chunks, cw)
+    plan = engine.build_plan("loss", k, outl)
+    layer = engine.layer_from_codes("loss", ref["codes"], ref["s_wo"], ref["s_wn"], plan)
+    xd = to_dev_bf16(xb)
+    batch = [(xd[row_off[i]:row_off[i + 1]], int(chunks[i])) for i in range(len(rows))]
+    return ref, layer, to_dev_bf16(wb), batch, cw, (x, w, row_off, chunks)
+
+
+@pytest.mark.parametrize("n,k,n_out,rows", [(256, 512, 32, (40, 77, 13)), (300, 1536, 64, (200, 129)),
+                                            (136, 320, 0, (128,)), (192, 896, 96, (1, 255, 256, 3))])
+def test_weighted_loss_vs_reference(cuda, ref_lib, n, k, n_out, rows):
+    """The fused tcgen05 Eq. 5 kernel vs the reference's f64 weighted_loss on the same
+    reference-initialised LearnableQuantState (codes, group scales and act scale exported by
+    the reference).  Tolerance rtol 2e-5: the GPU target is a bf16 x bf16 -> fp32 tensor-core
+    product and the prediction uses the f32 copies of the scales (QARQ precision); the
+    per-sample errors also match the oracle restatement to the same tolerance."""
+    ref, layer, wd, batch, cw, (x, w, row_off, chunks) = _ref_loss_case(n, k, n_out, rows, seed=n + k)
+    loss, err = calibrate.weighted_loss(batch, layer, wd, cw, ref["act_scale"], return_errors=True)
+    assert np.isclose(loss, ref["loss"], rtol=2e-5, atol=0), (loss, ref["loss"])
+    xq, _, _ = oracle.quantize_act(x, None, per_token=False, static_scale=ref["act_scale"])
+    _, err_o = oracle.weighted_loss(x, xq, ref["act_scale"], w, ref["codes"], ref["s_wo"], ref["s_wn"],
+                                    ref["mask"], row_off, chunks, cw)
+    np.testing.assert_allclose(err, err_o, rtol=2e-5)
+
+
+def test_weighted_loss_exact_zero_and_errors(cuda):
+    """W and X on the quantization grids (power-of-two scales) -> every product is exact and
+    the loss is exactly 0; the reference's error contract (calibrate.cpp:203, :207-208)."""
+    r = np.random.default_rng(5)
+    n, k = 256, 640
+    codes = r.integers(-40, 41, size=(n, k))
+    outl = np.arange(0, k, 20)[:32]
+    plan = engine.build_plan("grid", k, outl)
+    layer = engine.layer_from_codes("grid", codes, np.full(n, 2.0 ** -6), np.full(n, 2.0 ** -7), plan)
+    wv = codes * np.where(np.isin(np.arange(k), outl), 2.0 ** -6, 2.0 ** -7)[None, :]
+    xv = r.integers(-20, 21, size=(300, k)) * 2.0 ** -5
+    xv[:, 0] = 127 * 2.0 ** -5  # keeps the static scale's codes in range
+    wd = to_dev_bf16(oracle.f32_to_bf16_bits(wv.astype(np.float32)))
+    xd = to_dev_bf16(oracle.f32_to_bf16_bits(xv.astype(np.float32)))
+    loss, err = calibrate.weighted_loss([(xd[:100], 1), (xd[100:], 2)], layer, wd, [0.5, 0.5], 2.0 ** -5,
+                                        return_errors=True)
+    assert loss == 0.0 and np.all(err == 0.0)
+    with pytest.raises(qb.OutOfRange, match="outside the weight vector"):
+        calibrate.weighted_loss([(xd[:100], 3)], layer, wd, [0.5, 0.5], 2.0 ** -5)
+    with pytest.raises(qb.InvalidArgument, match="empty batch"):
+        calibrate.weighted_loss([], layer, wd, [0.5, 0.5], 2.0 ** -5)
+
+
+def test_weighted_loss_wan_shape_sample_independence(cuda):
+    """Full Wan shape (21 frames x 1560 tokens, 1536 -> 1536, K_o = 32): every sample's error
+    from one batched call equals (bit-exactly) the same sample evaluated alone, and the loss is
+    the chunk-weighted mean of those errors."""
+    spec = synth.wan_registry(blocks=1)[0]
+    w = synth.synth_weight(spec, seed=1)
+    rep = qb.analyze_layer(spec.name, w)
+    plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+    layer = engine.prepare_weights(spec.name, w, plan)
+    xs = [synth.synth_activation(1560, 1536, seed=3, frame=f) for f in range(21)]
+    amax = max(float(x.float().abs().max()) for x in xs)
+    cw = calibrate.weighting_strategy("heuristic_exp", 21)
+    batch = [(x, f + 1) for f, x in enumerate(xs)]
+    loss, err = calibrate.weighted_loss(batch, layer, w, cw, amax / 127.0, return_errors=True)
+    assert np.all(err > 0)
+    assert np.isclose(loss, float(np.dot(cw, err)) / 21, rtol=1e-14)
+    for f in (0, 7, 20):
+        _, e1 = calibrate.weighted_loss([batch[f]], layer, w, cw, amax / 127.0, return_errors=True)
+        assert e1[0] == err[f]
