@@ -4,7 +4,8 @@
 // calibrate.cpp:201-224): for every calibration sample X_s (rows of one captured chunk)
 //     err_s = || X_s W^T - FQ(X_s) What^T ||_F^2,   loss = (1/B) sum_s w[chunk_s] err_s.
 // The reference runs two f64 GEMMs per sample and materialises both [rows x N] outputs.
-// Here ONE persistent kernel computes, per 128 x 128 output tile, three tensor-memory
+// Here ONE persistent kernel computes, per 256 x 128 output tile (an SM pair,
+// cta_group::2, 256-byte K stages), three tensor-memory
 // accumulators from one shared-memory pipeline:
 //   acc_t = X W^T            tcgen05.mma.kind::f16 (bf16 x bf16 -> f32), K = 16 per MMA
 //   acc_o = xq_o . wq_o^T    tcgen05.mma.kind::i8 over the outlier K-slab (k < K_o)
@@ -19,8 +20,8 @@
 // TMEM: four 128-column slots; tile i of a CTA uses slots 3i, 3i+1, 3i+2 (mod 4) for
 // (acc_t, acc_o, acc_n).  The next tile's bf16 phase accumulates into the spare slot while
 // the epilogue drains the previous tile; its int8 phase waits only for the slots it reuses.
-// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 4..11 = epilogue
-// (two warps per TMEM lane quadrant, 64 columns each).
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (leader CTA), 2 = TMEM allocator,
+// 4..11 = epilogue (two warps per TMEM lane quadrant, 64 columns each, in both CTAs).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -34,12 +35,16 @@
 namespace qarvd_b200 {
 namespace {
 
-constexpr int LBM = 128;          // rows per tile (TMEM lanes)
+constexpr int LBM = 128;          // rows per CTA (TMEM lanes); an SM pair computes 256-row tiles
+constexpr int LTM = 2 * LBM;      // rows of a pair tile
 constexpr int LBN = 128;          // columns per tile
-constexpr int kLossStageA = LBM * 128;
-constexpr int kLossStageB = LBN * 128;
-constexpr int kLossStageBytes = kLossStageA + kLossStageB;  // one 128-byte K slice of each
-constexpr int kLossStages = 6;
+constexpr int LKS = 2;            // 128-byte K sub-tiles per stage (8 MMAs per mbarrier wait)
+constexpr int kLossSubA = LBM * 128;
+constexpr int kLossSubB = (LBN / 2) * 128;  // each CTA of the pair holds half of B
+constexpr int kLossStageA = LKS * kLossSubA;
+constexpr int kLossStageB = LKS * kLossSubB;
+constexpr int kLossStageBytes = kLossStageA + kLossStageB;
+constexpr int kLossStages = 4;
 constexpr int kLossEpiWarps = 8;
 constexpr int kLossThreads = 128 + 32 * kLossEpiWarps;
 constexpr size_t kLossSmem = static_cast<size_t>(kLossStages) * kLossStageBytes + 1024;
@@ -59,16 +64,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
+// SM-pair kernel (cluster of 2, cta_group::2): the leader CTA issues M = 256 MMAs whose A rows
+// are split over the two CTAs' shared memory (128 each) and whose B tile is split in halves;
+// each CTA's TMEM receives its own 128 rows of the three accumulators.
 __global__ void __launch_bounds__(kLossThreads, 1)
     recon_loss_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       const __grid_constant__ CUtensorMap tmXq, const __grid_constant__ CUtensorMap tmWq,
@@ -78,12 +86,16 @@ __global__ void __launch_bounds__(kLossThreads, 1)
   uint8_t* sB = smem + kLossStages * kLossStageA;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kLossStages * kLossStageBytes);
   uint64_t* empty = full + kLossStages;
-  uint64_t* tfull = empty + kLossStages;  // [2] tile accumulators complete
-  uint64_t* sfree = tfull + 2;            // [4] TMEM slot released by the epilogue
+  uint64_t* tfull = empty + kLossStages;  // [2] tile accumulators complete (both CTAs)
+  uint64_t* sfree = tfull + 2;            // [4] TMEM slot released (leader's copy counts)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = static_cast<int>(blockIdx.x) / 2;
+  const int num_pairs = static_cast<int>(gridDim.x) / 2;
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmX);
     ptx::prefetch_tmap(&tmW);
@@ -94,41 +106,47 @@ __global__ void __launch_bounds__(kLossThreads, 1)
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) ptx::mbar_init(&tfull[s], 1);
-    for (int s = 0; s < 4; ++s) ptx::mbar_init(&sfree[s], kLossEpiWarps);
+    for (int s = 0; s < 4; ++s) ptx::mbar_init(&sfree[s], 2 * kLossEpiWarps);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();
   pdl_launch_dependents();
 
-  const int nkf = static_cast<int>((p.k + 63) / 64);       // bf16 K blocks (64 values = 128 B)
-  const int nki = static_cast<int>((p.k_pad + 127) / 128);  // int8 K blocks (128 codes)
+  const int nkf = static_cast<int>((p.k + 64 * LKS - 1) / (64 * LKS));      // bf16 stages
+  const int nki = static_cast<int>((p.k_pad + 128 * LKS - 1) / (128 * LKS));  // int8 stages
   const int k16 = static_cast<int>((p.k + 15) / 16);
   const int k32 = static_cast<int>(p.k_pad / 32), ko32 = static_cast<int>(p.k_o / 32);
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs; bytes land on the leader's barrier) =====
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int a_row = (t % p.num_m_blks) * LBM;
-      const int b_row = (t / p.num_m_blks) * LBN;
+    for (int t = pair; t < p.num_tiles; t += num_pairs) {
+      const int a_row = (t % p.num_m_blks) * LTM + static_cast<int>(rank) * LBM;
+      const int b_row = (t / p.num_m_blks) * LBN + static_cast<int>(rank) * (LBN / 2);
       for (int i = 0; i < nkf + nki; ++i) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
-          ptx::mbar_expect_tx(&full[stage], kLossStageBytes);
-          uint8_t* a = sA + stage * kLossStageA;
-          uint8_t* b = sB + stage * kLossStageB;
-          if (i < nkf) {
-            ptx::tma_load_2d(a, &tmX, &full[stage], i * 64, a_row);
-            ptx::tma_load_2d(b, &tmW, &full[stage], i * 64, b_row);
-          } else {
-            ptx::tma_load_2d(a, &tmXq, &full[stage], (i - nkf) * 128, a_row);
-            ptx::tma_load_2d(b, &tmWq, &full[stage], (i - nkf) * 128, b_row);
+          if (leader) ptx::mbar_expect_tx(&full[stage], 2 * kLossStageBytes);
+#pragma unroll
+          for (int ks = 0; ks < LKS; ++ks) {
+            uint8_t* a = sA + stage * kLossStageA + ks * kLossSubA;
+            uint8_t* b = sB + stage * kLossStageB + ks * kLossSubB;
+            if (i < nkf) {
+              const int kc = (i * LKS + ks) * 64;
+              ptx::tma_load_2d_2sm(a, &tmX, &full[stage], kc, a_row);
+              ptx::tma_load_2d_2sm(b, &tmW, &full[stage], kc, b_row);
+            } else {
+              const int kc = ((i - nkf) * LKS + ks) * 128;
+              ptx::tma_load_2d_2sm(a, &tmXq, &full[stage], kc, a_row);
+              ptx::tma_load_2d_2sm(b, &tmWq, &full[stage], kc, b_row);
+            }
           }
         }
         __syncwarp();
@@ -138,10 +156,10 @@ __global__ void __launch_bounds__(kLossThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t id_f = idesc_bf16(LBM, LBN);
-    constexpr uint32_t id_i = ptx::idesc_i8(LBM, LBN);
+  } else if (warp == 1 && leader) {
+    // ===================== MMA issuer (leader CTA) =====================
+    constexpr uint32_t id_f = idesc_bf16(LTM, LBN);
+    constexpr uint32_t id_i = ptx::idesc_i8(LTM, LBN);
     const uint64_t a0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sA));
     const uint64_t b0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sB));
     int stage = 0;
@@ -153,7 +171,7 @@ __global__ void __launch_bounds__(kLossThreads, 1)
       ptx::tc_fence_after();
     };
     int ti = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++ti) {
+    for (int t = pair; t < p.num_tiles; t += num_pairs, ++ti) {
       const int st = (3 * ti) & 3, so = (3 * ti + 1) & 3, sn = (3 * ti + 2) & 3;
       const uint32_t d_t = tmem_base + static_cast<uint32_t>(st * LBN);
       const uint32_t d_o = tmem_base + static_cast<uint32_t>(so * LBN);
@@ -170,20 +188,23 @@ __global__ void __launch_bounds__(kLossThreads, 1)
         const uint64_t bd = b0 + static_cast<uint64_t>(stage * (kLossStageB >> 4));
         if (lane == 0) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < 4 * LKS; ++j) {
+            // sub-tile j/4, +32 bytes along K inside the 128B swizzle row = +2 per step
+            const uint64_t ao = static_cast<uint64_t>((j >> 2) * (kLossSubA >> 4) + 2 * (j & 3));
+            const uint64_t bo = static_cast<uint64_t>((j >> 2) * (kLossSubB >> 4) + 2 * (j & 3));
             if (i < nkf) {
-              const int s16 = i * 4 + j;
-              if (s16 < k16) mma_bf16(d_t, ad + 2 * j, bd + 2 * j, id_f, s16 > 0 ? 1u : 0u);
+              const int s16 = i * 4 * LKS + j;
+              if (s16 < k16) mma_bf16_2sm(d_t, ad + ao, bd + bo, id_f, s16 > 0 ? 1u : 0u);
             } else {
-              const int s32 = (i - nkf) * 4 + j;
+              const int s32 = (i - nkf) * 4 * LKS + j;
               if (s32 < k32) {
                 const bool outl = s32 < ko32;
                 const uint32_t acc = (outl ? s32 == 0 : s32 == ko32) ? 0u : 1u;
-                ptx::mma_i8(outl ? d_o : d_n, ad + 2 * j, bd + 2 * j, id_i, acc);
+                ptx::mma_i8_2sm(outl ? d_o : d_n, ad + ao, bd + bo, id_i, acc);
               }
             }
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
         }
         __syncwarp();
         if (++stage == kLossStages) {
@@ -191,20 +212,20 @@ __global__ void __launch_bounds__(kLossThreads, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) ptx::mma_commit(&tfull[ti & 1]);
+      if (lane == 0) ptx::mma_commit_2sm_mc(&tfull[ti & 1], 0x3);
       __syncwarp();
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (both CTAs, own 128 rows) =====================
     const int ew = warp - 4;
     const int q = warp & 3;          // TMEM lane quadrant
     const int h = ew >> 2;           // column half
     const bool has_o = p.k_o > 0;
     const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
     int ti = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++ti) {
+    for (int t = pair; t < p.num_tiles; t += num_pairs, ++ti) {
       const int m_blk = t % p.num_m_blks, n_blk = t / p.num_m_blks;
-      const int64_t row = static_cast<int64_t>(m_blk) * LBM + q * 32 + lane;
+      const int64_t row = static_cast<int64_t>(m_blk) * LTM + rank * LBM + q * 32 + lane;
       const float sx = row < p.m ? p.scale_x[row] : 0.f;
       const int st = (3 * ti) & 3, so = (3 * ti + 1) & 3, sn = (3 * ti + 2) & 3;
       ptx::mbar_wait(&tfull[ti & 1], (ti >> 1) & 1);
@@ -233,21 +254,22 @@ __global__ void __launch_bounds__(kLossThreads, 1)
         }
         acc += static_cast<double>(part);
       }
-      // all reads of this tile's slots are complete: release them to the MMA issuer
+      // all reads of this tile's slots are complete: release them to the leader's MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        ptx::mbar_arrive(&sfree[st]);
-        ptx::mbar_arrive(&sfree[so]);
-        ptx::mbar_arrive(&sfree[sn]);
+        ptx::mbar_arrive_leader(&sfree[st]);
+        ptx::mbar_arrive_leader(&sfree[so]);
+        ptx::mbar_arrive_leader(&sfree[sn]);
       }
       if (row < p.m) p.part[static_cast<int64_t>(2 * n_blk + h) * p.m + row] = acc;
     }
   }
   __syncthreads();
+  ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
+    ptx::tmem_dealloc_2sm(tmem_base, 512);
   }
 }
 
@@ -301,12 +323,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // K-major [rows x cols] operand, box = 128 bytes of K x 128 rows, 128B swizzle
 int make_kmajor_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize,
-                     int64_t rows, int64_t cols, int64_t ld_elems) {
+                     int64_t rows, int64_t cols, int64_t ld_elems, int box_rows) {
   auto encode = encode_fn();
   if (!encode) QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems * esize)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esize), 128};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esize), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -389,10 +411,10 @@ extern "C" int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_
   QARVD_CUDA_TRY(attr_err);
   CUtensorMap tx, tw, txq, twq;
   int st;
-  if ((st = make_kmajor_tmap(&tx, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, ldx))) return st;
-  if ((st = make_kmajor_tmap(&tw, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, k, ldw))) return st;
-  if ((st = make_kmajor_tmap(&txq, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, m, k_pad, ldq))) return st;
-  if ((st = make_kmajor_tmap(&twq, wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, n, k_pad, ldwq))) return st;
+  if ((st = make_kmajor_tmap(&tx, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, ldx, LBM))) return st;
+  if ((st = make_kmajor_tmap(&tw, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, k, ldw, LBN / 2))) return st;
+  if ((st = make_kmajor_tmap(&txq, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, m, k_pad, ldq, LBM))) return st;
+  if ((st = make_kmajor_tmap(&twq, wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, n, k_pad, ldwq, LBN / 2))) return st;
 
   LossParams p{};
   p.m = m;
@@ -403,7 +425,7 @@ extern "C" int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_
   p.scale_x = scale_x;
   p.scale_wo = scale_w_outlier;
   p.scale_wn = scale_w_normal;
-  p.num_m_blks = static_cast<int>((m + LBM - 1) / LBM);
+  p.num_m_blks = static_cast<int>((m + LTM - 1) / LTM);
   p.num_n_blks = static_cast<int>((n + LBN - 1) / LBN);
   p.num_tiles = p.num_m_blks * p.num_n_blks;
   double* ws = static_cast<double*>(workspace);
@@ -418,8 +440,9 @@ extern "C" int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_
                                  cudaMemcpyHostToDevice, s));
   QARVD_CUDA_TRY(cudaMemcpyAsync(d_wsamp, wsamp.data(), sizeof(double) * n_samples,
                                  cudaMemcpyHostToDevice, s));
-  const int grid = p.num_tiles < loss_sm_count() ? p.num_tiles : loss_sm_count();
-  QARVD_CUDA_TRY(launch_pdl(recon_loss_kernel, dim3(grid), dim3(kLossThreads), kLossSmem, s, 1, tx,
+  const int pairs = loss_sm_count() / 2;
+  const int grid = 2 * (p.num_tiles < pairs ? p.num_tiles : pairs);
+  QARVD_CUDA_TRY(launch_pdl(recon_loss_kernel, dim3(grid), dim3(kLossThreads), kLossSmem, s, 2, tx,
                             tw, txq, twq, p));
   count_launch();
   QARVD_LAUNCH_CHECK();
