@@ -128,41 +128,89 @@ class QuantizedChain:
         s = _stream() if stream is None else stream
         if events is not None:
             events[0].record()
-        for i, L in enumerate(self.layers):
-            src = self._src(i)
-            m = self.ms[i]
-            if self.stream_k1[i]:
-                rm = self.rowmax[self.inputs[i]]
-                _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), m, L.in_dim, src.stride(0),
-                          _ptr(rm), 0 if rm is None else rm.shape[1], L.act_granularity,
-                          float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
-                          None, None, s)
-            else:
-                _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, m, L.in_dim,
-                          src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
-                          float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
-                          None, None, s)
-            if events is not None:
-                events[2 * i + 1].record()
-            if self.rowmax[i] is not None:
-                _lib.call("qarvd_dual_gemm_pmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
-                          L.k_pad, m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
-                          L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
-                          self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(),
-                          self.rowmax[i].shape[1], s)
-            else:
-                _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
-                          m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
-                          L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
-                          self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
-            if events is not None:
-                events[2 * i + 2].record()
+        for i in range(len(self.layers)):
+            self._enqueue(i, s, events)
 
-    def capture(self, timed: bool = False):
+    def launch_parallel(self):
+        """launch() with the chain's dead-end layers (outputs consumed by no later layer, e.g.
+        q / k and the cross-attention k / v of the Wan stack) forked onto two side streams:
+        each waits only for its own producer (the context input needs none), so their
+        kernels fill the SMs the critical path leaves idle.  Captured into a graph, the
+        fork / join become graph edges."""
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_side"):
+            self._side = [torch.cuda.Stream(device=main.device) for _ in range(2)]
+        n = len(self.layers)
+        side = {i for i in range(n - 1) if i not in self.inputs}
+        wanted = {self.inputs[i] for i in side if self.inputs[i] >= 0}
+        start = torch.cuda.Event()
+        start.record(main)
+        for st in self._side:
+            st.wait_event(start)
+        after, k = {}, 0
+        for i in range(n):
+            if i in side:
+                st = self._side[k % len(self._side)]
+                k += 1
+                j = self.inputs[i]
+                if j >= 0:
+                    st.wait_event(after[j])
+                self._enqueue(i, st.cuda_stream)
+            else:
+                self._enqueue(i, main.cuda_stream)
+                if i in wanted:
+                    after[i] = torch.cuda.Event()
+                    after[i].record(main)
+        for st in self._side:
+            e = torch.cuda.Event()
+            e.record(st)
+            main.wait_event(e)
+
+    def _enqueue(self, i: int, s: int, events: Optional[List] = None):
+        """K1 + K2 of layer i on stream s."""
+        L = self.layers[i]
+        src = self._src(i)
+        m = self.ms[i]
+        if self.stream_k1[i]:
+            rm = self.rowmax[self.inputs[i]]
+            _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), m, L.in_dim, src.stride(0),
+                      _ptr(rm), 0 if rm is None else rm.shape[1], L.act_granularity,
+                      float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
+                      None, None, s)
+        else:
+            _lib.call("qarvd_quantize_act", src.data_ptr(), _lib.BF16, m, L.in_dim,
+                      src.stride(0), _ptr(L.gather_dev), L.k_pad, L.act_granularity,
+                      float(L.act_scale), 8, self.xq[i].data_ptr(), L.k_pad, self.sx[i].data_ptr(),
+                      None, None, s)
+        if events is not None:
+            events[2 * i + 1].record()
+        if self.rowmax[i] is not None:
+            _lib.call("qarvd_dual_gemm_pmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
+                      L.k_pad, m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                      self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(),
+                      self.rowmax[i].shape[1], s)
+        else:
+            _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
+                      m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                      self.epilogues[i], _lib.BF16, self.y[i].data_ptr(), L.out_dim, None, None, s)
+        if events is not None:
+            events[2 * i + 2].record()
+
+    def capture(self, timed: bool = False, parallel: bool = False):
         """Capture launch() into a CUDA graph (after one eager warm-up launch).  With
-        ``timed`` the graph also records per-kernel timing events (``self.events``)."""
+        ``timed`` the graph also records per-kernel timing events (``self.events``); with
+        ``parallel`` the graph holds launch_parallel()'s side branches."""
         self.launch()
         torch.cuda.synchronize()
+        if parallel:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.launch_parallel()
+            torch.cuda.synchronize()
+            self.graph = g
+            return g
         self.events = ([torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * len(self.layers) + 1)]
                        if timed else None)  # kept by the caller with the returned graph
         g = torch.cuda.CUDAGraph()

@@ -623,6 +623,15 @@ def test_wan_stack_chain_fold_invariant(cuda):
     torch.cuda.synchronize()
     assert torch.equal(ch.output.view(torch.int16), ref.output.view(torch.int16))
     assert ch.int_ops() == ref.int_ops()
+    # forked side branches (dead-end layers on side streams) reproduce every layer's output
+    outs = [y.clone() for y in ch.y]
+    for y in ch.y:
+        y.zero_()
+    ch.capture(parallel=True)
+    ch.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ch.y):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
 # ---------------------------------------------------------------- Eq. 5 weighted loss
