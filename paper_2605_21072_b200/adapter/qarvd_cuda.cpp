@@ -276,6 +276,102 @@ Tensor CudaQuantizedProvider::forward(const std::string& layer, const Tensor& x)
   return gemm_to_host(L, xq, sx, m);
 }
 
+namespace {
+// bf16 round-to-nearest-even of an f64 value (through f32, as bytes.hpp:40-45 for finite values)
+uint16_t bf16_rne(double v) {
+  const float f = static_cast<float>(v);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+double bf16_value(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+// rows of [a_hi a_hi a_lo] (x side) or [a_hi a_lo a_hi] (w side), 3k bf16 per row
+std::vector<uint16_t> split3(const double* a, size_t rows, size_t k, bool x_side) {
+  std::vector<uint16_t> out(rows * 3 * k);
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t c = 0; c < k; ++c) {
+      const double v = a[r * k + c];
+      const uint16_t hi = bf16_rne(v);
+      const uint16_t lo = bf16_rne(v - bf16_value(hi));
+      uint16_t* o = out.data() + r * 3 * k;
+      o[c] = hi;
+      o[k + c] = x_side ? hi : lo;
+      o[2 * k + c] = x_side ? lo : hi;
+    }
+  return out;
+}
+}  // namespace
+
+double weighted_loss(const std::vector<const CalibSample*>& batch, const LearnableQuantState& state,
+                     const std::vector<double>& chunk_weights) {
+  if (batch.empty()) throw std::invalid_argument("weighted loss: empty batch");
+  const size_t n = state.weight.rows(), k = state.weight.cols();
+  std::vector<int64_t> rows{0}, chunks;
+  for (const CalibSample* s : batch) {
+    if (s->x.cols() != k) throw std::invalid_argument("weighted loss: sample width does not match the weight");
+    rows.push_back(rows.back() + static_cast<int64_t>(s->x.rows()));
+    chunks.push_back(static_cast<int64_t>(s->chunk));
+  }
+  const size_t m = static_cast<size_t>(rows.back());
+  // stacked samples (f64, for K1) and the split bf16 operands of the target
+  std::vector<double> x64(m * k);
+  size_t off = 0;
+  for (const CalibSample* s : batch) {
+    std::memcpy(x64.data() + off, s->x.data(), s->x.size() * sizeof(double));
+    off += s->x.size();
+  }
+  const std::vector<uint16_t> xs = split3(x64.data(), m, k, true);
+  const std::vector<uint16_t> ws = split3(state.weight.data(), n, k, false);
+  // deployable state: hard codes in the kernel layout, learned group scales (f32), act scale
+  const Layout L = make_layout(state.plan, k);
+  const IntTensor hc = state.hard_codes();
+  std::vector<int8_t> wq(n * L.k_pad, 0);
+  std::vector<float> so(n), sn(n);
+  for (size_t r = 0; r < n; ++r) {
+    for (size_t c = 0; c < k; ++c) {
+      const size_t pc = state.plan.enabled ? static_cast<size_t>(state.plan.permutation[c]) : c;
+      wq[r * L.k_pad + L.pos[c]] = static_cast<int8_t>(hc.data[r * k + pc]);
+    }
+    sn[r] = static_cast<float>(state.weight_scale(r, false));
+    so[r] = static_cast<float>(state.plan.enabled ? state.weight_scale(r, true) : state.weight_scale(r, false));
+  }
+  const QuantParams act = state.act_params();
+  DevBuf x_dev(xs.data(), xs.size() * 2), w_dev(ws.data(), ws.size() * 2);
+  DevBuf x64_dev(x64.data(), x64.size() * sizeof(double));
+  DevBuf wq_dev(wq.data(), wq.size()), so_dev(so.data(), n * 4), sn_dev(sn.data(), n * 4);
+  DevBuf gather_dev(L.gather.data(), L.gather.size() * 4);
+  DevBuf xq_dev(m * L.k_pad), sx_dev(m * 4), err_dev(sizeof(int64_t));
+  check(qarvd_quantize_act(x64_dev.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(k),
+                           static_cast<int64_t>(k), gather_dev.as<int32_t>(), static_cast<int64_t>(L.k_pad),
+                           QARVD_ACT_PER_TENSOR, act.scale[0], act.bits, xq_dev.as<int8_t>(),
+                           static_cast<int64_t>(L.k_pad), sx_dev.as<float>(), nullptr, err_dev.as<int64_t>(),
+                           nullptr));
+  int64_t bad = 0;
+  check_cuda(cudaMemcpy(&bad, err_dev.p, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != INT64_MAX) throw std::invalid_argument("quantize: non-finite input");
+  const int64_t wsb = qarvd_weighted_loss_workspace(static_cast<int64_t>(m), static_cast<int64_t>(n),
+                                                    static_cast<int64_t>(batch.size()));
+  DevBuf work(static_cast<size_t>(wsb)), err(batch.size() * 8), loss(8);
+  check(qarvd_weighted_loss(x_dev.as<uint16_t>(), static_cast<int64_t>(3 * k), w_dev.as<uint16_t>(),
+                            static_cast<int64_t>(3 * k), xq_dev.as<int8_t>(), static_cast<int64_t>(L.k_pad),
+                            wq_dev.as<int8_t>(), static_cast<int64_t>(L.k_pad), static_cast<int64_t>(m),
+                            static_cast<int64_t>(n), static_cast<int64_t>(3 * k),
+                            static_cast<int64_t>(L.k_pad), static_cast<int64_t>(L.k_outlier),
+                            sx_dev.as<float>(), so_dev.as<float>(), sn_dev.as<float>(), rows.data(),
+                            chunks.data(), static_cast<int64_t>(batch.size()), chunk_weights.data(),
+                            static_cast<int64_t>(chunk_weights.size()), err.as<double>(), loss.as<double>(),
+                            work.p, wsb, nullptr));
+  double out = 0.0;
+  check_cuda(cudaMemcpy(&out, loss.p, 8, cudaMemcpyDeviceToHost));
+  return out;
+}
+
 Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed) {
   const CudaQuantizedProvider provider(qm);
   return run_rollout(qm.cfg, provider, &provider, QuantTarget::all, 0, prompt_seed);

@@ -7,6 +7,7 @@
 //     qarvd::kernel_b_gemm_dequant         -> qarvd::cuda::kernel_b_gemm_dequant
 //     qarvd::quantized_layer_forward       -> qarvd::cuda::quantized_layer_forward
 //     qarvd::analyze_layer                 -> qarvd::cuda::analyze_layer
+//     qarvd::weighted_loss                 -> qarvd::cuda::weighted_loss
 //     QuantizedProvider (engine.cpp:146-171) -> qarvd::cuda::CudaQuantizedProvider
 // Signatures, argument meaning and exception types/messages follow the
 // reference.  All arithmetic runs in libqarvd_b200.so (sm_100a); this file only
@@ -19,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "qarvd/calibrate.hpp"
 #include "qarvd/engine.hpp"
 #include "qarvd/outlier.hpp"
 #include "qarvd/quant.hpp"
@@ -45,6 +47,14 @@ Tensor quantized_layer_forward(const QuantizedLayer& layer, const Tensor& x, Eng
 OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w,
                             double tau = kDefaultTau, double alpha_min = kDefaultAlphaMin,
                             size_t align = kDefaultAlign);
+
+// calibrate.hpp:80-82 — Eq. 5 with the deployable (hard-rounded) weights, evaluated by one
+// fused tcgen05 kernel (qarvd_weighted_loss).  The f64 operands of the target X W^T are split
+// into bf16 hi/lo parts and stacked along K ([X_hi X_hi X_lo] . [W_hi W_lo W_hi]^T, ~24-bit
+// products, fp32 tensor-core accumulation); the prediction FQ(X) What^T is exact int8 x int8.
+// Equals the reference within ~1e-5 relative; same exceptions (empty batch, chunk range).
+double weighted_loss(const std::vector<const CalibSample*>& batch, const LearnableQuantState& state,
+                     const std::vector<double>& chunk_weights);
 
 // Device-resident copy of one QuantizedLayer (codes padded into the kernel layout).
 class DeviceLayer;

@@ -386,9 +386,9 @@ extern "C" int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_
     if (sample_rows[s + 1] < sample_rows[s])
       QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "weighted loss: sample rows must be non-decreasing");
   if (m <= 0 || n <= 0 || k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "weighted loss: empty shape");
-  if (k_pad % 32 || k_outlier % 32 || k_outlier < 0 || k_outlier >= k_pad || k_pad < k)
+  if (k_pad % 32 || k_outlier % 32 || k_outlier < 0 || k_outlier >= k_pad)
     QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
-               "weighted loss: k_pad and k_outlier must be multiples of 32 with 0 <= k_outlier < k_pad, k_pad >= k");
+               "weighted loss: k_pad and k_outlier must be multiples of 32 with 0 <= k_outlier < k_pad");
   if (k_pad > 132104)
     QARVD_FAIL(QARVD_ERR_LOGIC, "weighted loss: reduction dimension too large for exact int32 accumulation");
   if (ldx < k || ldw < k || ldq < k_pad || ldwq < k_pad || ldx % 8 || ldw % 8 || ldq % 16 || ldwq % 16)

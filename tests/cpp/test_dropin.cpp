@@ -81,6 +81,48 @@ int main() {
   }
   std::printf("checked %zu quantized layers\n", n_layers);
 
+  // ---- Eq. 5 weighted_loss (calibrate.cpp:201-224) through the fused GPU kernel, on
+  // reference-initialised LearnableQuantStates of every quantized layer (f64 toy data)
+  {
+    double worst = 0.0;
+    size_t n_loss = 0;
+    for (const auto& l : qm.layers) {
+      if (l.preserved) continue;
+      const Tensor& W = model.weight(l.name);
+      const OutlierReport rep = qarvd::analyze_layer(l.name, W);
+      const DualScalePlan plan = build_plan(W, rep, 8);
+      std::vector<CalibSample> samples(3);
+      std::vector<const CalibSample*> batch;
+      for (size_t s = 0; s < samples.size(); ++s) {
+        samples[s].layer = l.name;
+        samples[s].chunk = s + 1;
+        samples[s].x = random_tensor(16 + 7 * s, l.in_dim, 900 + 31 * n_loss + s, 1.0);
+        batch.push_back(&samples[s]);
+      }
+      const QuantParams act = init_scale_minmax(samples[0].x, 8, Granularity::per_tensor, 0);
+      const LearnableQuantState st = LearnableQuantState::init(W, plan, act, opts.base);
+      const double ref = qarvd::weighted_loss(batch, st, w);
+      const double gpu = qarvd::cuda::weighted_loss(batch, st, w);
+      const double rel = std::fabs(gpu - ref) / std::fabs(ref);
+      worst = std::max(worst, rel);
+      EXPECT(rel <= 1e-4, ("weighted_loss within 1e-4 " + l.name).c_str());
+      ++n_loss;
+    }
+    std::printf("weighted_loss on %zu layers: worst relative difference %.3e\n", n_loss, worst);
+    bool ok = false;
+    try {
+      const Tensor& W = model.weight(qm.layers[1].name);
+      const DualScalePlan plan = build_plan(W, qarvd::analyze_layer("l", W), 8);
+      const LearnableQuantState st = LearnableQuantState::init(
+          W, plan, QuantParams::per_tensor_symmetric(8, 0.1), opts.base);
+      CalibSample s{"l", 9, random_tensor(4, W.cols(), 1, 1.0)};
+      qarvd::cuda::weighted_loss({&s}, st, w);
+    } catch (const std::out_of_range& e) {
+      ok = std::string(e.what()) == "weighted loss: sample chunk outside the weight vector";
+    }
+    EXPECT(ok, "weighted_loss chunk out of range -> std::out_of_range with the reference message");
+  }
+
   // ---- the seam: run_rollout with the CUDA provider vs the reference int engine
   for (uint64_t seed : {5000ull, 5001ull}) {
     const Rollout ref = run_quantized(qm, seed, Engine::int_kernels);
