@@ -393,6 +393,60 @@ def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
     return out
 
 
+def recon_loss_bench(torch, peaks, iters=10):
+    """Eq. 5 objective (weighted_loss, calibrate.cpp:201-224) on one Wan layer's calibration set:
+    1536 -> 1536 (K_o from K3), 21 frames x 1560 tokens, heuristic_exp chunk weights; one
+    qarvd_weighted_loss call = bf16 target GEMM + dual int8 GEMM + squared-error reduction."""
+    import paper_2605_21072_b200 as qb
+    from paper_2605_21072_b200 import calibrate, engine, synth
+
+    spec = synth.wan_registry(blocks=1)[0]
+    w = synth.synth_weight(spec, seed=1)
+    rep = qb.analyze_layer(spec.name, w)
+    layer = engine.prepare_weights(spec.name, w, engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers))
+    frames, rows = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME
+    xs = torch.cat([synth.synth_activation(rows, spec.in_dim, seed=3, frame=f) for f in range(frames)])
+    m, k, n = xs.shape[0], spec.in_dim, spec.out_dim
+    xq, s32, _ = engine.kernel_a_quantize_activation(xs, layer, qb.ACT_PER_TENSOR,
+                                                     static_scale=float(xs.float().abs().max()) / 127.0)
+    row_off = np.arange(frames + 1, dtype=np.int64) * rows
+    chunks = np.arange(1, frames + 1, dtype=np.int64)
+    cw = calibrate.weighting_strategy("heuristic_exp", frames)
+    wsb = int(qb._lib.load().qarvd_weighted_loss_workspace(m, n, frames))
+    ws = torch.empty(wsb // 8, dtype=torch.float64, device="cuda")
+    err = torch.empty(frames, dtype=torch.float64, device="cuda")
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        qb._lib.call("qarvd_weighted_loss", xs.data_ptr(), k, w.data_ptr(), k, xq.data_ptr(), layer.k_pad,
+                     layer.wq.data_ptr(), layer.k_pad, m, n, k, layer.k_pad, layer.k_outlier, s32.data_ptr(),
+                     layer.scale_outlier32.data_ptr(), layer.scale_normal32.data_ptr(), row_off.ctypes.data,
+                     chunks.ctypes.data, frames, cw.ctypes.data, frames, err.data_ptr(), loss.data_ptr(),
+                     ws.data_ptr(), wsb, st)
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    flops, iops = 2.0 * m * n * k, 2.0 * m * n * layer.k_pad
+    pb, pi = peaks.get("bf16_tflops", 1590.0), 2.0 * peaks.get("bf16_tflops", 1590.0)
+    ideal_ms = (flops / (pb * 1e12) + iops / (pi * 1e12)) * 1e3
+    return {"workload": f"Eq.5 weighted loss, {n}x{k} layer, {frames} frames x {rows} tokens (M={m})",
+            "ms_per_loss": ms, "bf16_tflops": flops / (ms * 1e-3) / 1e12, "int8_tops": iops / (ms * 1e-3) / 1e12,
+            "roofline": {"bound": "tensor", "ideal_ms": ideal_ms, "frac": ideal_ms / ms,
+                         "note": "ideal = bf16 target at measured bf16 burst + int8 slabs at 2x that"},
+            "loss": float(loss.item())}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -508,6 +562,7 @@ def main():
     if not args.no_calib:
         calib = calibration_bench(torch, world, rank, args.calib_steps, peaks.get("hbm_gbs", 6650.0))
 
+    recon = recon_loss_bench(torch, peaks)
     stack = None
     if not args.no_stack:
         stack = stack_bench(torch, world, rank, args.stack_steps, 2.0 * peaks.get("bf16_tflops", 1590.0),
@@ -557,6 +612,7 @@ def main():
             "gpu_launches": int(launches),
             "calibration": calib,
             "stack": stack,
+            "recon_loss": recon,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

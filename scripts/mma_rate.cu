@@ -101,6 +101,7 @@ int main() {
   run<0, 128>("i8   M128 N128 K32", 32, 148);
   run<1, 256>("bf16 M128 N256 K16", 16, 1);
   run<1, 256>("bf16 M128 N256 K16", 16, 148);
+  run<1, 128>("bf16 M128 N128 K16", 16, 148);
   run<2, 256>("e4m3 M128 N256 K32", 32, 148);
   return 0;
 }
