@@ -37,24 +37,27 @@ namespace {
 
 constexpr int LBM = 128;          // rows per CTA (TMEM lanes); an SM pair computes 256-row tiles
 constexpr int LTM = 2 * LBM;      // rows of a pair tile
-constexpr int LBN = 128;          // columns per tile
+constexpr int LBN = 256;          // columns per tile (each CTA of the pair holds half of B)
 constexpr int LKS = 2;            // 128-byte K sub-tiles per stage (8 MMAs per mbarrier wait)
 constexpr int kLossSubA = LBM * 128;
-constexpr int kLossSubB = (LBN / 2) * 128;  // each CTA of the pair holds half of B
+constexpr int kLossSubB = (LBN / 2) * 128;
 constexpr int kLossStageA = LKS * kLossSubA;
 constexpr int kLossStageB = LKS * kLossSubB;
 constexpr int kLossStageBytes = kLossStageA + kLossStageB;
-constexpr int kLossStages = 4;
-constexpr int kLossEpiWarps = 8;
+constexpr int kLossStages = 3;
+constexpr int kLossEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kLossThreads = 128 + 32 * kLossEpiWarps;
+constexpr int kLossCtrlRegs = 32;  // setmaxnreg split of 640 x 96 registers
+constexpr int kLossEpiRegs = 112;
 constexpr size_t kLossSmem = static_cast<size_t>(kLossStages) * kLossStageBytes + 1024;
+constexpr int kLossParts = 4;      // column partials per row and tile (one per epilogue warp)
 
 struct LossParams {
   int64_t m, n, k, k_pad, k_o;
   const float* scale_x;   // [m]
   const float* scale_wo;  // [n]
   const float* scale_wn;  // [n]
-  double* part;           // [2 * num_n_blks][m] per-row partial sums of d^2
+  double* part;           // [kLossParts * num_n_blks][m] per-row partial sums of d^2
   int num_m_blks, num_n_blks, num_tiles;
 };
 
@@ -74,9 +77,34 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
       : "memory");
 }
 
-// SM-pair kernel (cluster of 2, cta_group::2): the leader CTA issues M = 256 MMAs whose A rows
-// are split over the two CTAs' shared memory (128 each) and whose B tile is split in halves;
-// each CTA's TMEM receives its own 128 rows of the three accumulators.
+// Stage sequence of one tile: F1 (first half of the bf16 target stages), O (int8 stages holding
+// outlier steps; only those issue), F2 (the other bf16 stages), N (int8 stages holding normal
+// steps).  Every TMEM hand-off then overlaps MMA work: acc_o is folded during F2, acc_t read
+// during N, acc_n read during the next tile's F1.  A stage straddling K_o loads in O and N.
+struct LossPhases {
+  int no, nf, nf1, nn, n0;  // stage counts; n0 = first int8 stage of N
+  __device__ LossPhases(const LossParams& p) {
+    const int ko32 = static_cast<int>(p.k_o / 32), k32 = static_cast<int>(p.k_pad / 32);
+    no = (ko32 + 4 * LKS - 1) / (4 * LKS);
+    nf = static_cast<int>((p.k + 64 * LKS - 1) / (64 * LKS));
+    nf1 = no > 0 ? nf / 2 : nf;
+    n0 = ko32 / (4 * LKS);
+    nn = (k32 + 4 * LKS - 1) / (4 * LKS) - n0;
+  }
+  __device__ int total() const { return no + nf + nn; }
+  // stage i of a tile -> kind (0 bf16, 1 int8 outlier, 2 int8 normal) and K block
+  __device__ void at(int i, int& kind, int& blk) const {
+    if (i < nf1) { kind = 0; blk = i; }
+    else if (i < nf1 + no) { kind = 1; blk = i - nf1; }
+    else if (i < nf + no) { kind = 0; blk = i - no; }
+    else { kind = 2; blk = n0 + i - nf - no; }
+  }
+};
+
+// SM-pair kernel (cluster of 2, cta_group::2).  TMEM: R1 = columns [0, 256) hold acc_t; R2 =
+// [256, 512) holds acc_o, then (after the epilogue folded s_wo*acc_o into registers) acc_n.
+// Epilogue per row and column: e = acc_t - s_x*(s_wo*acc_o) once acc_t lands (R1 released),
+// then d = e - s_x*(s_wn*acc_n) once acc_n lands (R2 released).
 __global__ void __launch_bounds__(kLossThreads, 1)
     recon_loss_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       const __grid_constant__ CUtensorMap tmXq, const __grid_constant__ CUtensorMap tmWq,
@@ -86,9 +114,12 @@ __global__ void __launch_bounds__(kLossThreads, 1)
   uint8_t* sB = smem + kLossStages * kLossStageA;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kLossStages * kLossStageBytes);
   uint64_t* empty = full + kLossStages;
-  uint64_t* tfull = empty + kLossStages;  // [2] tile accumulators complete (both CTAs)
-  uint64_t* sfree = tfull + 2;            // [4] TMEM slot released (leader's copy counts)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 4);
+  uint64_t* ofull = empty + kLossStages;  // acc_o complete (both CTAs)
+  uint64_t* ffull = ofull + 1;            // acc_t complete (both CTAs)
+  uint64_t* tfull = ffull + 1;            // acc_n complete: tile done (both CTAs)
+  uint64_t* r1free = tfull + 1;           // R1 read by every epilogue warp (leader's copy)
+  uint64_t* r2free = r1free + 1;          // R2 read (once per use)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r2free + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -105,8 +136,11 @@ __global__ void __launch_bounds__(kLossThreads, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) ptx::mbar_init(&tfull[s], 1);
-    for (int s = 0; s < 4; ++s) ptx::mbar_init(&sfree[s], 2 * kLossEpiWarps);
+    ptx::mbar_init(ofull, 1);
+    ptx::mbar_init(ffull, 1);
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(r1free, 2 * kLossEpiWarps);
+    ptx::mbar_init(r2free, 2 * kLossEpiWarps);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
@@ -118,32 +152,36 @@ __global__ void __launch_bounds__(kLossThreads, 1)
   pdl_wait();
   pdl_launch_dependents();
 
-  const int nkf = static_cast<int>((p.k + 64 * LKS - 1) / (64 * LKS));      // bf16 stages
-  const int nki = static_cast<int>((p.k_pad + 128 * LKS - 1) / (128 * LKS));  // int8 stages
+  const LossPhases ph(p);
   const int k16 = static_cast<int>((p.k + 15) / 16);
   const int k32 = static_cast<int>(p.k_pad / 32), ko32 = static_cast<int>(p.k_o / 32);
+  const bool has_o = ko32 > 0;
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs; bytes land on the leader's barrier) =====
+    ptx::setmaxnreg_dec<kLossCtrlRegs>();
     int stage = 0;
     uint32_t phase = 0;
     for (int t = pair; t < p.num_tiles; t += num_pairs) {
       const int a_row = (t % p.num_m_blks) * LTM + static_cast<int>(rank) * LBM;
       const int b_row = (t / p.num_m_blks) * LBN + static_cast<int>(rank) * (LBN / 2);
-      for (int i = 0; i < nkf + nki; ++i) {
+      for (int i = 0; i < ph.total(); ++i) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           if (leader) ptx::mbar_expect_tx(&full[stage], 2 * kLossStageBytes);
+          int kind, blk;
+          ph.at(i, kind, blk);
+          const bool bf = kind == 0;
 #pragma unroll
           for (int ks = 0; ks < LKS; ++ks) {
             uint8_t* a = sA + stage * kLossStageA + ks * kLossSubA;
             uint8_t* b = sB + stage * kLossStageB + ks * kLossSubB;
-            if (i < nkf) {
-              const int kc = (i * LKS + ks) * 64;
+            if (bf) {
+              const int kc = (blk * LKS + ks) * 64;
               ptx::tma_load_2d_2sm(a, &tmX, &full[stage], kc, a_row);
               ptx::tma_load_2d_2sm(b, &tmW, &full[stage], kc, b_row);
             } else {
-              const int kc = ((i - nkf) * LKS + ks) * 128;
+              const int kc = (blk * LKS + ks) * 128;
               ptx::tma_load_2d_2sm(a, &tmXq, &full[stage], kc, a_row);
               ptx::tma_load_2d_2sm(b, &tmWq, &full[stage], kc, b_row);
             }
@@ -156,115 +194,143 @@ __global__ void __launch_bounds__(kLossThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && leader) {
+  } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    constexpr uint32_t id_f = idesc_bf16(LTM, LBN);
-    constexpr uint32_t id_i = ptx::idesc_i8(LTM, LBN);
-    const uint64_t a0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sA));
-    const uint64_t b0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sB));
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t slot_par = 0;  // per-slot parity of the next use
-    auto take_slot = [&](int s) {
-      ptx::mbar_wait(&sfree[s], ((slot_par >> s) & 1u) ^ 1u);
-      slot_par ^= 1u << s;
-      ptx::tc_fence_after();
-    };
-    int ti = 0;
-    for (int t = pair; t < p.num_tiles; t += num_pairs, ++ti) {
-      const int st = (3 * ti) & 3, so = (3 * ti + 1) & 3, sn = (3 * ti + 2) & 3;
-      const uint32_t d_t = tmem_base + static_cast<uint32_t>(st * LBN);
-      const uint32_t d_o = tmem_base + static_cast<uint32_t>(so * LBN);
-      const uint32_t d_n = tmem_base + static_cast<uint32_t>(sn * LBN);
-      take_slot(st);
-      for (int i = 0; i < nkf + nki; ++i) {
-        if (i == nkf) {
-          take_slot(so);
-          take_slot(sn);
-        }
-        ptx::mbar_wait(&full[stage], phase);
+    ptx::setmaxnreg_dec<kLossCtrlRegs>();
+    if (leader) {
+      constexpr uint32_t id_f = idesc_bf16(LTM, LBN);
+      constexpr uint32_t id_i = ptx::idesc_i8(LTM, LBN);
+      const uint64_t a0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sA));
+      const uint64_t b0 = ptx::sw128_kmajor_desc(ptx::smem_u32(sB));
+      const uint32_t r1 = tmem_base, r2 = tmem_base + LBN;
+      int stage = 0;
+      uint32_t phase = 0, u1 = 0, u2 = 0;  // uses of R1 / R2 so far
+      auto take = [&](uint64_t* bar, uint32_t& u) {
+        ptx::mbar_wait(bar, (u & 1u) ^ 1u);
+        ++u;
         ptx::tc_fence_after();
-        const uint64_t ad = a0 + static_cast<uint64_t>(stage * (kLossStageA >> 4));
-        const uint64_t bd = b0 + static_cast<uint64_t>(stage * (kLossStageB >> 4));
-        if (lane == 0) {
+      };
+      for (int t = pair; t < p.num_tiles; t += num_pairs) {
+        for (int i = 0; i < ph.total(); ++i) {
+          int kind, blk;
+          ph.at(i, kind, blk);
+          if (kind == 0 && blk == 0) take(r1free, u1);        // acc_t(prev) read
+          if (kind == 1 && blk == 0) take(r2free, u2);        // acc_n(prev) read
+          if (kind == 2 && blk == ph.n0) take(r2free, u2);    // acc_o folded (or acc_n(prev) read)
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t ad = a0 + static_cast<uint64_t>(stage * (kLossStageA >> 4));
+          const uint64_t bd = b0 + static_cast<uint64_t>(stage * (kLossStageB >> 4));
+          if (lane == 0) {
 #pragma unroll
-          for (int j = 0; j < 4 * LKS; ++j) {
-            // sub-tile j/4, +32 bytes along K inside the 128B swizzle row = +2 per step
-            const uint64_t ao = static_cast<uint64_t>((j >> 2) * (kLossSubA >> 4) + 2 * (j & 3));
-            const uint64_t bo = static_cast<uint64_t>((j >> 2) * (kLossSubB >> 4) + 2 * (j & 3));
-            if (i < nkf) {
-              const int s16 = i * 4 * LKS + j;
-              if (s16 < k16) mma_bf16_2sm(d_t, ad + ao, bd + bo, id_f, s16 > 0 ? 1u : 0u);
-            } else {
-              const int s32 = (i - nkf) * 4 * LKS + j;
-              if (s32 < k32) {
-                const bool outl = s32 < ko32;
-                const uint32_t acc = (outl ? s32 == 0 : s32 == ko32) ? 0u : 1u;
-                ptx::mma_i8_2sm(outl ? d_o : d_n, ad + ao, bd + bo, id_i, acc);
+            for (int j = 0; j < 4 * LKS; ++j) {
+              const uint64_t ao = static_cast<uint64_t>((j >> 2) * (kLossSubA >> 4) + 2 * (j & 3));
+              const uint64_t bo = static_cast<uint64_t>((j >> 2) * (kLossSubB >> 4) + 2 * (j & 3));
+              if (kind == 0) {
+                const int s16 = blk * 4 * LKS + j;
+                if (s16 < k16) mma_bf16_2sm(r1, ad + ao, bd + bo, id_f, s16 > 0 ? 1u : 0u);
+              } else {
+                const int s32 = blk * 4 * LKS + j;
+                const bool outl = kind == 1;
+                if (s32 < k32 && (s32 < ko32) == outl) {
+                  const uint32_t acc = (outl ? s32 == 0 : s32 == ko32) ? 0u : 1u;
+                  ptx::mma_i8_2sm(r2, ad + ao, bd + bo, id_i, acc);
+                }
               }
             }
+            ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+            if (kind == 1 && blk == ph.no - 1) ptx::mma_commit_2sm_mc(ofull, 0x3);
+            if (kind == 0 && blk == ph.nf - 1) ptx::mma_commit_2sm_mc(ffull, 0x3);
           }
-          ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+          __syncwarp();
+          if (++stage == kLossStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        if (lane == 0) ptx::mma_commit_2sm_mc(tfull, 0x3);
         __syncwarp();
-        if (++stage == kLossStages) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
-      if (lane == 0) ptx::mma_commit_2sm_mc(&tfull[ti & 1], 0x3);
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs, own 128 rows) =====================
+    ptx::setmaxnreg_inc<kLossEpiRegs>();
     const int ew = warp - 4;
     const int q = warp & 3;          // TMEM lane quadrant
-    const int h = ew >> 2;           // column half
-    const bool has_o = p.k_o > 0;
+    const int h = ew >> 2;           // 64-column quarter of the tile
     const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t r1 = tmem_base + t_lane + static_cast<uint32_t>(h * 64);
+    const uint32_t r2 = r1 + LBN;
     int ti = 0;
     for (int t = pair; t < p.num_tiles; t += num_pairs, ++ti) {
       const int m_blk = t % p.num_m_blks, n_blk = t / p.num_m_blks;
       const int64_t row = static_cast<int64_t>(m_blk) * LTM + rank * LBM + q * 32 + lane;
+      const int64_t col0 = static_cast<int64_t>(n_blk) * LBN + h * 64;
       const float sx = row < p.m ? p.scale_x[row] : 0.f;
-      const int st = (3 * ti) & 3, so = (3 * ti + 1) & 3, sn = (3 * ti + 2) & 3;
-      ptx::mbar_wait(&tfull[ti & 1], (ti >> 1) & 1);
+      float ev[64];  // s_wo*acc_o, then e = acc_t - s_x*(s_wo*acc_o), of this row's 64 columns
+      if (has_o) {
+        ptx::mbar_wait(ofull, ti & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) {
+          uint32_t ro[16];
+          ptx::tmem_ld16(r2 + c, ro);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int64_t j = col0 + c + e;
+            const float swo = j < p.n ? __ldg(p.scale_wo + j) : 0.f;
+            ev[c + e] = __fmul_rn(swo, __int2float_rn(static_cast<int>(ro[e])));
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(r2free);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) ev[c] = 0.f;
+      }
+      ptx::mbar_wait(ffull, ti & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        uint32_t rt[16];
+        ptx::tmem_ld16(r1 + c, rt);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          ev[c + e] = __fmaf_rn(-sx, ev[c + e], __uint_as_float(rt[e]));
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_leader(r1free);
+      ptx::mbar_wait(tfull, ti & 1);
       ptx::tc_fence_after();
       double acc = 0.0;
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < 64; c += 16) {
-        const int col = h * 64 + c;
-        uint32_t rt[16], ro[16], rn[16];
-        ptx::tmem_ld16(tmem_base + t_lane + static_cast<uint32_t>(st * LBN + col), rt);
-        ptx::tmem_ld16(tmem_base + t_lane + static_cast<uint32_t>(sn * LBN + col), rn);
-        if (has_o) ptx::tmem_ld16(tmem_base + t_lane + static_cast<uint32_t>(so * LBN + col), ro);
+        uint32_t rn[16];
+        ptx::tmem_ld16(r2 + c, rn);
         ptx::tmem_wait_ld();
         float part = 0.f;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int64_t j = static_cast<int64_t>(n_blk) * LBN + col + e;  // warp-uniform
+          const int64_t j = col0 + c + e;
           const float swn = j < p.n ? __ldg(p.scale_wn + j) : 0.f;
-          float pr = __fmul_rn(swn, __int2float_rn(static_cast<int>(rn[e])));
-          if (has_o) {
-            const float swo = j < p.n ? __ldg(p.scale_wo + j) : 0.f;
-            pr = __fmaf_rn(swo, __int2float_rn(static_cast<int>(ro[e])), pr);
-          }
-          const float d = __fsub_rn(__uint_as_float(rt[e]), __fmul_rn(sx, pr));
+          const float d = __fmaf_rn(-sx, __fmul_rn(swn, __int2float_rn(static_cast<int>(rn[e]))), ev[c + e]);
           part = __fmaf_rn(d, d, part);
         }
         acc += static_cast<double>(part);
       }
-      // all reads of this tile's slots are complete: release them to the leader's MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive_leader(&sfree[st]);
-        ptx::mbar_arrive_leader(&sfree[so]);
-        ptx::mbar_arrive_leader(&sfree[sn]);
-      }
-      if (row < p.m) p.part[static_cast<int64_t>(2 * n_blk + h) * p.m + row] = acc;
+      if (lane == 0) ptx::mbar_arrive_leader(r2free);
+      if (row < p.m) p.part[static_cast<int64_t>(kLossParts * n_blk + h) * p.m + row] = acc;
     }
+  } else {
+    ptx::setmaxnreg_dec<kLossCtrlRegs>();  // warps 2-3
   }
+  ptx::tc_fence_before();
   __syncthreads();
   ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
@@ -350,7 +416,7 @@ int loss_sm_count() {
   return count;
 }
 
-int64_t part_count(int64_t n) { return 2 * ((n + LBN - 1) / LBN); }
+int64_t part_count(int64_t n) { return kLossParts * ((n + LBN - 1) / LBN); }
 
 }  // namespace
 }  // namespace qarvd_b200
