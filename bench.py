@@ -447,6 +447,49 @@ def recon_loss_bench(torch, peaks, iters=10):
             "loss": float(loss.item())}
 
 
+def cpu_baselines_calib_loss(torch, threads):
+    """The reference CPU path (oracle/_ref, compiled reference sources) beside configs 4 and the
+    Eq. 5 objective, on bounded samples: (a) init_scale_percentile_search (quant.cpp:185-226) +
+    analyze_layer (outlier.cpp:80-102) on `threads` K=1536 Wan layers at the full 21 x 1560
+    token shape, layer-parallel (calibrate.cpp:440-484 runs layers in parallel); (b)
+    weighted_loss (calibrate.cpp:220-224) on one 1560-token frame of a 1536 x 1536 layer, single
+    thread, extrapolated x21 to the 21-frame layer objective."""
+    import concurrent.futures as cf
+    import oracle
+    from paper_2605_21072_b200 import synth
+
+    if not oracle.ref_available():
+        return None
+    r = oracle.ref()
+    r.ref_set_threads(1)
+    frames, rows, k = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME, synth.WAN_DIM
+    x64 = torch.cat([synth.synth_activation(rows, k, seed=3, frame=f) for f in range(frames)]).double().cpu().numpy()
+    spec = synth.wan_registry(blocks=1)[0]
+    w64 = synth.synth_weight(spec, seed=1).double().cpu().numpy()
+    n_layers = max(1, min(threads, 8))
+
+    def one_layer(_):
+        oracle.ref_analyze_layer(w64)
+        return oracle.ref_percentile_search(x64, frames, rows, k)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(n_layers) as ex:
+        list(ex.map(one_layer, range(n_layers)))
+    t_cal = time.perf_counter() - t0
+    out = {"calibration": {"value": n_layers / t_cal, "unit": "layers/s", "cores": n_layers, "kind": "reference",
+                           "sample": f"{n_layers} K=1536 layers (analyze_layer + init_scale_percentile_search, "
+                                     f"{frames} x {rows} tokens each), one layer per thread"}}
+    xs = x64[:rows]
+    t0 = time.perf_counter()
+    oracle.ref_weighted_loss(w64, np.zeros(0, np.int64), float(np.abs(xs).max()) / 127.0, xs,
+                             np.array([0, rows]), np.array([1]), np.ones(1))
+    t_loss = time.perf_counter() - t0
+    out["recon_loss"] = {"value": 1e3 * t_loss * frames, "unit": "ms per layer objective (21 frames)",
+                         "cores": 1, "kind": "reference",
+                         "sample": f"weighted_loss on 1 of {frames} frames ({rows} x {k} -> {k}), x{frames}"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -632,6 +675,14 @@ def main():
                                             "sample": f"{rows} of {M_TOKENS} rows through ffn.0 + ffn.2 (permute -> kernel A -> kernel B), reference parallel_for"}
             except Exception as ex:  # reported, never fatal
                 line["cpu_baseline"] = {"error": str(ex)}
+            try:
+                extra = cpu_baselines_calib_loss(torch, os.cpu_count() or 1)
+                if extra:
+                    if line.get("calibration"):
+                        line["calibration"]["cpu_baseline"] = extra["calibration"]
+                    line["recon_loss"]["cpu_baseline"] = extra["recon_loss"]
+            except Exception as ex:  # reported, never fatal
+                line["recon_loss"]["cpu_baseline"] = {"error": str(ex)}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

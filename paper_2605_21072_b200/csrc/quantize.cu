@@ -1300,7 +1300,7 @@ int launch_act_rows_g(const uint16_t* x, int64_t m, int k, int64_t ldx, const in
   int w = k1_team_warps(k / 8), slots = w == 1 ? 1 : 3;
   // diagnostics: QARVD_K1_SHAPE=<warps>x<slots> overrides the team shape of one-CTA teams
   static const char* shape = getenv("QARVD_K1_SHAPE");
-  if (shape && w > 1) sscanf(shape, "%dx%d", &w, &slots);
+  if (shape) sscanf(shape, "%dx%d", &w, &slots);
   const int key = w * 10 + slots;
   switch (key) {
 #define QARVD_K1_CASE(WW, SS, TEAMS)                                                              \

@@ -163,8 +163,10 @@ __global__ void __launch_bounds__(kLossThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int t = pair; t < p.num_tiles; t += num_pairs) {
-      const int a_row = (t % p.num_m_blks) * LTM + static_cast<int>(rank) * LBM;
-      const int b_row = (t / p.num_m_blks) * LBN + static_cast<int>(rank) * (LBN / 2);
+      // n-fastest tile order: the pairs in flight share a few A row blocks (L2-resident), so X
+      // and xq stream from HBM about once instead of once per column block
+      const int a_row = (t / p.num_n_blks) * LTM + static_cast<int>(rank) * LBM;
+      const int b_row = (t % p.num_n_blks) * LBN + static_cast<int>(rank) * (LBN / 2);
       for (int i = 0; i < ph.total(); ++i) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kLossThreads, 1)
     const uint32_t r2 = r1 + LBN;
     int ti = 0;
     for (int t = pair; t < p.num_tiles; t += num_pairs, ++ti) {
-      const int m_blk = t % p.num_m_blks, n_blk = t / p.num_m_blks;
+      const int m_blk = t / p.num_n_blks, n_blk = t % p.num_n_blks;
       const int64_t row = static_cast<int64_t>(m_blk) * LTM + rank * LBM + q * 32 + lane;
       const int64_t col0 = static_cast<int64_t>(n_blk) * LBN + h * 64;
       const float sx = row < p.m ? p.scale_x[row] : 0.f;
