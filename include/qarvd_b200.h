@@ -197,6 +197,19 @@ int qarvd_dual_gemm_rowmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int6
  *   row_pmax[i * pm_count + p] = max over output columns of tile/epilogue-warp p of
  *                                (bf16 bits of y[i, j]) & 0x7fff,
  * pm_count = qarvd_dual_gemm_pmax_count(m, n, k) partials per row, rewritten every call. */
+/* Stream-K variant of qarvd_dual_gemm for bf16 outputs: when the last wave of 256 x 256 pair
+ * tiles is partial and K is long, the remainder tiles are split along K over all SM pairs
+ * (int32 partial sums of the normal slab exchanged through `workspace`, exact).  Results are
+ * bit-identical to qarvd_dual_gemm.  workspace: device, 256-byte aligned, ZERO-FILLED once
+ * before first use (its counters reset themselves), >= qarvd_dual_gemm_workspace_size bytes
+ * (0 = this shape runs data-parallel; the call then ignores the workspace).  One workspace
+ * per concurrently running call. */
+int64_t qarvd_dual_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int64_t k_outlier);
+int qarvd_dual_gemm_ws(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                       int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                       const float* scale_w_outlier, const float* scale_w_normal, const float* bias,
+                       int epilogue, uint16_t* y, int64_t ldy, void* workspace,
+                       int64_t workspace_bytes, void* stream);
 int64_t qarvd_dual_gemm_pmax_count(int64_t m, int64_t n, int64_t k);
 int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
                          int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,

@@ -173,6 +173,10 @@ SIGNATURES = {
         [POINTER(SearchJob), c_int, POINTER(c_double), c_int, POINTER(c_double), c_int, c_void_p],
     ),
     "qarvd_weighted_loss_workspace": (c_int64, [c_int64, c_int64, c_int64]),
+    "qarvd_dual_gemm_workspace_size": (c_int64, [c_int64, c_int64, c_int64, c_int64]),
+    "qarvd_dual_gemm_ws": (
+        c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p]),
     "qarvd_weighted_loss": (
         c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                 c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -88,7 +88,72 @@ struct GemmParams {
   int epi_regs;       // fast path holds acc_n in registers (QARVD_GEMM_EPIREG=0 disables)
   int spin;
   int trace;  // QARVD_GEMM_TRACE: CTA 0 prints per-tile clocks (diagnostic)
+  // stream-K (optional, qarvd_dual_gemm_ws): tiles [0, sk_tiles) are split along K into
+  // contiguous ranges of k-blocks over all SM pairs (processed first), the rest are
+  // data-parallel.  A pair that does not own a tile's last k-block stores its partial acc_n
+  // (int32, exact) in sk_slots; the owner adds them in its epilogue.
+  int sk_tiles;
+  int sk_slots_per_tile;
+  int32_t* sk_slots;    // [sk_tiles][sk_slots_per_tile][BN][TM] int32, column-major per tile
+  uint32_t* sk_count;   // [sk_tiles][2]: writer-warp arrivals, owner-warp reads (self-resetting)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
+};
+
+// Work list of one SM pair: its stream-K k-block range over the split tiles first, then its
+// data-parallel tiles (t = sk_tiles + pair, + pairs, ...).  Unit u = tile * nkb + issue index.
+struct SkSched {
+  int tiles, pairs, sk, nkb;
+  int64_t units;  // sk * nkb
+  __host__ __device__ SkSched(int tiles_, int pairs_, int sk_, int nkb_)
+      : tiles(tiles_), pairs(pairs_), sk(sk_), nkb(nkb_), units(static_cast<int64_t>(sk_) * nkb_) {}
+  __host__ __device__ int64_t u_begin(int c) const { return units * c / pairs; }
+  // the pair whose range holds unit u (the largest c with u_begin(c) <= u)
+  __host__ __device__ int pair_of(int64_t u) const {
+    return static_cast<int>(((u + 1) * pairs - 1) / units);
+  }
+  // partial contributors (non-owners) of split tile t, and the slot of pair c
+  __host__ __device__ int partials(int t) const {
+    return pair_of(static_cast<int64_t>(t) * nkb + nkb - 1) - pair_of(static_cast<int64_t>(t) * nkb);
+  }
+  __host__ __device__ int slot_of(int t, int c) const { return c - pair_of(static_cast<int64_t>(t) * nkb); }
+};
+// A pair's items: its stream-K segments in DESCENDING tile order (the prefix of its last tile,
+// which it only contributes to, comes first; the suffix of its first tile, which it owns and
+// whose partials the neighbouring pairs publish as THEIR first items, comes last -- so no owner
+// waits on a pair that is itself waiting), then its data-parallel tiles.
+template <bool SKT>
+struct SkIter {
+  int64_t u0 = 0, u1 = 0;
+  int tcur = 0, tlo = 0;
+  int dp;
+  __host__ __device__ SkIter(const SkSched& s, int c) : dp(SKT ? s.sk + c : c) {
+    if (SKT && s.units) {
+      u0 = s.u_begin(c);
+      u1 = s.u_begin(c + 1);
+      tlo = static_cast<int>(u0 / s.nkb);
+      tcur = u1 > u0 ? static_cast<int>((u1 - 1) / s.nkb) : tlo - 1;
+    } else {
+      tcur = -1;
+    }
+  }
+  // next work item: tile t, issue-index range [i0, i1); false when done
+  __host__ __device__ bool next(const SkSched& s, int& t, int& i0, int& i1) {
+    if (SKT && tcur >= tlo) {
+      t = tcur--;
+      const int64_t b = static_cast<int64_t>(t) * s.nkb;
+      i0 = static_cast<int>((u0 > b ? u0 : b) - b);
+      i1 = static_cast<int>((u1 < b + s.nkb ? u1 : b + s.nkb) - b);
+      return true;
+    }
+    if (dp < s.tiles) {
+      t = dp;
+      i0 = 0;
+      i1 = s.nkb;
+      dp += s.pairs;
+      return true;
+    }
+    return false;
+  }
 };
 
 // ---- packed fp32x2 helpers (sm_100a FFMA2 / FMUL2: one instruction per element pair,
@@ -192,7 +257,7 @@ __device__ __forceinline__ void epi_math(uint32_t (&rn)[CW], const uint32_t (&ro
   }
 }
 
-template <int BN, int CG, int KS>
+template <int BN, int CG, int KS, bool SKT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     dual_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
@@ -280,12 +345,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     const int rot = kblock_rotation(static_cast<int>(p.k_o / 32), num_kb);  // = the MMA issuer's
-    for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
+    const SkSched sks(p.num_tiles, num_ctas, p.sk_tiles, num_kb);
+    SkIter<SKT> it(sks, cta_id);
+    int t, i0, i1;
+    while (it.next(sks, t, i0, i1)) {
       const int m_blk = t % p.num_m_blks;
       const int n_blk = t / p.num_m_blks;
       const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
       const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
-      for (int i = 0; i < num_kb; ++i) {
+      for (int i = i0; i < i1; ++i) {
         const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
         ctl_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
@@ -343,21 +411,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
+      const SkSched sks(p.num_tiles, num_ctas, p.sk_tiles, num_kb);
+      SkIter<SKT> it(sks, cta_id);
+      int t, i0, i1, item = 0;
+      while (it.next(sks, t, i0, i1)) {
+        // the first acc_n step this item issues (accumulate = 0) and its k-block
+        int seg_first_n = first_n, kb_seg_first_n = kb_first_n;
+        if (SKT && i0 > 0) {
+          seg_first_n = -1;
+          for (int i = i0; i < i1 && seg_first_n < 0; ++i) {
+            const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
+            const int s0 = kb * SPB > ko32 ? kb * SPB : ko32;
+            if (s0 < (kb + 1) * SPB && s0 < k32) {
+              seg_first_n = s0;
+              kb_seg_first_n = kb;
+            }
+          }
+        }
         const long long tr0 = clock64();
         if (C::kAccStages == 2) ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         const long long tr1 = clock64();
         ptx::tc_fence_after();
         const uint32_t d_o = tmem_base + static_cast<uint32_t>(acc * 2 * BN);
         const uint32_t d_n = d_o + BN;
-        for (int i = 0; i < num_kb; ++i) {
+        for (int i = i0; i < i1; ++i) {
           const int kb = (i + rot) < num_kb ? i + rot : i + rot - num_kb;
           // acc_o is needed only by the outlier steps: in the (last-issued) outlier block the
           // normal steps go first and the wait for the epilogue's acc_o release sits right
           // before the first outlier step
           const bool wait_o = C::kAccStages == 1 && ko32 > 0 && kb == 0;
           if (C::kAccStages == 1) {
-            if (kb == kb_first_n) ctl_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
+            if (kb == kb_seg_first_n) ctl_wait(&tempty[0], acc_phase ^ 1);   // acc_n free
             ptx::tc_fence_after();
           }
           ctl_wait(&full[stage], phase);
@@ -372,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool outl = s32 < ko32;
                 if (s32 < k32 && outl == outlier_pass) {
                   const uint32_t d = outl ? d_o : d_n;
-                  const uint32_t accumulate = (outl ? s32 == 0 : s32 == first_n) ? 0u : 1u;
+                  const uint32_t accumulate = (outl ? s32 == 0 : s32 == seg_first_n) ? 0u : 1u;
                   // sub-tile j/4; +32 bytes along K inside the 128B swizzle row = +2 in the
                   // >>4 address field
                   const uint64_t ao = static_cast<uint64_t>((j >> 2) * (C::kASub >> 4) + 2 * (j & 3));
@@ -387,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool plain = kb * SPB >= ko32 && (kb + 1) * SPB <= k32;
           if (plain) {
             if (p.debug != 1 && ptx::elect_one()) {
-              const uint32_t acc0 = kb * SPB == first_n ? 0u : 1u;
+              const uint32_t acc0 = kb * SPB == seg_first_n ? 0u : 1u;
 #pragma unroll
               for (int j = 0; j < SPB; ++j) {
                 constexpr uint64_t kA = C::kASub >> 4, kB = C::kBSub >> 4;
@@ -420,12 +504,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           if (CG == 1) ptx::mma_commit(&tfull[acc]);
           else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
-          const int ti = (t - cta_id) / num_ctas;
-          if (p.trace && blockIdx.x == 0 && ti < 32) {
+          const int ti = item;
+          if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && ti < 32) {
             s_trace[0][ti] = tr0;
             s_trace[1][ti] = clock64();
           }
         }
+        ++item;
         __syncwarp();
         if (++acc == C::kAccStages) {
           acc = 0;
@@ -550,10 +635,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
-    prefetch(cta_id);
+    const SkSched sks(p.num_tiles, num_ctas, p.sk_tiles, num_kb);
+    SkIter<SKT> it(sks, cta_id);
+    int t, i0, i1, item = 0;
+    int nt = -1, ni0 = 0, ni1 = 0;  // the item after this one (scale prefetch)
+    bool have = it.next(sks, t, i0, i1);
+    if (have) prefetch(t);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cta_id; t < p.num_tiles; t += num_ctas) {
+    for (; have; have = nt >= 0 ? (t = nt, i0 = ni0, i1 = ni1, true) : false, ++item) {
+      nt = it.next(sks, nt, ni0, ni1) ? nt : -1;
       const int m_blk = t % p.num_m_blks;
       const int n_blk = t / p.num_m_blks;
 #pragma unroll
@@ -563,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         wsc[2 * WC + lane + 32 * u] = pf_b[u];
       }
       const float sx = pf_x;
-      prefetch(t + num_ctas);
+      prefetch(nt >= 0 ? nt : p.num_tiles);
       const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM + q * 32;
       const int64_t row = row0 + lane;
       const bool row_ok = row < p.m;
@@ -590,9 +681,65 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < NCH; ++i) ptx::tmem_ld16(t_n + (half + i * kSubs) * CW, an[i]);
         ptx::tmem_wait_ld();
         release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
-        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
-          const int ti = (t - cta_id) / num_ctas;
+        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4) {
+          const int ti = item;
           if (ti < 32) s_trace[5][ti] = clock64();
+        }
+        // stream-K: slot layout [tile][slot][BN columns][TM rows] (a warp's 32 rows of one
+        // column are 128 contiguous bytes)
+        const int trow = static_cast<int>(rank) * BM + q * 32 + lane;
+        bool sk_partial = false;
+        if (SKT && t < p.sk_tiles) {
+          uint32_t* cnt = p.sk_count + 2 * t;
+          if (i1 < num_kb) {
+            // not the owner: publish this pair's partial acc_n and signal the owner
+            int32_t* slot = p.sk_slots + (static_cast<int64_t>(t) * p.sk_slots_per_tile + sks.slot_of(t, cta_id)) *
+                                             (static_cast<int64_t>(BN) * TM);
+#pragma unroll
+            for (int i = 0; i < NCH; ++i)
+#pragma unroll
+              for (int e = 0; e < CW; ++e)
+                slot[static_cast<int64_t>((half + i * kSubs) * CW + e) * TM + trow] =
+                    static_cast<int32_t>(an[i][e]);
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence();  // cumulative over the warp's stores ordered by the barrier
+              atomicAdd(cnt, 1u);
+            }
+            release(&tofree[0]);
+            sk_partial = true;
+          } else if (sks.partials(t) > 0) {
+            // owner: wait for every partial (one arrival per writer warp), add them (int32,
+            // exact), and the last reader warp resets the counters for the next launch
+            const uint32_t want = static_cast<uint32_t>(sks.partials(t) * kEpiWarps * CG);
+            if (lane == 0) {
+              uint32_t got;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(cnt) : "memory");
+              while (got < want) {
+                __nanosleep(256);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(cnt) : "memory");
+              }
+            }
+            __syncwarp();
+            __threadfence();
+            const int32_t* slot0 = p.sk_slots + static_cast<int64_t>(t) * p.sk_slots_per_tile *
+                                                    (static_cast<int64_t>(BN) * TM);
+            for (int sl = 0; sl < sks.partials(t); ++sl) {
+              const int32_t* slot = slot0 + static_cast<int64_t>(sl) * BN * TM;
+#pragma unroll
+              for (int i = 0; i < NCH; ++i)
+#pragma unroll
+                for (int e = 0; e < CW; ++e)
+                  an[i][e] = static_cast<uint32_t>(
+                      static_cast<int32_t>(an[i][e]) +
+                      __ldcg(slot + static_cast<int64_t>((half + i * kSubs) * CW + e) * TM + trow));
+            }
+            __syncwarp();
+            if (lane == 0 && atomicAdd(cnt + 1, 1u) == static_cast<uint32_t>(kEpiWarps * CG) - 1u) {
+              cnt[0] = 0u;
+              cnt[1] = 0u;
+            }
+          }
         }
         using T_ = std::true_type;
         using F_ = std::false_type;
@@ -637,6 +784,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         };
+        if (sk_partial) {
+        } else {
         if (has_outlier) fold(T_{});
         else fold(F_{});
         release(&tofree[0]);  // acc_o free: the next tile's outlier steps may issue
@@ -682,6 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.bias) tail(T_{}, F_{});
           else tail(F_{}, F_{});
         }
+        }  // owner / data-parallel item
       } else if (fast) {
         // phase 1 (blocks the next tile's normal slab): t = s_wn*acc_n (+ s_wo*acc_o), folded
         // into acc_o's columns as f32 bits; phase 2 (overlaps the next tile's MMAs):
@@ -731,8 +881,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         else phase1(F_{});
         ptx::tmem_wait_st();
         release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
-        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
-          const int ti = (t - cta_id) / num_ctas;
+        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4) {
+          const int ti = item;
           if (ti < 32) s_trace[5][ti] = clock64();
         }
         const uint64_t sx2 = pk2(sx, sx);
@@ -869,8 +1019,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (two_step) {
         ptx::tmem_wait_st();
         release(&tempty[0]);  // acc_n free: the next tile's normal-slab MMAs may start
-        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4) {
-          const int ti = (t - cta_id) / num_ctas;
+        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4) {
+          const int ti = item;
           if (ti < 32) s_trace[5][ti] = clock64();
         }
 #pragma unroll 1
@@ -903,8 +1053,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.row_pmax && row_ok)
         p.row_pmax[row * p.pm_count + n_blk * kSubs + half] = max(tile_mx & 0xffffu, tile_mx >> 16);
       {
-        const int ti = (t - cta_id) / num_ctas;
-        if (p.trace && blockIdx.x == 0 && lane == 0 && warp == 4 && ti < 32) {
+        const int ti = item;
+        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4 && ti < 32) {
           s_trace[2][ti] = te0;
           s_trace[3][ti] = te1;
           s_trace[4][ti] = clock64();
@@ -922,14 +1072,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && threadIdx.x == 0) {
     unsigned long long g1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     const long long c1 = clock64();
     printf("effective SM clock over the kernel: %.0f MHz\n",
            1e3 * static_cast<double>(c1 - s_clk0) / static_cast<double>(g1 - s_g0));
-    const int nt = (p.num_tiles - cta_id + num_ctas - 1) / num_ctas;
+    const int nt = SKT ? 3 : (p.num_tiles - cta_id + num_ctas - 1) / num_ctas;
     const long long t0 = s_trace[0][0];
+    printf("CTA %d (kernel start -> first MMA %lld clk, end %lld clk)\n", static_cast<int>(blockIdx.x),
+           t0 - s_clk0, c1 - t0);
     for (int i = 0; i < nt && i < 32; ++i)
       printf("tile %2d: mma %7lld..%7lld  epi wait %7lld tfull %7lld phase1 %7lld done %7lld\n", i,
              s_trace[0][i] - t0, s_trace[1][i] - t0, s_trace[2][i] - t0, s_trace[3][i] - t0,
@@ -1011,7 +1163,9 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS>, static_cast<int>(C::kSmemBytes));
+    attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, false>, static_cast<int>(C::kSmemBytes));
+    if (attr_err == cudaSuccess && BN == 256 && CG == 2 && KS == 2)
+      attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, true>, static_cast<int>(C::kSmemBytes));
   });
   QARVD_CUDA_TRY(attr_err);
   CUtensorMap ta, tb;
@@ -1035,14 +1189,21 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
     st = make_y_tmap(&ty, p.y, p.m, p.n, p.ldy);
     if (st) return st;
   }
+  if (!p.use_tma_store || !p.epi_regs || p.debug) p.sk_tiles = 0;  // stream-K needs the fast path
   p.num_m_blks = static_cast<int>((p.m + BM * CG - 1) / (BM * CG));
   p.num_n_blks = static_cast<int>((p.n + BN - 1) / BN);
   p.pm_count = p.num_n_blks * (kEpiWarps / 4);
   p.num_tiles = p.num_m_blks * p.num_n_blks;
   const int units = sm_count() / CG;
   const int grid = CG * (p.num_tiles < units ? p.num_tiles : units);
-  QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS>, dim3(grid), dim3(kThreads), C::kSmemBytes,
-                            stream, CG, ta, tb, ty, p));
+  // stream-K instance only for the deployed tile shape (the data-parallel instance keeps the
+  // register budget of its epilogue)
+  if (BN == 256 && CG == 2 && KS == 2 && p.sk_tiles > 0)
+    QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS, (BN == 256 && CG == 2 && KS == 2)>, dim3(grid),
+                              dim3(kThreads), C::kSmemBytes, stream, CG, ta, tb, ty, p));
+  else
+    QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS, false>, dim3(grid), dim3(kThreads), C::kSmemBytes,
+                              stream, CG, ta, tb, ty, p));
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;
@@ -1079,7 +1240,48 @@ TileCfg choose_cfg(int64_t m, int64_t n, int64_t k) {
   return c;
 }
 
+// Stream-K workspace of one call (QARVD_GEMM_SK=1), or bytes = 0 when the call runs
+// data-parallel: only the
+// deployed configuration (256 x 256 pair tiles, 256-byte stages, bf16 TMA-store epilogue
+// holding acc_n in registers, N a multiple of 256, the outlier slab inside one k-block) with
+// a partial last wave and long K ranges (>= 8 k-blocks per pair) splits tiles.
+struct SkLayout {
+  int sk_tiles = 0, slots_per_tile = 0;
+  int64_t count_bytes = 0, bytes = 0;
+};
+SkLayout sk_layout(int64_t m, int64_t n, int64_t k, int64_t k_o, int out_dtype, bool dumps) {
+  SkLayout L;
+  const TileCfg c = choose_cfg(m, n, k);
+  // opt-in (QARVD_GEMM_SK=1): measured on the FFN-down shape it does not pay yet -- the
+  // non-owners' partial stores take 10-30K cycles under the GEMM's load traffic and the owners'
+  // fixups wait on them (K2)
+  const char* sk_env = getenv("QARVD_GEMM_SK");
+  const bool off = !(sk_env && sk_env[0] == '1');
+  const char* er = std::getenv("QARVD_GEMM_EPIREG");
+  if (off || (er && er[0] == '0') || c.bn != 256 || c.cg != 2 || c.ks != 2 ||
+      out_dtype != QARVD_BF16 || dumps || n % 256 != 0 || k_o >= 256 || m <= 0)
+    return L;
+  const int pairs = sm_count() / 2;
+  const int tiles = static_cast<int>((m + 255) / 256) * static_cast<int>(n / 256);
+  const int nkb = static_cast<int>((k + 255) / 256);
+  const int rem = tiles % pairs;
+  if (rem == 0 || tiles < pairs) return L;
+  const SkSched s(tiles, pairs, rem, nkb);
+  if (s.units < 8LL * pairs) return L;
+  int mx = 0;
+  for (int t = 0; t < rem; ++t) mx = s.partials(t) > mx ? s.partials(t) : mx;
+  L.sk_tiles = rem;
+  L.slots_per_tile = mx > 0 ? mx : 1;
+  L.count_bytes = (static_cast<int64_t>(rem) * 2 * 4 + 255) / 256 * 256;
+  L.bytes = L.count_bytes + static_cast<int64_t>(rem) * L.slots_per_tile * 256 * 256 * 4;
+  return L;
+}
+
 }  // namespace
+
+int64_t dual_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int64_t k_o) {
+  return sk_layout(m, n, k, k_o, QARVD_BF16, false).bytes;
+}
 
 int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
                      int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
@@ -1087,7 +1289,8 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
                      int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
                      int32_t* acc_n, cudaStream_t stream, const double* sx64 = nullptr,
                      const double* so64 = nullptr, const double* sn64 = nullptr,
-                     uint32_t* row_absmax = nullptr, uint32_t* row_pmax = nullptr) {
+                     uint32_t* row_absmax = nullptr, uint32_t* row_pmax = nullptr,
+                     void* sk_workspace = nullptr, int64_t sk_workspace_bytes = 0) {
   GemmParams p{};
   p.row_absmax = row_absmax;
   p.row_pmax = row_pmax;
@@ -1107,10 +1310,19 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.acc_o_dbg = acc_o;
   p.acc_n_dbg = acc_n;
   p.debug = getenv("QARVD_GEMM_DEBUG") ? atoi(getenv("QARVD_GEMM_DEBUG")) : 0;
-  p.trace = getenv("QARVD_GEMM_TRACE") ? 1 : 0;
+  p.trace = getenv("QARVD_GEMM_TRACE") ? 1 + (getenv("QARVD_GEMM_TRACE_CTA") ? atoi(getenv("QARVD_GEMM_TRACE_CTA")) : 0) : 0;
   p.epilogue = epilogue;
   p.out_dtype = out_dtype;
   const TileCfg c = choose_cfg(m, n, k);
+  if (sk_workspace) {
+    const SkLayout L = sk_layout(m, n, k, k_outlier, out_dtype, acc_o || acc_n || row_absmax || row_pmax);
+    if (L.bytes > 0 && sk_workspace_bytes >= L.bytes) {
+      p.sk_tiles = L.sk_tiles;
+      p.sk_slots_per_tile = L.slots_per_tile;
+      p.sk_count = static_cast<uint32_t*>(sk_workspace);
+      p.sk_slots = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(sk_workspace) + L.count_bytes);
+    }
+  }
   if (c.cg == 2) {
     if (c.bn == 256) return c.ks == 2 ? launch_gemm<256, 2, 2>(xq, ldq, wq, ldw, p, stream)
                                       : launch_gemm<256, 2, 1>(xq, ldq, wq, ldw, p, stream);
@@ -1213,6 +1425,40 @@ extern "C" int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* 
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, nullptr, nullptr, nullptr, nullptr,
                           QARVD_EPI_NONE, QARVD_F64, y, ldy, nullptr, nullptr, as_stream(stream),
                           scale_x, scale_w_outlier, scale_w_normal);
+}
+
+extern "C" int64_t qarvd_dual_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int64_t k_outlier) {
+  if (m <= 0 || n <= 0 || k <= 0) return 0;
+  return qarvd_b200::dual_gemm_workspace_size(m, n, k, k_outlier);
+}
+
+extern "C" int qarvd_dual_gemm_ws(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                  int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                  const float* scale_x, const float* scale_w_outlier,
+                                  const float* scale_w_normal, const float* bias, int epilogue,
+                                  uint16_t* y, int64_t ldy, void* workspace, int64_t workspace_bytes,
+                                  void* stream) {
+  if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255)) {
+    clear_error();
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: workspace must be 256-byte aligned");
+  }
+  clear_error();
+  if (m <= 0 || n <= 0 || k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
+  if (k % 32 != 0 || k_outlier % 32 != 0 || k_outlier < 0 || k_outlier >= k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "kernel_b: k and k_outlier must be multiples of 32 with 0 <= k_outlier < k");
+  if (k > 132104)
+    QARVD_FAIL(QARVD_ERR_LOGIC, "kernel_b: reduction dimension too large for exact int32 accumulation");
+  if (ldq < k || ldw < k || ldq % 16 || ldw % 16 || ldy < n)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: leading dimensions must be >= k (n for y) and multiples of 16");
+  if ((reinterpret_cast<uintptr_t>(xq) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: operand pointers must be 16-byte aligned");
+  if (!xq || !wq || !scale_x || !scale_w_normal || !y || (k_outlier > 0 && !scale_w_outlier))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
+  if (int st = require_device()) return st;
+  return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier, scale_w_normal,
+                          bias, epilogue, QARVD_BF16, y, ldy, nullptr, nullptr, as_stream(stream), nullptr,
+                          nullptr, nullptr, nullptr, nullptr, workspace, workspace_bytes);
 }
 
 extern "C" int64_t qarvd_dual_gemm_pmax_count(int64_t m, int64_t n, int64_t k) {

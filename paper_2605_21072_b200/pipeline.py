@@ -114,6 +114,11 @@ class QuantizedChain:
         self.xq = [torch.empty((mi, L.k_pad), dtype=torch.int8, device=dev) for mi, L in zip(self.ms, self.layers)]
         self.sx = [torch.empty(mi, dtype=torch.float32, device=dev) for mi in self.ms]
         self.y = [torch.empty((mi, L.out_dim), dtype=torch.bfloat16, device=dev) for mi, L in zip(self.ms, self.layers)]
+        # stream-K workspaces (zero-filled; one per layer so concurrent branches never share)
+        self.sk_ws = []
+        for mi, L in zip(self.ms, self.layers):
+            nb = int(_lib.load().qarvd_dual_gemm_workspace_size(mi, L.out_dim, L.k_pad, L.k_outlier))
+            self.sk_ws.append(torch.zeros(nb, dtype=torch.uint8, device=dev) if nb > 0 else None)
         self.graph = None
 
     def _src(self, i):
@@ -190,6 +195,12 @@ class QuantizedChain:
                       L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
                       self.epilogues[i], self.y[i].data_ptr(), L.out_dim, self.rowmax[i].data_ptr(),
                       self.rowmax[i].shape[1], s)
+        elif self.sk_ws[i] is not None:
+            ws = self.sk_ws[i]
+            _lib.call("qarvd_dual_gemm_ws", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
+                      m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                      self.epilogues[i], self.y[i].data_ptr(), L.out_dim, ws.data_ptr(), ws.numel(), s)
         else:
             _lib.call("qarvd_dual_gemm", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
                       m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),

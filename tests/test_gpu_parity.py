@@ -710,3 +710,34 @@ def test_weighted_loss_wan_shape_sample_independence(cuda):
     for f in (0, 7, 20):
         _, e1 = calibrate.weighted_loss([batch[f]], layer, w, cw, amax / 127.0, return_errors=True)
         assert e1[0] == err[f]
+
+
+@pytest.mark.parametrize("m,n,k,n_out", [(4680, 1536, 8960, 188), (3000, 1792, 16384, 60), (4680, 1536, 8960, 0)])
+def test_k2_stream_k_bitexact(cuda, m, n, k, n_out, monkeypatch):
+    """Stream-K K2 (qarvd_dual_gemm_ws: remainder tiles split along K over all SM pairs, int32
+    partials through the workspace) is bit-identical to the data-parallel kernel, on repeated
+    launches (self-resetting counters) and after another shape reused the workspace."""
+    monkeypatch.setenv("QARVD_GEMM_SK", "1")  # stream-K is opt-in
+    lib = qb._lib.load()
+    plan = make_plan(k, n_out, seed=3)
+    wb, _ = bf16_values((n, k), seed=4, scale=1.0 / np.sqrt(k), heavy_cols=plan.outlier_indices if n_out else None)
+    L = engine.prepare_weights("sk", to_dev_bf16(wb), plan)
+    xb, _ = bf16_values((m, k), seed=5, heavy_cols=plan.outlier_indices if n_out else None, gamma=4.0)
+    xq, s32, _ = engine.kernel_a_quantize_activation(to_dev_bf16(xb), L)
+    nb = int(lib.qarvd_dual_gemm_workspace_size(m, n, L.k_pad, L.k_outlier))
+    assert nb > 0  # these shapes have a partial last wave and long K
+    ws = torch.zeros(nb + 256, dtype=torch.uint8, device="cuda")
+    y_dp = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    y_sk = torch.empty_like(y_dp)
+    qb._lib.call("qarvd_dual_gemm", xq.data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad, m, n, L.k_pad,
+                 L.k_outlier, s32.data_ptr(), L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(),
+                 None, qb.EPI_GELU, qb.BF16, y_dp.data_ptr(), n, None, None, None)
+    for rep in range(3):
+        y_sk.zero_()
+        qb._lib.call("qarvd_dual_gemm_ws", xq.data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad, m, n, L.k_pad,
+                     L.k_outlier, s32.data_ptr(), L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(),
+                     None, qb.EPI_GELU, y_sk.data_ptr(), n, ws.data_ptr(), ws.numel(), None)
+        torch.cuda.synchronize()
+        assert torch.equal(y_dp.view(torch.int16), y_sk.view(torch.int16)), rep
+    # counters are back to zero after every launch
+    assert int(ws[:256].view(torch.int32).abs().sum()) == 0
