@@ -325,6 +325,37 @@ int qarvd_weighted_loss(const uint16_t* x, int64_t ldx, const uint16_t* w, int64
                         const double* chunk_weights, int64_t n_chunks, double* sample_err,
                         double* loss, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---- K7: AdaRound layer calibration (f64, the reference's calibrator) ------
+ * Replaces  calibrate_layer(w, plan, act_init, samples, chunk_weights, cfg)  calibrate.hpp:112-116
+ *           (calibrate.cpp:298-396, LearnableQuantState calibrate.cpp:77-199,
+ *           soft_loss_gradients calibrate.cpp:232-296).
+ * All tensors are f64 device arrays: w [n x k]; outlier_mask u8 [k] (1 = outlier column of the
+ * plan); the plan's initial group scales [n] (scale_outlier_init ignored when !plan_enabled);
+ * x = the samples stacked [rows x k], sample s = rows sample_rows[s] .. sample_rows[s+1]
+ * (HOST int64 [S+1]); sample_chunk HOST int64 [S] (1-based); chunk_weights HOST f64.
+ * layer_name seeds the batch sampler exactly as the reference (mix_seed(seed, fnv1a(name))).
+ * Outputs (device): codes int8 [n x k] original column order (hard_codes), learned scales [n],
+ * scalars_out f64 [3] = {act scale, initial hard loss, final hard loss}, trace_out f64
+ * [iterations] running-min batch loss (may be NULL).  Divergence -> QARVD_ERR_RUNTIME with the
+ * reference message; invalid configs -> the reference's CalibConfig::validate messages.
+ */
+typedef struct qarvd_calib_config {
+  int iterations, batch_size;
+  double lr_round, lr_scale;
+  uint64_t seed;
+  int train_activation_scale;
+  double zeta, gamma_lo, reg_lambda, beta_start, beta_end, warmup_frac;
+} qarvd_calib_config;
+int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, const uint8_t* outlier_mask,
+                          int plan_enabled, const double* scale_normal_init,
+                          const double* scale_outlier_init, double act_scale_init, int act_bits,
+                          int w_bits, const double* x, const int64_t* sample_rows,
+                          const int64_t* sample_chunk, int64_t n_samples,
+                          const double* chunk_weights, int64_t n_chunks,
+                          const qarvd_calib_config* cfg, const char* layer_name, int8_t* codes,
+                          double* scale_normal_out, double* scale_outlier_out, double* scalars_out,
+                          double* trace_out, void* stream);
+
 /* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
  * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)
  * weights with a seeded set of input columns scaled by gamma.  Values are

@@ -91,6 +91,10 @@ def ref():
         _r.ref_percentile_search.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p,
                                              c_void_p, c_void_p]
         _r.ref_weighting.argtypes = [c_int, c_void_p, c_int64, c_void_p]
+        _r.ref_calibrate_layer.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
+                                           c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                                           c_int, c_int, ctypes.c_uint64, ctypes.c_char_p, c_void_p,
+                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
         _r.ref_weighted_loss.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
                                          c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
@@ -387,3 +391,24 @@ def ref_weighted_loss(w64, outliers, act_scale, x64, row_off, chunks, chunk_w):
                                 _p(ch), len(ch), _p(cw), len(cw), ctypes.byref(loss), _p(codes),
                                 _p(so), _p(sn), ctypes.byref(act), _p(mask)))
     return dict(loss=loss.value, codes=codes, s_wo=so, s_wn=sn, act_scale=act.value, mask=mask)
+
+
+def ref_calibrate_layer(w64, outliers, act_scale, x64, row_off, chunks, chunk_w, iterations, batch_size,
+                        seed, name):
+    """The reference calibrate_layer (calibrate.cpp:298-396) on build_plan(W, outliers)."""
+    w64 = np.ascontiguousarray(w64, dtype=np.float64)
+    n, k = w64.shape
+    x64 = np.ascontiguousarray(x64, dtype=np.float64)
+    o = np.ascontiguousarray(outliers, dtype=np.int64)
+    ro = np.ascontiguousarray(row_off, dtype=np.int64)
+    ch = np.ascontiguousarray(chunks, dtype=np.int64)
+    cw = np.ascontiguousarray(chunk_w, dtype=np.float64)
+    codes = np.empty((n, k), dtype=np.int32)
+    sn, so, isn, iso = np.empty(n), np.empty(n), np.empty(n), np.empty(n)
+    sc = np.empty(3)
+    tr = np.empty(max(1, iterations))
+    _rc(ref().ref_calibrate_layer(_p(w64), n, k, _p(o), len(o), float(act_scale), _p(x64), _p(ro), _p(ch),
+                                  len(ch), _p(cw), len(cw), iterations, batch_size, seed, name.encode(),
+                                  _p(codes), _p(sn), _p(so), _p(sc), _p(tr), _p(isn), _p(iso)))
+    return dict(codes=codes, scale_normal=sn, scale_outlier=so, act_scale=sc[0], initial_loss=sc[1],
+                final_loss=sc[2], trace=tr[:iterations], init_scale_normal=isn, init_scale_outlier=iso)

@@ -331,3 +331,51 @@ extern "C" int ref_weighted_loss(const double* w, int64_t n, int64_t k, const in
       for (size_t c : plan.outlier_indices) outlier_mask[c] = 1;
   });
 }
+
+// calibrate_layer (calibrate.cpp:298-396) with build_plan(W, aligned outliers) and a per-tensor
+// act_init; default CalibConfig except iterations / batch size / seed.  Exports the learned
+// scales, hard codes, act scale, losses and the trace.
+extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const int64_t* outliers,
+                                   int64_t n_out, double act_scale, const double* x,
+                                   const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
+                                   const double* chunk_w, int64_t n_chunks, int iterations,
+                                   int batch_size, uint64_t seed, const char* name, int32_t* codes,
+                                   double* s_n, double* s_o, double* scalars, double* trace,
+                                   double* init_s_n, double* init_s_o) {
+  return guarded([&] {
+    const Tensor W = make_tensor(w, n, k);
+    OutlierReport rep;
+    rep.layer_name = name;
+    rep.aligned_outliers.assign(outliers, outliers + n_out);
+    DualScalePlan plan = build_plan(W, rep, 8);
+    plan.layer_name = name;
+    for (int64_t r = 0; r < n; ++r) {
+      init_s_n[r] = plan.params_normal.scale[r];
+      init_s_o[r] = plan.params_outlier.scale[r];
+    }
+    CalibConfig cfg;
+    cfg.iterations = iterations;
+    cfg.batch_size = batch_size;
+    cfg.seed = seed;
+    std::vector<CalibSample> samples(static_cast<size_t>(n_samples));
+    std::vector<const CalibSample*> ptrs;
+    for (int64_t s = 0; s < n_samples; ++s) {
+      samples[s].layer = name;
+      samples[s].chunk = static_cast<size_t>(chunk[s]);
+      samples[s].x = make_tensor(x + row_off[s] * k, row_off[s + 1] - row_off[s], k);
+      ptrs.push_back(&samples[s]);
+    }
+    const std::vector<double> cw(chunk_w, chunk_w + n_chunks);
+    const LayerCalibResult r = calibrate_layer(W, plan, QuantParams::per_tensor_symmetric(8, act_scale),
+                                               ptrs, cw, cfg);
+    std::memcpy(codes, r.codes.data.data(), sizeof(int32_t) * n * k);
+    for (int64_t i = 0; i < n; ++i) {
+      s_n[i] = r.plan.params_normal.scale[i];
+      s_o[i] = r.plan.params_outlier.scale[i];
+    }
+    scalars[0] = r.act.scale[0];
+    scalars[1] = r.initial_loss;
+    scalars[2] = r.final_loss;
+    for (size_t t = 0; t < r.trace.size(); ++t) trace[t] = r.trace[t];
+  });
+}

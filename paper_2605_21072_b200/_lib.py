@@ -88,6 +88,31 @@ class SearchJob(ctypes.Structure):
     ]
 
 
+class CalibConfig(ctypes.Structure):
+    """qarvd_calib_config = CalibConfig (calibrate.hpp:16-33); defaults are the reference's."""
+    _fields_ = [
+        ("iterations", c_int),
+        ("batch_size", c_int),
+        ("lr_round", c_double),
+        ("lr_scale", c_double),
+        ("seed", c_uint64),
+        ("train_activation_scale", c_int),
+        ("zeta", c_double),
+        ("gamma_lo", c_double),
+        ("reg_lambda", c_double),
+        ("beta_start", c_double),
+        ("beta_end", c_double),
+        ("warmup_frac", c_double),
+    ]
+
+    def __init__(self, **kw):
+        d = dict(iterations=200, batch_size=4, lr_round=2e-3, lr_scale=4e-5, seed=0,
+                 train_activation_scale=1, zeta=1.1, gamma_lo=-0.1, reg_lambda=1e-2,
+                 beta_start=10.0, beta_end=2.0, warmup_frac=0.2)
+        d.update(kw)
+        super().__init__(**d)
+
+
 class WeightJob(ctypes.Structure):
     _fields_ = [
         ("w", c_void_p),
@@ -173,6 +198,10 @@ SIGNATURES = {
         [POINTER(SearchJob), c_int, POINTER(c_double), c_int, POINTER(c_double), c_int, c_void_p],
     ),
     "qarvd_weighted_loss_workspace": (c_int64, [c_int64, c_int64, c_int64]),
+    "qarvd_calibrate_layer": (
+        c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_double, c_int, c_int,
+                c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_char_p, c_void_p,
+                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "qarvd_dual_gemm_workspace_size": (c_int64, [c_int64, c_int64, c_int64, c_int64]),
     "qarvd_dual_gemm_ws": (
         c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

@@ -17,6 +17,7 @@ threading.hpp:13-14, lifted to GPU count).
 """
 from __future__ import annotations
 
+import ctypes
 import heapq
 from dataclasses import dataclass
 from typing import Callable, Dict, List, Optional, Sequence
@@ -370,3 +371,61 @@ def weighted_loss(batch: Sequence, layer, w: torch.Tensor, chunk_weights: Sequen
     if return_errors:
         return float(loss.item()), err.cpu().numpy()
     return float(loss.item())
+
+
+@dataclass
+class LayerCalibResult:
+    """LayerCalibResult (calibrate.hpp:102-110): learned plan scales, hard codes (original
+    column order), the learned per-tensor activation scale, losses and the running-min trace."""
+
+    layer: str
+    scale_normal: np.ndarray
+    scale_outlier: np.ndarray
+    codes: np.ndarray
+    act_scale: float
+    initial_loss: float
+    final_loss: float
+    trace: np.ndarray
+
+
+def calibrate_layer(name: str, w: torch.Tensor, plan, scale_normal: torch.Tensor,
+                    scale_outlier: torch.Tensor, act_scale: float, samples: Sequence,
+                    chunk_weights: Sequence[float], cfg: Optional["_lib.CalibConfig"] = None,
+                    act_bits: int = 8, w_bits: int = 8) -> LayerCalibResult:
+    """calibrate_layer (calibrate.cpp:298-396) on the GPU (K7, f64): AdaRound rounding variables,
+    learned group and activation scales, frame-weighted Eq. 5 objective, Adam + cosine LR.
+
+    ``w``: the layer's FP weight [n x k] (any float dtype; computed in f64). ``plan``: an
+    engine.DualScalePlan; ``scale_normal`` / ``scale_outlier``: its initial per-row group scales
+    (e.g. prepare_weights' scale_*64, bit-identical to build_plan). ``samples``: (x [rows x k],
+    chunk) pairs (CalibSample, calibrate.hpp:37-41)."""
+    cfg = cfg if cfg is not None else _lib.CalibConfig()
+    if len(samples) == 0:
+        raise _lib.InvalidArgument("calibrate_layer: no calibration samples")
+    dev = w.device
+    w64 = w.to(torch.float64).contiguous()
+    n, k = w64.shape
+    x64 = torch.cat([x.to(torch.float64) for x, _ in samples], 0).contiguous()
+    rows = np.zeros(len(samples) + 1, dtype=np.int64)
+    rows[1:] = np.cumsum([x.shape[0] for x, _ in samples])
+    chunks = np.asarray([int(c) for _, c in samples], dtype=np.int64)
+    cw = np.ascontiguousarray(chunk_weights, dtype=np.float64)
+    mask = np.zeros(k, dtype=np.uint8)
+    if plan.enabled:
+        mask[np.asarray(plan.outlier_indices, dtype=np.int64)] = 1
+    mask_d = torch.from_numpy(mask).to(dev)
+    sn = scale_normal.to(torch.float64).contiguous()
+    so = scale_outlier.to(torch.float64).contiguous()
+    codes = torch.empty((n, k), dtype=torch.int8, device=dev)
+    sn_out = torch.empty(n, dtype=torch.float64, device=dev)
+    so_out = torch.empty(n, dtype=torch.float64, device=dev)
+    scal = torch.empty(3, dtype=torch.float64, device=dev)
+    trace = torch.empty(max(1, cfg.iterations), dtype=torch.float64, device=dev)
+    _lib.call("qarvd_calibrate_layer", w64.data_ptr(), n, k, mask_d.data_ptr(), int(plan.enabled),
+              sn.data_ptr(), so.data_ptr(), float(act_scale), act_bits, w_bits, x64.data_ptr(),
+              rows.ctypes.data, chunks.ctypes.data, len(samples), cw.ctypes.data, len(cw),
+              ctypes.byref(cfg), name.encode(), codes.data_ptr(), sn_out.data_ptr(), so_out.data_ptr(),
+              scal.data_ptr(), trace.data_ptr(), _stream())
+    sc = scal.cpu().numpy()
+    return LayerCalibResult(name, sn_out.cpu().numpy(), so_out.cpu().numpy(), codes.cpu().numpy(),
+                            float(sc[0]), float(sc[1]), float(sc[2]), trace.cpu().numpy()[:cfg.iterations])

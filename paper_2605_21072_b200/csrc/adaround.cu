@@ -1,0 +1,488 @@
+// K7 — AdaRound calibration of one layer on the GPU (f64), the reference's calibrator.
+//
+// Replaces calibrate_layer (/root/reference/proj/core/src/calibrate.cpp:298-396) with its
+// state LearnableQuantState (calibrate.cpp:77-199) and gradients soft_loss_gradients
+// (calibrate.cpp:232-296): learned rounding variables V with the rectified sigmoid
+// h(V) = clip(sigmoid(V)(zeta - gamma) + gamma, 0, 1), learned per-row log group scales and
+// a learned log activation scale, trained with the frame-weighted Eq. 5 objective
+// (1/B) sum_s w[chunk_s] ||X_s W^T - FQ(X_s) What^T||^2, the corner-pushing regulariser
+// after warm-up, and bias-corrected Adam with a cosine-annealed learning rate.
+//
+// Everything stays in f64 like the reference, so the trajectory follows it to rounding:
+// the three products per sample (prediction X^ What^T - target, dL/dWhat = D^T X^,
+// dL/dX^ = D What) are cuBLAS DGEMMs (plain library GEMMs); every elementwise step,
+// reduction and Adam update is a kernel here with the reference's per-element formula, and
+// every reduction runs in a fixed order (deterministic).  The target X_s W^T is computed
+// once per sample (W is fixed during calibration).  The host only replays the reference's
+// batch sampler (Prng(mix_seed(seed, fnv1a(layer)))) and enqueues launches; losses,
+// divergence and results stay on the device until the end.
+#include <cublas_v2.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qarvd_b200 {
+namespace {
+
+// ---- host restatement of rng.hpp (splitmix64, mix_seed, fnv1a) ------------------------
+uint64_t splitmix64_h(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+uint64_t mix_seed_h(uint64_t a, uint64_t b) {
+  uint64_t s = a;
+  const uint64_t h = splitmix64_h(s);
+  s = h ^ (b + 0x9e3779b97f4a7c15ULL);
+  return splitmix64_h(s);
+}
+uint64_t fnv1a_h(const char* d, size_t n) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= static_cast<unsigned char>(d[i]);
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+constexpr int kT = 256;
+inline unsigned blocks_for(int64_t n) {
+  const int64_t b = (n + kT - 1) / kT;
+  return static_cast<unsigned>(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+// weight_scale(r, outlier_group) = exp(log scale) (calibrate.cpp:117-119); log_s = [normal n | outlier n]
+__device__ __forceinline__ double wscale(const double* log_s, int64_t n, int64_t r, bool outl) {
+  return exp(outl ? log_s[n + r] : log_s[r]);
+}
+
+// LearnableQuantState::init V (calibrate.cpp:96-114): h(V) = frac(w/s), clamped to [1e-4, 1-1e-4]
+__global__ void init_v_kernel(const double* w, const uint8_t* mask, int enabled, const double* s_n,
+                              const double* s_o, int64_t n, int64_t k, double zeta, double gamma,
+                              double* v) {
+  const double span = zeta - gamma;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / k, c = i - r * k;
+    const double s = (enabled && mask[c]) ? s_o[r] : s_n[r];
+    const double ratio = w[i] / s;
+    double frac = ratio - floor(ratio);
+    frac = clampd(frac, 1e-4, 1.0 - 1e-4);
+    const double p = (frac - gamma) / span;
+    v[i] = log(p / (1.0 - p));
+  }
+}
+
+// soft weights (calibrate.cpp:245-266): what = s*clip(floor(w/s) + h(V)), the clipped code and
+// dh/dV (0 where the pre-activation or the code clips).  hard = 1: h -> [h > 0.5] (hard_weight,
+// calibrate.cpp:159-161), codes_out = int8 codes (hard_codes, calibrate.cpp:163-183).
+__global__ void weights_kernel(const double* w, const double* v, const uint8_t* mask, int enabled,
+                               const double* log_s, int64_t n, int64_t k, double zeta, double gamma,
+                               int qmin, int qmax, int hard, double* what, double* code,
+                               double* dhdv, int8_t* codes_out) {
+  const double span = zeta - gamma;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / k, c = i - r * k;
+    const bool outl = enabled && mask[c];
+    const double s = wscale(log_s, n, r, outl);
+    const double sig = sigmoid_d(v[i]);
+    const double pre = sig * span + gamma;
+    const double h = clampd(pre, 0.0, 1.0);
+    const double u = floor(w[i] / s) + (hard ? (h > 0.5 ? 1.0 : 0.0) : h);
+    const double cl = clampd(u, static_cast<double>(qmin), static_cast<double>(qmax));
+    what[i] = s * cl;
+    if (code) code[i] = cl;
+    if (dhdv) {
+      const bool inside_code = u > static_cast<double>(qmin) && u < static_cast<double>(qmax);
+      const bool inside_h = pre > 0.0 && pre < 1.0;
+      dhdv[i] = (inside_code && inside_h) ? span * sig * (1.0 - sig) : 0.0;
+    }
+    if (codes_out) codes_out[i] = static_cast<int8_t>(cl);
+  }
+}
+
+// fake_quant(x, act) (quant.cpp:113-159, per-tensor symmetric, s = exp(log_sa)): xhat and the
+// code as f64; a non-finite input sets *bad (the reference throws)
+__global__ void xhat_kernel(const double* x, int64_t count, const double* log_sa, int qmax,
+                            double* xhat, double* xcode, int* bad) {
+  const double s = exp(*log_sa);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double xv = x[i];
+    if (!isfinite(xv)) {
+      *bad = 1;
+      xhat[i] = 0.0;
+      xcode[i] = 0.0;
+      continue;
+    }
+    const double q = clampd(rint(xv / s), -static_cast<double>(qmax), static_cast<double>(qmax));
+    xcode[i] = q;
+    xhat[i] = q * s;
+  }
+}
+
+// fixed-order partial sums of a[i]*b[i] (b = nullptr: a[i]^2): block p sums a contiguous range
+constexpr int kRedBlocks = 296;
+__global__ void __launch_bounds__(kT) dot_partial_kernel(const double* a, const double* b, int64_t count,
+                                                          double* partial) {
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = lo + per < count ? lo + per : count;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kT) {
+    const double av = a[i];
+    acc += b ? av * b[i] : av * av;
+  }
+  __shared__ double red[kT];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+// *acc (+)= scale * sum(partial) in block order; mode 1 multiplies by exp(*log_sa) (act grad)
+__global__ void dot_final_kernel(const double* partial, int np, double scale, const double* log_sa,
+                                 int accumulate, double* acc) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < np; ++i) s += partial[i];
+  double v = scale * s;
+  if (log_sa) v *= exp(*log_sa);
+  *acc = accumulate ? *acc + v : v;
+}
+
+// per-iteration loss bookkeeping: loss = acc / B; best = min(best, loss) -> trace[t];
+// the first non-finite iteration is recorded (the reference throws at it)
+__global__ void trace_kernel(const double* acc, double inv_b, double* best, double* trace, int t,
+                             int* diverged_at) {
+  const double loss = *acc * inv_b;
+  if (!isfinite(loss) && *diverged_at < 0) *diverged_at = t;
+  const double b = *best < loss ? *best : loss;
+  *best = b;
+  trace[t] = b;
+}
+
+// gradients (calibrate.cpp:276-289, :345-362): v_grad = gW*s*dh_dv (+ regulariser), per-row
+// log-scale grads sum_c gW*s*code split by group; one CTA per row, fixed-order reduction
+__global__ void __launch_bounds__(kT) grad_kernel(const double* gw, const double* v, const double* code,
+                                                  const double* dhdv, const uint8_t* mask, int enabled,
+                                                  const double* log_s, int64_t n, int64_t k, int reg_on,
+                                                  double reg_lambda, double beta, double zeta, double gamma,
+                                                  double* vgrad, double* sgrad) {
+  const int64_t r = blockIdx.x;
+  double gn = 0.0, go = 0.0;
+  const double span = zeta - gamma;
+  for (int64_t c = threadIdx.x; c < k; c += kT) {
+    const int64_t i = r * k + c;
+    const bool outl = enabled && mask[c];
+    const double s = wscale(log_s, n, r, outl);
+    const double gwe = gw[i];
+    double g = gwe * s * dhdv[i];
+    if (reg_on) {
+      const double sig = sigmoid_d(v[i]);
+      const double pre = sig * span + gamma;
+      const double h = clampd(pre, 0.0, 1.0);
+      const double centered = 2.0 * h - 1.0;
+      const double mag = fabs(centered);
+      const double dreg_dh = -2.0 * beta * pow(mag > 1e-12 ? mag : 1e-12, beta - 1.0) *
+                             (centered >= 0 ? 1.0 : -1.0);
+      const double dh_dv = (pre > 0.0 && pre < 1.0) ? span * sig * (1.0 - sig) : 0.0;
+      g += reg_lambda * dreg_dh * dh_dv;
+    }
+    vgrad[i] = g;
+    const double gs = gwe * s * code[i];
+    if (outl) go += gs;
+    else gn += gs;
+  }
+  __shared__ double rn[kT], ro[kT];
+  rn[threadIdx.x] = gn;
+  ro[threadIdx.x] = go;
+  __syncthreads();
+  for (int s = kT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      rn[threadIdx.x] += rn[threadIdx.x + s];
+      ro[threadIdx.x] += ro[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sgrad[r] = rn[0];
+    sgrad[n + r] = enabled ? ro[0] : 0.0;  // calibrate.cpp:374
+  }
+}
+
+// AdamBuffer::step (calibrate.cpp:27-40); c1 / c2 = 1 - b^t from the host (std::pow)
+__global__ void adam_kernel(double* p, const double* g, double* m, double* v, int64_t count, double lr,
+                            double c1, double c2) {
+  constexpr double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+    v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+    p[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
+  }
+}
+
+__global__ void log_kernel(const double* a, double* out, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = log(a[i]);
+}
+__global__ void exp_kernel(const double* a, double* out, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = exp(a[i]);
+}
+__global__ void loss_kernel(const double* acc, double inv, double* out) { *out = *acc * inv; }
+__global__ void set_scalars_kernel(double* log_sa, double act_scale, double* best, int* diverged,
+                                   int* bad) {
+  *log_sa = log(act_scale);
+  *best = INFINITY;
+  *diverged = -1;
+  *bad = 0;
+}
+
+const char* cublas_msg(cublasStatus_t s) {
+  switch (s) {
+    case CUBLAS_STATUS_NOT_INITIALIZED: return "not initialized";
+    case CUBLAS_STATUS_ALLOC_FAILED: return "alloc failed";
+    case CUBLAS_STATUS_INVALID_VALUE: return "invalid value";
+    case CUBLAS_STATUS_EXECUTION_FAILED: return "execution failed";
+    default: return "error";
+  }
+}
+#define QARVD_CUBLAS_TRY(expr)                                                           \
+  do {                                                                                   \
+    cublasStatus_t _s = (expr);                                                          \
+    if (_s != CUBLAS_STATUS_SUCCESS)                                                     \
+      QARVD_FAIL(QARVD_ERR_CUDA, std::string("cuBLAS: ") + cublas_msg(_s) + " at " +     \
+                                     __FILE__ + ":" + std::to_string(__LINE__));         \
+  } while (0)
+
+struct DevArena {
+  std::vector<void*> ptrs;
+  cudaStream_t s;
+  explicit DevArena(cudaStream_t st) : s(st) {}
+  ~DevArena() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* get(int64_t count) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, static_cast<size_t>(count > 0 ? count : 1) * sizeof(T), s) != cudaSuccess)
+      return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+}  // namespace qarvd_b200
+
+using namespace qarvd_b200;
+
+extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, const uint8_t* outlier_mask,
+                                     int plan_enabled, const double* scale_normal_init,
+                                     const double* scale_outlier_init, double act_scale_init,
+                                     int act_bits, int w_bits, const double* x,
+                                     const int64_t* sample_rows, const int64_t* sample_chunk,
+                                     int64_t n_samples, const double* chunk_weights, int64_t n_chunks,
+                                     const qarvd_calib_config* cfg, const char* layer_name,
+                                     int8_t* codes, double* scale_normal_out, double* scale_outlier_out,
+                                     double* scalars_out, double* trace_out, void* stream) {
+  clear_error();
+  if (!cfg) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calib config: null");
+  // CalibConfig::validate (calibrate.cpp:45-52)
+  if (cfg->iterations < 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calib config: iterations must be >= 0");
+  if (cfg->batch_size < 1) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calib config: batch size must be >= 1");
+  if (!(cfg->lr_round > 0.0) || !(cfg->lr_scale > 0.0))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calib config: learning rates must be positive");
+  if (!(cfg->zeta > 1.0) || !(cfg->gamma_lo < 0.0))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calib config: rectified sigmoid needs zeta > 1 > 0 > gamma");
+  if (n_samples <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calibrate_layer: no calibration samples");
+  if (n <= 0 || k <= 0 || !w || !x || !outlier_mask || !scale_normal_init || !sample_rows ||
+      !sample_chunk || !chunk_weights || !codes || !scale_normal_out || !scale_outlier_out ||
+      !scalars_out || (plan_enabled && !scale_outlier_init))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calibrate_layer: null pointer or empty shape");
+  if (act_bits < 2 || act_bits > 8 || w_bits < 2 || w_bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "calibrate_layer: bit widths outside [2, 8]");
+  if (!(act_scale_init > 0.0) || !std::isfinite(act_scale_init))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quant params: scale must be positive and finite");
+  for (int64_t s = 0; s < n_samples; ++s) {
+    if (sample_rows[s + 1] <= sample_rows[s])
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calibrate_layer: empty or unordered sample rows");
+    if (sample_chunk[s] < 1 || sample_chunk[s] > n_chunks)
+      QARVD_FAIL(QARVD_ERR_OUT_OF_RANGE, "weighted loss: sample chunk outside the weight vector");
+  }
+  if (sample_rows[0] != 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "calibrate_layer: sample rows must start at 0");
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+
+  static thread_local cublasHandle_t handle = nullptr;
+  if (!handle) QARVD_CUBLAS_TRY(cublasCreate(&handle));
+  QARVD_CUBLAS_TRY(cublasSetStream(handle, s));
+  QARVD_CUBLAS_TRY(cublasSetPointerMode(handle, CUBLAS_POINTER_MODE_HOST));
+
+  const int64_t nk = n * k, m_all = sample_rows[n_samples];
+  int64_t max_rows = 0;
+  for (int64_t i = 0; i < n_samples; ++i) {
+    const int64_t r = sample_rows[i + 1] - sample_rows[i];
+    max_rows = r > max_rows ? r : max_rows;
+  }
+  const int wq_max = (1 << (w_bits - 1)) - 1, aq_max = (1 << (act_bits - 1)) - 1;
+  const double zeta = cfg->zeta, gamma = cfg->gamma_lo;
+
+  DevArena A(s);
+  double* v = A.get<double>(nk);
+  double* mv = A.get<double>(nk);
+  double* vv = A.get<double>(nk);
+  double* what = A.get<double>(nk);
+  double* code = A.get<double>(nk);
+  double* dhdv = A.get<double>(nk);
+  double* gw = A.get<double>(nk);
+  double* log_s = A.get<double>(2 * n);
+  double* ms = A.get<double>(2 * n);
+  double* vs = A.get<double>(2 * n);
+  double* sgrad = A.get<double>(2 * n);
+  double* target = A.get<double>(m_all * n);
+  double* d = A.get<double>(max_rows * n);
+  double* xhat = A.get<double>(max_rows * k);
+  double* xcode = A.get<double>(max_rows * k);
+  double* gx = A.get<double>(max_rows * k);
+  double* partial = A.get<double>(kRedBlocks);
+  // scalars: [0] log_sa [1] m_a [2] v_a [3] g_a [4] loss acc [5] best
+  double* sc = A.get<double>(8);
+  int* flags = A.get<int>(2);  // [0] diverged_at, [1] non-finite input
+  if (!v || !mv || !vv || !what || !code || !dhdv || !gw || !log_s || !ms || !vs || !sgrad || !target ||
+      !d || !xhat || !xcode || !gx || !partial || !sc || !flags)
+    QARVD_FAIL(QARVD_ERR_CUDA, "calibrate_layer: device allocation failed");
+  QARVD_CUDA_TRY(cudaMemsetAsync(mv, 0, nk * 8, s));
+  QARVD_CUDA_TRY(cudaMemsetAsync(vv, 0, nk * 8, s));
+  QARVD_CUDA_TRY(cudaMemsetAsync(ms, 0, 2 * n * 8, s));
+  QARVD_CUDA_TRY(cudaMemsetAsync(vs, 0, 2 * n * 8, s));
+  QARVD_CUDA_TRY(cudaMemsetAsync(sc, 0, 8 * 8, s));
+  set_scalars_kernel<<<1, 1, 0, s>>>(sc + 0, act_scale_init, sc + 5, flags, flags + 1);
+  // LearnableQuantState::init (calibrate.cpp:77-115)
+  const double* s_o_init = plan_enabled ? scale_outlier_init : scale_normal_init;
+  log_kernel<<<blocks_for(n), kT, 0, s>>>(scale_normal_init, log_s, n);
+  log_kernel<<<blocks_for(n), kT, 0, s>>>(s_o_init, log_s + n, n);
+  init_v_kernel<<<blocks_for(nk), kT, 0, s>>>(w, outlier_mask, plan_enabled, scale_normal_init, s_o_init,
+                                             n, k, zeta, gamma, v);
+  count_launch(4);
+  QARVD_LAUNCH_CHECK();
+  // targets X_s W^T for every sample, once (row-major [rows x n] = col-major W^T-op GEMM)
+  const double one = 1.0, zero = 0.0, minus_one = -1.0;
+  QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(m_all),
+                               static_cast<int>(k), &one, w, static_cast<int>(k), x, static_cast<int>(k), &zero,
+                               target, static_cast<int>(n)));
+
+  std::vector<double> wsamp(static_cast<size_t>(n_samples));
+  for (int64_t i = 0; i < n_samples; ++i) wsamp[i] = chunk_weights[sample_chunk[i] - 1];
+
+  // one pass of the objective over `batch` with the current weights in `what`:
+  // sc[4] = sum_b w_b ||D_b||^2; with grads: gw = sum coeff D^T X^, sc[3] = act-scale grad
+  auto objective = [&](const std::vector<int64_t>& batch, bool grads) -> int {
+    const double inv_b = 1.0 / static_cast<double>(batch.size());
+    for (size_t bi = 0; bi < batch.size(); ++bi) {
+      const int64_t si = batch[bi];
+      const int64_t r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
+      xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat, xcode,
+                                                     flags + 1);
+      QARVD_CUDA_TRY(cudaMemcpyAsync(d, target + r0 * n, rows * n * 8, cudaMemcpyDeviceToDevice, s));
+      // D = X^ What^T - T
+      QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows),
+                                   static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
+                                   static_cast<int>(k), &minus_one, d, static_cast<int>(n)));
+      dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(d, nullptr, rows * n, partial);
+      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, wsamp[si], nullptr, bi > 0, sc + 4);
+      count_launch(3);
+      if (grads) {
+        const double coeff = 2.0 * wsamp[si] * inv_b;
+        const double beta_acc = bi > 0 ? 1.0 : 0.0;
+        // dL/dWhat (+)= coeff D^T X^   [n x k]
+        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(k), static_cast<int>(n),
+                                     static_cast<int>(rows), &coeff, xhat, static_cast<int>(k), d,
+                                     static_cast<int>(n), &beta_acc, gw, static_cast<int>(k)));
+        // dL/dX^ = coeff D What   [rows x k]; act grad += sum gx * s_a * code_x
+        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(k), static_cast<int>(rows),
+                                     static_cast<int>(n), &coeff, what, static_cast<int>(k), d,
+                                     static_cast<int>(n), &zero, gx, static_cast<int>(k)));
+        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(gx, xcode, rows * k, partial);
+        dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1.0, sc + 0, bi > 0, sc + 3);
+        count_launch(2);
+      }
+    }
+    QARVD_LAUNCH_CHECK();
+    return QARVD_OK;
+  };
+  std::vector<int64_t> all(static_cast<size_t>(n_samples));
+  for (int64_t i = 0; i < n_samples; ++i) all[i] = i;
+
+  // initial hard loss (calibrate.cpp:320)
+  weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+                                              -wq_max, wq_max, 1, what, nullptr, nullptr, nullptr);
+  count_launch();
+  if (int st = objective(all, false)) return st;
+  loss_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(n_samples), scalars_out + 1);  // initial
+  count_launch();
+
+  uint64_t st_rng = mix_seed_h(cfg->seed, fnv1a_h(layer_name ? layer_name : "", layer_name ? std::strlen(layer_name) : 0));
+  const int iters = cfg->iterations;
+  const int warmup = static_cast<int>(cfg->warmup_frac * static_cast<double>(iters));
+  std::vector<int64_t> batch(static_cast<size_t>(cfg->batch_size));
+  for (int t = 0; t < iters; ++t) {
+    for (int b = 0; b < cfg->batch_size; ++b)
+      batch[b] = static_cast<int64_t>(splitmix64_h(st_rng) % static_cast<uint64_t>(n_samples));
+    weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+                                                -wq_max, wq_max, 0, what, code, dhdv, nullptr);
+    count_launch();
+    if (int st = objective(batch, true)) return st;
+    trace_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(batch.size()), sc + 5,
+                                 trace_out ? trace_out : sc + 7, trace_out ? t : 0, flags);
+    const bool reg_on = t >= warmup && cfg->reg_lambda > 0.0;
+    const double frac = iters > 1 ? static_cast<double>(t) / static_cast<double>(iters - 1) : 1.0;
+    const double beta = cfg->beta_start + (cfg->beta_end - cfg->beta_start) * frac;
+    grad_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(gw, v, code, dhdv, outlier_mask, plan_enabled, log_s,
+                                                       n, k, reg_on ? 1 : 0, cfg->reg_lambda, beta, zeta,
+                                                       gamma, gw, sgrad);
+    const double anneal = 0.5 * (1.0 + std::cos(M_PI * static_cast<double>(t) / static_cast<double>(iters)));
+    const double c1 = 1.0 - std::pow(0.9, t + 1), c2 = 1.0 - std::pow(0.999, t + 1);
+    adam_kernel<<<blocks_for(nk), kT, 0, s>>>(v, gw, mv, vv, nk, cfg->lr_round * anneal, c1, c2);
+    adam_kernel<<<blocks_for(2 * n), kT, 0, s>>>(log_s, sgrad, ms, vs, 2 * n, cfg->lr_scale * anneal, c1, c2);
+    if (cfg->train_activation_scale)
+      adam_kernel<<<1, 32, 0, s>>>(sc + 0, sc + 3, sc + 1, sc + 2, 1, cfg->lr_scale * anneal, c1, c2);
+    count_launch(5);
+    QARVD_LAUNCH_CHECK();
+  }
+
+  // final hard loss, hard codes, learned scales and act scale (calibrate.cpp:391-395)
+  weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+                                              -wq_max, wq_max, 1, what, nullptr, nullptr, codes);
+  count_launch();
+  if (int st = objective(all, false)) return st;
+  loss_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(n_samples), scalars_out + 2);  // final
+  exp_kernel<<<blocks_for(n), kT, 0, s>>>(log_s, scale_normal_out, n);
+  exp_kernel<<<blocks_for(n), kT, 0, s>>>(log_s + n, scale_outlier_out, n);
+  exp_kernel<<<1, 32, 0, s>>>(sc + 0, scalars_out, 1);  // scalars_out[0] = act scale
+  count_launch(4);
+  QARVD_LAUNCH_CHECK();
+  int fl[2] = {0, 0};
+  QARVD_CUDA_TRY(cudaMemcpyAsync(fl, flags, sizeof(fl), cudaMemcpyDeviceToHost, s));
+  QARVD_CUDA_TRY(cudaStreamSynchronize(s));
+  if (fl[1]) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize: non-finite input");
+  if (fl[0] >= 0)
+    QARVD_FAIL(QARVD_ERR_RUNTIME, "calibration diverged for layer " + std::string(layer_name ? layer_name : "") +
+                                      " at iteration " + std::to_string(fl[0]));
+  return QARVD_OK;
+}
