@@ -372,6 +372,77 @@ double weighted_loss(const std::vector<const CalibSample*>& batch, const Learnab
   return out;
 }
 
+LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, const QuantParams& act_init,
+                                 const std::vector<const CalibSample*>& samples,
+                                 const std::vector<double>& chunk_weights, const CalibConfig& cfg) {
+  cfg.validate();
+  if (samples.empty()) throw std::invalid_argument("calibrate_layer: no calibration samples");
+  if (act_init.per_channel() || act_init.zero_point[0] != 0)
+    throw std::invalid_argument("calibrate_layer: the activation init must be per-tensor symmetric");
+  const size_t n = w.rows(), k = w.cols();
+  std::vector<uint8_t> mask(k, 0);
+  if (plan.enabled)
+    for (size_t c : plan.outlier_indices) mask[c] = 1;
+  std::vector<int64_t> rows{0}, chunks;
+  for (const CalibSample* s : samples) {
+    if (s->x.cols() != k) throw std::invalid_argument("calibrate_layer: sample width does not match the weight");
+    rows.push_back(rows.back() + static_cast<int64_t>(s->x.rows()));
+    chunks.push_back(static_cast<int64_t>(s->chunk));
+  }
+  std::vector<double> x(static_cast<size_t>(rows.back()) * k);
+  size_t off = 0;
+  for (const CalibSample* s : samples) {
+    std::memcpy(x.data() + off, s->x.data(), s->x.size() * sizeof(double));
+    off += s->x.size();
+  }
+  const std::vector<double>& sn = plan.params_normal.scale;
+  const std::vector<double>& so = plan.enabled ? plan.params_outlier.scale : plan.params_normal.scale;
+  DevBuf w_d(w.data(), w.size() * 8), mask_d(mask.data(), k), sn_d(sn.data(), n * 8), so_d(so.data(), n * 8);
+  DevBuf x_d(x.data(), x.size() * 8), codes_d(n * k), sn_out(n * 8), so_out(n * 8), sc_out(3 * 8),
+      tr_out(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 1) * 8);
+  qarvd_calib_config c{};
+  c.iterations = cfg.iterations;
+  c.batch_size = cfg.batch_size;
+  c.lr_round = cfg.lr_round;
+  c.lr_scale = cfg.lr_scale;
+  c.seed = cfg.seed;
+  c.train_activation_scale = cfg.train_activation_scale ? 1 : 0;
+  c.zeta = cfg.zeta;
+  c.gamma_lo = cfg.gamma_lo;
+  c.reg_lambda = cfg.reg_lambda;
+  c.beta_start = cfg.beta_start;
+  c.beta_end = cfg.beta_end;
+  c.warmup_frac = cfg.warmup_frac;
+  check(qarvd_calibrate_layer(w_d.as<double>(), static_cast<int64_t>(n), static_cast<int64_t>(k),
+                              mask_d.as<uint8_t>(), plan.enabled ? 1 : 0, sn_d.as<double>(), so_d.as<double>(),
+                              act_init.scale[0], act_init.bits, plan.params_normal.bits, x_d.as<double>(),
+                              rows.data(), chunks.data(), static_cast<int64_t>(samples.size()),
+                              chunk_weights.data(), static_cast<int64_t>(chunk_weights.size()), &c,
+                              plan.layer_name.c_str(), codes_d.as<int8_t>(), sn_out.as<double>(),
+                              so_out.as<double>(), sc_out.as<double>(), tr_out.as<double>(), nullptr));
+  std::vector<int8_t> codes(n * k);
+  std::vector<double> lsn(n), lso(n), sc(3), tr(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0));
+  check_cuda(cudaMemcpy(codes.data(), codes_d.p, n * k, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(lsn.data(), sn_out.p, n * 8, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(lso.data(), so_out.p, n * 8, cudaMemcpyDeviceToHost));
+  check_cuda(cudaMemcpy(sc.data(), sc_out.p, 3 * 8, cudaMemcpyDeviceToHost));
+  if (!tr.empty()) check_cuda(cudaMemcpy(tr.data(), tr_out.p, tr.size() * 8, cudaMemcpyDeviceToHost));
+  LayerCalibResult r;
+  r.layer = plan.layer_name;
+  // plan_with_learned_scales (calibrate.cpp:185-199)
+  r.plan = plan;
+  r.plan.params_normal = QuantParams::per_channel_symmetric(plan.params_normal.bits, 0, lsn);
+  r.plan.params_outlier = QuantParams::per_channel_symmetric(plan.params_outlier.bits, 0, lso);
+  r.codes.shape = {n, k};
+  r.codes.bits = plan.params_normal.bits;
+  r.codes.data.assign(codes.begin(), codes.end());
+  r.act = QuantParams::per_tensor_symmetric(act_init.bits, sc[0]);
+  r.initial_loss = sc[1];
+  r.final_loss = sc[2];
+  r.trace = tr;
+  return r;
+}
+
 Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed) {
   const CudaQuantizedProvider provider(qm);
   return run_rollout(qm.cfg, provider, &provider, QuantTarget::all, 0, prompt_seed);

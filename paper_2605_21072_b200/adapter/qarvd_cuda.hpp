@@ -8,6 +8,7 @@
 //     qarvd::quantized_layer_forward       -> qarvd::cuda::quantized_layer_forward
 //     qarvd::analyze_layer                 -> qarvd::cuda::analyze_layer
 //     qarvd::weighted_loss                 -> qarvd::cuda::weighted_loss
+//     qarvd::calibrate_layer               -> qarvd::cuda::calibrate_layer
 //     QuantizedProvider (engine.cpp:146-171) -> qarvd::cuda::CudaQuantizedProvider
 // Signatures, argument meaning and exception types/messages follow the
 // reference.  All arithmetic runs in libqarvd_b200.so (sm_100a); this file only
@@ -55,6 +56,13 @@ OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w,
 // Equals the reference within ~1e-5 relative; same exceptions (empty batch, chunk range).
 double weighted_loss(const std::vector<const CalibSample*>& batch, const LearnableQuantState& state,
                      const std::vector<double>& chunk_weights);
+
+// calibrate.hpp:112-116 — AdaRound calibration of one layer on the GPU (K7, f64): the same
+// sampler, formulas and Adam schedule as the reference; identical hard codes, learned scales
+// and losses to ~1e-9 relative.  Same config validation and exceptions.
+LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, const QuantParams& act_init,
+                                 const std::vector<const CalibSample*>& samples,
+                                 const std::vector<double>& chunk_weights, const CalibConfig& cfg);
 
 // Device-resident copy of one QuantizedLayer (codes padded into the kernel layout).
 class DeviceLayer;
