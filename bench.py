@@ -490,6 +490,43 @@ def cpu_baselines_calib_loss(torch, threads):
     return out
 
 
+def adaround_bench(torch, iters=10):
+    """K7 (AdaRound calibrate_layer, f64) on one Wan 1536 -> 1536 layer: 21 frames x 1560 tokens
+    as samples, batch 8 (the paper's setting); reports ms per iteration."""
+    import paper_2605_21072_b200 as qb
+    from paper_2605_21072_b200 import calibrate, engine, synth
+
+    spec = synth.wan_registry(blocks=1)[0]
+    w = synth.synth_weight(spec, seed=1)
+    rep = qb.analyze_layer(spec.name, w)
+    plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+    layer = engine.prepare_weights(spec.name, w, plan)
+    frames, rows = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME
+    xs = [synth.synth_activation(rows, spec.in_dim, seed=3, frame=f).double() for f in range(frames)]
+    act = max(float(x.abs().max()) for x in xs) / 127.0
+    cw = calibrate.weighting_strategy("heuristic_exp", frames)
+    samples = [(x, f + 1) for f, x in enumerate(xs)]
+    run = lambda it: calibrate.calibrate_layer(spec.name, w, plan, layer.scale_normal64, layer.scale_outlier64,
+                                                act, samples, cw, qb._lib.CalibConfig(iterations=it, batch_size=8))
+    run(1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run(0)
+    torch.cuda.synchronize()
+    t_fixed = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = run(iters)
+    torch.cuda.synchronize()
+    t_it = (time.perf_counter() - t0 - t_fixed) / iters
+    flops = 8 * 3 * 2.0 * rows * spec.in_dim * spec.out_dim
+    return {"workload": f"AdaRound calibrate_layer (f64), {spec.out_dim}x{spec.in_dim} layer, {frames} x {rows}-token samples, batch 8",
+            "ms_per_iteration": 1e3 * t_it, "fixed_ms": 1e3 * t_fixed,
+            "dgemm_tflops": flops / t_it / 1e12,
+            "projected_s_per_layer_2000_iters": t_fixed + 2000 * t_it,
+            "final_loss": res.final_loss, "initial_loss": res.initial_loss,
+            "note": "fixed = state init + per-sample targets + initial/final losses; wall clock (host-enqueued launch sequence)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -606,6 +643,11 @@ def main():
         calib = calibration_bench(torch, world, rank, args.calib_steps, peaks.get("hbm_gbs", 6650.0))
 
     recon = recon_loss_bench(torch, peaks)
+    try:
+        adaround = adaround_bench(torch)
+    except Exception as ex:  # reported, never fatal
+        adaround = {"error": str(ex)}
+    torch.cuda.empty_cache()
     stack = None
     if not args.no_stack:
         stack = stack_bench(torch, world, rank, args.stack_steps, 2.0 * peaks.get("bf16_tflops", 1590.0),
@@ -656,6 +698,7 @@ def main():
             "calibration": calib,
             "stack": stack,
             "recon_loss": recon,
+            "adaround": adaround,
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:
