@@ -1019,23 +1019,28 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
     prep_weights_batched_kernel(const WeightJobDev* __restrict__ jobs, int qmax, double rqmax,
                                 unsigned long long* __restrict__ err) {
   extern __shared__ __align__(128) uint16_t wsm[];
-  __shared__ __align__(8) uint64_t full[kWTeams];
+  __shared__ __align__(8) uint64_t full[kWTeams][2];
   const WeightJobDev J = jobs[blockIdx.y];
   const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kWTeams + team;
   if (static_cast<int64_t>(blockIdx.x) * kWTeams >= J.n) return;  // CTA-uniform
   const int k = static_cast<int>(J.k), k_pad = static_cast<int>(J.k_pad), k_o = static_cast<int>(J.k_o);
   const int row_stride = (k + 8 + 63) & ~63;
-  uint16_t* srow = wsm + team * row_stride;
-  int16_t* gidx = reinterpret_cast<int16_t*>(wsm + kWTeams * row_stride);
+  // two row slots per team: row j+1 streams in while row j is rounded
+  uint16_t* slots = wsm + team * 2 * row_stride;
+  int16_t* gidx = reinterpret_cast<int16_t*>(wsm + kWTeams * 2 * row_stride);
   const int64_t step = static_cast<int64_t>(gridDim.x) * kWTeams;
   const uint32_t row_bytes = static_cast<uint32_t>(k) * 2u;
-  if (threadIdx.x < kWTeams) ptx::mbar_init(&full[threadIdx.x], 1);
+  if (threadIdx.x < 2 * kWTeams) ptx::mbar_init(&full[threadIdx.x >> 1][threadIdx.x & 1], 1);
   ptx::fence_mbar_init();
   __syncthreads();
-  if (lane == 0 && row0 < J.n) {
-    ptx::mbar_expect_tx(&full[team], row_bytes);
-    ptx::bulk_load_1d(srow, J.w + row0 * J.ldw, row_bytes, &full[team]);
+  auto load = [&](int sl, int64_t row) {
+    ptx::mbar_expect_tx(&full[team][sl], row_bytes);
+    ptx::bulk_load_1d(slots + sl * row_stride, J.w + row * J.ldw, row_bytes, &full[team][sl]);
+  };
+  if (lane == 0) {
+    if (row0 < J.n) load(0, row0);
+    if (row0 + step < J.n) load(1, row0 + step);
   }
   for (int c4 = threadIdx.x; c4 < (k_pad >> 2); c4 += blockDim.x) {
     const int4 g = __ldg(reinterpret_cast<const int4*>(J.gather) + c4);
@@ -1043,12 +1048,16 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
     const uint32_t hi = static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16);
     reinterpret_cast<uint2*>(gidx)[c4] = make_uint2(lo, hi);
   }
-  if (lane < 8) srow[k + lane] = 0;
+  if (lane < 8) {
+    slots[k + lane] = 0;
+    slots[row_stride + k + lane] = 0;
+  }
   __syncthreads();
 
   int j = 0;
   for (int64_t row = row0; row < J.n; row += step, ++j) {
-    ptx::mbar_wait_spin(&full[team], static_cast<uint32_t>(j & 1));
+    const uint16_t* srow = slots + (j & 1) * row_stride;
+    ptx::mbar_wait_spin(&full[team][j & 1], static_cast<uint32_t>((j >> 1) & 1));
     // ---- pass 1: group maxima through the gather (sign-cleared bf16 bits)
     uint32_t mo = 0, mn = 0;
     for (int c0 = lane * 4; c0 < k_pad; c0 += 128) {
@@ -1113,10 +1122,7 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
       *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
     }
     __syncwarp();
-    if (lane == 0 && row + step < J.n) {
-      ptx::mbar_expect_tx(&full[team], row_bytes);
-      ptx::bulk_load_1d(srow, J.w + (row + step) * J.ldw, row_bytes, &full[team]);
-    }
+    if (lane == 0 && row + 2 * step < J.n) load(j & 1, row + 2 * step);
   }
 }
 
@@ -1580,7 +1586,7 @@ extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int n
     if (j.k_outlier < 0 || j.k_outlier >= j.k_pad)
       QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "build_plan: outlier set would leave no normal channels");
     const bool ok = w_dtype == QARVD_BF16 && j.gather && j.k % 8 == 0 && j.ldw % 8 == 0 &&
-                    j.k_pad % 4 == 0 && j.ldq % 4 == 0 && j.k_outlier % 4 == 0 && j.k <= 12288 &&
+                    j.k_pad % 4 == 0 && j.ldq % 4 == 0 && j.k_outlier % 4 == 0 && j.k <= 10240 &&
                     j.k_pad <= 16384 && (reinterpret_cast<uintptr_t>(j.w) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(j.gather) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(j.wq) & 3) == 0;
@@ -1601,23 +1607,35 @@ extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int n
       }
     }
   }
-  if (!fast.empty() && max_n > 0) {
+  // two launches: rows of <= 2048 values (small shared-memory footprint, many CTAs per SM)
+  // and the wide rows, each with its own slot size
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] { attr = set_smem_attrs(prep_weights_batched_kernel, 200 * 1024); });
+  QARVD_CUDA_TRY(attr);
+  for (int group = 0; group < 2; ++group) {
+    std::vector<WeightJobDev> sel;
+    int64_t g_n = 0, g_k = 0, g_kp = 0;
+    for (const WeightJobDev& jd : fast)
+      if ((jd.k <= 2048) == (group == 0)) {
+        sel.push_back(jd);
+        g_n = jd.n > g_n ? jd.n : g_n;
+        g_k = jd.k > g_k ? jd.k : g_k;
+        g_kp = jd.k_pad > g_kp ? jd.k_pad : g_kp;
+      }
+    if (sel.empty() || g_n == 0) continue;
     WeightJobDev* d_jobs = nullptr;
-    const size_t bytes = fast.size() * sizeof(WeightJobDev);
+    const size_t bytes = sel.size() * sizeof(WeightJobDev);
     QARVD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_jobs), bytes, s));
-    QARVD_CUDA_TRY(cudaMemcpyAsync(d_jobs, fast.data(), bytes, cudaMemcpyHostToDevice, s));
-    const size_t smem = static_cast<size_t>(kWTeams) * ((max_k + 8 + 63) & ~int64_t(63)) * 2 + max_kp * 2;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [] { attr = set_smem_attrs(prep_weights_batched_kernel, 110 * 1024); });
-    QARVD_CUDA_TRY(attr);
-    if (smem > 110 * 1024) QARVD_FAIL(QARVD_ERR_LOGIC, "prepare_weights_batched: rows too wide");
+    QARVD_CUDA_TRY(cudaMemcpyAsync(d_jobs, sel.data(), bytes, cudaMemcpyHostToDevice, s));
+    const size_t smem = static_cast<size_t>(kWTeams) * 2 * ((g_k + 8 + 63) & ~int64_t(63)) * 2 + g_kp * 2;
+    if (smem > 200 * 1024) QARVD_FAIL(QARVD_ERR_LOGIC, "prepare_weights_batched: rows too wide");
     // enough CTAs per layer to fill the GPU a few times over, rows strided across teams
-    int64_t gx = (max_n + kWTeams - 1) / kWTeams;
-    const int64_t cap = (static_cast<int64_t>(kNumSMs) * 16 + static_cast<int64_t>(fast.size()) - 1) /
-                        static_cast<int64_t>(fast.size());
+    int64_t gx = (g_n + kWTeams - 1) / kWTeams;
+    const int64_t cap = (static_cast<int64_t>(kNumSMs) * 16 + static_cast<int64_t>(sel.size()) - 1) /
+                        static_cast<int64_t>(sel.size());
     gx = gx < cap ? gx : (cap < 1 ? 1 : cap);
-    prep_weights_batched_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(fast.size())),
+    prep_weights_batched_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(sel.size())),
                                   32 * kWTeams, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
     count_launch();
     QARVD_LAUNCH_CHECK();
