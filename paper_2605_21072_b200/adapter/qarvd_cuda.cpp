@@ -7,6 +7,7 @@
 #include <stdexcept>
 
 #include "../../include/qarvd_b200.h"
+#include "qarvd/bytes.hpp"
 
 namespace qarvd {
 namespace cuda {
@@ -441,6 +442,72 @@ LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, con
   r.final_loss = sc[2];
   r.trace = tr;
   return r;
+}
+
+ModelCalibResult calibrate_model(const ToyModel& model, const std::vector<double>& chunk_weights,
+                                 const ModelCalibOptions& opts) {
+  opts.base.validate();
+  if (chunk_weights.size() != model.config().chunks)
+    throw std::invalid_argument("calibrate_model: weight vector length must equal chunk count");
+  std::vector<std::string> quant_layers;
+  for (const auto& spec : model.registry())
+    if (!matches_keep_list(spec.name, opts.keep_list)) quant_layers.push_back(spec.name);
+  const std::vector<CalibSample> samples = collect_calibration(model, opts.prompt_seeds, quant_layers);
+  ModelCalibResult out;
+  out.qmodel.cfg = model.config();
+  out.qmodel.scheme = opts.base.scheme;
+  out.qmodel.keep_list = opts.keep_list;
+  out.qmodel.layers.resize(model.registry().size());
+  for (size_t li = 0; li < model.registry().size(); ++li) {
+    const LayerSpec& spec = model.registry()[li];
+    if (matches_keep_list(spec.name, opts.keep_list)) {  // preserved: bf16 passthrough
+      QuantizedLayer l;
+      l.name = spec.name;
+      l.out_dim = spec.out_dim;
+      l.in_dim = spec.in_dim;
+      l.preserved = true;
+      Tensor fp = model.weight(spec.name);
+      for (size_t i = 0; i < fp.size(); ++i) fp[i] = static_cast<double>(bf16_to_float(float_to_bf16(static_cast<float>(fp[i]))));
+      l.fp_weight = fp;
+      out.qmodel.layers[li] = std::move(l);
+      continue;
+    }
+    const Tensor& w = model.weight(spec.name);
+    DualScalePlan plan;
+    if (opts.dual_scale) {
+      const OutlierReport report = qarvd::cuda::analyze_layer(spec.name, w, opts.tau, opts.alpha_min, opts.align);
+      plan = build_plan(w, report, opts.base.scheme.weight_bits);
+    } else {
+      plan = build_single_scale_plan(spec.name, w, opts.base.scheme.weight_bits);
+    }
+    std::vector<const CalibSample*> ls;
+    std::vector<Tensor> acts;
+    for (const auto& smp : samples)
+      if (smp.layer == spec.name) {
+        ls.push_back(&smp);
+        acts.push_back(smp.x);
+      }
+    // percentile activation init of the f64 captures (quant.cpp:190-226; the GPU search, K4,
+    // works on bf16 bit-pattern histograms)
+    const PercentileSearchResult act_init = init_scale_percentile_search(acts, opts.base.scheme.activation_bits);
+    LayerCalibResult res = qarvd::cuda::calibrate_layer(w, plan, act_init.params, ls, chunk_weights, opts.base);
+    QuantizedLayer l;
+    l.name = spec.name;
+    l.out_dim = spec.out_dim;
+    l.in_dim = spec.in_dim;
+    l.preserved = false;
+    l.plan = res.plan;
+    l.act = res.act;
+    l.wq.shape = {spec.out_dim, spec.in_dim};
+    l.wq.bits = res.codes.bits;
+    l.wq.data.resize(spec.out_dim * spec.in_dim);
+    for (size_t r = 0; r < spec.out_dim; ++r)  // pre-permuted [outlier | normal] (calibrate.cpp:474-480)
+      for (size_t pos = 0; pos < spec.in_dim; ++pos)
+        l.wq.data[r * spec.in_dim + pos] = res.codes.at(r, res.plan.permutation[pos]);
+    out.qmodel.layers[li] = std::move(l);
+    out.layer_results.push_back(std::move(res));
+  }
+  return out;
 }
 
 Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed) {

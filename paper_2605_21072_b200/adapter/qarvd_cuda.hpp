@@ -9,6 +9,7 @@
 //     qarvd::analyze_layer                 -> qarvd::cuda::analyze_layer
 //     qarvd::weighted_loss                 -> qarvd::cuda::weighted_loss
 //     qarvd::calibrate_layer               -> qarvd::cuda::calibrate_layer
+//     qarvd::calibrate_model               -> qarvd::cuda::calibrate_model
 //     QuantizedProvider (engine.cpp:146-171) -> qarvd::cuda::CudaQuantizedProvider
 // Signatures, argument meaning and exception types/messages follow the
 // reference.  All arithmetic runs in libqarvd_b200.so (sm_100a); this file only
@@ -63,6 +64,14 @@ double weighted_loss(const std::vector<const CalibSample*>& batch, const Learnab
 LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, const QuantParams& act_init,
                                  const std::vector<const CalibSample*>& samples,
                                  const std::vector<double>& chunk_weights, const CalibConfig& cfg);
+
+// calibrate.hpp:137-139 — the whole-model pipeline with every per-layer step on the GPU:
+// capture (the reference's full-precision rollouts, host f64 glue), outlier detection (K3),
+// build_plan, the percentile activation init, AdaRound (K7) and the pre-permuted codes.
+// Layers run one after another on the device (the reference's parallel_for is slot-indexed,
+// so the result does not depend on the order).
+ModelCalibResult calibrate_model(const ToyModel& model, const std::vector<double>& chunk_weights,
+                                 const ModelCalibOptions& opts);
 
 // Device-resident copy of one QuantizedLayer (codes padded into the kernel layout).
 class DeviceLayer;

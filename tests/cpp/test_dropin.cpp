@@ -154,6 +154,38 @@ int main() {
     }
   }
 
+  // ---- calibrate_model with every per-layer step on the GPU vs the reference pipeline
+  {
+    const ModelCalibResult gcal = qarvd::cuda::calibrate_model(model, w, opts);
+    const QuantizedModel& gq = gcal.qmodel;
+    size_t same = 0, total = 0, diff_codes = 0, n_codes = 0;
+    double worst = 0.0;
+    for (size_t li = 0; li < qm.layers.size(); ++li) {
+      const QuantizedLayer& a = qm.layers[li];
+      const QuantizedLayer& b = gq.layers[li];
+      EXPECT(a.preserved == b.preserved && a.name == b.name, "calibrate_model layer set");
+      if (a.preserved) {
+        EXPECT(a.fp_weight.vec() == b.fp_weight.vec(), "calibrate_model preserved bf16 weights");
+        continue;
+      }
+      ++total;
+      EXPECT(a.plan.permutation == b.plan.permutation, "calibrate_model plans identical");
+      same += a.wq.data == b.wq.data;
+      for (size_t i = 0; i < a.wq.data.size(); ++i) diff_codes += a.wq.data[i] != b.wq.data[i];
+      n_codes += a.wq.data.size();
+      for (size_t r = 0; r < a.out_dim; ++r)
+        worst = std::max(worst, std::fabs(a.plan.params_normal.scale[r] - b.plan.params_normal.scale[r]) /
+                                    a.plan.params_normal.scale[r]);
+      worst = std::max(worst, std::fabs(a.act.scale[0] - b.act.scale[0]) / a.act.scale[0]);
+    }
+    std::printf("calibrate_model: %zu / %zu layers with identical pre-permuted codes (%zu of %zu codes differ), "
+                "worst scale rel diff %.3e\n", same, total, diff_codes, n_codes, worst);
+    // 8 AdaRound iterations leave V at its nearest-rounding init, where an exact .5 tie can
+    // round either way between glibc's and CUDA's exp/log (see calibrate_layer above)
+    EXPECT(diff_codes * 10000 <= n_codes, "calibrate_model codes (<= 1e-4 of elements at init ties)");
+    EXPECT(worst <= 1e-3, "calibrate_model scales");
+  }
+
   // ---- the seam: run_rollout with the CUDA provider vs the reference int engine
   for (uint64_t seed : {5000ull, 5001ull}) {
     const Rollout ref = run_quantized(qm, seed, Engine::int_kernels);
