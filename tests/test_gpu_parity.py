@@ -791,3 +791,33 @@ def test_calibrate_layer_errors(cuda):
         calibrate.calibrate_layer("l", w, plan, s, s, 0.01, [(x, 1)], [1.0], qb._lib.CalibConfig(lr_round=0.0))
     with pytest.raises(qb.OutOfRange, match="outside the weight vector"):
         calibrate.calibrate_layer("l", w, plan, s, s, 0.01, [(x, 2)], [1.0])
+
+
+@pytest.mark.parametrize("m,n,k,n_out,epi", [(4680, 8960, 1536, 32, qb.EPI_GELU), (4680, 1536, 8960, 188, qb.EPI_NONE),
+                                             (4680, 1536, 1536, 32, qb.EPI_NONE), (1000, 8960, 1536, 0, qb.EPI_GELU)])
+def test_k2_deployed_path_full_shape(cuda, m, n, k, n_out, epi):
+    """The deployed K2 path (bf16 TMA-store epilogue holding acc_n in registers, no debug dumps)
+    at the full FFN / qkv shapes, on 48 sampled rows: bit-exact vs the oracle's fp32 epilogue
+    (same op order) without GELU; with GELU within bf16 rounding of the f64 erf-GELU of the
+    oracle's fp32 pre-activation (|err| <= 2^-8 |y| + 1e-6, the A&S erf bound is 3.4e-7)."""
+    import math
+    plan, layer, xq, s32, s64, _, _ = _gemm_case(m, n, k, n_out, seed=m % 97 + n)
+    y = engine.kernel_b_gemm_dequant(xq, s32, layer, epilogue=epi)
+    rows = np.sort(np.random.default_rng(m + n).choice(m, 48, replace=False))
+    xq_h = xq.cpu().numpy()[rows]
+    _, ao, an = oracle.kernel_b(xq_h, layer.wq.cpu().numpy(), plan.k_outlier, s64.cpu().numpy()[rows],
+                                layer.scale_outlier64.cpu().numpy(), layer.scale_normal64.cpu().numpy(),
+                                with_acc=True)
+    yd = dev_bits(y)[rows]
+    if epi == qb.EPI_NONE:
+        y_ref = oracle.epilogue_f32(ao, an, plan.k_outlier > 0, s32.cpu().numpy()[rows],
+                                    layer.scale_outlier32.cpu().numpy(), layer.scale_normal32.cpu().numpy())
+        np.testing.assert_array_equal(yd, y_ref)
+    else:
+        v = oracle.epilogue_f32(ao, an, plan.k_outlier > 0, s32.cpu().numpy()[rows],
+                                layer.scale_outlier32.cpu().numpy(), layer.scale_normal32.cpu().numpy(),
+                                out="f32").astype(np.float64)
+        erf = np.vectorize(math.erf)
+        g = 0.5 * v * (1.0 + erf(v / math.sqrt(2.0)))
+        yf = (yd.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        assert np.all(np.abs(yf - g) <= 2.0 ** -8 * np.abs(g) + 1e-6)
