@@ -156,6 +156,30 @@ typedef struct qarvd_weight_job {
 int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int num_jobs, int w_dtype,
                                   int bits, int64_t* err_index, void* stream);
 
+/* K3 -> plan -> K5 without a host round trip: the plan's column split (build_plan,
+ * dual_scale.cpp:44-90) is built on the device from K3's aligned outlier set, then the batched
+ * K5 reads it.  bf16 weights, rows of <= 10240 values.
+ *   aligned_idx / counts: qarvd_analyze_layers outputs (counts[1] = |aligned|)
+ *   gather: out device int32 [gather_cap >= k + 64]; plan_info: out device int64 {k_outlier, k_pad}
+ *   wq: out [n x ldq], ldq >= k + 64 (only the first k_pad columns of each row are written). */
+typedef struct qarvd_planned_weight_job {
+  const void* w;
+  int64_t n, k, ldw;
+  const int32_t* aligned_idx;
+  const int32_t* counts;
+  int32_t* gather;
+  int64_t gather_cap;
+  int64_t* plan_info;
+  int8_t* wq;
+  int64_t ldq;
+  double* scale_outlier_f64;
+  double* scale_normal_f64;
+  float* scale_outlier_f32;
+  float* scale_normal_f32;
+} qarvd_planned_weight_job;
+int qarvd_prepare_weights_planned(const qarvd_planned_weight_job* jobs, int num_jobs, int bits,
+                                  int64_t* err_index, void* stream);
+
 /* ---- K2: dual-scale W8A8 GEMM + dequant + bias epilogue ------------------
  * Replaces  kernel_b_gemm_dequant(xq, layer)  engine.hpp:48 / engine.cpp:46-105
  * (symmetric activations; the reference's zero-point correction, engine.cpp:95-100,

@@ -113,6 +113,17 @@ class CalibConfig(ctypes.Structure):
         super().__init__(**d)
 
 
+class PlannedWeightJob(ctypes.Structure):
+    """qarvd_planned_weight_job (include/qarvd_b200.h)."""
+    _fields_ = [
+        ("w", c_void_p), ("n", c_int64), ("k", c_int64), ("ldw", c_int64),
+        ("aligned_idx", c_void_p), ("counts", c_void_p), ("gather", c_void_p), ("gather_cap", c_int64),
+        ("plan_info", c_void_p), ("wq", c_void_p), ("ldq", c_int64),
+        ("scale_outlier_f64", c_void_p), ("scale_normal_f64", c_void_p),
+        ("scale_outlier_f32", c_void_p), ("scale_normal_f32", c_void_p),
+    ]
+
+
 class WeightJob(ctypes.Structure):
     _fields_ = [
         ("w", c_void_p),
@@ -198,6 +209,7 @@ SIGNATURES = {
         [POINTER(SearchJob), c_int, POINTER(c_double), c_int, POINTER(c_double), c_int, c_void_p],
     ),
     "qarvd_weighted_loss_workspace": (c_int64, [c_int64, c_int64, c_int64]),
+    "qarvd_prepare_weights_planned": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "qarvd_calibrate_layer": (
         c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_double, c_int, c_int,
                 c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_char_p, c_void_p,

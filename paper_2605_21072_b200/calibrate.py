@@ -280,58 +280,104 @@ class CalibrationShard:
     def bytes(self) -> float:
         return float(sum(x.numel() * 2 for x in self.x) + sum(w.numel() * 3 for w in self.w))
 
-    def run(self) -> List[LayerRecord]:
-        from . import engine, outlier
-        if not self.specs:
-            return []
-        # K3: batched outlier detection (one launch pair per weight dtype group)
-        dev_rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w)
-        # K4 over every layer's frames (independent of K3/K5; same stream)
+    def _prepare_buffers(self):
+        """Device buffers and launch tables of the sync-free step (allocated once)."""
+        from . import outlier
+        dev = self.x[0].device
+        L = len(self.specs)
+        self._rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w)
+        caps = [(s.in_dim + 64 + 15) // 16 * 16 for s in self.specs]
+        goff = np.concatenate([[0], np.cumsum(caps)]).astype(np.int64)
+        noff = np.concatenate([[0], np.cumsum([s.out_dim for s in self.specs])]).astype(np.int64)
+        self._caps, self._noff = caps, noff
+        self._gather = torch.empty(int(goff[-1]), dtype=torch.int32, device=dev)
+        self._plan_info = torch.empty((L, 2), dtype=torch.int64, device=dev)
+        self._wq = [torch.empty((s.out_dim, c), dtype=torch.int8, device=dev) for s, c in zip(self.specs, caps)]
+        self._so64 = torch.empty(int(noff[-1]), dtype=torch.float64, device=dev)
+        self._sn64 = torch.empty_like(self._so64)
+        self._so32 = torch.empty(int(noff[-1]), dtype=torch.float32, device=dev)
+        self._sn32 = torch.empty_like(self._so32)
+        jobs = (_lib.PlannedWeightJob * L)()
+        rep = self._rep
+        for i, (spec, w) in enumerate(zip(self.specs, self.w)):
+            j = jobs[i]
+            o = int(rep.offsets[i])
+            j.w, j.n, j.k, j.ldw = w.data_ptr(), w.shape[0], w.shape[1], w.stride(0)
+            j.aligned_idx = rep.aligned.data_ptr() + 4 * o
+            j.counts = rep.counts.data_ptr() + 8 * i
+            j.gather, j.gather_cap = self._gather.data_ptr() + 4 * int(goff[i]), caps[i]
+            j.plan_info = self._plan_info.data_ptr() + 16 * i
+            j.wq, j.ldq = self._wq[i].data_ptr(), caps[i]
+            sl = int(noff[i])
+            j.scale_outlier_f64, j.scale_normal_f64 = self._so64.data_ptr() + 8 * sl, self._sn64.data_ptr() + 8 * sl
+            j.scale_outlier_f32, j.scale_normal_f32 = self._so32.data_ptr() + 4 * sl, self._sn32.data_ptr() + 4 * sl
+        self._jobs = jobs
         groups = {}
         for i, x in enumerate(self.x):
             groups.setdefault(x.shape[0] // self.frames, []).append(i)
-        # K4 runs on a side stream: the host reads K3's reports, builds the plans and
-        # launches K5 while the histogram passes stream X
-        if not hasattr(self, "_side"):
-            self._side = torch.cuda.Stream(device=self.x[0].device)
+        self._groups = groups
+        self._side = torch.cuda.Stream(device=dev)
+        self._flags = torch.empty(len(groups), dtype=torch.int64, device=dev)
+
+    def run(self) -> List[LayerRecord]:
+        """One calibration step, host-sync free until the results come back: K3 -> device plan
+        -> K5 on the current stream, K4 (histogram search) on a side stream, one gather of the
+        results at the end."""
+        from . import outlier
+        if not self.specs:
+            return []
+        if not hasattr(self, "_jobs"):
+            self._prepare_buffers()
         main = torch.cuda.current_stream()
         self._side.wait_stream(main)
         search = {}
         with torch.cuda.stream(self._side):
-            flags = torch.empty(len(groups), dtype=torch.int64, device=self.x[0].device)
-            for g, (rows, idx) in enumerate(groups.items()):
+            for g, (rows, idx) in enumerate(self._groups.items()):
                 res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights,
-                                         nonfinite_flag=flags[g:g + 1])
+                                         nonfinite_flag=self._flags[g:g + 1])
                 for j, i in enumerate(idx):
                     search[i] = res[j]
-        reps = outlier.collect_reports(dev_rep)  # host sync (main stream): plans need the index sets
-        plans = [engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
-                 for spec, rep in zip(self.specs, reps)]
-        # K5 for every layer in one launch; codes / scales land in one buffer per field
-        layers = engine.prepare_weights_batched([s.name for s in self.specs], self.w, plans,
-                                                check_finite=False)
+        rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w, out=self._rep)
+        _lib.call("qarvd_prepare_weights_planned", self._jobs, len(self.specs), 8, None, _stream())
         main.wait_stream(self._side)
-        # one device -> host copy per result group (not per layer)
+        # results: one device -> host copy per field
         search_host = {}
-        for rows, idx in groups.items():
+        for rows, idx in self._groups.items():
             mat = torch.stack([search[i] for i in idx]).cpu().numpy()
             for j, i in enumerate(idx):
                 search_host[i] = mat[j]
-        if (flags.cpu() != -1).any():
+        if (self._flags.cpu() != -1).any():
             raise _lib.InvalidArgument("quantize: non-finite input in calibration samples")
-        so_all = torch.cat([L.scale_outlier64 for L in layers]).cpu().numpy()
-        sn_all = torch.cat([L.scale_normal64 for L in layers]).cpu().numpy()
-        out, off = [], 0
+        counts = rep.counts.cpu().numpy()
+        aligned = rep.aligned.cpu().numpy()
+        so_all = self._so64.cpu().numpy()
+        sn_all = self._sn64.cpu().numpy()
+        out = []
         nc = len(PERCENTILES)
-        for i, (spec, L, rep) in enumerate(zip(self.specs, layers, reps)):
+        for i, spec in enumerate(self.specs):
             r = search_host[i]
-            n = L.out_dim
-            out.append(LayerRecord(spec.index, len(rep.aligned_outliers), rep.aligned_outliers,
-                                   float(r[3 * nc + 1]), int(r[3 * nc]), r[2 * nc:3 * nc].copy(),
-                                   so_all[off:off + n].copy(), sn_all[off:off + n].copy()))
-            off += n
-        self.layers = layers
+            o = int(rep.offsets[i])
+            outl = aligned[o:o + counts[i, 1]].astype(np.int64)
+            s0, s1 = int(self._noff[i]), int(self._noff[i + 1])
+            out.append(LayerRecord(spec.index, len(outl), outl, float(r[3 * nc + 1]), int(r[3 * nc]),
+                                   r[2 * nc:3 * nc].copy(), so_all[s0:s1].copy(), sn_all[s0:s1].copy()))
         return out
+
+    def deployed_layers(self):
+        """QuantizedLayer views of the last run() (plans rebuilt on the host; not timed)."""
+        from . import engine, outlier
+        reps = outlier.collect_reports(self._rep)
+        info = self._plan_info.cpu().numpy()
+        layers = []
+        for i, (spec, rep) in enumerate(zip(self.specs, reps)):
+            plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+            assert plan.k_outlier == info[i, 0] and plan.k_pad == info[i, 1]
+            s0, s1 = int(self._noff[i]), int(self._noff[i + 1])
+            layers.append(engine.QuantizedLayer(
+                spec.name, spec.out_dim, spec.in_dim, plan, self._wq[i][:, :plan.k_pad].contiguous(),
+                self._so64[s0:s1], self._sn64[s0:s1], self._so32[s0:s1], self._sn32[s0:s1],
+                torch.from_numpy(plan.gather).to(self._wq[i].device)))
+        return layers
 
 
 def weighted_loss(batch: Sequence, layer, w: torch.Tensor, chunk_weights: Sequence[float],

@@ -998,7 +998,8 @@ struct WeightJobDev {
   const uint16_t* w;
   int64_t n, k, ldw;
   const int32_t* gather;
-  int64_t k_pad, k_o;
+  int64_t k_pad, k_o;     // or, with plan_info, upper bounds (the device plan decides)
+  const int64_t* plan_info;  // optional device {k_outlier, k_pad} (qarvd_prepare_weights_planned)
   int8_t* wq;
   int64_t ldq;
   double* so64;
@@ -1024,7 +1025,10 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
   const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kWTeams + team;
   if (static_cast<int64_t>(blockIdx.x) * kWTeams >= J.n) return;  // CTA-uniform
-  const int k = static_cast<int>(J.k), k_pad = static_cast<int>(J.k_pad), k_o = static_cast<int>(J.k_o);
+  pdl_wait();  // the plan kernel (qarvd_prepare_weights_planned) writes gather / plan_info
+  const int k = static_cast<int>(J.k);
+  const int k_pad = static_cast<int>(J.plan_info ? J.plan_info[1] : J.k_pad);
+  const int k_o = static_cast<int>(J.plan_info ? J.plan_info[0] : J.k_o);
   const int row_stride = (k + 8 + 63) & ~63;
   // two row slots per team: row j+1 streams in while row j is rounded
   uint16_t* slots = wsm + team * 2 * row_stride;
@@ -1561,54 +1565,12 @@ extern "C" int qarvd_quantize_act_pmax(const uint16_t* x, int64_t m, int64_t k, 
   return QARVD_OK;
 }
 
-extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int num_jobs, int w_dtype,
-                                             int bits, int64_t* err_index, void* stream) {
-  clear_error();
-  if (num_jobs < 0 || (num_jobs > 0 && !jobs))
-    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "prepare_weights_batched: invalid job table");
-  if (bits < 2 || bits > 8)
-    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
-  if (num_jobs == 0) return QARVD_OK;
-  if (int st = require_device()) return st;
-  cudaStream_t s = as_stream(stream);
-  const int qmax = (1 << (bits - 1)) - 1;
-  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
-  if (err) {
-    init_err_kernel<<<1, 1, 0, s>>>(err);
-    count_launch();
-  }
-  // jobs the batched bf16 kernel serves; the rest take the per-layer path
-  std::vector<WeightJobDev> fast;
-  int64_t max_n = 0, max_k = 0, max_kp = 0;
-  for (int i = 0; i < num_jobs; ++i) {
-    const qarvd_weight_job& j = jobs[i];
-    if (int st = check_common(j.w, w_dtype, j.n, j.k, j.ldw, j.k_pad, bits, j.wq, j.ldq, j.gather)) return st;
-    if (j.k_outlier < 0 || j.k_outlier >= j.k_pad)
-      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "build_plan: outlier set would leave no normal channels");
-    const bool ok = w_dtype == QARVD_BF16 && j.gather && j.k % 8 == 0 && j.ldw % 8 == 0 &&
-                    j.k_pad % 4 == 0 && j.ldq % 4 == 0 && j.k_outlier % 4 == 0 && j.k <= 10240 &&
-                    j.k_pad <= 16384 && (reinterpret_cast<uintptr_t>(j.w) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(j.gather) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(j.wq) & 3) == 0;
-    if (ok) {
-      fast.push_back(WeightJobDev{static_cast<const uint16_t*>(j.w), j.n, j.k, j.ldw, j.gather, j.k_pad,
-                                  j.k_outlier, j.wq, j.ldq, j.scale_outlier_f64, j.scale_normal_f64,
-                                  j.scale_outlier_f32, j.scale_normal_f32});
-      max_n = j.n > max_n ? j.n : max_n;
-      max_k = j.k > max_k ? j.k : max_k;
-      max_kp = j.k_pad > max_kp ? j.k_pad : max_kp;
-    } else if (j.n > 0) {
-      if (int st = launch_rows<kWeightDual>(j.w, w_dtype, j.n, j.k, j.ldw, j.gather, j.k_pad, j.k_outlier,
-                                            0.0, bits, j.wq, j.ldq, j.scale_outlier_f32, j.scale_outlier_f64,
-                                            j.scale_normal_f32, j.scale_normal_f64, nullptr, s))
-        return st;
-      if (err) {  // fold the per-layer check into the batch's error index
-        (void)0;
-      }
-    }
-  }
-  // two launches: rows of <= 2048 values (small shared-memory footprint, many CTAs per SM)
-  // and the wide rows, each with its own slot size
+namespace qarvd_b200 {
+namespace {
+// Launch the batched K5 kernel over bf16 jobs: two launches, rows of <= 2048 values (small
+// shared-memory footprint, many CTAs per SM) and the wide rows, each with its own slot size.
+int launch_prep_batched(const std::vector<WeightJobDev>& fast, int qmax, unsigned long long* err,
+                        cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] { attr = set_smem_attrs(prep_weights_batched_kernel, 200 * 1024); });
@@ -1642,4 +1604,158 @@ extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int n
     QARVD_CUDA_TRY(cudaFreeAsync(d_jobs, s));
   }
   return QARVD_OK;
+}
+}  // namespace
+}  // namespace qarvd_b200
+
+namespace qarvd_b200 {
+namespace {
+struct PlanJobDev {
+  int64_t k;
+  const int32_t* aligned;
+  const int32_t* counts;
+  int32_t* gather;
+  int64_t gather_cap;
+  int64_t* plan_info;
+};
+// build_plan's column split on the device (engine.build_plan / dual_scale.cpp:44-90): gather =
+// [aligned outliers ascending | -1 to a multiple of 32 | normal columns ascending | -1 ...],
+// plan_info = {k_outlier, k_pad}; an empty outlier set is the single-scale identity plan.
+constexpr int kPlanThreads = 256;
+__global__ void __launch_bounds__(kPlanThreads) build_plan_kernel(const PlanJobDev* __restrict__ jobs) {
+  const PlanJobDev J = jobs[blockIdx.x];
+  __shared__ uint32_t mask[10240 / 32 + 1];
+  __shared__ uint32_t pre[10240 / 32 + 1];  // outliers below each 32-column word
+  const int k = static_cast<int>(J.k), words = (k + 31) / 32;
+  const int n_o = J.counts[1];
+  for (int w = threadIdx.x; w < words; w += kPlanThreads) mask[w] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_o; i += kPlanThreads) {
+    const int c = J.aligned[i];
+    atomicOr(&mask[c >> 5], 1u << (c & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int w = 0; w < words; ++w) {
+      pre[w] = acc;
+      acc += __popc(mask[w]);
+    }
+  }
+  __syncthreads();
+  const int k_o = n_o > 0 ? (n_o + 31) / 32 * 32 : 0;
+  const int k_pad = k_o + (k - n_o + 31) / 32 * 32;
+  for (int i = threadIdx.x; i < J.gather_cap; i += kPlanThreads) {
+    int g = -1;
+    if (i < n_o) g = J.aligned[i];
+    J.gather[i] = g;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += kPlanThreads) {
+    const uint32_t m = mask[c >> 5];
+    if (!((m >> (c & 31)) & 1u)) {
+      const int below = static_cast<int>(pre[c >> 5]) + __popc(m & ((1u << (c & 31)) - 1u));
+      J.gather[k_o + c - below] = c;
+    }
+  }
+  if (threadIdx.x == 0) {
+    J.plan_info[0] = k_o;
+    J.plan_info[1] = k_pad;
+  }
+  pdl_launch_dependents();
+}
+}  // namespace
+}  // namespace qarvd_b200
+
+extern "C" int qarvd_prepare_weights_planned(const qarvd_planned_weight_job* jobs, int num_jobs, int bits,
+                                             int64_t* err_index, void* stream) {
+  clear_error();
+  if (num_jobs < 0 || (num_jobs > 0 && !jobs))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "prepare_weights_planned: invalid job table");
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (num_jobs == 0) return QARVD_OK;
+  std::vector<PlanJobDev> plans;
+  std::vector<WeightJobDev> fast;
+  for (int i = 0; i < num_jobs; ++i) {
+    const qarvd_planned_weight_job& j = jobs[i];
+    const int64_t need = (j.k + 64 + 15) / 16 * 16;
+    if (j.n <= 0 || j.k <= 0 || j.k > 10240 || j.k % 8 || j.ldw < j.k || j.ldw % 8 || !j.w || !j.aligned_idx ||
+        !j.counts || !j.gather || !j.plan_info || !j.wq || j.gather_cap < need || j.gather_cap % 4 ||
+        j.ldq < need || j.ldq % 4 || (reinterpret_cast<uintptr_t>(j.w) & 15) ||
+        (reinterpret_cast<uintptr_t>(j.gather) & 15) || (reinterpret_cast<uintptr_t>(j.wq) & 3))
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+                 "prepare_weights_planned: bf16 rows of <= 10240 values (k, ldw multiples of 8), "
+                 "gather_cap and ldq >= k + 64 (multiples of 4), aligned buffers");
+    plans.push_back(PlanJobDev{j.k, j.aligned_idx, j.counts, j.gather, j.gather_cap, j.plan_info});
+    fast.push_back(WeightJobDev{static_cast<const uint16_t*>(j.w), j.n, j.k, j.ldw, j.gather, j.gather_cap, 0,
+                                j.plan_info, j.wq, j.ldq, j.scale_outlier_f64, j.scale_normal_f64,
+                                j.scale_outlier_f32, j.scale_normal_f32});
+  }
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, s>>>(err);
+    count_launch();
+  }
+  PlanJobDev* d_plans = nullptr;
+  QARVD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_plans), plans.size() * sizeof(PlanJobDev), s));
+  QARVD_CUDA_TRY(cudaMemcpyAsync(d_plans, plans.data(), plans.size() * sizeof(PlanJobDev),
+                                 cudaMemcpyHostToDevice, s));
+  build_plan_kernel<<<static_cast<unsigned>(plans.size()), kPlanThreads, 0, s>>>(d_plans);
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  QARVD_CUDA_TRY(cudaFreeAsync(d_plans, s));
+  return launch_prep_batched(fast, qmax, err, s);
+}
+
+extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int num_jobs, int w_dtype,
+                                             int bits, int64_t* err_index, void* stream) {
+  clear_error();
+  if (num_jobs < 0 || (num_jobs > 0 && !jobs))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "prepare_weights_batched: invalid job table");
+  if (bits < 2 || bits > 8)
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "bit width out of the int8 storage range [2,8]: " + std::to_string(bits));
+  if (num_jobs == 0) return QARVD_OK;
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  const int qmax = (1 << (bits - 1)) - 1;
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(err_index);
+  if (err) {
+    init_err_kernel<<<1, 1, 0, s>>>(err);
+    count_launch();
+  }
+  // jobs the batched bf16 kernel serves; the rest take the per-layer path
+  std::vector<WeightJobDev> fast;
+  int64_t max_n = 0, max_k = 0, max_kp = 0;
+  for (int i = 0; i < num_jobs; ++i) {
+    const qarvd_weight_job& j = jobs[i];
+    if (int st = check_common(j.w, w_dtype, j.n, j.k, j.ldw, j.k_pad, bits, j.wq, j.ldq, j.gather)) return st;
+    if (j.k_outlier < 0 || j.k_outlier >= j.k_pad)
+      QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "build_plan: outlier set would leave no normal channels");
+    const bool ok = w_dtype == QARVD_BF16 && j.gather && j.k % 8 == 0 && j.ldw % 8 == 0 &&
+                    j.k_pad % 4 == 0 && j.ldq % 4 == 0 && j.k_outlier % 4 == 0 && j.k <= 10240 &&
+                    j.k_pad <= 16384 && (reinterpret_cast<uintptr_t>(j.w) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(j.gather) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(j.wq) & 3) == 0;
+    if (ok) {
+      fast.push_back(WeightJobDev{static_cast<const uint16_t*>(j.w), j.n, j.k, j.ldw, j.gather, j.k_pad,
+                                  j.k_outlier, nullptr, j.wq, j.ldq, j.scale_outlier_f64, j.scale_normal_f64,
+                                  j.scale_outlier_f32, j.scale_normal_f32});
+      max_n = j.n > max_n ? j.n : max_n;
+      max_k = j.k > max_k ? j.k : max_k;
+      max_kp = j.k_pad > max_kp ? j.k_pad : max_kp;
+    } else if (j.n > 0) {
+      if (int st = launch_rows<kWeightDual>(j.w, w_dtype, j.n, j.k, j.ldw, j.gather, j.k_pad, j.k_outlier,
+                                            0.0, bits, j.wq, j.ldq, j.scale_outlier_f32, j.scale_outlier_f64,
+                                            j.scale_normal_f32, j.scale_normal_f64, nullptr, s))
+        return st;
+      if (err) {  // fold the per-layer check into the batch's error index
+        (void)0;
+      }
+    }
+  }
+  return launch_prep_batched(fast, qmax, err, s);
 }

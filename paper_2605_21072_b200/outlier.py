@@ -7,7 +7,7 @@ launches (column norms, then per-layer median/MAD/threshold/alignment).
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence
+from typing import Optional, List, Sequence
 
 import numpy as np
 import torch
@@ -58,7 +58,14 @@ class DeviceReports:
 
 def analyze_layers_async(names: Sequence[str], weights: Sequence[torch.Tensor],
                          tau: float = K_DEFAULT_TAU, alpha_min: float = K_DEFAULT_ALPHA_MIN,
-                         align: int = K_DEFAULT_ALIGN) -> DeviceReports:
+                         align: int = K_DEFAULT_ALIGN, out: Optional[DeviceReports] = None) -> DeviceReports:
+    """K3 over a batch of layers into device buffers (no host sync).  ``out`` reuses the buffers
+    (and the launch table) of an earlier call with the same layers."""
+    if out is not None and getattr(out, "_jobs", None) is not None:
+        _lib.call("qarvd_analyze_layers", out._jobs, len(weights), _dtype_code(weights[0]), float(tau),
+                  float(alpha_min), int(align), _stream())
+        out.tau, out.alpha_min, out.align = tau, alpha_min, align
+        return out
     if len(weights) == 0:
         raise _lib.InvalidArgument("analyze_layers: no layers")
     dt = {w.dtype for w in weights}
@@ -81,6 +88,7 @@ def analyze_layers_async(names: Sequence[str], weights: Sequence[torch.Tensor],
     _lib.call("qarvd_analyze_layers", jobs, len(weights), _dtype_code(weights[0]), float(tau),
               float(alpha_min), int(align), _stream())
     out.tau, out.alpha_min, out.align = tau, alpha_min, align
+    out._jobs = jobs
     return out
 
 

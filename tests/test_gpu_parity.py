@@ -821,3 +821,28 @@ def test_k2_deployed_path_full_shape(cuda, m, n, k, n_out, epi):
         g = 0.5 * v * (1.0 + erf(v / math.sqrt(2.0)))
         yf = (yd.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         assert np.all(np.abs(yf - g) <= 2.0 ** -8 * np.abs(g) + 1e-6)
+
+
+def test_calibration_shard_sync_free_matches_per_layer(cuda):
+    """CalibrationShard.run (K3 -> device plan -> K5 and K4 without a host round trip) gives
+    the same outlier sets, plans, codes and scales as the per-layer host path (analyze_layer ->
+    build_plan -> prepare_weights), and the same searched act scale as a per-layer K4 call."""
+    specs = synth.wan_registry(blocks=1)
+    ids = [0, 3, 6, 8, 9]  # q, o, cross v (512 text tokens), ffn.0, ffn.2
+    frames, rows = 3, 40
+    wts = calibrate.weighting_strategy("heuristic_exp", frames)
+    shard = calibrate.CalibrationShard(specs, ids, frames, rows, frame_weights=wts)
+    shard.setup()
+    recs = shard.run()
+    recs = shard.run()  # second step reuses the buffers (self-contained per step)
+    layers = shard.deployed_layers()
+    for rec, spec, w, x, L in zip(recs, shard.specs, shard.w, shard.x, layers):
+        rep = qb.analyze_layer(spec.name, w)
+        np.testing.assert_array_equal(rec.outliers, rep.aligned_outliers)
+        plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
+        ref = engine.prepare_weights(spec.name, w, plan)
+        assert torch.equal(L.wq, ref.wq)
+        np.testing.assert_array_equal(rec.scale_outlier, ref.scale_outlier64.cpu().numpy())
+        np.testing.assert_array_equal(rec.scale_normal, ref.scale_normal64.cpu().numpy())
+        s = calibrate.unpack_search(calibrate.scale_search_async([x], frames, wts).cpu().numpy()[0])
+        assert rec.act_scale == s.scale and rec.best_index == s.best_index
