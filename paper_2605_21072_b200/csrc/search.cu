@@ -34,6 +34,7 @@ constexpr int kHistThreads = 512;
 constexpr int kBlockBins = 256;
 constexpr int kNumBlocks = kBins / kBlockBins;  // 128
 constexpr int kEvalThreads = 512;
+constexpr int kEvalGroup = 4;  // blocks whose squared errors are staged together
 
 struct HistUnit {
   const uint16_t* x;  // first row of the unit
@@ -195,25 +196,36 @@ __global__ void __launch_bounds__(kEvalThreads)
   }
   __syncthreads();
 
-  // 3. per (candidate, block): partial sums for every frame, ascending bins
-  for (int item = threadIdx.x; item < nc * kNumBlocks; item += blockDim.x) {
-    const int c = item / kNumBlocks, blk = item - c * kNumBlocks;
-    const double s = s_scale[c];
-    double acc[QARVD_MAX_FRAMES];
-    for (int f = 0; f < F; ++f) acc[f] = 0.0;
-    if (blk_tot[blk]) {
-      for (int b = blk * kBlockBins; b < (blk + 1) * kBlockBins; ++b) {
-        if (!pooled[b]) continue;  // every frame count is 0: adding +0.0 is exact
-        const double e = fq_err(bin_value(b), s, cst.qmax);
-        for (int f = 0; f < F; ++f) {
-          const uint32_t cnt = job.hist[static_cast<int64_t>(f) * kBins + b];
-          acc[f] = __dadd_rn(acc[f], __dmul_rn(static_cast<double>(cnt), e));
+  // 3. per (frame, candidate, block): the block's bins summed in ascending order (the canonical
+  //    order; zero counts add +0.0 and are skipped).  Blocks go in groups of kEvalGroup: the
+  //    group's squared errors e_c(v_b) are computed once into shared memory, then one thread per
+  //    (frame, candidate, block) chain streams its frame's counts of that block.
+  double* e_sm = reinterpret_cast<double*>(part + static_cast<size_t>(F) * nc * kNumBlocks);
+  const int chains = F * nc * kEvalGroup;
+  for (int g0 = 0; g0 < kNumBlocks; g0 += kEvalGroup) {
+    for (int i = threadIdx.x; i < nc * kEvalGroup * kBlockBins; i += blockDim.x) {
+      const int c = i / (kEvalGroup * kBlockBins), r = i - c * (kEvalGroup * kBlockBins);
+      const int b = g0 * kBlockBins + r;
+      e_sm[i] = pooled[b] ? fq_err(bin_value(b), s_scale[c], cst.qmax) : 0.0;
+    }
+    __syncthreads();
+    for (int ch = threadIdx.x; ch < chains; ch += blockDim.x) {
+      const int gb = ch % kEvalGroup, fc = ch / kEvalGroup;
+      const int f = fc / nc, c = fc - f * nc;
+      const int blk = g0 + gb;
+      double acc = 0.0;
+      if (blk_tot[blk]) {
+        const uint32_t* h = job.hist + static_cast<int64_t>(f) * kBins + blk * kBlockBins;
+        const double* e = e_sm + (c * kEvalGroup + gb) * kBlockBins;
+        for (int b = 0; b < kBlockBins; ++b) {
+          const uint32_t cnt = __ldg(h + b);
+          if (cnt) acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(cnt), e[b]));
         }
       }
+      part[(f * nc + c) * kNumBlocks + blk] = acc;
     }
-    for (int f = 0; f < F; ++f) part[(f * nc + c) * kNumBlocks + blk] = acc[f];
+    __syncthreads();
   }
-  __syncthreads();
   // 4. per (frame, candidate): sum the block partials in order, / n_f
   for (int item = threadIdx.x; item < F * nc; item += blockDim.x) {
     double t = 0.0;
@@ -379,7 +391,8 @@ int scale_search_impl(const qarvd_search_job* jobs, int num_jobs, const double* 
   QARVD_LAUNCH_CHECK();
 
   const size_t eval_smem = kBins * sizeof(uint32_t) + kNumBlocks * sizeof(uint32_t) +
-                           static_cast<size_t>(F) * num_cand * kNumBlocks * sizeof(double);
+                           static_cast<size_t>(F) * num_cand * kNumBlocks * sizeof(double) +
+                           static_cast<size_t>(num_cand) * kEvalGroup * kBlockBins * sizeof(double);
   if (eval_smem > 227 * 1024)
     QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "scale_search: frames x candidates too large for one CTA");
   QARVD_CUDA_TRY(set_smem_attrs(eval_kernel, static_cast<int>(eval_smem)));
