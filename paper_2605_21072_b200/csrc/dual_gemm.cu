@@ -217,24 +217,6 @@ __device__ __forceinline__ uint64_t gelu2(uint64_t v) {
   return fma2(g, pk2(ex2_approx(-s0), ex2_approx(-s1)), pk2(fmaxf(v0, 0.f), fmaxf(v1, 0.f)));
 }
 
-// diagnostic (QARVD_GEMM_DEBUG & 128): gelu2's FMA-pipe work with the two MUFU ops replaced by
-// FMAs (wrong values; isolates the XU pipe)
-__device__ __forceinline__ uint64_t gelu2_nomufu(uint64_t v) {
-  const uint64_t w = mul2(v, pk2(0.8493218f, 0.8493218f));
-  float w0, w1, v0, v1;
-  upk2(w, w0, w1);
-  upk2(v, v0, v1);
-  const uint64_t aw = pk2(fabsf(w0), fabsf(w1));
-  const uint64_t t = fma2(pk2(0.272737481f, 0.272737481f), aw, pk2(1.0f, 1.0f));
-  uint64_t q = fma2(pk2(-0.624854695f, -0.624854695f), t, pk2(0.85547788f, 0.85547788f));
-  q = fma2(q, t, pk2(-0.836793392f, -0.836793392f));
-  q = fma2(q, t, pk2(0.167484654f, 0.167484654f));
-  q = fma2(q, t, pk2(-0.150019458f, -0.150019458f));
-  const uint64_t g = mul2(mul2(aw, t), q);
-  const uint64_t e = fma2(w, w, pk2(1.f, 1.f));
-  return fma2(g, e, pk2(fmaxf(v0, 0.f), fmaxf(v1, 0.f)));
-}
-
 // y = s_x * (s_wo*acc_o + s_wn*acc_n) (+ bias) [gelu], written back into rn as float bits.
 // Same per-element op order as the scalar form (oracle_epilogue_f32), on packed pairs;
 // specialised on (outlier slab?, bias?, gelu?) so every variant is straight-line code.
@@ -825,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint64_t v;
                 if (HB) v = fma2(sx2, tt, h ? pk2(sb4.z, sb4.w) : pk2(sb4.x, sb4.y));
                 else v = mul2(sx2, tt);
-                if (GL) v = (p.debug & 128) ? gelu2_nomufu(v) : gelu2(v);
+                if (GL) v = gelu2(v);
                 float y0, y1;
                 upk2(v, y0, y1);
                 an[i][e] = __float_as_uint(y0);
