@@ -50,12 +50,6 @@ int require_device() {
   return QARVD_OK;
 }
 
-int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
-                     int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
-                     const float* scale_wo, const float* scale_wn, const float* bias,
-                     int epilogue, int out_dtype, void* y, int64_t ldy, int32_t* acc_o,
-                     int32_t* acc_n, cudaStream_t stream, const double* sx64,
-                     const double* so64, const double* sn64);
 
 // ---- synthetic data ---------------------------------------------------------
 namespace {
