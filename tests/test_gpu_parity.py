@@ -846,3 +846,34 @@ def test_calibration_shard_sync_free_matches_per_layer(cuda):
         np.testing.assert_array_equal(rec.scale_normal, ref.scale_normal64.cpu().numpy())
         s = calibrate.unpack_search(calibrate.scale_search_async([x], frames, wts).cpu().numpy()[0])
         assert rec.act_scale == s.scale and rec.best_index == s.best_index
+
+
+# ---------------------------------------------------------------- W4A8 (BitwidthScheme w4a8)
+@pytest.mark.parametrize("wbits", [4, 6])
+def test_w4a8_weights_and_linear(cuda, ref_lib, wbits):
+    """Low-bit weights (the paper's W4A8 setting, BitwidthScheme): K5 at weight_bits = 4 (6)
+    gives the reference's build_plan scales (absmax / 7) and codes bit-for-bit; the codes are
+    stored as int8 (|code| <= 7) so K2 runs them unchanged -- at these token counts the GEMM is
+    tensor-bound and packed int4 storage (tensor.cpp:221-264) would only save weight bytes --
+    and its int32 accumulators and bf16 output stay bit-exact vs the oracle."""
+    n, k, m = 384, 1536, 700
+    plan = make_plan(k, 32, seed=4)
+    wb, w64 = bf16_values((n, k), seed=11, scale=1.0 / np.sqrt(k), heavy_cols=plan.outlier_indices)
+    ref = oracle.ref_build_plan_codes(w64, plan.outlier_indices, bits=wbits)
+    layer = engine.prepare_weights("w4", to_dev_bf16(wb), plan, bits=wbits)
+    np.testing.assert_array_equal(layer.scale_outlier64.cpu().numpy(), ref["scale_outlier"])
+    np.testing.assert_array_equal(layer.scale_normal64.cpu().numpy(), ref["scale_normal"])
+    np.testing.assert_array_equal(layer.wq.cpu().numpy().astype(np.int32), ref["wq"])
+    qmax = (1 << (wbits - 1)) - 1
+    assert int(layer.wq.abs().max()) <= qmax
+    xb, x64 = bf16_values((m, k), seed=12, heavy_cols=plan.outlier_indices, gamma=4.0)
+    xq, s32, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(xb), layer)
+    y, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, layer, dump_acc=True)
+    _, ao, an = oracle.kernel_b(xq.cpu().numpy(), layer.wq.cpu().numpy(), plan.k_outlier, s64.cpu().numpy(),
+                                layer.scale_outlier64.cpu().numpy(), layer.scale_normal64.cpu().numpy(),
+                                with_acc=True)
+    np.testing.assert_array_equal(acc_o.cpu().numpy(), ao)
+    np.testing.assert_array_equal(acc_n.cpu().numpy(), an)
+    y_ref = oracle.epilogue_f32(ao, an, True, s32.cpu().numpy(), layer.scale_outlier32.cpu().numpy(),
+                                layer.scale_normal32.cpu().numpy())
+    np.testing.assert_array_equal(dev_bits(y), y_ref)
