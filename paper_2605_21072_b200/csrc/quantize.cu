@@ -1729,7 +1729,6 @@ extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int n
   }
   // jobs the batched bf16 kernel serves; the rest take the per-layer path
   std::vector<WeightJobDev> fast;
-  int64_t max_n = 0, max_k = 0, max_kp = 0;
   for (int i = 0; i < num_jobs; ++i) {
     const qarvd_weight_job& j = jobs[i];
     if (int st = check_common(j.w, w_dtype, j.n, j.k, j.ldw, j.k_pad, bits, j.wq, j.ldq, j.gather)) return st;
@@ -1744,17 +1743,11 @@ extern "C" int qarvd_prepare_weights_batched(const qarvd_weight_job* jobs, int n
       fast.push_back(WeightJobDev{static_cast<const uint16_t*>(j.w), j.n, j.k, j.ldw, j.gather, j.k_pad,
                                   j.k_outlier, nullptr, j.wq, j.ldq, j.scale_outlier_f64, j.scale_normal_f64,
                                   j.scale_outlier_f32, j.scale_normal_f32});
-      max_n = j.n > max_n ? j.n : max_n;
-      max_k = j.k > max_k ? j.k : max_k;
-      max_kp = j.k_pad > max_kp ? j.k_pad : max_kp;
     } else if (j.n > 0) {
       if (int st = launch_rows<kWeightDual>(j.w, w_dtype, j.n, j.k, j.ldw, j.gather, j.k_pad, j.k_outlier,
                                             0.0, bits, j.wq, j.ldq, j.scale_outlier_f32, j.scale_outlier_f64,
                                             j.scale_normal_f32, j.scale_normal_f64, nullptr, s))
         return st;
-      if (err) {  // fold the per-layer check into the batch's error index
-        (void)0;
-      }
     }
   }
   return launch_prep_batched(fast, qmax, err, s);
