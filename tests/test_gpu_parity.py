@@ -877,3 +877,27 @@ def test_w4a8_weights_and_linear(cuda, ref_lib, wbits):
     y_ref = oracle.epilogue_f32(ao, an, True, s32.cpu().numpy(), layer.scale_outlier32.cpu().numpy(),
                                 layer.scale_normal32.cpu().numpy())
     np.testing.assert_array_equal(dev_bits(y), y_ref)
+
+
+def test_bench_json_contract(cuda):
+    """bench.py prints one JSON line with the driver's keys (short run, no calibration / stack)."""
+    import json
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "5", "--warmup", "3",
+                        "--no-calib", "--no-stack", "--no-cpu-baseline"], capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["steps"] == 5 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["gpu_launches"] >= 4 and d["e2e"]["h2d_bytes_per_step"] > 0
+    rf = d["roofline"]
+    assert rf["bound"] == "tensor" and 0 < rf["frac"] < 1 and rf["unit"] == "TOPS"
+    assert "workload" in d["config"]
