@@ -322,7 +322,7 @@ def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
     from paper_2605_21072_b200 import synth
     from paper_2605_21072_b200.pipeline import QuantizedChain, wan_stack_chain
 
-    chain = wan_stack_chain()
+    chain = wan_stack_chain(fuse_qkv=True)
     chain.x.copy_(synth.synth_activation(chain.m, synth.WAN_DIM, seed=11 + rank))
     chain.ctx.copy_(synth.synth_activation(synth.WAN_TEXT_LEN, synth.WAN_DIM, seed=13 + rank))
     chain.capture(parallel=True)
@@ -348,7 +348,7 @@ def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
     out = {"workload": "wan_stack_30blocks_300_linears_M4680_text512", "int_ops_per_forward": ops,
            "ms_per_forward": ms, "value": world * ops / (ms * 1e-3) / 1e12, "unit": "TOPS",
            "frac_of_peak": ops / (ms * 1e-3) / 1e12 / peak, "kernels_per_forward": chain.kernels_per_step(),
-           "graph": "one CUDA graph; dead-end layers (q, k, cross k/v) on two forked side branches",
+           "graph": "one CUDA graph; q/k/v fused into one dual-slab layer per block (engine.fuse_siblings, bit-identical); dead-end layers (cross k/v) on two forked side branches",
            "steps": steps, "l2": "flushed before every forward (weights 1.4 GB > L2 anyway)"}
     if rollouts > 0:
         per = max(1, rollouts // world)

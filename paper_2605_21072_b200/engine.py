@@ -354,3 +354,57 @@ def chain_forward_host(handles: Sequence[LinearHandle], x_host: torch.Tensor,
     _lib.call("qarvd_linear_chain_forward_host", arr, len(handles), x_host.data_ptr(),
               x_host.shape[0], y_host.data_ptr(), _stream())
     return y_host
+
+
+def fuse_siblings(name: str, layers: Sequence[QuantizedLayer]) -> QuantizedLayer:
+    """One dual-slab layer for sibling linears that read the same input (e.g. a block's
+    self-attention q, k, v), bit-identical per output column to the separate layers.
+
+    The fused K axis is [outlier slab of layer 0 | ... | outlier slab of layer L-1 | all d_in
+    columns in original order | pad]: every layer keeps its own outlier columns (and group
+    scales) in its own slab, holds zero codes in the other layers' slabs, and zero codes at its
+    own outlier columns of the shared normal part.  acc_o / acc_n of each output column are
+    therefore the same integer sums as in the separate layer (extra terms are 0 x code), and
+    the epilogue is per column.  One K1 (its gather duplicates the slab columns) and one K2
+    replace L of each; the K overhead is the sum of the slabs (~6% for three K_o = 32 slabs
+    at d_in = 1536)."""
+    if not layers:
+        raise _lib.InvalidArgument("fuse_siblings: no layers")
+    d_in = layers[0].in_dim
+    for L in layers:
+        if L.in_dim != d_in or L.gather_dev is None:
+            raise _lib.InvalidArgument("fuse_siblings: layers must share the input width and carry their gather")
+    dev = layers[0].wq.device
+    k_o = sum(L.k_outlier for L in layers)
+    k_pad = k_o + _round_up(d_in, 32)
+    gather = np.full(k_pad, -1, dtype=np.int32)
+    off = 0
+    for L in layers:
+        n_o = L.plan.outlier_count() if L.plan.enabled else 0
+        gather[off:off + n_o] = L.plan.gather[:n_o]
+        off += L.k_outlier
+    gather[k_o:k_o + d_in] = np.arange(d_in, dtype=np.int32)
+    n_tot = sum(L.out_dim for L in layers)
+    wq = torch.zeros((n_tot, k_pad), dtype=torch.int8, device=dev)
+    r0, off = 0, 0
+    for L in layers:
+        n = L.out_dim
+        g = L.plan.gather
+        if L.k_outlier:
+            wq[r0:r0 + n, off:off + L.k_outlier] = L.wq[:, :L.k_outlier]
+        # the layer's normal slab, scattered back to original column order
+        pos = np.nonzero(g[L.k_outlier:] >= 0)[0] + L.k_outlier
+        cols = torch.as_tensor(k_o + g[pos].astype(np.int64), device=dev)
+        wq[r0:r0 + n].index_copy_(1, cols, L.wq[:, torch.as_tensor(pos, device=dev)])
+        r0 += n
+        off += L.k_outlier
+    cat = lambda xs: torch.cat(xs, 0)
+    plan = DualScalePlan(name, True, d_in, np.zeros(0, dtype=np.int64), np.arange(d_in, dtype=np.int64),
+                         np.arange(d_in, dtype=np.uint32), gather, k_o, k_pad)
+    return QuantizedLayer(name, n_tot, d_in, plan, wq, cat([L.scale_outlier64 for L in layers]),
+                          cat([L.scale_normal64 for L in layers]), cat([L.scale_outlier32 for L in layers]),
+                          cat([L.scale_normal32 for L in layers]), torch.from_numpy(gather).to(dev),
+                          layers[0].act_granularity, layers[0].act_scale,
+                          None if all(L.bias is None for L in layers) else
+                          cat([L.bias if L.bias is not None else torch.zeros(L.out_dim, dtype=torch.float32, device=dev)
+                               for L in layers]))

@@ -14,10 +14,19 @@ from __future__ import annotations
 import dataclasses
 from typing import List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 
 from . import _lib
 from .engine import QuantizedLayer, _ptr, _stream
+
+
+def _is_permutation(layer: QuantizedLayer) -> bool:
+    """True when the layer's gather lists every input column exactly once (not the case for a
+    fused sibling layer, whose gather repeats the outlier columns in their slabs)."""
+    g = layer.plan.gather
+    v = g[g >= 0]
+    return len(v) == layer.in_dim and len(np.unique(v)) == layer.in_dim
 
 
 def fold_output_permutation(producer: QuantizedLayer,
@@ -80,7 +89,11 @@ class QuantizedChain:
         self.source_layers = list(layers)  # as given (before any output-permutation fold)
         self.m = m
         self.epilogues = list(epilogues) if epilogues is not None else [_lib.EPI_NONE] * len(layers)
-        self.inputs = list(inputs) if inputs is not None else list(range(-1, len(layers) - 1))
+        raw_inputs = list(inputs) if inputs is not None else list(range(-1, len(layers) - 1))
+        # an input may be a column slice (producer, first column, width) of a producer's output,
+        # e.g. the v part of a fused q/k/v layer (engine.fuse_siblings)
+        self.inputs = [j[0] if isinstance(j, tuple) else j for j in raw_inputs]
+        self.in_cols = [(j[1], j[2]) if isinstance(j, tuple) else None for j in raw_inputs]
         self.ms = list(ms) if ms is not None else [m] * len(self.layers)
         for i, j in enumerate(self.inputs):
             want = m if j == -1 else (ctx_rows if j == -2 else self.ms[j])
@@ -89,7 +102,8 @@ class QuantizedChain:
         self.source_ops = float(sum(2.0 * mi * L.out_dim * L.in_dim for mi, L in zip(self.ms, self.layers)))
         if fold:
             for j, i in enumerate(self.inputs):
-                if i >= 0 and self.inputs.count(i) == 1 and self.layers[j].gather_dev is not None:
+                if (i >= 0 and self.inputs.count(i) == 1 and self.in_cols[j] is None
+                        and self.layers[j].gather_dev is not None and _is_permutation(self.layers[j])):
                     self.layers[i], self.layers[j] = fold_output_permutation(self.layers[i], self.layers[j])
         dev = self.layers[0].wq.device
         # A folded consumer of a single producer gets that producer's per-row |y| max from
@@ -101,6 +115,7 @@ class QuantizedChain:
             for j, i in enumerate(self.inputs):
                 L = self.layers[j]
                 if (i >= 0 and L.gather_dev is None and self.inputs.count(i) == 1 and fuse_rowmax
+                        and self.in_cols[j] is None
                         and L.in_dim >= 512 and L.in_dim % 8 == 0):
                     self.stream_k1[j] = True
                     if L.act_granularity == _lib.ACT_PER_TOKEN:
@@ -123,7 +138,14 @@ class QuantizedChain:
 
     def _src(self, i):
         j = self.inputs[i]
-        return self.x if j == -1 else (self.ctx if j == -2 else self.y[j])
+        if j == -1:
+            return self.x
+        if j == -2:
+            return self.ctx
+        if self.in_cols[i] is not None:
+            c0, w = self.in_cols[i]
+            return self.y[j][:, c0:c0 + w]
+        return self.y[j]
 
     def launch(self, stream: Optional[int] = None, events: Optional[List] = None):
         """Enqueue K1 + K2 for every layer (2 kernels per layer).  With ``events`` (a list of
@@ -254,7 +276,8 @@ class QuantizedChain:
 
 
 def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
-                    text_len: Optional[int] = None, fuse_rowmax: bool = False) -> "QuantizedChain":
+                    text_len: Optional[int] = None, fuse_rowmax: bool = False,
+                    fuse_qkv: bool = False) -> "QuantizedChain":
     """BASELINE config 3: every quantized linear of a Wan-1.3B-shaped DiT stack for one chunk.
 
     Per block (toy_model.cpp:25-27 layer types, Wan2.1 shapes): self_attn.{q,k,v} read the
@@ -264,6 +287,8 @@ def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
     modulation and residual glue between the linears is not on the quantized path (the
     reference's own f64 glue) and is elided: each linear still sees its real
     shape, its own outlier plan (K3 on its synthetic weight) and a real per-token K1.
+    With ``fuse_qkv`` the three self-attention projections run as one fused dual-slab layer
+    (engine.fuse_siblings: bit-identical per output column) and o reads its v columns.
     """
     from . import engine, synth
     from .outlier import analyze_layer
@@ -273,20 +298,30 @@ def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
     text_len = synth.WAN_TEXT_LEN if text_len is None else text_len
     layers, inputs, epis, ms = [], [], [], []
     block_in = -1
+    qkv_types = ("self_attn.q", "self_attn.k", "self_attn.v")
     for b in range(blocks):
-        base = len(layers)
-        idx = {t: base + i for i, t in enumerate(synth.BLOCK_LAYER_TYPES)}
-        src = {"self_attn.q": block_in, "self_attn.k": block_in, "self_attn.v": block_in,
-               "self_attn.o": idx["self_attn.v"], "cross_attn.q": idx["self_attn.o"],
-               "cross_attn.k": -2, "cross_attn.v": -2, "cross_attn.o": idx["cross_attn.q"],
-               "ffn.0": idx["cross_attn.o"], "ffn.2": idx["ffn.0"]}
-        for t in synth.BLOCK_LAYER_TYPES:
-            spec = specs[idx[t]]
+        built = {}
+        for i, t in enumerate(synth.BLOCK_LAYER_TYPES):
+            spec = specs[b * len(synth.BLOCK_LAYER_TYPES) + i]
             w = synth.synth_weight(spec, seed=seed)
             rep = analyze_layer(spec.name, w)
             plan = engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)
-            layers.append(engine.prepare_weights(spec.name, w, plan))
+            built[t] = engine.prepare_weights(spec.name, w, plan)
             del w
+        order = list(synth.BLOCK_LAYER_TYPES)
+        if fuse_qkv:
+            built["self_attn.qkv"] = engine.fuse_siblings(f"block{b}.self_attn.qkv", [built[t] for t in qkv_types])
+            order = ["self_attn.qkv"] + [t for t in order if t not in qkv_types]
+        base = len(layers)
+        idx = {t: base + i for i, t in enumerate(order)}
+        d = synth.WAN_DIM
+        src = {"self_attn.q": block_in, "self_attn.k": block_in, "self_attn.v": block_in,
+               "self_attn.qkv": block_in,
+               "self_attn.o": (idx["self_attn.qkv"], 2 * d, d) if fuse_qkv else idx["self_attn.v"],
+               "cross_attn.q": idx["self_attn.o"], "cross_attn.k": -2, "cross_attn.v": -2,
+               "cross_attn.o": idx["cross_attn.q"], "ffn.0": idx["cross_attn.o"], "ffn.2": idx["ffn.0"]}
+        for t in order:
+            layers.append(built[t])
             inputs.append(src[t])
             epis.append(_lib.EPI_GELU if t == "ffn.0" else _lib.EPI_NONE)
             ms.append(text_len if src[t] == -2 else m)

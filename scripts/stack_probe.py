@@ -6,7 +6,8 @@ from paper_2605_21072_b200 import synth
 from paper_2605_21072_b200.pipeline import wan_stack_chain
 
 blocks = int(os.environ.get("BLOCKS", "4"))
-ch = wan_stack_chain(blocks=blocks, fuse_rowmax=os.environ.get("FUSE", "0") == "1")
+ch = wan_stack_chain(blocks=blocks, fuse_rowmax=os.environ.get("FUSE", "0") == "1",
+                     fuse_qkv=os.environ.get("FUSEQKV", "0") == "1")
 ch.x.copy_(synth.synth_activation(ch.m, 1536, seed=11))
 ch.ctx.copy_(synth.synth_activation(512, 1536, seed=13))
 g = ch.capture(timed=True)
@@ -21,7 +22,7 @@ kt = np.mean(np.asarray(kts[3:]), axis=0) * 1e3
 names = synth.BLOCK_LAYER_TYPES
 b = blocks - 1
 tot = 0
-for i, t in enumerate(names):
+for i, t in enumerate(names if len(ch.layers) == 10 * blocks else []):
     li = b * 10 + i
     L = ch.layers[li]
     print(f"{t:14s} M={ch.ms[li]:5d} {L.in_dim:5d}->{L.out_dim:5d} Ko={L.k_outlier:3d} gather={L.gather_dev is not None!s:5s} "

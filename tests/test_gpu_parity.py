@@ -901,3 +901,40 @@ def test_bench_json_contract(cuda):
     rf = d["roofline"]
     assert rf["bound"] == "tensor" and 0 < rf["frac"] < 1 and rf["unit"] == "TOPS"
     assert "workload" in d["config"]
+
+
+def test_fused_qkv_bitexact(cuda):
+    """engine.fuse_siblings (one dual-slab layer for q, k, v) gives bit-identical outputs per
+    column to the three separate layers, alone and inside the config-3 stack."""
+    from paper_2605_21072_b200.pipeline import wan_stack_chain
+    allspecs = synth.wan_registry(blocks=2)
+    specs = [allspecs[0], allspecs[11], allspecs[2]]  # q0, k1, v0: outlier plans and a plain one
+    Ls = []
+    for spec in specs:
+        w = synth.synth_weight(spec, seed=1)
+        rep = qb.analyze_layer(spec.name, w)
+        Ls.append(engine.prepare_weights(spec.name, w, engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers)))
+    F = engine.fuse_siblings("qkv", Ls)
+    x = synth.synth_activation(500, 1536, seed=5)
+    xq, s32, _ = engine.kernel_a_quantize_activation(x, F)
+    y = engine.kernel_b_gemm_dequant(xq, s32, F)
+    for i, L in enumerate(Ls):
+        xqi, si, _ = engine.kernel_a_quantize_activation(x, L)
+        assert torch.equal(si, s32)
+        yi = engine.kernel_b_gemm_dequant(xqi, si, L)
+        assert torch.equal(y[:, i * 1536:(i + 1) * 1536].view(torch.int16), yi.view(torch.int16))
+    a = wan_stack_chain(blocks=2, m=300, text_len=64)
+    b = wan_stack_chain(blocks=2, m=300, text_len=64, fuse_qkv=True)
+    xs = synth.synth_activation(300, 1536, seed=3)
+    cs = synth.synth_activation(64, 1536, seed=4)
+    for ch in (a, b):
+        ch.x.copy_(xs)
+        ch.ctx.copy_(cs)
+        ch.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(a.output.view(torch.int16), b.output.view(torch.int16))
+    assert a.int_ops() == b.int_ops()
+    b.capture(parallel=True)
+    b.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(a.output.view(torch.int16), b.output.view(torch.int16))
