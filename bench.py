@@ -353,7 +353,7 @@ def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
     if rollouts > 0:
         per = max(1, rollouts // world)
         chunks, tsteps = 7, 4
-        rc = QuantizedChain(chain.layers, per * chain.m, epilogues=chain.epilogues, inputs=chain.inputs,
+        rc = QuantizedChain(chain.layers, per * chain.m, epilogues=chain.epilogues, inputs=chain.raw_inputs,
                             ms=[per * mi for mi in chain.ms], ctx_rows=per * chain.ctx.shape[0])
         del chain
         rc.ctx.copy_(synth.synth_activation(rc.ctx.shape[0], synth.WAN_DIM, seed=17 + rank))

@@ -94,6 +94,7 @@ class QuantizedChain:
         # e.g. the v part of a fused q/k/v layer (engine.fuse_siblings)
         self.inputs = [j[0] if isinstance(j, tuple) else j for j in raw_inputs]
         self.in_cols = [(j[1], j[2]) if isinstance(j, tuple) else None for j in raw_inputs]
+        self.raw_inputs = raw_inputs
         self.ms = list(ms) if ms is not None else [m] * len(self.layers)
         for i, j in enumerate(self.inputs):
             want = m if j == -1 else (ctx_rows if j == -2 else self.ms[j])
@@ -287,8 +288,9 @@ def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
     modulation and residual glue between the linears is not on the quantized path (the
     reference's own f64 glue) and is elided: each linear still sees its real
     shape, its own outlier plan (K3 on its synthetic weight) and a real per-token K1.
-    With ``fuse_qkv`` the three self-attention projections run as one fused dual-slab layer
-    (engine.fuse_siblings: bit-identical per output column) and o reads its v columns.
+    With ``fuse_qkv`` the three self-attention projections (and the two cross-attention k / v
+    projections of the text tokens) run as one fused dual-slab layer each
+    (engine.fuse_siblings: bit-identical per output column); o reads the v columns.
     """
     from . import engine, synth
     from .outlier import analyze_layer
@@ -311,14 +313,17 @@ def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
         order = list(synth.BLOCK_LAYER_TYPES)
         if fuse_qkv:
             built["self_attn.qkv"] = engine.fuse_siblings(f"block{b}.self_attn.qkv", [built[t] for t in qkv_types])
-            order = ["self_attn.qkv"] + [t for t in order if t not in qkv_types]
+            built["cross_attn.kv"] = engine.fuse_siblings(f"block{b}.cross_attn.kv",
+                                                          [built["cross_attn.k"], built["cross_attn.v"]])
+            order = ["self_attn.qkv"] + [t for t in order if t not in qkv_types + ("cross_attn.k", "cross_attn.v")]
+            order.insert(order.index("cross_attn.o"), "cross_attn.kv")
         base = len(layers)
         idx = {t: base + i for i, t in enumerate(order)}
         d = synth.WAN_DIM
         src = {"self_attn.q": block_in, "self_attn.k": block_in, "self_attn.v": block_in,
                "self_attn.qkv": block_in,
                "self_attn.o": (idx["self_attn.qkv"], 2 * d, d) if fuse_qkv else idx["self_attn.v"],
-               "cross_attn.q": idx["self_attn.o"], "cross_attn.k": -2, "cross_attn.v": -2,
+               "cross_attn.q": idx["self_attn.o"], "cross_attn.k": -2, "cross_attn.v": -2, "cross_attn.kv": -2,
                "cross_attn.o": idx["cross_attn.q"], "ffn.0": idx["cross_attn.o"], "ffn.2": idx["ffn.0"]}
         for t in order:
             layers.append(built[t])
