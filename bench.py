@@ -701,7 +701,7 @@ def main():
             "adaround": adaround,
             "clocks": clk.summary(),
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N = 1 figure
             try:
                 import oracle
                 if oracle.ref_available():
