@@ -335,23 +335,41 @@ class CalibrationShard:
             for g, (rows, idx) in enumerate(self._groups.items()):
                 res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights,
                                          nonfinite_flag=self._flags[g:g + 1])
-                for j, i in enumerate(idx):
-                    search[i] = res[j]
+                search[g] = res
         rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w, out=self._rep)
         _lib.call("qarvd_prepare_weights_planned", self._jobs, len(self.specs), 8, None, _stream())
         main.wait_stream(self._side)
-        # results: one device -> host copy per field
+        # results: every field into one pinned host buffer with async copies, one sync
+        if not hasattr(self, "_pin"):
+            self._pin = {
+                "search": [torch.empty(search[g].shape, dtype=search[g].dtype).pin_memory()
+                           for g in range(len(self._groups))],
+                "flags": torch.empty(self._flags.shape, dtype=torch.int64).pin_memory(),
+                "counts": torch.empty(rep.counts.shape, dtype=torch.int32).pin_memory(),
+                "aligned": torch.empty(rep.aligned.shape, dtype=torch.int32).pin_memory(),
+                "so": torch.empty(self._so64.shape, dtype=torch.float64).pin_memory(),
+                "sn": torch.empty(self._sn64.shape, dtype=torch.float64).pin_memory(),
+            }
+        pin = self._pin
+        for g in range(len(self._groups)):
+            pin["search"][g].copy_(search[g], non_blocking=True)
+        pin["flags"].copy_(self._flags, non_blocking=True)
+        pin["counts"].copy_(rep.counts, non_blocking=True)
+        pin["aligned"].copy_(rep.aligned, non_blocking=True)
+        pin["so"].copy_(self._so64, non_blocking=True)
+        pin["sn"].copy_(self._sn64, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if (pin["flags"].numpy() != -1).any():
+            raise _lib.InvalidArgument("quantize: non-finite input in calibration samples")
         search_host = {}
-        for rows, idx in self._groups.items():
-            mat = torch.stack([search[i] for i in idx]).cpu().numpy()
+        for g, (rows, idx) in enumerate(self._groups.items()):
+            mat = pin["search"][g].numpy()
             for j, i in enumerate(idx):
                 search_host[i] = mat[j]
-        if (self._flags.cpu() != -1).any():
-            raise _lib.InvalidArgument("quantize: non-finite input in calibration samples")
-        counts = rep.counts.cpu().numpy()
-        aligned = rep.aligned.cpu().numpy()
-        so_all = self._so64.cpu().numpy()
-        sn_all = self._sn64.cpu().numpy()
+        counts = pin["counts"].numpy()
+        aligned = pin["aligned"].numpy()
+        so_all = pin["so"].numpy()
+        sn_all = pin["sn"].numpy()
         out = []
         nc = len(PERCENTILES)
         for i, spec in enumerate(self.specs):
