@@ -330,11 +330,25 @@ class CalibrationShard:
             self._prepare_buffers()
         main = torch.cuda.current_stream()
         self._side.wait_stream(main)
+        if not hasattr(self, "_k4"):  # launch tables of the K4 groups, built once
+            nc = len(PERCENTILES)
+            self._k4 = []
+            for g, (rows, idx) in enumerate(self._groups.items()):
+                res = torch.empty((len(idx), 3 * nc + 2), dtype=torch.float64, device=self.x[0].device)
+                jobs = (_lib.SearchJob * len(idx))()
+                for j, i in enumerate(idx):
+                    x = self.x[i]
+                    jobs[j].x, jobs[j].frames, jobs[j].rows = x.data_ptr(), self.frames, x.shape[0] // self.frames
+                    jobs[j].k, jobs[j].ldx, jobs[j].result = x.shape[1], x.stride(0), res[j].data_ptr()
+                pct = (_lib.ctypes.c_double * nc)(*PERCENTILES)
+                w = (None if self.weights is None else
+                     (_lib.ctypes.c_double * self.frames)(*[float(v) for v in self.weights]))
+                self._k4.append((jobs, len(idx), pct, nc, w, res))
         search = {}
         with torch.cuda.stream(self._side):
-            for g, (rows, idx) in enumerate(self._groups.items()):
-                res = scale_search_async([self.x[i] for i in idx], self.frames, self.weights,
-                                         nonfinite_flag=self._flags[g:g + 1])
+            for g, (jobs, nj, pct, nc, w, res) in enumerate(self._k4):
+                _lib.call("qarvd_scale_search_async", jobs, nj, pct, nc, w, 8,
+                          self._flags[g:g + 1].data_ptr(), _stream())
                 search[g] = res
         rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w, out=self._rep)
         _lib.call("qarvd_prepare_weights_planned", self._jobs, len(self.specs), 8, None, _stream())
