@@ -95,6 +95,9 @@ def ref():
                                            c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                                            c_int, c_int, ctypes.c_uint64, ctypes.c_char_p, c_void_p,
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+        _r.ref_toy_qarq.argtypes = [ctypes.c_char_p, c_int, c_void_p]
+        _r.ref_qarq_layer.argtypes = [ctypes.c_char_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]
         _r.ref_weighted_loss.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
                                          c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
@@ -412,3 +415,28 @@ def ref_calibrate_layer(w64, outliers, act_scale, x64, row_off, chunks, chunk_w,
                                   _p(codes), _p(sn), _p(so), _p(sc), _p(tr), _p(isn), _p(iso)))
     return dict(codes=codes, scale_normal=sn, scale_outlier=so, act_scale=sc[0], initial_loss=sc[1],
                 final_loss=sc[2], trace=tr[:iterations], init_scale_normal=isn, init_scale_outlier=iso)
+
+
+def ref_toy_qarq(path: str, iterations: int = 8) -> int:
+    """The reference's calibrated toy model saved as a QARQ file; returns the layer count."""
+    n = ctypes.c_int64()
+    _rc(ref().ref_toy_qarq(path.encode(), iterations, ctypes.byref(n)))
+    return n.value
+
+
+def ref_qarq_layer(path: str, idx: int):
+    """Layer idx of the reference's load_quantized_model(path)."""
+    meta = np.zeros(6, dtype=np.int64)
+    _rc(ref().ref_qarq_layer(path.encode(), idx, _p(meta), None, None, None, None, None))
+    pres, n, k = bool(meta[0]), int(meta[1]), int(meta[2])
+    out = dict(preserved=pres, out_dim=n, in_dim=k, enabled=bool(meta[3]), outlier_count=int(meta[4]),
+               bits=int(meta[5]))
+    if pres:
+        return out
+    wq = np.empty((n, k), dtype=np.int32)
+    sn, so = np.empty(n), np.empty(n)
+    perm = np.empty(k, dtype=np.uint32)
+    act = np.empty(2)
+    _rc(ref().ref_qarq_layer(path.encode(), idx, _p(meta), _p(wq), _p(sn), _p(so), _p(perm), _p(act)))
+    out.update(wq=wq, scale_normal=sn, scale_outlier=so, permutation=perm, act_scale=act[0], act_zero=act[1])
+    return out

@@ -379,3 +379,48 @@ extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const 
     for (size_t t = 0; t < r.trace.size(); ++t) trace[t] = r.trace[t];
   });
 }
+
+// The reference pipeline's own model file: ToyModel::build (two injections) -> calibrate_model
+// (heuristic_exp chunk weights, `iterations` AdaRound steps) -> save_quantized_model(path).
+extern "C" int ref_toy_qarq(const char* path, int iterations, int64_t* n_layers) {
+  return guarded([&] {
+    ToyModelConfig cfg;
+    cfg.injections = {{"ffn.2", 0.05, 8.0}, {"self_attn.q", 0.03, 6.0}};
+    const ToyModel model = ToyModel::build(cfg);
+    SensitivityProfile prof;
+    prof.alpha_raw.assign(cfg.chunks, 1.0);
+    prof.alpha_normalized = normalize_alpha(prof.alpha_raw);
+    const std::vector<double> w = weighting_strategy(prof, WeightingKind::heuristic_exp);
+    ModelCalibOptions opts;
+    opts.base.iterations = iterations;
+    opts.base.batch_size = 2;
+    const ModelCalibResult r = calibrate_model(model, w, opts);
+    save_quantized_model(path, r.qmodel);
+    *n_layers = static_cast<int64_t>(r.qmodel.layers.size());
+  });
+}
+
+// load_quantized_model(path) layer idx: meta = {preserved, out_dim, in_dim, enabled,
+// outlier_count, bits}; arrays sized by the caller from a first call with null arrays.
+extern "C" int ref_qarq_layer(const char* path, int64_t idx, int64_t* meta, int32_t* wq, double* s_n,
+                              double* s_o, uint32_t* perm, double* act) {
+  return guarded([&] {
+    const QuantizedModel qm = load_quantized_model(path);
+    const QuantizedLayer& l = qm.layers.at(static_cast<size_t>(idx));
+    meta[0] = l.preserved;
+    meta[1] = static_cast<int64_t>(l.out_dim);
+    meta[2] = static_cast<int64_t>(l.in_dim);
+    meta[3] = l.preserved ? 0 : l.plan.enabled;
+    meta[4] = l.preserved ? 0 : static_cast<int64_t>(l.plan.enabled ? l.plan.outlier_count() : 0);
+    meta[5] = l.preserved ? 16 : l.wq.bits;
+    if (l.preserved || !wq) return;
+    std::memcpy(wq, l.wq.data.data(), sizeof(int32_t) * l.wq.data.size());
+    for (size_t r = 0; r < l.out_dim; ++r) {
+      s_n[r] = l.plan.params_normal.scale[r];
+      s_o[r] = l.plan.params_outlier.scale[r];
+    }
+    std::memcpy(perm, l.plan.permutation.data(), sizeof(uint32_t) * l.in_dim);
+    act[0] = l.act.scale[0];
+    act[1] = l.act.zero_point[0];
+  });
+}

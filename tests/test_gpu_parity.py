@@ -1002,3 +1002,40 @@ def test_calibrate_layer_zero_iterations_and_large_batch(cuda, ref_lib):
         assert len(res.trace) == iters
         if iters == 0:
             assert res.final_loss == res.initial_loss
+
+
+def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path):
+    """A QARQ file written by the reference pipeline, loaded by qarq.load_qarq and uploaded by
+    qarq.to_device: K1 codes bit-exact vs the reference quantize with the file's static act
+    scale, and the bf16 K2 output within the stated tolerance of kernel_b_gemm_dequant."""
+    from paper_2605_21072_b200 import qarq
+    path = str(tmp_path / "toy.qarq")
+    oracle.ref_toy_qarq(path, iterations=4)
+    _, layers = qarq.load_qarq(path)
+    checked = 0
+    for i, L in enumerate(layers):
+        if L.preserved:
+            with pytest.raises(qb.InvalidArgument):
+                qarq.to_device(L)
+            continue
+        ref = oracle.ref_qarq_layer(path, i)
+        D = qarq.to_device(L)
+        xb, x64 = bf16_values((37, L.in_dim), seed=i, gamma=3.0)
+        xq, s32, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(xb), D, qb.ACT_PER_TENSOR,
+                                                           static_scale=ref["act_scale"])
+        perm = ref["permutation"]
+        codes, _ = oracle.ref_quantize(oracle.ref_permute(x64, perm, ref["enabled"]), per_token=False,
+                                       s=ref["act_scale"])
+        n_o = ref["outlier_count"]
+        xq_h = xq.cpu().numpy()
+        np.testing.assert_array_equal(xq_h[:, :n_o], codes[:, :n_o])
+        np.testing.assert_array_equal(xq_h[:, D.k_outlier:D.k_outlier + L.in_dim - n_o], codes[:, n_o:])
+        y_ref = oracle.ref_kernel_b(codes, ref["wq"], perm, n_o, ref["enabled"], np.full(37, ref["act_scale"]),
+                                    ref["scale_outlier"], ref["scale_normal"])
+        y, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, D, dump_acc=True)
+        mag = (np.abs(ref["act_scale"] * ref["scale_outlier"][None] * acc_o.cpu().numpy()) +
+               np.abs(ref["act_scale"] * ref["scale_normal"][None] * acc_n.cpu().numpy()))
+        yd = y.float().cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(yd - y_ref) <= 2.0 ** -8 * np.abs(y_ref) + 2.0 ** -22 * mag + 1e-30)
+        checked += 1
+    assert checked > 0

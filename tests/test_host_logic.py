@@ -104,3 +104,47 @@ def test_record_pack_roundtrip():
         np.testing.assert_array_equal(a.scale_normal, b.scale_normal)
         np.testing.assert_array_equal(a.scale_outlier, b.scale_outlier)
         np.testing.assert_array_equal(a.losses, b.losses)
+
+
+@pytest.fixture(scope="module")
+def toy_qarq(tmp_path_factory):
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    path = str(tmp_path_factory.mktemp("qarq") / "toy.qarq")
+    n = oracle.ref_toy_qarq(path, iterations=4)
+    return path, n
+
+
+def test_qarq_parser_matches_reference_loader(toy_qarq):
+    """qarq.load_qarq reads the reference's own saved model exactly as load_quantized_model
+    (engine.cpp:315-333): codes, f32 scales, permutation, act scale, preserved layers."""
+    import oracle
+    from paper_2605_21072_b200 import qarq
+    path, n = toy_qarq
+    header, layers = qarq.load_qarq(path)
+    assert len(layers) == n == len(header["layers"])
+    n_quant = 0
+    for i, L in enumerate(layers):
+        ref = oracle.ref_qarq_layer(path, i)
+        assert L.preserved == ref["preserved"] and (L.out_dim, L.in_dim) == (ref["out_dim"], ref["in_dim"])
+        if L.preserved:
+            assert L.fp_weight_bf16.shape == (L.out_dim, L.in_dim)
+            continue
+        n_quant += 1
+        np.testing.assert_array_equal(L.codes.astype(np.int32), ref["wq"])
+        np.testing.assert_array_equal(L.scale_normal.astype(np.float64), ref["scale_normal"])
+        if ref["enabled"]:
+            np.testing.assert_array_equal(L.scale_outlier.astype(np.float64), ref["scale_outlier"])
+            np.testing.assert_array_equal(L.permutation, ref["permutation"])
+            assert L.outlier_count == ref["outlier_count"]
+        assert np.float64(np.float32(L.act_scale)) == ref["act_scale"] and L.act_zero == ref["act_zero"]
+    assert n_quant > 0
+
+
+def test_qarq_bad_magic(tmp_path):
+    from paper_2605_21072_b200 import qarq, _lib
+    p = tmp_path / "bad.qarq"
+    p.write_bytes(b"NOPE" + b"\0" * 32)
+    with pytest.raises(_lib.QarvdError, match="bad magic"):
+        qarq.load_qarq(str(p))
