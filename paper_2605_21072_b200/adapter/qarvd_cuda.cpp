@@ -373,6 +373,96 @@ double weighted_loss(const std::vector<const CalibSample*>& batch, const Learnab
   return out;
 }
 
+CudaMinMaxFakeQuantProvider::CudaMinMaxFakeQuantProvider(const ToyModel& model, BitwidthScheme scheme,
+                                                         std::vector<std::string> keep_list)
+    : model_(model), scheme_(scheme), keep_list_(std::move(keep_list)) {
+  if (scheme_.is_lossless()) return;
+  for (const auto& spec : model.registry()) {
+    if (matches_keep_list(spec.name, keep_list_)) continue;
+    const Tensor& w = model.weight(spec.name);
+    const size_t n = w.rows(), k = w.cols();
+    // K5 on the f64 weight with the single-scale (identity) plan: per-row absmax / qmax scales
+    // (init_scale_minmax per_channel axis 0, quant.cpp:170-182) and nearest codes
+    DualScalePlan plan = build_single_scale_plan(spec.name, w, scheme_.weight_bits);
+    const Layout L = make_layout(plan, k);
+    DevBuf w_d(w.data(), w.size() * 8), g_d(L.gather.data(), L.gather.size() * 4);
+    DevBuf wq_d(n * L.k_pad), so_d(n * 8), sn_d(n * 8), err(8);
+    check(qarvd_prepare_weights(w_d.p, QARVD_F64, static_cast<int64_t>(n), static_cast<int64_t>(k),
+                                static_cast<int64_t>(k), g_d.as<int32_t>(), static_cast<int64_t>(L.k_pad), 0,
+                                scheme_.weight_bits, wq_d.as<int8_t>(), static_cast<int64_t>(L.k_pad),
+                                so_d.as<double>(), sn_d.as<double>(), nullptr, nullptr, err.as<int64_t>(), nullptr));
+    std::vector<int8_t> wq(n * L.k_pad);
+    check_cuda(cudaMemcpy(wq.data(), wq_d.p, wq.size(), cudaMemcpyDeviceToHost));
+    check_cuda(cudaMemcpy(plan.params_normal.scale.data(), sn_d.p, n * 8, cudaMemcpyDeviceToHost));
+    plan.params_outlier = plan.params_normal;
+    QuantizedLayer ql;
+    ql.name = spec.name;
+    ql.out_dim = n;
+    ql.in_dim = k;
+    ql.preserved = false;
+    ql.plan = plan;
+    ql.wq.shape = {n, k};
+    ql.wq.bits = scheme_.weight_bits;
+    ql.wq.data.resize(n * k);
+    for (size_t r = 0; r < n; ++r)
+      for (size_t c = 0; c < k; ++c) ql.wq.data[r * k + c] = wq[r * L.k_pad + L.pos[c]];
+    layers_.emplace(spec.name, std::make_shared<DeviceLayer>(ql));
+  }
+}
+
+CudaMinMaxFakeQuantProvider::~CudaMinMaxFakeQuantProvider() = default;
+
+Tensor CudaMinMaxFakeQuantProvider::forward(const std::string& layer, const Tensor& x) const {
+  if (scheme_.is_lossless() || matches_keep_list(layer, keep_list_)) return matmul_nt(x, model_.weight(layer));
+  const DeviceLayer& L = *layers_.at(layer);
+  const size_t m = x.rows();
+  // per-tensor minmax scale = max over rows of K1's exact per-row scales fl(absmax_r / qmax)
+  // (rounding is monotone, so it equals fl(absmax / qmax), quant.cpp:165-168)
+  DevBuf xd(x.data(), x.size() * 8), xq(m * L.layout.k_pad + 16), s_rows(m * 8), err(8);
+  check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(x.cols()),
+                           static_cast<int64_t>(x.cols()), L.gather_dev->as<int32_t>(),
+                           static_cast<int64_t>(L.layout.k_pad), QARVD_ACT_PER_TOKEN, 0.0,
+                           scheme_.activation_bits, xq.as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
+                           nullptr, s_rows.as<double>(), err.as<int64_t>(), nullptr));
+  std::vector<double> sr(m);
+  check_cuda(cudaMemcpy(sr.data(), s_rows.p, m * 8, cudaMemcpyDeviceToHost));
+  double s = 0.0;
+  for (double v : sr) s = std::max(s, v);
+  QuantParams act = QuantParams::per_tensor_symmetric(scheme_.activation_bits, s);
+  DevBuf sx(m * 8);
+  quantize_to_device(x, L.layout, *L.gather_dev, act, xq, sx, m);
+  return gemm_to_host(L, xq, sx, m);
+}
+
+SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme scheme,
+                                       const std::vector<uint64_t>& seeds) {
+  if (seeds.empty()) throw std::invalid_argument("profile_sensitivity: need at least one seed");
+  const size_t n_chunks = model.config().chunks;
+  const FpProvider fp(model);
+  const CudaMinMaxFakeQuantProvider quant(model, scheme);
+  std::vector<Rollout> references(seeds.size());
+  for (size_t s = 0; s < seeds.size(); ++s)
+    references[s] = run_rollout(model.config(), fp, nullptr, QuantTarget::none, 0, seeds[s]);
+  std::vector<std::vector<double>> per_seed(seeds.size(), std::vector<double>(n_chunks, 0.0));
+  for (size_t s = 0; s < seeds.size(); ++s)
+    for (size_t i = 0; i < n_chunks; ++i) {
+      const Rollout probe = run_rollout(model.config(), fp, &quant, QuantTarget::only_chunk, i + 1, seeds[s]);
+      per_seed[s][i] = latent_mse(references[s], probe);
+    }
+  SensitivityProfile profile;
+  profile.scheme = scheme;
+  profile.seeds = seeds;
+  profile.per_seed = std::move(per_seed);
+  profile.alpha_raw.assign(n_chunks, 0.0);
+  for (size_t i = 0; i < n_chunks; ++i) {
+    double acc = 0.0;
+    for (size_t s = 0; s < seeds.size(); ++s) acc += profile.per_seed[s][i];
+    profile.alpha_raw[i] = acc / static_cast<double>(seeds.size());
+  }
+  profile.alpha_normalized = normalize_alpha(profile.alpha_raw);
+  return profile;
+}
+
 LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, const QuantParams& act_init,
                                  const std::vector<const CalibSample*>& samples,
                                  const std::vector<double>& chunk_weights, const CalibConfig& cfg) {

@@ -26,6 +26,7 @@
 #include "qarvd/engine.hpp"
 #include "qarvd/outlier.hpp"
 #include "qarvd/quant.hpp"
+#include "qarvd/sensitivity.hpp"
 #include "qarvd/tensor.hpp"
 #include "qarvd/toy_model.hpp"
 
@@ -88,6 +89,29 @@ class CudaQuantizedProvider : public LinearProvider {
   const QuantizedModel& qm_;
   std::map<std::string, std::shared_ptr<DeviceLayer>> layers_;
 };
+
+// MinMaxFakeQuantProvider (toy_model.cpp:306-325) on the tensor cores: fake_quant(x, per-tensor
+// minmax) . fake_quant(W, per-channel minmax)^T = s_x * s_w[j] * (codes_x . codes_w), i.e. a
+// single-slab int8 GEMM with the reference's f64 epilogue.  Weight codes / scales come from K5
+// (single-scale plan), the activation scale from K1's exact per-row scales (max over rows).
+class CudaMinMaxFakeQuantProvider : public LinearProvider {
+ public:
+  CudaMinMaxFakeQuantProvider(const ToyModel& model, BitwidthScheme scheme,
+                              std::vector<std::string> keep_list = default_keep_list());
+  ~CudaMinMaxFakeQuantProvider() override;
+  Tensor forward(const std::string& layer, const Tensor& x) const override;
+
+ private:
+  const ToyModel& model_;
+  BitwidthScheme scheme_;
+  std::vector<std::string> keep_list_;
+  std::map<std::string, std::shared_ptr<DeviceLayer>> layers_;
+};
+
+// profile_sensitivity (sensitivity.cpp:29-66) with the probes' quantized linears served by
+// CudaMinMaxFakeQuantProvider (the full-precision references stay on FpProvider).
+SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme scheme,
+                                       const std::vector<uint64_t>& seeds);
 
 // run_quantized (engine.cpp:175-178) with the CUDA provider.
 Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed);

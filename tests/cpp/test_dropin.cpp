@@ -186,6 +186,18 @@ int main() {
     EXPECT(worst <= 1e-3, "calibrate_model scales");
   }
 
+  // ---- profile_sensitivity with the fake-quant probes on the tensor cores
+  {
+    const BitwidthScheme sch = BitwidthScheme::parse("w8a8");
+    const SensitivityProfile a = qarvd::profile_sensitivity(model, sch, {5000, 5001});
+    const SensitivityProfile b = qarvd::cuda::profile_sensitivity(model, sch, {5000, 5001});
+    double worst = 0.0;
+    for (size_t i = 0; i < a.alpha_raw.size(); ++i)
+      worst = std::max(worst, std::fabs(a.alpha_raw[i] - b.alpha_raw[i]) / std::fabs(a.alpha_raw[i]));
+    std::printf("profile_sensitivity: %zu chunks, worst alpha_raw rel diff %.3e\n", a.alpha_raw.size(), worst);
+    EXPECT(worst <= 1e-6, "profile_sensitivity alpha within 1e-6");
+  }
+
   // ---- the seam: run_rollout with the CUDA provider vs the reference int engine
   for (uint64_t seed : {5000ull, 5001ull}) {
     const Rollout ref = run_quantized(qm, seed, Engine::int_kernels);
