@@ -32,3 +32,17 @@ print("CTA duration us: all p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(d,
 print("CTAs holding a pow2 row: n=%d mean %.2f  | others mean %.2f" % (cta_pow2.sum(), d[cta_pow2].mean(), d[~cta_pow2].mean()))
 slow = np.argsort(d)[-10:]
 print("10 slowest CTAs:", [(int(c), round(float(d[c]), 2), bool(cta_pow2[c])) for c in slow])
+t = trace.view(-1, 3).cpu().numpy()[:1170]
+sm = t[:, 2]
+st = (t[:, 0] - t[:, 0].min()) / 1e3
+en = (t[:, 1] - t[:, 0].min()) / 1e3
+print("start spread us:", np.percentile(st, [0, 50, 100]).round(2), " end:", np.percentile(en, [0, 50, 90, 99, 100]).round(2))
+per_sm_end = np.zeros(148); per_sm_n = np.zeros(148)
+for s_, e_ in zip(sm, en):
+    per_sm_end[int(s_)] = max(per_sm_end[int(s_)], e_); per_sm_n[int(s_)] += 1
+order = np.argsort(per_sm_end)[::-1][:10]
+print("latest-finishing SMs (sm, end us, ctas):", [(int(i), round(float(per_sm_end[i]), 2), int(per_sm_n[i])) for i in order])
+print("SM end percentiles:", np.percentile(per_sm_end, [0, 50, 90, 100]).round(2))
+# durations by CTA index order (launch order)
+d_last = en - st
+print("dur by CTA index quartile:", [round(float(np.median(d_last[q * 292:(q + 1) * 292])), 2) for q in range(4)])
