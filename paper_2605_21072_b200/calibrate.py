@@ -197,43 +197,56 @@ def unpack_records(buf: np.ndarray) -> List[LayerRecord]:
     return out
 
 
-def allgather_records(local: Sequence[LayerRecord], group=None, device=None) -> List[LayerRecord]:
-    """One all-gather of the packed per-layer records (NCCL on GPU, gloo on CPU).
-    Payloads are padded to the largest rank's size; the result is sorted by layer index."""
+def allgather_bytes(payload: np.ndarray, group=None, device=None) -> List[np.ndarray]:
+    """One all-gather of a per-rank byte payload (NCCL on GPU, gloo on CPU): the sizes first,
+    then the payloads padded to the largest.  Returns every rank's bytes, in rank order."""
     import torch.distributed as dist
 
-    payload = pack_records(local)
+    payload = np.ascontiguousarray(payload).view(np.uint8).reshape(-1)
     dev = device if device is not None else torch.device("cpu")
     world = dist.get_world_size(group)
     size = torch.tensor([payload.size], dtype=torch.int64, device=dev)
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, size, group=group)
     sizes = [int(s.item()) for s in sizes]
-    cap = max(max(sizes), 1)
-    buf = torch.zeros(cap, dtype=torch.float64, device=dev)
-    buf[:payload.size] = torch.from_numpy(payload).to(dev)
-    gathered = torch.empty(world * cap, dtype=torch.float64, device=dev)
+    cap = max(max(sizes), 8)
+    buf = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    buf[:payload.size] = torch.from_numpy(payload.copy()).to(dev)
+    gathered = torch.empty(world * cap, dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(gathered, buf, group=group)
     g = gathered.cpu().numpy()
-    recs: List[LayerRecord] = []
-    for r in range(world):
-        recs.extend(unpack_records(g[r * cap: r * cap + sizes[r]]))
+    return [g[r * cap: r * cap + sizes[r]].copy() for r in range(world)]
+
+
+def allgather_records(local: Sequence, group=None, device=None, unpack=None) -> List:
+    """All-gather of packed per-layer records (``LayerRecord`` by default; any record with
+    ``.index`` and ``.pack()`` plus its ``unpack`` over the concatenated bytes), sorted by
+    layer index."""
+    unpack = unpack if unpack is not None else (lambda b: unpack_records(b.view(np.float64)))
+    payload = (np.concatenate([np.ascontiguousarray(r.pack()).view(np.uint8) for r in local])
+               if local else np.zeros(0, dtype=np.uint8))
+    recs: List = []
+    for b in allgather_bytes(payload, group=group, device=device):
+        recs.extend(unpack(b))
     recs.sort(key=lambda r: r.index)
     return recs
 
 
-def calibrate_model_sharded(costs: Sequence[float], compute: Callable[[List[int]], List[LayerRecord]],
-                            rank: int = 0, world: int = 1, group=None, device=None) -> List[LayerRecord]:
+def calibrate_model_sharded(costs: Sequence[float], compute: Callable[[List[int]], List],
+                            rank: int = 0, world: int = 1, group=None, device=None,
+                            unpack=None) -> List:
     """calibrate_model's layer loop (calibrate.cpp:440-484) over `world` ranks.
 
     ``compute(layer_ids)`` runs this rank's layers (on its GPU) and returns their
     records; one all-gather assembles the full result.  The output is identical
-    for every world size (slot-indexed by layer, as the reference's parallel_for)."""
+    for every world size (slot-indexed by layer, as the reference's parallel_for).
+    ``unpack`` selects the record type (default ``LayerRecord``; ``unpack_calib_records``
+    for the AdaRound results of ``calibrate_model_adaround``)."""
     assign = lpt_assign(costs, world)
     local = compute(assign[rank]) if assign[rank] else []
     if world == 1:
         return sorted(local, key=lambda r: r.index)
-    return allgather_records(local, group=group, device=device)
+    return allgather_records(local, group=group, device=device, unpack=unpack)
 
 
 # ---------------------------------------------------------------------------
@@ -509,3 +522,91 @@ def calibrate_layer(name: str, w: torch.Tensor, plan, scale_normal: torch.Tensor
     sc = scal.cpu().numpy()
     return LayerCalibResult(name, sn_out.cpu().numpy(), so_out.cpu().numpy(), codes.cpu().numpy(),
                             float(sc[0]), float(sc[1]), float(sc[2]), trace.cpu().numpy()[:cfg.iterations])
+
+
+# ---------------------------------------------------------------------------
+# calibrate_model with AdaRound per layer, sharded over ranks (calibrate.cpp:440-484)
+
+@dataclass
+class CalibRecord:
+    """One quantized layer's AdaRound result (LayerCalibResult) under its registry slot, as
+    it travels in the all-gather: a little-endian byte record
+    [i64 index, n, k, trace_len, name_len | f64 act_scale, initial, final | f64 scale_normal[n] |
+    f64 scale_outlier[n] | f64 trace | i8 codes[n*k] | name | pad to 8]."""
+
+    index: int
+    result: LayerCalibResult
+
+    def pack(self) -> np.ndarray:
+        r = self.result
+        n, k = r.codes.shape
+        name = r.layer.encode()
+        head = np.asarray([self.index, n, k, len(r.trace), len(name)], dtype="<i8")
+        f = np.concatenate([np.asarray([r.act_scale, r.initial_loss, r.final_loss]),
+                            r.scale_normal, r.scale_outlier, r.trace]).astype("<f8")
+        body = b"".join([head.tobytes(), f.tobytes(), np.ascontiguousarray(r.codes, dtype=np.int8).tobytes(),
+                         name])
+        return np.frombuffer(body + b"\0" * (-len(body) % 8), dtype=np.uint8)
+
+    @staticmethod
+    def unpack(buf: np.ndarray, pos: int):
+        idx, n, k, nt, nl = (int(v) for v in np.frombuffer(buf, dtype="<i8", count=5, offset=pos))
+        p = pos + 40
+        f = np.frombuffer(buf, dtype="<f8", count=3 + 2 * n + nt, offset=p).copy()
+        p += 8 * len(f)
+        codes = np.frombuffer(buf, dtype=np.int8, count=n * k, offset=p).reshape(n, k).copy()
+        p += n * k
+        name = bytes(buf[p:p + nl]).decode()
+        p += nl
+        p += -(p - pos) % 8
+        res = LayerCalibResult(name, f[3:3 + n], f[3 + n:3 + 2 * n], codes, float(f[0]), float(f[1]),
+                               float(f[2]), f[3 + 2 * n:])
+        return CalibRecord(idx, res), p
+
+
+def unpack_calib_records(buf: np.ndarray) -> List[CalibRecord]:
+    buf = np.ascontiguousarray(buf).view(np.uint8)
+    out, pos = [], 0
+    while pos < len(buf):
+        r, pos = CalibRecord.unpack(buf, pos)
+        out.append(r)
+    return out
+
+
+def adaround_cost(n: int, k: int, rows: int, iterations: int) -> float:
+    """LPT weight of one layer's AdaRound: its f64 GEMM work, iterations x rows x n x k (the
+    forward X.W_soft^T and the weight gradient X^T.E dominate K7)."""
+    return float(max(1, iterations)) * rows * n * k
+
+
+def calibrate_model_adaround(layers: Sequence, samples_of: Callable[[int], Sequence],
+                             chunk_weights: Sequence[float], cfg: Optional["_lib.CalibConfig"] = None,
+                             rank: int = 0, world: int = 1, group=None, device=None,
+                             act_bits: int = 8, w_bits: int = 8,
+                             sample_rows: Optional[Sequence[int]] = None) -> List[CalibRecord]:
+    """calibrate_model's AdaRound loop (calibrate.cpp:440-484: calibrate_layer per quantized
+    layer, independent across layers) over ``world`` GPUs: LPT on ``adaround_cost``, each rank
+    runs K7 for its layers, one all-gather of the codes, learned scales and traces.
+
+    ``layers[i]``: (name, w [n x k] device tensor, plan, scale_normal, scale_outlier, act_scale)
+    — the inputs of calibrate_layer; ``samples_of(i)``: that layer's (x, chunk) samples on this
+    rank's device, called only for this rank's layers; ``sample_rows[i]``: its total sample rows
+    for the LPT weights (default: equal).  Identical result for every world size (slot-indexed as the reference's
+    parallel_for; K7 is deterministic per layer)."""
+    cfg = cfg if cfg is not None else _lib.CalibConfig()
+    costs = []
+    for i, L in enumerate(layers):
+        n, k = L[1].shape
+        rows = int(sample_rows[i]) if sample_rows is not None else 1
+        costs.append(adaround_cost(n, k, rows, cfg.iterations))
+
+    def compute(ids):
+        out = []
+        for i in ids:
+            name, w, plan, sn, so, act = layers[i]
+            out.append(CalibRecord(i, calibrate_layer(name, w, plan, sn, so, act, samples_of(i),
+                                                      chunk_weights, cfg, act_bits, w_bits)))
+        return out
+
+    return calibrate_model_sharded(costs, compute, rank, world, group=group, device=device,
+                                   unpack=unpack_calib_records)

@@ -793,6 +793,42 @@ def test_calibrate_layer_errors(cuda):
         calibrate.calibrate_layer("l", w, plan, s, s, 0.01, [(x, 2)], [1.0])
 
 
+def test_calibrate_model_adaround_matches_reference_layers(cuda, ref_lib):
+    """calibrate_model's AdaRound loop through the sharded driver (world 1; world 2 of the same
+    records is tests/test_sharding_gloo.py): every slot equals the reference calibrate_layer of
+    that layer — codes bit-exact, scales / final loss within 1e-9."""
+    specs = [(24, 96, 4, "blk0.attn.q"), (40, 64, 0, "blk0.ffn.0"), (16, 128, 8, "blk0.ffn.2")]
+    rows = [17, 9, 22]
+    chunks = np.array([1, 2, 2])
+    cw = calibrate.weighting_strategy("heuristic_exp", 2)
+    cfg = qb._lib.CalibConfig(iterations=6, batch_size=2, seed=5)
+    layers, samples, refs = [], [], []
+    for li, (n, k, n_out, name) in enumerate(specs):
+        r = np.random.default_rng(100 + li)
+        outl = np.sort(r.choice(k, n_out, replace=False)) if n_out else np.zeros(0, np.int64)
+        _, w = bf16_values((n, k), seed=li + 7, scale=1.0 / np.sqrt(k), heavy_cols=outl if n_out else None)
+        _, x = bf16_values((sum(rows), k), seed=li + 70, heavy_cols=outl if n_out else None, gamma=3.0)
+        row_off = np.concatenate([[0], np.cumsum(rows)])
+        act = float(np.abs(x).max() / 127.0)
+        ref = oracle.ref_calibrate_layer(w, outl, act, x, row_off, chunks, cw, 6, 2, 5, name)
+        refs.append(ref)
+        xd = torch.from_numpy(x).cuda()
+        samples.append([(xd[row_off[i]:row_off[i + 1]], int(chunks[i])) for i in range(len(rows))])
+        layers.append((name, torch.from_numpy(w).cuda(), engine.build_plan(name, k, outl),
+                       torch.from_numpy(ref["init_scale_normal"]).cuda(),
+                       torch.from_numpy(ref["init_scale_outlier"]).cuda(), act))
+    got = calibrate.calibrate_model_adaround(layers, lambda i: samples[i], cw, cfg,
+                                             sample_rows=[sum(rows)] * 3)
+    assert [g.index for g in got] == [0, 1, 2]
+    for g, ref, (n, k, n_out, name) in zip(got, refs, specs):
+        assert g.result.layer == name and g.result.codes.shape == (n, k)
+        np.testing.assert_array_equal(g.result.codes.astype(np.int32), ref["codes"])
+        np.testing.assert_allclose(g.result.scale_normal, ref["scale_normal"], rtol=1e-9)
+        assert np.isclose(g.result.final_loss, ref["final_loss"], rtol=1e-9)
+        back = calibrate.unpack_calib_records(g.pack())[0]
+        np.testing.assert_array_equal(back.result.codes, g.result.codes)
+
+
 @pytest.mark.parametrize("m,n,k,n_out,epi", [(4680, 8960, 1536, 32, qb.EPI_GELU), (4680, 1536, 8960, 188, qb.EPI_NONE),
                                              (4680, 1536, 1536, 32, qb.EPI_NONE), (1000, 8960, 1536, 0, qb.EPI_GELU)])
 def test_k2_deployed_path_full_shape(cuda, m, n, k, n_out, epi):

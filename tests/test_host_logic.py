@@ -106,6 +106,38 @@ def test_record_pack_roundtrip():
         np.testing.assert_array_equal(a.losses, b.losses)
 
 
+def _fake_calib_record(i, rng):
+    n, k, nt = int(rng.integers(1, 9)), int(rng.integers(1, 13)), int(rng.integers(0, 6))
+    res = calibrate.LayerCalibResult(f"blocks.{i}.attn.q" + "x" * (i % 4), rng.random(n), rng.random(n),
+                                     rng.integers(-128, 128, (n, k)).astype(np.int8), rng.random(),
+                                     rng.random(), rng.random(), rng.random(nt))
+    return calibrate.CalibRecord(i, res)
+
+
+def test_calib_record_pack_roundtrip():
+    rng = np.random.default_rng(1)
+    recs = [_fake_calib_record(i, rng) for i in range(9)]
+    packed = np.concatenate([r.pack() for r in recs])
+    assert packed.dtype == np.uint8 and all(len(r.pack()) % 8 == 0 for r in recs)
+    back = calibrate.unpack_calib_records(packed)
+    assert len(back) == 9
+    for a, b in zip(recs, back):
+        ra, rb = a.result, b.result
+        assert a.index == b.index and ra.layer == rb.layer
+        assert (ra.act_scale, ra.initial_loss, ra.final_loss) == (rb.act_scale, rb.initial_loss, rb.final_loss)
+        np.testing.assert_array_equal(ra.codes, rb.codes)
+        np.testing.assert_array_equal(ra.scale_normal, rb.scale_normal)
+        np.testing.assert_array_equal(ra.scale_outlier, rb.scale_outlier)
+        np.testing.assert_array_equal(ra.trace, rb.trace)
+
+
+def test_adaround_cost_orders_lpt():
+    costs = [calibrate.adaround_cost(n, k, r, 100) for n, k, r in ((1536, 8960, 10), (1536, 1536, 10),
+                                                                  (8960, 1536, 10), (1536, 1536, 40))]
+    assert costs[0] == costs[2] and costs[3] == 4 * costs[1]
+    assert calibrate.lpt_assign(costs, 2) == [[0, 3], [1, 2]]
+
+
 @pytest.fixture(scope="module")
 def toy_qarq(tmp_path_factory):
     import oracle
