@@ -9,8 +9,10 @@
 // after warm-up, and bias-corrected Adam with a cosine-annealed learning rate.
 //
 // Everything stays in f64 like the reference, so the trajectory follows it to rounding:
-// the three products per sample (prediction X^ What^T - target, dL/dWhat = D^T X^,
-// dL/dX^ = D What) are cuBLAS DGEMMs (plain library GEMMs); every elementwise step,
+// the three products (prediction X^ What^T - target, dL/dWhat = D^T X^, dL/dX^ = D What) are
+// cuBLAS DGEMMs (plain library GEMMs), each over the batch's samples stacked along the rows
+// (one GEMM per product, not per sample: 1560-row GEMMs leave DGEMM at 31 of its 35 TF/s);
+// every elementwise step,
 // reduction and Adam update is a kernel here with the reference's per-element formula, and
 // every reduction runs in a fixed order (deterministic).  The target X_s W^T is computed
 // once per sample (W is fixed during calibration).  The host only replays the reference's
@@ -131,35 +133,64 @@ __global__ void xhat_kernel(const double* x, int64_t count, const double* log_sa
   }
 }
 
-// fixed-order partial sums of a[i]*b[i] (b = nullptr: a[i]^2): block p sums a contiguous range
+// fixed-order block sums: block p of the grid reduces the contiguous range p of [0, count)
+// (four independent accumulators per thread, then a shuffle tree) -> partial[p]
 constexpr int kRedBlocks = 296;
-__global__ void __launch_bounds__(kT) dot_partial_kernel(const double* a, const double* b, int64_t count,
-                                                          double* partial) {
+constexpr int kMaxGroup = 16;  // samples stacked into one GEMM
+__device__ __forceinline__ double block_sum(double acc) {
+  __shared__ double red[kT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kT / 32; ++w) t += red[w];
+  return t;
+}
+// partial[p] = sum a[i]*b[i] over block p's range (b = nullptr: a[i]^2); with scale != 0 the
+// range is also rescaled in place (a[i] *= scale, with rescale) after being read
+__global__ void __launch_bounds__(kT) dot_partial_kernel(double* a, const double* b, int64_t count,
+                                                          int rescale, double scale, double* partial) {
   const int64_t per = (count + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = lo + per < count ? lo + per : count;
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kT) {
-    const double av = a[i];
-    acc += b ? av * b[i] : av * av;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = lo + threadIdx.x;
+  for (; i + 3 * kT < hi; i += 4 * kT) {
+    const double v0 = a[i], v1 = a[i + kT], v2 = a[i + 2 * kT], v3 = a[i + 3 * kT];
+    if (b) {
+      a0 += v0 * b[i], a1 += v1 * b[i + kT], a2 += v2 * b[i + 2 * kT], a3 += v3 * b[i + 3 * kT];
+    } else {
+      a0 += v0 * v0, a1 += v1 * v1, a2 += v2 * v2, a3 += v3 * v3;
+    }
+    if (rescale) a[i] = v0 * scale, a[i + kT] = v1 * scale, a[i + 2 * kT] = v2 * scale, a[i + 3 * kT] = v3 * scale;
   }
-  __shared__ double red[kT];
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = kT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
+  for (; i < hi; i += kT) {
+    const double v0 = a[i];
+    a0 += b ? v0 * b[i] : v0 * v0;
+    if (rescale) a[i] = v0 * scale;
   }
-  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+  const double t = block_sum((a0 + a1) + (a2 + a3));
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
-// *acc (+)= scale * sum(partial) in block order; mode 1 multiplies by exp(*log_sa) (act grad)
-__global__ void dot_final_kernel(const double* partial, int np, double scale, const double* log_sa,
-                                 int accumulate, double* acc) {
+struct GroupWeights {
+  double w[kMaxGroup];
+};
+// *acc (+)= sum_g wt.w[g] * (sum of partial[g*np .. g*np+np)) (one warp, fixed order);
+// with log_sa the total is multiplied by exp(*log_sa) (act grad)
+__global__ void dot_final_kernel(const double* partial, int np, int groups, GroupWeights wt,
+                                 const double* log_sa, int accumulate, double* acc) {
+  double total = 0.0;
+  for (int g = 0; g < groups; ++g) {
+    double sum = 0.0;
+    for (int i = threadIdx.x; i < np; i += 32) sum += partial[g * np + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+    total += wt.w[g] * sum;
+  }
   if (threadIdx.x != 0) return;
-  double s = 0.0;
-  for (int i = 0; i < np; ++i) s += partial[i];
-  double v = scale * s;
-  if (log_sa) v *= exp(*log_sa);
-  *acc = accumulate ? *acc + v : v;
+  if (log_sa) total *= exp(*log_sa);
+  *acc = accumulate ? *acc + total : total;
 }
 
 // per-iteration loss bookkeeping: loss = acc / B; best = min(best, loss) -> trace[t];
@@ -356,11 +387,14 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   double* vs = A.get<double>(2 * n);
   double* sgrad = A.get<double>(2 * n);
   double* target = A.get<double>(m_all * n);
-  double* d = A.get<double>(max_rows * n);
-  double* xhat = A.get<double>(max_rows * k);
-  double* xcode = A.get<double>(max_rows * k);
-  double* gx = A.get<double>(max_rows * k);
-  double* partial = A.get<double>(kRedBlocks);
+  // samples are stacked G at a time (rows <= cap_rows) so each product is one GEMM
+  const int64_t G = cfg->batch_size < kMaxGroup ? cfg->batch_size : kMaxGroup;
+  const int64_t cap_rows = G * max_rows;
+  double* d = A.get<double>(cap_rows * n);
+  double* xhat = A.get<double>(cap_rows * k);
+  double* xcode = A.get<double>(cap_rows * k);
+  double* gx = A.get<double>(cap_rows * k);
+  double* partial = A.get<double>(kMaxGroup * kRedBlocks);
   // scalars: [0] log_sa [1] m_a [2] v_a [3] g_a [4] loss acc [5] best
   double* sc = A.get<double>(8);
   int* flags = A.get<int>(2);  // [0] diverged_at, [1] non-finite input
@@ -390,38 +424,61 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   std::vector<double> wsamp(static_cast<size_t>(n_samples));
   for (int64_t i = 0; i < n_samples; ++i) wsamp[i] = chunk_weights[sample_chunk[i] - 1];
 
-  // one pass of the objective over `batch` with the current weights in `what`:
-  // sc[4] = sum_b w_b ||D_b||^2; with grads: gw = sum coeff D^T X^, sc[3] = act-scale grad
-  auto objective = [&](const std::vector<int64_t>& batch, bool grads) -> int {
-    const double inv_b = 1.0 / static_cast<double>(batch.size());
-    for (size_t bi = 0; bi < batch.size(); ++bi) {
-      const int64_t si = batch[bi];
-      const int64_t r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
-      xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat, xcode,
-                                                     flags + 1);
-      QARVD_CUDA_TRY(cudaMemcpyAsync(d, target + r0 * n, rows * n * 8, cudaMemcpyDeviceToDevice, s));
-      // D = X^ What^T - T
-      QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows),
+  // one pass of the objective over `list` with the current weights in `what`:
+  // sc[4] = sum_b w_b ||D_b||^2; with grads: gw = sum_b coeff_b D_b^T X^_b, sc[3] = act-scale
+  // grad.  Up to G consecutive samples are stacked along the rows, so D = X^ What^T - T,
+  // dL/dWhat = D'^T X^ and dL/dX^ = D' What are one GEMM each per group, with D' = coeff_b D_b
+  // (rows rescaled in place once ||D_b||^2 is read).
+  auto objective = [&](const std::vector<int64_t>& list, bool grads) -> int {
+    const double inv_b = 1.0 / static_cast<double>(list.size());
+    size_t pos = 0;
+    for (int gi = 0; pos < list.size(); ++gi) {
+      size_t end = pos;
+      int64_t rows_g = 0;
+      while (end < list.size() && static_cast<int64_t>(end - pos) < G) {
+        const int64_t r = sample_rows[list[end] + 1] - sample_rows[list[end]];
+        if (rows_g + r > cap_rows) break;
+        rows_g += r;
+        ++end;
+      }
+      GroupWeights wl{};
+      for (size_t j = pos, off = 0; j < end; ++j) {
+        const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
+        xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat + off * k,
+                                                       xcode + off * k, flags + 1);
+        QARVD_CUDA_TRY(cudaMemcpyAsync(d + off * n, target + r0 * n, rows * n * 8, cudaMemcpyDeviceToDevice, s));
+        off += rows;
+      }
+      // D = X^ What^T - T   [rows_g x n]
+      QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows_g),
                                    static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
                                    static_cast<int>(k), &minus_one, d, static_cast<int>(n)));
-      dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(d, nullptr, rows * n, partial);
-      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, wsamp[si], nullptr, bi > 0, sc + 4);
-      count_launch(3);
+      for (size_t j = pos, off = 0; j < end; ++j) {
+        const int64_t si = list[j], rows = sample_rows[si + 1] - sample_rows[si];
+        wl.w[j - pos] = wsamp[si];
+        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(d + off * n, nullptr, rows * n, grads ? 1 : 0,
+                                                     2.0 * wsamp[si] * inv_b, partial + (j - pos) * kRedBlocks);
+        off += rows;
+      }
+      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, static_cast<int>(end - pos), wl, nullptr, gi > 0,
+                                        sc + 4);
+      count_launch(2 * static_cast<int>(end - pos) + 2);
       if (grads) {
-        const double coeff = 2.0 * wsamp[si] * inv_b;
-        const double beta_acc = bi > 0 ? 1.0 : 0.0;
-        // dL/dWhat (+)= coeff D^T X^   [n x k]
+        // dL/dWhat (+)= D'^T X^   [n x k]
         QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(k), static_cast<int>(n),
-                                     static_cast<int>(rows), &coeff, xhat, static_cast<int>(k), d,
-                                     static_cast<int>(n), &beta_acc, gw, static_cast<int>(k)));
-        // dL/dX^ = coeff D What   [rows x k]; act grad += sum gx * s_a * code_x
-        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(k), static_cast<int>(rows),
-                                     static_cast<int>(n), &coeff, what, static_cast<int>(k), d,
+                                     static_cast<int>(rows_g), &one, xhat, static_cast<int>(k), d,
+                                     static_cast<int>(n), gi > 0 ? &one : &zero, gw, static_cast<int>(k)));
+        // dL/dX^ = D' What   [rows_g x k]; act grad (+)= sum gx * s_a * code_x
+        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(k), static_cast<int>(rows_g),
+                                     static_cast<int>(n), &one, what, static_cast<int>(k), d,
                                      static_cast<int>(n), &zero, gx, static_cast<int>(k)));
-        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(gx, xcode, rows * k, partial);
-        dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1.0, sc + 0, bi > 0, sc + 3);
+        GroupWeights unit{};
+        unit.w[0] = 1.0;
+        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(gx, xcode, rows_g * k, 0, 0.0, partial);
+        dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1, unit, sc + 0, gi > 0, sc + 3);
         count_launch(2);
       }
+      pos = end;
     }
     QARVD_LAUNCH_CHECK();
     return QARVD_OK;
