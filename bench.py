@@ -540,10 +540,13 @@ def adaround_bench(torch, iters=10):
     res = run(iters)
     torch.cuda.synchronize()
     t_it = (time.perf_counter() - t0 - t_fixed) / iters
-    flops = 8 * 3 * 2.0 * rows * spec.in_dim * spec.out_dim
+    # two stacked GEMMs per iteration (D = X^ What^T - T and D'^T X^); the reference's third
+    # (D What, for the act-scale gradient) is replaced by <What, dL/dWhat>
+    flops = 8 * 2 * 2.0 * rows * spec.in_dim * spec.out_dim
     return {"workload": f"AdaRound calibrate_layer (f64), {spec.out_dim}x{spec.in_dim} layer, {frames} x {rows}-token samples, batch 8",
             "ms_per_iteration": 1e3 * t_it, "fixed_ms": 1e3 * t_fixed,
             "dgemm_tflops": flops / t_it / 1e12,
+            "gemms_per_iteration": "2 over the stacked batch (reference: 3 per sample)",
             "projected_s_per_layer_2000_iters": t_fixed + 2000 * t_it,
             "final_loss": res.final_loss, "initial_loss": res.initial_loss,
             "note": "fixed = state init + per-sample targets + initial/final losses; wall clock (host-enqueued launch sequence)"}

@@ -9,9 +9,10 @@
 // after warm-up, and bias-corrected Adam with a cosine-annealed learning rate.
 //
 // Everything stays in f64 like the reference, so the trajectory follows it to rounding:
-// the three products (prediction X^ What^T - target, dL/dWhat = D^T X^, dL/dX^ = D What) are
-// cuBLAS DGEMMs (plain library GEMMs), each over the batch's samples stacked along the rows
-// (one GEMM per product, not per sample: 1560-row GEMMs leave DGEMM at 31 of its 35 TF/s);
+// the products (prediction X^ What^T - target, dL/dWhat = D^T X^) are cuBLAS DGEMMs (plain
+// library GEMMs), each over the batch's samples stacked along the rows (one GEMM per product,
+// not per sample: 1560-row GEMMs leave DGEMM at 31 of its 35 TF/s); the reference's third
+// product dL/dX^ = D What only feeds the act-scale gradient, which equals <What, dL/dWhat>;
 // every elementwise step,
 // reduction and Adam update is a kernel here with the reference's per-element formula, and
 // every reduction runs in a fixed order (deterministic).  The target X_s W^T is computed
@@ -113,10 +114,10 @@ __global__ void weights_kernel(const double* w, const double* v, const uint8_t* 
   }
 }
 
-// fake_quant(x, act) (quant.cpp:113-159, per-tensor symmetric, s = exp(log_sa)): xhat and the
-// code as f64; a non-finite input sets *bad (the reference throws)
+// fake_quant(x, act) (quant.cpp:113-159, per-tensor symmetric, s = exp(log_sa)): xhat = code * s
+// in f64; a non-finite input sets *bad (the reference throws)
 __global__ void xhat_kernel(const double* x, int64_t count, const double* log_sa, int qmax,
-                            double* xhat, double* xcode, int* bad) {
+                            double* xhat, int* bad) {
   const double s = exp(*log_sa);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -124,11 +125,9 @@ __global__ void xhat_kernel(const double* x, int64_t count, const double* log_sa
     if (!isfinite(xv)) {
       *bad = 1;
       xhat[i] = 0.0;
-      xcode[i] = 0.0;
       continue;
     }
     const double q = clampd(rint(xv / s), -static_cast<double>(qmax), static_cast<double>(qmax));
-    xcode[i] = q;
     xhat[i] = q * s;
   }
 }
@@ -392,14 +391,12 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   const int64_t cap_rows = G * max_rows;
   double* d = A.get<double>(cap_rows * n);
   double* xhat = A.get<double>(cap_rows * k);
-  double* xcode = A.get<double>(cap_rows * k);
-  double* gx = A.get<double>(cap_rows * k);
   double* partial = A.get<double>(kMaxGroup * kRedBlocks);
   // scalars: [0] log_sa [1] m_a [2] v_a [3] g_a [4] loss acc [5] best
   double* sc = A.get<double>(8);
   int* flags = A.get<int>(2);  // [0] diverged_at, [1] non-finite input
   if (!v || !mv || !vv || !what || !code || !dhdv || !gw || !log_s || !ms || !vs || !sgrad || !target ||
-      !d || !xhat || !xcode || !gx || !partial || !sc || !flags)
+      !d || !xhat || !partial || !sc || !flags)
     QARVD_FAIL(QARVD_ERR_CUDA, "calibrate_layer: device allocation failed");
   QARVD_CUDA_TRY(cudaMemsetAsync(mv, 0, nk * 8, s));
   QARVD_CUDA_TRY(cudaMemsetAsync(vv, 0, nk * 8, s));
@@ -426,9 +423,9 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
 
   // one pass of the objective over `list` with the current weights in `what`:
   // sc[4] = sum_b w_b ||D_b||^2; with grads: gw = sum_b coeff_b D_b^T X^_b, sc[3] = act-scale
-  // grad.  Up to G consecutive samples are stacked along the rows, so D = X^ What^T - T,
-  // dL/dWhat = D'^T X^ and dL/dX^ = D' What are one GEMM each per group, with D' = coeff_b D_b
-  // (rows rescaled in place once ||D_b||^2 is read).
+  // grad.  Up to G consecutive samples are stacked along the rows, so D = X^ What^T - T and
+  // dL/dWhat = D'^T X^ are one GEMM each per group, with D' = coeff_b D_b (rows rescaled in
+  // place once ||D_b||^2 is read).
   auto objective = [&](const std::vector<int64_t>& list, bool grads) -> int {
     const double inv_b = 1.0 / static_cast<double>(list.size());
     size_t pos = 0;
@@ -445,7 +442,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
       for (size_t j = pos, off = 0; j < end; ++j) {
         const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
         xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat + off * k,
-                                                       xcode + off * k, flags + 1);
+                                                       flags + 1);
         QARVD_CUDA_TRY(cudaMemcpyAsync(d + off * n, target + r0 * n, rows * n * 8, cudaMemcpyDeviceToDevice, s));
         off += rows;
       }
@@ -468,17 +465,19 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
         QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(k), static_cast<int>(n),
                                      static_cast<int>(rows_g), &one, xhat, static_cast<int>(k), d,
                                      static_cast<int>(n), gi > 0 ? &one : &zero, gw, static_cast<int>(k)));
-        // dL/dX^ = D' What   [rows_g x k]; act grad (+)= sum gx * s_a * code_x
-        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(k), static_cast<int>(rows_g),
-                                     static_cast<int>(n), &one, what, static_cast<int>(k), d,
-                                     static_cast<int>(n), &zero, gx, static_cast<int>(k)));
-        GroupWeights unit{};
-        unit.w[0] = 1.0;
-        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(gx, xcode, rows_g * k, 0, 0.0, partial);
-        dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1, unit, sc + 0, gi > 0, sc + 3);
-        count_launch(2);
+        count_launch(1);
       }
       pos = end;
+    }
+    if (grads && cfg->train_activation_scale) {
+      // act-scale grad sum_b coeff_b sum (D_b What) * s_a * code_x (calibrate.cpp:300-304)
+      // = <What, sum_b coeff_b D_b^T X^_b> = <What, gw>, since X^ = s_a code_x: the dL/dX^
+      // product is never formed
+      GroupWeights unit{};
+      unit.w[0] = 1.0;
+      dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(what, gw, nk, 0, 0.0, partial);
+      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1, unit, nullptr, 0, sc + 3);
+      count_launch(2);
     }
     QARVD_LAUNCH_CHECK();
     return QARVD_OK;
