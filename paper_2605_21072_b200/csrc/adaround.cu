@@ -147,27 +147,32 @@ __device__ __forceinline__ double block_sum(double acc) {
     for (int w = 0; w < kT / 32; ++w) t += red[w];
   return t;
 }
-// partial[p] = sum a[i]*b[i] over block p's range (b = nullptr: a[i]^2); with scale != 0 the
-// range is also rescaled in place (a[i] *= scale, with rescale) after being read
+// partial[p] = sum a[i]*b[i] over block p's range (b = nullptr: a[i]^2); with sub, a[i] is
+// first replaced by a[i] - sub[i]; with rescale the range is written back as a[i] * scale
+// (sub or rescale: written back whenever either is set)
 __global__ void __launch_bounds__(kT) dot_partial_kernel(double* a, const double* b, int64_t count,
-                                                          int rescale, double scale, double* partial) {
+                                                          int rescale, double scale, double* partial,
+                                                          const double* sub = nullptr) {
   const int64_t per = (count + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = lo + per < count ? lo + per : count;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int64_t i = lo + threadIdx.x;
   for (; i + 3 * kT < hi; i += 4 * kT) {
-    const double v0 = a[i], v1 = a[i + kT], v2 = a[i + 2 * kT], v3 = a[i + 3 * kT];
+    double v0 = a[i], v1 = a[i + kT], v2 = a[i + 2 * kT], v3 = a[i + 3 * kT];
+    if (sub) v0 -= sub[i], v1 -= sub[i + kT], v2 -= sub[i + 2 * kT], v3 -= sub[i + 3 * kT];
     if (b) {
       a0 += v0 * b[i], a1 += v1 * b[i + kT], a2 += v2 * b[i + 2 * kT], a3 += v3 * b[i + 3 * kT];
     } else {
       a0 += v0 * v0, a1 += v1 * v1, a2 += v2 * v2, a3 += v3 * v3;
     }
     if (rescale) a[i] = v0 * scale, a[i + kT] = v1 * scale, a[i + 2 * kT] = v2 * scale, a[i + 3 * kT] = v3 * scale;
+    else if (sub) a[i] = v0, a[i + kT] = v1, a[i + 2 * kT] = v2, a[i + 3 * kT] = v3;
   }
   for (; i < hi; i += kT) {
-    const double v0 = a[i];
+    const double v0 = sub ? a[i] - sub[i] : a[i];
     a0 += b ? v0 * b[i] : v0 * v0;
     if (rescale) a[i] = v0 * scale;
+    else if (sub) a[i] = v0;
   }
   const double t = block_sum((a0 + a1) + (a2 + a3));
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -413,7 +418,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   count_launch(4);
   QARVD_LAUNCH_CHECK();
   // targets X_s W^T for every sample, once (row-major [rows x n] = col-major W^T-op GEMM)
-  const double one = 1.0, zero = 0.0, minus_one = -1.0;
+  const double one = 1.0, zero = 0.0;
   QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(m_all),
                                static_cast<int>(k), &one, w, static_cast<int>(k), x, static_cast<int>(k), &zero,
                                target, static_cast<int>(n)));
@@ -443,18 +448,19 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
         const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
         xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat + off * k,
                                                        flags + 1);
-        QARVD_CUDA_TRY(cudaMemcpyAsync(d + off * n, target + r0 * n, rows * n * 8, cudaMemcpyDeviceToDevice, s));
         off += rows;
       }
-      // D = X^ What^T - T   [rows_g x n]
+      // P = X^ What^T   [rows_g x n]; D = P - T is formed by the reduction below
       QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows_g),
                                    static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
-                                   static_cast<int>(k), &minus_one, d, static_cast<int>(n)));
+                                   static_cast<int>(k), &zero, d, static_cast<int>(n)));
       for (size_t j = pos, off = 0; j < end; ++j) {
-        const int64_t si = list[j], rows = sample_rows[si + 1] - sample_rows[si];
+        const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
         wl.w[j - pos] = wsamp[si];
+        // D_b = P_b - T_b (calibrate.cpp:279-280), ||D_b||^2, and D_b *= coeff_b for the gradient
         dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(d + off * n, nullptr, rows * n, grads ? 1 : 0,
-                                                     2.0 * wsamp[si] * inv_b, partial + (j - pos) * kRedBlocks);
+                                                     2.0 * wsamp[si] * inv_b, partial + (j - pos) * kRedBlocks,
+                                                     target + r0 * n);
         off += rows;
       }
       dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, static_cast<int>(end - pos), wl, nullptr, gi > 0,
