@@ -180,19 +180,34 @@ __global__ void __launch_bounds__(kT) dot_partial_kernel(double* a, const double
 struct GroupWeights {
   double w[kMaxGroup];
 };
-// *acc (+)= sum_g wt.w[g] * (sum of partial[g*np .. g*np+np)) (one warp, fixed order);
-// with log_sa the total is multiplied by exp(*log_sa) (act grad)
-__global__ void dot_final_kernel(const double* partial, int np, int groups, GroupWeights wt,
-                                 const double* log_sa, int accumulate, double* acc) {
-  double total = 0.0;
-  for (int g = 0; g < groups; ++g) {
+// *acc (+)= sum_g wt.w[g] * (sum of partial[g*kRedBlocks ..][kRedBlocks]) in a fixed order:
+// warp g sums group g (all of its loads issued before the adds), thread 0 combines the groups
+// in order; with log_sa the total is multiplied by exp(*log_sa) (act grad).  Launch with
+// kMaxGroup * 32 threads.
+__global__ void __launch_bounds__(kMaxGroup * 32) dot_final_kernel(const double* partial, int groups,
+                                                                  GroupWeights wt, const double* log_sa,
+                                                                  int accumulate, double* acc) {
+  constexpr int kPer = (kRedBlocks + 31) / 32;
+  __shared__ double gsum[kMaxGroup];
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (g < groups) {
+    double v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = lane + 32 * j;
+      v[j] = i < kRedBlocks ? partial[g * kRedBlocks + i] : 0.0;
+    }
     double sum = 0.0;
-    for (int i = threadIdx.x; i < np; i += 32) sum += partial[g * np + i];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) sum += v[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
-    total += wt.w[g] * sum;
+    if (lane == 0) gsum[g] = sum;
   }
+  __syncthreads();
   if (threadIdx.x != 0) return;
+  double total = 0.0;
+  for (int i = 0; i < groups; ++i) total += wt.w[i] * gsum[i];
   if (log_sa) total *= exp(*log_sa);
   *acc = accumulate ? *acc + total : total;
 }
@@ -463,7 +478,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
                                                      target + r0 * n);
         off += rows;
       }
-      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, static_cast<int>(end - pos), wl, nullptr, gi > 0,
+      dot_final_kernel<<<1, kMaxGroup * 32, 0, s>>>(partial, static_cast<int>(end - pos), wl, nullptr, gi > 0,
                                         sc + 4);
       count_launch(2 * static_cast<int>(end - pos) + 2);
       if (grads) {
@@ -482,7 +497,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
       GroupWeights unit{};
       unit.w[0] = 1.0;
       dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(what, gw, nk, 0, 0.0, partial);
-      dot_final_kernel<<<1, 32, 0, s>>>(partial, kRedBlocks, 1, unit, nullptr, 0, sc + 3);
+      dot_final_kernel<<<1, kMaxGroup * 32, 0, s>>>(partial, 1, unit, nullptr, 0, sc + 3);
       count_launch(2);
     }
     QARVD_LAUNCH_CHECK();
