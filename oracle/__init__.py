@@ -95,6 +95,7 @@ def ref():
                                            c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                                            c_int, c_int, ctypes.c_uint64, ctypes.c_char_p, c_void_p,
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+        _r.ref_calibrate_layer_bits.argtypes = list(_r.ref_calibrate_layer.argtypes) + [c_int, c_int]
         _r.ref_toy_qarq.argtypes = [ctypes.c_char_p, c_int, c_void_p]
         _r.ref_qarq_layer.argtypes = [ctypes.c_char_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p]
@@ -397,8 +398,9 @@ def ref_weighted_loss(w64, outliers, act_scale, x64, row_off, chunks, chunk_w):
 
 
 def ref_calibrate_layer(w64, outliers, act_scale, x64, row_off, chunks, chunk_w, iterations, batch_size,
-                        seed, name):
-    """The reference calibrate_layer (calibrate.cpp:298-396) on build_plan(W, outliers)."""
+                        seed, name, w_bits=8, act_bits=8):
+    """The reference calibrate_layer (calibrate.cpp:298-396) on build_plan(W, outliers, w_bits)
+    with a per-tensor symmetric act_bits activation scale."""
     w64 = np.ascontiguousarray(w64, dtype=np.float64)
     n, k = w64.shape
     x64 = np.ascontiguousarray(x64, dtype=np.float64)
@@ -410,9 +412,10 @@ def ref_calibrate_layer(w64, outliers, act_scale, x64, row_off, chunks, chunk_w,
     sn, so, isn, iso = np.empty(n), np.empty(n), np.empty(n), np.empty(n)
     sc = np.empty(3)
     tr = np.empty(max(1, iterations))
-    _rc(ref().ref_calibrate_layer(_p(w64), n, k, _p(o), len(o), float(act_scale), _p(x64), _p(ro), _p(ch),
-                                  len(ch), _p(cw), len(cw), iterations, batch_size, seed, name.encode(),
-                                  _p(codes), _p(sn), _p(so), _p(sc), _p(tr), _p(isn), _p(iso)))
+    _rc(ref().ref_calibrate_layer_bits(_p(w64), n, k, _p(o), len(o), float(act_scale), _p(x64), _p(ro),
+                                       _p(ch), len(ch), _p(cw), len(cw), iterations, batch_size, seed,
+                                       name.encode(), _p(codes), _p(sn), _p(so), _p(sc), _p(tr), _p(isn),
+                                       _p(iso), int(w_bits), int(act_bits)))
     return dict(codes=codes, scale_normal=sn, scale_outlier=so, act_scale=sc[0], initial_loss=sc[1],
                 final_loss=sc[2], trace=tr[:iterations], init_scale_normal=isn, init_scale_outlier=iso)
 

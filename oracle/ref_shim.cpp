@@ -335,19 +335,19 @@ extern "C" int ref_weighted_loss(const double* w, int64_t n, int64_t k, const in
 // calibrate_layer (calibrate.cpp:298-396) with build_plan(W, aligned outliers) and a per-tensor
 // act_init; default CalibConfig except iterations / batch size / seed.  Exports the learned
 // scales, hard codes, act scale, losses and the trace.
-extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const int64_t* outliers,
-                                   int64_t n_out, double act_scale, const double* x,
-                                   const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
-                                   const double* chunk_w, int64_t n_chunks, int iterations,
-                                   int batch_size, uint64_t seed, const char* name, int32_t* codes,
-                                   double* s_n, double* s_o, double* scalars, double* trace,
-                                   double* init_s_n, double* init_s_o) {
+extern "C" int ref_calibrate_layer_bits(const double* w, int64_t n, int64_t k, const int64_t* outliers,
+                                        int64_t n_out, double act_scale, const double* x,
+                                        const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
+                                        const double* chunk_w, int64_t n_chunks, int iterations,
+                                        int batch_size, uint64_t seed, const char* name, int32_t* codes,
+                                        double* s_n, double* s_o, double* scalars, double* trace,
+                                        double* init_s_n, double* init_s_o, int w_bits, int act_bits) {
   return guarded([&] {
     const Tensor W = make_tensor(w, n, k);
     OutlierReport rep;
     rep.layer_name = name;
     rep.aligned_outliers.assign(outliers, outliers + n_out);
-    DualScalePlan plan = build_plan(W, rep, 8);
+    DualScalePlan plan = build_plan(W, rep, w_bits);
     plan.layer_name = name;
     for (int64_t r = 0; r < n; ++r) {
       init_s_n[r] = plan.params_normal.scale[r];
@@ -366,7 +366,7 @@ extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const 
       ptrs.push_back(&samples[s]);
     }
     const std::vector<double> cw(chunk_w, chunk_w + n_chunks);
-    const LayerCalibResult r = calibrate_layer(W, plan, QuantParams::per_tensor_symmetric(8, act_scale),
+    const LayerCalibResult r = calibrate_layer(W, plan, QuantParams::per_tensor_symmetric(act_bits, act_scale),
                                                ptrs, cw, cfg);
     std::memcpy(codes, r.codes.data.data(), sizeof(int32_t) * n * k);
     for (int64_t i = 0; i < n; ++i) {
@@ -378,6 +378,18 @@ extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const 
     scalars[2] = r.final_loss;
     for (size_t t = 0; t < r.trace.size(); ++t) trace[t] = r.trace[t];
   });
+}
+
+extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const int64_t* outliers,
+                                   int64_t n_out, double act_scale, const double* x,
+                                   const int64_t* row_off, const int64_t* chunk, int64_t n_samples,
+                                   const double* chunk_w, int64_t n_chunks, int iterations,
+                                   int batch_size, uint64_t seed, const char* name, int32_t* codes,
+                                   double* s_n, double* s_o, double* scalars, double* trace,
+                                   double* init_s_n, double* init_s_o) {
+  return ref_calibrate_layer_bits(w, n, k, outliers, n_out, act_scale, x, row_off, chunk, n_samples,
+                                  chunk_w, n_chunks, iterations, batch_size, seed, name, codes, s_n, s_o,
+                                  scalars, trace, init_s_n, init_s_o, 8, 8);
 }
 
 // The reference pipeline's own model file: ToyModel::build (two injections) -> calibrate_model
