@@ -290,11 +290,12 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
   // chunks overlap the compute and each other (PCIe is full duplex).  QARVD_HOST_CHUNKS
   // overrides the chunk count (1 = the sequential H2D -> chain -> D2H).
   qarvd_linear* L0 = layers[0];
-  // Equal row chunks, 128-row aligned.  (Measured: 4 chunks 0.49 ms per Wan FFN step vs
-  // 0.73 ms sequential; the PCIe floor with both directions busy is 0.33 ms.  Smaller or
-  // uneven chunks lose more GEMM efficiency -- N = 1536 has only 6 tile columns -- than they
-  // gain in pipeline fill.)
-  int nchunks = m >= 2048 ? 4 : 1;
+  // Equal row chunks, 128-row aligned (so the last one is the smallest).  Measured per Wan
+  // FFN step (M = 4680, 3 x 300 steps each): 3 chunks 488 µs, 4: 469-477, 5: 447-455,
+  // 6: 467-471; sequential 0.73 ms; the PCIe floor with both directions busy is 0.33 ms.
+  // More chunks lose more GEMM efficiency -- N = 1536 has only 6 tile columns -- than they
+  // gain in pipeline fill.
+  int nchunks = m >= 2048 ? 5 : 1;
   if (const char* env = getenv("QARVD_HOST_CHUNKS")) nchunks = atoi(env);
   nchunks = nchunks < 1 ? 1 : (nchunks > 8 ? 8 : nchunks);
   int64_t bounds[9] = {0};
