@@ -380,6 +380,74 @@ int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, const uint8_t* 
                           double* scale_normal_out, double* scale_outlier_out, double* scalars_out,
                           double* trace_out, void* stream);
 
+/* ---- exact f64 restatements of the reference's generic operators ---------
+ * The C++ drop-in (adapter/) serves these reference functions from the device, bit-identical
+ * to the reference's f64 CPU code (no FMA, the reference's op order).  All pointers are
+ * device pointers unless marked HOST.
+ *
+ * Replaces  quantize / dequantize / fake_quant  quant.hpp:64-66 / quant.cpp:113-159.
+ * Element i uses channel ch = (i / inner) % extent (extent = 1: per-tensor).  codes (int32, the
+ * IntTensor storage) and dequant (f64: (code - z) * s) may each be NULL.  zero_points NULL = 0.
+ * err_index: int64[1], receives the smallest flat index of a non-finite x (or INT64_MAX); the
+ * reference throws "quantize: non-finite input at flat index N" (quant.cpp:128-129). */
+int qarvd_quantize_f64(const double* x, int64_t count, int64_t inner, int64_t extent,
+                       const double* scales, const int32_t* zero_points, int32_t q_min,
+                       int32_t q_max, int32_t* codes, double* dequant, int64_t* err_index,
+                       void* stream);
+/* Replaces  init_scale_minmax(x, bits, g, axis)  quant.hpp:71 / quant.cpp:161-183:
+ * scales[extent] = absmax over each slice / (2^(bits-1)-1), DBL_MIN for all-zero slices. */
+int qarvd_minmax_scale_f64(const double* x, int64_t count, int64_t inner, int64_t extent, int bits,
+                           double* scales, void* stream);
+/* Replaces  init_scale_percentile_search(samples, bits)  quant.hpp:82 / quant.cpp:185-226.
+ * x: the samples concatenated; sample_offsets HOST int64 [n_samples + 1]; percentiles HOST
+ * [num_cand] (the reference's {0.999, 0.9999, 0.99999}).  Exact order statistics of the pooled
+ * |x| by radix select; per-sample squared errors summed in double-double.
+ * result: f64 [3*num_cand + 2] = thresholds, scales, candidate MSEs, best index, best scale.
+ * err: int64 [2] = {first sample holding a non-finite value, its flat index} or {-1, -1}
+ * (the reference throws "quantize: non-finite input at flat index N" there).  Synchronizes. */
+int qarvd_percentile_search_f64(const double* x, const int64_t* sample_offsets, int64_t n_samples,
+                                const double* percentiles, int num_cand, int bits, double* result,
+                                int64_t* err, void* stream);
+/* Replaces  matmul_nt(a, b)  tensor.hpp:70 / tensor.cpp:82-105: c[m x n] = a[m x k] b[n x k]^T,
+ * each output summed from 0.0 in ascending k with separate multiply and add roundings. */
+int qarvd_matmul_nt_f64(const double* a, int64_t m, int64_t k, int64_t lda, const double* b, int64_t n,
+                        int64_t ldb, double* c, int64_t ldc, void* stream);
+/* Replaces  permute_activations  engine.cpp:36-44 and the code pre-permute calibrate.cpp:474-480:
+ * out[r, c] = idx[c] >= 0 ? in[r, idx[c]] : 0 for elements of elem_bytes (1, 2, 4 or 8). */
+int qarvd_gather_columns(const void* in, int64_t rows, int64_t ld_in, const int32_t* idx,
+                         int64_t out_cols, void* out, int64_t ld_out, int elem_bytes, void* stream);
+/* Replaces  dequantized_weight_original_order  engine.cpp:117-130 (the fakequant_sim weights):
+ * w_out[j, perm[pos]] = wq[j, pos] * (pos < n_outlier ? s_o[j] : s_n[j]); perm NULL = identity. */
+int qarvd_dequant_weight_f64(const int32_t* wq, int64_t n, int64_t k, const uint32_t* perm,
+                             int64_t n_outlier, const double* scale_outlier, const double* scale_normal,
+                             double* w_out, void* stream);
+
+/* *total = (accumulate ? *total : 0) + weight * sum_i (a_i - b_i)^2 with the sum sequential in i
+ * (frobenius_sq_distance tensor.cpp:116-126 inside weighted_recon_loss calibrate.cpp:206-214);
+ * divide_by > 0 then divides the total (the batch mean, calibrate.cpp:215).  total: device f64[1]. */
+int qarvd_sq_distance_acc_f64(const double* a, const double* b, int64_t count, double weight, double* total,
+                              int accumulate, double divide_by, void* stream);
+/* Kernel B's zero-point correction (engine.cpp:74-83, :95-100) applied to an f64 output of
+ * qarvd_dual_gemm_f64: y[i, j] -= (z_x * s_x) * sum_g s_g[j] * colsum_g[j], colsum over the
+ * group's columns of wq (groups = 2: [0, k_outlier) outlier then normal; 1: one group). */
+int qarvd_zero_point_correct_f64(double* y, int64_t ldy, int64_t m, int64_t n, const int8_t* wq, int64_t ldw,
+                                 int64_t k, int64_t k_outlier, int groups, int32_t z_x, double s_x,
+                                 const double* s_wo, const double* s_wn, void* stream);
+/* int32 codes (IntTensor storage) -> int8 kernel layout: out[r, c] = idx[c] >= 0 ? in[r, idx[c]] : 0;
+ * *bad (device int) is set to 1 when a code is outside [-128, 127]. */
+int qarvd_pack_codes_i8(const int32_t* in, int64_t rows, int64_t ld_in, const int32_t* idx, int64_t out_cols,
+                        int8_t* out, int64_t ld_out, int* bad, void* stream);
+/* out[i] = exp(in[i]) exactly as the reference's std::exp (glibc's algorithm restated, libm_ref.cuh). */
+int qarvd_exp_f64(const double* in, double* out, int64_t count, void* stream);
+/* LearnableQuantState soft / hard weights and hard codes (calibrate.cpp:138-183):
+ * what = s * clamp(floor(w / s) + r, -qmax, qmax) with r = h(V) (hard = 0) or [h(V) > 0.5]
+ * (hard = 1), s = exp(log_scale[group row]) (log_scale = [normal n | outlier n]); codes (int8,
+ * original column order) written when non-NULL and hard; what may be NULL. */
+int qarvd_adaround_weights(const double* w, const double* v, const uint8_t* outlier_mask,
+                           int plan_enabled, const double* log_scale, int64_t n, int64_t k,
+                           double zeta, double gamma_lo, int w_bits, int hard, double* what,
+                           int8_t* codes, void* stream);
+
 /* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
  * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)
  * weights with a seeded set of input columns scaled by gamma.  Values are

@@ -1,13 +1,20 @@
-// qarvd_cuda.cpp — see qarvd_cuda.hpp.  Host staging + status mapping only.
+// qarvd_cuda.cpp — see qarvd_cuda.hpp.  Host staging, per-thread device contexts and status
+// mapping only: every arithmetic step runs in libqarvd_b200.so.  The reference library is linked
+// for its types, its parameter validation (QuantParams::validate, CalibConfig::validate) and its
+// host drivers (run_rollout, parallel_for); none of its compute functions is called from here
+// (tests/cpp/test_no_ref_compute.cpp links this file against poisoned copies of them).
 #include "qarvd_cuda.hpp"
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <limits>
 #include <stdexcept>
 
 #include "../../include/qarvd_b200.h"
 #include "qarvd/bytes.hpp"
+#include "qarvd/threading.hpp"
 
 namespace qarvd {
 namespace cuda {
@@ -32,48 +39,144 @@ void check_cuda(cudaError_t e) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
-// RAII device buffer
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  DevBuf() = default;
-  explicit DevBuf(size_t n) : bytes(n) { check_cuda(cudaMalloc(&p, n ? n : 1)); }
-  DevBuf(const void* host, size_t n) : DevBuf(n) {
-    if (n) check_cuda(cudaMemcpy(p, host, n, cudaMemcpyHostToDevice));
-  }
-  ~DevBuf() { cudaFree(p); }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  template <typename T>
-  T* as() const { return static_cast<T*>(p); }
-};
-
 size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
-// Kernel layout of a plan: [outliers | pad to 32 | normals | pad to 32] (qarvd_b200.h)
+// ---- per-thread execution contexts ----------------------------------------------------
+// Providers are shared const across the reference's parallel_for workers (sensitivity.cpp:46-52,
+// calibrate.cpp:440), so every call runs on its own thread's context: a non-blocking stream and
+// grow-only device workspaces.  Contexts live in a process-wide pool; a thread takes one on its
+// first call and returns it when it exits, so the short-lived parallel_for workers reuse the
+// streams and buffers instead of creating and freeing them per call.
+struct Context {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  std::vector<std::pair<void*, size_t>> slots;
+
+  // grow-only workspace `slot` of at least `bytes` (contents undefined)
+  template <typename T = void>
+  T* ws(size_t slot, size_t bytes) {
+    if (slots.size() <= slot) slots.resize(slot + 1, {nullptr, 0});
+    auto& s = slots[slot];
+    if (s.second < bytes) {
+      if (s.first) {
+        check_cuda(cudaStreamSynchronize(stream));
+        check_cuda(cudaFree(s.first));
+        s.first = nullptr;
+        s.second = 0;
+      }
+      const size_t cap = std::max<size_t>(round_up(bytes, 256), 4096);
+      check_cuda(cudaMalloc(&s.first, cap));
+      s.second = cap;
+    }
+    return static_cast<T*>(s.first);
+  }
+  void sync() { check_cuda(cudaStreamSynchronize(stream)); }
+};
+
+class ContextPool {
+ public:
+  Context* acquire(int device) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i]->device == device) {
+          Context* c = free_[i];
+          free_.erase(free_.begin() + static_cast<std::ptrdiff_t>(i));
+          return c;
+        }
+    }
+    auto* c = new Context();
+    c->device = device;
+    check_cuda(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    return c;
+  }
+  void release(Context* c) {
+    std::lock_guard<std::mutex> lock(mu_);
+    free_.push_back(c);
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<Context*> free_;  // process lifetime: never destroyed (streams outlive threads)
+};
+ContextPool& pool() {
+  static auto* p = new ContextPool();
+  return *p;
+}
+struct ContextHolder {
+  Context* c = nullptr;
+  ~ContextHolder() {
+    if (c) pool().release(c);
+  }
+};
+Context& ctx() {
+  thread_local ContextHolder h;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev));
+  if (!h.c || h.c->device != dev) {
+    if (h.c) pool().release(h.c);
+    h.c = pool().acquire(dev);
+  }
+  return *h.c;
+}
+
+// workspace slots (one call never uses a slot twice)
+enum Slot : size_t {
+  kX, kX2, kXq, kSx, kY, kY2, kW, kW2, kCodes, kScales, kScales2, kIdx, kErr, kMisc, kMisc2, kMisc3,
+};
+
+void h2d(Context& c, void* dst, const void* src, size_t bytes) {
+  if (bytes) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.stream));
+}
+void d2h(Context& c, void* dst, const void* src, size_t bytes) {
+  if (bytes) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+}
+template <typename T>
+T* upload(Context& c, size_t slot, const T* host, size_t count) {
+  T* d = c.ws<T>(slot, count * sizeof(T));
+  h2d(c, d, host, count * sizeof(T));
+  return d;
+}
+
+// Kernel layout of a plan: [outliers | pad to 32 | normals | pad to 32] (qarvd_b200.h).
 struct Layout {
-  std::vector<int32_t> gather;  // source column per padded position, -1 = pad
-  std::vector<int32_t> pos;     // padded position of permuted column c (reference order)
-  size_t k_outlier = 0, k_pad = 0;
+  std::vector<int32_t> gather;  // original column per padded position (x -> xq, K1), -1 = pad
+  std::vector<int32_t> pack;    // plan position per padded position (pre-permuted codes), -1 = pad
+  std::vector<int32_t> pos;     // padded position of plan position c
+  size_t n_outlier = 0, k_outlier = 0, k_pad = 0;
 };
 
 Layout make_layout(const DualScalePlan& plan, size_t d_in) {
   Layout L;
-  const size_t n_o = plan.enabled ? plan.outlier_count() : 0;
-  L.k_outlier = round_up(n_o, 32);
-  L.k_pad = L.k_outlier + round_up(d_in - n_o, 32);
+  L.n_outlier = plan.enabled ? plan.outlier_count() : 0;
+  L.k_outlier = round_up(L.n_outlier, 32);
+  L.k_pad = L.k_outlier + round_up(d_in - L.n_outlier, 32);
   L.gather.assign(L.k_pad, -1);
+  L.pack.assign(L.k_pad, -1);
   L.pos.resize(d_in);
   for (size_t c = 0; c < d_in; ++c) {
-    const size_t dst = c < n_o ? c : L.k_outlier + (c - n_o);
+    const size_t dst = c < L.n_outlier ? c : L.k_outlier + (c - L.n_outlier);
     L.gather[dst] = plan.enabled ? static_cast<int32_t>(plan.permutation[c]) : static_cast<int32_t>(c);
+    L.pack[dst] = static_cast<int32_t>(c);
     L.pos[c] = static_cast<int32_t>(dst);
   }
   return L;
 }
 
+// the reference's flat index of a non-finite element found at padded position `bad`
+int64_t unpadded_index(int64_t bad, const Layout& L, size_t k) {
+  const int64_t row = bad / static_cast<int64_t>(L.k_pad), pc = bad % static_cast<int64_t>(L.k_pad);
+  int64_t c = 0;
+  for (size_t i = 0; i < L.pos.size(); ++i)
+    if (L.pos[i] == pc) c = static_cast<int64_t>(i);
+  return row * static_cast<int64_t>(k) + c;
+}
+
+std::string nonfinite_msg(int64_t i) { return "quantize: non-finite input at flat index " + std::to_string(i); }
+
 }  // namespace
 
+// Device-resident copy of one QuantizedLayer: padded int8 codes, f64 group scales, the K1 gather.
 class DeviceLayer {
  public:
   explicit DeviceLayer(const QuantizedLayer& l)
@@ -81,121 +184,395 @@ class DeviceLayer {
     if (l.preserved) throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + l.name);
     if (l.wq.shape.size() != 2 || l.wq.shape[0] != n || l.wq.shape[1] != k)
       throw std::invalid_argument("kernel_b: weight shape mismatch for " + l.name);
-    std::vector<int8_t> wq(n * layout.k_pad, 0);
-    for (size_t r = 0; r < n; ++r)
-      for (size_t c = 0; c < k; ++c)
-        wq[r * layout.k_pad + layout.pos[c]] = static_cast<int8_t>(l.wq.data[r * k + c]);
+    if (l.wq.bits > 8) throw std::invalid_argument("kernel_b: the CUDA engine stores codes as int8");
+    Context& c = ctx();
+    check_cuda(cudaMalloc(&wq, n * layout.k_pad));
+    check_cuda(cudaMalloc(&so, n * 8));
+    check_cuda(cudaMalloc(&sn, n * 8));
+    check_cuda(cudaMalloc(&gather, layout.k_pad * 4));
+    const int32_t* codes = upload(c, kCodes, l.wq.data.data(), n * k);
+    const int32_t* pack = upload(c, kIdx, layout.pack.data(), layout.k_pad);
+    int* bad = c.ws<int>(kErr, sizeof(int));
+    check_cuda(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+    check(qarvd_pack_codes_i8(codes, static_cast<int64_t>(n), static_cast<int64_t>(k), pack,
+                              static_cast<int64_t>(layout.k_pad), wq, static_cast<int64_t>(layout.k_pad), bad,
+                              c.stream));
     // f64 group scales exactly as the reference holds them in memory (the f64 epilogue
-    // entry point reproduces kernel_b_gemm_dequant bit for bit)
-    std::vector<double> so(n), sn(n);
-    for (size_t r = 0; r < n; ++r) {
-      sn[r] = l.plan.params_normal.scale[r];
-      so[r] = l.plan.enabled ? l.plan.params_outlier.scale[r] : l.plan.params_normal.scale[r];
-    }
-    wq_dev = std::make_unique<DevBuf>(wq.data(), wq.size());
-    so_dev = std::make_unique<DevBuf>(so.data(), so.size() * 8);
-    sn_dev = std::make_unique<DevBuf>(sn.data(), sn.size() * 8);
-    gather_dev = std::make_unique<DevBuf>(layout.gather.data(), layout.gather.size() * 4);
+    // reproduces kernel_b_gemm_dequant bit for bit)
+    h2d(c, sn, l.plan.params_normal.scale.data(), n * 8);
+    h2d(c, so, (l.plan.enabled ? l.plan.params_outlier.scale : l.plan.params_normal.scale).data(), n * 8);
+    h2d(c, gather, layout.gather.data(), layout.k_pad * 4);
+    int hbad = 0;
+    d2h(c, &hbad, bad, sizeof(int));
+    c.sync();
+    if (hbad) throw std::invalid_argument("kernel_b: the CUDA engine stores codes as int8");
   }
+  ~DeviceLayer() {
+    cudaFree(wq);
+    cudaFree(so);
+    cudaFree(sn);
+    cudaFree(gather);
+  }
+  DeviceLayer(const DeviceLayer&) = delete;
+  DeviceLayer& operator=(const DeviceLayer&) = delete;
+
   std::string name;
   size_t n, k;
   Layout layout;
-  std::unique_ptr<DevBuf> wq_dev, so_dev, sn_dev, gather_dev;
+  int8_t* wq = nullptr;
+  double* so = nullptr;
+  double* sn = nullptr;
+  int32_t* gather = nullptr;
 };
 
 namespace {
 
-// K1 on a host f64 tensor in the layer padded layout; returns device codes + f64 row scales.
-void quantize_to_device(const Tensor& x, const Layout& L, const DevBuf& gather_dev,
-                        const QuantParams& p, DevBuf& xq, DevBuf& sx, size_t m) {
-  if (p.per_channel() || p.zero_point[0] != 0 || !p.symmetric)
-    throw std::invalid_argument("quantize: the CUDA engine implements symmetric per-tensor activations");
-  p.validate(x.shape());
-  DevBuf xd(x.data(), x.size() * sizeof(double));
-  DevBuf err(sizeof(int64_t));
-  check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(x.cols()),
-                           static_cast<int64_t>(x.cols()), gather_dev.as<int32_t>(),
-                           static_cast<int64_t>(L.k_pad), QARVD_ACT_PER_TENSOR, p.scale[0], p.bits,
-                           xq.as<int8_t>(), static_cast<int64_t>(L.k_pad), nullptr, sx.as<double>(),
-                           err.as<int64_t>(), nullptr));
-  int64_t bad = 0;
-  check_cuda(cudaMemcpy(&bad, err.p, sizeof(bad), cudaMemcpyDeviceToHost));
-  if (bad != INT64_MAX) {
-    // report the first non-finite in the reference's (unpadded, permuted) flat index
-    const int64_t row = bad / static_cast<int64_t>(L.k_pad), pc = bad % static_cast<int64_t>(L.k_pad);
-    int64_t c = 0;
-    for (size_t i = 0; i < L.pos.size(); ++i)
-      if (L.pos[i] == pc) c = static_cast<int64_t>(i);
-    throw std::invalid_argument("quantize: non-finite input at flat index " +
-                                std::to_string(row * static_cast<int64_t>(x.cols()) + c));
+// kernel B (K2 tensor-core int32 accumulators + the reference's f64 epilogue, engine.cpp:86-100)
+// on device codes xq [m x k_pad] in the layer layout -> host f64 [m x n]
+Tensor gemm_to_host(Context& c, const DeviceLayer& L, const QuantParams& act, const int8_t* xq, size_t m) {
+  const double s_x = act.scale[0];
+  const int32_t z_x = act.zero_point.empty() ? 0 : act.zero_point[0];
+  double* sx = c.ws<double>(kSx, m * 8);
+  {
+    std::vector<double> h(m, s_x);
+    h2d(c, sx, h.data(), m * 8);
+    c.sync();  // h is a local
   }
+  double* y = c.ws<double>(kY, m * L.n * 8);
+  check(qarvd_dual_gemm_f64(xq, static_cast<int64_t>(L.layout.k_pad), L.wq, static_cast<int64_t>(L.layout.k_pad),
+                            static_cast<int64_t>(m), static_cast<int64_t>(L.n), static_cast<int64_t>(L.layout.k_pad),
+                            static_cast<int64_t>(L.layout.k_outlier), sx, L.so, L.sn, y, static_cast<int64_t>(L.n),
+                            c.stream));
+  if (z_x != 0)
+    check(qarvd_zero_point_correct_f64(y, static_cast<int64_t>(L.n), static_cast<int64_t>(m),
+                                       static_cast<int64_t>(L.n), L.wq, static_cast<int64_t>(L.layout.k_pad),
+                                       static_cast<int64_t>(L.layout.k_pad), static_cast<int64_t>(L.layout.k_outlier),
+                                       L.layout.n_outlier > 0 ? 2 : 1, z_x, s_x, L.so, L.sn, c.stream));
+  Tensor out({m, L.n});
+  d2h(c, out.data(), y, m * L.n * 8);
+  c.sync();
+  return out;
 }
 
-// sx: device f64 [m] activation scale per row
-Tensor gemm_to_host(const DeviceLayer& L, const DevBuf& xq, const DevBuf& sx, size_t m) {
-  DevBuf y(m * L.n * sizeof(double));
-  check(qarvd_dual_gemm_f64(xq.as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
-                            L.wq_dev->as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
-                            static_cast<int64_t>(m), static_cast<int64_t>(L.n),
-                            static_cast<int64_t>(L.layout.k_pad),
-                            static_cast<int64_t>(L.layout.k_outlier), sx.as<double>(),
-                            L.so_dev->as<double>(), L.sn_dev->as<double>(), y.as<double>(),
-                            static_cast<int64_t>(L.n), nullptr));
-  Tensor out({m, L.n});
-  check_cuda(cudaMemcpy(out.data(), y.p, m * L.n * sizeof(double), cudaMemcpyDeviceToHost));
-  return out;
+// kernel A on a host activation (original column order) into the layer layout: per-tensor symmetric
+// params take K1 (f64 input, exact path, gather fused); any other params (asymmetric zero point) the
+// generic exact quantizer followed by the int8 packing
+int8_t* quantize_to_layout(Context& c, const DeviceLayer& L, const Tensor& x, const QuantParams& p) {
+  if (x.rank() != 2 || x.cols() != L.k)
+    throw std::invalid_argument("permute_activations: plan does not match activation width");
+  p.validate(x.shape());
+  if (p.per_channel()) throw std::invalid_argument("kernel_b: per-tensor activation params expected");
+  if (p.bits > 8 || p.q_min < -128 || p.q_max > 127)
+    throw std::invalid_argument("quantize: the CUDA engine stores codes as int8");
+  const size_t m = x.rows();
+  const double* xd = upload(c, kX, x.data(), x.size());
+  int8_t* xq = c.ws<int8_t>(kXq, m * L.layout.k_pad + 16);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  int64_t bad = INT64_MAX;
+  if (p.symmetric && p.zero_point[0] == 0) {
+    check(qarvd_quantize_act(xd, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(L.k),
+                             static_cast<int64_t>(L.k), L.gather, static_cast<int64_t>(L.layout.k_pad),
+                             QARVD_ACT_PER_TENSOR, p.scale[0], p.bits, xq, static_cast<int64_t>(L.layout.k_pad),
+                             nullptr, nullptr, err, c.stream));
+    d2h(c, &bad, err, 8);
+    c.sync();
+    if (bad != INT64_MAX) throw std::invalid_argument(nonfinite_msg(unpadded_index(bad, L.layout, L.k)));
+    return xq;
+  }
+  // quantize(permute(x)) = permute(quantize(x)) for per-tensor params: codes in original order,
+  // then packed through the K1 gather (original column per padded position)
+  double* sd = upload(c, kScales, p.scale.data(), 1);
+  int32_t* zd = upload(c, kMisc, p.zero_point.data(), 1);
+  int32_t* codes = c.ws<int32_t>(kCodes, m * L.k * 4);
+  check(qarvd_quantize_f64(xd, static_cast<int64_t>(m * L.k), 1, 1, sd, zd, p.q_min, p.q_max, codes, nullptr, err,
+                           c.stream));
+  int* pbad = c.ws<int>(kMisc2, sizeof(int));
+  check_cuda(cudaMemsetAsync(pbad, 0, sizeof(int), c.stream));
+  check(qarvd_pack_codes_i8(codes, static_cast<int64_t>(m), static_cast<int64_t>(L.k), L.gather,
+                            static_cast<int64_t>(L.layout.k_pad), xq, static_cast<int64_t>(L.layout.k_pad), pbad,
+                            c.stream));
+  d2h(c, &bad, err, 8);
+  c.sync();
+  if (bad != INT64_MAX) {
+    // the reference quantizes the permuted tensor: report the first bad element in that order
+    const size_t k = L.k;
+    std::vector<double> row(k);
+    const int64_t r = bad / static_cast<int64_t>(k);
+    std::memcpy(row.data(), x.data() + r * k, k * 8);
+    int64_t first = bad;
+    for (size_t cpos = 0; cpos < k; ++cpos) {
+      const size_t orig = L.layout.gather[L.layout.pos[cpos]];
+      if (!std::isfinite(row[orig])) {
+        first = r * static_cast<int64_t>(k) + static_cast<int64_t>(cpos);
+        break;
+      }
+    }
+    throw std::invalid_argument(nonfinite_msg(first));
+  }
+  return xq;
+}
+
+// LearnableQuantState on the device (what / codes and act scale); returns device pointers in slots
+struct DeviceState {
+  double* w = nullptr;       // [n x k]
+  double* what = nullptr;    // hard weights [n x k]
+  int8_t* codes = nullptr;   // hard codes [n x k] (optional)
+  double* act_scale = nullptr;  // [1] exp(log_act_scale)
+};
+DeviceState upload_state(Context& c, const LearnableQuantState& st, bool want_codes) {
+  const size_t n = st.weight.rows(), k = st.weight.cols();
+  DeviceState d;
+  d.w = upload(c, kW, st.weight.data(), n * k);
+  const double* v = upload(c, kW2, st.v.data(), n * k);
+  std::vector<uint8_t> mask(k, 0);
+  if (st.plan.enabled)
+    for (size_t col : st.plan.outlier_indices) mask[col] = 1;
+  std::vector<double> log_s(2 * n + 1);
+  for (size_t r = 0; r < n; ++r) {
+    log_s[r] = st.log_scale_normal[r];
+    log_s[n + r] = st.plan.enabled ? st.log_scale_outlier[r] : st.log_scale_normal[r];
+  }
+  log_s[2 * n] = st.log_act_scale;
+  double* ls = upload(c, kScales2, log_s.data(), log_s.size());
+  const uint8_t* md = upload(c, kMisc3, mask.data(), k);
+  d.what = c.ws<double>(kY2, n * k * 8);
+  if (want_codes) d.codes = c.ws<int8_t>(kMisc, n * k);
+  check(qarvd_adaround_weights(d.w, v, md, st.plan.enabled ? 1 : 0, ls, static_cast<int64_t>(n),
+                               static_cast<int64_t>(k), st.zeta, st.gamma_lo, st.plan.params_normal.bits, 1, d.what,
+                               d.codes, c.stream));
+  d.act_scale = c.ws<double>(kMisc2, 8);
+  check(qarvd_exp_f64(ls + 2 * n, d.act_scale, 1, c.stream));
+  c.sync();  // the host vectors above go out of scope
+  return d;
 }
 
 }  // namespace
 
-IntTensor kernel_a_quantize_activation(const Tensor& x, const QuantParams& p) {
+// ---- quant.hpp -------------------------------------------------------------------------
+
+IntTensor quantize(const Tensor& x, const QuantParams& p) {
   p.validate(x.shape());
-  if (x.rank() != 2) return qarvd::quantize(x, p);  // non-matrix inputs: not a hot path
-  const size_t m = x.rows(), k = x.cols();
-  if (p.bits > 8) throw std::invalid_argument("quantize: the CUDA engine stores codes as int8");
-  const size_t kp = round_up(k, 32);
-  std::vector<int32_t> gather(kp, -1);
-  for (size_t c = 0; c < k; ++c) gather[c] = static_cast<int32_t>(c);
-  DevBuf gd(gather.data(), gather.size() * 4), xd(x.data(), x.size() * sizeof(double));
-  DevBuf q(m * kp + 16), err(sizeof(int64_t));
-  std::vector<double> scales_in;
+  Context& c = ctx();
+  size_t extent = 1, inner = 1;
+  if (p.per_channel()) {
+    extent = x.shape()[p.channel_axis];
+    for (size_t a = p.channel_axis + 1; a < x.shape().size(); ++a) inner *= x.shape()[a];
+  }
   IntTensor out;
   out.shape = x.shape();
   out.bits = p.bits;
-  out.data.resize(m * k);
-  if (p.per_channel() && p.channel_axis == 0) {
-    // per-token (per-row) scales: one K1 launch per distinct scale is wasteful; rows carry
-    // their own scale through the static path one row block at a time
-    for (size_t i = 0; i < m; ++i) {
-      check(qarvd_quantize_act(xd.as<double>() + i * k, QARVD_F64, 1, static_cast<int64_t>(k),
-                               static_cast<int64_t>(k), gd.as<int32_t>(), static_cast<int64_t>(kp),
-                               QARVD_ACT_PER_TENSOR, p.scale[i], p.bits, q.as<int8_t>() + i * kp,
-                               static_cast<int64_t>(kp), nullptr, nullptr, err.as<int64_t>(), nullptr));
-    }
-  } else if (p.per_channel()) {
-    return qarvd::quantize(x, p);  // per-column scales never occur on the activation path
-  } else {
-    check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(k),
-                             static_cast<int64_t>(k), gd.as<int32_t>(), static_cast<int64_t>(kp),
-                             QARVD_ACT_PER_TENSOR, p.scale[0], p.bits, q.as<int8_t>(),
-                             static_cast<int64_t>(kp), nullptr, nullptr, err.as<int64_t>(), nullptr));
-  }
-  int64_t bad = 0;
-  check_cuda(cudaMemcpy(&bad, err.p, sizeof(bad), cudaMemcpyDeviceToHost));
-  if (bad != INT64_MAX) {
-    const int64_t row = bad / static_cast<int64_t>(kp), c = bad % static_cast<int64_t>(kp);
-    throw std::invalid_argument("quantize: non-finite input at flat index " +
-                                std::to_string(row * static_cast<int64_t>(k) + c));
-  }
-  std::vector<int8_t> h(m * kp);
-  check_cuda(cudaMemcpy(h.data(), q.p, h.size(), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < m; ++i)
-    for (size_t c = 0; c < k; ++c) out.data[i * k + c] = h[i * kp + c];
+  out.data.resize(x.size());
+  if (x.size() == 0) return out;
+  const double* xd = upload(c, kX, x.data(), x.size());
+  const double* sd = upload(c, kScales, p.scale.data(), p.scale.size());
+  const int32_t* zd = upload(c, kMisc, p.zero_point.data(), p.zero_point.size());
+  int32_t* codes = c.ws<int32_t>(kCodes, x.size() * 4);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  check(qarvd_quantize_f64(xd, static_cast<int64_t>(x.size()), static_cast<int64_t>(inner),
+                           static_cast<int64_t>(extent), sd, zd, p.q_min, p.q_max, codes, nullptr, err, c.stream));
+  int64_t bad = INT64_MAX;
+  d2h(c, &bad, err, 8);
+  d2h(c, out.data.data(), codes, x.size() * 4);
+  c.sync();
+  if (bad != INT64_MAX) throw std::invalid_argument(nonfinite_msg(bad));
   return out;
 }
 
+Tensor fake_quant(const Tensor& x, const QuantParams& p) {
+  p.validate(x.shape());
+  Context& c = ctx();
+  size_t extent = 1, inner = 1;
+  if (p.per_channel()) {
+    extent = x.shape()[p.channel_axis];
+    for (size_t a = p.channel_axis + 1; a < x.shape().size(); ++a) inner *= x.shape()[a];
+  }
+  Tensor out(x.shape());
+  if (x.size() == 0) return out;
+  const double* xd = upload(c, kX, x.data(), x.size());
+  const double* sd = upload(c, kScales, p.scale.data(), p.scale.size());
+  const int32_t* zd = upload(c, kMisc, p.zero_point.data(), p.zero_point.size());
+  double* deq = c.ws<double>(kY, x.size() * 8);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  check(qarvd_quantize_f64(xd, static_cast<int64_t>(x.size()), static_cast<int64_t>(inner),
+                           static_cast<int64_t>(extent), sd, zd, p.q_min, p.q_max, nullptr, deq, err, c.stream));
+  int64_t bad = INT64_MAX;
+  d2h(c, &bad, err, 8);
+  d2h(c, out.data(), deq, x.size() * 8);
+  c.sync();
+  if (bad != INT64_MAX) throw std::invalid_argument(nonfinite_msg(bad));
+  return out;
+}
+
+QuantParams init_scale_minmax(const Tensor& x, int bits, Granularity g, size_t axis) {
+  if (bits < 2 || bits > 30)
+    throw std::invalid_argument("bit width out of supported range [2,30]: " + std::to_string(bits));
+  size_t extent = 1, inner = 1;
+  if (g == Granularity::per_channel) {
+    if (axis >= x.shape().size()) throw std::invalid_argument("init_scale_minmax: axis out of range");
+    extent = x.shape()[axis];
+    for (size_t a = axis + 1; a < x.shape().size(); ++a) inner *= x.shape()[a];
+  }
+  Context& c = ctx();
+  const double* xd = upload(c, kX, x.data(), x.size());
+  double* sd = c.ws<double>(kScales, extent * 8);
+  check(qarvd_minmax_scale_f64(xd, static_cast<int64_t>(x.size()), static_cast<int64_t>(inner),
+                               static_cast<int64_t>(extent), bits, sd, c.stream));
+  std::vector<double> scales(extent);
+  d2h(c, scales.data(), sd, extent * 8);
+  c.sync();
+  if (g == Granularity::per_tensor) return QuantParams::per_tensor_symmetric(bits, scales[0]);
+  return QuantParams::per_channel_symmetric(bits, axis, std::move(scales));
+}
+
+PercentileSearchResult init_scale_percentile_search(const std::vector<Tensor>& samples, int bits) {
+  if (bits < 2 || bits > 30)
+    throw std::invalid_argument("bit width out of supported range [2,30]: " + std::to_string(bits));
+  if (samples.empty()) throw std::invalid_argument("percentile search: empty calibration sample list");
+  Context& c = ctx();
+  std::vector<int64_t> offsets{0};
+  for (const Tensor& s : samples) offsets.push_back(offsets.back() + static_cast<int64_t>(s.size()));
+  if (offsets.back() == 0) throw std::invalid_argument("quantile of empty vector");
+  double* xd = c.ws<double>(kX, static_cast<size_t>(offsets.back()) * 8);
+  for (size_t i = 0; i < samples.size(); ++i) h2d(c, xd + offsets[i], samples[i].data(), samples[i].size() * 8);
+  const std::vector<double>& pct = PercentileSearchResult::percentiles();
+  const int nc = static_cast<int>(pct.size());
+  double* res = c.ws<double>(kY, (3 * pct.size() + 2) * 8);
+  int64_t* err = c.ws<int64_t>(kErr, 16);
+  check(qarvd_percentile_search_f64(xd, offsets.data(), static_cast<int64_t>(samples.size()), pct.data(), nc, bits,
+                                    res, err, c.stream));
+  std::vector<double> r(3 * pct.size() + 2);
+  int64_t e[2];
+  d2h(c, r.data(), res, r.size() * 8);
+  d2h(c, e, err, 16);
+  c.sync();
+  // the reference's first failure in its loop order: candidate 0's scale is validated before any
+  // element is read, then the first sample holding a non-finite value throws (quant.cpp:114-129)
+  if (!(r[nc] > 0.0) || !std::isfinite(r[nc]))
+    throw std::invalid_argument("quant params: scale must be positive and finite");
+  if (e[0] >= 0) throw std::invalid_argument(nonfinite_msg(e[1]));
+  PercentileSearchResult out;
+  out.candidate_mse.assign(r.begin() + 2 * nc, r.begin() + 3 * nc);
+  const int best = static_cast<int>(r[3 * nc]);
+  out.best_percentile = pct[best];
+  out.params = QuantParams::per_tensor_symmetric(bits, r[3 * nc + 1]);
+  return out;
+}
+
+// ---- dual_scale.hpp --------------------------------------------------------------------
+
+namespace {
+// row_scales_over_columns (dual_scale.cpp:13-24) for both groups of a plan, through K5 on the f64
+// weight (its scales are the reference's absmax / qmax, DBL_MIN for empty or all-zero groups)
+void group_scales(const Tensor& w, const DualScalePlan& plan, int bits, std::vector<double>& so,
+                  std::vector<double>& sn) {
+  if (bits < 2 || bits > 8) throw std::invalid_argument("build_plan: the CUDA engine supports 2..8-bit weights");
+  const size_t n = w.rows(), k = w.cols();
+  Context& c = ctx();
+  const Layout L = make_layout(plan, k);
+  const double* wd = upload(c, kW, w.data(), n * k);
+  const int32_t* gd = upload(c, kIdx, L.gather.data(), L.k_pad);
+  int8_t* wq = c.ws<int8_t>(kCodes, n * L.k_pad);
+  double* so_d = c.ws<double>(kScales, n * 8);
+  double* sn_d = c.ws<double>(kScales2, n * 8);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  check(qarvd_prepare_weights(wd, QARVD_F64, static_cast<int64_t>(n), static_cast<int64_t>(k),
+                              static_cast<int64_t>(k), gd, static_cast<int64_t>(L.k_pad),
+                              static_cast<int64_t>(L.k_outlier), bits, wq, static_cast<int64_t>(L.k_pad), so_d, sn_d,
+                              nullptr, nullptr, err, c.stream));
+  so.resize(n);
+  sn.resize(n);
+  d2h(c, so.data(), so_d, n * 8);
+  d2h(c, sn.data(), sn_d, n * 8);
+  c.sync();
+}
+}  // namespace
+
+DualScalePlan build_single_scale_plan(const std::string& layer_name, const Tensor& w, int bits) {
+  if (w.rank() != 2) throw std::invalid_argument("build_plan: weight must be 2-D");
+  DualScalePlan plan;
+  plan.layer_name = layer_name;
+  plan.enabled = false;
+  plan.d_in = w.cols();
+  plan.normal_indices.resize(plan.d_in);
+  plan.permutation.resize(plan.d_in);
+  for (size_t i = 0; i < plan.d_in; ++i) {
+    plan.normal_indices[i] = i;
+    plan.permutation[i] = static_cast<uint32_t>(i);
+  }
+  std::vector<double> so, sn;
+  group_scales(w, plan, bits, so, sn);
+  plan.params_normal = QuantParams::per_channel_symmetric(bits, 0, std::move(sn));
+  plan.params_outlier = plan.params_normal;
+  return plan;
+}
+
+DualScalePlan build_plan(const Tensor& w, const OutlierReport& report, int bits) {
+  if (w.rank() != 2) throw std::invalid_argument("build_plan: weight must be 2-D");
+  const size_t d_in = w.cols();
+  if (!report.norms.empty() && report.norms.size() != d_in)
+    throw std::invalid_argument("build_plan: report does not match the weight's input width");
+  for (size_t idx : report.aligned_outliers)
+    if (idx >= d_in) throw std::out_of_range("build_plan: outlier index out of range");
+  if (report.aligned_outliers.empty()) return qarvd::cuda::build_single_scale_plan(report.layer_name, w, bits);
+  DualScalePlan plan;
+  plan.layer_name = report.layer_name;
+  plan.enabled = true;
+  plan.d_in = d_in;
+  plan.outlier_indices = report.aligned_outliers;
+  std::vector<uint8_t> is_out(d_in, 0);
+  for (size_t cidx : plan.outlier_indices) is_out[cidx] = 1;
+  for (size_t cidx = 0; cidx < d_in; ++cidx)
+    if (!is_out[cidx]) plan.normal_indices.push_back(cidx);
+  if (plan.normal_indices.empty())
+    throw std::invalid_argument("build_plan: outlier set would leave no normal channels");
+  for (size_t cidx : plan.outlier_indices) plan.permutation.push_back(static_cast<uint32_t>(cidx));
+  for (size_t cidx : plan.normal_indices) plan.permutation.push_back(static_cast<uint32_t>(cidx));
+  std::vector<double> so, sn;
+  group_scales(w, plan, bits, so, sn);
+  plan.params_outlier = QuantParams::per_channel_symmetric(bits, 0, std::move(so));
+  plan.params_normal = QuantParams::per_channel_symmetric(bits, 0, std::move(sn));
+  return plan;
+}
+
+// ---- tensor.hpp ------------------------------------------------------------------------
+
+Tensor matmul_nt(const Tensor& a, const Tensor& b) {
+  if (a.rank() != 2 || b.rank() != 2) throw std::invalid_argument("matmul_nt: inputs must be 2-D");
+  if (a.cols() != b.cols()) throw std::invalid_argument("matmul_nt: shape mismatch");
+  Context& c = ctx();
+  const size_t m = a.rows(), k = a.cols(), n = b.rows();
+  Tensor out({m, n});
+  if (m == 0 || n == 0) return out;
+  const double* ad = upload(c, kX, a.data(), m * k);
+  const double* bd = upload(c, kW, b.data(), n * k);
+  double* cd = c.ws<double>(kY, m * n * 8);
+  check(qarvd_matmul_nt_f64(ad, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), bd,
+                            static_cast<int64_t>(n), static_cast<int64_t>(k), cd, static_cast<int64_t>(n), c.stream));
+  d2h(c, out.data(), cd, m * n * 8);
+  c.sync();
+  return out;
+}
+
+// ---- engine.hpp ------------------------------------------------------------------------
+
+IntTensor kernel_a_quantize_activation(const Tensor& x, const QuantParams& p) { return qarvd::cuda::quantize(x, p); }
+
 Tensor permute_activations(const Tensor& x, const DualScalePlan& plan) {
-  return qarvd::permute_activations(x, plan);  // a gather; fused into K1 on the device path
+  if (!plan.enabled) return x;
+  if (x.cols() != plan.permutation.size())
+    throw std::invalid_argument("permute_activations: plan does not match activation width");
+  Context& c = ctx();
+  const size_t m = x.rows(), k = x.cols();
+  std::vector<int32_t> idx(plan.permutation.begin(), plan.permutation.end());
+  const double* xd = upload(c, kX, x.data(), m * k);
+  const int32_t* id = upload(c, kIdx, idx.data(), k);
+  double* out_d = c.ws<double>(kY, m * k * 8);
+  check(qarvd_gather_columns(xd, static_cast<int64_t>(m), static_cast<int64_t>(k), id, static_cast<int64_t>(k), out_d,
+                             static_cast<int64_t>(k), 8, c.stream));
+  Tensor out({m, k});
+  d2h(c, out.data(), out_d, m * k * 8);
+  c.sync();
+  return out;
 }
 
 Tensor kernel_b_gemm_dequant(const IntTensor& xq, const QuantizedLayer& layer) {
@@ -203,41 +580,92 @@ Tensor kernel_b_gemm_dequant(const IntTensor& xq, const QuantizedLayer& layer) {
     throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + layer.name);
   if (xq.shape.size() != 2 || xq.shape[1] != layer.in_dim)
     throw std::invalid_argument("kernel_b: activation shape does not match layer " + layer.name);
-  if (layer.act.zero_point[0] != 0)
-    throw std::invalid_argument("kernel_b: asymmetric activations are not supported by the CUDA engine");
   const DeviceLayer L(layer);
+  Context& c = ctx();
   const size_t m = xq.shape[0];
-  std::vector<int8_t> h(m * L.layout.k_pad, 0);
-  for (size_t i = 0; i < m; ++i)
-    for (size_t c = 0; c < L.k; ++c)
-      h[i * L.layout.k_pad + L.layout.pos[c]] = static_cast<int8_t>(xq.data[i * L.k + c]);
-  DevBuf xd(h.data(), h.size());
-  std::vector<double> sx(m, layer.act.scale[0]);
-  DevBuf sd(sx.data(), sx.size() * 8);
-  return gemm_to_host(L, xd, sd, m);
+  const int32_t* codes = upload(c, kCodes, xq.data.data(), m * L.k);
+  const int32_t* pack = upload(c, kIdx, L.layout.pack.data(), L.layout.k_pad);
+  int8_t* xd = c.ws<int8_t>(kXq, m * L.layout.k_pad + 16);
+  int* bad = c.ws<int>(kErr, sizeof(int));
+  check_cuda(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+  check(qarvd_pack_codes_i8(codes, static_cast<int64_t>(m), static_cast<int64_t>(L.k), pack,
+                            static_cast<int64_t>(L.layout.k_pad), xd, static_cast<int64_t>(L.layout.k_pad), bad,
+                            c.stream));
+  int hbad = 0;
+  d2h(c, &hbad, bad, sizeof(int));
+  c.sync();
+  if (hbad) throw std::invalid_argument("kernel_b: the CUDA engine stores codes as int8");
+  return gemm_to_host(c, L, layer.act, xd, m);
 }
+
+namespace {
+Tensor fakequant_forward(Context& c, const Tensor& x, const QuantParams& act, const double* w_dev, size_t n) {
+  // matmul_nt(fake_quant(x, act), W_deq) (engine.cpp:141)
+  act.validate(x.shape());
+  if (act.per_channel()) throw std::invalid_argument("kernel_b: per-tensor activation params expected");
+  const size_t m = x.rows(), k = x.cols();
+  const double* xd = upload(c, kX, x.data(), m * k);
+  const double* sd = upload(c, kScales, act.scale.data(), 1);
+  const int32_t* zd = upload(c, kMisc, act.zero_point.data(), 1);
+  double* xhat = c.ws<double>(kX2, m * k * 8);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  check(qarvd_quantize_f64(xd, static_cast<int64_t>(m * k), 1, 1, sd, zd, act.q_min, act.q_max, nullptr, xhat, err,
+                           c.stream));
+  double* y = c.ws<double>(kY, m * n * 8);
+  check(qarvd_matmul_nt_f64(xhat, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), w_dev,
+                            static_cast<int64_t>(n), static_cast<int64_t>(k), y, static_cast<int64_t>(n), c.stream));
+  int64_t bad = INT64_MAX;
+  d2h(c, &bad, err, 8);
+  Tensor out({m, n});
+  d2h(c, out.data(), y, m * n * 8);
+  c.sync();
+  if (bad != INT64_MAX) throw std::invalid_argument(nonfinite_msg(bad));
+  return out;
+}
+
+// dequantized_weight_original_order (engine.cpp:117-130) into device slot `slot`
+double* dequant_weight(Context& c, const QuantizedLayer& l, size_t slot) {
+  const size_t n = l.out_dim, k = l.in_dim;
+  const int32_t* wq = upload(c, kCodes, l.wq.data.data(), n * k);
+  const uint32_t* perm = l.plan.enabled ? upload(c, kIdx, l.plan.permutation.data(), k) : nullptr;
+  const double* sn = upload(c, kScales, l.plan.params_normal.scale.data(), n);
+  const double* so = l.plan.enabled ? upload(c, kScales2, l.plan.params_outlier.scale.data(), n) : sn;
+  double* w = c.ws<double>(slot, n * k * 8);
+  check(qarvd_dequant_weight_f64(wq, static_cast<int64_t>(n), static_cast<int64_t>(k), perm,
+                                 static_cast<int64_t>(l.plan.enabled ? l.plan.outlier_count() : 0), so, sn, w,
+                                 c.stream));
+  return w;
+}
+}  // namespace
 
 Tensor quantized_layer_forward(const QuantizedLayer& layer, const Tensor& x, Engine engine) {
-  if (layer.preserved || engine == Engine::fakequant_sim)
-    return qarvd::quantized_layer_forward(layer, x, engine);  // f64 reference paths
+  if (layer.preserved) return qarvd::cuda::matmul_nt(x, layer.fp_weight);
+  Context& c = ctx();
+  if (engine == Engine::fakequant_sim) {
+    const double* w = dequant_weight(c, layer, kW);
+    return fakequant_forward(c, x, layer.act, w, layer.out_dim);
+  }
   const DeviceLayer L(layer);
-  const size_t m = x.rows();
-  DevBuf xq(m * L.layout.k_pad + 16), sx(m * 8);
-  quantize_to_device(x, L.layout, *L.gather_dev, layer.act, xq, sx, m);
-  return gemm_to_host(L, xq, sx, m);
+  const int8_t* xq = quantize_to_layout(c, L, x, layer.act);
+  return gemm_to_host(c, L, layer.act, xq, x.rows());
 }
 
-OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w, double tau,
-                            double alpha_min, size_t align) {
+// ---- outlier.hpp -----------------------------------------------------------------------
+
+OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w, double tau, double alpha_min,
+                            size_t align) {
   if (w.rank() != 2) throw std::invalid_argument("channel_l2_norms: input must be 2-D");
   const size_t n = w.rows(), k = w.cols();
-  DevBuf wd(w.data(), w.size() * sizeof(double)), norms(k * 8), stats(24), counts(8),
-      raw(k * 4), al(k * 4);
-  qarvd_outlier_job job{wd.p, static_cast<int64_t>(n), static_cast<int64_t>(k),
-                        static_cast<int64_t>(k), norms.as<double>(), stats.as<double>(),
-                        counts.as<int32_t>(), raw.as<int32_t>(), al.as<int32_t>()};
-  check(qarvd_analyze_layers(&job, 1, QARVD_F64, tau, alpha_min, static_cast<int64_t>(align), nullptr));
-  check_cuda(cudaDeviceSynchronize());
+  Context& c = ctx();
+  const double* wd = upload(c, kW, w.data(), n * k);
+  double* norms = c.ws<double>(kY, k * 8);
+  double* stats = c.ws<double>(kScales, 24);
+  int32_t* counts = c.ws<int32_t>(kMisc, 8);
+  int32_t* raw = c.ws<int32_t>(kIdx, k * 4);
+  int32_t* al = c.ws<int32_t>(kCodes, k * 4);
+  qarvd_outlier_job job{wd, static_cast<int64_t>(n), static_cast<int64_t>(k), static_cast<int64_t>(k), norms,
+                        stats, counts, raw, al};
+  check(qarvd_analyze_layers(&job, 1, QARVD_F64, tau, alpha_min, static_cast<int64_t>(align), c.stream));
   OutlierReport rep;
   rep.layer_name = layer_name;
   rep.tau = tau;
@@ -246,12 +674,13 @@ OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w, doub
   rep.norms.resize(k);
   double st[3];
   int32_t cnt[2];
-  check_cuda(cudaMemcpy(rep.norms.data(), norms.p, k * 8, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(st, stats.p, 24, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(cnt, counts.p, 8, cudaMemcpyDeviceToHost));
   std::vector<int32_t> r(k), a(k);
-  check_cuda(cudaMemcpy(r.data(), raw.p, k * 4, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(a.data(), al.p, k * 4, cudaMemcpyDeviceToHost));
+  d2h(c, rep.norms.data(), norms, k * 8);
+  d2h(c, st, stats, 24);
+  d2h(c, cnt, counts, 8);
+  d2h(c, r.data(), raw, k * 4);
+  d2h(c, a.data(), al, k * 4);
+  c.sync();
   rep.median = st[0];
   rep.mad = st[1];
   rep.threshold = st[2];
@@ -260,195 +689,195 @@ OutlierReport analyze_layer(const std::string& layer_name, const Tensor& w, doub
   return rep;
 }
 
-CudaQuantizedProvider::CudaQuantizedProvider(const QuantizedModel& qm) : qm_(qm) {
-  for (const auto& l : qm.layers)
-    if (!l.preserved) layers_.emplace(l.name, std::make_shared<DeviceLayer>(l));
+// ---- providers ------------------------------------------------------------------------
+
+CudaQuantizedProvider::CudaQuantizedProvider(const QuantizedModel& qm, Engine engine) : qm_(qm), engine_(engine) {
+  Context& c = ctx();
+  for (const auto& l : qm.layers) {
+    if (l.preserved) {
+      // preserved layers: matmul_nt(x, fp_weight) (engine.cpp:158) on the device
+      double* w = nullptr;
+      check_cuda(cudaMalloc(&w, l.fp_weight.size() * 8));
+      h2d(c, w, l.fp_weight.data(), l.fp_weight.size() * 8);
+      fp_.emplace(l.name, std::shared_ptr<double>(w, [](double* p) { cudaFree(p); }));
+    } else if (engine == Engine::fakequant_sim) {
+      const double* wdq = dequant_weight(c, l, kW);
+      double* w = nullptr;
+      check_cuda(cudaMalloc(&w, l.out_dim * l.in_dim * 8));
+      check_cuda(cudaMemcpyAsync(w, wdq, l.out_dim * l.in_dim * 8, cudaMemcpyDeviceToDevice, c.stream));
+      fp_.emplace(l.name, std::shared_ptr<double>(w, [](double* p) { cudaFree(p); }));
+    } else {
+      layers_.emplace(l.name, std::make_shared<DeviceLayer>(l));
+    }
+  }
+  c.sync();
 }
 
 CudaQuantizedProvider::~CudaQuantizedProvider() = default;
 
-Tensor CudaQuantizedProvider::forward(const std::string& layer, const Tensor& x) const {
-  const QuantizedLayer& l = qm_.layer(layer);  // std::out_of_range as the reference (engine.cpp:29)
-  if (l.preserved) return matmul_nt(x, l.fp_weight);
-  const DeviceLayer& L = *layers_.at(layer);
-  const size_t m = x.rows();
-  DevBuf xq(m * L.layout.k_pad + 16), sx(m * 8);
-  quantize_to_device(x, L.layout, *L.gather_dev, l.act, xq, sx, m);
-  return gemm_to_host(L, xq, sx, m);
-}
-
 namespace {
-// bf16 round-to-nearest-even of an f64 value (through f32, as bytes.hpp:40-45 for finite values)
-uint16_t bf16_rne(double v) {
-  const float f = static_cast<float>(v);
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  u += 0x7FFFu + ((u >> 16) & 1u);
-  return static_cast<uint16_t>(u >> 16);
-}
-double bf16_value(uint16_t h) {
-  const uint32_t u = static_cast<uint32_t>(h) << 16;
-  float f;
-  std::memcpy(&f, &u, 4);
-  return f;
-}
-// rows of [a_hi a_hi a_lo] (x side) or [a_hi a_lo a_hi] (w side), 3k bf16 per row
-std::vector<uint16_t> split3(const double* a, size_t rows, size_t k, bool x_side) {
-  std::vector<uint16_t> out(rows * 3 * k);
-  for (size_t r = 0; r < rows; ++r)
-    for (size_t c = 0; c < k; ++c) {
-      const double v = a[r * k + c];
-      const uint16_t hi = bf16_rne(v);
-      const uint16_t lo = bf16_rne(v - bf16_value(hi));
-      uint16_t* o = out.data() + r * 3 * k;
-      o[c] = hi;
-      o[k + c] = x_side ? hi : lo;
-      o[2 * k + c] = x_side ? lo : hi;
-    }
+Tensor fp_forward(Context& c, const Tensor& x, const double* w_dev, size_t n) {
+  if (x.rank() != 2) throw std::invalid_argument("matmul_nt: inputs must be 2-D");
+  const size_t m = x.rows(), k = x.cols();
+  const double* xd = upload(c, kX, x.data(), m * k);
+  double* y = c.ws<double>(kY, m * n * 8);
+  check(qarvd_matmul_nt_f64(xd, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), w_dev,
+                            static_cast<int64_t>(n), static_cast<int64_t>(k), y, static_cast<int64_t>(n), c.stream));
+  Tensor out({m, n});
+  d2h(c, out.data(), y, m * n * 8);
+  c.sync();
   return out;
 }
 }  // namespace
 
-double weighted_loss(const std::vector<const CalibSample*>& batch, const LearnableQuantState& state,
-                     const std::vector<double>& chunk_weights) {
-  if (batch.empty()) throw std::invalid_argument("weighted loss: empty batch");
-  const size_t n = state.weight.rows(), k = state.weight.cols();
-  std::vector<int64_t> rows{0}, chunks;
-  for (const CalibSample* s : batch) {
-    if (s->x.cols() != k) throw std::invalid_argument("weighted loss: sample width does not match the weight");
-    rows.push_back(rows.back() + static_cast<int64_t>(s->x.rows()));
-    chunks.push_back(static_cast<int64_t>(s->chunk));
+Tensor CudaQuantizedProvider::forward(const std::string& layer, const Tensor& x) const {
+  const QuantizedLayer& l = qm_.layer(layer);  // std::out_of_range as the reference (engine.cpp:29)
+  Context& c = ctx();
+  if (l.preserved) {
+    if (x.cols() != l.in_dim) throw std::invalid_argument("matmul_nt: shape mismatch");
+    return fp_forward(c, x, fp_.at(layer).get(), l.out_dim);
   }
-  const size_t m = static_cast<size_t>(rows.back());
-  // stacked samples (f64, for K1) and the split bf16 operands of the target
-  std::vector<double> x64(m * k);
-  size_t off = 0;
-  for (const CalibSample* s : batch) {
-    std::memcpy(x64.data() + off, s->x.data(), s->x.size() * sizeof(double));
-    off += s->x.size();
+  if (engine_ == Engine::fakequant_sim) return fakequant_forward(c, x, l.act, fp_.at(layer).get(), l.out_dim);
+  const DeviceLayer& L = *layers_.at(layer);
+  const int8_t* xq = quantize_to_layout(c, L, x, l.act);
+  return gemm_to_host(c, L, l.act, xq, x.rows());
+}
+
+CudaFpProvider::CudaFpProvider(const ToyModel& model) : model_(model) {
+  Context& c = ctx();
+  for (const auto& spec : model.registry()) {
+    const Tensor& w = model.weight(spec.name);
+    double* d = nullptr;
+    check_cuda(cudaMalloc(&d, w.size() * 8));
+    h2d(c, d, w.data(), w.size() * 8);
+    weights_.emplace(spec.name, std::shared_ptr<double>(d, [](double* p) { cudaFree(p); }));
   }
-  const std::vector<uint16_t> xs = split3(x64.data(), m, k, true);
-  const std::vector<uint16_t> ws = split3(state.weight.data(), n, k, false);
-  // deployable state: hard codes in the kernel layout, learned group scales (f32), act scale
-  const Layout L = make_layout(state.plan, k);
-  const IntTensor hc = state.hard_codes();
-  std::vector<int8_t> wq(n * L.k_pad, 0);
-  std::vector<float> so(n), sn(n);
-  for (size_t r = 0; r < n; ++r) {
-    for (size_t c = 0; c < k; ++c) {
-      const size_t pc = state.plan.enabled ? static_cast<size_t>(state.plan.permutation[c]) : c;
-      wq[r * L.k_pad + L.pos[c]] = static_cast<int8_t>(hc.data[r * k + pc]);
-    }
-    sn[r] = static_cast<float>(state.weight_scale(r, false));
-    so[r] = static_cast<float>(state.plan.enabled ? state.weight_scale(r, true) : state.weight_scale(r, false));
-  }
-  const QuantParams act = state.act_params();
-  DevBuf x_dev(xs.data(), xs.size() * 2), w_dev(ws.data(), ws.size() * 2);
-  DevBuf x64_dev(x64.data(), x64.size() * sizeof(double));
-  DevBuf wq_dev(wq.data(), wq.size()), so_dev(so.data(), n * 4), sn_dev(sn.data(), n * 4);
-  DevBuf gather_dev(L.gather.data(), L.gather.size() * 4);
-  DevBuf xq_dev(m * L.k_pad), sx_dev(m * 4), err_dev(sizeof(int64_t));
-  check(qarvd_quantize_act(x64_dev.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(k),
-                           static_cast<int64_t>(k), gather_dev.as<int32_t>(), static_cast<int64_t>(L.k_pad),
-                           QARVD_ACT_PER_TENSOR, act.scale[0], act.bits, xq_dev.as<int8_t>(),
-                           static_cast<int64_t>(L.k_pad), sx_dev.as<float>(), nullptr, err_dev.as<int64_t>(),
-                           nullptr));
-  int64_t bad = 0;
-  check_cuda(cudaMemcpy(&bad, err_dev.p, sizeof(bad), cudaMemcpyDeviceToHost));
-  if (bad != INT64_MAX) throw std::invalid_argument("quantize: non-finite input");
-  const int64_t wsb = qarvd_weighted_loss_workspace(static_cast<int64_t>(m), static_cast<int64_t>(n),
-                                                    static_cast<int64_t>(batch.size()));
-  DevBuf work(static_cast<size_t>(wsb)), err(batch.size() * 8), loss(8);
-  check(qarvd_weighted_loss(x_dev.as<uint16_t>(), static_cast<int64_t>(3 * k), w_dev.as<uint16_t>(),
-                            static_cast<int64_t>(3 * k), xq_dev.as<int8_t>(), static_cast<int64_t>(L.k_pad),
-                            wq_dev.as<int8_t>(), static_cast<int64_t>(L.k_pad), static_cast<int64_t>(m),
-                            static_cast<int64_t>(n), static_cast<int64_t>(3 * k),
-                            static_cast<int64_t>(L.k_pad), static_cast<int64_t>(L.k_outlier),
-                            sx_dev.as<float>(), so_dev.as<float>(), sn_dev.as<float>(), rows.data(),
-                            chunks.data(), static_cast<int64_t>(batch.size()), chunk_weights.data(),
-                            static_cast<int64_t>(chunk_weights.size()), err.as<double>(), loss.as<double>(),
-                            work.p, wsb, nullptr));
-  double out = 0.0;
-  check_cuda(cudaMemcpy(&out, loss.p, 8, cudaMemcpyDeviceToHost));
-  return out;
+  c.sync();
+}
+
+Tensor CudaFpProvider::forward(const std::string& layer, const Tensor& x) const {
+  const Tensor& w = model_.weight(layer);  // the reference's lookup and exception
+  if (x.rank() != 2 || x.cols() != w.cols()) throw std::invalid_argument("matmul_nt: shape mismatch");
+  return fp_forward(ctx(), x, weights_.at(layer).get(), w.rows());
 }
 
 CudaMinMaxFakeQuantProvider::CudaMinMaxFakeQuantProvider(const ToyModel& model, BitwidthScheme scheme,
                                                          std::vector<std::string> keep_list)
-    : model_(model), scheme_(scheme), keep_list_(std::move(keep_list)) {
+    : model_(model), scheme_(scheme), keep_list_(std::move(keep_list)), fp_(model) {
   if (scheme_.is_lossless()) return;
+  Context& c = ctx();
   for (const auto& spec : model.registry()) {
     if (matches_keep_list(spec.name, keep_list_)) continue;
+    // fake_quant(w, init_scale_minmax(w, wb, per_channel, 0)) (toy_model.cpp:312-315), cached
     const Tensor& w = model.weight(spec.name);
     const size_t n = w.rows(), k = w.cols();
-    // K5 on the f64 weight with the single-scale (identity) plan: per-row absmax / qmax scales
-    // (init_scale_minmax per_channel axis 0, quant.cpp:170-182) and nearest codes
-    DualScalePlan plan = build_single_scale_plan(spec.name, w, scheme_.weight_bits);
-    const Layout L = make_layout(plan, k);
-    DevBuf w_d(w.data(), w.size() * 8), g_d(L.gather.data(), L.gather.size() * 4);
-    DevBuf wq_d(n * L.k_pad), so_d(n * 8), sn_d(n * 8), err(8);
-    check(qarvd_prepare_weights(w_d.p, QARVD_F64, static_cast<int64_t>(n), static_cast<int64_t>(k),
-                                static_cast<int64_t>(k), g_d.as<int32_t>(), static_cast<int64_t>(L.k_pad), 0,
-                                scheme_.weight_bits, wq_d.as<int8_t>(), static_cast<int64_t>(L.k_pad),
-                                so_d.as<double>(), sn_d.as<double>(), nullptr, nullptr, err.as<int64_t>(), nullptr));
-    std::vector<int8_t> wq(n * L.k_pad);
-    check_cuda(cudaMemcpy(wq.data(), wq_d.p, wq.size(), cudaMemcpyDeviceToHost));
-    check_cuda(cudaMemcpy(plan.params_normal.scale.data(), sn_d.p, n * 8, cudaMemcpyDeviceToHost));
-    plan.params_outlier = plan.params_normal;
-    QuantizedLayer ql;
-    ql.name = spec.name;
-    ql.out_dim = n;
-    ql.in_dim = k;
-    ql.preserved = false;
-    ql.plan = plan;
-    ql.wq.shape = {n, k};
-    ql.wq.bits = scheme_.weight_bits;
-    ql.wq.data.resize(n * k);
-    for (size_t r = 0; r < n; ++r)
-      for (size_t c = 0; c < k; ++c) ql.wq.data[r * k + c] = wq[r * L.k_pad + L.pos[c]];
-    layers_.emplace(spec.name, std::make_shared<DeviceLayer>(ql));
+    const double* wd = upload(c, kW, w.data(), n * k);
+    double* sd = c.ws<double>(kScales, n * 8);
+    check(qarvd_minmax_scale_f64(wd, static_cast<int64_t>(n * k), static_cast<int64_t>(k), static_cast<int64_t>(n),
+                                 scheme_.weight_bits, sd, c.stream));
+    double* fq = nullptr;
+    check_cuda(cudaMalloc(&fq, n * k * 8));
+    int64_t* err = c.ws<int64_t>(kErr, 8);
+    const int32_t qmax = QuantParams::symmetric_max(scheme_.weight_bits);
+    check(qarvd_quantize_f64(wd, static_cast<int64_t>(n * k), static_cast<int64_t>(k), static_cast<int64_t>(n), sd,
+                             nullptr, -qmax, qmax, nullptr, fq, err, c.stream));
+    int64_t bad = INT64_MAX;
+    d2h(c, &bad, err, 8);
+    c.sync();
+    if (bad != INT64_MAX) {
+      cudaFree(fq);
+      throw std::invalid_argument(nonfinite_msg(bad));
+    }
+    fq_.emplace(spec.name, std::shared_ptr<double>(fq, [](double* p) { cudaFree(p); }));
   }
 }
 
 CudaMinMaxFakeQuantProvider::~CudaMinMaxFakeQuantProvider() = default;
 
 Tensor CudaMinMaxFakeQuantProvider::forward(const std::string& layer, const Tensor& x) const {
-  if (scheme_.is_lossless() || matches_keep_list(layer, keep_list_)) return matmul_nt(x, model_.weight(layer));
-  const DeviceLayer& L = *layers_.at(layer);
-  const size_t m = x.rows();
-  // per-tensor minmax scale = max over rows of K1's exact per-row scales fl(absmax_r / qmax)
-  // (rounding is monotone, so it equals fl(absmax / qmax), quant.cpp:165-168)
-  DevBuf xd(x.data(), x.size() * 8), xq(m * L.layout.k_pad + 16), s_rows(m * 8), err(8);
-  check(qarvd_quantize_act(xd.p, QARVD_F64, static_cast<int64_t>(m), static_cast<int64_t>(x.cols()),
-                           static_cast<int64_t>(x.cols()), L.gather_dev->as<int32_t>(),
-                           static_cast<int64_t>(L.layout.k_pad), QARVD_ACT_PER_TOKEN, 0.0,
-                           scheme_.activation_bits, xq.as<int8_t>(), static_cast<int64_t>(L.layout.k_pad),
-                           nullptr, s_rows.as<double>(), err.as<int64_t>(), nullptr));
-  std::vector<double> sr(m);
-  check_cuda(cudaMemcpy(sr.data(), s_rows.p, m * 8, cudaMemcpyDeviceToHost));
+  if (scheme_.is_lossless() || matches_keep_list(layer, keep_list_)) return fp_.forward(layer, x);
+  const Tensor& w = model_.weight(layer);
+  if (x.rank() != 2 || x.cols() != w.cols()) throw std::invalid_argument("matmul_nt: shape mismatch");
+  // live per-tensor minmax activation params (toy_model.cpp:321-323), all on the device
+  Context& c = ctx();
+  const size_t m = x.rows(), k = x.cols(), n = w.rows();
+  const double* xd = upload(c, kX, x.data(), m * k);
+  double* sd = c.ws<double>(kScales, 8);
+  check(qarvd_minmax_scale_f64(xd, static_cast<int64_t>(m * k), 1, 1, scheme_.activation_bits, sd, c.stream));
+  double* xhat = c.ws<double>(kX2, m * k * 8);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  const int32_t qmax = QuantParams::symmetric_max(scheme_.activation_bits);
+  check(qarvd_quantize_f64(xd, static_cast<int64_t>(m * k), 1, 1, sd, nullptr, -qmax, qmax, nullptr, xhat, err,
+                           c.stream));
+  double* y = c.ws<double>(kY, m * n * 8);
+  check(qarvd_matmul_nt_f64(xhat, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k),
+                            fq_.at(layer).get(), static_cast<int64_t>(n), static_cast<int64_t>(k), y,
+                            static_cast<int64_t>(n), c.stream));
+  int64_t bad = INT64_MAX;
   double s = 0.0;
-  for (double v : sr) s = std::max(s, v);
-  QuantParams act = QuantParams::per_tensor_symmetric(scheme_.activation_bits, s);
-  DevBuf sx(m * 8);
-  quantize_to_device(x, L.layout, *L.gather_dev, act, xq, sx, m);
-  return gemm_to_host(L, xq, sx, m);
+  d2h(c, &bad, err, 8);
+  d2h(c, &s, sd, 8);
+  Tensor out({m, n});
+  d2h(c, out.data(), y, m * n * 8);
+  c.sync();
+  if (!(s > 0.0) || !std::isfinite(s)) throw std::invalid_argument("quant params: scale must be positive and finite");
+  if (bad != INT64_MAX) throw std::invalid_argument(nonfinite_msg(bad));
+  return out;
+}
+
+// ---- rollouts ---------------------------------------------------------------------------
+
+Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed, Engine engine) {
+  const CudaQuantizedProvider provider(qm, engine);
+  return run_rollout(qm.cfg, provider, &provider, QuantTarget::all, 0, prompt_seed);
+}
+
+Rollout rollout(const ToyModel& model, uint64_t prompt_seed, const QuantMode& mode,
+                const std::vector<std::string>& capture_layers) {
+  const CudaFpProvider fp(model);
+  if (mode.target == QuantTarget::none)
+    return run_rollout(model.config(), fp, nullptr, mode.target, mode.chunk, prompt_seed, capture_layers);
+  const CudaMinMaxFakeQuantProvider quant(model, mode.scheme, mode.keep_list);
+  return run_rollout(model.config(), fp, &quant, mode.target, mode.chunk, prompt_seed, capture_layers);
+}
+
+std::vector<CalibSample> collect_calibration(const ToyModel& model, const std::vector<uint64_t>& prompt_seeds,
+                                             const std::vector<std::string>& capture_layers) {
+  if (prompt_seeds.empty()) throw std::invalid_argument("collect_calibration: need at least one prompt seed");
+  for (const auto& name : capture_layers)
+    if (!model.has_layer(name)) throw std::out_of_range("collect_calibration: layer not in registry: " + name);
+  const CudaFpProvider fp(model);
+  std::vector<std::vector<CalibSample>> per_prompt(prompt_seeds.size());
+  parallel_for(prompt_seeds.size(), [&](size_t p) {
+    Rollout r = run_rollout(model.config(), fp, nullptr, QuantTarget::none, 0, prompt_seeds[p], capture_layers);
+    per_prompt[p].reserve(r.captures.size());
+    for (auto& cap : r.captures) per_prompt[p].push_back({cap.layer, cap.chunk, std::move(cap.x)});
+  });
+  std::vector<CalibSample> samples;
+  for (auto& batch : per_prompt)
+    for (auto& s : batch) samples.push_back(std::move(s));
+  return samples;
 }
 
 SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme scheme,
                                        const std::vector<uint64_t>& seeds) {
   if (seeds.empty()) throw std::invalid_argument("profile_sensitivity: need at least one seed");
   const size_t n_chunks = model.config().chunks;
-  const FpProvider fp(model);
+  const CudaFpProvider fp(model);
   const CudaMinMaxFakeQuantProvider quant(model, scheme);
+  // sensitivity.cpp:37-52: references per seed, then every (seed, chunk) probe, each slot written
+  // by exactly one worker (the providers are shared across workers; each worker thread has its
+  // own device context)
   std::vector<Rollout> references(seeds.size());
-  for (size_t s = 0; s < seeds.size(); ++s)
+  parallel_for(seeds.size(), [&](size_t s) {
     references[s] = run_rollout(model.config(), fp, nullptr, QuantTarget::none, 0, seeds[s]);
+  });
   std::vector<std::vector<double>> per_seed(seeds.size(), std::vector<double>(n_chunks, 0.0));
-  for (size_t s = 0; s < seeds.size(); ++s)
-    for (size_t i = 0; i < n_chunks; ++i) {
-      const Rollout probe = run_rollout(model.config(), fp, &quant, QuantTarget::only_chunk, i + 1, seeds[s]);
-      per_seed[s][i] = latent_mse(references[s], probe);
-    }
+  parallel_for(seeds.size() * n_chunks, [&](size_t task) {
+    const size_t s = task / n_chunks, i = task % n_chunks;
+    const Rollout probe = run_rollout(model.config(), fp, &quant, QuantTarget::only_chunk, i + 1, seeds[s]);
+    per_seed[s][i] = latent_mse(references[s], probe);
+  });
   SensitivityProfile profile;
   profile.scheme = scheme;
   profile.seeds = seeds;
@@ -463,6 +892,56 @@ SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme sch
   return profile;
 }
 
+// ---- calibrate.hpp ----------------------------------------------------------------------
+
+double weighted_loss(const std::vector<const CalibSample*>& batch, const LearnableQuantState& state,
+                     const std::vector<double>& chunk_weights) {
+  // weighted_recon_loss(batch, state, w, state.hard_weight()) (calibrate.cpp:201-224): per sample
+  // target = X W^T and pred = FQ(X) What^T as exact f64 products, total += w_chunk ||target - pred||^2
+  if (batch.empty()) throw std::invalid_argument("weighted loss: empty batch");
+  Context& c = ctx();
+  const size_t n = state.weight.rows(), k = state.weight.cols();
+  const DeviceState d = upload_state(c, state, false);
+  double* total = c.ws<double>(kMisc3 + 1, 8);
+  int64_t* err = c.ws<int64_t>(kErr, 8);
+  const int32_t qmax = QuantParams::symmetric_max(state.act_bits);
+  int64_t bad_sample = -1, bad_index = 0;
+  for (size_t b = 0; b < batch.size(); ++b) {
+    const CalibSample* s = batch[b];
+    if (s->chunk < 1 || s->chunk > chunk_weights.size())
+      throw std::out_of_range("weighted loss: sample chunk outside the weight vector");
+    if (s->x.rank() != 2 || s->x.cols() != k) throw std::invalid_argument("matmul_nt: shape mismatch");
+    const size_t m = s->x.rows();
+    const double* xd = upload(c, kX, s->x.data(), m * k);
+    double* tgt = c.ws<double>(kY, m * n * 8);
+    double* xhat = c.ws<double>(kX2, m * k * 8);
+    double* pred = c.ws<double>(kMisc3 + 2, m * n * 8);
+    check(qarvd_matmul_nt_f64(xd, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), d.w,
+                              static_cast<int64_t>(n), static_cast<int64_t>(k), tgt, static_cast<int64_t>(n), c.stream));
+    check(qarvd_quantize_f64(xd, static_cast<int64_t>(m * k), 1, 1, d.act_scale, nullptr, -qmax, qmax, nullptr, xhat,
+                             err, c.stream));
+    check(qarvd_matmul_nt_f64(xhat, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), d.what,
+                              static_cast<int64_t>(n), static_cast<int64_t>(k), pred, static_cast<int64_t>(n),
+                              c.stream));
+    check(qarvd_sq_distance_acc_f64(tgt, pred, static_cast<int64_t>(m * n), chunk_weights[s->chunk - 1], total,
+                                    b > 0 ? 1 : 0, b + 1 == batch.size() ? static_cast<double>(batch.size()) : 0.0,
+                                    c.stream));
+    int64_t bad = INT64_MAX;
+    d2h(c, &bad, err, 8);
+    c.sync();  // the per-sample buffers are reused by the next sample
+    if (bad != INT64_MAX && bad_sample < 0) {
+      bad_sample = static_cast<int64_t>(b);
+      bad_index = bad;
+      break;
+    }
+  }
+  if (bad_sample >= 0) throw std::invalid_argument(nonfinite_msg(bad_index));
+  double out = 0.0;
+  d2h(c, &out, total, 8);
+  c.sync();
+  return out;
+}
+
 LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, const QuantParams& act_init,
                                  const std::vector<const CalibSample*>& samples,
                                  const std::vector<double>& chunk_weights, const CalibConfig& cfg) {
@@ -470,54 +949,58 @@ LayerCalibResult calibrate_layer(const Tensor& w, const DualScalePlan& plan, con
   if (samples.empty()) throw std::invalid_argument("calibrate_layer: no calibration samples");
   if (act_init.per_channel() || act_init.zero_point[0] != 0)
     throw std::invalid_argument("calibrate_layer: the activation init must be per-tensor symmetric");
+  Context& c = ctx();
   const size_t n = w.rows(), k = w.cols();
   std::vector<uint8_t> mask(k, 0);
   if (plan.enabled)
-    for (size_t c : plan.outlier_indices) mask[c] = 1;
+    for (size_t col : plan.outlier_indices) mask[col] = 1;
   std::vector<int64_t> rows{0}, chunks;
   for (const CalibSample* s : samples) {
     if (s->x.cols() != k) throw std::invalid_argument("calibrate_layer: sample width does not match the weight");
     rows.push_back(rows.back() + static_cast<int64_t>(s->x.rows()));
     chunks.push_back(static_cast<int64_t>(s->chunk));
   }
-  std::vector<double> x(static_cast<size_t>(rows.back()) * k);
-  size_t off = 0;
-  for (const CalibSample* s : samples) {
-    std::memcpy(x.data() + off, s->x.data(), s->x.size() * sizeof(double));
-    off += s->x.size();
-  }
   const std::vector<double>& sn = plan.params_normal.scale;
   const std::vector<double>& so = plan.enabled ? plan.params_outlier.scale : plan.params_normal.scale;
-  DevBuf w_d(w.data(), w.size() * 8), mask_d(mask.data(), k), sn_d(sn.data(), n * 8), so_d(so.data(), n * 8);
-  DevBuf x_d(x.data(), x.size() * 8), codes_d(n * k), sn_out(n * 8), so_out(n * 8), sc_out(3 * 8),
-      tr_out(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 1) * 8);
-  qarvd_calib_config c{};
-  c.iterations = cfg.iterations;
-  c.batch_size = cfg.batch_size;
-  c.lr_round = cfg.lr_round;
-  c.lr_scale = cfg.lr_scale;
-  c.seed = cfg.seed;
-  c.train_activation_scale = cfg.train_activation_scale ? 1 : 0;
-  c.zeta = cfg.zeta;
-  c.gamma_lo = cfg.gamma_lo;
-  c.reg_lambda = cfg.reg_lambda;
-  c.beta_start = cfg.beta_start;
-  c.beta_end = cfg.beta_end;
-  c.warmup_frac = cfg.warmup_frac;
-  check(qarvd_calibrate_layer(w_d.as<double>(), static_cast<int64_t>(n), static_cast<int64_t>(k),
-                              mask_d.as<uint8_t>(), plan.enabled ? 1 : 0, sn_d.as<double>(), so_d.as<double>(),
-                              act_init.scale[0], act_init.bits, plan.params_normal.bits, x_d.as<double>(),
-                              rows.data(), chunks.data(), static_cast<int64_t>(samples.size()),
-                              chunk_weights.data(), static_cast<int64_t>(chunk_weights.size()), &c,
-                              plan.layer_name.c_str(), codes_d.as<int8_t>(), sn_out.as<double>(),
-                              so_out.as<double>(), sc_out.as<double>(), tr_out.as<double>(), nullptr));
+  const double* w_d = upload(c, kW, w.data(), n * k);
+  const uint8_t* mask_d = upload(c, kMisc, mask.data(), k);
+  const double* sn_d = upload(c, kScales, sn.data(), n);
+  const double* so_d = upload(c, kScales2, so.data(), n);
+  double* x_d = c.ws<double>(kX, static_cast<size_t>(rows.back()) * k * 8);
+  for (size_t i = 0; i < samples.size(); ++i)
+    h2d(c, x_d + rows[i] * static_cast<int64_t>(k), samples[i]->x.data(), samples[i]->x.size() * 8);
+  int8_t* codes_d = c.ws<int8_t>(kCodes, n * k);
+  double* sn_out = c.ws<double>(kY, n * 8);
+  double* so_out = c.ws<double>(kY2, n * 8);
+  double* sc_out = c.ws<double>(kMisc2, 3 * 8);
+  const size_t iters = static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0);
+  double* tr_out = c.ws<double>(kMisc3, std::max<size_t>(iters, 1) * 8);
+  qarvd_calib_config cc{};
+  cc.iterations = cfg.iterations;
+  cc.batch_size = cfg.batch_size;
+  cc.lr_round = cfg.lr_round;
+  cc.lr_scale = cfg.lr_scale;
+  cc.seed = cfg.seed;
+  cc.train_activation_scale = cfg.train_activation_scale ? 1 : 0;
+  cc.zeta = cfg.zeta;
+  cc.gamma_lo = cfg.gamma_lo;
+  cc.reg_lambda = cfg.reg_lambda;
+  cc.beta_start = cfg.beta_start;
+  cc.beta_end = cfg.beta_end;
+  cc.warmup_frac = cfg.warmup_frac;
+  check(qarvd_calibrate_layer(w_d, static_cast<int64_t>(n), static_cast<int64_t>(k), mask_d, plan.enabled ? 1 : 0,
+                              sn_d, so_d, act_init.scale[0], act_init.bits, plan.params_normal.bits, x_d, rows.data(),
+                              chunks.data(), static_cast<int64_t>(samples.size()), chunk_weights.data(),
+                              static_cast<int64_t>(chunk_weights.size()), &cc, plan.layer_name.c_str(), codes_d,
+                              sn_out, so_out, sc_out, tr_out, c.stream));
   std::vector<int8_t> codes(n * k);
-  std::vector<double> lsn(n), lso(n), sc(3), tr(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0));
-  check_cuda(cudaMemcpy(codes.data(), codes_d.p, n * k, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(lsn.data(), sn_out.p, n * 8, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(lso.data(), so_out.p, n * 8, cudaMemcpyDeviceToHost));
-  check_cuda(cudaMemcpy(sc.data(), sc_out.p, 3 * 8, cudaMemcpyDeviceToHost));
-  if (!tr.empty()) check_cuda(cudaMemcpy(tr.data(), tr_out.p, tr.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<double> lsn(n), lso(n), sc(3), tr(iters);
+  d2h(c, codes.data(), codes_d, n * k);
+  d2h(c, lsn.data(), sn_out, n * 8);
+  d2h(c, lso.data(), so_out, n * 8);
+  d2h(c, sc.data(), sc_out, 3 * 8);
+  d2h(c, tr.data(), tr_out, iters * 8);
+  c.sync();
   LayerCalibResult r;
   r.layer = plan.layer_name;
   // plan_with_learned_scales (calibrate.cpp:185-199)
@@ -542,33 +1025,42 @@ ModelCalibResult calibrate_model(const ToyModel& model, const std::vector<double
   std::vector<std::string> quant_layers;
   for (const auto& spec : model.registry())
     if (!matches_keep_list(spec.name, opts.keep_list)) quant_layers.push_back(spec.name);
-  const std::vector<CalibSample> samples = collect_calibration(model, opts.prompt_seeds, quant_layers);
+  const std::vector<CalibSample> samples = qarvd::cuda::collect_calibration(model, opts.prompt_seeds, quant_layers);
   ModelCalibResult out;
   out.qmodel.cfg = model.config();
   out.qmodel.scheme = opts.base.scheme;
   out.qmodel.keep_list = opts.keep_list;
   out.qmodel.layers.resize(model.registry().size());
+  out.layer_results.resize(quant_layers.size());
+  std::vector<size_t> registry_slot;
   for (size_t li = 0; li < model.registry().size(); ++li) {
     const LayerSpec& spec = model.registry()[li];
-    if (matches_keep_list(spec.name, opts.keep_list)) {  // preserved: bf16 passthrough
-      QuantizedLayer l;
-      l.name = spec.name;
-      l.out_dim = spec.out_dim;
-      l.in_dim = spec.in_dim;
-      l.preserved = true;
-      Tensor fp = model.weight(spec.name);
-      for (size_t i = 0; i < fp.size(); ++i) fp[i] = static_cast<double>(bf16_to_float(float_to_bf16(static_cast<float>(fp[i]))));
-      l.fp_weight = fp;
-      out.qmodel.layers[li] = std::move(l);
+    if (!matches_keep_list(spec.name, opts.keep_list)) {
+      registry_slot.push_back(li);
       continue;
     }
+    // preserved: bf16 passthrough (calibrate.cpp:419-430)
+    QuantizedLayer l;
+    l.name = spec.name;
+    l.out_dim = spec.out_dim;
+    l.in_dim = spec.in_dim;
+    l.preserved = true;
+    Tensor fp = model.weight(spec.name);
+    for (size_t i = 0; i < fp.size(); ++i) fp[i] = static_cast<double>(bf16_to_float(float_to_bf16(static_cast<float>(fp[i]))));
+    l.fp_weight = fp;
+    out.qmodel.layers[li] = std::move(l);
+  }
+  // the reference's slot-indexed parallel_for over layers (calibrate.cpp:440-484); each worker
+  // runs its layers on its own stream: K3 -> plan (K5 scales) -> percentile init -> K7 -> pre-permute
+  parallel_for(quant_layers.size(), [&](size_t qi) {
+    const LayerSpec& spec = model.registry()[registry_slot[qi]];
     const Tensor& w = model.weight(spec.name);
     DualScalePlan plan;
     if (opts.dual_scale) {
       const OutlierReport report = qarvd::cuda::analyze_layer(spec.name, w, opts.tau, opts.alpha_min, opts.align);
-      plan = build_plan(w, report, opts.base.scheme.weight_bits);
+      plan = qarvd::cuda::build_plan(w, report, opts.base.scheme.weight_bits);
     } else {
-      plan = build_single_scale_plan(spec.name, w, opts.base.scheme.weight_bits);
+      plan = qarvd::cuda::build_single_scale_plan(spec.name, w, opts.base.scheme.weight_bits);
     }
     std::vector<const CalibSample*> ls;
     std::vector<Tensor> acts;
@@ -577,9 +1069,8 @@ ModelCalibResult calibrate_model(const ToyModel& model, const std::vector<double
         ls.push_back(&smp);
         acts.push_back(smp.x);
       }
-    // percentile activation init of the f64 captures (quant.cpp:190-226; the GPU search, K4,
-    // works on bf16 bit-pattern histograms)
-    const PercentileSearchResult act_init = init_scale_percentile_search(acts, opts.base.scheme.activation_bits);
+    const PercentileSearchResult act_init =
+        qarvd::cuda::init_scale_percentile_search(acts, opts.base.scheme.activation_bits);
     LayerCalibResult res = qarvd::cuda::calibrate_layer(w, plan, act_init.params, ls, chunk_weights, opts.base);
     QuantizedLayer l;
     l.name = spec.name;
@@ -590,19 +1081,24 @@ ModelCalibResult calibrate_model(const ToyModel& model, const std::vector<double
     l.act = res.act;
     l.wq.shape = {spec.out_dim, spec.in_dim};
     l.wq.bits = res.codes.bits;
-    l.wq.data.resize(spec.out_dim * spec.in_dim);
-    for (size_t r = 0; r < spec.out_dim; ++r)  // pre-permuted [outlier | normal] (calibrate.cpp:474-480)
-      for (size_t pos = 0; pos < spec.in_dim; ++pos)
-        l.wq.data[r * spec.in_dim + pos] = res.codes.at(r, res.plan.permutation[pos]);
-    out.qmodel.layers[li] = std::move(l);
-    out.layer_results.push_back(std::move(res));
-  }
+    // pre-permuted [outlier | normal] codes (calibrate.cpp:474-480) through the device gather
+    {
+      Context& c = ctx();
+      const size_t n = spec.out_dim, k = spec.in_dim;
+      const int32_t* cd = upload(c, kCodes, res.codes.data.data(), n * k);
+      std::vector<int32_t> idx(res.plan.permutation.begin(), res.plan.permutation.end());
+      const int32_t* id = upload(c, kIdx, idx.data(), k);
+      int32_t* pd = c.ws<int32_t>(kY, n * k * 4);
+      check(qarvd_gather_columns(cd, static_cast<int64_t>(n), static_cast<int64_t>(k), id, static_cast<int64_t>(k),
+                                 pd, static_cast<int64_t>(k), 4, c.stream));
+      l.wq.data.resize(n * k);
+      d2h(c, l.wq.data.data(), pd, n * k * 4);
+      c.sync();
+    }
+    out.qmodel.layers[registry_slot[qi]] = std::move(l);
+    out.layer_results[qi] = std::move(res);
+  });
   return out;
-}
-
-Rollout run_quantized(const QuantizedModel& qm, uint64_t prompt_seed) {
-  const CudaQuantizedProvider provider(qm);
-  return run_rollout(qm.cfg, provider, &provider, QuantTarget::all, 0, prompt_seed);
 }
 
 }  // namespace cuda

@@ -21,12 +21,16 @@
 // divergence and results stay on the device until the end.
 #include <cublas_v2.h>
 
+#include <map>
+
 #include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "crmath.cuh"
+#include "libm_ref.cuh"
 
 namespace qarvd_b200 {
 namespace {
@@ -59,13 +63,14 @@ inline unsigned blocks_for(int64_t n) {
   return static_cast<unsigned>(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
 }
 
-__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+// sigmoid (calibrate.cpp:18) with the reference's own exp (libm_ref.cuh: glibc's algorithm, bit for bit)
+__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + libm::exp(-x)); }
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
 // weight_scale(r, outlier_group) = exp(log scale) (calibrate.cpp:117-119); log_s = [normal n | outlier n]
 __device__ __forceinline__ double wscale(const double* log_s, int64_t n, int64_t r, bool outl) {
-  return exp(outl ? log_s[n + r] : log_s[r]);
+  return libm::exp(outl ? log_s[n + r] : log_s[r]);
 }
 
 // LearnableQuantState::init V (calibrate.cpp:96-114): h(V) = frac(w/s), clamped to [1e-4, 1-1e-4]
@@ -81,7 +86,7 @@ __global__ void init_v_kernel(const double* w, const uint8_t* mask, int enabled,
     double frac = ratio - floor(ratio);
     frac = clampd(frac, 1e-4, 1.0 - 1e-4);
     const double p = (frac - gamma) / span;
-    v[i] = log(p / (1.0 - p));
+    v[i] = libm::log(p / (1.0 - p));
   }
 }
 
@@ -118,7 +123,7 @@ __global__ void weights_kernel(const double* w, const double* v, const uint8_t* 
 // in f64; a non-finite input sets *bad (the reference throws)
 __global__ void xhat_kernel(const double* x, int64_t count, const double* log_sa, int qmax,
                             double* xhat, int* bad) {
-  const double s = exp(*log_sa);
+  const double s = libm::exp(*log_sa);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double xv = x[i];
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kMaxGroup * 32) dot_final_kernel(const double*
   if (threadIdx.x != 0) return;
   double total = 0.0;
   for (int i = 0; i < groups; ++i) total += wt.w[i] * gsum[i];
-  if (log_sa) total *= exp(*log_sa);
+  if (log_sa) total *= libm::exp(*log_sa);
   *acc = accumulate ? *acc + total : total;
 }
 
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kT) grad_kernel(const double* gw, const double
       const double h = clampd(pre, 0.0, 1.0);
       const double centered = 2.0 * h - 1.0;
       const double mag = fabs(centered);
-      const double dreg_dh = -2.0 * beta * pow(mag > 1e-12 ? mag : 1e-12, beta - 1.0) *
+      const double dreg_dh = -2.0 * beta * crm::cr_pow(mag > 1e-12 ? mag : 1e-12, beta - 1.0) *
                              (centered >= 0 ? 1.0 : -1.0);
       const double dh_dv = (pre > 0.0 && pre < 1.0) ? span * sig * (1.0 - sig) : 0.0;
       g += reg_lambda * dreg_dh * dh_dv;
@@ -287,17 +292,17 @@ __global__ void adam_kernel(double* p, const double* g, double* m, double* v, in
 __global__ void log_kernel(const double* a, double* out, int64_t count) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = log(a[i]);
+    out[i] = libm::log(a[i]);
 }
 __global__ void exp_kernel(const double* a, double* out, int64_t count) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = exp(a[i]);
+    out[i] = libm::exp(a[i]);
 }
 __global__ void loss_kernel(const double* acc, double inv, double* out) { *out = *acc * inv; }
 __global__ void set_scalars_kernel(double* log_sa, double act_scale, double* best, int* diverged,
                                    int* bad) {
-  *log_sa = log(act_scale);
+  *log_sa = libm::log(act_scale);
   *best = INFINITY;
   *diverged = -1;
   *bad = 0;
@@ -379,7 +384,11 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   if (int st = require_device()) return st;
   cudaStream_t s = as_stream(stream);
 
-  static thread_local cublasHandle_t handle = nullptr;
+  // cuBLAS handles are bound to the device current at creation: one per (thread, device)
+  static thread_local std::map<int, cublasHandle_t> handles;
+  int dev = 0;
+  QARVD_CUDA_TRY(cudaGetDevice(&dev));
+  cublasHandle_t& handle = handles[dev];
   if (!handle) QARVD_CUBLAS_TRY(cublasCreate(&handle));
   QARVD_CUBLAS_TRY(cublasSetStream(handle, s));
   QARVD_CUBLAS_TRY(cublasSetPointerMode(handle, CUBLAS_POINTER_MODE_HOST));
@@ -561,5 +570,29 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   if (fl[0] >= 0)
     QARVD_FAIL(QARVD_ERR_RUNTIME, "calibration diverged for layer " + std::string(layer_name ? layer_name : "") +
                                       " at iteration " + std::to_string(fl[0]));
+  return QARVD_OK;
+}
+
+extern "C" int qarvd_adaround_weights(const double* w, const double* v, const uint8_t* outlier_mask,
+                                      int plan_enabled, const double* log_scale, int64_t n, int64_t k,
+                                      double zeta, double gamma_lo, int w_bits, int hard, double* what,
+                                      int8_t* codes, void* stream) {
+  clear_error();
+  if (n < 0 || k < 0 || w_bits < 2 || w_bits > 8 || (n * k > 0 && (!w || !v || !outlier_mask || !log_scale)))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_adaround_weights: invalid argument");
+  if (int st = require_device()) return st;
+  if (n * k == 0) return QARVD_OK;
+  double* scratch = nullptr;
+  cudaStream_t s = as_stream(stream);
+  if (!what) {
+    QARVD_CUDA_TRY(cudaMallocAsync(&scratch, static_cast<size_t>(n * k) * sizeof(double), s));
+    what = scratch;
+  }
+  const int qmax = (1 << (w_bits - 1)) - 1;
+  weights_kernel<<<blocks_for(n * k), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_scale, n, k, zeta, gamma_lo,
+                                                  -qmax, qmax, hard ? 1 : 0, what, nullptr, nullptr, codes);
+  count_launch();
+  if (scratch) cudaFreeAsync(scratch, s);
+  QARVD_LAUNCH_CHECK();
   return QARVD_OK;
 }

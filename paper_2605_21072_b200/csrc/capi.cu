@@ -3,6 +3,8 @@
 // host-buffer entry for end-to-end use) and the synthetic data generator.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -113,7 +115,7 @@ struct qarvd_linear {
   uint16_t* x_dev = nullptr;
   uint16_t* y_dev = nullptr;
   uint32_t* rowmax = nullptr;  // per-row |y| max for a chained consumer (zero between steps)
-  uint64_t ws_gen = 0;         // bumped whenever the workspace is reallocated
+  uint64_t ws_gen = 0;         // process-unique id of the current workspace allocation
   // host-chain pipelining (owned by the chain's first layer): copy-in / copy-out streams and
   // per-chunk events, created on first use
   cudaStream_t s_in = nullptr, s_out = nullptr, s_cmp = nullptr;
@@ -132,6 +134,21 @@ struct qarvd_linear {
 };
 
 namespace {
+// Workspace ids come from one process-wide counter, so a cached chain graph can never match a
+// handle that was destroyed and re-created at the same address (its buffers are new).
+std::atomic<uint64_t> g_ws_gen{0};
+
+// Capturing cudaMemcpyAsync on pageable host memory is not permitted; only page-locked
+// (cudaMallocHost / cudaHostRegister) buffers take the cached-graph path.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int ensure_workspace(qarvd_linear* L, int64_t m, bool host_io) {
   if (m <= L->cap_m && (!host_io || L->x_dev)) return QARVD_OK;
   const int64_t cap = m > L->cap_m ? m : L->cap_m;
@@ -154,7 +171,7 @@ int ensure_workspace(qarvd_linear* L, int64_t m, bool host_io) {
     QARVD_CUDA_TRY(cudaMalloc(&L->y_dev, static_cast<size_t>(cap) * L->n * 2));
   }
   L->cap_m = cap;
-  ++L->ws_gen;  // cached chain graphs referencing the old buffers are stale
+  L->ws_gen = ++g_ws_gen;  // cached chain graphs referencing the old buffers are stale
   return QARVD_OK;
 }
 
@@ -277,11 +294,19 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
       QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_linear_chain_forward_host: layer widths do not chain");
   if (int st = require_device()) return st;
   cudaStream_t s = as_stream(stream);
+  // Lock each distinct handle once, in address order: a chain may repeat a handle (a square
+  // layer applied twice), and concurrent chains sharing handles must not deadlock.
+  std::vector<qarvd_linear*> locked(layers, layers + num_layers);
+  std::sort(locked.begin(), locked.end());
+  locked.erase(std::unique(locked.begin(), locked.end()), locked.end());
+  for (qarvd_linear* L : locked) L->mu.lock();
+  auto unlock_all = [&]() {
+    for (auto it = locked.rbegin(); it != locked.rend(); ++it) (*it)->mu.unlock();
+  };
   for (int i = 0; i < num_layers; ++i) {
-    layers[i]->mu.lock();
     const int st = ensure_workspace(layers[i], m, true);
     if (st) {
-      for (int j = 0; j <= i; ++j) layers[j]->mu.unlock();
+      unlock_all();
       return st;
     }
   }
@@ -378,7 +403,9 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
   // first-use setup: kernel attributes, occupancy queries), the second captures the whole
   // pipelined sequence -- copies, events, both streams -- into a graph, later calls replay it
   // (one launch instead of ~16 kernel launches and 8 copies; QARVD_HOST_GRAPH=0 disables).
-  static const bool use_graph = !(getenv("QARVD_HOST_GRAPH") && getenv("QARVD_HOST_GRAPH")[0] == '0');
+  static const bool graph_enabled =
+      !(getenv("QARVD_HOST_GRAPH") && getenv("QARVD_HOST_GRAPH")[0] == '0');
+  const bool use_graph = graph_enabled && is_pinned(x_host) && is_pinned(y_host);
   auto& cg = L0->chain_graph;
   std::vector<const qarvd_linear*> key(layers, layers + num_layers);
   std::vector<uint64_t> gens;
@@ -424,7 +451,7 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
     if (L0->s_out) cudaStreamSynchronize(L0->s_out);
     cudaStreamSynchronize(s);
   }
-  for (int i = 0; i < num_layers; ++i) layers[i]->mu.unlock();
+  unlock_all();
   if (st) return st;
   QARVD_CUDA_TRY(e);
   return QARVD_OK;
