@@ -123,6 +123,7 @@ Context& ctx() {
 // workspace slots (one call never uses a slot twice)
 enum Slot : size_t {
   kX, kX2, kXq, kSx, kY, kY2, kW, kW2, kCodes, kScales, kScales2, kIdx, kErr, kMisc, kMisc2, kMisc3,
+  kLoss0, kLoss1, kLayerWq, kLayerSo, kLayerSn, kLayerGather,
 };
 
 void h2d(Context& c, void* dst, const void* src, size_t bytes) {
@@ -177,19 +178,28 @@ std::string nonfinite_msg(int64_t i) { return "quantize: non-finite input at fla
 }  // namespace
 
 // Device-resident copy of one QuantizedLayer: padded int8 codes, f64 group scales, the K1 gather.
+// Owned by a provider (uploaded once), or transient: a free function's per-call copy lives in the
+// calling thread's grow-only workspace slots, so steady-state calls allocate nothing.
 class DeviceLayer {
  public:
-  explicit DeviceLayer(const QuantizedLayer& l)
-      : name(l.name), n(l.out_dim), k(l.in_dim), layout(make_layout(l.plan, l.in_dim)) {
+  explicit DeviceLayer(const QuantizedLayer& l, bool transient = false)
+      : name(l.name), n(l.out_dim), k(l.in_dim), layout(make_layout(l.plan, l.in_dim)), owned(!transient) {
     if (l.preserved) throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + l.name);
     if (l.wq.shape.size() != 2 || l.wq.shape[0] != n || l.wq.shape[1] != k)
       throw std::invalid_argument("kernel_b: weight shape mismatch for " + l.name);
     if (l.wq.bits > 8) throw std::invalid_argument("kernel_b: the CUDA engine stores codes as int8");
     Context& c = ctx();
-    check_cuda(cudaMalloc(&wq, n * layout.k_pad));
-    check_cuda(cudaMalloc(&so, n * 8));
-    check_cuda(cudaMalloc(&sn, n * 8));
-    check_cuda(cudaMalloc(&gather, layout.k_pad * 4));
+    if (owned) {
+      check_cuda(cudaMalloc(&wq, n * layout.k_pad));
+      check_cuda(cudaMalloc(&so, n * 8));
+      check_cuda(cudaMalloc(&sn, n * 8));
+      check_cuda(cudaMalloc(&gather, layout.k_pad * 4));
+    } else {
+      wq = c.ws<int8_t>(kLayerWq, n * layout.k_pad);
+      so = c.ws<double>(kLayerSo, n * 8);
+      sn = c.ws<double>(kLayerSn, n * 8);
+      gather = c.ws<int32_t>(kLayerGather, layout.k_pad * 4);
+    }
     const int32_t* codes = upload(c, kCodes, l.wq.data.data(), n * k);
     const int32_t* pack = upload(c, kIdx, layout.pack.data(), layout.k_pad);
     int* bad = c.ws<int>(kErr, sizeof(int));
@@ -208,6 +218,7 @@ class DeviceLayer {
     if (hbad) throw std::invalid_argument("kernel_b: the CUDA engine stores codes as int8");
   }
   ~DeviceLayer() {
+    if (!owned) return;
     cudaFree(wq);
     cudaFree(so);
     cudaFree(sn);
@@ -223,6 +234,7 @@ class DeviceLayer {
   double* so = nullptr;
   double* sn = nullptr;
   int32_t* gather = nullptr;
+  bool owned;
 };
 
 namespace {
@@ -580,7 +592,7 @@ Tensor kernel_b_gemm_dequant(const IntTensor& xq, const QuantizedLayer& layer) {
     throw std::invalid_argument("kernel_b: layer is preserved, no integer path: " + layer.name);
   if (xq.shape.size() != 2 || xq.shape[1] != layer.in_dim)
     throw std::invalid_argument("kernel_b: activation shape does not match layer " + layer.name);
-  const DeviceLayer L(layer);
+  const DeviceLayer L(layer, /*transient=*/true);
   Context& c = ctx();
   const size_t m = xq.shape[0];
   const int32_t* codes = upload(c, kCodes, xq.data.data(), m * L.k);
@@ -645,7 +657,7 @@ Tensor quantized_layer_forward(const QuantizedLayer& layer, const Tensor& x, Eng
     const double* w = dequant_weight(c, layer, kW);
     return fakequant_forward(c, x, layer.act, w, layer.out_dim);
   }
-  const DeviceLayer L(layer);
+  const DeviceLayer L(layer, /*transient=*/true);
   const int8_t* xq = quantize_to_layout(c, L, x, layer.act);
   return gemm_to_host(c, L, layer.act, xq, x.rows());
 }
@@ -902,7 +914,7 @@ double weighted_loss(const std::vector<const CalibSample*>& batch, const Learnab
   Context& c = ctx();
   const size_t n = state.weight.rows(), k = state.weight.cols();
   const DeviceState d = upload_state(c, state, false);
-  double* total = c.ws<double>(kMisc3 + 1, 8);
+  double* total = c.ws<double>(kLoss0, 8);
   int64_t* err = c.ws<int64_t>(kErr, 8);
   const int32_t qmax = QuantParams::symmetric_max(state.act_bits);
   int64_t bad_sample = -1, bad_index = 0;
@@ -915,7 +927,7 @@ double weighted_loss(const std::vector<const CalibSample*>& batch, const Learnab
     const double* xd = upload(c, kX, s->x.data(), m * k);
     double* tgt = c.ws<double>(kY, m * n * 8);
     double* xhat = c.ws<double>(kX2, m * k * 8);
-    double* pred = c.ws<double>(kMisc3 + 2, m * n * 8);
+    double* pred = c.ws<double>(kLoss1, m * n * 8);
     check(qarvd_matmul_nt_f64(xd, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k), d.w,
                               static_cast<int64_t>(n), static_cast<int64_t>(k), tgt, static_cast<int64_t>(n), c.stream));
     check(qarvd_quantize_f64(xd, static_cast<int64_t>(m * k), 1, 1, d.act_scale, nullptr, -qmax, qmax, nullptr, xhat,
