@@ -203,83 +203,230 @@ def cublas_bf16_ffn_ms(torch, x, w0, w2, iters=10):
     return float(np.median(ts)), float(np.median(gemm_ts))
 
 
-def reference_ffn_sample(layers_host, x64, u64, threads, rows):
-    """Time the reference CPU path (oracle/_ref = compiled reference sources) for `rows` rows
-    of both FFN linears: permute -> kernel A -> kernel B (engine.cpp:137-139)."""
+def ref_layers(ws, gelu_first=False):
+    """Reference-format copies of bf16 weights (f64): the reference's own analyze_layer ->
+    build_plan -> nearest codes (oracle.RefLinear, compiled reference sources)."""
     import oracle
 
-    r = oracle.ref()
-    r.ref_set_threads(threads)
-    total = 0.0
-    ops = 0.0
-    for (spec, wq32, perm, n_o, so, sn, s_x), xin in zip(layers_host, (x64, u64)):
-        xs = np.ascontiguousarray(xin[:rows])
-        secs = r.ref_time_linear(oracle._p(xs), rows, spec.in_dim, oracle._p(wq32), spec.out_dim,
-                                 oracle._p(perm), n_o, 1, oracle._p(so), oracle._p(sn), s_x,
-                                 max(1, rows // (threads * 4)), None)
-        if secs < 0:
-            raise RuntimeError(r.ref_last_error().decode())
-        total += secs
-        ops += 2.0 * rows * spec.out_dim * spec.in_dim
-    return total, ops
+    return [oracle.RefLinear(np.ascontiguousarray(w, dtype=np.float64), gelu_after=(gelu_first and i == 0))
+            for i, w in enumerate(ws)]
 
 
-def host_reference_layers(torch, layers):
-    """Reference-format (int32 codes in the reference's permuted order, f64 scales) copies."""
-    out = []
-    for spec, w, layer, rep in layers:
-        plan = layer.plan
-        wq = layer.wq.cpu().numpy()
-        # reference layout has no pad columns: drop gather == -1 positions
-        keep = plan.gather >= 0
-        wq32 = np.ascontiguousarray(wq[:, keep].astype(np.int32))
-        out.append((spec, wq32, plan.permutation.astype(np.uint32), plan.outlier_count(),
-                    layer.scale_outlier64.cpu().numpy(), layer.scale_normal64.cpu().numpy(), 0.05))
-    return out
+def ref_chain_rate(layers, x64, threads, budget_s, min_rows=None):
+    """int-ops / s of the reference per-token chain (oracle.ref_time_chain_per_token) on a
+    bounded row sample sized to ~budget_s of CPU time; returns (TOPS, rows, seconds)."""
+    import oracle
+
+    min_rows = min_rows or max(2, threads)
+    probe = min(x64.shape[0], min_rows)
+    t = oracle.ref_time_chain_per_token(x64[:probe], layers, threads)
+    rows = int(min(x64.shape[0], max(min_rows, probe * budget_s / max(t, 1e-3))))
+    rows = max(min_rows, (rows // threads) * threads) if rows >= threads else rows
+    t = oracle.ref_time_chain_per_token(x64[:rows], layers, threads)
+    ops = 2.0 * rows * sum(L.n * L.k for L in layers)
+    return ops / t / 1e12, rows, t
 
 
 def run_reference_arm(args, world, rank):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref) on the host cores."""
+    """--impl reference: the reference's own CPU implementation (oracle/_ref: the unmodified
+    reference sources compiled by oracle/Makefile) of the headline workload, on all host cores.
+    Same config as our arm: Wan FFN ffn.0 (GELU) -> ffn.2 at M = 4680 with per-token activation
+    scales (init_scale_minmax(x, 8, per_channel, axis 0), quant.cpp:161-183) and dual-scale
+    weights the reference prepares itself (analyze_layer -> build_plan -> nearest codes), the
+    second linear fed the real GELU'd output of the first.  Inputs come from numpy
+    (oracle.synth_np, the product's synthetic recipe); nothing from paper_2605_21072_b200 is
+    imported on this path.  Each step is a bounded row sample (rows are independent)."""
     if rank != 0:
         return
     import oracle
-    import torch
+    from oracle import synth_np
 
     threads = os.cpu_count() or 1
     line = {"impl": "reference", "metric": METRIC, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8 codes, f64 epilogue (reference)",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "M": M_TOKENS, "parallelism": "cpu threads"}}
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 codes (int32 storage), int64 accumulators, f64 epilogue (reference engine)",
+            "data": "synthetic (Wan-1.3B-shaped bf16-exact weights, 2.1% outlier input channels x8; bf16 N(0,1) activations with heavy channels; numpy)",
+            "config": {"workload": WORKLOAD, "M": M_TOKENS, "activation_quant": "per-token dynamic",
+                       "parallelism": f"reference parallel_for, {threads} host threads"}}
     if not oracle.ref_available():
         line["unavailable"] = "oracle/_ref/libqarvd_ref.so was not built (reference sources absent at build time)"
         print(json.dumps(line))
         return
-    # inputs: same synthetic layers as our arm, generated on the GPU when present, else numpy
-    if torch.cuda.is_available():
-        layers = build_ffn_layers(torch)
-        host = host_reference_layers(torch, layers)
-        from paper_2605_21072_b200 import synth
-        x = synth.synth_activation(M_TOKENS, DIM, seed=7).float().cpu().numpy().astype(np.float64)
-    else:
-        raise SystemExit("reference arm: input generation needs the GPU box")
-    r = np.random.default_rng(0)
-    u = np.abs(r.standard_normal((M_TOKENS, FFN))) * 0.5
-    # size the per-step sample to ~4 s of CPU work
-    t_probe, ops_probe = reference_ffn_sample(host, x, u, threads, 32)
-    rows = int(min(M_TOKENS, max(32, 32 * 4.0 / max(t_probe, 1e-3))))
-    for _ in range(args.warmup):
-        reference_ffn_sample(host, x, u, threads, min(rows, 64))
-    tot_t, tot_ops = 0.0, 0.0
-    for _ in range(args.steps):
-        t, ops = reference_ffn_sample(host, x, u, threads, rows)
-        tot_t += t
-        tot_ops += ops
-    v = tot_ops / tot_t / 1e12
+    w0 = synth_np.weight(FFN, DIM, 8)
+    w2 = synth_np.weight(DIM, FFN, 9)
+    x = synth_np.activation(M_TOKENS, DIM, 7)
+    layers = ref_layers([w0, w2], gelu_first=True)
+    line["config"].update({"ffn0": [FFN, DIM, layers[0].n_outlier], "ffn2": [DIM, FFN, layers[1].n_outlier]})
+    # per-step sample sized so the whole --steps/--warmup run stays within ~2 minutes
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    _, rows, _ = ref_chain_rate(layers, x, threads, max(budget, 0.05))
+    for i in range(args.warmup):
+        oracle.ref_time_chain_per_token(x[:rows], layers, threads)
+    tot_t = 0.0
+    for i in range(args.steps):
+        r0 = (i * rows) % max(1, M_TOKENS - rows + 1)
+        tot_t += oracle.ref_time_chain_per_token(x[r0:r0 + rows], layers, threads)
+    ops = 2.0 * rows * sum(L.n * L.k for L in layers) * args.steps
+    v = ops / tot_t / 1e12
     line.update({"value": v, "ms_per_step": 1e3 * tot_t / args.steps,
                  "cpu_baseline": {"value": v, "unit": "TOPS", "cores": threads, "kind": "reference",
-                                  "sample": f"{rows} of {M_TOKENS} rows of ffn.0 + ffn.2 per step (reference parallel_for row shards)"},
+                                  "sample": f"{rows} of {M_TOKENS} rows of ffn.0 -> GELU -> ffn.2 per step "
+                                            f"(permute -> per-token kernel A -> kernel B, reference parallel_for)"},
                  "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line))
+
+
+def timed_graph(torch, chain, flush, steps):
+    """Mean device ms of `steps` replays of the chain's plain graph (L2 flushed before each)
+    and mean per-kernel ms from its event-node graph."""
+    g_timed = chain.capture(timed=True)
+    evs_k = chain.events
+    chain.capture(timed=False)
+    for _ in range(5):
+        chain.replay()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        chain.replay()
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    kts = []
+    for _ in range(min(steps, 200)):
+        flush.fill_(1)
+        g_timed.replay()
+        evs_k[-1].synchronize()
+        kts.append([evs_k[i].elapsed_time(evs_k[i + 1]) for i in range(len(evs_k) - 1)])
+    return float(np.mean([a.elapsed_time(b) for a, b in evs])), np.mean(np.asarray(kts), axis=0)
+
+
+def event_ms(torch, fn, flush, iters=50):
+    """Median device ms of fn() (L2 flushed before each call)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def single_linear_bench(torch, flush, int8_peak, steps, cpu_baseline=True):
+    """Config 1 (BASELINE.json configs[0]): one dual-scale W8A8 linear 1536 -> 1536 (the
+    self-attn q shape, 2.1% outlier input channels, K_o from K3) at M = 4680 tokens, per-token
+    activations: K1 + K2 as one CUDA graph.  Beside it, at the same shape: cuBLAS bf16
+    (F.linear) and cuBLASLt int8 (torch._int_mm, a single-scale int8 GEMM with no quantize or
+    dequant), and the reference CPU path (1 thread and all cores)."""
+    import torch.nn.functional as F
+    import paper_2605_21072_b200 as qb
+    from paper_2605_21072_b200 import engine, synth
+    from paper_2605_21072_b200.pipeline import QuantizedChain
+
+    spec = synth.wan_registry(blocks=1)[0]
+    w = synth.synth_weight(spec, seed=1)
+    rep = qb.analyze_layer(spec.name, w)
+    layer = engine.prepare_weights(spec.name, w, engine.build_plan(spec.name, spec.in_dim, rep.aligned_outliers))
+    x = synth.synth_activation(M_TOKENS, DIM, seed=21)
+    chain = QuantizedChain([layer], M_TOKENS)
+    chain.x.copy_(x)
+    step_ms, kt = timed_graph(torch, chain, flush, steps)
+    ops = 2.0 * M_TOKENS * spec.out_dim * spec.in_dim
+    k1_ms, k2_ms = float(kt[0]), float(kt[1])
+    cub_ms = event_ms(torch, lambda: F.linear(x, w), flush)
+    xq8 = chain.xq[0][:, :DIM].contiguous()
+    w8 = layer.wq[:, :DIM].contiguous()
+    try:
+        int_mm_ms = event_ms(torch, lambda: torch._int_mm(xq8, w8.t()), flush)
+    except Exception:
+        int_mm_ms = None
+    h = engine.LinearHandle(layer)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((M_TOKENS, spec.out_dim), dtype=torch.bfloat16).pin_memory()
+    for _ in range(3):
+        h.forward_host(xh, yh)
+    e2e = []
+    for _ in range(50):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h.forward_host(xh, yh)
+        e2e.append(1e3 * (time.perf_counter() - t0))
+    h.close()
+    out = {"workload": "single dual-scale W8A8 linear 1536->1536 (block0.self_attn.q), M=4680, per-token",
+           "k_outlier": layer.k_outlier, "ms_per_step": step_ms, "value": ops / (step_ms * 1e-3) / 1e12,
+           "unit": "TOPS", "kernel_ms": {"quant_x": k1_ms, "gemm": k2_ms},
+           "roofline": {"bound": "tensor", "achieved": ops / (k2_ms * 1e-3) / 1e12, "peak": int8_peak,
+                        "unit": "TOPS", "frac": ops / (k2_ms * 1e-3) / 1e12 / int8_peak,
+                        "peak_source": "qarvd_probe_int8_peak (measured live)",
+                        "target_us_at_60pct": ops / (0.6 * int8_peak * 1e12) * 1e6},
+           "quantize_roofline": {"bound": "hbm", "bytes": M_TOKENS * (DIM * 2 + layer.k_pad + 4),
+                                 "achieved_gbs": M_TOKENS * (DIM * 2 + layer.k_pad + 4) / (k1_ms * 1e-3) / 1e9},
+           "cublas_bf16_ms": cub_ms, "speedup_vs_cublas_bf16_step": cub_ms / step_ms,
+           "speedup_vs_cublas_bf16_gemm": cub_ms / k2_ms,
+           "cublaslt_int8_ms": int_mm_ms,
+           "cublaslt_int8_tops": ops / (int_mm_ms * 1e-3) / 1e12 if int_mm_ms else None,
+           "e2e": {"value": ops / (float(np.median(e2e)) * 1e-3) / 1e12, "unit": "TOPS",
+                   "ms_per_step": float(np.median(e2e)), "h2d_bytes_per_step": M_TOKENS * DIM * 2,
+                   "d2h_bytes_per_step": M_TOKENS * DIM * 2, "path": "qarvd_linear_forward_host (C-ABI)"}}
+    if cpu_baseline:
+        try:
+            layers = ref_layers([w.double().cpu().numpy()])
+            x64 = x.double().cpu().numpy()
+            all_c = os.cpu_count() or 1
+            v1, rows1, _ = ref_chain_rate(layers, x64, 1, 5.0)
+            va, rowsa, _ = ref_chain_rate(layers, x64, all_c, 8.0)
+            out["cpu_baseline"] = {"value": va, "unit": "TOPS", "cores": all_c, "kind": "reference",
+                                   "value_1_thread": v1,
+                                   "sample": f"{rowsa} (all cores) / {rows1} (1 thread) of {M_TOKENS} rows: "
+                                             "permute -> per-token kernel A -> kernel B"}
+        except Exception as ex:
+            out["cpu_baseline"] = {"error": str(ex)}
+    return out
+
+
+def cpu_baselines_stack_rollouts(torch, threads):
+    """Reference CPU baselines for configs 3 and 5.  Config 3: per-row costs of a
+    1536 -> 1536 linear and of the ffn.0 -> GELU -> ffn.2 pair through the reference per-token path,
+    extrapolated to the 30-block stack (per block 6 square linears on 4680 tokens, 2 on the 512
+    text tokens, the FFN on 4680).  Config 5: Wan-shaped CPU rollouts are infeasible (the stack
+    alone is hours), so the reference's own toy run_quantized rollouts (8 seeds, 7 chunks x 4
+    steps, QuantizedProvider(int)) are timed instead."""
+    import oracle
+    from paper_2605_21072_b200 import synth
+
+    if not oracle.ref_available():
+        return None
+    spec_q = synth.wan_registry(blocks=1)[0]
+    specs = [s for s in synth.wan_registry(blocks=1) if s.name.startswith("block0.ffn")]
+    wq = synth.synth_weight(spec_q, seed=1).double().cpu().numpy()
+    w0, w2 = (synth.synth_weight(s, seed=1).double().cpu().numpy() for s in specs)
+    x64 = synth.synth_activation(M_TOKENS, DIM, seed=7).double().cpu().numpy()
+    sq = ref_layers([wq])
+    ffn = ref_layers([w0, w2], gelu_first=True)
+    v_sq, rows_sq, t_sq = ref_chain_rate(sq, x64, threads, 4.0)
+    v_ffn, rows_ffn, t_ffn = ref_chain_rate(ffn, x64, threads, 6.0)
+    per_row_sq, per_row_ffn = t_sq / rows_sq, t_ffn / rows_ffn
+    block_s = (6 * M_TOKENS + 2 * synth.WAN_TEXT_LEN) * per_row_sq + M_TOKENS * per_row_ffn
+    stack_s = 30 * block_s
+    stack_ops = 30 * (2.0 * (6 * M_TOKENS + 2 * synth.WAN_TEXT_LEN) * DIM * DIM + 2.0 * M_TOKENS * 2 * DIM * FFN)
+    t_roll = oracle.ref_time_toy_rollouts(8, 8, threads)
+    return {"stack": {"value": stack_ops / stack_s / 1e12, "unit": "TOPS", "cores": threads, "kind": "reference",
+                      "seconds_per_forward_extrapolated": stack_s,
+                      "sample": f"extrapolated: {rows_sq} rows through a 1536x1536 linear and {rows_ffn} rows "
+                                f"through ffn.0 -> GELU -> ffn.2 (per-token), scaled to 30 blocks"},
+            "rollouts": {"value": 8 / t_roll, "unit": "toy rollouts/s", "cores": threads, "kind": "reference",
+                         "sample": "8 toy-shape rollouts (reference run_quantized, QuantizedProvider(int); "
+                                   "hidden 64, 2 blocks, 7 chunks x 4 steps); Wan-shaped CPU rollouts infeasible"}}
 
 
 def calibration_bench(torch, world, rank, steps, hbm_peak):
@@ -564,8 +711,14 @@ def main():
     ap.add_argument("--no-stack", action="store_true")
     ap.add_argument("--stack-steps", type=int, default=10)
     ap.add_argument("--rollouts", type=int, default=8)
+    ap.add_argument("--no-single", action="store_true", help="skip the config-1 single-linear leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Eq. 5 loss and AdaRound legs")
+    ap.add_argument("--ffn-only", action="store_true",
+                    help="headline FFN step only (short command for ncu captures)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.ffn_only:
+        args.no_single = args.no_extras = args.no_calib = args.no_stack = args.no_cpu_baseline = True
     world, rank, local = dist_setup(args.gpus)
 
     if args.impl == "reference":
@@ -663,15 +816,25 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e = float(tt.item())
 
+    # dense INT8 peak at this board's tensor-load clocks (roofline denominator), right after the
+    # timed region so the clocks are comparable
+    int8_peak, int8_probe_ms = _lib.probe_int8_peak()
+    single = None
+    if not args.no_single:
+        single = single_linear_bench(torch, flush, int8_peak, min(args.steps, 1000),
+                                     cpu_baseline=(not args.no_cpu_baseline and world == 1 and rank == 0))
+
     calib = None
     if not args.no_calib:
         calib = calibration_bench(torch, world, rank, args.calib_steps, peaks.get("hbm_gbs", 6650.0))
 
-    recon = recon_loss_bench(torch, peaks)
-    try:
-        adaround = adaround_bench(torch)
-    except Exception as ex:  # reported, never fatal
-        adaround = {"error": str(ex)}
+    recon = adaround = None
+    if not args.no_extras:
+        recon = recon_loss_bench(torch, peaks)
+        try:
+            adaround = adaround_bench(torch)
+        except Exception as ex:  # reported, never fatal
+            adaround = {"error": str(ex)}
     torch.cuda.empty_cache()
     stack = None
     if not args.no_stack:
@@ -684,7 +847,7 @@ def main():
         achieved = ops_per_step / (gemm * 1e-3) / 1e12
         quant_bytes = [M_TOKENS * (L.in_dim * 2 + L.k_pad + 4) for L in chain.layers]
         peak_bf16 = peaks.get("bf16_tflops", 1590.0)
-        peak = 2.0 * peak_bf16  # int8 dense rate = 2x bf16 on sm_100 (4.5 vs 2.25 PF datasheet)
+        proxy = 2.0 * peak_bf16  # int8 dense rate = 2x bf16 on sm_100 (4.5 vs 2.25 PF datasheet)
         int8_cublas = int8_peak_cublas(torch)
         cub_ms, cub_gemm_ms = cublas_bf16_ffn_ms(torch, x, w0, w2)
         line = {
@@ -697,12 +860,17 @@ def main():
                        "chain": "ffn.0 output channels folded into ffn.2's plan order (no gather in K1 for U)",
                        "l2": flush.describe() + "; step timed with CUDA events",
                        "parallelism": f"replicas x{world}"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                         "frac": achieved / peak, "traffic": k2_traffic_bytes(),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
+                         "frac": achieved / int8_peak, "traffic": k2_traffic_bytes(),
                          "kernel": "dual_gemm_kernel (K2), both FFN GEMMs",
-                         "peak_source": f"2 x measured bf16 burst {peak_bf16} TF/s ({peaks_src})",
+                         "peak_source": "dense INT8 tensor-pipe issue rate measured live on this GPU "
+                                        "(qarvd_probe_int8_peak: back-to-back tcgen05.mma kind::i8 M128xN256xK32 "
+                                        f"on all SMs, {int8_probe_ms:.1f} ms)",
+                         "frac_of_2x_bf16_measured": achieved / proxy,
+                         "two_x_bf16_measured_tops": proxy,
                          "frac_of_int8_datasheet_4500": achieved / INT8_DATASHEET_TOPS,
-                         "int8_cublas_measured_tops": int8_cublas},
+                         "int8_cublaslt_8192cube_tops": int8_cublas,
+                         "frac_of_cublaslt_int8": achieved / int8_cublas if int8_cublas else None},
             "cublas_bf16": {"ffn_ms": cub_ms, "gemm_ms": cub_gemm_ms,
                             "speedup_ours_gemm_vs_cublas_gemm": cub_gemm_ms / gemm,
                             "speedup_ours_step_vs_cublas_ffn": cub_ms / ms},
@@ -720,6 +888,7 @@ def main():
                     "h2d_bytes_per_step": M_TOKENS * DIM * 2, "d2h_bytes_per_step": M_TOKENS * DIM * 2,
                     "ms_per_step": e2e, "path": "qarvd_linear_chain_forward_host (C-ABI, pinned host buffers)"},
             "gpu_launches": int(launches),
+            "single_linear": single,
             "calibration": calib,
             "stack": stack,
             "recon_loss": recon,
@@ -730,17 +899,16 @@ def main():
             try:
                 import oracle
                 if oracle.ref_available():
-                    host = host_reference_layers(torch, layers)
-                    x64 = x.float().cpu().numpy().astype(np.float64)
-                    u64 = engine.kernel_b_gemm_dequant(*engine.kernel_a_quantize_activation(x, L0)[:2], L0,
-                                                       epilogue=qb.EPI_GELU).float().cpu().numpy().astype(np.float64)
-                    threads = os.cpu_count() or 1
-                    tp, _ = reference_ffn_sample(host, x64, u64, threads, 16)
-                    rows = int(min(M_TOKENS, max(16, 16 * 10.0 / max(tp, 1e-3))))
-                    tcpu, ops = reference_ffn_sample(host, x64, u64, threads, rows)
-                    line["cpu_baseline"] = {"value": ops / tcpu / 1e12, "unit": "TOPS", "cores": threads,
-                                            "kind": "reference",
-                                            "sample": f"{rows} of {M_TOKENS} rows through ffn.0 + ffn.2 (permute -> kernel A -> kernel B), reference parallel_for"}
+                    all_c = os.cpu_count() or 1
+                    rl = ref_layers([w0.double().cpu().numpy(), w2.double().cpu().numpy()], gelu_first=True)
+                    x64 = x.double().cpu().numpy()
+                    v1, rows1, _ = ref_chain_rate(rl, x64, 1, 8.0)
+                    va, rowsa, _ = ref_chain_rate(rl, x64, all_c, 15.0)
+                    line["cpu_baseline"] = {"value": va, "unit": "TOPS", "cores": all_c, "kind": "reference",
+                                            "value_1_thread": v1,
+                                            "sample": f"{rowsa} (all cores) / {rows1} (1 thread) of {M_TOKENS} rows "
+                                                      "through ffn.0 -> GELU -> ffn.2 (permute -> per-token kernel A "
+                                                      "-> kernel B, reference parallel_for row shards)"}
             except Exception as ex:  # reported, never fatal
                 line["cpu_baseline"] = {"error": str(ex)}
             try:
@@ -748,9 +916,19 @@ def main():
                 if extra:
                     if line.get("calibration"):
                         line["calibration"]["cpu_baseline"] = extra["calibration"]
-                    line["recon_loss"]["cpu_baseline"] = extra["recon_loss"]
+                    if line.get("recon_loss"):
+                        line["recon_loss"]["cpu_baseline"] = extra["recon_loss"]
             except Exception as ex:  # reported, never fatal
-                line["recon_loss"]["cpu_baseline"] = {"error": str(ex)}
+                line["cpu_baseline_calib_error"] = str(ex)
+            try:
+                sr = cpu_baselines_stack_rollouts(torch, os.cpu_count() or 1)
+                if sr and line.get("stack"):
+                    line["stack"]["cpu_baseline"] = sr["stack"]
+                    if line["stack"].get("rollouts"):
+                        line["stack"]["rollouts"]["cpu_baseline"] = sr["rollouts"]
+            except Exception as ex:  # reported, never fatal
+                if line.get("stack"):
+                    line["stack"]["cpu_baseline"] = {"error": str(ex)}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

@@ -448,6 +448,12 @@ int qarvd_adaround_weights(const double* w, const double* v, const uint8_t* outl
                            double zeta, double gamma_lo, int w_bits, int hard, double* what,
                            int8_t* codes, void* stream);
 
+/* ---- measurement -----------------------------------------------------------
+ * Dense INT8 tensor-pipe peak at the clocks this board holds under tensor load: back-to-back
+ * tcgen05.mma kind::i8 M128xN256xK32 on every SM from shared memory (no memory traffic), timed
+ * with CUDA events over `iters` x 4 MMAs per SM (after a short warm-up launch).  Synchronizes. */
+int qarvd_probe_int8_peak(int iters, double* tops_out, double* ms_out, void* stream);
+
 /* ---- synthetic Wan-shaped data (counter-based, deterministic on device) --
  * Follows the reference recipe toy_model.cpp:146-166: Gaussian-like / sqrt(fan_in)
  * weights with a seeded set of input columns scaled by gamma.  Values are

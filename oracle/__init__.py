@@ -107,6 +107,10 @@ def ref():
                                       c_void_p, c_void_p, c_void_p]
         _r.ref_round_half_even.restype = c_double
         _r.ref_round_half_even.argtypes = [c_double]
+        _r.ref_time_chain_per_token.restype = c_double
+        _r.ref_time_chain_per_token.argtypes = [c_void_p, c_int64, c_void_p, c_int, c_int64, c_void_p]
+        _r.ref_time_toy_rollouts.restype = c_double
+        _r.ref_time_toy_rollouts.argtypes = [c_int, c_int]
         _r.ref_time_linear.restype = c_double
         _r.ref_time_linear.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                        c_int64, c_int, c_void_p, c_void_p, c_double, c_int64,
@@ -443,3 +447,57 @@ def ref_qarq_layer(path: str, idx: int):
     _rc(ref().ref_qarq_layer(path.encode(), idx, _p(meta), _p(wq), _p(sn), _p(so), _p(perm), _p(act)))
     out.update(wq=wq, scale_normal=sn, scale_outlier=so, permutation=perm, act_scale=act[0], act_zero=act[1])
     return out
+
+
+# ---- timed reference paths (bench.py's CPU baselines and --impl reference arm) ---------------
+class _ChainLayer(ctypes.Structure):
+    _fields_ = [("wq", c_void_p), ("n", c_int64), ("k", c_int64), ("perm", c_void_p),
+                ("n_outlier", c_int64), ("enabled", c_int), ("s_o", c_void_p), ("s_n", c_void_p),
+                ("gelu_after", c_int)]
+
+
+class RefLinear:
+    """A reference-format quantized linear: ref analyze_layer -> build_plan -> nearest codes
+    (pre-permuted int32), its f64 group scales and permutation."""
+
+    def __init__(self, w64: np.ndarray, gelu_after: bool = False, bits: int = 8):
+        self.n, self.k = w64.shape
+        rep = ref_analyze_layer(w64)
+        self.outliers = np.asarray(rep["aligned"], dtype=np.int64)
+        plan = ref_build_plan_codes(w64, self.outliers, bits)
+        self.wq = np.ascontiguousarray(plan["wq"], dtype=np.int32)
+        self.perm = np.ascontiguousarray(plan["permutation"], dtype=np.uint32)
+        self.s_o = np.ascontiguousarray(plan["scale_outlier"], dtype=np.float64)
+        self.s_n = np.ascontiguousarray(plan["scale_normal"], dtype=np.float64)
+        self.enabled = int(plan["enabled"])
+        self.n_outlier = len(self.outliers) if self.enabled else 0
+        self.gelu_after = int(gelu_after)
+
+
+def ref_time_chain_per_token(x64: np.ndarray, layers, threads: int, rows_per_task: int = 0, want_y=False):
+    """Seconds for the reference CPU path of a chain of per-token quantized linears over the
+    rows of x64 (permute -> per-token kernel A -> kernel B [-> GELU] per layer), row blocks on
+    the reference parallel_for with `threads` workers; optionally the f64 output."""
+    r = ref()
+    r.ref_set_threads(threads)
+    x64 = np.ascontiguousarray(x64, dtype=np.float64)
+    m = x64.shape[0]
+    arr = (_ChainLayer * len(layers))()
+    for i, L in enumerate(layers):
+        arr[i] = _ChainLayer(L.wq.ctypes.data, L.n, L.k, L.perm.ctypes.data, L.n_outlier, L.enabled,
+                             L.s_o.ctypes.data, L.s_n.ctypes.data, L.gelu_after)
+    rpt = rows_per_task or max(1, (m + 4 * threads - 1) // (4 * threads))
+    y = np.empty((m, layers[-1].n)) if want_y else None
+    secs = r.ref_time_chain_per_token(_p(x64), m, ctypes.cast(arr, c_void_p), len(layers), rpt, _p(y))
+    if secs < 0:
+        raise RefError(r.ref_last_error().decode())
+    return (secs, y) if want_y else secs
+
+
+def ref_time_toy_rollouts(iterations: int, n_seeds: int, threads: int) -> float:
+    r = ref()
+    r.ref_set_threads(threads)
+    secs = r.ref_time_toy_rollouts(iterations, n_seeds)
+    if secs < 0:
+        raise RefError(r.ref_last_error().decode())
+    return secs

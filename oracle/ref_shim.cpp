@@ -7,6 +7,7 @@
 // reference CPU arm of bench.py (`--impl reference`).  Never linked into the
 // product library.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -287,6 +288,92 @@ double ref_time_linear(const double* x, int64_t m, int64_t k, const int32_t* wq,
   return secs;
 }
 
+
+// Timed reference CPU path for a CHAIN of quantized linears with per-token activation scales
+// (the BASELINE workloads): for each row, init_scale_minmax(row, 8, per_channel, axis 0)
+// (quant.cpp:161-183) gives the row's scale, then permute_activations -> kernel_a ->
+// kernel_b (engine.cpp:137-139) with that scale (kernel B reads act.scale[0], engine.cpp:57,
+// so per-token = kernel B row by row), an optional erf-GELU between layers
+// (toy_model.cpp:63-67), and the output feeds the next linear.  Row blocks run on the
+// reference parallel_for (rows are independent).  layer l: wq [n_l x k_l] pre-permuted int32,
+// perm [k_l], scales [n_l]; gelu_after[l] != 0 applies GELU to layer l's output.  Returns
+// seconds; y (optional) receives the last layer's f64 output [m x n_last].
+struct ChainLayerArgs {
+  const int32_t* wq;
+  int64_t n, k;
+  const uint32_t* perm;
+  int64_t n_outlier;
+  int enabled;
+  const double* s_o;
+  const double* s_n;
+  int gelu_after;
+};
+double ref_time_chain_per_token(const double* x, int64_t m, const ChainLayerArgs* layers, int n_layers,
+                                int64_t rows_per_task, double* y) {
+  double secs = -1.0;
+  guarded([&] {
+    std::vector<QuantizedLayer> ql;
+    for (int l = 0; l < n_layers; ++l)
+      ql.push_back(make_layer(layers[l].wq, layers[l].n, layers[l].k, layers[l].perm, layers[l].n_outlier,
+                              layers[l].enabled, layers[l].s_o, layers[l].s_n, 1.0));
+    const int64_t k0 = layers[0].k, n_last = layers[n_layers - 1].n;
+    const size_t tasks = static_cast<size_t>((m + rows_per_task - 1) / rows_per_task);
+    const auto t0 = std::chrono::steady_clock::now();
+    parallel_for(tasks, [&](size_t t) {
+      const int64_t r0 = static_cast<int64_t>(t) * rows_per_task;
+      const int64_t r1 = std::min<int64_t>(m, r0 + rows_per_task);
+      Tensor cur({static_cast<size_t>(r1 - r0), static_cast<size_t>(k0)});
+      std::memcpy(cur.data(), x + r0 * k0, sizeof(double) * (r1 - r0) * k0);
+      std::vector<QuantizedLayer> task_layers = ql;  // one copy per task: act is set per row
+      for (int l = 0; l < n_layers; ++l) {
+        QuantizedLayer& layer = task_layers[static_cast<size_t>(l)];
+        const QuantParams per_token = init_scale_minmax(cur, 8, Granularity::per_channel, 0);
+        const Tensor xp = permute_activations(cur, layer.plan);
+        Tensor out({cur.rows(), layer.out_dim});
+        for (size_t i = 0; i < cur.rows(); ++i) {
+          Tensor row({1, layer.in_dim});
+          std::memcpy(row.data(), xp.data() + i * layer.in_dim, sizeof(double) * layer.in_dim);
+          layer.act = QuantParams::per_tensor_symmetric(8, per_token.scale[i]);
+          const Tensor o = kernel_b_gemm_dequant(kernel_a_quantize_activation(row, layer.act), layer);
+          std::memcpy(out.data() + i * layer.out_dim, o.data(), sizeof(double) * layer.out_dim);
+        }
+        if (layers[l].gelu_after)
+          for (size_t e = 0; e < out.size(); ++e) out[e] = 0.5 * out[e] * (1.0 + std::erf(out[e] / std::sqrt(2.0)));
+        cur = std::move(out);
+      }
+      if (y) std::memcpy(y + r0 * n_last, cur.data(), sizeof(double) * cur.size());
+    });
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  return secs;
+}
+
+// Timed reference toy rollouts (config 5 at toy scale): run_quantized (engine.cpp:175-178)
+// through the reference QuantizedProvider(int) for `n_seeds` prompt seeds of a toy model
+// calibrated by the reference calibrate_model (`iterations` AdaRound steps).  Calibration is
+// untimed; the seeds run on the reference parallel_for.  Returns seconds for all rollouts.
+double ref_time_toy_rollouts(int iterations, int n_seeds) {
+  double secs = -1.0;
+  guarded([&] {
+    ToyModelConfig cfg;
+    cfg.injections = {{"ffn.2", 0.05, 8.0}, {"self_attn.q", 0.03, 6.0}};
+    const ToyModel model = ToyModel::build(cfg);
+    SensitivityProfile prof;
+    prof.alpha_raw.assign(cfg.chunks, 1.0);
+    prof.alpha_normalized = normalize_alpha(prof.alpha_raw);
+    ModelCalibOptions opts;
+    opts.base.iterations = iterations;
+    const ModelCalibResult calib =
+        calibrate_model(model, weighting_strategy(prof, WeightingKind::heuristic_exp), opts);
+    std::vector<Rollout> out(static_cast<size_t>(n_seeds));
+    const auto t0 = std::chrono::steady_clock::now();
+    parallel_for(static_cast<size_t>(n_seeds), [&](size_t s) {
+      out[s] = run_quantized(calib.qmodel, 5000 + s, Engine::int_kernels);
+    });
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  return secs;
+}
 }  // extern "C"
 
 // weighted_loss (calibrate.cpp:220-224) on a LearnableQuantState initialised by the reference

@@ -222,6 +222,28 @@ SIGNATURES = {
         c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                 c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                 c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    "qarvd_quantize_f64": (
+        c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, ctypes.c_int32, ctypes.c_int32,
+                c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qarvd_minmax_scale_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p]),
+    "qarvd_percentile_search_f64": (
+        c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "qarvd_matmul_nt_f64": (
+        c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
+    "qarvd_gather_columns": (
+        c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_void_p]),
+    "qarvd_dequant_weight_f64": (
+        c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qarvd_sq_distance_acc_f64": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_int, c_double, c_void_p]),
+    "qarvd_zero_point_correct_f64": (
+        c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int, ctypes.c_int32,
+                c_double, c_void_p, c_void_p, c_void_p]),
+    "qarvd_pack_codes_i8": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
+    "qarvd_exp_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "qarvd_adaround_weights": (
+        c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int64, c_double, c_double, c_int, c_int,
+                c_void_p, c_void_p, c_void_p]),
+    "qarvd_probe_int8_peak": (c_int, [c_int, POINTER(c_double), POINTER(c_double), c_void_p]),
     "qarvd_synth_bf16": (
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double, c_void_p, c_int64, c_double,
@@ -260,3 +282,10 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().qarvd_launch_count())
+
+
+def probe_int8_peak(iters: int = 20000, stream=None):
+    """Dense INT8 tensor-pipe peak measured live (qarvd_probe_int8_peak): (TOPS, ms)."""
+    tops, ms = c_double(), c_double()
+    call("qarvd_probe_int8_peak", iters, ctypes.byref(tops), ctypes.byref(ms), stream)
+    return tops.value, ms.value
