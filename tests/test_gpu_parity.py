@@ -1112,3 +1112,135 @@ def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path):
         assert np.all(np.abs(yd - y_ref) <= 2.0 ** -8 * np.abs(y_ref) + 2.0 ** -22 * mag + 1e-30)
         checked += 1
     assert checked > 0
+
+
+# ---------------------------------------------------------------- full config shapes
+def _bf16_bits(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _verify_chain_rows(chain, rows, ctx_rows):
+    """Every layer of a launched QuantizedChain checked on sampled rows against the oracle:
+    the layer's GPU input rows -> oracle K1 (quantize_act with the layer's gather, per-token)
+    -> oracle kernel B (exact int32 accumulators, both slabs) -> the fp32 epilogue
+    restatement.  K1 codes / scales and the bf16 outputs must be bit-identical; a GELU layer's
+    output (MUFU rcp / ex2 in the device GELU) within one bf16 ulp of erf-GELU on the exact
+    fp32 pre-activation.  Returns (layers checked, elements compared)."""
+    n_el = 0
+    for i, L in enumerate(chain.layers):
+        src = chain._src(i)
+        r = ctx_rows if chain.inputs[i] == -2 else rows
+        x_bits = _bf16_bits(src[r])
+        x64 = oracle.bf16_bits_to_f64(x_bits)
+        g = None if L.gather_dev is None else L.gather_dev.cpu().numpy()
+        q, s64, _ = oracle.quantize_act(x64, g, per_token=True)
+        np.testing.assert_array_equal(chain.xq[i][r].cpu().numpy(), q, err_msg=f"K1 codes, layer {i} {L.name}")
+        np.testing.assert_array_equal(chain.sx[i][r].cpu().numpy(), s64.astype(np.float32),
+                                      err_msg=f"K1 scales, layer {i}")
+        _, ao, an = oracle.kernel_b(q, L.wq.cpu().numpy(), L.k_outlier, s64, L.scale_outlier64.cpu().numpy(),
+                                    L.scale_normal64.cpu().numpy(), with_acc=True)
+        bias = None if L.bias is None else L.bias.cpu().numpy()
+        got = _bf16_bits(chain.y[i][r])
+        if chain.epilogues[i] == qb.EPI_GELU:
+            f32 = oracle.epilogue_f32(ao, an, L.k_outlier > 0, s64.astype(np.float32),
+                                      L.scale_outlier32.cpu().numpy(), L.scale_normal32.cpu().numpy(), bias, out="f32")
+            t = torch.from_numpy(f32).double()
+            ref = (0.5 * t * (1 + torch.erf(t / np.sqrt(2.0)))).float()
+            got_f = torch.from_numpy(got.view(np.int16)).view(torch.bfloat16).float()
+            # one bf16 ulp (2^-7 relative) plus the device GELU's 3.4e-7 absolute error bound
+            assert torch.all((got_f - ref).abs() <= 2.0 ** -7 * ref.abs() + 1e-6), f"GELU layer {i}"
+        else:
+            ref_bits = oracle.epilogue_f32(ao, an, L.k_outlier > 0, s64.astype(np.float32),
+                                           L.scale_outlier32.cpu().numpy(), L.scale_normal32.cpu().numpy(), bias)
+            np.testing.assert_array_equal(got, ref_bits, err_msg=f"K2 output, layer {i} {L.name}")
+        n_el += got.size
+    return len(chain.layers), n_el
+
+
+def test_config3_stack_rows_vs_oracle_chain(cuda):
+    """Config 3 at its real shape: the 30-block Wan stack (300 linears, q/k/v and cross k/v
+    fused as in bench.py, M = 4680, 512 text tokens), replayed from its parallel CUDA graph;
+    64 seeded token rows (and 32 text rows) of every layer vs the oracle chain."""
+    from paper_2605_21072_b200.pipeline import wan_stack_chain
+    chain = wan_stack_chain(fuse_qkv=True)
+    chain.x.copy_(synth.synth_activation(chain.m, synth.WAN_DIM, seed=11))
+    chain.ctx.copy_(synth.synth_activation(synth.WAN_TEXT_LEN, synth.WAN_DIM, seed=13))
+    chain.capture(parallel=True)
+    chain.replay()
+    torch.cuda.synchronize()
+    r = np.random.default_rng(3)
+    rows = torch.from_numpy(np.sort(r.choice(chain.m, 64, replace=False))).cuda()
+    ctx_rows = torch.from_numpy(np.sort(r.choice(synth.WAN_TEXT_LEN, 32, replace=False))).cuda()
+    n_layers, n_el = _verify_chain_rows(chain, rows, ctx_rows)
+    assert n_layers == 30 * 7 and n_el > 64 * 1536 * 200
+
+
+def test_config5_rollout_step_rows_vs_oracle_chain(cuda):
+    """Config 5's batched stack: the 8 rollouts of one GPU batched along M (M = 8 x 4680), one
+    denoising step's stack forward; 64 seeded rows spread over the rollouts vs the oracle chain."""
+    from paper_2605_21072_b200.pipeline import QuantizedChain, wan_stack_chain
+    base = wan_stack_chain(fuse_qkv=True, blocks=6)
+    per = 8
+    rc = QuantizedChain(base.layers, per * base.m, epilogues=base.epilogues, inputs=base.raw_inputs,
+                        ms=[per * mi for mi in base.ms], ctx_rows=per * base.ctx.shape[0])
+    del base
+    rc.x.copy_(synth.synth_activation(rc.x.shape[0], synth.WAN_DIM, seed=1000, frame=0))
+    rc.ctx.copy_(synth.synth_activation(rc.ctx.shape[0], synth.WAN_DIM, seed=17))
+    rc.launch_parallel()
+    torch.cuda.synchronize()
+    r = np.random.default_rng(5)
+    rows = torch.from_numpy(np.sort(r.choice(rc.x.shape[0], 64, replace=False))).cuda()
+    ctx_rows = torch.from_numpy(np.sort(r.choice(rc.ctx.shape[0], 32, replace=False))).cuda()
+    n_layers, _ = _verify_chain_rows(rc, rows, ctx_rows)
+    assert n_layers == 6 * 7
+
+
+@pytest.mark.parametrize("k,seed", [(1536, 1), (8960, 2)])
+def test_k4_full_wan_shape_vs_oracle(cuda, k, seed):
+    """Config 4 at its real shape: one layer's 21 frames x 1560 tokens (K = 1536, and the
+    ffn.2 input width K = 8960: 293 M values), heuristic_exp frame weights; thresholds, scales,
+    losses and the selection bit-identical to the oracle's histogram restatement."""
+    frames, rows = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME
+    xs = torch.cat([synth.synth_activation(rows, k, seed=seed, frame=f) for f in range(frames)])
+    w = calibrate.weighting_strategy("heuristic_exp", frames)
+    res = calibrate.scale_search_async([xs], frames, w).cpu().numpy()[0]
+    bits = _bf16_bits(xs)
+    del xs
+    np.testing.assert_array_equal(res, oracle.scale_search_hist(bits, frames, rows, k, weights=w))
+
+
+def test_k4_full_wan_shape_uniform_vs_reference(cuda, ref_lib):
+    """The uniform-weight limit at 21 x 1560 x 1536 against the compiled reference's
+    init_scale_percentile_search (pooled full sort, quant.cpp:190-226; ~5 s on one core): same
+    percentile, bit-identical scale, candidate MSEs within 1e-12."""
+    frames, rows, k = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME, synth.WAN_DIM
+    xs = torch.cat([synth.synth_activation(rows, k, seed=3, frame=f) for f in range(frames)])
+    res = calibrate.scale_search_async([xs], frames, None).cpu().numpy()[0]
+    x64 = oracle.bf16_bits_to_f64(_bf16_bits(xs))
+    del xs
+    best_pct, scale, mse = oracle.ref_percentile_search(x64, frames, rows, k)
+    assert calibrate.PERCENTILES[int(res[9])] == best_pct
+    assert res[10] == scale
+    np.testing.assert_allclose(res[6:9], mse, rtol=1e-12)
+
+
+def test_percentile_search_f64_full_shape_vs_reference(cuda, ref_lib):
+    """The drop-in's f64 percentile search (qarvd_percentile_search_f64: device radix select of
+    the order statistics + double-double MSEs) on 21 f64 samples of 1560 x 1536 against the
+    compiled reference: same percentile, bit-identical scale and thresholds' scales."""
+    frames, rows, k = synth.WAN_FRAMES, synth.WAN_TOKENS_PER_FRAME, synth.WAN_DIM
+    xs = torch.cat([synth.synth_activation(rows, k, seed=5, frame=f) for f in range(frames)]).double()
+    x64 = xs.cpu().numpy()
+    offs = (np.arange(frames + 1, dtype=np.int64) * rows * k)
+    pct = np.array(calibrate.PERCENTILES, dtype=np.float64)
+    res = torch.empty(3 * len(pct) + 2, dtype=torch.float64, device="cuda")
+    err = torch.empty(2, dtype=torch.int64, device="cuda")
+    qb._lib.call("qarvd_percentile_search_f64", xs.data_ptr(), offs.ctypes.data, frames, pct.ctypes.data, len(pct),
+                 8, res.data_ptr(), err.data_ptr(), None)
+    res = res.cpu().numpy()
+    assert err.cpu().numpy()[0] == -1
+    best_pct, scale, mse = oracle.ref_percentile_search(x64, frames, rows, k)
+    assert pct[int(res[9])] == best_pct and res[10] == scale
+    # the reference sums each sample's 2.4 M squared errors sequentially in f64 (~1e-12 relative
+    # rounding at this length); the device sum is double-double, i.e. the exact sum rounded
+    np.testing.assert_allclose(res[6:9], mse, rtol=1e-10)
