@@ -470,7 +470,25 @@ def calibration_bench(torch, world, rank, steps, hbm_peak):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     total_bytes = sum(costs)
+    native = None
+    if world == 1:  # the C++ multi-GPU driver (one host thread per rank, NCCL all-gather) on this GPU
+        try:
+            nms = []
+            for _ in range(2):
+                del recs
+                recs_n, ms_n, used = calibrate.calibrate_sharded_native(specs, frames, rows, 1,
+                                                                        devices=[torch.cuda.current_device()],
+                                                                        frame_weights=weights)
+                nms.append(ms_n)
+                recs = recs_n
+            native = {"layers_per_s": len(specs) / (min(nms) * 1e-3), "ms_per_calibration": min(nms),
+                      "nccl_allgather": used, "records": len(recs),
+                      "path": "qarvd_calibrate_sharded (C++ host threads, K3 -> plan -> K5 | K4, ncclAllGather)",
+                      "timing": "device time of the calibration unit per rank (inputs resident), max over ranks"}
+        except Exception as ex:  # reported, never fatal
+            native = {"error": str(ex)}
     return {"layers": len(specs), "layers_per_s": len(specs) / (ms * 1e-3), "ms_per_calibration": ms,
+            "native_cpp_driver": native,
             "steps": steps, "frames": frames, "tokens_per_frame": rows, "weighting": "heuristic_exp",
             "records_gathered": len(recs),
             "roofline": {"bound": "hbm", "achieved": total_bytes / world / (ms * 1e-3) / 1e9,

@@ -448,6 +448,43 @@ int qarvd_adaround_weights(const double* w, const double* v, const uint8_t* outl
                            double zeta, double gamma_lo, int w_bits, int hard, double* what,
                            int8_t* codes, void* stream);
 
+/* ---- multi-GPU calibration driver (C++ host, one thread per rank) ---------
+ * Replaces  calibrate_model's slot-indexed parallel_for over layers  calibrate.cpp:440-484,
+ * sharded over GPUs: a deterministic LPT split of the layers by algorithmic bytes (ties ->
+ * lower layer index, lower rank), each rank's share calibrated on devices[rank] with no host
+ * round trip -- K3 (analyze) -> device plan + K5 (weights) on one stream, K4 (frame-weighted
+ * percentile search, quant.cpp:185-226 + sensitivity.cpp:86-112 weights) on another -- then ONE
+ * ncclAllGather of the packed per-layer records over NVLink (communicator over the ranks'
+ * devices; when ranks share a device -- a single-GPU emulation of G ranks -- the records are
+ * gathered through host memory and *used_nccl is 0).  Results do not depend on `world`.
+ * A layer's inputs are host bf16 buffers or, when NULL, generated on the owning GPU by the
+ * counter-based synthetic generator (qarvd_synth_bf16) from its descriptors, so no input
+ * crosses PCIe.  records: f64, one record per layer in layer order:
+ *   [index, n, n_outliers, num_cand, act_scale, best_index, losses[num_cand],
+ *    scale_outlier[n], scale_normal[n], outliers[n_outliers]]
+ * (qarvd_calib_record_doubles gives a record's length); record_offsets [num_layers + 1].
+ * step_ms: max over ranks of the device time of the calibration unit (inputs resident). */
+typedef struct qarvd_synth_desc {
+  uint64_t seed;
+  double stddev;
+  const int32_t* outlier_cols; /* HOST int32 [num_outliers] */
+  int64_t num_outliers;
+  double gamma;
+} qarvd_synth_desc;
+typedef struct qarvd_calib_layer {
+  int64_t index;                   /* registry index (the record key)                        */
+  int64_t n, k, rows;              /* W [n x k]; X = frames consecutive blocks of rows x k    */
+  const uint16_t* w_host;          /* HOST bf16 [n x k], or NULL: generated from w_synth      */
+  qarvd_synth_desc w_synth;
+  const uint16_t* x_host;          /* HOST bf16 [frames*rows x k], or NULL: frame f generated */
+  const qarvd_synth_desc* x_synth; /*   from x_synth[f] (HOST array of frames descriptors)    */
+} qarvd_calib_layer;
+int64_t qarvd_calib_record_doubles(int64_t n, int64_t n_outliers, int num_cand);
+int qarvd_calibrate_sharded(const qarvd_calib_layer* layers, int num_layers, int frames,
+                            const double* frame_weights, const double* percentiles, int num_cand,
+                            int world, const int* devices, double* records, int64_t records_cap,
+                            int64_t* record_offsets, double* step_ms, int* used_nccl);
+
 /* ---- measurement -----------------------------------------------------------
  * Dense INT8 tensor-pipe peak at the clocks this board holds under tensor load: back-to-back
  * tcgen05.mma kind::i8 M128xN256xK32 on every SM from shared memory (no memory traffic), timed

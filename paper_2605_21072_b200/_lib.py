@@ -77,6 +77,17 @@ class OutlierJob(ctypes.Structure):
     ]
 
 
+class SynthDesc(ctypes.Structure):
+    _fields_ = [("seed", c_uint64), ("stddev", c_double), ("outlier_cols", c_void_p),
+                ("num_outliers", c_int64), ("gamma", c_double)]
+
+
+class CalibLayer(ctypes.Structure):
+    _fields_ = [("index", c_int64), ("n", c_int64), ("k", c_int64), ("rows", c_int64),
+                ("w_host", c_void_p), ("w_synth", SynthDesc), ("x_host", c_void_p),
+                ("x_synth", POINTER(SynthDesc))]
+
+
 class SearchJob(ctypes.Structure):
     _fields_ = [
         ("x", c_void_p),
@@ -243,6 +254,10 @@ SIGNATURES = {
     "qarvd_adaround_weights": (
         c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int64, c_double, c_double, c_int, c_int,
                 c_void_p, c_void_p, c_void_p]),
+    "qarvd_calib_record_doubles": (c_int64, [c_int64, c_int64, c_int]),
+    "qarvd_calibrate_sharded": (
+        c_int, [POINTER(CalibLayer), c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int64,
+                c_void_p, POINTER(c_double), POINTER(c_int)]),
     "qarvd_probe_int8_peak": (c_int, [c_int, POINTER(c_double), POINTER(c_double), c_void_p]),
     "qarvd_synth_bf16": (
         c_int,

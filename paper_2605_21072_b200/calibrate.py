@@ -610,3 +610,64 @@ def calibrate_model_adaround(layers: Sequence, samples_of: Callable[[int], Seque
 
     return calibrate_model_sharded(costs, compute, rank, world, group=group, device=device,
                                    unpack=unpack_calib_records)
+
+
+# ---------------------------------------------------------------------------
+# the C++ multi-GPU driver (qarvd_calibrate_sharded): the same calibration unit and records,
+# one host thread per rank, NCCL all-gather of the packed records
+
+def synth_descriptors(spec, frames: int, rows: int, seed: int = 1):
+    """qarvd_calib_layer inputs reproducing CalibrationShard.setup()'s synthetic data exactly
+    (synth.synth_weight / synth.synth_activation streams); keeps the host arrays alive."""
+    from . import synth
+    keep = []
+
+    def desc(seed_, std, cols, gamma):
+        d = _lib.SynthDesc()
+        d.seed, d.stddev, d.gamma = seed_ & synth.M64, float(std), float(gamma)
+        if cols is not None and len(cols) > 0 and gamma != 1.0:
+            a = np.ascontiguousarray(cols, dtype=np.int32)
+            keep.append(a)
+            d.outlier_cols, d.num_outliers = a.ctypes.data, len(a)
+        else:
+            d.outlier_cols, d.num_outliers = None, 0
+        return d
+
+    L = _lib.CalibLayer()
+    L.index, L.n, L.k, L.rows = spec.index, spec.out_dim, spec.in_dim, rows
+    wcols = (synth.pick_outlier_columns(seed, spec.index, spec.in_dim, spec.outlier_fraction)
+             if spec.outlier_fraction > 0 else None)
+    L.w_host, L.x_host = None, None
+    L.w_synth = desc(synth.mix_seed(seed, spec.index), 1.0 / np.sqrt(spec.in_dim), wcols, spec.gamma)
+    s_act = synth.mix_seed(seed, spec.index) ^ synth.K_ACT_SALT
+    heavy = synth.pick_outlier_columns(s_act, 0, spec.in_dim, 0.005)
+    xs = (_lib.SynthDesc * frames)(*[desc(synth.mix_seed(s_act, f + 1), 1.0 + 0.05 * f, heavy, 6.0)
+                                     for f in range(frames)])
+    keep.append(xs)
+    L.x_synth = xs
+    return L, keep
+
+
+def calibrate_sharded_native(specs, frames: int, rows: int, world: int, devices=None, seed: int = 1,
+                             frame_weights=None, percentiles=PERCENTILES):
+    """Config 4 through the C++ driver: returns (records sorted by layer, max-over-ranks step ms,
+    whether the records crossed NCCL)."""
+    from . import synth
+    layers = (_lib.CalibLayer * len(specs))()
+    keep = []
+    cap = 0
+    for i, spec in enumerate(specs):
+        r = rows if spec.tokens != synth.WAN_TEXT_LEN else synth.WAN_TEXT_LEN
+        layers[i], k = synth_descriptors(spec, frames, r, seed)
+        keep.append(k)
+        cap += int(_lib.load().qarvd_calib_record_doubles(spec.out_dim, spec.in_dim, len(percentiles)))
+    devs = np.ascontiguousarray(devices if devices is not None else list(range(world)), dtype=np.int32)
+    pct = np.ascontiguousarray(percentiles, dtype=np.float64)
+    w = None if frame_weights is None else np.ascontiguousarray(frame_weights, dtype=np.float64)
+    recs = np.empty(cap, dtype=np.float64)
+    offs = np.empty(len(specs) + 1, dtype=np.int64)
+    ms, used = _lib.ctypes.c_double(), _lib.ctypes.c_int()
+    _lib.call("qarvd_calibrate_sharded", layers, len(specs), frames, None if w is None else w.ctypes.data,
+              pct.ctypes.data, len(pct), world, devs.ctypes.data, recs.ctypes.data, cap, offs.ctypes.data,
+              _lib.ctypes.byref(ms), _lib.ctypes.byref(used))
+    return unpack_records(recs[:offs[-1]]), ms.value, bool(used.value)
