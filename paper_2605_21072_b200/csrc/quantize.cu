@@ -1334,11 +1334,264 @@ int launch_act_rows_g(const uint16_t* x, int64_t m, int k, int64_t ldx, const in
   QARVD_FAIL(QARVD_ERR_LOGIC, "unsupported K1 team shape");
 }
 
+
+// ---------------------------------------------------------------------------
+// K1, register-resident variant (the default for bf16 rows whose 16-byte chunks split evenly
+// over the team): a team (one warp for rows of <= 2048 values, four teams per CTA; else one CTA
+// of W warps) owns one row and every thread issues all of its V chunk loads at once
+// (ld.global.nc, no L1 allocation), so the whole step's rows are in flight together; the
+// |x| max is a packed 16-bit max over the registers (+ one shared-memory exchange for W > 1),
+// and the codes come straight from the registers (plan-order rows) or from a per-team
+// shared-memory copy through the plan's gather (read as int32 through L1).  One launch per
+// step, no producer warp, no per-row barriers: the previous slot-ring kernel spent half its
+// SM cycles waiting (ncu: 48% SMSP active, long_scoreboard) on a 1-row-per-team grid.
+template <int V, int W, bool kStatic, bool kGather>
+__device__ __noinline__ uint2 act_fix8_reg(uint4 d, ActScale sc, double s64, int qmax);
+template <bool kStatic>
+__device__ __noinline__ uint32_t act_fix4_reg(uint2 hv2, ActScale sc, double s64, int qmax);
+
+template <int V, int W, bool kStatic, bool kGather>
+__global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (32 * W) > 0 ? 1152 / (32 * W) : 1))
+    quant_act_reg_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                         const int32_t* __restrict__ gather, int k_out, double static_scale, int qmax,
+                         double rqmax, int8_t* __restrict__ q, int64_t ldq, float* __restrict__ s32_out,
+                         double* __restrict__ s64_out, unsigned long long* __restrict__ err) {
+  constexpr int kTeams = W == 1 ? 8 : 1;
+  constexpr int T = 32 * W;
+  extern __shared__ __align__(16) uint16_t k1r_smem[];
+  __shared__ uint32_t wmax[W];
+  const int row_stride = (k + 8 + 63) & ~63;
+  const int team = W == 1 ? static_cast<int>(threadIdx.x >> 5) : 0;
+  const int tt = W == 1 ? static_cast<int>(threadIdx.x & 31) : static_cast<int>(threadIdx.x);
+  const int lane = threadIdx.x & 31, warp = tt >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kTeams + team;
+  // the plan's gather as an int16 table, staged once per CTA (pad -> k: the zero sentinel of
+  // every row copy); read through L1 per row it cost more bytes than the row itself
+  int16_t* gidx = reinterpret_cast<int16_t*>(k1r_smem + kTeams * row_stride);
+  if (kGather) {
+    for (int c4 = threadIdx.x; c4 < (k_out >> 2); c4 += blockDim.x) {
+      const int4 g = __ldg(reinterpret_cast<const int4*>(gather) + c4);
+      reinterpret_cast<uint2*>(gidx)[c4] =
+          make_uint2(static_cast<uint16_t>(g.x < 0 ? k : g.x) | (static_cast<uint32_t>(g.y < 0 ? k : g.y) << 16),
+                     static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16));
+    }
+  }
+  pdl_wait();  // x is written by the previous kernel of the chain
+  pdl_launch_dependents();
+  uint4 d[V];
+  const bool live = row < m;
+  if (live) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = ldg_stream(xr + tt + i * T);
+  }
+  if (kGather) __syncthreads();  // the table is staged
+  if (!live) return;  // W > 1: one team per CTA, the whole CTA leaves together
+  uint32_t mx = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+    mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[i].x & 0x7fff7fffu, d[i].y & 0x7fff7fffu),
+                               __vmaxu2(d[i].z & 0x7fff7fffu, d[i].w & 0x7fff7fffu)));
+  uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+  if (W > 1) {
+    if (lane == 0) wmax[warp] = mag;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < W; ++w) mag = max(mag, wmax[w]);
+  }
+  const bool row_bad = mag >= 0x7f80u;
+  const float amax = __uint_as_float(mag << 16);
+  ActScale sc;
+  sc.fq = static_cast<float>(qmax);
+  double s64;
+  if (kStatic) {
+    const GroupScale g = scale_static(static_scale);
+    sc.r = g.r32;
+    sc.exact = g.exact;
+    s64 = static_scale;
+  } else {
+    // r = fl(fl(1/amax) * qmax) and s64 = fl64(amax / qmax): see quant_act_rows_kernel
+    sc.r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+    sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
+    if (!(amax > 0.f)) {
+      s64 = DBL_MIN;
+    } else {
+      const double a = static_cast<double>(amax), y = a * rqmax;
+      s64 = fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
+    }
+  }
+  sc.s64 = s64;
+  if (tt == T - 1) {
+    if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s64) : 0.f;
+    if (s64_out) s64_out[row] = s64;
+  }
+  int8_t* qr = q + row * ldq;
+  if (!kGather) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int c0 = (tt + i * T) * 8;
+      const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
+      uint32_t c[8];
+      if (row_bad || sc.exact) {  // rare rows: non-finite input (reported) or unusable fp32 reciprocal
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          c[h] = act_code_slow(static_cast<uint16_t>(h & 1 ? w[h >> 1] >> 16 : w[h >> 1] & 0xffffu), s64, qmax,
+                               err, row * k_out + c0 + h);
+      } else {
+        float dmax = 0.f;
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
+                              c[2 * h + 1], dmax);
+        if (dmax > tie_guard<kStatic>()) {  // a value within the tie guard: decide exactly
+          *reinterpret_cast<uint2*>(qr + c0) = act_fix8_reg<V, W, kStatic, kGather>(d[i], sc, s64, qmax);
+          continue;
+        }
+      }
+      *reinterpret_cast<uint2*>(qr + c0) = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+    }
+  } else {
+    // per-team row copy (+ 8 zero sentinels that pad slots of the gather read)
+    uint16_t* srow = k1r_smem + team * row_stride;
+#pragma unroll
+    for (int i = 0; i < V; ++i) reinterpret_cast<uint4*>(srow)[tt + i * T] = d[i];
+    if (tt < 8) srow[k + tt] = 0;
+    if (W > 1) __syncthreads();
+    else __syncwarp();
+#pragma unroll 4
+    for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
+      const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+      const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu], srow[gp.y >> 16]};
+      uint32_t c[4];
+      if (row_bad || sc.exact) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[e] = act_code_slow(hv[e], s64, qmax, err, row * k_out + c0 + e);
+      } else {
+        float dmax = 0.f;
+        act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                            __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
+        act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                            __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
+        if (dmax > tie_guard<kStatic>()) {
+          *reinterpret_cast<uint32_t*>(qr + c0) =
+              act_fix4_reg<kStatic>(make_uint2(hv[0] | (static_cast<uint32_t>(hv[1]) << 16),
+                                               hv[2] | (static_cast<uint32_t>(hv[3]) << 16)), sc, s64, qmax);
+          continue;
+        }
+      }
+      *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
+    }
+  }
+}
+
+// exact codes of one flagged 8-value chunk (plan-order rows) / 4 gathered values
+template <int V, int W, bool kStatic, bool kGather>
+__device__ __noinline__ uint2 act_fix8_reg(uint4 d, ActScale sc, double s64, int qmax) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint16_t hv[8];
+  uint32_t c[8];
+  float dmax = 0.f;
+#pragma unroll
+  for (int h = 0; h < 8; ++h) hv[h] = static_cast<uint16_t>(h & 1 ? w[h >> 1] >> 16 : w[h >> 1] & 0xffffu);
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+    act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h], c[2 * h + 1],
+                        dmax);
+  bool rescan = false;
+  act_fix_chunk<kStatic, 8, false>(hv, c, sc, s64, qmax, rescan);
+  if (rescan) act_fix_chunk<kStatic, 8, true>(hv, c, sc, s64, qmax, rescan);
+  return make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+}
+template <bool kStatic>
+__device__ __noinline__ uint32_t act_fix4_reg(uint2 hv2, ActScale sc, double s64, int qmax) {
+  const uint16_t hv[4] = {static_cast<uint16_t>(hv2.x & 0xffffu), static_cast<uint16_t>(hv2.x >> 16),
+                          static_cast<uint16_t>(hv2.y & 0xffffu), static_cast<uint16_t>(hv2.y >> 16)};
+  uint32_t c[4];
+  float dmax = 0.f;
+  act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                      __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
+  act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                      __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
+  bool rescan = false;
+  act_fix_chunk<kStatic, 4, false>(hv, c, sc, s64, qmax, rescan);
+  if (rescan) act_fix_chunk<kStatic, 4, true>(hv, c, sc, s64, qmax, rescan);
+  return pack4(c[0], c[1], c[2], c[3]);
+}
+
+template <int V, int W, bool kStatic, bool kGather>
+int launch_act_reg_t(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather, int k_out,
+                     double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                     unsigned long long* err, cudaStream_t stream) {
+  constexpr int kTeams = W == 1 ? 8 : 1;
+  constexpr int kThreads = W == 1 ? 256 : 32 * W;
+  auto kern = quant_act_reg_kernel<V, W, kStatic, kGather>;
+  const size_t smem =
+      kGather ? static_cast<size_t>(kTeams) * ((k + 8 + 63) & ~63) * 2 + static_cast<size_t>((k_out + 7) & ~7) * 2 : 0;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] { attr = set_smem_attrs(kern, 64 * 1024); });
+  QARVD_CUDA_TRY(attr);
+  const int64_t grid = (m + kTeams - 1) / kTeams;
+  QARVD_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, stream, 1, x, m, k,
+                            ldx, gather, k_out, static_scale, qmax, 1.0 / static_cast<double>(qmax), q, ldq, s32,
+                            s64, err));
+  return QARVD_OK;
+}
+
+// (V chunks per thread, W warps per team) of a row of nvec 16-byte chunks, or {0, 0}
+inline void k1_reg_shape(int nvec, int& V, int& W) {
+  V = W = 0;
+  if (nvec % 32 == 0 && nvec / 32 <= 8) {
+    V = nvec / 32;
+    W = 1;
+    return;
+  }
+  for (int w = 8; w >= 2; --w)
+    if (nvec % (32 * w) == 0 && nvec / (32 * w) <= 8) {
+      V = nvec / (32 * w);
+      W = w;
+      return;
+    }
+}
+
+template <bool kStatic, bool kGather>
+int launch_act_reg(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather, int k_out,
+                   double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                   unsigned long long* err, cudaStream_t stream) {
+  int V, W;
+  k1_reg_shape(k / 8, V, W);
+  switch (W * 16 + V) {
+#define QARVD_K1R_CASE(WW, VV) \
+  case WW * 16 + VV:           \
+    return launch_act_reg_t<VV, WW, kStatic, kGather>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32, s64, err, stream);
+    QARVD_K1R_CASE(1, 1) QARVD_K1R_CASE(1, 2) QARVD_K1R_CASE(1, 3) QARVD_K1R_CASE(1, 4)
+    QARVD_K1R_CASE(1, 5) QARVD_K1R_CASE(1, 6) QARVD_K1R_CASE(1, 7) QARVD_K1R_CASE(1, 8)
+    QARVD_K1R_CASE(4, 3) QARVD_K1R_CASE(4, 4) QARVD_K1R_CASE(4, 5) QARVD_K1R_CASE(4, 6)
+    QARVD_K1R_CASE(5, 5) QARVD_K1R_CASE(5, 6) QARVD_K1R_CASE(6, 5) QARVD_K1R_CASE(6, 6)
+    QARVD_K1R_CASE(7, 4) QARVD_K1R_CASE(7, 5) QARVD_K1R_CASE(7, 6) QARVD_K1R_CASE(8, 4)
+    QARVD_K1R_CASE(8, 5) QARVD_K1R_CASE(8, 6) QARVD_K1R_CASE(8, 7) QARVD_K1R_CASE(8, 8)
+#undef QARVD_K1R_CASE
+  }
+  return -1;  // no register shape: the caller takes the slot-ring kernel
+}
+
 template <bool kStatic>
 int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t ldx,
                     const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
                     int64_t ldq, float* s32, double* s64, unsigned long long* err,
                     cudaStream_t stream) {
+  // register-resident K1 for plan-order rows (measured on the Wan FFN intermediate, M = 4680 x
+  // 8960: 41 vs 45 us; scripts/k1_flush_probe.py); gathered rows keep the slot ring, which the
+  // register kernel does not beat (19.5 vs 18.4 us at 4680 x 1536).  QARVD_K1_REG=0 / =2: never /
+  // always (gathered too).
+  static const int reg = getenv("QARVD_K1_REG") ? atoi(getenv("QARVD_K1_REG")) : 1;
+  if (reg > 0 && (!gathered || (reg == 2 && k_out % 4 == 0))) {
+    const int st = gathered ? launch_act_reg<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
+                                                            ldq, s32, s64, err, stream)
+                            : launch_act_reg<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
+                                                             ldq, s32, s64, err, stream);
+    if (st >= 0) return st;
+  }
   return gathered ? launch_act_rows_g<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
                                                      ldq, s32, s64, err, stream)
                   : launch_act_rows_g<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax,
