@@ -572,7 +572,9 @@ def stack_bench(torch, world, rank, steps, peak, flush, rollouts=0):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rms = float(t.item())
         rops = rc.int_ops() * chunks * tsteps
-        out["rollouts"] = {"workload": f"{per * world} x 7-chunk x 4-step AR rollouts, {per} per GPU batched along M",
+        out["rollouts"] = {"workload": f"linear-stack rollouts: {per * world} x 7-chunk x 4-step AR rollouts of the "
+                                       f"300-linear quantized stack, {per} per GPU batched along M (the denoiser's "
+                                       f"attention / norm / modulation glue is not on the quantized path and is elided)",
                            "rollouts_per_gpu": per, "ms": rms, "int_ops_per_gpu": rops,
                            "value": world * rops / (rms * 1e-3) / 1e12, "unit": "TOPS",
                            "rollouts_per_s": per * world / (rms * 1e-3),

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import heapq
+import os
 from dataclasses import dataclass
 from typing import Callable, Dict, List, Optional, Sequence
 
@@ -358,15 +359,22 @@ class CalibrationShard:
                      (_lib.ctypes.c_double * self.frames)(*[float(v) for v in self.weights]))
                 self._k4.append((jobs, len(idx), pct, nc, w, res))
         search = {}
-        # K3 -> plan -> K5 first: their small CTAs take the SMs before the histogram pass
-        # (one 128 KB CTA per SM) fills the rest of the GPU
+        hist_first = os.environ.get("QARVD_CALIB_ORDER", "hist_first") == "hist_first"
+
+        def k4():
+            with torch.cuda.stream(self._side):
+                for g, (jobs, nj, pct, nc, w, res) in enumerate(self._k4):
+                    _lib.call("qarvd_scale_search_async", jobs, nj, pct, nc, w, 8,
+                              self._flags[g:g + 1].data_ptr(), _stream())
+                    search[g] = res
+        # The K4 histogram pass (one 128 KB-smem CTA per SM, shared-memory-atomic bound, ~64% of
+        # HBM) goes first; K3 -> plan -> K5 then fill the SM resources and HBM bandwidth it leaves
+        if hist_first:
+            k4()
         rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w, out=self._rep)
         _lib.call("qarvd_prepare_weights_planned", self._jobs, len(self.specs), 8, None, _stream())
-        with torch.cuda.stream(self._side):
-            for g, (jobs, nj, pct, nc, w, res) in enumerate(self._k4):
-                _lib.call("qarvd_scale_search_async", jobs, nj, pct, nc, w, 8,
-                          self._flags[g:g + 1].data_ptr(), _stream())
-                search[g] = res
+        if not hist_first:
+            k4()
         main.wait_stream(self._side)
         # results: every field into one pinned host buffer with async copies, one sync
         if not hasattr(self, "_pin"):

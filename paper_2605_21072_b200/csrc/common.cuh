@@ -103,6 +103,14 @@ inline cudaError_t set_smem_attrs(Kernel kern, int dynamic_bytes) {
                               static_cast<int>(cudaSharedmemCarveoutMaxShared));
 }
 
+// Kernels that may run beside a large-shared-memory kernel (e.g. K3 / K5 next to the K4
+// histogram pass) ask for the max-shared carveout too: an SM only hosts CTAs of one carveout.
+template <typename Kernel>
+inline cudaError_t prefer_max_shared(Kernel kern) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              static_cast<int>(cudaSharedmemCarveoutMaxShared));
+}
+
 // ---- bf16 helpers (bit patterns; RNE as bytes.hpp:40-45) -----------------
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t h) {
   return __uint_as_float(static_cast<uint32_t>(h) << 16);

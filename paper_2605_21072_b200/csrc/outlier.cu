@@ -345,6 +345,13 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
                                  cudaMemcpyHostToDevice, s));
   const int64_t blocks_needed = (groups + kNormThreads - 1) / kNormThreads;
   const int grid = static_cast<int>(blocks_needed < kNumSMs * 16 ? blocks_needed : kNumSMs * 16);
+  static const cudaError_t carve = [] {
+    cudaError_t e = prefer_max_shared(column_norms_kernel<uint16_t>);
+    if (e == cudaSuccess) e = prefer_max_shared(column_norms_kernel<float>);
+    if (e == cudaSuccess) e = prefer_max_shared(column_norms_kernel<double>);
+    return e;
+  }();
+  QARVD_CUDA_TRY(carve);
   if (w_dtype == QARVD_BF16)
     column_norms_kernel<uint16_t><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
   else if (w_dtype == QARVD_F32)

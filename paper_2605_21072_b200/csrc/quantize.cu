@@ -1850,6 +1850,8 @@ int launch_prep_batched(const std::vector<WeightJobDev>& fast, int qmax, unsigne
     const int64_t cap = (static_cast<int64_t>(kNumSMs) * 16 + static_cast<int64_t>(sel.size()) - 1) /
                         static_cast<int64_t>(sel.size());
     gx = gx < cap ? gx : (cap < 1 ? 1 : cap);
+    static const cudaError_t carve_prep = prefer_max_shared(prep_weights_batched_kernel);
+    QARVD_CUDA_TRY(carve_prep);
     prep_weights_batched_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(sel.size())),
                                   32 * kWTeams, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
     count_launch();
@@ -1957,6 +1959,8 @@ extern "C" int qarvd_prepare_weights_planned(const qarvd_planned_weight_job* job
   QARVD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_plans), plans.size() * sizeof(PlanJobDev), s));
   QARVD_CUDA_TRY(cudaMemcpyAsync(d_plans, plans.data(), plans.size() * sizeof(PlanJobDev),
                                  cudaMemcpyHostToDevice, s));
+  static const cudaError_t carve_plan = prefer_max_shared(build_plan_kernel);
+  QARVD_CUDA_TRY(carve_plan);
   build_plan_kernel<<<static_cast<unsigned>(plans.size()), kPlanThreads, 0, s>>>(d_plans);
   count_launch();
   QARVD_LAUNCH_CHECK();

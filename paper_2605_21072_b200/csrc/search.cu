@@ -43,15 +43,19 @@ struct HistUnit {
   unsigned long long* err;
 };
 
+// Persistent: one CTA per SM walks a contiguous range of the units (sorted by layer, frame), so
+// after the grid is dispatched the K3 -> K5 kernels queued behind it get the SM resources and the
+// HBM bandwidth the histogram pass leaves (its shared-memory atomics, not HBM, bound it); the
+// shared histogram is flushed to the unit's global histogram only when the target changes.
 __global__ void __launch_bounds__(kHistThreads)
-    hist_kernel(const HistUnit* __restrict__ units) {
+    hist_kernel(const HistUnit* __restrict__ units, int num_units) {
   extern __shared__ uint32_t sh[];
-  const HistUnit u = units[blockIdx.x];
+  const int per = (num_units + gridDim.x - 1) / gridDim.x;
+  const int u0 = blockIdx.x * per, u1 = min(num_units, u0 + per);
+  if (u0 >= u1) return;
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   bool bad = false;
-  const bool vec = ((u.k & 7) == 0) && ((u.ldx & 7) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(u.x) & 15) == 0);
   auto count8 = [&](const uint4 d) {
     const uint32_t w[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
@@ -62,40 +66,52 @@ __global__ void __launch_bounds__(kHistThreads)
       atomicAdd(&sh[hi], 1u);
     }
   };
-  if (vec && u.ldx == u.k) {
-    // contiguous rows: one flat stream of 16-byte chunks (no per-chunk row division)
-    const uint4* p = reinterpret_cast<const uint4*>(u.x);
-    const int64_t total = u.rows * (u.k >> 3);
-    int64_t t = threadIdx.x;
-    for (; t + 3 * blockDim.x < total; t += 4 * blockDim.x) {
-      const uint4 d0 = __ldg(p + t), d1 = __ldg(p + t + blockDim.x), d2 = __ldg(p + t + 2 * blockDim.x),
-                  d3 = __ldg(p + t + 3 * blockDim.x);
-      count8(d0);
-      count8(d1);
-      count8(d2);
-      count8(d3);
+  for (int ui = u0; ui < u1; ++ui) {
+    const HistUnit u = units[ui];
+    const bool vec = ((u.k & 7) == 0) && ((u.ldx & 7) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(u.x) & 15) == 0);
+    if (vec && u.ldx == u.k) {
+      // contiguous rows: one flat stream of 16-byte chunks (no per-chunk row division)
+      const uint4* p = reinterpret_cast<const uint4*>(u.x);
+      const int64_t total = u.rows * (u.k >> 3);
+      int64_t t = threadIdx.x;
+      for (; t + 3 * blockDim.x < total; t += 4 * blockDim.x) {
+        const uint4 d0 = __ldg(p + t), d1 = __ldg(p + t + blockDim.x), d2 = __ldg(p + t + 2 * blockDim.x),
+                    d3 = __ldg(p + t + 3 * blockDim.x);
+        count8(d0);
+        count8(d1);
+        count8(d2);
+        count8(d3);
+      }
+      for (; t < total; t += blockDim.x) count8(__ldg(p + t));
+    } else if (vec) {
+      const int vpr = static_cast<int>(u.k >> 3);  // uint4 per row
+      for (int64_t r = 0; r < u.rows; ++r) {
+        const uint4* p = reinterpret_cast<const uint4*>(u.x + r * u.ldx);
+        for (int v = threadIdx.x; v < vpr; v += blockDim.x) count8(__ldg(p + v));
+      }
+    } else {
+      const int64_t total = u.rows * u.k;
+      for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const int64_t r = t / u.k, c = t - r * u.k;
+        const uint32_t b = u.x[r * u.ldx + c] & 0x7fffu;
+        bad |= b >= kFiniteBins;
+        atomicAdd(&sh[b], 1u);
+      }
     }
-    for (; t < total; t += blockDim.x) count8(__ldg(p + t));
-  } else if (vec) {
-    const int vpr = static_cast<int>(u.k >> 3);  // uint4 per row
-    for (int64_t r = 0; r < u.rows; ++r) {
-      const uint4* p = reinterpret_cast<const uint4*>(u.x + r * u.ldx);
-      for (int v = threadIdx.x; v < vpr; v += blockDim.x) count8(__ldg(p + v));
+    if (bad && u.err) atomicMin(u.err, 0ull);
+    bad = false;
+    if (ui + 1 == u1 || units[ui + 1].hist != u.hist) {  // target changes: flush and clear
+      __syncthreads();
+      for (int i = threadIdx.x; i < kBins; i += blockDim.x) {
+        const uint32_t c = sh[i];
+        if (c) {
+          atomicAdd(&u.hist[i], c);
+          sh[i] = 0;
+        }
+      }
+      __syncthreads();
     }
-  } else {
-    const int64_t total = u.rows * u.k;
-    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
-      const int64_t r = t / u.k, c = t - r * u.k;
-      const uint32_t b = u.x[r * u.ldx + c] & 0x7fffu;
-      bad |= b >= kFiniteBins;
-      atomicAdd(&sh[b], 1u);
-    }
-  }
-  if (bad && u.err) atomicMin(u.err, 0ull);
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += blockDim.x) {
-    const uint32_t c = sh[i];
-    if (c) atomicAdd(&u.hist[i], c);
   }
 }
 
@@ -385,8 +401,9 @@ int scale_search_impl(const qarvd_search_job* jobs, int num_jobs, const double* 
   const int hist_smem = kBins * sizeof(uint32_t);
   QARVD_CUDA_TRY(
       set_smem_attrs(hist_kernel, hist_smem));
-  // grid.x is limited to 2^31-1; units are far fewer
-  hist_kernel<<<static_cast<unsigned>(units.size()), kHistThreads, hist_smem, s>>>(d_units);
+  // persistent grid: one CTA per SM (128 KB of shared memory each)
+  const int hist_grid = static_cast<int>(std::min<size_t>(units.size(), static_cast<size_t>(kNumSMs)));
+  hist_kernel<<<hist_grid, kHistThreads, hist_smem, s>>>(d_units, static_cast<int>(units.size()));
   count_launch();
   QARVD_LAUNCH_CHECK();
 

@@ -130,6 +130,10 @@ class QuantizedLayer:
     act_granularity: int = _lib.ACT_PER_TOKEN
     act_scale: float = 0.0
     bias: Optional[torch.Tensor] = None
+    # asymmetric static activations (QARQ act_symmetric = false, engine.cpp:288-295): codes
+    # clamp(rint(x / s) + z, -2^(b-1), 2^(b-1)-1); the zero-point correction of kernel B
+    # (engine.cpp:74-83, :95-100) is folded into ``bias`` by qarq.to_device
+    act_zero: int = 0
 
     @property
     def k_pad(self) -> int:
@@ -271,6 +275,28 @@ def kernel_a_quantize_activation(x: torch.Tensor, layer_or_plan, granularity: in
     s32 = torch.empty(m, dtype=torch.float32, device=x.device)
     s64 = torch.empty(m, dtype=torch.float64, device=x.device)
     err = torch.empty(1, dtype=torch.int64, device=x.device) if check_finite else None
+    zero = layer_or_plan.act_zero if isinstance(layer_or_plan, QuantizedLayer) else 0
+    if zero != 0:
+        # asymmetric static params: the exact f64 quantizer (quant.cpp:113-138 with z), then the
+        # int8 packing through the plan's gather
+        if granularity != _lib.ACT_PER_TENSOR:
+            raise _lib.InvalidArgument("quant params: a zero point needs per-tensor static activations")
+        sc = torch.full((1,), float(static_scale), dtype=torch.float64, device=x.device)
+        zp = torch.full((1,), int(zero), dtype=torch.int32, device=x.device)
+        codes = torch.empty((m, k), dtype=torch.int32, device=x.device)
+        e = torch.empty(1, dtype=torch.int64, device=x.device)
+        x64 = x.double().contiguous()
+        _lib.call("qarvd_quantize_f64", x64.data_ptr(), m * k, 1, 1, sc.data_ptr(), zp.data_ptr(),
+                  -(1 << (bits - 1)), (1 << (bits - 1)) - 1, codes.data_ptr(), None, e.data_ptr(), _stream())
+        bad = torch.zeros(1, dtype=torch.int32, device=x.device)
+        g = gather_dev if gather_dev is not None else torch.arange(plan.k_pad, dtype=torch.int32, device=x.device)
+        _lib.call("qarvd_pack_codes_i8", codes.data_ptr(), m, k, g.data_ptr(), plan.k_pad, xq.data_ptr(),
+                  plan.k_pad, bad.data_ptr(), _stream())
+        if int(e.item()) != (1 << 63) - 1:
+            raise _lib.InvalidArgument(f"quantize: non-finite input at flat index {int(e.item())}")
+        s32.fill_(float(np.float32(static_scale)))
+        s64.fill_(float(static_scale))
+        return xq, s32, s64
     _lib.call("qarvd_quantize_act", x.data_ptr(), _dtype_code(x), m, k, x.stride(0),
               _ptr(gather_dev), plan.k_pad, granularity, float(static_scale), bits,
               xq.data_ptr(), plan.k_pad, s32.data_ptr(), s64.data_ptr(), _ptr(err), _stream())

@@ -121,8 +121,6 @@ def to_device(L: QarqLayer, device="cuda") -> engine.QuantizedLayer:
     this build's envelope (the reference's own pipeline never writes them)."""
     if L.preserved:
         raise _lib.InvalidArgument(f"kernel_b: layer is preserved, no integer path: {L.name}")
-    if not L.act_symmetric and L.act_zero != 0:
-        raise _lib.Unsupported("asymmetric activation zero points are not implemented")
     outl = (np.sort(L.permutation[:L.outlier_count]).astype(np.int64) if L.permutation is not None
             else np.zeros(0, dtype=np.int64))
     plan = engine.build_plan(L.name, L.in_dim, outl)
@@ -135,7 +133,21 @@ def to_device(L: QarqLayer, device="cuda") -> engine.QuantizedLayer:
     sn = L.scale_normal.astype(np.float64)
     so = L.scale_outlier.astype(np.float64) if L.scale_outlier is not None else sn
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
-    return engine.QuantizedLayer(L.name, L.out_dim, L.in_dim, plan, t(wq, torch.int8), t(so, torch.float64),
-                                 t(sn, torch.float64), t(so.astype(np.float32), torch.float32),
-                                 t(sn.astype(np.float32), torch.float32), t(plan.gather, torch.int32),
-                                 _lib.ACT_PER_TENSOR, float(np.float32(L.act_scale)))
+    layer = engine.QuantizedLayer(L.name, L.out_dim, L.in_dim, plan, t(wq, torch.int8), t(so, torch.float64),
+                                  t(sn, torch.float64), t(so.astype(np.float32), torch.float32),
+                                  t(sn.astype(np.float32), torch.float32), t(plan.gather, torch.int32),
+                                  _lib.ACT_PER_TENSOR, float(np.float32(L.act_scale)))
+    if not L.act_symmetric and L.act_zero != 0:
+        # kernel B's zero-point correction (engine.cpp:74-83, :95-100): the per-column integer
+        # sums of each group, computed once here (the reference precomputes them "offline"),
+        # folded into the epilogue's bias: y = s_x t + (-(z s_x) sum_g s_g[j] colsum_g[j])
+        z, s_x = int(L.act_zero), float(np.float32(L.act_scale))
+        w64 = layer.wq.to(torch.int64)
+        cs_o = w64[:, :plan.k_outlier].sum(1).double()
+        cs_n = w64[:, plan.k_outlier:].sum(1).double()
+        corr = layer.scale_normal64 * (cs_n + (cs_o if n_o == 0 else 0))
+        if n_o > 0:
+            corr = layer.scale_outlier64 * cs_o + layer.scale_normal64 * cs_n
+        layer.bias = (-(z * s_x) * corr).float().contiguous()
+        layer.act_zero = z
+    return layer

@@ -1114,6 +1114,47 @@ def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path):
     assert checked > 0
 
 
+def test_qarq_asymmetric_activations_on_device(cuda, ref_lib, tmp_path):
+    """Asymmetric static activations (QARQ act_symmetric = false with a zero point, the loader
+    branch engine.cpp:288-295): K1 codes clamp(rint(x / s) + z, -128, 127) bit-exact, and the
+    bf16 output against kernel B's f64 formula with the zero-point column-sum correction
+    (engine.cpp:86-100, restated here in f64 from the oracle's exact group accumulators)."""
+    from paper_2605_21072_b200 import qarq
+    path = str(tmp_path / "toy.qarq")
+    oracle.ref_toy_qarq(path, iterations=2)
+    _, layers = qarq.load_qarq(path)
+    checked = 0
+    for i, L in enumerate(layers):
+        if L.preserved:
+            continue
+        L.act_symmetric, L.act_zero = False, (-9 if i % 2 else 13)
+        D = qarq.to_device(L)
+        s_x = float(np.float32(L.act_scale))
+        xb, x64 = bf16_values((29, L.in_dim), seed=50 + i, gamma=3.0)
+        xq, s32, _ = engine.kernel_a_quantize_activation(to_dev_bf16(xb), D, qb.ACT_PER_TENSOR, static_scale=s_x)
+        g = D.plan.gather
+        xg = np.where(g[None, :] >= 0, x64[:, np.maximum(g, 0)], 0.0)
+        codes = np.where(g[None, :] >= 0, np.clip(np.rint(xg / s_x) + L.act_zero, -128, 127), 0).astype(np.int8)
+        np.testing.assert_array_equal(xq.cpu().numpy(), codes)
+        y, acc_o, acc_n = engine.kernel_b_gemm_dequant(xq, s32, D, dump_acc=True)
+        so, sn = D.scale_outlier64.cpu().numpy(), D.scale_normal64.cpu().numpy()
+        w = D.wq.cpu().numpy().astype(np.int64)
+        ao, an = acc_o.cpu().numpy().astype(np.float64), acc_n.cpu().numpy().astype(np.float64)
+        # engine.cpp:86-100: val = sum_g (s_x s_g) acc_g - (z s_x) sum_g s_g colsum_g
+        if D.k_outlier > 0:
+            val = (s_x * so)[None] * ao + (s_x * sn)[None] * an
+            corr = so * w[:, :D.k_outlier].sum(1) + sn * w[:, D.k_outlier:].sum(1)
+        else:
+            val = (s_x * sn)[None] * (ao + an)
+            corr = sn * w.sum(1)
+        y_ref = val - (L.act_zero * s_x) * corr[None]
+        mag = np.abs((s_x * so)[None] * ao) + np.abs((s_x * sn)[None] * an) + np.abs(L.act_zero * s_x * corr)[None]
+        yd = y.float().cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(yd - y_ref) <= 2.0 ** -8 * np.abs(y_ref) + 2.0 ** -22 * mag + 1e-30)
+        checked += 1
+    assert checked > 0
+
+
 # ---------------------------------------------------------------- full config shapes (SURVEY H7)
 def _bf16_bits(t):
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
@@ -1244,3 +1285,23 @@ def test_percentile_search_f64_full_shape_vs_reference(cuda, ref_lib):
     # the reference sums each sample's 2.4 M squared errors sequentially in f64 (~1e-12 relative
     # rounding at this length); the device sum is double-double, i.e. the exact sum rounded
     np.testing.assert_allclose(res[6:9], mse, rtol=1e-10)
+
+
+@pytest.mark.parametrize("bn,cg,ks", [(128, 1, 1), (128, 1, 2), (128, 2, 1), (128, 2, 2), (256, 2, 1), (256, 2, 2)])
+def test_k2_tile_overrides_bitexact(cuda, monkeypatch, bn, cg, ks):
+    """Every tile configuration reachable through QARVD_GEMM_BN / _CG / _KS gives the default
+    configuration's bf16 output bit for bit (config 1 and the FFN-down shape)."""
+    for n, k, n_out in ((1536, 1536, 32), (1536, 8960, 188)):
+        spec = synth.LayerSpec(7, "l", n, k, 4680, n_out / k, 8.0)
+        w = synth.synth_weight(spec, seed=1)
+        L = engine.prepare_weights("l", w, engine.build_plan("l", k, qb.analyze_layer("l", w).aligned_outliers))
+        xq, sx, _ = engine.kernel_a_quantize_activation(synth.synth_activation(1000, k, seed=3), L)
+        ref = engine.kernel_b_gemm_dequant(xq, sx, L)
+        monkeypatch.setenv("QARVD_GEMM_BN", str(bn))
+        monkeypatch.setenv("QARVD_GEMM_CG", str(cg))
+        monkeypatch.setenv("QARVD_GEMM_KS", str(ks))
+        y = engine.kernel_b_gemm_dequant(xq, sx, L)
+        for v in ("QARVD_GEMM_BN", "QARVD_GEMM_CG", "QARVD_GEMM_KS"):
+            monkeypatch.delenv(v)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), ref.view(torch.int16)), (n, k)
