@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -755,22 +756,51 @@ Tensor CudaQuantizedProvider::forward(const std::string& layer, const Tensor& x)
   return gemm_to_host(c, L, l.act, xq, x.rows());
 }
 
+namespace {
+// device copy of `bytes` from `src` (any device or host) on device `dev`
+std::shared_ptr<double> copy_to_device(int dev, const void* src, size_t bytes, bool src_on_device) {
+  int cur = 0;
+  check_cuda(cudaGetDevice(&cur));
+  check_cuda(cudaSetDevice(dev));
+  double* d = nullptr;
+  check_cuda(cudaMalloc(&d, bytes));
+  check_cuda(cudaMemcpy(d, src, bytes, src_on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice));
+  check_cuda(cudaSetDevice(cur));
+  return std::shared_ptr<double>(d, [dev](double* p) {
+    int c = 0;
+    cudaGetDevice(&c);
+    cudaSetDevice(dev);
+    cudaFree(p);
+    cudaSetDevice(c);
+  });
+}
+}  // namespace
+
+const double* DeviceWeights::get(const std::string& name, const std::function<std::shared_ptr<double>(int)>& make) const {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu_);
+  auto& per = by_device_[dev];
+  auto it = per.find(name);
+  if (it == per.end()) it = per.emplace(name, make(dev)).first;
+  return it->second.get();
+}
+
 CudaFpProvider::CudaFpProvider(const ToyModel& model) : model_(model) {
-  Context& c = ctx();
-  for (const auto& spec : model.registry()) {
-    const Tensor& w = model.weight(spec.name);
-    double* d = nullptr;
-    check_cuda(cudaMalloc(&d, w.size() * 8));
-    h2d(c, d, w.data(), w.size() * 8);
-    weights_.emplace(spec.name, std::shared_ptr<double>(d, [](double* p) { cudaFree(p); }));
-  }
-  c.sync();
+  for (const auto& spec : model.registry()) weight_on_device(spec.name);  // upload to the current device
+}
+
+const double* CudaFpProvider::weight_on_device(const std::string& layer) const {
+  return weights_.get(layer, [&](int dev) {
+    const Tensor& w = model_.weight(layer);
+    return copy_to_device(dev, w.data(), w.size() * 8, false);
+  });
 }
 
 Tensor CudaFpProvider::forward(const std::string& layer, const Tensor& x) const {
   const Tensor& w = model_.weight(layer);  // the reference's lookup and exception
   if (x.rank() != 2 || x.cols() != w.cols()) throw std::invalid_argument("matmul_nt: shape mismatch");
-  return fp_forward(ctx(), x, weights_.at(layer).get(), w.rows());
+  return fp_forward(ctx(), x, weight_on_device(layer), w.rows());
 }
 
 CudaMinMaxFakeQuantProvider::CudaMinMaxFakeQuantProvider(const ToyModel& model, BitwidthScheme scheme,
@@ -800,8 +830,20 @@ CudaMinMaxFakeQuantProvider::CudaMinMaxFakeQuantProvider(const ToyModel& model, 
       cudaFree(fq);
       throw std::invalid_argument(nonfinite_msg(bad));
     }
-    fq_.emplace(spec.name, std::shared_ptr<double>(fq, [](double* p) { cudaFree(p); }));
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev));
+    std::shared_ptr<double> owned(fq, [](double* p) { cudaFree(p); });
+    fq_home_.emplace(spec.name, owned);
+    fq_.get(spec.name, [&](int) { return owned; });
   }
+}
+
+const double* CudaMinMaxFakeQuantProvider::fq_on_device(const std::string& layer) const {
+  // other devices get a copy of the cached fake-quantized weights (computed once, above)
+  return fq_.get(layer, [&](int dev) {
+    const Tensor& w = model_.weight(layer);
+    return copy_to_device(dev, fq_home_.at(layer).get(), w.size() * 8, true);
+  });
 }
 
 CudaMinMaxFakeQuantProvider::~CudaMinMaxFakeQuantProvider() = default;
@@ -823,7 +865,7 @@ Tensor CudaMinMaxFakeQuantProvider::forward(const std::string& layer, const Tens
                            c.stream));
   double* y = c.ws<double>(kY, m * n * 8);
   check(qarvd_matmul_nt_f64(xhat, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(k),
-                            fq_.at(layer).get(), static_cast<int64_t>(n), static_cast<int64_t>(k), y,
+                            fq_on_device(layer), static_cast<int64_t>(n), static_cast<int64_t>(k), y,
                             static_cast<int64_t>(n), c.stream));
   int64_t bad = INT64_MAX;
   double s = 0.0;
@@ -871,6 +913,16 @@ std::vector<CalibSample> collect_calibration(const ToyModel& model, const std::v
   return samples;
 }
 
+int sensitivity_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) n = 1;
+  if (const char* e = getenv("QARVD_SENSITIVITY_GPUS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v < n) n = v;
+  }
+  return n;
+}
+
 SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme scheme,
                                        const std::vector<uint64_t>& seeds) {
   if (seeds.empty()) throw std::invalid_argument("profile_sensitivity: need at least one seed");
@@ -880,12 +932,20 @@ SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme sch
   // sensitivity.cpp:37-52: references per seed, then every (seed, chunk) probe, each slot written
   // by exactly one worker (the providers are shared across workers; each worker thread has its
   // own device context)
+  // data-parallel over GPUs: task t runs on device t % G (every worker thread has a device
+  // context per GPU; the providers keep one weight copy per device)
+  int home = 0;
+  check_cuda(cudaGetDevice(&home));
+  const int gpus = sensitivity_devices();
+  auto on_device = [&](size_t task) { check_cuda(cudaSetDevice(static_cast<int>((home + task) % gpus))); };
   std::vector<Rollout> references(seeds.size());
   parallel_for(seeds.size(), [&](size_t s) {
+    on_device(s);
     references[s] = run_rollout(model.config(), fp, nullptr, QuantTarget::none, 0, seeds[s]);
   });
   std::vector<std::vector<double>> per_seed(seeds.size(), std::vector<double>(n_chunks, 0.0));
   parallel_for(seeds.size() * n_chunks, [&](size_t task) {
+    on_device(task);
     const size_t s = task / n_chunks, i = task % n_chunks;
     const Rollout probe = run_rollout(model.config(), fp, &quant, QuantTarget::only_chunk, i + 1, seeds[s]);
     per_seed[s][i] = latent_mse(references[s], probe);

@@ -18,6 +18,7 @@
 // each thread runs on its own stream, results do not depend on the thread count.
 #pragma once
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -109,6 +110,17 @@ class CudaQuantizedProvider : public LinearProvider {
   std::map<std::string, std::shared_ptr<double>> fp_;  // preserved / fakequant_sim f64 weights
 };
 
+// Per-device copies of a provider's f64 weights (created on a device's first use), so one
+// provider serves workers on any GPU.
+class DeviceWeights {
+ public:
+  const double* get(const std::string& name, const std::function<std::shared_ptr<double>(int)>& make) const;
+
+ private:
+  mutable std::mutex mu_;
+  mutable std::map<int, std::map<std::string, std::shared_ptr<double>>> by_device_;
+};
+
 // FpProvider (toy_model.hpp:84-91): X W^T with the exact f64 device product.
 class CudaFpProvider : public LinearProvider {
  public:
@@ -116,8 +128,9 @@ class CudaFpProvider : public LinearProvider {
   Tensor forward(const std::string& layer, const Tensor& x) const override;
 
  private:
+  const double* weight_on_device(const std::string& layer) const;
   const ToyModel& model_;
-  std::map<std::string, std::shared_ptr<double>> weights_;
+  DeviceWeights weights_;
 };
 
 // MinMaxFakeQuantProvider (toy_model.cpp:306-325) on the device: cached fake-quantized weights
@@ -133,12 +146,17 @@ class CudaMinMaxFakeQuantProvider : public LinearProvider {
   const ToyModel& model_;
   BitwidthScheme scheme_;
   std::vector<std::string> keep_list_;
+  const double* fq_on_device(const std::string& layer) const;
   CudaFpProvider fp_;
-  std::map<std::string, std::shared_ptr<double>> fq_;
+  std::map<std::string, std::shared_ptr<double>> fq_home_;  // computed on the constructing device
+  DeviceWeights fq_;
 };
 
 // profile_sensitivity (sensitivity.cpp:29-66): the reference's slot-indexed parallel_for over
-// seeds and (seed, chunk) probes, linears served by CudaFpProvider / CudaMinMaxFakeQuantProvider.
+// seeds and (seed, chunk) probes, linears served by CudaFpProvider / CudaMinMaxFakeQuantProvider,
+// the tasks spread round-robin over the visible GPUs (QARVD_SENSITIVITY_GPUS caps the count);
+// results are identical for any GPU or thread count.
+int sensitivity_devices();
 SensitivityProfile profile_sensitivity(const ToyModel& model, BitwidthScheme scheme,
                                        const std::vector<uint64_t>& seeds);
 
