@@ -10,9 +10,10 @@
 // round-to-nearest intrinsics (no FMA contraction), so norms, median, MAD,
 // threshold and both index sets are bit-identical to the f64 CPU code.
 //
-// Kernel 1 (HBM-bound): one thread owns 8 adjacent columns (one 16-byte bf16
-// load per row, a warp covers 512 contiguous bytes of a row) and accumulates
-// the 8 column sums sequentially over the rows, exactly the reference order.
+// Kernel 1 (HBM-bound): one thread owns 2 adjacent columns (kNormCols; one 4-byte bf16
+// load per row, a warp covers 128 contiguous bytes of a row) and accumulates the two
+// column sums sequentially over the rows, exactly the reference order, with 8 rows of
+// loads (kNormRows) in flight before they are added in order.
 // For bf16/f32 inputs w*w is exact in f64, so the sum is the only rounding.
 // Kernel 2 (tiny): one 1024-thread CTA per layer sorts the K norms (bitonic,
 // shared memory) for the medians and runs the selection / alignment.
