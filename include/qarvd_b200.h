@@ -249,6 +249,17 @@ int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t
                         const double* scale_w_outlier, const double* scale_w_normal, double* y,
                         int64_t ldy, void* stream);
 
+/* K2 with the f64 epilogue whose output columns come in runs of `slices` (2, 4, 8 or 16)
+ * consecutive products that are summed, last first, into one f64 column:
+ *   y[i, j] = sum_{t = slices-1 .. 0} v(i, j*slices + t),
+ *   v(i, c) = (s_x[i] * s_wo[c]) * acc_o(i, c) + (s_x[i] * s_wn[c]) * acc_n(i, c)   (no FMA).
+ * With int8 slices of a wider operand stacked along N this is an exact integer product
+ * recombined in f64 (K7's Ozaki-style products).  n % 16 == 0; y is [m x n / slices] (ldy). */
+int qarvd_dual_gemm_f64_slices(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                               int64_t n, int64_t k, int64_t k_outlier, const double* scale_x,
+                               const double* scale_w_outlier, const double* scale_w_normal, int slices,
+                               double* y, int64_t ldy, void* stream);
+
 /* ---- K1+K2: one quantized linear, host buffers (end-to-end entry) --------
  * Replaces  quantized_layer_forward(layer, x, Engine::int_kernels)
  *           engine.hpp:60 / engine.cpp:134-142 (per-token or static activations).

@@ -203,6 +203,11 @@ SIGNATURES = {
         [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
          c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     ),
+    "qarvd_dual_gemm_f64_slices": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+         c_void_p, c_void_p, c_int, c_void_p, c_int64, c_void_p],
+    ),
     "qarvd_linear_create": (
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,

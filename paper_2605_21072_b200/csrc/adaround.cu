@@ -8,10 +8,11 @@
 // (1/B) sum_s w[chunk_s] ||X_s W^T - FQ(X_s) What^T||^2, the corner-pushing regulariser
 // after warm-up, and bias-corrected Adam with a cosine-annealed learning rate.
 //
-// Everything stays in f64 like the reference, so the trajectory follows it to rounding:
-// the products (prediction X^ What^T - target, dL/dWhat = D^T X^) are cuBLAS DGEMMs (plain
-// library GEMMs), each over the batch's samples stacked along the rows (one GEMM per product,
-// not per sample: 1560-row GEMMs leave DGEMM at 31 of its 35 TF/s); the reference's third
+// Everything stays f64-accurate like the reference, so the trajectory follows it to rounding:
+// the per-iteration products (prediction X^ What^T - target, dL/dWhat = D^T X^) run on the int8
+// tensor cores as exact integer slice products (K2 with its f64 epilogue, Ozaki-style: see
+// kOzSlices), each over the batch's samples stacked along the rows (QARVD_K7_OZAKI=0 takes
+// cuBLAS DGEMM instead; the one-time target product X W^T stays a DGEMM); the reference's third
 // product dL/dX^ = D What only feeds the act-scale gradient, which equals <What, dL/dWhat>;
 // every elementwise step,
 // reduction and Adam update is a kernel here with the reference's per-element formula, and
@@ -325,6 +326,178 @@ const char* cublas_msg(cublasStatus_t s) {
                                      __FILE__ + ":" + std::to_string(__LINE__));         \
   } while (0)
 
+
+// ---- the two f64 products on the int8 tensor cores (Ozaki-style exact slices) ---------------
+// P = X^ What^T and dL/dWhat = D'^T X^ run as K2 (tcgen05 kind::i8, exact int32 accumulators)
+// over integer slices, recombined in f64:
+//   X^ = s_a * code_x exactly (act codes, |code| <= 127);
+//   What[j, c] = s_g(j) * u[j, c], u = clip(floor(w/s) + h) split into kOzSlices int8 slices
+//     u = q0 + q1 2^-7 + q2 2^-14 + ...  (q0 = rint(u), later slices rint of the scaled residual,
+//     |q_t| <= 64): the representation error is <= 2^-(7 kOzSlices - 6) absolute;
+//   D'[:, j] = 2^E_j d, |d| < 1 (E_j from the column's max |D'|), d = sum_t r_t 2^(-6 - 7t).
+// Each slice product is exact (|acc| < 2^31 for k <= 132K act columns / 264K batch rows), the
+// group scales (outlier / normal) ride in K2's dual-slab f64 epilogue, and the slices are summed
+// smallest first in K2's epilogue (qarvd_dual_gemm_f64_slices: the slices of one product are
+// consecutive output columns).  kOzSlices = 8 carries 7 + 7*7 = 56 bits of u and 6 + 7*7 = 55 bits
+// of d: both f64 operands are represented exactly, so the products are exact integer sums and
+// the only roundings are the f64 epilogue's (scale products and the slice sum) -- tighter than
+// the reference's own f64 matmul.
+constexpr int kOzSlices = 8;
+
+// int8 act codes of one sample in the K2 layout (pos[c] = padded position of column c), the
+// non-finite check of the reference's quantize (quant.cpp:128-129)
+__global__ void act_codes_kernel(const double* x, int64_t rows, int64_t k, const int32_t* pos, int64_t ldq,
+                                 const double* log_sa, int qmax, int8_t* cx, int* bad) {
+  const double s = libm::exp(*log_sa);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / k, c = i - r * k;
+    const double xv = x[i];
+    if (!isfinite(xv)) {
+      *bad = 1;
+      cx[r * ldq + pos[c]] = 0;
+      continue;
+    }
+    const double q = clampd(rint(xv / s), -static_cast<double>(qmax), static_cast<double>(qmax));
+    cx[r * ldq + pos[c]] = static_cast<int8_t>(q);
+  }
+}
+
+// the slices of u = What / s_g (the clipped soft code) in the K2 layout: slice t of row r at row
+// r * kOzSlices + t
+__global__ void w_slices_kernel(const double* code, int64_t n, int64_t k, const int32_t* pos, int64_t ldq,
+                                int8_t* wsl) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / k, c = i - r * k;
+    double u = code[i];
+    double q = rint(u);
+    wsl[(r * kOzSlices) * ldq + pos[c]] = static_cast<int8_t>(q);
+    double rem = u - q;  // exact, |rem| <= 0.5
+#pragma unroll
+    for (int t = 1; t < kOzSlices; ++t) {
+      rem *= 128.0;  // exact
+      q = rint(rem);
+      wsl[(r * kOzSlices + t) * ldq + pos[c]] = static_cast<int8_t>(q);
+      rem -= q;
+    }
+  }
+}
+
+// per-slice-row scales of the forward product: so / sn of row j at slice t = s_g(j) 2^-7t, and
+// the act scale per stacked row
+__global__ void oz_scales_kernel(const double* log_s, int64_t n, int enabled, const double* log_sa,
+                                 int64_t rows, double* so_sl, double* sn_sl, double* sx_rows) {
+  const double sa = libm::exp(*log_sa);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < kOzSlices * n || i < rows;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < kOzSlices * n) {
+      const int64_t j = i / kOzSlices, t = i - j * kOzSlices;
+      const double f = ldexp(1.0, static_cast<int>(-7 * t));
+      sn_sl[i] = libm::exp(log_s[j]) * f;
+      so_sl[i] = libm::exp(enabled ? log_s[n + j] : log_s[j]) * f;
+    }
+    if (i < rows) sx_rows[i] = sa;
+  }
+}
+
+// column max |D'| (as bits, non-negative doubles order like their bit patterns)
+__global__ void colmax_kernel(const double* d, int64_t rows, int64_t n, unsigned long long* mx) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long m = 0;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(fabs(d[r * n + j])));
+      m = b > m ? b : m;
+    }
+    atomicMax(mx + j, m);
+  }
+}
+
+// D' slices transposed for the gradient product: B[(j kOzSlices + t), i] = r_t(i, j) (K-major over
+// the batch rows); 32 x 32 tiles through shared memory
+__global__ void d_slices_t_kernel(const double* d, int64_t rows, int64_t n, const unsigned long long* mx,
+                                  int64_t lda, int8_t* a) {
+  __shared__ int8_t tile[kOzSlices][32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32 threads
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + tx;
+    double v = 0.0;
+    if (i < rows && j < n) {
+      const double m = __longlong_as_double(static_cast<long long>(mx[j]));
+      int e = 0;
+      if (m > 0.0) frexp(m, &e);  // m in [2^(e-1), 2^e): v in (-1, 1]
+      v = m > 0.0 ? ldexp(d[i * n + j], -e) : 0.0;
+    }
+    double rem = v * 64.0;
+    double q = rint(rem);
+    tile[0][tx][r] = static_cast<int8_t>(q);
+    rem -= q;
+#pragma unroll
+    for (int t = 1; t < kOzSlices; ++t) {
+      rem *= 128.0;
+      q = rint(rem);
+      tile[t][tx][r] = static_cast<int8_t>(q);
+      rem -= q;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + tx;
+    if (j < n && i < lda) {
+#pragma unroll
+      for (int t = 0; t < kOzSlices; ++t) a[(j * kOzSlices + t) * lda + i] = i < rows ? tile[t][r][tx] : 0;
+    }
+  }
+}
+
+// cx^T: B[c, i] = cx[i, c] (int8, K-major over the batch rows)
+__global__ void transpose_i8_kernel(const int8_t* cx, int64_t rows, int64_t cols, int64_t ldq, int64_t ldb,
+                                    int8_t* b) {
+  __shared__ int8_t tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, c = c0 + tx;
+    tile[r][tx] = (i < rows && c < cols) ? cx[i * ldq + c] : 0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t c = c0 + r, i = i0 + tx;
+    if (c < cols && i < ldb) b[c * ldb + i] = tile[tx][r];
+  }
+}
+
+// the gradient product's column scales 2^(E_j - 6 - 7t) (column j * kOzSlices + t) and its row
+// scale s_a (rows: the act columns)
+__global__ void oz_grad_scales_kernel(const unsigned long long* mx, int64_t n, const double* log_sa, int64_t kp,
+                                      double* scol, double* srow) {
+  const double sa = libm::exp(*log_sa);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < kOzSlices * n || i < kp;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < kOzSlices * n) {
+      const int64_t j = i / kOzSlices, t = i - j * kOzSlices;
+      const double m = __longlong_as_double(static_cast<long long>(mx[j]));
+      int e = 0;
+      if (m > 0.0) frexp(m, &e);
+      scol[i] = m > 0.0 ? ldexp(1.0, e - 6 - 7 * static_cast<int>(t)) : 0.0;
+    }
+    if (i < kp) srow[i] = sa;
+  }
+}
+
+// gw[j, c] (+)= Gt[pos[c], j]: the slice-summed product back to [n x k], original column order
+__global__ void oz_combine_grad_kernel(const double* gt, int64_t n, int64_t k, const int32_t* pos,
+                                       int accumulate, double* gw) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / k, c = i - j * k;
+    const double v = gt[static_cast<int64_t>(pos[c]) * n + j];
+    gw[i] = accumulate ? gw[i] + v : v;
+  }
+}
+
 struct DevArena {
   std::vector<void*> ptrs;
   cudaStream_t s;
@@ -419,13 +592,51 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   const int64_t G = cfg->batch_size < kMaxGroup ? cfg->batch_size : kMaxGroup;
   const int64_t cap_rows = G * max_rows;
   double* d = A.get<double>(cap_rows * n);
-  double* xhat = A.get<double>(cap_rows * k);
+  // per-iteration products on the int8 tensor cores (QARVD_K7_OZAKI=0: cuBLAS DGEMM, A/B)
+  static const bool ozaki = !(getenv("QARVD_K7_OZAKI") && getenv("QARVD_K7_OZAKI")[0] == '0');
+  double* xhat = ozaki ? nullptr : A.get<double>(cap_rows * k);
+  // K2 layout of the plan: [outlier columns | pad to 32 | normal columns | pad to 32]
+  std::vector<int32_t> pos_h(static_cast<size_t>(k));
+  int64_t k_o_pad = 0, k_pad = 0;
+  {
+    std::vector<uint8_t> mask_h(static_cast<size_t>(k));
+    QARVD_CUDA_TRY(cudaMemcpyAsync(mask_h.data(), outlier_mask, static_cast<size_t>(k), cudaMemcpyDeviceToHost, s));
+    QARVD_CUDA_TRY(cudaStreamSynchronize(s));
+    int64_t no = 0;
+    for (int64_t c = 0; c < k; ++c) no += (plan_enabled && mask_h[c]) ? 1 : 0;
+    k_o_pad = (no + 31) / 32 * 32;
+    k_pad = k_o_pad + (k - no + 31) / 32 * 32;
+    int64_t io = 0, in = 0;
+    for (int64_t c = 0; c < k; ++c)
+      pos_h[c] = static_cast<int32_t>((plan_enabled && mask_h[c]) ? io++ : k_o_pad + in++);
+  }
+  const int64_t tn = kOzSlices * n, kb_cap = (cap_rows + 31) / 32 * 32;
+  int32_t* ozpos = ozaki ? A.get<int32_t>(k) : nullptr;
+  int8_t* cx = ozaki ? A.get<int8_t>(kb_cap * k_pad) : nullptr;
+  int8_t* wsl = ozaki ? A.get<int8_t>(tn * k_pad) : nullptr;
+  double* so_sl = ozaki ? A.get<double>(tn) : nullptr;
+  double* sn_sl = ozaki ? A.get<double>(tn) : nullptr;
+  double* sx_rows = ozaki ? A.get<double>(kb_cap) : nullptr;
+  unsigned long long* cmax = ozaki ? A.get<unsigned long long>(n) : nullptr;
+  int8_t* amat = ozaki ? A.get<int8_t>(tn * kb_cap) : nullptr;
+  int8_t* bmat = ozaki ? A.get<int8_t>(k_pad * kb_cap) : nullptr;
+  double* sx_a = ozaki ? A.get<double>(tn) : nullptr;
+  double* srow_a = ozaki ? A.get<double>(k_pad) : nullptr;
+  double* gsl = ozaki ? A.get<double>(k_pad * n) : nullptr;
+  if (ozaki && (!ozpos || !cx || !wsl || !so_sl || !sn_sl || !sx_rows || !cmax || !amat || !bmat || !sx_a ||
+                !srow_a || !gsl))
+    QARVD_FAIL(QARVD_ERR_CUDA, "calibrate_layer: device allocation failed");
+  if (ozaki) {
+    QARVD_CUDA_TRY(cudaMemcpyAsync(ozpos, pos_h.data(), static_cast<size_t>(k) * 4, cudaMemcpyHostToDevice, s));
+    QARVD_CUDA_TRY(cudaMemsetAsync(cx, 0, static_cast<size_t>(kb_cap * k_pad), s));   // pad columns stay 0
+    QARVD_CUDA_TRY(cudaMemsetAsync(wsl, 0, static_cast<size_t>(tn * k_pad), s));
+  }
   double* partial = A.get<double>(kMaxGroup * kRedBlocks);
   // scalars: [0] log_sa [1] m_a [2] v_a [3] g_a [4] loss acc [5] best
   double* sc = A.get<double>(8);
   int* flags = A.get<int>(2);  // [0] diverged_at, [1] non-finite input
   if (!v || !mv || !vv || !what || !code || !dhdv || !gw || !log_s || !ms || !vs || !sgrad || !target ||
-      !d || !xhat || !partial || !sc || !flags)
+      !d || (!ozaki && !xhat) || !partial || !sc || !flags)
     QARVD_FAIL(QARVD_ERR_CUDA, "calibrate_layer: device allocation failed");
   QARVD_CUDA_TRY(cudaMemsetAsync(mv, 0, nk * 8, s));
   QARVD_CUDA_TRY(cudaMemsetAsync(vv, 0, nk * 8, s));
@@ -468,16 +679,33 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
         ++end;
       }
       GroupWeights wl{};
-      for (size_t j = pos, off = 0; j < end; ++j) {
-        const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
-        xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat + off * k,
-                                                       flags + 1);
-        off += rows;
+      if (ozaki) {
+        // P = s_a code_x . What^T as kOzSlices exact int8 products (K2, f64 epilogue carries the
+        // group scales and the slice weights), summed smallest slice first
+        for (size_t j = pos, off = 0; j < end; ++j) {
+          const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
+          act_codes_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows, k, ozpos, k_pad, sc + 0, aq_max,
+                                                              cx + off * k_pad, flags + 1);
+          off += rows;
+        }
+        oz_scales_kernel<<<blocks_for(tn > rows_g ? tn : rows_g), kT, 0, s>>>(log_s, n, plan_enabled, sc + 0, rows_g,
+                                                                           so_sl, sn_sl, sx_rows);
+        count_launch(static_cast<uint64_t>(end - pos) + 1);
+        if (int st = qarvd_dual_gemm_f64_slices(cx, k_pad, wsl, k_pad, rows_g, tn, k_pad, k_o_pad, sx_rows, so_sl,
+                                                sn_sl, kOzSlices, d, n, s))
+          return st;
+      } else {
+        for (size_t j = pos, off = 0; j < end; ++j) {
+          const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
+          xhat_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows * k, sc + 0, aq_max, xhat + off * k,
+                                                         flags + 1);
+          off += rows;
+        }
+        // P = X^ What^T   [rows_g x n]; D = P - T is formed by the reduction below
+        QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows_g),
+                                     static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
+                                     static_cast<int>(k), &zero, d, static_cast<int>(n)));
       }
-      // P = X^ What^T   [rows_g x n]; D = P - T is formed by the reduction below
-      QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows_g),
-                                   static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
-                                   static_cast<int>(k), &zero, d, static_cast<int>(n)));
       for (size_t j = pos, off = 0; j < end; ++j) {
         const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
         wl.w[j - pos] = wsamp[si];
@@ -490,7 +718,25 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
       dot_final_kernel<<<1, kMaxGroup * 32, 0, s>>>(partial, static_cast<int>(end - pos), wl, nullptr, gi > 0,
                                         sc + 4);
       count_launch(2 * static_cast<int>(end - pos) + 2);
-      if (grads) {
+      if (grads && ozaki) {
+        // dL/dWhat (+)= D'^T X^ = s_a D'^T code_x: D' split per column (2^E_j x int8 slices, K-major
+        // over the batch rows), code_x transposed, one K2 over all slices, recombined per column
+        const int64_t kb = (rows_g + 31) / 32 * 32;
+        QARVD_CUDA_TRY(cudaMemsetAsync(cmax, 0, static_cast<size_t>(n) * 8, s));
+        colmax_kernel<<<dim3(static_cast<unsigned>((n + kT - 1) / kT), 64), kT, 0, s>>>(d, rows_g, n, cmax);
+        d_slices_t_kernel<<<dim3(static_cast<unsigned>(kb / 32), static_cast<unsigned>((n + 31) / 32)), 256, 0, s>>>(
+            d, rows_g, n, cmax, kb, amat);
+        transpose_i8_kernel<<<dim3(static_cast<unsigned>(kb / 32), static_cast<unsigned>(k_pad / 32)), 256, 0, s>>>(
+            cx, rows_g, k_pad, k_pad, kb, bmat);
+        oz_grad_scales_kernel<<<blocks_for(tn > k_pad ? tn : k_pad), kT, 0, s>>>(cmax, n, sc + 0, k_pad, sx_a, srow_a);
+        count_launch(4);
+        // Gt [k_pad x n] = s_a code_x^T . D' (act columns as rows, the D' slices as columns)
+        if (int st = qarvd_dual_gemm_f64_slices(bmat, kb, amat, kb, k_pad, tn, kb, 0, srow_a, nullptr, sx_a,
+                                                kOzSlices, gsl, n, s))
+          return st;
+        oz_combine_grad_kernel<<<blocks_for(nk), kT, 0, s>>>(gsl, n, k, ozpos, gi > 0 ? 1 : 0, gw);
+        count_launch(1);
+      } else if (grads) {
         // dL/dWhat (+)= D'^T X^   [n x k]
         QARVD_CUBLAS_TRY(cublasDgemm(handle, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(k), static_cast<int>(n),
                                      static_cast<int>(rows_g), &one, xhat, static_cast<int>(k), d,
@@ -516,9 +762,16 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   for (int64_t i = 0; i < n_samples; ++i) all[i] = i;
 
   // initial hard loss (calibrate.cpp:320)
+  // the int8 slices of the clipped codes that What = s_g * code is built from (Ozaki products)
+  auto slice_weights = [&]() {
+    if (!ozaki) return;
+    w_slices_kernel<<<blocks_for(nk), kT, 0, s>>>(code, n, k, ozpos, k_pad, wsl);
+    count_launch();
+  };
   weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
-                                              -wq_max, wq_max, 1, what, nullptr, nullptr, nullptr);
+                                              -wq_max, wq_max, 1, what, ozaki ? code : nullptr, nullptr, nullptr);
   count_launch();
+  slice_weights();
   if (int st = objective(all, false)) return st;
   loss_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(n_samples), scalars_out + 1);  // initial
   count_launch();
@@ -533,6 +786,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
     weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
                                                 -wq_max, wq_max, 0, what, code, dhdv, nullptr);
     count_launch();
+    slice_weights();
     if (int st = objective(batch, true)) return st;
     trace_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(batch.size()), sc + 5,
                                  trace_out ? trace_out : sc + 7, trace_out ? t : 0, flags);
@@ -554,8 +808,9 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
 
   // final hard loss, hard codes, learned scales and act scale (calibrate.cpp:391-395)
   weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
-                                              -wq_max, wq_max, 1, what, nullptr, nullptr, codes);
+                                              -wq_max, wq_max, 1, what, ozaki ? code : nullptr, nullptr, codes);
   count_launch();
+  slice_weights();
   if (int st = objective(all, false)) return st;
   loss_kernel<<<1, 1, 0, s>>>(sc + 4, 1.0 / static_cast<double>(n_samples), scalars_out + 2);  // final
   exp_kernel<<<blocks_for(n), kT, 0, s>>>(log_s, scale_normal_out, n);

@@ -80,6 +80,8 @@ struct GemmParams {
   const double* sx64;  // QARVD_F64 output: f64 scales, reference epilogue (engine.cpp:86-94)
   const double* so64;
   const double* sn64;
+  int f64_slices;      // QARVD_F64 with f64_slices = T > 1: each run of T consecutive output columns
+                       // is summed (last first) into one f64 column (K7's exact integer slices)
   uint32_t* row_absmax;  // optional: atomicMax per row of the sign-cleared bf16 output bits
   uint32_t* row_pmax;    // optional: per-row partial maxima, [m][pm_count] (one per epilogue
   int pm_count;          //   warp and tile: pm_count = num_n_blks * 4), plain stores
@@ -976,17 +978,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           // val += (s_x*s_wn)*acc_n  (outlier group first, f64, no FMA)
           if (row_ok) {
             const double sx64 = p.sx64[row];
-            double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0;
+            double vv[CW];
 #pragma unroll
             for (int e = 0; e < CW; ++e) {
-              if (e >= ncols) continue;
               double v = 0.0;
-              if (has_outlier)
-                v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.so64[col0 + e]),
-                                           static_cast<double>(static_cast<int32_t>(ro[e]))));
-              v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.sn64[col0 + e]),
-                                         static_cast<double>(static_cast<int32_t>(rn[e]))));
-              yr[e] = v;
+              if (e < ncols) {
+                if (has_outlier)
+                  v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.so64[col0 + e]),
+                                             static_cast<double>(static_cast<int32_t>(ro[e]))));
+                v = __dadd_rn(v, __dmul_rn(__dmul_rn(sx64, p.sn64[col0 + e]),
+                                           static_cast<double>(static_cast<int32_t>(rn[e]))));
+              }
+              vv[e] = v;
+            }
+            const int T = p.f64_slices;
+            if (T > 1) {  // n % 16 == 0 and T | 16: whole runs only
+              double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0 / T;
+              for (int g = 0; g < CW / T; ++g) {
+                double acc = 0.0;
+                for (int t = T - 1; t >= 0; --t) acc = __dadd_rn(acc, vv[g * T + t]);
+                yr[g] = acc;
+              }
+            } else {
+              double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0;
+#pragma unroll
+              for (int e = 0; e < CW; ++e)
+                if (e < ncols) yr[e] = vv[e];
             }
           }
           continue;
@@ -1294,8 +1311,9 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
                      int32_t* acc_n, cudaStream_t stream, const double* sx64 = nullptr,
                      const double* so64 = nullptr, const double* sn64 = nullptr,
                      uint32_t* row_absmax = nullptr, uint32_t* row_pmax = nullptr,
-                     void* sk_workspace = nullptr, int64_t sk_workspace_bytes = 0) {
+                     void* sk_workspace = nullptr, int64_t sk_workspace_bytes = 0, int f64_slices = 0) {
   GemmParams p{};
+  p.f64_slices = f64_slices;
   p.row_absmax = row_absmax;
   p.row_pmax = row_pmax;
   p.sx64 = sx64;
@@ -1429,6 +1447,32 @@ extern "C" int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* 
   return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, nullptr, nullptr, nullptr, nullptr,
                           QARVD_EPI_NONE, QARVD_F64, y, ldy, nullptr, nullptr, as_stream(stream),
                           scale_x, scale_w_outlier, scale_w_normal);
+}
+
+extern "C" int qarvd_dual_gemm_f64_slices(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                          int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                          const double* scale_x, const double* scale_w_outlier,
+                                          const double* scale_w_normal, int slices, double* y, int64_t ldy,
+                                          void* stream) {
+  clear_error();
+  if (m <= 0 || n <= 0 || k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
+  if (!(slices == 2 || slices == 4 || slices == 8 || slices == 16) || n % 16 != 0)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_dual_gemm_f64_slices: slices in {2,4,8,16}, n % 16 == 0");
+  if (k % 32 != 0 || k_outlier % 32 != 0 || k_outlier < 0 || k_outlier >= k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "kernel_b: k and k_outlier must be multiples of 32 with 0 <= k_outlier < k");
+  if (k > 132104)
+    QARVD_FAIL(QARVD_ERR_LOGIC, "kernel_b: reduction dimension too large for exact int32 accumulation");
+  if (ldq < k || ldw < k || ldq % 16 || ldw % 16 || ldy < n / slices)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: invalid leading dimension");
+  if (!xq || !wq || !scale_x || !scale_w_normal || !y || (k_outlier > 0 && !scale_w_outlier))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
+  if ((reinterpret_cast<uintptr_t>(xq) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: operand pointers must be 16-byte aligned");
+  if (int st = require_device()) return st;
+  return dual_gemm_launch(xq, ldq, wq, ldw, m, n, k, k_outlier, nullptr, nullptr, nullptr, nullptr,
+                          QARVD_EPI_NONE, QARVD_F64, y, ldy, nullptr, nullptr, as_stream(stream),
+                          scale_x, scale_w_outlier, scale_w_normal, nullptr, nullptr, nullptr, 0, slices);
 }
 
 extern "C" int64_t qarvd_dual_gemm_workspace_size(int64_t m, int64_t n, int64_t k, int64_t k_outlier) {
