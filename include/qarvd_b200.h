@@ -250,11 +250,13 @@ int qarvd_dual_gemm_f64(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t
                         int64_t ldy, void* stream);
 
 /* K2 with the f64 epilogue whose output columns come in runs of `slices` (2, 4, 8 or 16)
- * consecutive products that are summed, last first, into one f64 column:
- *   y[i, j] = sum_{t = slices-1 .. 0} v(i, j*slices + t),
- *   v(i, c) = (s_x[i] * s_wo[c]) * acc_o(i, c) + (s_x[i] * s_wn[c]) * acc_n(i, c)   (no FMA).
- * With int8 slices of a wider operand stacked along N this is an exact integer product
- * recombined in f64 (K7's Ozaki-style products).  n % 16 == 0; y is [m x n / slices] (ldy). */
+ * consecutive products, slice t of a run weighted 2^-7t, recombined into one f64 column:
+ *   y[i, j] = (s_x[i] * s_wo[j]) * V_o(i, j) + (s_x[i] * s_wn[j]) * V_n(i, j)   (no FMA),
+ *   V(i, j) = sum_t 2^-7t acc(i, j*slices + t),
+ * where groups of four slices combine exactly in int64 and the groups add in f64, smallest
+ * first.  With int8 slices of a wider operand (t-th slice = t-th 7-bit digit) stacked along N
+ * this is an exact integer product recombined in f64 (K7's Ozaki-style products).  The scales
+ * are per run: s_wo / s_wn have n / slices entries.  n % 16 == 0; y is [m x n / slices] (ldy). */
 int qarvd_dual_gemm_f64_slices(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
                                int64_t n, int64_t k, int64_t k_outlier, const double* scale_x,
                                const double* scale_w_outlier, const double* scale_w_normal, int slices,

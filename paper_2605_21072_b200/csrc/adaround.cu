@@ -69,6 +69,10 @@ __device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + libm
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
+// 1.5 * 2^52: for |x| < 2^51, x + kRoundMagic rounds x to an integer (round-half-even, as rint) whose
+// two's complement sits in the low word, and (x + kRoundMagic) - kRoundMagic == rint(x) exactly
+constexpr double kRoundMagic = 6755399441055744.0;
+
 // weight_scale(r, outlier_group) = exp(log scale) (calibrate.cpp:117-119); log_s = [normal n | outlier n]
 __device__ __forceinline__ double wscale(const double* log_s, int64_t n, int64_t r, bool outl) {
   return libm::exp(outl ? log_s[n + r] : log_s[r]);
@@ -99,11 +103,13 @@ __global__ void weights_kernel(const double* w, const double* v, const uint8_t* 
                                int qmin, int qmax, int hard, double* what, double* code,
                                double* dhdv, int8_t* codes_out) {
   const double span = zeta - gamma;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / k, c = i - r * k;
+  // one CTA per weight row: the row's two group scales are computed once
+  const int64_t r = blockIdx.x;
+  const double s_n = wscale(log_s, n, r, false), s_o = wscale(log_s, n, r, true);
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
+    const int64_t i = r * k + c;
     const bool outl = enabled && mask[c];
-    const double s = wscale(log_s, n, r, outl);
+    const double s = outl ? s_o : s_n;
     const double sig = sigmoid_d(v[i]);
     const double pre = sig * span + gamma;
     const double h = clampd(pre, 0.0, 1.0);
@@ -186,13 +192,14 @@ __global__ void __launch_bounds__(kT) dot_partial_kernel(double* a, const double
 struct GroupWeights {
   double w[kMaxGroup];
 };
-// *acc (+)= sum_g wt.w[g] * (sum of partial[g*kRedBlocks ..][kRedBlocks]) in a fixed order:
+// *acc (+)= sum_g wt.w[g] * (sum of partial[g*per ..][per]) in a fixed order (per <= kRedBlocks):
 // warp g sums group g (all of its loads issued before the adds), thread 0 combines the groups
 // in order; with log_sa the total is multiplied by exp(*log_sa) (act grad).  Launch with
 // kMaxGroup * 32 threads.
 __global__ void __launch_bounds__(kMaxGroup * 32) dot_final_kernel(const double* partial, int groups,
                                                                   GroupWeights wt, const double* log_sa,
-                                                                  int accumulate, double* acc) {
+                                                                  int accumulate, double* acc,
+                                                                  int per = kRedBlocks) {
   constexpr int kPer = (kRedBlocks + 31) / 32;
   __shared__ double gsum[kMaxGroup];
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(kMaxGroup * 32) dot_final_kernel(const double*
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
       const int i = lane + 32 * j;
-      v[j] = i < kRedBlocks ? partial[g * kRedBlocks + i] : 0.0;
+      v[j] = i < per ? partial[g * per + i] : 0.0;
     }
     double sum = 0.0;
 #pragma unroll
@@ -239,10 +246,11 @@ __global__ void __launch_bounds__(kT) grad_kernel(const double* gw, const double
   const int64_t r = blockIdx.x;
   double gn = 0.0, go = 0.0;
   const double span = zeta - gamma;
+  const double s_n = wscale(log_s, n, r, false), s_o = wscale(log_s, n, r, true);
   for (int64_t c = threadIdx.x; c < k; c += kT) {
     const int64_t i = r * k + c;
     const bool outl = enabled && mask[c];
-    const double s = wscale(log_s, n, r, outl);
+    const double s = outl ? s_o : s_n;
     const double gwe = gw[i];
     double g = gwe * s * dhdv[i];
     if (reg_on) {
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(kT) grad_kernel(const double* gw, const double
       const double h = clampd(pre, 0.0, 1.0);
       const double centered = 2.0 * h - 1.0;
       const double mag = fabs(centered);
-      const double dreg_dh = -2.0 * beta * crm::cr_pow(mag > 1e-12 ? mag : 1e-12, beta - 1.0) *
+      const double dreg_dh = -2.0 * beta * libm::pow(mag > 1e-12 ? mag : 1e-12, beta - 1.0) *
                              (centered >= 0 ? 1.0 : -1.0);
       const double dh_dv = (pre > 0.0 && pre < 1.0) ? span * sig * (1.0 - sig) : 0.0;
       g += reg_lambda * dreg_dh * dh_dv;
@@ -344,23 +352,150 @@ const char* cublas_msg(cublasStatus_t s) {
 // the reference's own f64 matmul.
 constexpr int kOzSlices = 8;
 
-// int8 act codes of one sample in the K2 layout (pos[c] = padded position of column c), the
-// non-finite check of the reference's quantize (quant.cpp:128-129)
-__global__ void act_codes_kernel(const double* x, int64_t rows, int64_t k, const int32_t* pos, int64_t ldq,
-                                 const double* log_sa, int qmax, int8_t* cx, int* bad) {
+// the samples stacked into one group: stacked rows [off[j], off[j+1]) are rows [src[j], ...) of
+// the sample arrays; coef[j] = 2 w_j / B, the gradient's row scale of sample j
+struct GroupRows {
+  int64_t off[kMaxGroup + 1];
+  int64_t src[kMaxGroup];
+  double coef[kMaxGroup];
+  int count;
+};
+__device__ __forceinline__ int group_of(const GroupRows& g, int64_t r) {
+  int j = 0;
+  while (j + 1 < g.count && r >= g.off[j + 1]) ++j;
+  return j;
+}
+
+// clamp(rint(x / s)) (quant.cpp:132-135) without a division on the common path: t = x * (1/s) is
+// within |x/s| 2^-52 < 2^-37 of x / s while |t| <= qmax + 1 <= 2^15 (beyond that every path clamps
+// to the same code, so t is clamped there first), so rint(t) is the reference's code unless t is
+// within 2^-30 of a rounding boundary, where the exact quotient decides
+__device__ __forceinline__ int act_code(double xv, double rinv, double s, int qmax, double lim) {
+  double t = xv * rinv;
+  t = t > lim ? lim : (t < -lim ? -lim : t);
+  const double qm = t + kRoundMagic;
+  int q = __double2loint(qm);
+  if (fabs(t - (qm - kRoundMagic)) > 0.5 - 0x1p-30) q = __double2int_rn(__ddiv_rn(xv, s));
+  return max(-qmax, min(qmax, q));
+}
+
+// the act codes of a whole group in one pass over 64 x 64 tiles: cx [stacked rows x ldq] in the
+// K2 column order (GEMM1's A operand) and, when bt != NULL, the transpose bt[pos[c] * kb + row]
+// (GEMM2's B operand, K-major over the stacked rows; rows in [rows_g, kb) are zero)
+__global__ void __launch_bounds__(256) act_codes_group_kernel(const double* __restrict__ x, int64_t k, GroupRows g,
+                                                               int64_t rows_g, int64_t kb, const int32_t* pos,
+                                                               int64_t ldq, const double* log_sa, int qmax,
+                                                               int8_t* __restrict__ cx, int8_t* __restrict__ bt,
+                                                               int* bad) {
+  __shared__ int8_t tile[64][64 + 4];
   const double s = libm::exp(*log_sa);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * k;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / k, c = i - r * k;
-    const double xv = x[i];
-    if (!isfinite(xv)) {
-      *bad = 1;
-      cx[r * ldq + pos[c]] = 0;
-      continue;
+  const double rinv = 1.0 / s;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  __shared__ const double* rowp[64];  // source row of each tile row (NULL past the group)
+  if (threadIdx.x < 64) {
+    const int64_t row = r0 + threadIdx.x;
+    const double* p = nullptr;
+    if (row < rows_g) {
+      const int j = group_of(g, row);
+      p = x + (g.src[j] + row - g.off[j]) * k;
     }
-    const double q = clampd(rint(xv / s), -static_cast<double>(qmax), static_cast<double>(qmax));
-    cx[r * ldq + pos[c]] = static_cast<int8_t>(q);
+    rowp[threadIdx.x] = p;
   }
+  __syncthreads();
+  const double lim = static_cast<double>(qmax) + 1.0;
+  const int64_t c = c0 + tx;
+  const bool col_ok = c < k;
+  double xv[16];  // all 16 loads in flight before any store
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const double* p = rowp[ty + 4 * u];
+    xv[u] = (p && col_ok) ? p[c] : 0.0;
+  }
+  bool finite = true;
+  int8_t* cxc = cx + (col_ok ? pos[c] : 0) + (r0 + ty) * ldq;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int rr = ty + 4 * u;
+    int q = 0;
+    if (rowp[rr] && col_ok) {
+      if (isfinite(xv[u])) q = act_code(xv[u], rinv, s, qmax, lim);
+      else finite = false;
+      cxc[4 * u * ldq] = static_cast<int8_t>(q);
+    }
+    tile[rr][tx] = static_cast<int8_t>(q);
+  }
+  if (!finite) *bad = 1;
+  if (!bt) return;
+  __syncthreads();
+  for (int it = threadIdx.x; it < 64 * 16; it += 256) {  // 4 consecutive rows per store
+    const int cc = it >> 4, rg = (it & 15) * 4;
+    const int64_t c = c0 + cc, row = r0 + rg;
+    if (c >= k || row >= kb) continue;  // kb % 32 == 0: all four rows are < kb
+    const uint32_t w = static_cast<uint8_t>(tile[rg][cc]) | static_cast<uint32_t>(static_cast<uint8_t>(tile[rg + 1][cc])) << 8 |
+                       static_cast<uint32_t>(static_cast<uint8_t>(tile[rg + 2][cc])) << 16 |
+                       static_cast<uint32_t>(static_cast<uint8_t>(tile[rg + 3][cc])) << 24;
+    *reinterpret_cast<uint32_t*>(bt + static_cast<int64_t>(pos[c]) * kb + row) = w;
+  }
+}
+
+// D_b = P_b - T_b over a whole group (calibrate.cpp:279-280): per (sample, row chunk, column
+// block) CTA the partial ||D||^2 -> partial[j * per + chunk * gridDim.x + blockIdx.x] (fixed
+// order); with grads, D is rescaled in place to D' = coef_j D and the column maxima |D'| are
+// folded into cmax (as bits: non-negative doubles order like their bit patterns).  Two adjacent
+// columns per thread (n even) so rows are read as 16-byte pairs.
+__global__ void __launch_bounds__(kT) resid_kernel(double* __restrict__ d, const double* __restrict__ target,
+                                                    int64_t n, GroupRows g,
+                                                    int chunks, int grads, double* partial, int per,
+                                                    unsigned long long* cmax) {
+  const int j = blockIdx.y / chunks, ch = blockIdx.y - j * chunks;
+  const int64_t rows = g.off[j + 1] - g.off[j];
+  const int64_t per_ch = (rows + chunks - 1) / chunks;
+  const int64_t lo = ch * per_ch, hi = lo + per_ch < rows ? lo + per_ch : rows;
+  const int64_t c = 2 * (static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x);
+  const double coef = g.coef[j];
+  double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
+  if (c < n) {
+    const bool two = c + 1 < n;
+    double* dp = d + (g.off[j] + lo) * n + c;
+    const double* tp = target + (g.src[j] + lo) * n + c;
+    if ((n & 1) == 0) {
+#pragma unroll 4
+      for (int64_t r = lo; r < hi; ++r, dp += n, tp += n) {
+        const double2 pv = *reinterpret_cast<const double2*>(dp);
+        const double2 tv = *reinterpret_cast<const double2*>(tp);
+        const double v0 = pv.x - tv.x, v1 = pv.y - tv.y;
+        a0 += v0 * v0;
+        a1 += v1 * v1;
+        if (grads) {
+          const double e0 = v0 * coef, e1 = v1 * coef;
+          *reinterpret_cast<double2*>(dp) = make_double2(e0, e1);
+          m0 = fmax(m0, fabs(e0));
+          m1 = fmax(m1, fabs(e1));
+        }
+      }
+    } else {
+      for (int64_t r = lo; r < hi; ++r, dp += n, tp += n) {
+        const double v0 = dp[0] - tp[0], v1 = two ? dp[1] - tp[1] : 0.0;
+        a0 += v0 * v0;
+        a1 += v1 * v1;
+        if (grads) {
+          dp[0] = v0 * coef;
+          m0 = fmax(m0, fabs(v0 * coef));
+          if (two) {
+            dp[1] = v1 * coef;
+            m1 = fmax(m1, fabs(v1 * coef));
+          }
+        }
+      }
+    }
+    if (grads && cmax) {
+      atomicMax(cmax + c, static_cast<unsigned long long>(__double_as_longlong(m0)));
+      if (two) atomicMax(cmax + c + 1, static_cast<unsigned long long>(__double_as_longlong(m1)));
+    }
+  }
+  const double t = block_sum(a0 + a1);
+  if (threadIdx.x == 0) partial[j * per + ch * gridDim.x + blockIdx.x] = t;
 }
 
 // the slices of u = What / s_g (the clipped soft code) in the K2 layout: slice t of row r at row
@@ -370,118 +505,95 @@ __global__ void w_slices_kernel(const double* code, int64_t n, int64_t k, const 
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * k;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = i / k, c = i - r * k;
-    double u = code[i];
-    double q = rint(u);
-    wsl[(r * kOzSlices) * ldq + pos[c]] = static_cast<int8_t>(q);
-    double rem = u - q;  // exact, |rem| <= 0.5
+    double rem = code[i];
+    int8_t* out = wsl + (r * kOzSlices) * ldq + pos[c];
 #pragma unroll
-    for (int t = 1; t < kOzSlices; ++t) {
-      rem *= 128.0;  // exact
-      q = rint(rem);
-      wsl[(r * kOzSlices + t) * ldq + pos[c]] = static_cast<int8_t>(q);
-      rem -= q;
+    for (int t = 0; t < kOzSlices; ++t) {
+      if (t > 0) rem *= 128.0;  // exact; |rem| <= 0.5 before the scaling
+      const double qm = rem + kRoundMagic;
+      out[t * ldq] = static_cast<int8_t>(__double2loint(qm));
+      rem -= qm - kRoundMagic;  // exact
     }
   }
 }
 
-// per-slice-row scales of the forward product: so / sn of row j at slice t = s_g(j) 2^-7t, and
-// the act scale per stacked row
+// per-run scales of the forward product: so / sn of row j = s_g(j) (slice t's 2^-7t is applied
+// by the GEMM epilogue), and the act scale per stacked row
 __global__ void oz_scales_kernel(const double* log_s, int64_t n, int enabled, const double* log_sa,
                                  int64_t rows, double* so_sl, double* sn_sl, double* sx_rows) {
   const double sa = libm::exp(*log_sa);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < kOzSlices * n || i < rows;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n || i < rows;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (i < kOzSlices * n) {
-      const int64_t j = i / kOzSlices, t = i - j * kOzSlices;
-      const double f = ldexp(1.0, static_cast<int>(-7 * t));
-      sn_sl[i] = libm::exp(log_s[j]) * f;
-      so_sl[i] = libm::exp(enabled ? log_s[n + j] : log_s[j]) * f;
+    if (i < n) {
+      sn_sl[i] = libm::exp(log_s[i]);
+      so_sl[i] = libm::exp(enabled ? log_s[n + i] : log_s[i]);
     }
     if (i < rows) sx_rows[i] = sa;
   }
 }
 
-// column max |D'| (as bits, non-negative doubles order like their bit patterns)
-__global__ void colmax_kernel(const double* d, int64_t rows, int64_t n, unsigned long long* mx) {
-  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    unsigned long long m = 0;
-    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(fabs(d[r * n + j])));
-      m = b > m ? b : m;
-    }
-    atomicMax(mx + j, m);
-  }
-}
-
 // D' slices transposed for the gradient product: B[(j kOzSlices + t), i] = r_t(i, j) (K-major over
-// the batch rows); 32 x 32 tiles through shared memory
-__global__ void d_slices_t_kernel(const double* d, int64_t rows, int64_t n, const unsigned long long* mx,
-                                  int64_t lda, int8_t* a) {
-  __shared__ int8_t tile[kOzSlices][32][33];
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32 threads
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t i = i0 + r, j = j0 + tx;
-    double v = 0.0;
-    if (i < rows && j < n) {
-      const double m = __longlong_as_double(static_cast<long long>(mx[j]));
-      int e = 0;
-      if (m > 0.0) frexp(m, &e);  // m in [2^(e-1), 2^e): v in (-1, 1]
-      v = m > 0.0 ? ldexp(d[i * n + j], -e) : 0.0;
+// the batch rows).  Tiles of 128 rows x 32 columns through shared memory: the loads are 256-byte
+// row segments (lane = column), the stores 128-byte runs of one (column, slice) row (4 rows per
+// lane); the column's 2^-E_j is formed once per thread.
+constexpr int kDsRows = 128;
+__global__ void __launch_bounds__(256) d_slices_t_kernel(const double* d, int64_t rows, int64_t n,
+                                                         const unsigned long long* mx, int64_t lda, int8_t* a) {
+  __shared__ __align__(4) int8_t tile[kOzSlices][32][kDsRows + 4];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kDsRows, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps x 16 rows
+  const int64_t j = j0 + lane;
+  double f = 0.0;  // 2^-E_j: m in [2^(E-1), 2^E), so D' f is in (-1, 1)
+  if (j < n) {
+    const double m = __longlong_as_double(static_cast<long long>(mx[j]));
+    int e = 0;
+    if (m > 0.0) {
+      frexp(m, &e);
+      f = ldexp(1.0, -e);
     }
-    double rem = v * 64.0;
-    double q = rint(rem);
-    tile[0][tx][r] = static_cast<int8_t>(q);
-    rem -= q;
+  }
+  double dv[kDsRows / 8];  // the warp's 16 rows, all loads in flight first
 #pragma unroll
-    for (int t = 1; t < kOzSlices; ++t) {
-      rem *= 128.0;
-      q = rint(rem);
-      tile[t][tx][r] = static_cast<int8_t>(q);
-      rem -= q;
+  for (int u = 0; u < kDsRows / 8; ++u) {
+    const int64_t i = i0 + warp + 8 * u;
+    dv[u] = (i < rows && j < n) ? d[i * n + j] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kDsRows / 8; ++u) {
+    const int r = warp + 8 * u;
+    double rem = dv[u] * f * 64.0;
+#pragma unroll
+    for (int t = 0; t < kOzSlices; ++t) {
+      if (t > 0) rem *= 128.0;
+      const double qm = rem + kRoundMagic;  // rint(rem) in the low word, no conversion unit
+      tile[t][lane][r] = static_cast<int8_t>(__double2loint(qm));
+      rem -= qm - kRoundMagic;
     }
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t j = j0 + r, i = i0 + tx;
-    if (j < n && i < lda) {
-#pragma unroll
-      for (int t = 0; t < kOzSlices; ++t) a[(j * kOzSlices + t) * lda + i] = i < rows ? tile[t][r][tx] : 0;
-    }
+  // lda % 32 == 0 and i0 % 128 == 0: a lane's 4 rows are all inside or all outside [0, lda)
+  const int64_t i = i0 + 4 * lane;
+  if (i >= lda) return;
+  for (int p = warp; p < 32 * kOzSlices; p += 8) {
+    const int jj = p / kOzSlices, t = p - jj * kOzSlices;
+    if (j0 + jj >= n) break;
+    *reinterpret_cast<uint32_t*>(a + ((j0 + jj) * kOzSlices + t) * lda + i) =
+        *reinterpret_cast<const uint32_t*>(&tile[t][jj][4 * lane]);
   }
 }
 
-// cx^T: B[c, i] = cx[i, c] (int8, K-major over the batch rows)
-__global__ void transpose_i8_kernel(const int8_t* cx, int64_t rows, int64_t cols, int64_t ldq, int64_t ldb,
-                                    int8_t* b) {
-  __shared__ int8_t tile[32][33];
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t i = i0 + r, c = c0 + tx;
-    tile[r][tx] = (i < rows && c < cols) ? cx[i * ldq + c] : 0;
-  }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t c = c0 + r, i = i0 + tx;
-    if (c < cols && i < ldb) b[c * ldb + i] = tile[tx][r];
-  }
-}
-
-// the gradient product's column scales 2^(E_j - 6 - 7t) (column j * kOzSlices + t) and its row
-// scale s_a (rows: the act columns)
+// the gradient product's per-run column scales 2^(E_j - 6) (slice t's 2^-7t is applied by the
+// GEMM epilogue) and its row scale s_a (rows: the act columns)
 __global__ void oz_grad_scales_kernel(const unsigned long long* mx, int64_t n, const double* log_sa, int64_t kp,
                                       double* scol, double* srow) {
   const double sa = libm::exp(*log_sa);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < kOzSlices * n || i < kp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n || i < kp;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (i < kOzSlices * n) {
-      const int64_t j = i / kOzSlices, t = i - j * kOzSlices;
-      const double m = __longlong_as_double(static_cast<long long>(mx[j]));
+    if (i < n) {
+      const double m = __longlong_as_double(static_cast<long long>(mx[i]));
       int e = 0;
       if (m > 0.0) frexp(m, &e);
-      scol[i] = m > 0.0 ? ldexp(1.0, e - 6 - 7 * static_cast<int>(t)) : 0.0;
+      scol[i] = m > 0.0 ? ldexp(1.0, e - 6) : 0.0;
     }
     if (i < kp) srow[i] = sa;
   }
@@ -593,7 +705,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   const int64_t cap_rows = G * max_rows;
   double* d = A.get<double>(cap_rows * n);
   // per-iteration products on the int8 tensor cores (QARVD_K7_OZAKI=0: cuBLAS DGEMM, A/B)
-  static const bool ozaki = !(getenv("QARVD_K7_OZAKI") && getenv("QARVD_K7_OZAKI")[0] == '0');
+  const bool ozaki = !(getenv("QARVD_K7_OZAKI") && getenv("QARVD_K7_OZAKI")[0] == '0');
   double* xhat = ozaki ? nullptr : A.get<double>(cap_rows * k);
   // K2 layout of the plan: [outlier columns | pad to 32 | normal columns | pad to 32]
   std::vector<int32_t> pos_h(static_cast<size_t>(k));
@@ -630,6 +742,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
     QARVD_CUDA_TRY(cudaMemcpyAsync(ozpos, pos_h.data(), static_cast<size_t>(k) * 4, cudaMemcpyHostToDevice, s));
     QARVD_CUDA_TRY(cudaMemsetAsync(cx, 0, static_cast<size_t>(kb_cap * k_pad), s));   // pad columns stay 0
     QARVD_CUDA_TRY(cudaMemsetAsync(wsl, 0, static_cast<size_t>(tn * k_pad), s));
+    QARVD_CUDA_TRY(cudaMemsetAsync(bmat, 0, static_cast<size_t>(k_pad * kb_cap), s));  // pad rows stay 0
   }
   double* partial = A.get<double>(kMaxGroup * kRedBlocks);
   // scalars: [0] log_sa [1] m_a [2] v_a [3] g_a [4] loss acc [5] best
@@ -679,18 +792,27 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
         ++end;
       }
       GroupWeights wl{};
+      GroupRows gr{};
+      gr.count = static_cast<int>(end - pos);
+      for (size_t j = pos; j < end; ++j) {
+        const int64_t si = list[j], jj = static_cast<int64_t>(j - pos);
+        gr.src[jj] = sample_rows[si];
+        gr.off[jj + 1] = gr.off[jj] + sample_rows[si + 1] - sample_rows[si];
+        gr.coef[jj] = 2.0 * wsamp[si] * inv_b;
+        wl.w[jj] = wsamp[si];
+      }
+      const int64_t kb = (rows_g + 31) / 32 * 32;
       if (ozaki) {
         // P = s_a code_x . What^T as kOzSlices exact int8 products (K2, f64 epilogue carries the
-        // group scales and the slice weights), summed smallest slice first
-        for (size_t j = pos, off = 0; j < end; ++j) {
-          const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
-          act_codes_kernel<<<blocks_for(rows * k), kT, 0, s>>>(x + r0 * k, rows, k, ozpos, k_pad, sc + 0, aq_max,
-                                                              cx + off * k_pad, flags + 1);
-          off += rows;
-        }
+        // group scales and the slice weights), summed smallest slice first; the act codes of
+        // the whole group in one pass, with their transpose for the gradient product
+        act_codes_group_kernel<<<dim3(static_cast<unsigned>((k + 63) / 64),
+                                      static_cast<unsigned>(((grads ? kb : rows_g) + 63) / 64)),
+                                 256, 0, s>>>(x, k, gr, rows_g, kb, ozpos, k_pad, sc + 0, aq_max, cx,
+                                              grads ? bmat : nullptr, flags + 1);
         oz_scales_kernel<<<blocks_for(tn > rows_g ? tn : rows_g), kT, 0, s>>>(log_s, n, plan_enabled, sc + 0, rows_g,
                                                                            so_sl, sn_sl, sx_rows);
-        count_launch(static_cast<uint64_t>(end - pos) + 1);
+        count_launch(2);
         if (int st = qarvd_dual_gemm_f64_slices(cx, k_pad, wsl, k_pad, rows_g, tn, k_pad, k_o_pad, sx_rows, so_sl,
                                                 sn_sl, kOzSlices, d, n, s))
           return st;
@@ -706,30 +828,24 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
                                      static_cast<int>(k), &one, what, static_cast<int>(k), xhat,
                                      static_cast<int>(k), &zero, d, static_cast<int>(n)));
       }
-      for (size_t j = pos, off = 0; j < end; ++j) {
-        const int64_t si = list[j], r0 = sample_rows[si], rows = sample_rows[si + 1] - r0;
-        wl.w[j - pos] = wsamp[si];
-        // D_b = P_b - T_b (calibrate.cpp:279-280), ||D_b||^2, and D_b *= coeff_b for the gradient
-        dot_partial_kernel<<<kRedBlocks, kT, 0, s>>>(d + off * n, nullptr, rows * n, grads ? 1 : 0,
-                                                     2.0 * wsamp[si] * inv_b, partial + (j - pos) * kRedBlocks,
-                                                     target + r0 * n);
-        off += rows;
-      }
-      dot_final_kernel<<<1, kMaxGroup * 32, 0, s>>>(partial, static_cast<int>(end - pos), wl, nullptr, gi > 0,
-                                        sc + 4);
-      count_launch(2 * static_cast<int>(end - pos) + 2);
+      // D_b = P_b - T_b (calibrate.cpp:279-280), ||D_b||^2, and D_b *= coeff_b for the gradient
+      // (with the column maxima of D' for its slices), one pass over the group
+      const bool colmax = grads && ozaki;
+      if (colmax) QARVD_CUDA_TRY(cudaMemsetAsync(cmax, 0, static_cast<size_t>(n) * 8, s));
+      const int gx = static_cast<int>((n + 2 * kT - 1) / (2 * kT));
+      const int chunks = std::max(1, kRedBlocks / gx);
+      resid_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(chunks * gr.count)), kT, 0, s>>>(
+          d, target, n, gr, chunks, grads ? 1 : 0, partial, chunks * gx, colmax ? cmax : nullptr);
+      dot_final_kernel<<<1, kMaxGroup * 32, 0, s>>>(partial, gr.count, wl, nullptr, gi > 0, sc + 4, chunks * gx);
+      count_launch(2);
       if (grads && ozaki) {
         // dL/dWhat (+)= D'^T X^ = s_a D'^T code_x: D' split per column (2^E_j x int8 slices, K-major
-        // over the batch rows), code_x transposed, one K2 over all slices, recombined per column
-        const int64_t kb = (rows_g + 31) / 32 * 32;
-        QARVD_CUDA_TRY(cudaMemsetAsync(cmax, 0, static_cast<size_t>(n) * 8, s));
-        colmax_kernel<<<dim3(static_cast<unsigned>((n + kT - 1) / kT), 64), kT, 0, s>>>(d, rows_g, n, cmax);
-        d_slices_t_kernel<<<dim3(static_cast<unsigned>(kb / 32), static_cast<unsigned>((n + 31) / 32)), 256, 0, s>>>(
+        // over the batch rows), code_x^T from the act-code pass, one K2 over all slices,
+        // recombined per column
+        d_slices_t_kernel<<<dim3(static_cast<unsigned>((kb + kDsRows - 1) / kDsRows), static_cast<unsigned>((n + 31) / 32)), 256, 0, s>>>(
             d, rows_g, n, cmax, kb, amat);
-        transpose_i8_kernel<<<dim3(static_cast<unsigned>(kb / 32), static_cast<unsigned>(k_pad / 32)), 256, 0, s>>>(
-            cx, rows_g, k_pad, k_pad, kb, bmat);
         oz_grad_scales_kernel<<<blocks_for(tn > k_pad ? tn : k_pad), kT, 0, s>>>(cmax, n, sc + 0, k_pad, sx_a, srow_a);
-        count_launch(4);
+        count_launch(2);
         // Gt [k_pad x n] = s_a code_x^T . D' (act columns as rows, the D' slices as columns)
         if (int st = qarvd_dual_gemm_f64_slices(bmat, kb, amat, kb, k_pad, tn, kb, 0, srow_a, nullptr, sx_a,
                                                 kOzSlices, gsl, n, s))
@@ -768,7 +884,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
     w_slices_kernel<<<blocks_for(nk), kT, 0, s>>>(code, n, k, ozpos, k_pad, wsl);
     count_launch();
   };
-  weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+  weights_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
                                               -wq_max, wq_max, 1, what, ozaki ? code : nullptr, nullptr, nullptr);
   count_launch();
   slice_weights();
@@ -783,7 +899,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   for (int t = 0; t < iters; ++t) {
     for (int b = 0; b < cfg->batch_size; ++b)
       batch[b] = static_cast<int64_t>(splitmix64_h(st_rng) % static_cast<uint64_t>(n_samples));
-    weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+    weights_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
                                                 -wq_max, wq_max, 0, what, code, dhdv, nullptr);
     count_launch();
     slice_weights();
@@ -807,7 +923,7 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   }
 
   // final hard loss, hard codes, learned scales and act scale (calibrate.cpp:391-395)
-  weights_kernel<<<blocks_for(nk), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
+  weights_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_s, n, k, zeta, gamma,
                                               -wq_max, wq_max, 1, what, ozaki ? code : nullptr, nullptr, codes);
   count_launch();
   slice_weights();
@@ -844,7 +960,7 @@ extern "C" int qarvd_adaround_weights(const double* w, const double* v, const ui
     what = scratch;
   }
   const int qmax = (1 << (w_bits - 1)) - 1;
-  weights_kernel<<<blocks_for(n * k), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_scale, n, k, zeta, gamma_lo,
+  weights_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(w, v, outlier_mask, plan_enabled, log_scale, n, k, zeta, gamma_lo,
                                                   -qmax, qmax, hard ? 1 : 0, what, nullptr, nullptr, codes);
   count_launch();
   if (scratch) cudaFreeAsync(scratch, s);

@@ -37,6 +37,54 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kCtrlRegs = 32;   // setmaxnreg split of 640 x 96 registers
 constexpr int kEpiRegs = 112;   //   (4 x 32 x 32 + 16 x 32 x 112 = 640 x 96)
 constexpr int CW = 16;            // columns per epilogue chunk (one tcgen05.ld .32x32b.x16)
+
+// K7's slice products (qarvd_dual_gemm_f64_slices): run j of T consecutive accumulator columns holds
+// the integer products of slices t = 0..T-1 whose weight is 2^-7t.  Groups of four slices combine
+// exactly in int64 (|acc| < 2^31, so a group stays below 2^53 and converts to f64 exactly); the
+// group values are scaled by exact powers of two and added smallest first, then
+// y = s_x (s_o v_o + s_n v_n) with the per-run scales.
+__device__ __forceinline__ double exp2_int(int e) {  // 2^e, e in the normal range
+  return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+// int64 -> f64 for |v| < 2^51 without the XU pipe's conversion: the bits of 1.5 * 2^52 + v are
+// the bits of 0x1.8p52 plus v, so one integer add and one exact f64 subtraction
+__device__ __forceinline__ double small_i64_to_f64(long long v) {
+  return __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL), 6755399441055744.0);
+}
+// MAGIC: |group| < 2^51 (k <= 32768: |acc| <= k * 127 * 128 < 2^29, a group of four < 2^50.1)
+template <int T, bool MAGIC>
+__device__ __forceinline__ double slice_value(const uint32_t* acc) {
+  double v = 0.0;
+#pragma unroll
+  for (int g0 = ((T - 1) / 4) * 4; g0 >= 0; g0 -= 4) {
+    const int last = (g0 + 4 < T ? g0 + 4 : T) - 1;
+    long long part = static_cast<int32_t>(acc[last]);
+#pragma unroll
+    for (int t = last - 1; t >= g0; --t)  // one IMAD.WIDE per slice
+      part += static_cast<long long>(static_cast<int32_t>(acc[t])) * (1LL << (7 * (last - t)));
+    const double pv = MAGIC ? small_i64_to_f64(part) : __ll2double_rn(part);
+    v = g0 == ((T - 1) / 4) * 4 ? __dmul_rn(pv, exp2_int(-7 * last))
+                                : __fma_rn(pv, exp2_int(-7 * last), v);
+  }
+  return v;
+}
+template <int T, bool MAGIC>
+__device__ __forceinline__ void slice_runs(const uint32_t* rn, const uint32_t* ro, bool has_outlier, double sx,
+                                           const double* so, const double* sn, int64_t run0, double* yr) {
+  double out[CW / T];
+#pragma unroll
+  for (int g = 0; g < CW / T; ++g) {
+    const double vn = __dmul_rn(__dmul_rn(sx, sn[run0 + g]), slice_value<T, MAGIC>(rn + g * T));
+    out[g] = has_outlier ? __dadd_rn(__dmul_rn(__dmul_rn(sx, so[run0 + g]), slice_value<T, MAGIC>(ro + g * T)), vn)
+                         : vn;
+  }
+  if (CW / T == 2 && (reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
+    *reinterpret_cast<double2*>(yr) = make_double2(out[0], out[1]);
+  } else {
+#pragma unroll
+    for (int g = 0; g < CW / T; ++g) yr[g] = out[g];
+  }
+}
 constexpr int kYStageBytes = 32 * CW * 2;  // one warp's bf16 staging tile: 32 rows x 32 B
 
 // BN = output columns of the (pair) tile; CG = CTAs per MMA (1, or 2 = an SM pair
@@ -81,7 +129,7 @@ struct GemmParams {
   const double* so64;
   const double* sn64;
   int f64_slices;      // QARVD_F64 with f64_slices = T > 1: each run of T consecutive output columns
-                       // is summed (last first) into one f64 column (K7's exact integer slices)
+                       // (slice t weighted 2^-7t, per-run scales) recombines into one f64 column
   uint32_t* row_absmax;  // optional: atomicMax per row of the sign-cleared bf16 output bits
   uint32_t* row_pmax;    // optional: per-row partial maxima, [m][pm_count] (one per epilogue
   int pm_count;          //   warp and tile: pm_count = num_n_blks * 4), plain stores
@@ -978,6 +1026,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           // val += (s_x*s_wn)*acc_n  (outlier group first, f64, no FMA)
           if (row_ok) {
             const double sx64 = p.sx64[row];
+            const int T = p.f64_slices;
+            if (T > 1) {  // n % 16 == 0 and T | 16: whole runs only
+              double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0 / T;
+              if (p.k <= 32768) {
+                switch (T) {
+                  case 2: slice_runs<2, true>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  case 4: slice_runs<4, true>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  case 8: slice_runs<8, true>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  default: slice_runs<16, true>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                }
+              } else {
+                switch (T) {
+                  case 2: slice_runs<2, false>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  case 4: slice_runs<4, false>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  case 8: slice_runs<8, false>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                  default: slice_runs<16, false>(rn, ro, has_outlier, sx64, p.so64, p.sn64, col0 / T, yr); break;
+                }
+              }
+              continue;
+            }
             double vv[CW];
 #pragma unroll
             for (int e = 0; e < CW; ++e) {
@@ -991,15 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               vv[e] = v;
             }
-            const int T = p.f64_slices;
-            if (T > 1) {  // n % 16 == 0 and T | 16: whole runs only
-              double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0 / T;
-              for (int g = 0; g < CW / T; ++g) {
-                double acc = 0.0;
-                for (int t = T - 1; t >= 0; --t) acc = __dadd_rn(acc, vv[g * T + t]);
-                yr[g] = acc;
-              }
-            } else {
+            {
               double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + col0;
 #pragma unroll
               for (int e = 0; e < CW; ++e)
@@ -1335,7 +1395,14 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.trace = getenv("QARVD_GEMM_TRACE") ? 1 + (getenv("QARVD_GEMM_TRACE_CTA") ? atoi(getenv("QARVD_GEMM_TRACE_CTA")) : 0) : 0;
   p.epilogue = epilogue;
   p.out_dtype = out_dtype;
-  const TileCfg c = choose_cfg(m, n, k);
+  TileCfg c = choose_cfg(m, n, k);
+  if (out_dtype == QARVD_F64 && f64_slices > 1 && !getenv("QARVD_GEMM_BN")) {
+    // K7's slice products: at 256 columns one accumulator stage fills TMEM, so the MMA of the
+    // next tile waits for the whole f64 epilogue; 128-column tiles double-buffer the
+    // accumulators and the epilogue overlaps the next tile's MMA (QARVD_F64_BN=256 for A/B)
+    const char* env = getenv("QARVD_F64_BN");
+    c.bn = env && atoi(env) == 256 ? 256 : 128;
+  }
   if (sk_workspace) {
     const SkLayout L = sk_layout(m, n, k, k_outlier, out_dtype, acc_o || acc_n || row_absmax || row_pmax);
     if (L.bytes > 0 && sk_workspace_bytes >= L.bytes) {

@@ -24,6 +24,9 @@ void ref_exp(const double* x, double* y, int64_t n) {
 void ref_log(const double* x, double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = qarvd_b200::libm::log(x[i]);
 }
+void ref_pow(const double* x, const double* e, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = qarvd_b200::libm::pow(x[i], e[i]);
+}
 void glibc_exp(const double* x, double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = std::exp(x[i]);
 }

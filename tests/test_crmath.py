@@ -100,3 +100,31 @@ def test_libm_restatement_special_values(crm):
     for f in ("exp", "log"):
         a, b = _call(crm, "ref_" + f, sp), _call(crm, "glibc_" + f, sp)
         assert np.array_equal(a, b, equal_nan=True), f
+
+
+@pytest.mark.parametrize("gen", [
+    # the regulariser's pow(max(|2h - 1|, 1e-12), beta - 1), beta annealed 20 -> 2 (calibrate.cpp:358)
+    lambda r: (np.maximum(np.abs(r.uniform(-1, 1, 2_000_000)), 1e-12), r.uniform(1.0, 19.0, 2_000_000)),
+    lambda r: (np.exp(r.uniform(-700, 700, 1_000_000)), r.uniform(-3, 3, 1_000_000)),
+    lambda r: (r.uniform(0.5, 2.0, 1_000_000), r.uniform(-1000, 1000, 1_000_000)),  # over / underflow
+    lambda r: (np.exp(r.uniform(-2, 2, 500_000)), r.uniform(300, 700, 500_000)),    # the exp specialcase
+    lambda r: (-r.integers(1, 50, 500_000).astype(np.float64) * r.uniform(0.9, 1.1, 500_000),
+               r.integers(-60, 60, 500_000).astype(np.float64)),                   # x < 0, integer y
+    lambda r: (r.uniform(0, 2.3e-308, 300_000), r.uniform(-0.5, 0.5, 300_000)),     # subnormal x
+])
+def test_libm_pow_matches_host_glibc(crm, gen):
+    x, e = gen(np.random.default_rng(17))
+    ours = _call(crm, "ref_pow", x, e)
+    glibc = _call(crm, "glibc_pow", x, e)
+    same = (ours == glibc) | (np.isnan(ours) & np.isnan(glibc))
+    assert same.all(), (x[~same][:5], e[~same][:5], ours[~same][:5], glibc[~same][:5])
+
+
+def test_libm_pow_special_values(crm):
+    v = np.array([0.0, -0.0, 1.0, -1.0, 2.0, -2.0, 0.5, np.inf, -np.inf, np.nan, 5e-324, 3.0, -3.0,
+                  1e-300, 1e300, 1 + 2 ** -52, 1e-20, 2.0 ** -70, 2.0 ** 70], dtype=np.float64)
+    x, e = np.meshgrid(v, v)
+    x, e = x.ravel().copy(), e.ravel().copy()
+    a, b = _call(crm, "ref_pow", x, e), _call(crm, "glibc_pow", x, e)
+    same = (a == b) | (np.isnan(a) & np.isnan(b))
+    assert same.all(), (x[~same], e[~same], a[~same], b[~same])
