@@ -721,7 +721,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       // outputs): compile-time chunk loops with the per-chunk checks hoisted to the tile.
       const bool fast = two_step && p.use_tma_store && !p.row_absmax &&
                         static_cast<int64_t>(n_blk + 1) * BN <= p.n;
-      if (fast && p.epi_regs) {
+      if (BN <= 128 && p.out_dtype == QARVD_F64 && p.f64_slices == 8 && p.k <= 32768 && !p.acc_n_dbg &&
+          !p.acc_o_dbg) {
+        // K7's slice products: every chunk of the warp (both slabs) is read into registers and
+        // the TMEM stage is released at once, so the next tile's MMAs overlap this tile's f64
+        // recombination
+        constexpr int NCH = BN / CW / kSubs;
+        uint32_t an[NCH][CW], ao[NCH][CW];
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          ptx::tmem_ld16(t_n + (half + i * kSubs) * CW, an[i]);
+          if (has_outlier) ptx::tmem_ld16(t_o + (half + i * kSubs) * CW, ao[i]);
+        }
+        const int64_t run_base = (static_cast<int64_t>(n_blk) * BN + half * CW) / 8;
+        const double sx64 = row_ok ? p.sx64[row] : 0.0;
+        ptx::tmem_wait_ld();
+        release(&tempty[acc]);
+        if (C::kAccStages == 1) release(&tofree[0]);
+        if (row_ok) {
+          double* yr = reinterpret_cast<double*>(p.y) + row * p.ldy + run_base;
+          const bool vec = ((reinterpret_cast<uintptr_t>(yr) | static_cast<uintptr_t>(p.ldy * 8)) & 15) == 0;
+#pragma unroll
+          for (int i = 0; i < NCH; ++i) {
+            if ((run_base + i * (kSubs * CW / 8)) * 8 >= p.n) break;
+            const int64_t r0 = run_base + i * (kSubs * CW / 8);
+            double out[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const double vn = __dmul_rn(__dmul_rn(sx64, p.sn64[r0 + g]), slice_value<8, true>(an[i] + 8 * g));
+              out[g] = has_outlier
+                           ? __dadd_rn(__dmul_rn(__dmul_rn(sx64, p.so64[r0 + g]), slice_value<8, true>(ao[i] + 8 * g)), vn)
+                           : vn;
+            }
+            double* dst = yr + i * (kSubs * CW / 8);
+            if (vec) {
+              *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+            } else {
+              dst[0] = out[0];
+              dst[1] = out[1];
+            }
+          }
+        }
+      } else if (fast && p.epi_regs) {
         // register-held variant: the warp's 4 acc_n chunks (64 columns) are read into
         // registers and acc_n is released at once; the dequant/GELU/stores then overlap the
         // next tile's normal-slab MMAs and only acc_o (read chunk by chunk) gates its outliers.
@@ -1402,6 +1443,10 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
     // accumulators and the epilogue overlaps the next tile's MMA (QARVD_F64_BN=256 for A/B)
     const char* env = getenv("QARVD_F64_BN");
     c.bn = env && atoi(env) == 256 ? 256 : 128;
+    // short K (the forward product, K = the layer width): 128-byte stages keep twice as many
+    // loads in flight (measured: QARVD_GEMM_KS=1 on both products cut the loss passes by 16%
+    // but slowed the long-K gradient product)
+    if (!getenv("QARVD_GEMM_KS") && k <= 4096) c.ks = 1;
   }
   if (sk_workspace) {
     const SkLayout L = sk_layout(m, n, k, k_outlier, out_dtype, acc_o || acc_n || row_absmax || row_pmax);
