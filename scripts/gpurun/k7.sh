@@ -12,4 +12,4 @@ for oz, bn in (("1", "128"), ("1", "256"), ("0", "128")):
     print("OZAKI", oz, "BN", bn, json.dumps({k: r[k] for k in ("ms_per_iteration", "fixed_ms", "final_loss", "initial_loss")}))
 PY
 unset QARVD_K7_OZAKI QARVD_F64_BN
-bash scripts/_r2_k7prof.sh
+bash scripts/gpurun/k7prof.sh
