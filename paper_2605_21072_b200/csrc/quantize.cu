@@ -1575,6 +1575,217 @@ int launch_act_reg(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32
   return -1;  // no register shape: the caller takes the slot-ring kernel
 }
 
+// ---------------------------------------------------------------------------
+// K1, bulk-staged variant (opt-in, QARVD_K1_BULK=1): persistent CTAs of 256 threads; a
+// team (one warp for rows of < 4096 values, eight teams per CTA; else the whole CTA) owns
+// every nteams-th row and keeps S of its rows in flight as 1-D bulk copies (cp.async.bulk,
+// mbarrier completion) into shared-memory slots.  Registers no longer bound the bytes in
+// flight (the register kernel held one row per team: 0.3-0.47 of HBM, long_scoreboard), and
+// there is no per-row CTA launch.  Per row: |x| max from the slot (team reduction), the row
+// scale, then the codes from the slot (plan order: 8 per lane per step; with a gather: 4
+// per lane through the staged int16 table, the slot's 8 trailing zero sentinels serving the
+// pad columns) -- same arithmetic, tie repair and error reporting as the register kernel.
+template <int TW>
+struct K1Bulk {
+  static constexpr int kThreads = 256;
+  static constexpr int kTeams = kThreads / (32 * TW);
+  static __host__ __device__ int slot_stride(int k) { return (k * 2 + 16 + 127) & ~127; }  // bytes
+};
+
+template <int TW, int S, bool kStatic, bool kGather>
+__global__ void __launch_bounds__(256)
+    quant_act_bulk_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
+                          const int32_t* __restrict__ gather, int k_out, double static_scale, int qmax,
+                          double rqmax, int8_t* __restrict__ q, int64_t ldq, float* __restrict__ s32_out,
+                          double* __restrict__ s64_out, unsigned long long* __restrict__ err) {
+  using B = K1Bulk<TW>;
+  constexpr int T = 32 * TW;
+  extern __shared__ __align__(128) uint8_t k1b_smem[];
+  __shared__ __align__(8) uint64_t full[B::kTeams][S];
+  __shared__ uint32_t wmax[TW];
+  const int stride = B::slot_stride(k);
+  const int team = static_cast<int>(threadIdx.x) / T, tt = static_cast<int>(threadIdx.x) % T;
+  const int lane = threadIdx.x & 31, warp = tt >> 5;
+  uint8_t* slots = k1b_smem + team * S * stride;
+  int16_t* gidx = reinterpret_cast<int16_t*>(k1b_smem + B::kTeams * S * stride);
+  if (threadIdx.x < B::kTeams * S) ptx::mbar_init(&full[threadIdx.x / S][threadIdx.x % S], 1);
+  // zero sentinels after every slot's row (the bulk copies never write them)
+  for (int i = threadIdx.x; i < B::kTeams * S; i += blockDim.x)
+    *reinterpret_cast<uint4*>(k1b_smem + i * stride + k * 2) = make_uint4(0u, 0u, 0u, 0u);
+  if (kGather) {
+    for (int c4 = threadIdx.x; c4 < (k_out >> 2); c4 += blockDim.x) {
+      const int4 g = __ldg(reinterpret_cast<const int4*>(gather) + c4);
+      reinterpret_cast<uint2*>(gidx)[c4] =
+          make_uint2(static_cast<uint16_t>(g.x < 0 ? k : g.x) | (static_cast<uint32_t>(g.y < 0 ? k : g.y) << 16),
+                     static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16));
+    }
+  }
+  ptx::fence_mbar_init();
+  __syncthreads();
+  pdl_wait();  // x is written by the previous kernel of the chain
+  pdl_launch_dependents();
+  const int64_t nteams = static_cast<int64_t>(gridDim.x) * B::kTeams;
+  const int64_t team_id = static_cast<int64_t>(blockIdx.x) * B::kTeams + team;
+  const uint32_t row_bytes = static_cast<uint32_t>(k) * 2u;
+  const bool producer = tt == 0;
+  if (producer) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t row = team_id + s * nteams;
+      if (row < m) {
+        ptx::mbar_expect_tx(&full[team][s], row_bytes);
+        ptx::bulk_load_1d(slots + s * stride, x + row * ldx, row_bytes, &full[team][s]);
+      }
+    }
+  }
+  const int nvec = k >> 3;
+  ActScale sc;
+  sc.fq = static_cast<float>(qmax);
+  for (int i = 0;; ++i) {
+    const int64_t row = team_id + static_cast<int64_t>(i) * nteams;
+    if (row >= m) break;
+    const int s = i % S;
+    ptx::mbar_wait(&full[team][s], static_cast<uint32_t>((i / S) & 1));
+    const uint16_t* srow = reinterpret_cast<const uint16_t*>(slots + s * stride);
+    const uint4* srow4 = reinterpret_cast<const uint4*>(srow);
+    uint32_t mx = 0;
+    for (int c = tt; c < nvec; c += T) {
+      const uint4 d = srow4[c];
+      mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
+                                 __vmaxu2(d.z & 0x7fff7fffu, d.w & 0x7fff7fffu)));
+    }
+    uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+    if (TW > 1) {
+      if (lane == 0) wmax[warp] = mag;
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < TW; ++w) mag = max(mag, wmax[w]);
+    }
+    const bool row_bad = mag >= 0x7f80u;
+    const float amax = __uint_as_float(mag << 16);
+    double s64;
+    if (kStatic) {
+      const GroupScale g = scale_static(static_scale);
+      sc.r = g.r32;
+      sc.exact = g.exact;
+      s64 = static_scale;
+    } else {  // r = fl(fl(1/amax) * qmax), s64 = fl64(amax / qmax): see quant_act_rows_kernel
+      sc.r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+      sc.exact = amax > 0.f && !(sc.r <= FLT_MAX && sc.r >= FLT_MIN);
+      if (!(amax > 0.f)) {
+        s64 = DBL_MIN;
+      } else {
+        const double a = static_cast<double>(amax), y = a * rqmax;
+        s64 = fma(fma(-y, static_cast<double>(qmax), a), rqmax, y);
+      }
+    }
+    sc.s64 = s64;
+    if (tt == T - 1) {
+      if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s64) : 0.f;
+      if (s64_out) s64_out[row] = s64;
+    }
+    int8_t* qr = q + row * ldq;
+    const bool slow = row_bad || sc.exact;  // rare rows: non-finite input (reported) or no usable fp32 reciprocal
+    if (!kGather) {
+      for (int c = tt; c < nvec; c += T) {
+        const uint4 d = srow4[c];
+        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+        uint32_t cd[8];
+        if (slow) {
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            cd[h] = act_code_slow(static_cast<uint16_t>(h & 1 ? w[h >> 1] >> 16 : w[h >> 1] & 0xffffu), s64, qmax,
+                                  err, row * k_out + c * 8 + h);
+        } else {
+          float dmax = 0.f;
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, cd[2 * h],
+                                cd[2 * h + 1], dmax);
+          if (dmax > tie_guard<kStatic>()) {  // a value within the tie guard: decide exactly
+            *reinterpret_cast<uint2*>(qr + c * 8) = act_fix8_reg<1, 1, kStatic, false>(d, sc, s64, qmax);
+            continue;
+          }
+        }
+        *reinterpret_cast<uint2*>(qr + c * 8) =
+            make_uint2(pack4(cd[0], cd[1], cd[2], cd[3]), pack4(cd[4], cd[5], cd[6], cd[7]));
+      }
+    } else {
+      for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
+        const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+        const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu], srow[gp.y >> 16]};
+        uint32_t cd[4];
+        if (slow) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cd[e] = act_code_slow(hv[e], s64, qmax, err, row * k_out + c0 + e);
+        } else {
+          float dmax = 0.f;
+          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
+                              __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, cd[0], cd[1], dmax);
+          act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
+                              __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, cd[2], cd[3], dmax);
+          if (dmax > tie_guard<kStatic>()) {
+            *reinterpret_cast<uint32_t*>(qr + c0) =
+                act_fix4_reg<kStatic>(make_uint2(hv[0] | (static_cast<uint32_t>(hv[1]) << 16),
+                                                 hv[2] | (static_cast<uint32_t>(hv[3]) << 16)), sc, s64, qmax);
+            continue;
+          }
+        }
+        *reinterpret_cast<uint32_t*>(qr + c0) = pack4(cd[0], cd[1], cd[2], cd[3]);
+      }
+    }
+    // the slot is free once the whole team has read it: refill it with the team's row i + S
+    if (TW > 1) __syncthreads();
+    else __syncwarp();
+    const int64_t next = row + S * nteams;
+    if (producer && next < m) {
+      ptx::fence_proxy_async_smem();  // generic-proxy reads of the slot before the async write
+      ptx::mbar_expect_tx(&full[team][s], row_bytes);
+      ptx::bulk_load_1d(slots + s * stride, x + next * ldx, row_bytes, &full[team][s]);
+    }
+  }
+}
+
+template <int TW, int S, bool kStatic, bool kGather>
+int launch_act_bulk_t(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather, int k_out,
+                      double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                      unsigned long long* err, cudaStream_t stream) {
+  using B = K1Bulk<TW>;
+  auto kern = quant_act_bulk_kernel<TW, S, kStatic, kGather>;
+  const size_t smem = static_cast<size_t>(B::kTeams) * S * B::slot_stride(k) +
+                      (kGather ? static_cast<size_t>((k_out + 7) & ~7) * 2 : 0);
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  static int per_sm = 1, sms = kNumSMs;
+  std::call_once(once, [&] {
+    attr = set_smem_attrs(kern, 200 * 1024);
+    if (attr == cudaSuccess) attr = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B::kThreads, smem);
+    int dev = 0;
+    if (attr == cudaSuccess) attr = cudaGetDevice(&dev);
+    if (attr == cudaSuccess) attr = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  QARVD_CUDA_TRY(attr);
+  const int64_t teams = (m + B::kTeams - 1) / B::kTeams;
+  const int64_t grid = std::min<int64_t>(teams, static_cast<int64_t>(sms) * std::max(per_sm, 1));
+  QARVD_CUDA_TRY(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(B::kThreads), smem, stream, 1, x, m,
+                            k, ldx, gather, k_out, static_scale, qmax, 1.0 / static_cast<double>(qmax), q, ldq,
+                            s32, s64, err));
+  return QARVD_OK;
+}
+
+// bulk-staged K1: rows of >= 4096 values as whole-CTA teams with 4 slots (3 CTAs per SM at
+// K = 8960), shorter rows as warp teams with 3 slots each
+template <bool kStatic, bool kGather>
+int launch_act_bulk(const uint16_t* x, int64_t m, int k, int64_t ldx, const int32_t* gather, int k_out,
+                    double static_scale, int qmax, int8_t* q, int64_t ldq, float* s32, double* s64,
+                    unsigned long long* err, cudaStream_t stream) {
+  if (k >= 4096)
+    return launch_act_bulk_t<8, 4, kStatic, kGather>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
+                                                     s64, err, stream);
+  return launch_act_bulk_t<1, 3, kStatic, kGather>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
+                                                   s64, err, stream);
+}
+
 template <bool kStatic>
 int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t ldx,
                     const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
@@ -1584,6 +1795,17 @@ int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t 
   // 8960: 41 vs 45 us; scripts/k1_flush_probe.py); gathered rows keep the slot ring, which the
   // register kernel does not beat (19.5 vs 18.4 us at 4680 x 1536).  QARVD_K1_REG=0 / =2: never /
   // always (gathered too).
+  // QARVD_K1_BULK=1: the bulk-staged kernel (opt-in: measured slower on the Wan shapes, x 23.6 vs
+  // 17.4 us and U 37.7 vs 33.8 us under the bench's L2 flush, scripts/k1_flush_probe.py -- it
+  // issues ~12 instructions per value and stays issue-bound with the bytes in flight solved)
+  const int bulk = getenv("QARVD_K1_BULK") ? atoi(getenv("QARVD_K1_BULK")) : 0;  // per call (tests A/B it)
+  const int64_t bulk_smem = static_cast<int64_t>(k >= 4096 ? 4 : 8 * 3) * K1Bulk<1>::slot_stride(k) +
+                            (gathered ? ((k_out + 7) & ~7) * 2 : 0);
+  if (bulk > 0 && (!gathered || k_out % 4 == 0) && bulk_smem <= 200 * 1024)
+    return gathered ? launch_act_bulk<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
+                                                     s64, err, stream)
+                    : launch_act_bulk<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
+                                                      s64, err, stream);
   static const int reg = getenv("QARVD_K1_REG") ? atoi(getenv("QARVD_K1_REG")) : 1;
   if (reg > 0 && (!gathered || (reg == 2 && k_out % 4 == 0))) {
     const int st = gathered ? launch_act_reg<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,

@@ -1305,3 +1305,32 @@ def test_k2_tile_overrides_bitexact(cuda, monkeypatch, bn, cg, ks):
             monkeypatch.delenv(v)
         torch.cuda.synchronize()
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16)), (n, k)
+
+
+# ---------------------------------------------------------------- K1 bulk-staged variant (opt-in)
+@pytest.mark.parametrize("m,k,n_out,gathered", [(4680, 1536, 32, True), (4680, 8960, 0, False),
+                                                (257, 1536, 0, True), (300, 2048, 0, False), (33, 200, 5, True)])
+def test_k1_bulk_staged_bitexact(cuda, monkeypatch, m, k, n_out, gathered):
+    """QARVD_K1_BULK=1 (persistent CTAs, rows staged by cp.async.bulk): same codes and scales as
+    the oracle, with and without the plan gather, including tie rows."""
+    monkeypatch.setenv("QARVD_K1_BULK", "1")
+    plan = make_plan(k, n_out, seed=m + 1)
+    bits, x64 = bf16_values((m, k), seed=k + 7 * m, heavy_cols=plan.outlier_indices if n_out else None)
+    # a few rows of exact .5 ties
+    for i in range(min(m, 8)):
+        a = float(2.0 ** (i - 3))
+        row = (np.arange(k, dtype=np.float64) % 255 - 127) * (a / 127.0) * 0.5
+        row[0] = a
+        bits[i] = oracle.f32_to_bf16_bits(row.astype(np.float32))
+    x64 = oracle.bf16_bits_to_f64(bits)
+    x = to_dev_bf16(bits)
+    g = plan.gather if gathered else None
+    kout = plan.k_pad if gathered else k
+    xq = torch.empty((m, kout), dtype=torch.int8, device="cuda")
+    s64 = torch.empty(m, dtype=torch.float64, device="cuda")
+    gdev = torch.from_numpy(plan.gather.astype(np.int32)).cuda() if gathered else None
+    qb._lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, m, k, k, None if gdev is None else gdev.data_ptr(),
+                 kout, qb.ACT_PER_TOKEN, 0.0, 8, xq.data_ptr(), kout, None, s64.data_ptr(), None, None)
+    q_ref, s_ref, _ = oracle.quantize_act(x64, g, per_token=True)
+    np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
+    np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
