@@ -1016,15 +1016,22 @@ __device__ __noinline__ void wq_fix_chunk(const uint16_t* hv, uint32_t* c, ActSc
   if (rescan) act_fix_chunk<false, 4, true>(hv, c, sc, s64, qmax, rescan);
 }
 
-__global__ void __launch_bounds__(32 * kWTeams, 4)
+// TW warps per row (1 for rows of <= 2048 values, 8 for the wide rows: one warp per 8960-wide
+// row kept 4-5 warps per SM busy), TEAMS row teams per CTA.  Pass 1 takes the two group maxima
+// from the contiguous row (16-byte reads) with an outlier-column bitmask instead of the gather.
+template <int TW, int TEAMS>
+__global__ void __launch_bounds__(32 * TW * TEAMS)
     prep_weights_batched_kernel(const WeightJobDev* __restrict__ jobs, int qmax, double rqmax,
                                 unsigned long long* __restrict__ err) {
+  constexpr int T = 32 * TW;
   extern __shared__ __align__(128) uint16_t wsm[];
-  __shared__ __align__(8) uint64_t full[kWTeams][2];
+  __shared__ __align__(8) uint64_t full[TEAMS][2];
+  __shared__ uint32_t red[TEAMS][TW][2];
   const WeightJobDev J = jobs[blockIdx.y];
-  const int team = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kWTeams + team;
-  if (static_cast<int64_t>(blockIdx.x) * kWTeams >= J.n) return;  // CTA-uniform
+  const int team = static_cast<int>(threadIdx.x) / T, tt = static_cast<int>(threadIdx.x) % T;
+  const int lane = threadIdx.x & 31, warp = tt >> 5;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * TEAMS + team;
+  if (static_cast<int64_t>(blockIdx.x) * TEAMS >= J.n) return;  // CTA-uniform
   pdl_wait();  // the plan kernel (qarvd_prepare_weights_planned) writes gather / plan_info
   const int k = static_cast<int>(J.k);
   const int k_pad = static_cast<int>(J.plan_info ? J.plan_info[1] : J.k_pad);
@@ -1032,17 +1039,20 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
   const int row_stride = (k + 8 + 63) & ~63;
   // two row slots per team: row j+1 streams in while row j is rounded
   uint16_t* slots = wsm + team * 2 * row_stride;
-  int16_t* gidx = reinterpret_cast<int16_t*>(wsm + kWTeams * 2 * row_stride);
-  const int64_t step = static_cast<int64_t>(gridDim.x) * kWTeams;
+  int16_t* gidx = reinterpret_cast<int16_t*>(wsm + TEAMS * 2 * row_stride);
+  uint32_t* omask = reinterpret_cast<uint32_t*>(wsm + TEAMS * 2 * row_stride + ((J.k_pad + 7) & ~int64_t(7)));
+  const int mask_words = (k + 31) >> 5;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * TEAMS;
   const uint32_t row_bytes = static_cast<uint32_t>(k) * 2u;
-  if (threadIdx.x < 2 * kWTeams) ptx::mbar_init(&full[threadIdx.x >> 1][threadIdx.x & 1], 1);
+  if (threadIdx.x < 2 * TEAMS) ptx::mbar_init(&full[threadIdx.x >> 1][threadIdx.x & 1], 1);
   ptx::fence_mbar_init();
+  for (int i = threadIdx.x; i < mask_words; i += blockDim.x) omask[i] = 0u;
   __syncthreads();
   auto load = [&](int sl, int64_t row) {
     ptx::mbar_expect_tx(&full[team][sl], row_bytes);
     ptx::bulk_load_1d(slots + sl * row_stride, J.w + row * J.ldw, row_bytes, &full[team][sl]);
   };
-  if (lane == 0) {
+  if (tt == 0) {
     if (row0 < J.n) load(0, row0);
     if (row0 + step < J.n) load(1, row0 + step);
   }
@@ -1052,27 +1062,64 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
     const uint32_t hi = static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16);
     reinterpret_cast<uint2*>(gidx)[c4] = make_uint2(lo, hi);
   }
-  if (lane < 8) {
-    slots[k + lane] = 0;
-    slots[row_stride + k + lane] = 0;
+  for (int p = threadIdx.x; p < k_o; p += blockDim.x) {  // the outlier slab's columns
+    const int g = __ldg(J.gather + p);
+    if (g >= 0 && g < k) atomicOr(&omask[g >> 5], 1u << (g & 31));
+  }
+  if (tt < 8) {
+    slots[k + tt] = 0;
+    slots[row_stride + k + tt] = 0;
   }
   __syncthreads();
 
+  const int nv = k >> 3;
+  const uint4* const slot4[2] = {reinterpret_cast<const uint4*>(slots), reinterpret_cast<const uint4*>(slots + row_stride)};
   int j = 0;
   for (int64_t row = row0; row < J.n; row += step, ++j) {
     const uint16_t* srow = slots + (j & 1) * row_stride;
     ptx::mbar_wait_spin(&full[team][j & 1], static_cast<uint32_t>((j >> 1) & 1));
-    // ---- pass 1: group maxima through the gather (sign-cleared bf16 bits)
+    // ---- pass 1: group maxima over the contiguous row (sign-cleared bf16 bits)
     uint32_t mo = 0, mn = 0;
-    for (int c0 = lane * 4; c0 < k_pad; c0 += 128) {
-      const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
-      const uint32_t a = max(max(srow[gp.x & 0xffffu] & 0x7fffu, srow[gp.x >> 16] & 0x7fffu),
-                             max(srow[gp.y & 0xffffu] & 0x7fffu, srow[gp.y >> 16] & 0x7fffu));
-      if (c0 < k_o) mo = max(mo, a);
-      else mn = max(mn, a);
+    const uint4* s4 = slot4[j & 1];
+    for (int c8 = tt; c8 < nv; c8 += T) {
+      const uint4 d = s4[c8];
+      const uint32_t mb = (omask[c8 >> 2] >> ((c8 & 3) * 8)) & 0xffu;
+      if (mb == 0u) {
+        const uint32_t m2 = __vmaxu2(__vmaxu2(d.x & 0x7fff7fffu, d.y & 0x7fff7fffu),
+                                     __vmaxu2(d.z & 0x7fff7fffu, d.w & 0x7fff7fffu));
+        mn = max(mn, max(m2 & 0xffffu, m2 >> 16));
+      } else {
+        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t lo = w[h] & 0x7fffu, hi = (w[h] >> 16) & 0x7fffu;
+          const bool olo = (mb >> (2 * h)) & 1u, ohi = (mb >> (2 * h + 1)) & 1u;
+          mo = max(mo, olo ? lo : 0u);
+          mn = max(mn, olo ? 0u : lo);
+          mo = max(mo, ohi ? hi : 0u);
+          mn = max(mn, ohi ? 0u : hi);
+        }
+      }
+    }
+    for (int c = nv * 8 + tt; c < k; c += T) {  // k % 8 tail
+      const uint32_t v = srow[c] & 0x7fffu;
+      if ((omask[c >> 5] >> (c & 31)) & 1u) mo = max(mo, v);
+      else mn = max(mn, v);
     }
     mo = __reduce_max_sync(0xffffffffu, mo);
     mn = __reduce_max_sync(0xffffffffu, mn);
+    if (TW > 1) {
+      if (lane == 0) {
+        red[team][warp][0] = mo;
+        red[team][warp][1] = mn;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < TW; ++w) {
+        mo = max(mo, red[team][w][0]);
+        mn = max(mn, red[team][w][1]);
+      }
+    }
     const bool bad = mo >= 0x7f80u || mn >= 0x7f80u;
     ActScale so, sn;
     double so64, sn64;
@@ -1095,15 +1142,15 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
       so = sn;
       so64 = sn64;  // single-scale plan: outlier scale = normal scale (dual_scale.cpp:55)
     }
-    if (lane == 0) {
+    if (tt == 0) {
       if (J.so64) J.so64[row] = so64;
       if (J.sn64) J.sn64[row] = sn64;
       if (J.so32) J.so32[row] = so64 == DBL_MIN ? 0.f : __double2float_rn(so64);
       if (J.sn32) J.sn32[row] = sn64 == DBL_MIN ? 0.f : __double2float_rn(sn64);
     }
     int8_t* qr = J.wq + row * J.ldq;
-    // ---- pass 2: codes, four per lane per step
-    for (int c0 = lane * 4; c0 < k_pad; c0 += 128) {
+    // ---- pass 2: codes in plan order through the gather, four per lane per step
+    for (int c0 = tt * 4; c0 < k_pad; c0 += 4 * T) {
       const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
       const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu], srow[gp.y >> 16]};
       const bool outl = c0 < k_o;
@@ -1125,8 +1172,9 @@ __global__ void __launch_bounds__(32 * kWTeams, 4)
       }
       *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
     }
-    __syncwarp();
-    if (lane == 0 && row + 2 * step < J.n) load(j & 1, row + 2 * step);
+    if (TW > 1) __syncthreads();  // the slot (and red) is free once the whole team is done
+    else __syncwarp();
+    if (tt == 0 && row + 2 * step < J.n) load(j & 1, row + 2 * step);
   }
 }
 
@@ -2048,7 +2096,10 @@ int launch_prep_batched(const std::vector<WeightJobDev>& fast, int qmax, unsigne
                         cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] { attr = set_smem_attrs(prep_weights_batched_kernel, 200 * 1024); });
+  std::call_once(once, [] {
+    attr = set_smem_attrs(prep_weights_batched_kernel<1, kWTeams>, 200 * 1024);
+    if (attr == cudaSuccess) attr = set_smem_attrs(prep_weights_batched_kernel<8, 1>, 200 * 1024);
+  });
   QARVD_CUDA_TRY(attr);
   for (int group = 0; group < 2; ++group) {
     std::vector<WeightJobDev> sel;
@@ -2065,17 +2116,28 @@ int launch_prep_batched(const std::vector<WeightJobDev>& fast, int qmax, unsigne
     const size_t bytes = sel.size() * sizeof(WeightJobDev);
     QARVD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_jobs), bytes, s));
     QARVD_CUDA_TRY(cudaMemcpyAsync(d_jobs, sel.data(), bytes, cudaMemcpyHostToDevice, s));
-    const size_t smem = static_cast<size_t>(kWTeams) * 2 * ((g_k + 8 + 63) & ~int64_t(63)) * 2 + g_kp * 2;
+    // group 0: warp teams (kWTeams per CTA); group 1 (wide rows): one 8-warp team per CTA
+    const int teams = group == 0 ? kWTeams : 1, threads = group == 0 ? 32 * kWTeams : 256;
+    // row slots, the int16 gather (k_pad values of the widest job, as the kernel lays it out per
+    // job) and the outlier-column bitmask
+    size_t smem = static_cast<size_t>(teams) * 2 * ((g_k + 8 + 63) & ~int64_t(63)) * 2 + ((g_kp + 7) & ~int64_t(7)) * 2 +
+                  static_cast<size_t>((g_k + 31) / 32) * 4;
     if (smem > 200 * 1024) QARVD_FAIL(QARVD_ERR_LOGIC, "prepare_weights_batched: rows too wide");
     // enough CTAs per layer to fill the GPU a few times over, rows strided across teams
-    int64_t gx = (g_n + kWTeams - 1) / kWTeams;
+    int64_t gx = (g_n + teams - 1) / teams;
     const int64_t cap = (static_cast<int64_t>(kNumSMs) * 16 + static_cast<int64_t>(sel.size()) - 1) /
                         static_cast<int64_t>(sel.size());
     gx = gx < cap ? gx : (cap < 1 ? 1 : cap);
-    static const cudaError_t carve_prep = prefer_max_shared(prep_weights_batched_kernel);
+    static const cudaError_t carve_prep = prefer_max_shared(prep_weights_batched_kernel<1, kWTeams>) == cudaSuccess
+                                              ? prefer_max_shared(prep_weights_batched_kernel<8, 1>)
+                                              : cudaErrorInvalidValue;
     QARVD_CUDA_TRY(carve_prep);
-    prep_weights_batched_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(sel.size())),
-                                  32 * kWTeams, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
+    if (group == 0)
+      prep_weights_batched_kernel<1, kWTeams><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(sel.size())),
+                                                threads, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
+    else
+      prep_weights_batched_kernel<8, 1><<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(sel.size())),
+                                          threads, smem, s>>>(d_jobs, qmax, 1.0 / qmax, err);
     count_launch();
     QARVD_LAUNCH_CHECK();
     QARVD_CUDA_TRY(cudaFreeAsync(d_jobs, s));
