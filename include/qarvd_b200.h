@@ -450,6 +450,12 @@ int qarvd_zero_point_correct_f64(double* y, int64_t ldy, int64_t m, int64_t n, c
  * *bad (device int) is set to 1 when a code is outside [-128, 127]. */
 int qarvd_pack_codes_i8(const int32_t* in, int64_t rows, int64_t ld_in, const int32_t* idx, int64_t out_cols,
                         int8_t* out, int64_t ld_out, int* bad, void* stream);
+/* Packed 4-bit codes as the reference stores them (tensor.cpp:221-264, save_int_tensor /
+ * load_int_tensor: two per byte, low nibble first, over the flat [rows x k_src] tensor) ->
+ * int8 kernel layout on the device: out[r, c] = idx[c] >= 0 ? sext(nibble(r * k_src + idx[c])) : 0.
+ * The W4A8 weights travel and sit in HBM packed until this one expansion (QARQ loader). */
+int qarvd_unpack_codes_i4(const uint8_t* packed, int64_t rows, int64_t k_src, const int32_t* idx,
+                          int64_t out_cols, int8_t* out, int64_t ld_out, void* stream);
 /* out[i] = exp(in[i]) exactly as the reference's std::exp (glibc's algorithm restated, libm_ref.cuh). */
 int qarvd_exp_f64(const double* in, double* out, int64_t count, void* stream);
 /* LearnableQuantState soft / hard weights and hard codes (calibrate.cpp:138-183):

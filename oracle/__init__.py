@@ -97,6 +97,7 @@ def ref():
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
         _r.ref_calibrate_layer_bits.argtypes = list(_r.ref_calibrate_layer.argtypes) + [c_int, c_int]
         _r.ref_toy_qarq.argtypes = [ctypes.c_char_p, c_int, c_void_p]
+        _r.ref_toy_qarq_bits.argtypes = [ctypes.c_char_p, c_int, c_int, c_void_p]
         _r.ref_qarq_layer.argtypes = [ctypes.c_char_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p]
         _r.ref_weighted_loss.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
@@ -424,10 +425,11 @@ def ref_calibrate_layer(w64, outliers, act_scale, x64, row_off, chunks, chunk_w,
                 final_loss=sc[2], trace=tr[:iterations], init_scale_normal=isn, init_scale_outlier=iso)
 
 
-def ref_toy_qarq(path: str, iterations: int = 8) -> int:
-    """The reference's calibrated toy model saved as a QARQ file; returns the layer count."""
+def ref_toy_qarq(path: str, iterations: int = 8, weight_bits: int = 8) -> int:
+    """The reference's calibrated toy model saved as a QARQ file (weight_bits = 4: packed 4-bit
+    codes); returns the layer count."""
     n = ctypes.c_int64()
-    _rc(ref().ref_toy_qarq(path.encode(), iterations, ctypes.byref(n)))
+    _rc(ref().ref_toy_qarq_bits(path.encode(), iterations, weight_bits, ctypes.byref(n)))
     return n.value
 
 

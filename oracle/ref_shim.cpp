@@ -481,7 +481,13 @@ extern "C" int ref_calibrate_layer(const double* w, int64_t n, int64_t k, const 
 
 // The reference pipeline's own model file: ToyModel::build (two injections) -> calibrate_model
 // (heuristic_exp chunk weights, `iterations` AdaRound steps) -> save_quantized_model(path).
+extern "C" int ref_toy_qarq_bits(const char* path, int iterations, int weight_bits, int64_t* n_layers);
 extern "C" int ref_toy_qarq(const char* path, int iterations, int64_t* n_layers) {
+  return ref_toy_qarq_bits(path, iterations, 8, n_layers);
+}
+// the same pipeline at another weight bit width (CalibConfig::scheme, e.g. W4A8: the QARQ file
+// then holds packed 4-bit codes, tensor.cpp:221-264)
+extern "C" int ref_toy_qarq_bits(const char* path, int iterations, int weight_bits, int64_t* n_layers) {
   return guarded([&] {
     ToyModelConfig cfg;
     cfg.injections = {{"ffn.2", 0.05, 8.0}, {"self_attn.q", 0.03, 6.0}};
@@ -493,6 +499,7 @@ extern "C" int ref_toy_qarq(const char* path, int iterations, int64_t* n_layers)
     ModelCalibOptions opts;
     opts.base.iterations = iterations;
     opts.base.batch_size = 2;
+    opts.base.scheme.weight_bits = weight_bits;
     const ModelCalibResult r = calibrate_model(model, w, opts);
     save_quantized_model(path, r.qmodel);
     *n_layers = static_cast<int64_t>(r.qmodel.layers.size());

@@ -254,6 +254,7 @@ SIGNATURES = {
     "qarvd_zero_point_correct_f64": (
         c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int, ctypes.c_int32,
                 c_double, c_void_p, c_void_p, c_void_p]),
+    "qarvd_unpack_codes_i4": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p]),
     "qarvd_pack_codes_i8": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
     "qarvd_exp_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "qarvd_adaround_weights": (

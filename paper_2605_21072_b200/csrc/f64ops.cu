@@ -358,6 +358,27 @@ __global__ void pack_codes_kernel(const int32_t* __restrict__ in, int64_t rows, 
   }
 }
 
+// packed 4-bit codes (tensor.cpp:221-264 storage: two per byte, low nibble first, over the flat
+// [rows x k_src] tensor) -> int8 kernel layout through the column map
+__global__ void unpack_i4_kernel(const uint8_t* __restrict__ packed, int64_t rows, int64_t k_src,
+                                 const int32_t* __restrict__ idx, int64_t cols, int8_t* __restrict__ out,
+                                 int64_t ld_out) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const int32_t src = idx[c];
+    int8_t v = 0;
+    if (src >= 0) {
+      const int64_t f = r * k_src + src;
+      const uint8_t b = packed[f >> 1];
+      const uint8_t nib = (f & 1) ? (b >> 4) : (b & 0x0fu);
+      v = static_cast<int8_t>(static_cast<int8_t>(nib << 4) >> 4);  // sign-extend
+    }
+    out[r * ld_out + c] = v;
+  }
+}
+
 __global__ void cr_exp_kernel(const double* in, double* out, int64_t count) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -632,6 +653,21 @@ int qarvd_pack_codes_i8(const int32_t* in, int64_t rows, int64_t ld_in, const in
   if (rows == 0 || out_cols == 0) return QARVD_OK;
   pack_codes_kernel<<<grid_for(rows * out_cols, 4), kT, 0, as_stream(stream)>>>(in, rows, ld_in, idx, out_cols,
                                                                                 out, ld_out, bad);
+  count_launch();
+  QARVD_LAUNCH_CHECK();
+  return QARVD_OK;
+}
+
+int qarvd_unpack_codes_i4(const uint8_t* packed, int64_t rows, int64_t k_src, const int32_t* idx,
+                          int64_t out_cols, int8_t* out, int64_t ld_out, void* stream) {
+  clear_error();
+  if (rows < 0 || k_src < 0 || out_cols < 0 || ld_out < out_cols || (rows * out_cols > 0 && (!idx || !out)) ||
+      (rows * k_src > 0 && !packed))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "qarvd_unpack_codes_i4: invalid argument");
+  if (int st = require_device()) return st;
+  if (rows == 0 || out_cols == 0) return QARVD_OK;
+  unpack_i4_kernel<<<grid_for(rows * out_cols, 4), kT, 0, as_stream(stream)>>>(packed, rows, k_src, idx, out_cols,
+                                                                               out, ld_out);
   count_launch();
   QARVD_LAUNCH_CHECK();
   return QARVD_OK;

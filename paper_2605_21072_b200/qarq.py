@@ -41,6 +41,7 @@ class QarqLayer:
     act_scale: float = 0.0
     act_zero: int = 0
     fp_weight_bf16: Optional[np.ndarray] = None  # uint16 bits [out x in] (preserved layers)
+    codes_packed: Optional[np.ndarray] = None    # 4-bit layers: the file's packed bytes (uint8)
 
 
 def _read_qtns_int(buf: memoryview, pos: int):
@@ -63,10 +64,12 @@ def _read_qtns_int(buf: memoryview, pos: int):
         nib = np.empty(2 * nbytes, dtype=np.int8)
         nib[0::2], nib[1::2] = lo, hi
         codes = ((nib << 4).astype(np.int8) >> 4)[:count]  # sign-extend the nibbles
+        packed = raw.copy()
     else:
         nbytes = count
         codes = np.frombuffer(buf, dtype=np.int8, count=count, offset=pos).copy()
-    return codes.reshape(shape), bits, pos + nbytes
+        packed = None
+    return codes.reshape(shape), bits, pos + nbytes, packed
 
 
 def load_qarq(path: str):
@@ -91,12 +94,12 @@ def load_qarq(path: str):
             pos += 2 * n * k
             layers.append(L)
             continue
-        codes, bits, pos = _read_qtns_int(buf, pos)
+        codes, bits, pos, packed = _read_qtns_int(buf, pos)
         if codes.shape != (n, k):
             raise _lib.QarvdError(f"quantized model: weight shape mismatch for {L.name}")
         if bits != int(lj["weight_bits"]):
             raise _lib.QarvdError(f"quantized model: bit-width mismatch for {L.name}")
-        L.codes, L.bits = codes, bits
+        L.codes, L.bits, L.codes_packed = codes, bits, packed
         L.scale_normal = np.frombuffer(buf, dtype="<f4", count=n, offset=pos).copy()
         pos += 4 * n
         dual = bool(lj["dual_scale"])
@@ -127,13 +130,25 @@ def to_device(L: QarqLayer, device="cuda") -> engine.QuantizedLayer:
     if L.permutation is not None and not np.array_equal(plan.permutation, L.permutation):
         raise _lib.QarvdError(f"quantized model: permutation of {L.name} is not [outliers | normals] sorted")
     n_o = len(outl)
-    wq = np.zeros((L.out_dim, plan.k_pad), dtype=np.int8)
-    wq[:, :n_o] = L.codes[:, :n_o]
-    wq[:, plan.k_outlier:plan.k_outlier + (L.in_dim - n_o)] = L.codes[:, n_o:]
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
+    if L.codes_packed is not None:
+        # 4-bit layers: the packed bytes go to the device as stored (half the bytes of int8) and
+        # one kernel expands them into the K2 layout (qarvd_unpack_codes_i4)
+        idx = np.full(plan.k_pad, -1, dtype=np.int32)
+        idx[:n_o] = np.arange(n_o, dtype=np.int32)
+        idx[plan.k_outlier:plan.k_outlier + (L.in_dim - n_o)] = np.arange(n_o, L.in_dim, dtype=np.int32)
+        wq_dev = torch.empty((L.out_dim, plan.k_pad), dtype=torch.int8, device=device)
+        packed_dev, idx_dev = t(L.codes_packed, torch.uint8), t(idx, torch.int32)
+        _lib.call("qarvd_unpack_codes_i4", packed_dev.data_ptr(), L.out_dim, L.in_dim, idx_dev.data_ptr(),
+                  plan.k_pad, wq_dev.data_ptr(), plan.k_pad, torch.cuda.current_stream().cuda_stream)
+    else:
+        wq = np.zeros((L.out_dim, plan.k_pad), dtype=np.int8)
+        wq[:, :n_o] = L.codes[:, :n_o]
+        wq[:, plan.k_outlier:plan.k_outlier + (L.in_dim - n_o)] = L.codes[:, n_o:]
+        wq_dev = t(wq, torch.int8)
     sn = L.scale_normal.astype(np.float64)
     so = L.scale_outlier.astype(np.float64) if L.scale_outlier is not None else sn
-    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)
-    layer = engine.QuantizedLayer(L.name, L.out_dim, L.in_dim, plan, t(wq, torch.int8), t(so, torch.float64),
+    layer = engine.QuantizedLayer(L.name, L.out_dim, L.in_dim, plan, wq_dev, t(so, torch.float64),
                                   t(sn, torch.float64), t(so.astype(np.float32), torch.float32),
                                   t(sn.astype(np.float32), torch.float32), t(plan.gather, torch.int32),
                                   _lib.ACT_PER_TENSOR, float(np.float32(L.act_scale)))

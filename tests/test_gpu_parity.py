@@ -1077,13 +1077,16 @@ def test_calibrate_layer_zero_iterations_and_large_batch(cuda, ref_lib):
             assert res.final_loss == res.initial_loss
 
 
-def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path):
+@pytest.mark.parametrize("wbits", [8, 4])
+def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path, wbits):
     """A QARQ file written by the reference pipeline, loaded by qarq.load_qarq and uploaded by
     qarq.to_device: K1 codes bit-exact vs the reference quantize with the file's static act
-    scale, and the bf16 K2 output within the stated tolerance of kernel_b_gemm_dequant."""
+    scale, and the bf16 K2 output within the stated tolerance of kernel_b_gemm_dequant.  At
+    W4 the file holds packed 4-bit codes, uploaded packed and expanded on the device
+    (qarvd_unpack_codes_i4): the device codes equal the reference loader's exactly."""
     from paper_2605_21072_b200 import qarq
     path = str(tmp_path / "toy.qarq")
-    oracle.ref_toy_qarq(path, iterations=4)
+    oracle.ref_toy_qarq(path, iterations=4, weight_bits=wbits)
     _, layers = qarq.load_qarq(path)
     checked = 0
     for i, L in enumerate(layers):
@@ -1092,7 +1095,13 @@ def test_qarq_loaded_layers_run_on_device(cuda, ref_lib, tmp_path):
                 qarq.to_device(L)
             continue
         ref = oracle.ref_qarq_layer(path, i)
+        assert L.bits == wbits and (L.codes_packed is not None) == (wbits == 4)
         D = qarq.to_device(L)
+        n_o = ref["outlier_count"]
+        wq_dev = D.wq.cpu().numpy().astype(np.int32)
+        np.testing.assert_array_equal(wq_dev[:, :n_o], ref["wq"][:, :n_o])
+        np.testing.assert_array_equal(wq_dev[:, D.k_outlier:D.k_outlier + L.in_dim - n_o], ref["wq"][:, n_o:])
+        assert not wq_dev[:, n_o:D.k_outlier].any() and not wq_dev[:, D.k_outlier + L.in_dim - n_o:].any()
         xb, x64 = bf16_values((37, L.in_dim), seed=i, gamma=3.0)
         xq, s32, s64 = engine.kernel_a_quantize_activation(to_dev_bf16(xb), D, qb.ACT_PER_TENSOR,
                                                            static_scale=ref["act_scale"])
