@@ -329,6 +329,24 @@ int qarvd_linear_chain_forward_host(const qarvd_linear_t* layers, int num_layers
     crow = (crow + 127) / 128 * 128;
     for (int c = 0; c < nchunks; ++c) bounds[c + 1] = (c + 1) * crow < m ? (c + 1) * crow : m;
   }
+  // QARVD_HOST_CHUNK_ROWS="r0,r1,...": explicit leading chunk sizes (the rest is the last chunk),
+  // for A/B.  Measured (round 2): small first / last chunks do not beat the equal split --
+  // 384,1024x3 620 us, 256,768,1024x3 568, 256,512,1024x3,512 484, 6 equal 473, default 452.
+  if (const char* env = getenv("QARVD_HOST_CHUNK_ROWS")) {
+    int c = 0;
+    int64_t acc = 0;
+    const char* p = env;
+    while (*p && c < 7) {
+      const int64_t r = atoll(p);
+      if (r <= 0 || acc + r >= m) break;
+      acc += r;
+      bounds[++c] = acc;
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    bounds[++c] = m;
+    nchunks = c;
+  }
   cudaError_t e = cudaSuccess;
   if (!L0->s_in) {
     e = cudaStreamCreateWithFlags(&L0->s_in, cudaStreamNonBlocking);

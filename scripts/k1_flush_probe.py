@@ -31,14 +31,15 @@ def timeit(fn, mode, reps=30):
     return float(np.median(ts))
 
 
-for name, k, n in (("x (1536, gathered)", 1536, 1536), ("U (8960, plan order)", 8960, 1536)):
+for name, k, n in (("x (1536, gathered)", 1536, 1536), ("x (1536, plan order)", 1536, 1537),
+                    ("U (8960, plan order)", 8960, 1536)):
     spec = synth.LayerSpec(7, "l", n, k, M, 0.021, 8.0)
     w = synth.synth_weight(spec, seed=1)
     L = engine.prepare_weights("l", w, engine.build_plan("l", k, qb.analyze_layer("l", w).aligned_outliers))
     x = synth.synth_activation(M, k, seed=3)
     xq = torch.empty((M, L.k_pad), dtype=torch.int8, device="cuda")
     sx = torch.empty(M, dtype=torch.float32, device="cuda")
-    g = L.gather_dev if k == 1536 else None
+    g = L.gather_dev if n == 1536 and k == 1536 else None
     kout = L.k_pad if g is not None else k
     st = torch.cuda.current_stream().cuda_stream
     f = lambda: qb._lib.call("qarvd_quantize_act", x.data_ptr(), qb.BF16, M, k, k, None if g is None else g.data_ptr(),
