@@ -15,8 +15,11 @@
 // column sums sequentially over the rows, exactly the reference order, with 8 rows of
 // loads (kNormRows) in flight before they are added in order.
 // For bf16/f32 inputs w*w is exact in f64, so the sum is the only rounding.
-// Kernel 2 (tiny): one 1024-thread CTA per layer sorts the K norms (bitonic,
-// shared memory) for the medians and runs the selection / alignment.
+// Kernel 2 (tiny): one 1024-thread CTA per layer takes the medians and the alignment pivot by
+// exact radix selection over the norms' bit patterns (no sort) and runs the selection /
+// alignment.  The norm jobs run longest columns first (their sequential sums are the
+// kernel's critical path) with 32 rows of loads in flight on columns of >= 4096 rows.
+#include <algorithm>
 #include <climits>
 #include <vector>
 
@@ -97,6 +100,20 @@ __global__ void __launch_bounds__(kNormThreads)
     if (pair) {
       const T* base = w + c0;
       int64_t i = 0;
+      if (job.n >= 4096) {  // long chains: 4x the loads in flight (the chain is latency-bound)
+        for (; i + 4 * kNormRows <= job.n; i += 4 * kNormRows) {
+          PV d[4 * kNormRows];
+#pragma unroll
+          for (int u = 0; u < 4 * kNormRows; ++u) d[u] = __ldg(reinterpret_cast<const PV*>(base + (i + u) * job.ldw));
+#pragma unroll
+          for (int u = 0; u < 4 * kNormRows; ++u) {
+            T e0, e1;
+            Pair<T>::split(d[u], e0, e1);
+            a0 = __dadd_rn(a0, sq<T>(e0));
+            a1 = __dadd_rn(a1, sq<T>(e1));
+          }
+        }
+      }
       for (; i + kNormRows <= job.n; i += kNormRows) {
         PV d[kNormRows];
 #pragma unroll
@@ -129,30 +146,68 @@ __global__ void __launch_bounds__(kNormThreads)
 }
 
 // ---- selection -------------------------------------------------------------
-__device__ __forceinline__ void bitonic_sort_u64(unsigned long long* s, int P) {
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool asc = ((lo & size) == 0);
-        const unsigned long long a = s[lo], b = s[hi];
-        if ((a > b) == asc) {
-          s[lo] = b;
-          s[hi] = a;
-        }
-      }
-      __syncthreads();
+// The r-th smallest (0-based) of k keys key(i) (order-preserving u64 images of non-negative
+// doubles): MSB-first radix select, 8 bits per pass, a 256-bin shared histogram of the keys
+// that match the prefix so far, one warp scans it.  Exact, no sort (the previous bitonic sorts
+// of P = 2048 / 16384 keys took ~25 / 60 us per layer).
+template <typename KeyFn>
+__device__ unsigned long long radix_select(int k, KeyFn key, unsigned long long r, uint32_t* hist,
+                                           unsigned long long* s_pick) {
+  unsigned long long prefix = 0, mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const unsigned long long x = key(i);
+      if ((x & mask) == prefix) atomicAdd(&hist[(x >> shift) & 0xffu], 1u);
     }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[lane * 8 + j];
+        tot += c[j];
+      }
+      uint32_t incl = tot;  // inclusive prefix over lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      unsigned long long before = incl - tot;
+      const bool mine = before <= r && r < before + tot;
+      if (mine) {
+        int b = lane * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (before + c[j] > r) break;
+          before += c[j];
+          ++b;
+        }
+        s_pick[0] = static_cast<unsigned long long>(b);
+        s_pick[1] = before;
+      }
+    }
+    __syncthreads();
+    const unsigned long long b = s_pick[0], before = s_pick[1];
+    __syncthreads();
+    prefix |= b << shift;
+    mask |= 0xffull << shift;
+    r -= before;
   }
+  return prefix;
 }
 
-// sorted_median (outlier.cpp:13-18) over an ascending array of non-negative doubles
-__device__ __forceinline__ double median_sorted(const unsigned long long* s, int n) {
-  if (n & 1) return __longlong_as_double(static_cast<long long>(s[n / 2]));
-  const double a = __longlong_as_double(static_cast<long long>(s[n / 2 - 1]));
-  const double b = __longlong_as_double(static_cast<long long>(s[n / 2]));
-  return __dmul_rn(0.5, __dadd_rn(a, b));
+// sorted_median (outlier.cpp:13-18) of k keys via selection
+template <typename KeyFn>
+__device__ double median_select(int k, KeyFn key, uint32_t* hist, unsigned long long* s_pick) {
+  const unsigned long long hi = radix_select(k, key, static_cast<unsigned long long>(k / 2), hist, s_pick);
+  if (k & 1) return __longlong_as_double(static_cast<long long>(hi));
+  const unsigned long long lo = radix_select(k, key, static_cast<unsigned long long>(k / 2 - 1), hist, s_pick);
+  return __dmul_rn(0.5, __dadd_rn(__longlong_as_double(static_cast<long long>(lo)),
+                                  __longlong_as_double(static_cast<long long>(hi))));
 }
 
 // block-wide ordered compaction: writes indices i (ascending) with pred(i) true
@@ -190,32 +245,32 @@ struct SelJobDev {
 __global__ void __launch_bounds__(kSelThreads)
     select_outliers_kernel(const SelJobDev* __restrict__ jobs, double tau, double alpha_min,
                            int64_t align) {
-  extern __shared__ unsigned long long sbuf[];
+  extern __shared__ unsigned long long sbuf[];  // scratch: the norms' keys, then int32 indices
   __shared__ int warp_tot[32];
   __shared__ double s_val[4];
+  __shared__ uint32_t s_hist[256];
+  __shared__ unsigned long long s_pick[2];
   const SelJobDev job = jobs[blockIdx.x];
   const int k = static_cast<int>(job.k);
-  int P = 1;
-  while (P < k) P <<= 1;
   const double* v = job.norms;
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    sbuf[i] = static_cast<unsigned long long>(__double_as_longlong(v[i]));
+  __syncthreads();
+  const unsigned long long* keys = sbuf;
 
-  // median of norms
-  for (int i = threadIdx.x; i < P; i += blockDim.x)
-    sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(v[i])) : ~0ull;
-  __syncthreads();
-  bitonic_sort_u64(sbuf, P);
-  if (threadIdx.x == 0) s_val[0] = median_sorted(sbuf, k);
-  __syncthreads();
-  const double med = s_val[0];
+  // median of norms (norms are non-negative: their bit patterns order like the values)
+  const double med = median_select(k, [&](int i) { return keys[i]; }, s_hist, s_pick);
 
   // MAD = median |v - med|   (outlier.cpp:35-36)
-  for (int i = threadIdx.x; i < P; i += blockDim.x)
-    sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(v[i], med))))
-                    : ~0ull;
-  __syncthreads();
-  bitonic_sort_u64(sbuf, P);
+  const double mad_sel = median_select(
+      k,
+      [&](int i) {
+        return static_cast<unsigned long long>(
+            __double_as_longlong(fabs(__dsub_rn(__longlong_as_double(static_cast<long long>(keys[i])), med))));
+      },
+      s_hist, s_pick);
   if (threadIdx.x == 0) {
-    const double mad = median_sorted(sbuf, k);
+    const double mad = mad_sel;
     const double zc = __ddiv_rn(tau, 0.6745);  // kModifiedZScoreFactor (outlier.hpp:13)
     const double a = __dadd_rn(med, __dmul_rn(zc, mad));
     const double b = __dmul_rn(alpha_min, med);
@@ -247,29 +302,26 @@ __global__ void __launch_bounds__(kSelThreads)
     A = R;
   } else {
     // the `target` largest norms, ties -> lower index: pivot value = target-th largest
-    for (int i = threadIdx.x; i < P; i += blockDim.x)
-      sbuf[i] = i < k ? static_cast<unsigned long long>(__double_as_longlong(v[i])) : ~0ull;
-    __syncthreads();
-    bitonic_sort_u64(sbuf, P);
-    const unsigned long long pivot = sbuf[k - target];
-    __syncthreads();
+    const unsigned long long pivot = radix_select(
+        k, [&](int i) { return keys[i]; }, static_cast<unsigned long long>(k - target), s_hist, s_pick);
     // count strictly greater, then take equal ones in index order
     const double pv = __longlong_as_double(static_cast<long long>(pivot));
-    // number of values > pivot = k - (index of first element > pivot in sorted order)
+    int greater = 0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) greater += keys[i] > pivot ? 1 : 0;
+    greater = __reduce_add_sync(0xffffffffu, greater);
+    if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = greater;
+    __syncthreads();
     if (threadIdx.x == 0) {
-      int lo = k - static_cast<int>(target), hi = k;  // first index with value > pivot in [lo, k]
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sbuf[mid] > pivot) hi = mid;
-        else lo = mid + 1;
-      }
-      warp_tot[0] = static_cast<int>(target) - (k - lo);  // equal ones to take
+      int g = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) g += warp_tot[w];
+      warp_tot[0] = static_cast<int>(target) - g;  // equal ones to take
     }
     __syncthreads();
     const int need_eq = warp_tot[0];
     __syncthreads();
-    // rank of each equal element among equals (index order) via compaction into sbuf scratch
-    int32_t* eq_idx = reinterpret_cast<int32_t*>(sbuf);
+    // rank of each equal element among equals (index order) via compaction into scratch after
+    // the keys (k u64 keys, then k int32 indices)
+    int32_t* eq_idx = reinterpret_cast<int32_t*>(sbuf + k);
     const int n_eq = compact_indices(k, [&](int i) { return v[i] == pv; }, eq_idx, warp_tot);
     (void)n_eq;
     // mark: greater, or one of the first need_eq equals
@@ -328,10 +380,17 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
       QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "analyze_layers: invalid job " + std::to_string(i));
     if (J.k > kMaxSelK)
       QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "analyze_layers: d_in above 16384 is not supported");
-    nj[i] = NormJobDev{J.w, J.n, J.k, J.ldw, J.norms, (J.k + kNormCols - 1) / kNormCols, groups};
-    groups += (J.k + kNormCols - 1) / kNormCols;
+    nj[i] = NormJobDev{J.w, J.n, J.k, J.ldw, J.norms, (J.k + kNormCols - 1) / kNormCols, 0};
     sj[i] = SelJobDev{J.k, J.norms, J.stats, J.counts, J.raw_idx, J.aligned_idx};
     if (J.k > max_k) max_k = J.k;
+  }
+  // the longest column chains (most rows) first: their sequential sums set the kernel's
+  // critical path (e.g. the 8960-row FFN-up layers), so they start in the first wave and the
+  // short columns fill in around them (order of the norm jobs does not change any result)
+  std::stable_sort(nj.begin(), nj.end(), [](const NormJobDev& a, const NormJobDev& b) { return a.n > b.n; });
+  for (int i = 0; i < num_jobs; ++i) {
+    nj[i].group_begin = groups;
+    groups += nj[i].col_groups;
   }
   if (int st = require_device()) return st;
   cudaStream_t s = as_stream(stream);
@@ -361,10 +420,8 @@ extern "C" int qarvd_analyze_layers(const qarvd_outlier_job* jobs, int num_jobs,
     column_norms_kernel<double><<<grid, kNormThreads, 0, s>>>(d_nj, num_jobs, groups);
   count_launch();
   QARVD_LAUNCH_CHECK();
-  int P = 1;
-  while (P < max_k) P <<= 1;
-  const size_t smem = static_cast<size_t>(P) * sizeof(unsigned long long);
-  QARVD_CUDA_TRY(set_smem_attrs(select_outliers_kernel, kMaxSelK * static_cast<int>(sizeof(unsigned long long))));
+  const size_t smem = static_cast<size_t>(max_k) * (sizeof(unsigned long long) + sizeof(int32_t));
+  QARVD_CUDA_TRY(set_smem_attrs(select_outliers_kernel, kMaxSelK * static_cast<int>(sizeof(unsigned long long) + sizeof(int32_t))));
   select_outliers_kernel<<<num_jobs, kSelThreads, smem, s>>>(d_sj, tau, alpha_min, align);
   count_launch();
   QARVD_LAUNCH_CHECK();
