@@ -1,0 +1,252 @@
+// K1 structure microbenchmark (not product code): per-token int8 quantization of M x 1536 bf16
+// rows, one warp per row, variants of the rows per warp and of the grid; tie repair omitted (the
+// point is the memory / latency structure).  nvcc -gencode arch=compute_100a,code=sm_100a -O3
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+__device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t q8(uint32_t w, float r) {
+  const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xffff0000u);
+  const int a = __float2int_rn(lo * r), b = __float2int_rn(hi * r);
+  return (static_cast<uint32_t>(a) & 0xffu) | ((static_cast<uint32_t>(b) & 0xffu) << 8);
+}
+// exact repair of a flagged chunk (f64 division per value), out of line like the product's
+__device__ __noinline__ uint2 fix8(uint4 d, double s64) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const uint32_t bits = h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16);
+    c[h] = static_cast<uint32_t>(static_cast<int>(rint(__ddiv_rn(static_cast<double>(__uint_as_float(bits)), s64)))) & 0xffu;
+  }
+  return make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
+}
+// inline variant: the value near a tie decided by one f64 fma against the half-integer
+// boundary (no division): r = v - hc*s64 exactly in sign
+__device__ __forceinline__ uint2 fix8_fma(uint4 d, float rr, double s64) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+    const float t = v * rr;
+    const float lower = floorf(t);
+    const double hc = static_cast<double>(lower) + 0.5;
+    const double r = fma(-hc, s64, static_cast<double>(v));
+    const int lo = static_cast<int>(lower);
+    const int code = r > 0.0 ? lo + 1 : (r < 0.0 ? lo : ((lo & 1) ? lo + 1 : lo));
+    c[h] = static_cast<uint32_t>(code) & 0xffu;
+  }
+  return make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
+}
+__device__ __noinline__ uint2 fix8_fma_ool(uint4 d, float rr, double s64) { return fix8_fma(d, rr, s64); }
+__device__ __noinline__ uint2 fix8_f32_ool(uint4 d, float rr) {  // fp32-only work of similar size
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+    const float t = v * rr;
+    const float lower = floorf(t);
+    const float r = fmaf(-(lower + 0.5f), 1.0f / rr, v);
+    const int lo = static_cast<int>(lower);
+    c[h] = static_cast<uint32_t>(r > 0.f ? lo + 1 : (r < 0.f ? lo : ((lo & 1) ? lo + 1 : lo))) & 0xffu;
+  }
+  return make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
+}
+// FEAT bit 0: exact f64 scale (fma correction) + s64 store; bit 1: tie detection + out-of-line fix
+// bit 2: the fix inline with the fma decision instead
+template <int V, int FEAT>
+__global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m, int8_t* __restrict__ q,
+                                           float* __restrict__ s, double* __restrict__ s64o) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= m) return;
+  uint4 d[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) d[i] = ldg_nc(reinterpret_cast<const uint4*>(x + (int64_t)row * (V * 256)) + lane + 32 * i);
+  uint32_t mx = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+    mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[i].x & 0x7fff7fffu, d[i].y & 0x7fff7fffu),
+                               __vmaxu2(d[i].z & 0x7fff7fffu, d[i].w & 0x7fff7fffu)));
+  const uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+  const float amax = __uint_as_float(mag << 16);
+  const float rr = amax > 0.f ? __fmul_rn(__frcp_rn(amax), 127.f) : 0.f;
+  double s64 = 1.0;
+  if (FEAT & 1) {
+    const double a = amax, y = a * (1.0 / 127.0);
+    s64 = fma(fma(-y, 127.0, a), 1.0 / 127.0, y);
+    if (lane == 31) { s[row] = __double2float_rn(s64); s64o[row] = s64; }
+  } else if (lane == 0) s[row] = amax / 127.f;
+  int8_t* qr = q + (int64_t)row * (V * 256);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
+    uint32_t c[8];
+    float dmax = 0.f;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+      const float t = v * rr;
+      const float y = t + 12582912.0f;
+      c[h] = __float_as_uint(y) & 0xffu;
+      dmax = fmaxf(dmax, fabsf(t - (y - 12582912.0f)));
+    }
+    if (FEAT & 64) {  // per-value inline exact decision of the values within the guard
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+        const float t = v * rr;
+        const float fr = t - floorf(t);
+        if (fabsf(fr - 0.5f) < 3e-5f) {
+          const float lower = floorf(t);
+          const double r = fma(-(static_cast<double>(lower) + 0.5), s64, static_cast<double>(v));
+          const int lo = static_cast<int>(lower);
+          c[h] = static_cast<uint32_t>(r > 0.0 ? lo + 1 : (r < 0.0 ? lo : ((lo & 1) ? lo + 1 : lo))) & 0xffu;
+        }
+      }
+    }
+    uint2 out = make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
+    if ((FEAT & 2) && dmax > 0.49997f) out = fix8(d[i], s64);
+    if ((FEAT & 4) && dmax > 0.49997f) out = fix8_fma(d[i], rr, s64);
+    if ((FEAT & 128) && dmax > 0.49997f) out = fix8_fma_ool(d[i], rr, s64);
+    if ((FEAT & 256) && dmax > 0.49997f) out = fix8_f32_ool(d[i], rr);
+    if (FEAT & 8) out.x ^= dmax > 0.49997f ? 1u : 0u;  // dmax kept, no branch
+    if ((FEAT & 16) && dmax > 0.49997f) out.x ^= 1u;   // trivial branch
+    if ((FEAT & 32) && dmax > 0.4999999f) out = fix8(d[i], s64);  // tight guard (count test)
+    *reinterpret_cast<uint2*>(qr + (lane + 32 * i) * 8) = out;
+  }
+}
+__device__ unsigned int g_flag_count;
+template <int V>
+__global__ void countflags(const uint16_t* __restrict__ x, int m, float guard) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= m) return;
+  uint4 d[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) d[i] = ldg_nc(reinterpret_cast<const uint4*>(x + (int64_t)row * (V * 256)) + lane + 32 * i);
+  uint32_t mx = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+    mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[i].x & 0x7fff7fffu, d[i].y & 0x7fff7fffu),
+                               __vmaxu2(d[i].z & 0x7fff7fffu, d[i].w & 0x7fff7fffu)));
+  const uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+  const float amax = __uint_as_float(mag << 16);
+  const float rr = amax > 0.f ? __fmul_rn(__frcp_rn(amax), 127.f) : 0.f;
+  unsigned int n = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
+    float dmax = 0.f;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+      const float t = v * rr;
+      const float y = t + 12582912.0f;
+      dmax = fmaxf(dmax, fabsf(t - (y - 12582912.0f)));
+    }
+    n += dmax > guard;
+  }
+  atomicAdd(&g_flag_count, n);
+}
+template <int V, int R>  // V uint4 per lane per row, R rows per warp
+__global__ void __launch_bounds__(256) k1v(const uint16_t* __restrict__ x, int m, int8_t* __restrict__ q,
+                                           float* __restrict__ s, int rows_per_grid_step) {
+  const int lane = threadIdx.x & 31;
+  const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int base = warp_g * R; base < m; base += nw * R) {
+    uint4 d[R][V];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (base + r < m) d[r][i] = ldg_nc(reinterpret_cast<const uint4*>(x + (int64_t)(base + r) * (V * 256)) + lane + 32 * i);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (base + r >= m) break;
+      uint32_t mx = 0;
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[r][i].x & 0x7fff7fffu, d[r][i].y & 0x7fff7fffu),
+                                   __vmaxu2(d[r][i].z & 0x7fff7fffu, d[r][i].w & 0x7fff7fffu)));
+      const uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
+      const float amax = __uint_as_float(mag << 16);
+      const float rr = amax > 0.f ? 127.f / amax : 0.f;
+      if (lane == 0) s[base + r] = amax / 127.f;
+      int8_t* qr = q + (int64_t)(base + r) * (V * 256);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const uint32_t a = q8(d[r][i].x, rr), b = q8(d[r][i].y, rr), c = q8(d[r][i].z, rr), e = q8(d[r][i].w, rr);
+        *reinterpret_cast<uint2*>(qr + (lane + 32 * i) * 8) = make_uint2(a | (b << 16), c | (e << 16));
+      }
+    }
+  }
+}
+__global__ void copyk(const uint4* __restrict__ a, uint4* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+int main(int argc, char** argv) {
+  const int m = 4680, k = 1536;
+  uint16_t* x; int8_t* q; float* s; uint8_t* fl; uint4* y;
+  cudaMalloc(&x, (size_t)m * k * 2); cudaMalloc(&q, (size_t)m * k); cudaMalloc(&s, m * 4);
+  cudaMalloc(&fl, 256 << 20); cudaMalloc(&y, (size_t)m * k * 2);
+  std::vector<uint16_t> h((size_t)m * k);
+  uint32_t st = 1;
+  for (auto& v : h) { st = st * 1664525u + 1013904223u; v = 0x3c00 + (st >> 20) % 0x600; if (st & 1) v |= 0x8000; }
+  if (argc > 1) {  // real activations (bf16 bits, m x k) from a file
+    FILE* f = fopen(argv[1], "rb");
+    if (f) { size_t got = fread(h.data(), 2, h.size(), f); fclose(f); printf("loaded %zu values from %s\n", got, argv[1]); }
+  }
+  cudaMemcpy(x, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  auto timeit = [&](const char* name, auto fn) {
+    float best = 1e9, sum = 0;
+    for (int it = 0; it < 30; ++it) {
+      cudaMemset(fl, it, 256 << 20);
+      cudaEventRecord(a); fn(); cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b); best = ms < best ? ms : best; if (it >= 5) sum += ms;
+    }
+    printf("%-40s best %6.1f us  mean %6.1f us\n", name, best * 1e3, sum / 25 * 1e3);
+  };
+  timeit("copy (2x bytes)", [&] { copyk<<<148 * 8, 256>>>(reinterpret_cast<uint4*>(x), y, (int64_t)m * k / 8); });
+  timeit("1 row/warp, 1 wave (585 CTAs)", [&] { k1v<6, 1><<<(m + 7) / 8, 256>>>(x, m, q, s, 0); });
+  timeit("2 rows/warp (293 CTAs)", [&] { k1v<6, 2><<<(m + 15) / 16, 256>>>(x, m, q, s, 0); });
+  timeit("1 row/warp, persistent 148x4", [&] { k1v<6, 1><<<148 * 4, 256>>>(x, m, q, s, 0); });
+  timeit("1 row/warp, persistent 148x2", [&] { k1v<6, 1><<<148 * 2, 256>>>(x, m, q, s, 0); });
+  timeit("2 rows/warp, persistent 148x2", [&] { k1v<6, 2><<<148 * 2, 256>>>(x, m, q, s, 0); });
+  timeit("1 row/warp, 128-thread CTAs (1170)", [&] { k1v<6, 1><<<(m + 3) / 4, 128>>>(x, m, q, s, 0); });
+  timeit("1 row/warp, 64-thread CTAs (2340)", [&] { k1v<6, 1><<<(m + 1) / 2, 64>>>(x, m, q, s, 0); });
+  double* s64o; cudaMalloc(&s64o, m * 8);
+  timeit("feat 0 (magic rounding)", [&] { k1f<6, 0><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 1 (+ exact f64 scale, s64 store)", [&] { k1f<6, 1><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 2 (+ tie detect, out-of-line fix)", [&] { k1f<6, 2><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 3 (both)", [&] { k1f<6, 3><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 5 (scale + inline fma tie fix)", [&] { k1f<6, 5><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 9 (dmax, no branch)", [&] { k1f<6, 9><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 17 (dmax, trivial branch)", [&] { k1f<6, 17><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 33 (out-of-line fix, guard 1e-7)", [&] { k1f<6, 33><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 65 (per-value inline fma decision)", [&] { k1f<6, 65><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 129 (out-of-line fma fix)", [&] { k1f<6, 129><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 257 (out-of-line fp32-only fix)", [&] { k1f<6, 257><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 1 again", [&] { k1f<6, 1><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  timeit("feat 3 again", [&] { k1f<6, 3><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  for (float gd : {0.49997f, 0.4999999f}) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(g_flag_count, &z, 4);
+    countflags<6><<<(m + 7) / 8, 256>>>(x, m, gd);
+    cudaMemcpyFromSymbol(&z, g_flag_count, 4);
+    printf("guard %.7f: %u flagged lane-chunks of %d\n", gd, z, m * 32 * 6);
+  }
+  cudaDeviceSynchronize();
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+}
