@@ -705,7 +705,9 @@ extern "C" int qarvd_calibrate_layer(const double* w, int64_t n, int64_t k, cons
   const int64_t cap_rows = G * max_rows;
   double* d = A.get<double>(cap_rows * n);
   // per-iteration products on the int8 tensor cores (QARVD_K7_OZAKI=0: cuBLAS DGEMM, A/B)
-  const bool ozaki = !(getenv("QARVD_K7_OZAKI") && getenv("QARVD_K7_OZAKI")[0] == '0');
+  // the slice products stack kOzSlices = 8 digit rows per output row: K2 needs 8n % 16 == 0, so
+  // an odd out_dim takes the DGEMM path
+  const bool ozaki = !(getenv("QARVD_K7_OZAKI") && getenv("QARVD_K7_OZAKI")[0] == '0') && (n % 2 == 0);
   double* xhat = ozaki ? nullptr : A.get<double>(cap_rows * k);
   // K2 layout of the plan: [outlier columns | pad to 32 | normal columns | pad to 32]
   std::vector<int32_t> pos_h(static_cast<size_t>(k));

@@ -744,7 +744,9 @@ def test_k2_stream_k_bitexact(cuda, m, n, k, n_out, monkeypatch):
 
 
 # ---------------------------------------------------------------- K7 AdaRound calibrate_layer
-@pytest.mark.parametrize("n,k,n_out,iters,batch", [(48, 64, 32, 60, 2), (96, 192, 32, 40, 3), (64, 128, 0, 30, 2)])
+@pytest.mark.parametrize("n,k,n_out,iters,batch", [(48, 64, 32, 60, 2), (96, 192, 32, 40, 3), (64, 128, 0, 30, 2),
+                                                   (45, 100, 8, 20, 3),   # odd N: the DGEMM path
+                                                   (38, 200, 0, 20, 4)])  # K off the 32 grid
 def test_calibrate_layer_matches_reference(cuda, ref_lib, n, k, n_out, iters, batch):
     """K7 (f64 AdaRound on the GPU) follows the reference calibrate_layer: same sampler, same
     per-element formulas, f64 throughout -> identical hard codes and the learned scales, act
