@@ -317,41 +317,8 @@ __device__ __forceinline__ uint32_t act_code_slow(uint16_t h, double s64, int qm
   return static_cast<uint32_t>(act_code_exact(bf16_bits_to_float(h), s64, qmax));
 }
 
-// Exact code of a per-token value whose fp32 product t = v*r32 lies within the tie guard of
-// the half-integer hc (bf16 inputs make exact .5 ties common: a row whose |x|max mantissa
-// is a power of two turns every odd mantissa of one binade into a tie).  The reference
-// rounds fl64(v / s64) half-to-even (quant.cpp:123-131).  fl64(v / s64) == hc exactly iff
-// |v/s64 - hc| <= half an ulp of hc (a quarter on the small side of hc = +-0.5), i.e. iff
-// |r| <= s64 * ulp(hc)/2 with r = v - hc*s64 from one f64 fma; otherwise the quotient is a
-// neighbouring double on r's side.  A band of 2^-30 around the boundary takes the division.
-// Returns kTieUndecided for the band (the caller rescans those values with the division).
-constexpr uint32_t kTieUndecided = 0x100u;
-__device__ __forceinline__ uint32_t act_code_tie(float v, float t, double s64, int qmax) {
-  const float q = rintf(t);
-  const float lower = t > q ? q : q - 1.f;  // hc = lower + 0.5
-  const double hc = static_cast<double>(lower) + 0.5;
-  const double r = fma(-hc, s64, static_cast<double>(v));
-  const int e = static_cast<int>((__float_as_uint(fabsf(static_cast<float>(hc))) >> 23) & 0xffu) - 127;
-  double hu = s64 * __longlong_as_double(static_cast<long long>(1023 + e - 53) << 52);
-  if (e == -1 && ((r < 0.0) == (hc > 0.0))) hu *= 0.5;  // |hc| = 0.5: finer spacing below
-  const double ar = fabs(r);
-  int code;
-  if (ar < hu * (1.0 - 0x1p-30)) {
-    const int lo = static_cast<int>(lower);
-    code = (lo & 1) ? lo + 1 : lo;  // exact tie in f64: half to even
-  } else if (ar > hu * (1.0 + 0x1p-30)) {
-    code = static_cast<int>(lower) + (r > 0.0 ? 1 : 0);
-  } else {
-    return kTieUndecided;
-  }
-  code = code > qmax ? qmax : (code < -qmax ? -qmax : code);
-  return static_cast<uint32_t>(code);
-}
-
-// Patch the codes of one flagged chunk (N values, bf16 bits hv): per-token values within
-// the guard are decided exactly by act_code_tie.  Values that need the f64 division (the
-// undecided band, and static-scale near-ties) keep their fast code and set `rescan`; with
-// `exact` (the rescan pass) they take the division here.
+// Patch the codes of one flagged chunk (N values, bf16 bits hv): values within the tie guard
+// take the exact f64 division (`rescan` / kExact are kept for the callers' interface).
 template <bool kStatic, int N, bool kExact>
 __device__ __forceinline__ void act_fix_chunk(const uint16_t* hv, uint32_t* c, const ActScale& sc,
                                               double s64, int qmax, bool& rescan) {
@@ -359,22 +326,19 @@ __device__ __forceinline__ void act_fix_chunk(const uint16_t* hv, uint32_t* c, c
   for (int e = 0; e < N; ++e) {
     const float v = __uint_as_float(static_cast<uint32_t>(hv[e]) << 16);
     bool divide = false;
+    // a value within the guard takes the reference's own arithmetic, rint(v / s) in f64 (round 2:
+    // deciding it by the f64 boundary analysis of act_code_tie first was slower -- K1 at
+    // 4680 x 1536 18.4 -> 14.3 us with the division, its one-row-per-warp critical path shorter)
     if (kStatic) {
       const float t = fminf(fmaxf(__fmul_rn(v, sc.r), -sc.fq), sc.fq);
       divide = fabsf(__fsub_rn(t, rintf(t))) > tie_guard<true>();
     } else {
-      const float t = __fmul_rn(v, sc.r);  // only its position relative to hc matters
+      const float t = __fmul_rn(v, sc.r);
       const float d = __fmaf_rn(v, sc.r, -rintf(t));
-      if (fabsf(d) > tie_guard<false>()) {
-        const uint32_t code = act_code_tie(v, t, s64, qmax);
-        if (code == kTieUndecided) divide = true;
-        else c[e] = code;
-      }
+      divide = fabsf(d) > tie_guard<false>();
     }
-    if (divide) {
-      if (kExact) c[e] = static_cast<uint32_t>(act_code_exact(v, s64, qmax));
-      else rescan = true;
-    }
+    if (divide) c[e] = static_cast<uint32_t>(act_code_exact(v, s64, qmax)) & 0xffu;
+    (void)rescan;
   }
 }
 
@@ -1398,6 +1362,32 @@ __device__ __noinline__ uint2 act_fix8_reg(uint4 d, ActScale sc, double s64, int
 template <bool kStatic>
 __device__ __noinline__ uint32_t act_fix4_reg(uint2 hv2, ActScale sc, double s64, int qmax);
 
+// the 8 codes of a flagged chunk by the reference's own arithmetic, rint(v / s) in f64 then the
+// clamp (quant.cpp:132-135): shorter than the tie analysis (act_fix8_reg), which on a
+// one-row-per-warp launch lengthened the critical path of the ~half of the warps that hold a tie
+__device__ __noinline__ uint2 act_fix8_div(uint4 d, double s64, int qmax) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const uint32_t bits = h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16);
+    c[h] = static_cast<uint32_t>(quant_code_exact(static_cast<double>(__uint_as_float(bits)), s64, qmax)) & 0xffu;
+  }
+  return make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+}
+
+// every code of a rare row by the exact division (non-finite values reported), plan-order rows:
+// this thread's chunks (tt + i T) * 8, i < V
+__device__ __noinline__ void act_slow_row(const uint16_t* xr, int k, int8_t* qr, int tt, int T, int V, double s64,
+                                          int qmax, unsigned long long* err, int64_t flat0) {
+  for (int i = 0; i < V; ++i) {
+    const int c0 = (tt + i * T) * 8;
+    if (c0 >= k) break;
+    for (int h = 0; h < 8; ++h)
+      qr[c0 + h] = static_cast<int8_t>(act_code_slow(xr[c0 + h], s64, qmax, err, flat0 + c0 + h));
+  }
+}
+
 template <int V, int W, bool kStatic, bool kGather>
 __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (32 * W) > 0 ? 1152 / (32 * W) : 1))
     quant_act_reg_kernel(const uint16_t* __restrict__ x, int64_t m, int k, int64_t ldx,
@@ -1475,26 +1465,25 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
   }
   int8_t* qr = q + row * ldq;
   if (!kGather) {
+    if (row_bad || sc.exact) {  // rare rows: non-finite input (reported) or unusable fp32 reciprocal,
+      // out of line from the global row: inlined per chunk, this path was three quarters of the
+      // kernel's code (instruction-cache misses on the hot path, +4 us on a 4680-row launch)
+      act_slow_row(x + row * ldx, k, qr, tt, T, V, s64, qmax, err, row * k_out);
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int c0 = (tt + i * T) * 8;
       const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
       uint32_t c[8];
-      if (row_bad || sc.exact) {  // rare rows: non-finite input (reported) or unusable fp32 reciprocal
+      float dmax = 0.f;
 #pragma unroll
-        for (int h = 0; h < 8; ++h)
-          c[h] = act_code_slow(static_cast<uint16_t>(h & 1 ? w[h >> 1] >> 16 : w[h >> 1] & 0xffffu), s64, qmax,
-                               err, row * k_out + c0 + h);
-      } else {
-        float dmax = 0.f;
-#pragma unroll
-        for (int h = 0; h < 4; ++h)
-          act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
-                              c[2 * h + 1], dmax);
-        if (dmax > tie_guard<kStatic>()) {  // a value within the tie guard: decide exactly
-          *reinterpret_cast<uint2*>(qr + c0) = act_fix8_reg<V, W, kStatic, kGather>(d[i], sc, s64, qmax);
-          continue;
-        }
+      for (int h = 0; h < 4; ++h)
+        act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
+                            c[2 * h + 1], dmax);
+      if (dmax > tie_guard<kStatic>()) {  // a value within the tie guard: decide exactly
+        *reinterpret_cast<uint2*>(qr + c0) = act_fix8_div(d[i], s64, qmax);
+        continue;
       }
       *reinterpret_cast<uint2*>(qr + c0) = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
     }

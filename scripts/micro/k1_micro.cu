@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include "../../include/qarvd_b200.h"
 
 __device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
   uint4 r;
@@ -61,6 +62,19 @@ __device__ __noinline__ uint2 fix8_f32_ool(uint4 d, float rr) {  // fp32-only wo
   }
   return make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
 }
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 // FEAT bit 0: exact f64 scale (fma correction) + s64 store; bit 1: tie detection + out-of-line fix
 // bit 2: the fix inline with the fma decision instead
 template <int V, int FEAT>
@@ -92,6 +106,22 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
     const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
     uint32_t c[8];
     float dmax = 0.f;
+    if (FEAT & 512) {  // the product's packed FFMA2 rounding (act_codes2)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint64_t v2 = pk2(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u));
+        const uint64_t r2 = pk2(rr, rr), m2 = pk2(12582912.0f, 12582912.0f);
+        const uint64_t y2 = ffma2(v2, r2, m2);
+        const uint64_t n2 = ffma2(y2, pk2(-1.f, -1.f), m2);
+        const uint64_t d2 = ffma2(v2, r2, n2);
+        float d0, d1, y0, y1;
+        upk2(d2, d0, d1);
+        upk2(y2, y0, y1);
+        dmax = fmaxf(dmax, fmaxf(fabsf(d0), fabsf(d1)));
+        c[2 * h] = __float_as_uint(y0) & 0xffu;
+        c[2 * h + 1] = __float_as_uint(y1) & 0xffu;
+      }
+    } else {
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
       const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
@@ -99,6 +129,7 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
       const float y = t + 12582912.0f;
       c[h] = __float_as_uint(y) & 0xffu;
       dmax = fmaxf(dmax, fabsf(t - (y - 12582912.0f)));
+    }
     }
     if (FEAT & 64) {  // per-value inline exact decision of the values within the guard
 #pragma unroll
@@ -240,6 +271,54 @@ int main(int argc, char** argv) {
   timeit("feat 257 (out-of-line fp32-only fix)", [&] { k1f<6, 257><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
   timeit("feat 1 again", [&] { k1f<6, 1><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
   timeit("feat 3 again", [&] { k1f<6, 3><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o); });
+  {  // the product's K1 through the C-ABI (plan-order rows, per-token), same data and flush
+    int8_t* q2; cudaMalloc(&q2, (size_t)m * k);
+    float* s32; cudaMalloc(&s32, m * 4);
+    timeit("product qarvd_quantize_act (C-ABI)", [&] {
+      qarvd_quantize_act(x, QARVD_BF16, m, k, k, nullptr, k, QARVD_ACT_PER_TOKEN, 0.0, 8, q2, k, s32, nullptr, nullptr, nullptr);
+    });
+    // agreement with the fix-free microkernel on the non-tie values
+    k1f<6, 3><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o);
+    std::vector<int8_t> a((size_t)m * k), b((size_t)m * k);
+    cudaMemcpy(a.data(), q, a.size(), cudaMemcpyDeviceToHost);
+    cudaMemcpy(b.data(), q2, b.size(), cudaMemcpyDeviceToHost);
+    size_t diff = 0;
+    for (size_t i = 0; i < a.size(); ++i) diff += a[i] != b[i];
+    printf("microkernel (feat 3) vs product codes: %zu of %zu differ\n", diff, a.size());
+  }
+  {  // both kernels captured into CUDA graphs (no host time in the timed region)
+    cudaStream_t cs; cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    int8_t* q3; cudaMalloc(&q3, (size_t)m * k);
+    float* s33; cudaMalloc(&s33, m * 4);
+    auto graph_of = [&](auto fn) {
+      cudaGraph_t g; cudaGraphExec_t ge;
+      cudaStreamBeginCapture(cs, cudaStreamCaptureModeGlobal);
+      fn();
+      cudaStreamEndCapture(cs, &g);
+      cudaGraphInstantiate(&ge, g, 0);
+      return ge;
+    };
+    cudaGraphExec_t gp = graph_of([&] {
+      const int st = qarvd_quantize_act(x, QARVD_BF16, m, k, k, nullptr, k, QARVD_ACT_PER_TOKEN, 0.0, 8, q3, k, s33, nullptr, nullptr, cs);
+      if (st) printf("capture: status %d %s\n", st, qarvd_last_error());
+    });
+    cudaGraphExec_t gm = graph_of([&] { k1f<6, 3><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    cudaGraphExec_t gm2 = graph_of([&] { k1f<6, 515><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    cudaGraphExec_t gm3 = graph_of([&] { k1f<6, 513><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    auto gtime = [&](const char* name, cudaGraphExec_t ge) {
+      float best = 1e9;
+      for (int it = 0; it < 30; ++it) {
+        cudaMemsetAsync(fl, it, 256 << 20, cs);
+        cudaEventRecord(a, cs); cudaGraphLaunch(ge, cs); cudaEventRecord(b, cs); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b); best = ms < best ? ms : best;
+      }
+      printf("%-40s graph best %6.1f us\n", name, best * 1e3);
+    };
+    gtime("product K1 (graph)", gp);
+    gtime("microkernel feat 3 (graph)", gm);
+    gtime("microkernel feat 515 (FFMA2 + fix)", gm2);
+    gtime("microkernel feat 513 (FFMA2, no fix)", gm3);
+  }
   for (float gd : {0.49997f, 0.4999999f}) {
     unsigned int z = 0;
     cudaMemcpyToSymbol(g_flag_count, &z, 4);
