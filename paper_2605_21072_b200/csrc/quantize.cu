@@ -1376,6 +1376,16 @@ __device__ __noinline__ uint2 act_fix8_div(uint4 d, double s64, int qmax) {
   return make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
 }
 
+// the gathered twin: plan positions c = tt, tt + T, ... < k_out through the int16 table
+__device__ __noinline__ void act_slow_row_g(const uint16_t* xr, const int16_t* gidx, int k, int k_out, int8_t* qr,
+                                            int tt, int T, double s64, int qmax, unsigned long long* err,
+                                            int64_t flat0) {
+  for (int c = tt; c < k_out; c += T) {
+    const int g = gidx[c];
+    qr[c] = g >= k ? static_cast<int8_t>(0) : static_cast<int8_t>(act_code_slow(xr[g], s64, qmax, err, flat0 + c));
+  }
+}
+
 // every code of a rare row by the exact division (non-finite values reported), plan-order rows:
 // this thread's chunks (tt + i T) * 8, i < V
 __device__ __noinline__ void act_slow_row(const uint16_t* xr, int k, int8_t* qr, int tt, int T, int V, double s64,
@@ -1488,35 +1498,37 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
       *reinterpret_cast<uint2*>(qr + c0) = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
     }
   } else {
-    // per-team row copy (+ 8 zero sentinels that pad slots of the gather read)
-    uint16_t* srow = k1r_smem + team * row_stride;
+    // Codes first, in natural column order from the registers (8 per lane per step, the same
+    // fast path and tie repair as plan-order rows) into the team's shared slot, then the plan's
+    // gather on the codes (4 bytes per lane per step): the rounding is off the gather's
+    // dependent shared-memory loads.
+    if (row_bad || sc.exact) {
+      act_slow_row_g(x + row * ldx, gidx, k, k_out, qr, tt, T, s64, qmax, err, row * k_out);
+      return;
+    }
+    uint8_t* crow = reinterpret_cast<uint8_t*>(k1r_smem + team * row_stride);
 #pragma unroll
-    for (int i = 0; i < V; ++i) reinterpret_cast<uint4*>(srow)[tt + i * T] = d[i];
-    if (tt < 8) srow[k + tt] = 0;
+    for (int i = 0; i < V; ++i) {
+      const int c0 = (tt + i * T) * 8;
+      const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
+      uint32_t c[8];
+      float dmax = 0.f;
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
+                            c[2 * h + 1], dmax);
+      *reinterpret_cast<uint2*>(crow + c0) =
+          dmax > tie_guard<kStatic>() ? act_fix8_div(d[i], s64, qmax)
+                                      : make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+    }
+    if (tt < 8) crow[k + tt] = 0;  // the pad columns' sentinel (the table maps pads to k)
     if (W > 1) __syncthreads();
     else __syncwarp();
 #pragma unroll 4
     for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
       const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
-      const uint16_t hv[4] = {srow[gp.x & 0xffffu], srow[gp.x >> 16], srow[gp.y & 0xffffu], srow[gp.y >> 16]};
-      uint32_t c[4];
-      if (row_bad || sc.exact) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c[e] = act_code_slow(hv[e], s64, qmax, err, row * k_out + c0 + e);
-      } else {
-        float dmax = 0.f;
-        act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[0]) << 16),
-                            __uint_as_float(static_cast<uint32_t>(hv[1]) << 16), sc, c[0], c[1], dmax);
-        act_codes2<kStatic>(__uint_as_float(static_cast<uint32_t>(hv[2]) << 16),
-                            __uint_as_float(static_cast<uint32_t>(hv[3]) << 16), sc, c[2], c[3], dmax);
-        if (dmax > tie_guard<kStatic>()) {
-          *reinterpret_cast<uint32_t*>(qr + c0) =
-              act_fix4_reg<kStatic>(make_uint2(hv[0] | (static_cast<uint32_t>(hv[1]) << 16),
-                                               hv[2] | (static_cast<uint32_t>(hv[3]) << 16)), sc, s64, qmax);
-          continue;
-        }
-      }
-      *reinterpret_cast<uint32_t*>(qr + c0) = pack4(c[0], c[1], c[2], c[3]);
+      *reinterpret_cast<uint32_t*>(qr + c0) =
+          pack4(crow[gp.x & 0xffffu], crow[gp.x >> 16], crow[gp.y & 0xffffu], crow[gp.y >> 16]);
     }
   }
 }
@@ -1828,10 +1840,10 @@ int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t 
                     const int32_t* gather, int k_out, double static_scale, int qmax, int8_t* q,
                     int64_t ldq, float* s32, double* s64, unsigned long long* err,
                     cudaStream_t stream) {
-  // register-resident K1 for plan-order rows (measured on the Wan FFN intermediate, M = 4680 x
-  // 8960: 41 vs 45 us; scripts/k1_flush_probe.py); gathered rows keep the slot ring, which the
-  // register kernel does not beat (19.5 vs 18.4 us at 4680 x 1536).  QARVD_K1_REG=0 / =2: never /
-  // always (gathered too).
+  // register-resident K1 for every row shape it covers (round 2, after the tie repair became the
+  // plain division and gathered rows quantize in natural order before the gather: U 34.5 us,
+  // gathered 4680 x 1536 16.4 us vs the slot ring's 18.4; scripts/k1_flush_probe.py).
+  // QARVD_K1_REG=0 / =1: never / plan-order rows only.
   // QARVD_K1_BULK=1: the bulk-staged kernel (opt-in: measured slower on the Wan shapes, x 23.6 vs
   // 17.4 us and U 37.7 vs 33.8 us under the bench's L2 flush, scripts/k1_flush_probe.py -- it
   // issues ~12 instructions per value and stays issue-bound with the bytes in flight solved)
@@ -1843,7 +1855,7 @@ int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t 
                                                      s64, err, stream)
                     : launch_act_bulk<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
                                                       s64, err, stream);
-  static const int reg = getenv("QARVD_K1_REG") ? atoi(getenv("QARVD_K1_REG")) : 1;
+  static const int reg = getenv("QARVD_K1_REG") ? atoi(getenv("QARVD_K1_REG")) : 2;
   if (reg > 0 && (!gathered || (reg == 2 && k_out % 4 == 0))) {
     const int st = gathered ? launch_act_reg<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
                                                             ldq, s32, s64, err, stream)
