@@ -236,8 +236,10 @@ class QuantizedChain:
         """Capture launch() into a CUDA graph (after one eager warm-up launch).  With
         ``timed`` the graph also records per-kernel timing events (``self.events``); with
         ``parallel`` the graph holds launch_parallel()'s side branches."""
+        c0 = _lib.launch_count()
         self.launch()
         torch.cuda.synchronize()
+        self._launches = _lib.launch_count() - c0  # K1 (+ its deferred tie repair) + K2 per layer
         if parallel:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -269,7 +271,8 @@ class QuantizedChain:
         return self.y[-1]
 
     def kernels_per_step(self) -> int:
-        return 2 * len(self.layers)
+        """Kernel launches of one step (counted on the eager launch before capture)."""
+        return getattr(self, "_launches", 2 * len(self.layers))
 
     def int_ops(self) -> float:
         """Algorithmic ops of the chain as specified (unfolded shapes, no pad rows)."""
