@@ -77,12 +77,17 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
 }
 // FEAT bit 0: exact f64 scale (fma correction) + s64 store; bit 1: tie detection + out-of-line fix
 // bit 2: the fix inline with the fma decision instead
+__device__ long long g_t[4680][4];
+__device__ unsigned int g_smid[4680];
 template <int V, int FEAT>
 __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m, int8_t* __restrict__ q,
                                            float* __restrict__ s, double* __restrict__ s64o) {
   const int lane = threadIdx.x & 31;
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= m) return;
+  long long t0 = 0;
+  unsigned int nfix = 0;
+  if (FEAT & 2048) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); t0 = (long long)g; }
   uint4 d[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) d[i] = ldg_nc(reinterpret_cast<const uint4*>(x + (int64_t)row * (V * 256)) + lane + 32 * i);
@@ -101,11 +106,15 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
     if (lane == 31) { s[row] = __double2float_rn(s64); s64o[row] = s64; }
   } else if (lane == 0) s[row] = amax / 127.f;
   int8_t* qr = q + (int64_t)row * (V * 256);
+  uint32_t tailmask = 0;
+  const bool p2 = (mag & 0x7fu) == 0u && mag >= 0x80u;
+  const bool tie_dn = p2 && fma(s64, 127.0, -(double)amax) > 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
     uint32_t c[8];
     float dmax = 0.f;
+    uint32_t vmask = 0;  // FEAT 8192: values within the guard
     if (FEAT & 512) {  // the product's packed FFMA2 rounding (act_codes2)
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
@@ -128,7 +137,9 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
       const float t = v * rr;
       const float y = t + 12582912.0f;
       c[h] = __float_as_uint(y) & 0xffu;
-      dmax = fmaxf(dmax, fabsf(t - (y - 12582912.0f)));
+      const float dd = fabsf(t - (y - 12582912.0f));
+      dmax = fmaxf(dmax, dd);
+      if (FEAT & 8192) vmask |= (dd > 0.49997f ? 1u : 0u) << h;
     }
     }
     if (FEAT & 64) {  // per-value inline exact decision of the values within the guard
@@ -146,7 +157,33 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
       }
     }
     uint2 out = make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
-    if ((FEAT & 2) && dmax > 0.49997f) out = fix8(d[i], s64);
+    if ((FEAT & 1024) && dmax > 0.49997f) tailmask |= 1u << i;
+    if ((FEAT & 8192) && vmask) {  // divide only the flagged values
+      while (vmask) {
+        const int h = __ffs(vmask) - 1;
+        vmask &= vmask - 1;
+        const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+        c[h] = static_cast<uint32_t>(static_cast<int>(rint(__ddiv_rn(static_cast<double>(v), s64)))) & 0xffu;
+      }
+      out = make_uint2(c[0] | c[1] << 8 | c[2] << 16 | c[3] << 24, c[4] | c[5] << 8 | c[6] << 16 | c[7] << 24);
+      ++nfix;
+    } else if ((FEAT & 2) && dmax > 0.49997f) {
+      if ((FEAT & 4096) && p2) {  // power-of-two |x|max: fp32 rule, ties by the sign of s64's rounding
+        uint32_t cc[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+          const float t = v * rr;
+          const float fl_ = floorf(t);
+          const float qq = (t - fl_) == 0.5f ? ((tie_dn != (t < 0.f)) ? fl_ : fl_ + 1.f) : rintf(t);
+          cc[h] = static_cast<uint32_t>(static_cast<int>(qq)) & 0xffu;
+        }
+        out = make_uint2(cc[0] | cc[1] << 8 | cc[2] << 16 | cc[3] << 24, cc[4] | cc[5] << 8 | cc[6] << 16 | cc[7] << 24);
+      } else {
+        out = fix8(d[i], s64);
+      }
+      ++nfix;
+    }
     if ((FEAT & 4) && dmax > 0.49997f) out = fix8_fma(d[i], rr, s64);
     if ((FEAT & 128) && dmax > 0.49997f) out = fix8_fma_ool(d[i], rr, s64);
     if ((FEAT & 256) && dmax > 0.49997f) out = fix8_f32_ool(d[i], rr);
@@ -154,6 +191,19 @@ __global__ void __launch_bounds__(256) k1f(const uint16_t* __restrict__ x, int m
     if ((FEAT & 16) && dmax > 0.49997f) out.x ^= 1u;   // trivial branch
     if ((FEAT & 32) && dmax > 0.4999999f) out = fix8(d[i], s64);  // tight guard (count test)
     *reinterpret_cast<uint2*>(qr + (lane + 32 * i) * 8) = out;
+  }
+  if (FEAT & 2048) {
+    unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    const unsigned int nf = __reduce_add_sync(0xffffffffu, nfix);
+    if (lane == 0) { g_t[row][0] = t0; g_t[row][1] = (long long)g; g_t[row][2] = nf; unsigned int sm; asm("mov.u32 %0, %%smid;" : "=r"(sm)); g_smid[row] = sm; }
+  }
+  if (FEAT & 1024) {  // repairs after every fast store of the row
+    while (tailmask) {
+      const int i = __ffs(tailmask) - 1;
+      tailmask &= tailmask - 1;
+      const uint4 dd = ldg_nc(reinterpret_cast<const uint4*>(x + (int64_t)row * (V * 256)) + lane + 32 * i);
+      *reinterpret_cast<uint2*>(qr + (lane + 32 * i) * 8) = fix8(dd, s64);
+    }
   }
 }
 __device__ unsigned int g_flag_count;
@@ -318,6 +368,31 @@ int main(int argc, char** argv) {
     gtime("microkernel feat 3 (graph)", gm);
     gtime("microkernel feat 515 (FFMA2 + fix)", gm2);
     gtime("microkernel feat 513 (FFMA2, no fix)", gm3);
+    cudaGraphExec_t gm4 = graph_of([&] { k1f<6, 1025><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    gtime("microkernel feat 1025 (tail repair)", gm4);
+    cudaGraphExec_t gm5 = graph_of([&] { k1f<6, 3 + 4096><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    gtime("microkernel feat 4099 (p2 rule + division)", gm5);
+    cudaGraphExec_t gm6 = graph_of([&] { k1f<6, 1 + 8192><<<(m + 7) / 8, 256, 0, cs>>>(x, m, q, s, s64o); });
+    gtime("microkernel feat 8193 (divide flagged values)", gm6);
+    for (int feat : {2049 + 2, 2049, 2049 + 8192}) {
+      cudaMemset(fl, 1, 256 << 20);
+      cudaDeviceSynchronize();
+      if (feat == 2051) k1f<6, 2051><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o);
+      else if (feat == 2049 + 8192) k1f<6, 2049 + 8192><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o);
+      else k1f<6, 2049><<<(m + 7) / 8, 256>>>(x, m, q, s, s64o);
+      cudaDeviceSynchronize();
+      static long long ht[4680][4]; static unsigned int hs[4680];
+      cudaMemcpyFromSymbol(ht, g_t, sizeof(ht)); cudaMemcpyFromSymbol(hs, g_smid, sizeof(hs));
+      long long tmin = ht[0][0], tmax = 0;
+      for (int r = 0; r < m; ++r) { tmin = ht[r][0] < tmin ? ht[r][0] : tmin; tmax = ht[r][1] > tmax ? ht[r][1] : tmax; }
+      double dfix = 0, dnofix = 0; int nf = 0, nn = 0; long long worst = 0; int worst_r = 0;
+      for (int r = 0; r < m; ++r) { long long du = ht[r][1] - ht[r][0]; if (ht[r][2]) { dfix += du; ++nf; } else { dnofix += du; ++nn; } if (ht[r][1] > worst) { worst = ht[r][1]; worst_r = r; } }
+      printf("feat %d: span %lld ns; warps with repairs %d (mean %.0f ns), without %d (mean %.0f ns); last to finish row %d (%lld fixes, start +%lld ns, dur %lld ns, sm %u)\n",
+             feat, tmax - tmin, nf, nf ? dfix / nf : 0, nn, nn ? dnofix / nn : 0, worst_r, ht[worst_r][2], ht[worst_r][0] - tmin, ht[worst_r][1] - ht[worst_r][0], hs[worst_r]);
+      // start-time distribution
+      long long late = 0; for (int r = 0; r < m; ++r) late = (ht[r][0] - tmin) > late ? (ht[r][0] - tmin) : late;
+      printf("   latest warp start +%lld ns\n", late);
+    }
   }
   for (float gd : {0.49997f, 0.4999999f}) {
     unsigned int z = 0;
