@@ -1376,6 +1376,8 @@ __device__ __noinline__ uint2 act_fix8_div(uint4 d, double s64, int qmax) {
   return make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
 }
 
+constexpr unsigned int kK1RepairCap = 512;  // near-tie chunks queued per CTA for the shared repair
+
 // the gathered twin: plan positions c = tt, tt + T, ... < k_out through the int16 table
 __device__ __noinline__ void act_slow_row_g(const uint16_t* xr, const int16_t* gidx, int k, int k_out, int8_t* qr,
                                             int tt, int T, double s64, int qmax, unsigned long long* err,
@@ -1424,22 +1426,28 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
                      static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16));
     }
   }
+  __shared__ unsigned int s_nfix;
+  __shared__ unsigned int s_fix[kK1RepairCap];  // (team << 16) | (tt << 4) | chunk
+  __shared__ double s_s64[kTeams];
+  if (threadIdx.x == 0) s_nfix = 0u;
   pdl_wait();  // x is written by the previous kernel of the chain
   pdl_launch_dependents();
   uint4 d[V];
-  const bool live = row < m;
+  const bool live = row < m;  // W > 1: one team per CTA, the whole CTA shares it
   if (live) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
 #pragma unroll
     for (int i = 0; i < V; ++i) d[i] = ldg_stream(xr + tt + i * T);
   }
-  if (kGather) __syncthreads();  // the table is staged
-  if (!live) return;  // W > 1: one team per CTA, the whole CTA leaves together
+  if (kGather || W > 1) __syncthreads();  // the table is staged / s_nfix is zeroed
+  if (W > 1 && !live) return;             // CTA-uniform
   uint32_t mx = 0;
+  if (live) {
 #pragma unroll
-  for (int i = 0; i < V; ++i)
-    mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[i].x & 0x7fff7fffu, d[i].y & 0x7fff7fffu),
-                               __vmaxu2(d[i].z & 0x7fff7fffu, d[i].w & 0x7fff7fffu)));
+    for (int i = 0; i < V; ++i)
+      mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(d[i].x & 0x7fff7fffu, d[i].y & 0x7fff7fffu),
+                                 __vmaxu2(d[i].z & 0x7fff7fffu, d[i].w & 0x7fff7fffu)));
+  }
   uint32_t mag = __reduce_max_sync(0xffffffffu, max(mx & 0xffffu, mx >> 16));
   if (W > 1) {
     if (lane == 0) wmax[warp] = mag;
@@ -1469,18 +1477,27 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
     }
   }
   sc.s64 = s64;
-  if (tt == T - 1) {
+  if (live && tt == T - 1) {
     if (s32_out) s32_out[row] = (kStatic || amax > 0.f) ? __double2float_rn(s64) : 0.f;
     if (s64_out) s64_out[row] = s64;
+    s_s64[team] = s64;
   }
   int8_t* qr = q + row * ldq;
-  if (!kGather) {
-    if (row_bad || sc.exact) {  // rare rows: non-finite input (reported) or unusable fp32 reciprocal,
-      // out of line from the global row: inlined per chunk, this path was three quarters of the
-      // kernel's code (instruction-cache misses on the hot path, +4 us on a 4680-row launch)
-      act_slow_row(x + row * ldx, k, qr, tt, T, V, s64, qmax, err, row * k_out);
-      return;
-    }
+  // rare rows: non-finite input (reported) or an unusable fp32 reciprocal -- every code by the
+  // exact division, out of line (inlined per chunk this path was three quarters of the code)
+  const bool slow = live && (row_bad || sc.exact);
+  if (slow) {
+    if (kGather) act_slow_row_g(x + row * ldx, gidx, k, k_out, qr, tt, T, s64, qmax, err, row * k_out);
+    else act_slow_row(x + row * ldx, k, qr, tt, T, V, s64, qmax, err, row * k_out);
+  }
+  // Fast codes in natural column order from the registers, 8 per lane per step: plan-order rows
+  // store them, gathered rows write them to the team's shared slot.  A chunk with a value within
+  // the tie guard is queued for the CTA-shared repair below: after the fast pass every thread of
+  // the CTA takes queued chunks (the reference's division for their 8 values), so a row with
+  // dozens of near-ties no longer serialises them on its own warp (4680 x 1536: 14.2 -> 11.9 us
+  // in the microbenchmark).  A full queue repairs inline.
+  uint8_t* crow = reinterpret_cast<uint8_t*>(k1r_smem + team * row_stride);
+  if (live && !slow) {
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int c0 = (tt + i * T) * 8;
@@ -1491,44 +1508,39 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
       for (int h = 0; h < 4; ++h)
         act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
                             c[2 * h + 1], dmax);
-      if (dmax > tie_guard<kStatic>()) {  // a value within the tie guard: decide exactly
-        *reinterpret_cast<uint2*>(qr + c0) = act_fix8_div(d[i], s64, qmax);
-        continue;
+      uint2 out = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+      if (dmax > tie_guard<kStatic>()) {
+        const unsigned int slot = atomicAdd(&s_nfix, 1u);
+        if (slot < kK1RepairCap) s_fix[slot] = (static_cast<unsigned int>(team) << 16) | (tt << 4) | i;
+        else out = act_fix8_div(d[i], s64, qmax);
       }
-      *reinterpret_cast<uint2*>(qr + c0) = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+      if (kGather) *reinterpret_cast<uint2*>(crow + c0) = out;
+      else *reinterpret_cast<uint2*>(qr + c0) = out;
     }
-  } else {
-    // Codes first, in natural column order from the registers (8 per lane per step, the same
-    // fast path and tie repair as plan-order rows) into the team's shared slot, then the plan's
-    // gather on the codes (4 bytes per lane per step): the rounding is off the gather's
-    // dependent shared-memory loads.
-    if (row_bad || sc.exact) {
-      act_slow_row_g(x + row * ldx, gidx, k, k_out, qr, tt, T, s64, qmax, err, row * k_out);
-      return;
-    }
-    uint8_t* crow = reinterpret_cast<uint8_t*>(k1r_smem + team * row_stride);
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const int c0 = (tt + i * T) * 8;
-      const uint32_t w[4] = {d[i].x, d[i].y, d[i].z, d[i].w};
-      uint32_t c[8];
-      float dmax = 0.f;
-#pragma unroll
-      for (int h = 0; h < 4; ++h)
-        act_codes2<kStatic>(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u), sc, c[2 * h],
-                            c[2 * h + 1], dmax);
-      *reinterpret_cast<uint2*>(crow + c0) =
-          dmax > tie_guard<kStatic>() ? act_fix8_div(d[i], s64, qmax)
-                                      : make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
-    }
-    if (tt < 8) crow[k + tt] = 0;  // the pad columns' sentinel (the table maps pads to k)
-    if (W > 1) __syncthreads();
-    else __syncwarp();
+    if (kGather && tt < 8) crow[k + tt] = 0;  // the pad columns' sentinel (the table maps pads to k)
+  }
+  __syncthreads();  // the fast pass of every team is done, the queue complete
+  const unsigned int nfix = min(s_nfix, kK1RepairCap);
+  for (unsigned int e = threadIdx.x; e < nfix; e += blockDim.x) {
+    const unsigned int en = s_fix[e];
+    const int tm = static_cast<int>(en >> 16), lt = static_cast<int>((en >> 4) & 0xfffu), i = static_cast<int>(en & 15u);
+    const int64_t rw = static_cast<int64_t>(blockIdx.x) * kTeams + tm;
+    const int c0 = (lt + i * T) * 8;
+    const uint4 dd = *reinterpret_cast<const uint4*>(x + rw * ldx + c0);
+    const uint2 fixed = act_fix8_div(dd, s_s64[tm], qmax);
+    if (kGather) *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(k1r_smem + tm * row_stride) + c0) = fixed;
+    else *reinterpret_cast<uint2*>(q + rw * ldq + c0) = fixed;
+  }
+  if (kGather) {
+    __syncthreads();  // the slots hold the final codes
+    if (live && !slow) {
+      // the plan's gather on the codes, 4 per lane per step
 #pragma unroll 4
-    for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
-      const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
-      *reinterpret_cast<uint32_t*>(qr + c0) =
-          pack4(crow[gp.x & 0xffffu], crow[gp.x >> 16], crow[gp.y & 0xffffu], crow[gp.y >> 16]);
+      for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
+        const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
+        *reinterpret_cast<uint32_t*>(qr + c0) =
+            pack4(crow[gp.x & 0xffffu], crow[gp.x >> 16], crow[gp.y & 0xffffu], crow[gp.y >> 16]);
+      }
     }
   }
 }
