@@ -971,7 +971,7 @@ struct WeightJobDev {
   float* so32;
   float* sn32;
 };
-constexpr int kWTeams = 4;
+constexpr int kWTeams = 8;
 
 template <bool dummy = false>
 __device__ __noinline__ void wq_fix_chunk(const uint16_t* hv, uint32_t* c, ActScale sc, double s64, int qmax) {
