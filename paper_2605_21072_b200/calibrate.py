@@ -359,7 +359,10 @@ class CalibrationShard:
                      (_lib.ctypes.c_double * self.frames)(*[float(v) for v in self.weights]))
                 self._k4.append((jobs, len(idx), pct, nc, w, res))
         search = {}
-        hist_first = os.environ.get("QARVD_CALIB_ORDER", "hist_first") == "hist_first"
+        # launch order of the two streams' work (QARVD_CALIB_ORDER=hist_first / k3_first): after
+        # round 2's faster K3 / K5, K3 -> plan -> K5 first measures 15.0-15.1 ms per step against
+        # 15.5 ms with the histogram pass first
+        hist_first = os.environ.get("QARVD_CALIB_ORDER", "k3_first") == "hist_first"
 
         def k4():
             with torch.cuda.stream(self._side):
@@ -367,8 +370,8 @@ class CalibrationShard:
                     _lib.call("qarvd_scale_search_async", jobs, nj, pct, nc, w, 8,
                               self._flags[g:g + 1].data_ptr(), _stream())
                     search[g] = res
-        # The K4 histogram pass (one 128 KB-smem CTA per SM, shared-memory-atomic bound, ~64% of
-        # HBM) goes first; K3 -> plan -> K5 then fill the SM resources and HBM bandwidth it leaves
+        # The K4 histogram pass (one 128 KB-smem CTA per SM, shared-memory-atomic bound) and
+        # K3 -> plan -> K5 share the SMs; whichever is enqueued first gets them first
         if hist_first:
             k4()
         rep = outlier.analyze_layers_async([s.name for s in self.specs], self.w, out=self._rep)
