@@ -762,7 +762,12 @@ def main():
     from paper_2605_21072_b200.pipeline import QuantizedChain
 
     fuse = os.environ.get("QARVD_BENCH_FUSE", "0") == "1"
-    chain = QuantizedChain([L0, L2], M_TOKENS, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fuse_rowmax=fuse)
+    fuse_quant = os.environ.get("QARVD_FUSE_QUANT", "0") == "1"
+    if os.environ.get("QARVD_BENCH_STATIC", "0") == "1":  # A/B: static per-tensor activations
+        L0.act_granularity, L0.act_scale = qb.ACT_PER_TENSOR, 0.0513457
+        L2.act_granularity, L2.act_scale = qb.ACT_PER_TENSOR, 0.0213457
+    chain = QuantizedChain([L0, L2], M_TOKENS, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fuse_rowmax=fuse,
+                           fuse_quant=fuse_quant)
     chain.x.copy_(x)
     # two graphs of the same step: one with CUDA event nodes between the kernels (per-kernel
     # device times) and a plain one for the headline timing -- event nodes would also cut the

@@ -241,6 +241,30 @@ int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_
                          const float* bias, int epilogue, uint16_t* y, int64_t ldy,
                          uint32_t* row_pmax, int64_t pm_count, void* stream);
 
+/* K2 of a chained producer with its consumer's per-token K1 fused into the epilogue:
+ *   quantized_layer_forward(layer_b, quantized_layer_forward(layer_a, x)) without the
+ *   intermediate ever reaching memory (engine.cpp:134-142 twice; kernel_a on kernel_b's output).
+ * y = act(s_x (s_wo acc_o + s_wn acc_n) + b) is rounded to bf16 exactly as qarvd_dual_gemm
+ * writes it, and each row is quantized as
+ *   qarvd_quantize_act(y, QARVD_BF16, m, n, n, NULL, n, granularity, static_scale, bits,
+ *                      q, ldq_out, scale_f32, scale_f64, err_index, stream)
+ * would (per-token: the row max waits for the row's other N tiles; per-tensor static: the codes
+ * come straight from the epilogue registers): same codes (columns 0..n-1 of each row; columns n..ldq_out-1 untouched), same scales,
+ * same non-finite reporting (flat index row * ldq_out + c).  The consumer's input channels must
+ * be in this layer's output order (no gather; pipeline.fold_output_permutation does that).
+ * n % 256 == 0; q rows 16-byte aligned.  workspace: device, 16-byte aligned, ZERO-FILLED once
+ * before first use (it resets itself), >= qarvd_dual_gemm_quant_workspace_size(m) bytes, one
+ * per concurrently running call.  QARVD_ERR_UNSUPPORTED when the persistent grid cannot be
+ * co-resident on this device (the caller then runs qarvd_dual_gemm + qarvd_quantize_act). */
+int64_t qarvd_dual_gemm_quant_workspace_size(int64_t m);
+int qarvd_dual_gemm_quant(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
+                          int64_t n, int64_t k, int64_t k_outlier, const float* scale_x,
+                          const float* scale_w_outlier, const float* scale_w_normal,
+                          const float* bias, int epilogue, int granularity, double static_scale,
+                          int bits, int8_t* q, int64_t ldq_out,
+                          float* scale_f32, double* scale_f64, int64_t* err_index,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+
 /* K2 with the reference's exact f64 epilogue (engine.cpp:86-94: val = 0; val += (s_x*s_wo[j])*acc_o;
  * val += (s_x*s_wn[j])*acc_n) on f64 scales -> f64 y.  Bit-identical to kernel_b_gemm_dequant
  * for symmetric activations; used by the C++ drop-in adapter (toy / reference-parity path). */

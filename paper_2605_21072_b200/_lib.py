@@ -230,6 +230,11 @@ SIGNATURES = {
         c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_double, c_int, c_int,
                 c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_char_p, c_void_p,
                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qarvd_dual_gemm_quant_workspace_size": (c_int64, [c_int64]),
+    "qarvd_dual_gemm_quant": (
+        c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                c_void_p, c_void_p, c_void_p, c_int, c_int, c_double, c_int, c_void_p, c_int64, c_void_p,
+                c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "qarvd_dual_gemm_workspace_size": (c_int64, [c_int64, c_int64, c_int64, c_int64]),
     "qarvd_dual_gemm_ws": (
         c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

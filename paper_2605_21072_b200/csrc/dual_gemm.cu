@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -147,6 +148,24 @@ struct GemmParams {
   int32_t* sk_slots;    // [sk_tiles][sk_slots_per_tile][BN][TM] int32, column-major per tile
   uint32_t* sk_count;   // [sk_tiles][2]: writer-warp arrivals, owner-warp reads (self-resetting)
   int debug;  // QARVD_GEMM_DEBUG: 1 = skip the MMAs, 2 = skip the TMA loads (throughput probes)
+  // fused consumer K1 (qarvd_dual_gemm_quant; the kernel's QZ instance, tiles in row-major
+  // order): the bf16 output is quantized per token in the epilogue instead of being stored.
+  // qz_rowmax [m]: (launch epoch << 16) | row |y| max as sign-cleared bf16 bits; qz_count
+  // [num_m_blks]: arrivals per row block, growing across launches (zero-filled once).
+  int row_major;  // tile order: all N tiles of a row block consecutive (the per-token fused quantizer)
+  int qz;
+  int qz_qmax;
+  int qz_static;       // per-tensor static scale: codes in phase 2, no row-block wait
+  double qz_s_static;  //   the scale (validated finite > 0)
+  unsigned long long* qz_rowmax;
+  unsigned long long* qz_count;
+  unsigned long long* qz_epoch;  // launches completed on this workspace
+  unsigned int* qz_done;         // CTAs finished in the running launch
+  int8_t* qz_q;
+  int64_t qz_ldq;
+  float* qz_sx;
+  double* qz_s64;
+  unsigned long long* qz_err;
 };
 
 // Work list of one SM pair: its stream-K k-block range over the split tiles first, then its
@@ -307,7 +326,78 @@ __device__ __forceinline__ void epi_math(uint32_t (&rn)[CW], const uint32_t (&ro
   }
 }
 
-template <int BN, int CG, int KS, bool SKT = false>
+// ---- fused consumer K1 (qarvd_dual_gemm_quant): the per-token arithmetic of K1's register
+// kernel (quantize.cu: quant_act_reg_kernel, act_codes2<false>, act_fix8_div), restated on the
+// epilogue's registers so the codes are those qarvd_quantize_act writes for the bf16 output.
+constexpr float kQzMagic = 12582912.0f;  // 1.5 * 2^23: an fp32 add rounds to an integer (RNE)
+constexpr float kQzGuard = 0.49997f;     // quantize.cu tie_guard<false>()
+// 8 codes by the reference's f64 division (quant.cpp:132-135); non-finite values are reported
+// (the reference throws, quant.cpp:113-121) and give 0 -- quantize.cu act_code_slow
+__device__ __forceinline__ uint2 qz_div8_body(uint4 d, double s64, int qmax, unsigned long long* err, int64_t flat) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const uint32_t bits = h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16);
+    if ((bits & 0x7f800000u) == 0x7f800000u) {
+      if (err) atomicMin(err, static_cast<unsigned long long>(flat + h));
+      c[h] = 0u;
+    } else {
+      c[h] = static_cast<uint32_t>(quant_code_exact(static_cast<double>(__uint_as_float(bits)), s64, qmax)) & 0xffu;
+    }
+  }
+  return make_uint2(__byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410));
+}
+__device__ __noinline__ uint2 qz_div8(uint4 d, double s64, int qmax, unsigned long long* err, int64_t flat) {
+  return qz_div8_body(d, s64, qmax, err, flat);
+}
+// fast codes of 8 bf16 values (4 packed words): magic + rint(v r) by one packed FMA, the exact
+// residual v r - rint(v r) by a second; |residual| > guard flags the group for the division
+__device__ __forceinline__ uint2 qz_codes8(uint4 d, float r, float& dmax) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  const uint64_t r2 = pk2(r, r), m2 = pk2(kQzMagic, kQzMagic);
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const uint64_t v2 = pk2(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xffff0000u));
+    const uint64_t y2 = fma2(v2, r2, m2);
+    const uint64_t n2 = fma2(y2, pk2(-1.f, -1.f), m2);
+    const uint64_t d2 = fma2(v2, r2, n2);
+    float d0, d1, y0, y1;
+    upk2(d2, d0, d1);
+    upk2(y2, y0, y1);
+    dmax = fmaxf(dmax, fmaxf(fabsf(d0), fabsf(d1)));
+    c[2 * h] = __float_as_uint(y0);
+    c[2 * h + 1] = __float_as_uint(y1);
+  }
+  return make_uint2(__byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410));
+}
+// static per-tensor codes of 8 bf16 values: t = clamp(v r, +-qmax), magic + rint(t); |t - rint t|
+// above the guard flags the group (quantize.cu act_codes2<true>, tie_guard<true>)
+constexpr float kQzGuardStatic = 0.4999f;
+__device__ __forceinline__ uint2 qz_codes8_static(uint4 d, float r, float fq, float& dmax) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const float v = __uint_as_float(h & 1 ? (w[h >> 1] & 0xffff0000u) : (w[h >> 1] << 16));
+    const float t = fminf(fmaxf(__fmul_rn(v, r), -fq), fq);
+    const float y = __fadd_rn(t, kQzMagic);
+    dmax = fmaxf(dmax, fabsf(__fsub_rn(t, __fsub_rn(y, kQzMagic))));
+    c[h] = __float_as_uint(y);
+  }
+  return make_uint2(__byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410));
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+
+template <int BN, int CG, int KS, bool SKT = false, bool QZ = false>
 __global__ void __launch_bounds__(kThreads, 1)
     dual_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
@@ -347,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (p.use_tma_store) ptx::prefetch_tmap(&tmY);
+    if (p.use_tma_store || QZ) ptx::prefetch_tmap(&tmY);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -399,8 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     SkIter<SKT> it(sks, cta_id);
     int t, i0, i1;
     while (it.next(sks, t, i0, i1)) {
-      const int m_blk = t % p.num_m_blks;
-      const int n_blk = t / p.num_m_blks;
+      const int m_blk = p.row_major ? t / p.num_n_blks : t % p.num_m_blks;
+      const int n_blk = p.row_major ? t % p.num_n_blks : t / p.num_m_blks;
       const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
       const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
       for (int i = i0; i < i1; ++i) {
@@ -601,14 +691,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < WC / 32; ++u) {
         const int jl = lane + 32 * u;
-        const int64_t j = static_cast<int64_t>(tt / p.num_m_blks) * BN +
+        const int64_t j = static_cast<int64_t>(p.row_major ? tt % p.num_n_blks : tt / p.num_m_blks) * BN +
                           (half + (jl / CW) * kSubs) * CW + jl % CW;
         const int64_t jc = j < p.n ? j : p.n - 1;
         pf_n[u] = __ldg(p.scale_wn + jc);
         if (has_outlier) pf_o[u] = __ldg(p.scale_wo + jc);
         if (p.bias) pf_b[u] = __ldg(p.bias + jc);
       }
-      const int64_t r = static_cast<int64_t>(tt % p.num_m_blks) * TM + rank * BM + q * 32 + lane;
+      const int64_t r = static_cast<int64_t>(p.row_major ? tt / p.num_n_blks : tt % p.num_m_blks) * TM +
+                        rank * BM + q * 32 + lane;
       pf_x = (r < p.m && p.scale_x) ? __ldg(p.scale_x + r) : 0.f;
     };
     auto release = [&](uint64_t* bar) {
@@ -691,12 +782,121 @@ __global__ void __launch_bounds__(kThreads, 1)
     int nt = -1, ni0 = 0, ni1 = 0;  // the item after this one (scale prefetch)
     bool have = it.next(sks, t, i0, i1);
     if (have) prefetch(t);
+    // fused quantizer: this launch's epoch (launches completed on the workspace + 1) and 1/qmax
+    const unsigned long long qz_epoch = QZ ? __ldcg(p.qz_epoch) + 1ull : 0ull;
+    const double qz_rq = QZ ? 1.0 / static_cast<double>(p.qz_qmax) : 0.0;
+    // static per-tensor mode: r = fl32(1 / s) (quantize.cu scale_static), unusable r -> division
+    const double qz_rd = QZ && p.qz_static ? 1.0 / p.qz_s_static : 0.0;
+    const float qz_sr = static_cast<float>(qz_rd);
+    const float qz_fq = static_cast<float>(p.qz_qmax);
+    const bool qz_sexact = QZ && p.qz_static && !(qz_rd <= static_cast<double>(FLT_MAX) && qz_rd >= static_cast<double>(FLT_MIN));
+    // fused quantizer, static per-tensor scale: bf16-round one 16-column chunk (fp32 bits in rn),
+    // its codes straight away (no row maximum to wait for), staged and TMA-stored
+    auto qz_static_chunk = [&](const uint32_t (&rn)[CW], int64_t row0_, bool row_ok_, int64_t row_, int64_t col0,
+                               int i) {
+      uint32_t pk[CW / 2];
+      uint32_t cm = 0;
+#pragma unroll
+      for (int e = 0; e < CW / 2; ++e) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(rn[2 * e]), __uint_as_float(rn[2 * e + 1]));
+        pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+        cm = __vmaxu2(cm, pk[e] & 0x7fff7fffu);
+      }
+      const bool bad = max(cm & 0xffffu, cm >> 16) >= 0x7f80u;  // non-finite: reported
+      const uint4 d0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      const uint4 d1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      float dm0 = 0.f, dm1 = 0.f;
+      uint2 lo = qz_codes8_static(d0, qz_sr, qz_fq, dm0);
+      uint2 hi = qz_codes8_static(d1, qz_sr, qz_fq, dm1);
+      if (row_ok_ && (qz_sexact || bad || dm0 > kQzGuardStatic || dm1 > kQzGuardStatic)) {
+        const int64_t flat = row_ * p.qz_ldq + col0;
+        if (qz_sexact || bad || dm0 > kQzGuardStatic) lo = qz_div8(d0, p.qz_s_static, p.qz_qmax, p.qz_err, flat);
+        if (qz_sexact || bad || dm1 > kQzGuardStatic) hi = qz_div8(d1, p.qz_s_static, p.qz_qmax, p.qz_err, flat + 8);
+      }
+      uint8_t* stg = ystage0 + (i & 1) * (kYStageBytes / 2);
+      if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
+      __syncwarp();
+      *reinterpret_cast<uint4*>(stg + lane * 16) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && row0_ < p.m) {
+        ptx::tma_store_2d(&tmY, stg, static_cast<int32_t>(col0), static_cast<int32_t>(row0_));
+        ptx::bulk_commit();
+      }
+    };
+    // Fused quantizer, phase B of a tile (deferred by one tile, see below): wait until the tile's
+    // row block is complete, read the row maxima and round the codes held in `u` (bf16 pairs).
+    uint32_t qz_u[QZ ? BN / CW / (kEpiWarps / 4) : 1][CW / 2];
+    int qz_prev_m = -1, qz_prev_n = 0;
+    auto qz_phase_b = [&](int pm_blk, int pn_blk) {
+      constexpr int kSubsQ = kEpiWarps / 4;
+      constexpr int NCHQ = BN / CW / kSubsQ;
+      const int halfq = ew >> 2;
+      const int64_t prow0 = static_cast<int64_t>(pm_blk) * TM + rank * BM + q * 32;
+      const int64_t prow = prow0 + lane;
+      const bool prow_ok = prow < p.m;
+      const unsigned long long P = static_cast<unsigned long long>(p.num_n_blks) * CG;
+      if (ew == 0 && lane == 0) {
+        const unsigned long long want = qz_epoch * P;
+        for (uint32_t polls = 0; ld_acquire_u64(p.qz_count + pm_blk) < want; ++polls) {
+          if (polls > (1u << 24)) __trap();  // a row block that never completes: fail loudly
+          __nanosleep(64);
+        }
+      }
+      ptx::named_bar_sync(1, kEpiWarps * 32);
+      uint32_t mag = 0;
+      if (prow_ok) {
+        const unsigned long long v = ld_acquire_u64(p.qz_rowmax + prow);
+        mag = (v >> 16) == qz_epoch ? static_cast<uint32_t>(v & 0xffffu) : 0u;
+      }
+      const float amax = __uint_as_float(mag << 16);
+      const int qmax = p.qz_qmax;
+      const float r = amax > 0.f ? __fmul_rn(__frcp_rn(amax), static_cast<float>(qmax)) : 0.f;
+      const bool slow = mag >= 0x7f80u || (amax > 0.f && !(r <= FLT_MAX && r >= FLT_MIN));
+      double s64 = DBL_MIN;
+      if (amax > 0.f) {
+        const double a = static_cast<double>(amax), y = a * qz_rq;
+        s64 = fma(fma(-y, static_cast<double>(qmax), a), qz_rq, y);
+      }
+      if (prow_ok && pn_blk == 0 && halfq == 0) {
+        p.qz_sx[prow] = amax > 0.f ? __double2float_rn(s64) : 0.f;
+        if (p.qz_s64) p.qz_s64[prow] = s64;
+      }
+      // fast codes for each group of 8; a group with a value within the tie guard (every group of
+      // a rare row) again by the reference's division, out of line.  Codes go through the warp's
+      // staging tile (32 rows x 16 B, two buffers) and a TMA store per chunk
+#pragma unroll
+      for (int i = 0; i < NCHQ; ++i) {
+        const int c = halfq + i * kSubsQ;
+        const uint4 d0 = make_uint4(qz_u[i][0], qz_u[i][1], qz_u[i][2], qz_u[i][3]);
+        const uint4 d1 = make_uint4(qz_u[i][4], qz_u[i][5], qz_u[i][6], qz_u[i][7]);
+        float dm0 = 0.f, dm1 = 0.f;
+        uint2 lo = qz_codes8(d0, r, dm0);
+        uint2 hi = qz_codes8(d1, r, dm1);
+        if (prow_ok && (slow || dm0 > kQzGuard || dm1 > kQzGuard)) {
+          const int64_t flat = prow * p.qz_ldq + static_cast<int64_t>(pn_blk) * BN + c * CW;
+          if (slow || dm0 > kQzGuard) lo = qz_div8(d0, s64, qmax, slow ? p.qz_err : nullptr, flat);
+          if (slow || dm1 > kQzGuard) hi = qz_div8(d1, s64, qmax, slow ? p.qz_err : nullptr, flat + 8);
+        }
+        uint8_t* stg = ystage0 + (i & 1) * (kYStageBytes / 2);
+        if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer has read it
+        __syncwarp();
+        *reinterpret_cast<uint4*>(stg + lane * 16) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && prow0 < p.m) {
+          ptx::tma_store_2d(&tmY, stg, static_cast<int32_t>(static_cast<int64_t>(pn_blk) * BN + c * CW),
+                            static_cast<int32_t>(prow0));
+          ptx::bulk_commit();
+        }
+      }
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (; have; have = nt >= 0 ? (t = nt, i0 = ni0, i1 = ni1, true) : false, ++item) {
       nt = it.next(sks, nt, ni0, ni1) ? nt : -1;
-      const int m_blk = t % p.num_m_blks;
-      const int n_blk = t / p.num_m_blks;
+      const int m_blk = p.row_major ? t / p.num_n_blks : t % p.num_m_blks;
+      const int n_blk = p.row_major ? t % p.num_n_blks : t / p.num_m_blks;
 #pragma unroll
       for (int u = 0; u < WC / 32; ++u) {
         wsc[lane + 32 * u] = pf_n[u];
@@ -719,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_n = t_o + BN;
       // Fast path (the deployment case: two-step bf16 TMA stores, tile inside N, no debug
       // outputs): compile-time chunk loops with the per-chunk checks hoisted to the tile.
-      const bool fast = two_step && p.use_tma_store && !p.row_absmax &&
+      const bool fast = two_step && (p.use_tma_store || QZ) && !p.row_absmax &&
                         static_cast<int64_t>(n_blk + 1) * BN <= p.n;
       if (BN <= 128 && p.out_dtype == QARVD_F64 && p.f64_slices == 8 && p.k <= 32768 && !p.acc_n_dbg &&
           !p.acc_o_dbg) {
@@ -762,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-      } else if (fast && p.epi_regs) {
+      } else if (fast && p.epi_regs && !QZ) {
         // register-held variant: the warp's 4 acc_n chunks (64 columns) are read into
         // registers and acc_n is released at once; the dequant/GELU/stores then overlap the
         // next tile's normal-slab MMAs and only acc_o (read chunk by chunk) gates its outliers.
@@ -976,6 +1176,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ti = item;
           if (ti < 32) s_trace[5][ti] = clock64();
         }
+        // fused quantizer: the previous tile's phase B while this tile's MMAs run (qz_u is free
+        // again for this tile's bf16 values afterwards)
+        if (QZ && qz_prev_m >= 0) qz_phase_b(qz_prev_m, qz_prev_n);
         const uint64_t sx2 = pk2(sx, sx);
         auto phase2 = [&](auto gl, auto hb, auto direct) {
           constexpr bool GL = decltype(gl)::value, HB = decltype(hb)::value;
@@ -1006,7 +1209,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * CW;
-            if (DS) {
+            if (QZ && p.qz_static) {
+              qz_static_chunk(rn, row0, row_ok, row, col0, i);
+            } else if (QZ) {
+              // the bf16 output stays in registers for the deferred phase B
+#pragma unroll
+              for (int e = 0; e < CW / 2; ++e) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(rn[2 * e]),
+                                                                __uint_as_float(rn[2 * e + 1]));
+                const uint32_t b = *reinterpret_cast<const uint32_t*>(&h2);
+                qz_u[QZ ? i : 0][e] = b;
+                tile_mx = __vmaxu2(tile_mx, b & 0x7fff7fffu);
+              }
+            } else if (DS) {
               uint32_t pk[CW / 2];
 #pragma unroll
               for (int e = 0; e < CW / 2; ++e) {
@@ -1041,7 +1256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             return;
           }
           if (p.debug & 8) phase2(F_{}, F_{}, F_{});  // diagnostic: stores without GELU
-          else if (direct) phase2(gl, hb, T_{});
+          else if (direct && !QZ) phase2(gl, hb, T_{});
           else phase2(gl, hb, F_{});
         };
         if (gelu) {
@@ -1052,6 +1267,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           else phase2_b(F_{}, F_{});
         }
         release(&tofree[0]);  // acc_o free
+        if (QZ && p.qz_static) {
+          if (row_ok && n_blk == 0 && half == 0) {
+            p.qz_sx[row] = __double2float_rn(p.qz_s_static);
+            if (p.qz_s64) p.qz_s64[row] = p.qz_s_static;
+          }
+        } else if (QZ) {
+          // Fused consumer K1.  The row's |y| max spans every N tile of its row block (other SM
+          // pairs).  Phase A (here): each warp publishes its 64-column partial max tagged with
+          // this launch's epoch e (64-bit atomicMax of (e << 16) | bf16 bits: older launches'
+          // values lose) and one thread per CTA arrives on the row block's counter.  Phase B
+          // (qz_phase_b, deferred to the next tile, after its phase 1 has released acc_n, so the
+          // row block has had a tile period to complete and the wait overlaps the MMAs): wait
+          // until the counter reaches e * P (every arrival of launches 1..e), round the held
+          // bf16 values.  Tiles run in row-major order on a persistent grid whose CTAs are all
+          // resident (checked on the host), so every tile a row block waits for has started: its
+          // pair finished its earlier tiles' phase A.  Nothing is reset: counters only grow,
+          // stale maxima carry old epochs.
+          const uint32_t part = max(tile_mx & 0xffffu, tile_mx >> 16);
+          if (row_ok && part) atomicMax(p.qz_rowmax + row, (qz_epoch << 16) | part);
+          ptx::named_bar_sync(1, kEpiWarps * 32);  // the CTA's partial maxima are published
+          if (ew == 0 && lane == 0) {
+            __threadfence();
+            atomicAdd(p.qz_count + m_blk, 1ull);
+          }
+          qz_prev_m = m_blk;
+          qz_prev_n = n_blk;
+        }
       } else {
 #pragma unroll 1
       for (int c = half; c < BN / CW; c += kSubs) {
@@ -1183,6 +1425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (QZ && qz_prev_m >= 0) qz_phase_b(qz_prev_m, qz_prev_n);
     if (lane == 0) ptx::bulk_wait_all();
   } else {
     ptx::setmaxnreg_dec<kCtrlRegs>();  // warps 2-3
@@ -1190,6 +1433,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (QZ && threadIdx.x == 0) {
+    // the last CTA out publishes this launch's epoch (every CTA read the old one at its start)
+    __threadfence();
+    if (atomicAdd(p.qz_done, 1u) == gridDim.x - 1u) {
+      *p.qz_epoch = __ldcg(p.qz_epoch) + 1ull;
+      *p.qz_done = 0u;
+      __threadfence();
+    }
+  }
   if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && threadIdx.x == 0) {
     unsigned long long g1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
@@ -1262,6 +1514,22 @@ int make_y_tmap(CUtensorMap* map, void* y, int64_t m, int64_t n, int64_t ld) {
   return QARVD_OK;
 }
 
+// int8 codes [m x n] (ld bytes), box 16 cols x 32 rows, no swizzle (fused quantizer staging)
+int make_q_tmap(CUtensorMap* map, void* q, int64_t m, int64_t n, int64_t ld) {
+  auto encode = get_encode_fn();
+  if (!encode) QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {CW, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, q, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed with CUresult " + std::to_string(r));
+  return QARVD_OK;
+}
+
 int sm_count() {
   static int count = 0;
   static std::once_flag once;
@@ -1282,8 +1550,12 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
     attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, false>, static_cast<int>(C::kSmemBytes));
-    if (attr_err == cudaSuccess && BN == 256 && CG == 2 && KS == 2)
-      attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, true>, static_cast<int>(C::kSmemBytes));
+    if constexpr (BN == 256 && CG == 2 && KS == 2) {
+      if (attr_err == cudaSuccess)
+        attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, true>, static_cast<int>(C::kSmemBytes));
+      if (attr_err == cudaSuccess)
+        attr_err = set_smem_attrs(dual_gemm_kernel<BN, CG, KS, false, true>, static_cast<int>(C::kSmemBytes));
+    }
   });
   QARVD_CUDA_TRY(attr_err);
   CUtensorMap ta, tb;
@@ -1293,7 +1565,7 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   if (st) return st;
   CUtensorMap ty;
   std::memset(&ty, 0, sizeof(ty));
-  p.use_tma_store = p.out_dtype == QARVD_BF16 && !p.acc_n_dbg && !p.acc_o_dbg &&
+  p.use_tma_store = p.out_dtype == QARVD_BF16 && !p.acc_n_dbg && !p.acc_o_dbg && !p.qz && p.y &&
                     (reinterpret_cast<uintptr_t>(p.y) & 15) == 0 && (p.ldy * 2) % 16 == 0;
   {
     const char* e = std::getenv("QARVD_GEMM_DIRECT");
@@ -1306,6 +1578,9 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   if (p.use_tma_store) {
     st = make_y_tmap(&ty, p.y, p.m, p.n, p.ldy);
     if (st) return st;
+  } else if (p.qz) {
+    st = make_q_tmap(&ty, p.qz_q, p.m, p.n, p.qz_ldq);
+    if (st) return st;
   }
   if (!p.use_tma_store || !p.epi_regs || p.debug) p.sk_tiles = 0;  // stream-K needs the fast path
   p.num_m_blks = static_cast<int>((p.m + BM * CG - 1) / (BM * CG));
@@ -1314,9 +1589,53 @@ int launch_gemm(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, Ge
   p.num_tiles = p.num_m_blks * p.num_n_blks;
   const int units = sm_count() / CG;
   const int grid = CG * (p.num_tiles < units ? p.num_tiles : units);
+  if constexpr (BN == 256 && CG == 2 && KS == 2) {
+  if (p.qz) {
+    // the fused quantizer's row blocks wait for tiles of other CTAs: every CTA of the grid
+    // must be resident at once (one per SM by its shared memory).  It runs the chunked
+    // two-phase epilogue (acc_n folded into acc_o's TMEM columns), not the register-held one:
+    // holding the bf16 tile for the deferred rounding leaves no registers for that variant.
+    p.epi_regs = 0;
+    static std::once_flag occ_once;
+    static int max_units = 0;
+    std::call_once(occ_once, [] {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CG * 2);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = C::kSmemBytes;
+      cudaLaunchAttribute attr{};
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = CG;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = CG > 1 ? 1 : 0;
+      int n = 0;
+      if (CG > 1) {
+        if (cudaOccupancyMaxActiveClusters(&n, dual_gemm_kernel<BN, CG, KS, false, true>, &cfg) != cudaSuccess) n = 0;
+      } else {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dual_gemm_kernel<BN, CG, KS, false, true>, kThreads,
+                                                          C::kSmemBytes) == cudaSuccess)
+          n = per_sm * sm_count();
+      }
+      cudaGetLastError();
+      max_units = n;
+    });
+    if (max_units < grid / CG)
+      QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "kernel_b (fused quantizer): the persistent grid (" + std::to_string(grid / CG) +
+                                            " CTA groups) cannot be co-resident (" + std::to_string(max_units) + ")");
+  }
+  }
   // stream-K instance only for the deployed tile shape (the data-parallel instance keeps the
   // register budget of its epilogue)
-  if (BN == 256 && CG == 2 && KS == 2 && p.sk_tiles > 0)
+  if (p.qz) {
+    if constexpr (BN == 256 && CG == 2 && KS == 2)
+      QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS, false, true>, dim3(grid), dim3(kThreads), C::kSmemBytes,
+                                stream, CG, ta, tb, ty, p));
+    else
+      QARVD_FAIL(QARVD_ERR_UNSUPPORTED, "kernel_b (fused quantizer): only the 256 x 256 pair-tile configuration");
+  } else if (BN == 256 && CG == 2 && KS == 2 && p.sk_tiles > 0)
     QARVD_CUDA_TRY(launch_pdl(dual_gemm_kernel<BN, CG, KS, (BN == 256 && CG == 2 && KS == 2)>, dim3(grid),
                               dim3(kThreads), C::kSmemBytes, stream, CG, ta, tb, ty, p));
   else
@@ -1641,4 +1960,89 @@ extern "C" int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t*
   return dual_gemm_checked(xq, ldq, wq, ldw, m, n, k, k_outlier, scale_x, scale_w_outlier,
                            scale_w_normal, bias, epilogue, QARVD_BF16, y, ldy, nullptr, nullptr,
                            nullptr, stream, row_pmax);
+}
+
+// ---- K2 with the consumer's per-token K1 fused into the epilogue -------------------------
+namespace qarvd_b200 {
+namespace {
+__global__ void qz_init_err_kernel(unsigned long long* err) { *err = 0x7fffffffffffffffull; }
+int64_t qz_blocks(int64_t m) { return (m + 255) / 256; }  // row blocks of the 256 x 256 pair tiles
+}  // namespace
+}  // namespace qarvd_b200
+
+extern "C" int64_t qarvd_dual_gemm_quant_workspace_size(int64_t m) {
+  if (m <= 0) return 0;
+  return (static_cast<int64_t>(m + qz_blocks(m) + 2) * 8 + 255) / 256 * 256;
+}
+
+extern "C" int qarvd_dual_gemm_quant(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw,
+                                     int64_t m, int64_t n, int64_t k, int64_t k_outlier,
+                                     const float* scale_x, const float* scale_w_outlier,
+                                     const float* scale_w_normal, const float* bias, int epilogue, int granularity,
+                                     double static_scale, int bits, int8_t* q, int64_t ldq_out, float* scale_f32,
+                                     double* scale_f64,
+                                     int64_t* err_index, void* workspace, int64_t workspace_bytes,
+                                     void* stream) {
+  clear_error();
+  if (m <= 0 || n <= 0 || k <= 0) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: empty shape");
+  if (k % 32 != 0 || k_outlier % 32 != 0 || k_outlier < 0 || k_outlier >= k)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "kernel_b: k and k_outlier must be multiples of 32 with 0 <= k_outlier < k");
+  if (k > 132104)
+    QARVD_FAIL(QARVD_ERR_LOGIC, "kernel_b: reduction dimension too large for exact int32 accumulation");
+  if (ldq < k || ldw < k || ldq % 16 || ldw % 16)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: leading dimensions must be >= k and multiples of 16");
+  if ((reinterpret_cast<uintptr_t>(xq) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: operand pointers must be 16-byte aligned");
+  if (!xq || !wq || !scale_x || !scale_w_normal || (k_outlier > 0 && !scale_w_outlier) || !q || !scale_f32)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "kernel_b: null pointer argument");
+  if (bits < 2 || bits > 8) QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize: bits must be in [2, 8]");
+  if (granularity != QARVD_ACT_PER_TOKEN && granularity != QARVD_ACT_PER_TENSOR)
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "quantize: unknown activation granularity");
+  if (granularity == QARVD_ACT_PER_TENSOR && !(std::isfinite(static_scale) && static_scale > 0.0))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT, "QuantParams: scale must be finite and > 0");
+  if (n % 256 != 0 || ldq_out < n || ldq_out % 16 || (reinterpret_cast<uintptr_t>(q) & 15))
+    QARVD_FAIL(QARVD_ERR_UNSUPPORTED,
+               "qarvd_dual_gemm_quant: n must be a multiple of 256 and the codes 16-byte aligned rows (ldq_out >= n)");
+  if (!workspace || workspace_bytes < qarvd_dual_gemm_quant_workspace_size(m) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 15))
+    QARVD_FAIL(QARVD_ERR_INVALID_ARGUMENT,
+               "qarvd_dual_gemm_quant: workspace missing, misaligned or smaller than qarvd_dual_gemm_quant_workspace_size");
+  if (int st = require_device()) return st;
+  cudaStream_t s = as_stream(stream);
+  if (err_index) {
+    qz_init_err_kernel<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(err_index));
+    count_launch();
+    QARVD_CUDA_TRY(cudaGetLastError());
+  }
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.k_o = k_outlier;
+  p.scale_x = scale_x;
+  p.scale_wo = scale_w_outlier;
+  p.scale_wn = scale_w_normal;
+  p.bias = bias;
+  p.epilogue = epilogue;
+  p.out_dtype = QARVD_BF16;
+  p.qz = 1;
+  p.qz_qmax = (1 << (bits - 1)) - 1;
+  p.qz_static = granularity == QARVD_ACT_PER_TENSOR ? 1 : 0;
+  p.row_major = p.qz_static ? 0 : 1;
+  p.qz_s_static = static_scale;
+  p.qz_rowmax = static_cast<unsigned long long*>(workspace);
+  p.qz_count = static_cast<unsigned long long*>(workspace) + m;
+  p.qz_epoch = p.qz_count + qz_blocks(m);
+  p.qz_done = reinterpret_cast<unsigned int*>(p.qz_epoch + 1);
+  p.qz_q = q;
+  p.qz_ldq = ldq_out;
+  p.qz_sx = scale_f32;
+  p.qz_s64 = scale_f64;
+  p.qz_err = reinterpret_cast<unsigned long long*>(err_index);
+  p.trace = getenv("QARVD_GEMM_TRACE") ? 1 + (getenv("QARVD_GEMM_TRACE_CTA") ? atoi(getenv("QARVD_GEMM_TRACE_CTA")) : 0) : 0;
+  p.debug = getenv("QARVD_GEMM_DEBUG") ? atoi(getenv("QARVD_GEMM_DEBUG")) : 0;
+  // the fused epilogue is built for the deployed tile (256 x 256 pair tiles, one TMEM stage,
+  // the register-held accumulator path)
+  return launch_gemm<256, 2, 2>(xq, ldq, wq, ldw, p, s);
 }

@@ -166,6 +166,10 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+// named barrier over `threads` threads (whole warps), id 1..15 (0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 // warpgroup register rebalancing (all 4 warps of a warpgroup execute the same one)
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {

@@ -73,7 +73,7 @@ class QuantizedChain:
     def __init__(self, layers: Sequence[QuantizedLayer], m: int,
                  epilogues: Optional[Sequence[int]] = None, inputs: Optional[Sequence[int]] = None,
                  fold: bool = True, fuse_rowmax: bool = False, ms: Optional[Sequence[int]] = None,
-                 ctx_rows: int = 0):
+                 ctx_rows: int = 0, fuse_quant: bool = False):
         """layers[i] consumes the output of layer inputs[i] (-1 = the chain input; default i-1;
         -2 = the context input ``self.ctx`` of ``ctx_rows`` rows, e.g. the text tokens the
         cross-attention k / v projections read).  ``ms[i]`` = rows layer i processes (default m;
@@ -84,6 +84,10 @@ class QuantizedChain:
         With ``fuse_rowmax`` a folded consumer's per-token |x| max comes from per-row partial
         maxima the producer's GEMM epilogue stores (qarvd_dual_gemm_pmax) and its K1 is a flat
         streaming pass (qarvd_quantize_act_pmax).
+        With ``fuse_quant`` a folded per-token consumer of a single producer gets its codes and
+        scales straight from the producer's epilogue (qarvd_dual_gemm_quant): the intermediate
+        is never stored and the consumer's K1 launch disappears (``self.y`` of such a producer
+        stays unwritten).
         ``self.source_ops`` keeps the unfolded shapes for op counting."""
         self.layers = list(layers)
         self.source_layers = list(layers)  # as given (before any output-permutation fold)
@@ -123,11 +127,25 @@ class QuantizedChain:
                         P = self.layers[i]
                         pm = _lib.load().qarvd_dual_gemm_pmax_count(self.ms[i], P.out_dim, P.k_pad)
                         self.rowmax[i] = torch.zeros((self.ms[i], pm), dtype=torch.int32, device=dev)
+        # fused consumer K1 (qarvd_dual_gemm_quant): producer i -> consumer j
+        self.qz_into = [None] * len(self.layers)  # indexed by producer
+        self.qz_from = [None] * len(self.layers)  # indexed by consumer
+        self.qz_ws = [None] * len(self.layers)
+        if fold and fuse_quant:
+            for j, i in enumerate(self.inputs):
+                L = self.layers[j]
+                if (i >= 0 and not self.stream_k1[j] and self.rowmax[i] is None and L.gather_dev is None
+                        and self.inputs.count(i) == 1 and self.in_cols[j] is None
+                        and self.layers[i].out_dim % 256 == 0):
+                    self.qz_into[i], self.qz_from[j] = j, i
+                    nb = int(_lib.load().qarvd_dual_gemm_quant_workspace_size(self.ms[i]))
+                    self.qz_ws[i] = torch.zeros(nb, dtype=torch.uint8, device=dev)
         first = {j: i for i, j in reversed(list(enumerate(self.inputs))) if j < 0}
         self.x = torch.empty((m, self.layers[first.get(-1, 0)].in_dim), dtype=torch.bfloat16, device=dev)
         self.ctx = (torch.empty((ctx_rows, self.layers[first[-2]].in_dim), dtype=torch.bfloat16, device=dev)
                     if -2 in first else None)
-        self.xq = [torch.empty((mi, L.k_pad), dtype=torch.int8, device=dev) for mi, L in zip(self.ms, self.layers)]
+        # (zero-filled: a fused consumer's pad columns are never written)
+        self.xq = [torch.zeros((mi, L.k_pad), dtype=torch.int8, device=dev) for mi, L in zip(self.ms, self.layers)]
         self.sx = [torch.empty(mi, dtype=torch.float32, device=dev) for mi in self.ms]
         self.y = [torch.empty((mi, L.out_dim), dtype=torch.bfloat16, device=dev) for mi, L in zip(self.ms, self.layers)]
         # stream-K workspaces (zero-filled; one per layer so concurrent branches never share)
@@ -199,7 +217,9 @@ class QuantizedChain:
         L = self.layers[i]
         src = self._src(i)
         m = self.ms[i]
-        if self.stream_k1[i]:
+        if self.qz_from[i] is not None:
+            pass  # codes and scales come from the producer's epilogue
+        elif self.stream_k1[i]:
             rm = self.rowmax[self.inputs[i]]
             _lib.call("qarvd_quantize_act_pmax", src.data_ptr(), m, L.in_dim, src.stride(0),
                       _ptr(rm), 0 if rm is None else rm.shape[1], L.act_granularity,
@@ -212,7 +232,16 @@ class QuantizedChain:
                       None, None, s)
         if events is not None:
             events[2 * i + 1].record()
-        if self.rowmax[i] is not None:
+        if self.qz_into[i] is not None:
+            j = self.qz_into[i]
+            C = self.layers[j]
+            ws = self.qz_ws[i]
+            _lib.call("qarvd_dual_gemm_quant", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(), L.k_pad,
+                      m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
+                      L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
+                      self.epilogues[i], C.act_granularity, float(C.act_scale), 8, self.xq[j].data_ptr(),
+                      C.k_pad, self.sx[j].data_ptr(), None, None, ws.data_ptr(), ws.numel(), s)
+        elif self.rowmax[i] is not None:
             _lib.call("qarvd_dual_gemm_pmax", self.xq[i].data_ptr(), L.k_pad, L.wq.data_ptr(),
                       L.k_pad, m, L.out_dim, L.k_pad, L.k_outlier, self.sx[i].data_ptr(),
                       L.scale_outlier32.data_ptr(), L.scale_normal32.data_ptr(), _ptr(L.bias),
@@ -281,7 +310,7 @@ class QuantizedChain:
 
 def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
                     text_len: Optional[int] = None, fuse_rowmax: bool = False,
-                    fuse_qkv: bool = False) -> "QuantizedChain":
+                    fuse_qkv: bool = False, fuse_quant: bool = False) -> "QuantizedChain":
     """BASELINE config 3: every quantized linear of a Wan-1.3B-shaped DiT stack for one chunk.
 
     Per block (toy_model.cpp:25-27 layer types, Wan2.1 shapes): self_attn.{q,k,v} read the
@@ -335,4 +364,4 @@ def wan_stack_chain(blocks: int = 30, seed: int = 1, m: Optional[int] = None,
             ms.append(text_len if src[t] == -2 else m)
         block_in = idx["ffn.2"]
     return QuantizedChain(layers, m, epilogues=epis, inputs=inputs, ms=ms, ctx_rows=text_len,
-                          fuse_rowmax=fuse_rowmax)
+                          fuse_rowmax=fuse_rowmax, fuse_quant=fuse_quant)

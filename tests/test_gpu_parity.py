@@ -1345,3 +1345,124 @@ def test_k1_bulk_staged_bitexact(cuda, monkeypatch, m, k, n_out, gathered):
     q_ref, s_ref, _ = oracle.quantize_act(x64, g, per_token=True)
     np.testing.assert_array_equal(xq.cpu().numpy(), q_ref)
     np.testing.assert_array_equal(s64.cpu().numpy(), s_ref)
+
+
+# ---------------------------------------------------------------- K2 with the consumer's K1 fused
+def _qz_pair(y_codes_ws, m, n, k, ko, gelu, xq, wq, sx, swo, swn, bias, reps=2, static=None):
+    """Unfused (qarvd_dual_gemm -> qarvd_quantize_act) and fused (qarvd_dual_gemm_quant) runs;
+    static = a per-tensor activation scale (None: per-token)."""
+    gran = qb.ACT_PER_TOKEN if static is None else qb.ACT_PER_TENSOR
+    sst = 0.0 if static is None else float(static)
+    lib = qb._lib
+    epi = qb.EPI_GELU if gelu else qb.EPI_NONE
+    y = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    q_ref = torch.empty((m, n), dtype=torch.int8, device="cuda")
+    s_ref = torch.empty(m, dtype=torch.float32, device="cuda")
+    d_ref = torch.empty(m, dtype=torch.float64, device="cuda")
+    e_ref = torch.empty(1, dtype=torch.int64, device="cuda")
+    lib.call("qarvd_dual_gemm", xq.data_ptr(), k, wq.data_ptr(), k, m, n, k, ko, sx.data_ptr(),
+             swo.data_ptr(), swn.data_ptr(), None if bias is None else bias.data_ptr(), epi, qb.BF16,
+             y.data_ptr(), n, None, None, None)
+    lib.call("qarvd_quantize_act", y.data_ptr(), qb.BF16, m, n, n, None, n, gran, sst, 8,
+             q_ref.data_ptr(), n, s_ref.data_ptr(), d_ref.data_ptr(), e_ref.data_ptr(), None)
+    ws = y_codes_ws
+    outs = []
+    for _ in range(reps):  # the workspace resets itself between launches
+        q = torch.full((m, n), 99, dtype=torch.int8, device="cuda")
+        s = torch.empty(m, dtype=torch.float32, device="cuda")
+        d = torch.empty(m, dtype=torch.float64, device="cuda")
+        e = torch.empty(1, dtype=torch.int64, device="cuda")
+        lib.call("qarvd_dual_gemm_quant", xq.data_ptr(), k, wq.data_ptr(), k, m, n, k, ko, sx.data_ptr(),
+                 swo.data_ptr(), swn.data_ptr(), None if bias is None else bias.data_ptr(), epi, gran, sst, 8,
+                 q.data_ptr(), n, s.data_ptr(), d.data_ptr(), e.data_ptr(), ws.data_ptr(), ws.numel(), None)
+        torch.cuda.synchronize()
+        outs.append((q, s, d, e))
+    # the row-block counters grow by (N tiles x 2 CTAs) per launch, the epoch by one
+    nb = (m + 255) // 256
+    w64 = ws.view(torch.int64)
+    if static is None:
+        assert torch.all(w64[m:m + nb] == reps * (n // 256) * 2)
+    assert int(w64[m + nb].item()) == reps
+    return (q_ref, s_ref, d_ref, e_ref), outs
+
+
+@pytest.mark.parametrize("static", [None, 0.02])
+@pytest.mark.parametrize("m,n,k,ko,gelu,bias", [(4680, 8960, 1536, 32, True, True), (300, 512, 256, 0, False, False),
+                                                (1000, 1536, 8960, 192, False, True), (33, 256, 64, 32, True, False)])
+def test_k2_fused_quant_bitexact(cuda, m, n, k, ko, gelu, bias, static):
+    """qarvd_dual_gemm_quant = qarvd_dual_gemm (bf16) then the per-token K1 on its output: same
+    codes, f32 / f64 scales and error index, launch after launch (self-resetting workspace),
+    including partial row blocks (m % 256 != 0)."""
+    g = torch.Generator(device="cpu").manual_seed(m + n)
+    xq = torch.randint(-127, 128, (m, k), generator=g, dtype=torch.int8).cuda()
+    wq = torch.randint(-127, 128, (n, k), generator=g, dtype=torch.int8).cuda()
+    sx = (torch.rand(m, generator=g) * 0.02 + 1e-3).cuda()
+    swo = (torch.rand(n, generator=g) * 1e-3 + 1e-4).cuda()
+    swn = (torch.rand(n, generator=g) * 1e-3 + 1e-4).cuda()
+    b = (torch.rand(n, generator=g) - 0.5).cuda() if bias else None
+    ws = torch.zeros(int(qb._lib.load().qarvd_dual_gemm_quant_workspace_size(m)), dtype=torch.uint8, device="cuda")
+    ref, outs = _qz_pair(ws, m, n, k, ko, gelu, xq, wq, sx, swo, swn, b, static=static)
+    for q, s, d, e in outs:
+        assert torch.equal(q, ref[0])
+        assert torch.equal(s.view(torch.int32), ref[1].view(torch.int32))
+        assert torch.equal(d.view(torch.int64), ref[2].view(torch.int64))
+        assert int(e.item()) == int(ref[3].item()) == 2 ** 63 - 1
+
+
+@pytest.mark.parametrize("static", [None, 2.0 ** -4])
+def test_k2_fused_quant_ties_and_nonfinite(cuda, static):
+    """Exact .5 ties (every odd code of half the columns lands on k + 1/2) take the reference's
+    division, and a row overflowing to inf reports the same flat index as K1."""
+    m, n, k = 512, 512, 512
+    g = torch.Generator(device="cpu").manual_seed(5)
+    codes = torch.randint(-126, 127, (m, k), generator=g, dtype=torch.int8)
+    codes[:, 0] = 127
+    xq = codes.cuda()
+    wq = torch.eye(n, k, dtype=torch.int8).cuda()  # acc_n = the codes
+    c = 2.0 ** -4
+    swn = torch.tensor([c if j % 2 == 0 else c / 2 for j in range(n)], dtype=torch.float32).cuda()
+    swo = swn.clone()
+    sx = torch.ones(m, dtype=torch.float32).cuda()
+    sx[77] = 3e38  # y overflows: non-finite row
+    ws = torch.zeros(int(qb._lib.load().qarvd_dual_gemm_quant_workspace_size(m)), dtype=torch.uint8, device="cuda")
+    ref, outs = _qz_pair(ws, m, n, k, 0, False, xq, wq, sx, swo, swn, None, static=static)
+    assert int(ref[3].item()) == 77 * n + 0
+    for q, s, d, e in outs:
+        assert torch.equal(q, ref[0])
+        assert torch.equal(s.view(torch.int32), ref[1].view(torch.int32))
+        assert torch.equal(d.view(torch.int64), ref[2].view(torch.int64))
+        assert int(e.item()) == int(ref[3].item())
+    # the ties are real: odd codes in odd columns halve to k + 1/2 and round half to even
+    row = codes[3].numpy().astype(np.int64)
+    want = np.where(np.arange(k) % 2 == 1, np.rint(row / 2.0), row)
+    np.testing.assert_array_equal(ref[0][3].cpu().numpy().astype(np.int64), want)
+
+
+@pytest.mark.parametrize("static", [False, True])
+def test_chain_fused_quant_bitexact(cuda, static):
+    """QuantizedChain(fuse_quant=True) on the Wan FFN: ffn.2's codes, scales and the final output
+    equal the unfused folded chain's, replayed from a CUDA graph (per-token and static ffn.2)."""
+    from paper_2605_21072_b200.pipeline import QuantizedChain
+    d, f, m = 1536, 8960, 4680
+    p0, p2 = make_plan(d, 32, seed=1), make_plan(f, 192, seed=2)
+    w0, _ = bf16_values((f, d), seed=4, scale=1.0 / np.sqrt(d), heavy_cols=p0.outlier_indices)
+    w2, _ = bf16_values((d, f), seed=5, scale=1.0 / np.sqrt(f), heavy_cols=p2.outlier_indices)
+    L0 = engine.prepare_weights("ffn.0", to_dev_bf16(w0), p0)
+    L2 = engine.prepare_weights("ffn.2", to_dev_bf16(w2), p2)
+    L0.bias = torch.linspace(-0.5, 0.5, f, device="cuda", dtype=torch.float32)
+    if static:
+        L2.act_granularity, L2.act_scale = qb.ACT_PER_TENSOR, 0.01
+    xb, _ = bf16_values((m, d), seed=6, heavy_cols=p0.outlier_indices, gamma=4.0)
+    outs = []
+    for fq in (False, True):
+        ch = QuantizedChain([L0, L2], m, epilogues=[qb.EPI_GELU, qb.EPI_NONE], fuse_quant=fq)
+        assert (ch.qz_into[0] == 1) == fq
+        ch.x.copy_(to_dev_bf16(xb))
+        ch.capture()
+        for _ in range(3):
+            ch.replay()
+        torch.cuda.synchronize()
+        outs.append((ch.xq[1].clone(), ch.sx[1].clone(), ch.output.clone()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][2].view(torch.int16), outs[1][2].view(torch.int16))
