@@ -489,8 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     SkIter<SKT> it(sks, cta_id);
     int t, i0, i1;
     while (it.next(sks, t, i0, i1)) {
-      const int m_blk = p.row_major ? t / p.num_n_blks : t % p.num_m_blks;
-      const int n_blk = p.row_major ? t % p.num_n_blks : t / p.num_m_blks;
+      const int m_blk = (QZ && p.row_major) ? t / p.num_n_blks : t % p.num_m_blks;
+      const int n_blk = (QZ && p.row_major) ? t % p.num_n_blks : t / p.num_m_blks;
       const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
       const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / CG);
       for (int i = i0; i < i1; ++i) {
@@ -691,14 +691,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < WC / 32; ++u) {
         const int jl = lane + 32 * u;
-        const int64_t j = static_cast<int64_t>(p.row_major ? tt % p.num_n_blks : tt / p.num_m_blks) * BN +
+        const int64_t j = static_cast<int64_t>((QZ && p.row_major) ? tt % p.num_n_blks : tt / p.num_m_blks) * BN +
                           (half + (jl / CW) * kSubs) * CW + jl % CW;
         const int64_t jc = j < p.n ? j : p.n - 1;
         pf_n[u] = __ldg(p.scale_wn + jc);
         if (has_outlier) pf_o[u] = __ldg(p.scale_wo + jc);
         if (p.bias) pf_b[u] = __ldg(p.bias + jc);
       }
-      const int64_t r = static_cast<int64_t>(p.row_major ? tt / p.num_n_blks : tt % p.num_m_blks) * TM +
+      const int64_t r = static_cast<int64_t>((QZ && p.row_major) ? tt / p.num_n_blks : tt % p.num_m_blks) * TM +
                         rank * BM + q * 32 + lane;
       pf_x = (r < p.m && p.scale_x) ? __ldg(p.scale_x + r) : 0.f;
     };
@@ -895,8 +895,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (; have; have = nt >= 0 ? (t = nt, i0 = ni0, i1 = ni1, true) : false, ++item) {
       nt = it.next(sks, nt, ni0, ni1) ? nt : -1;
-      const int m_blk = p.row_major ? t / p.num_n_blks : t % p.num_m_blks;
-      const int n_blk = p.row_major ? t % p.num_n_blks : t / p.num_m_blks;
+      const int m_blk = (QZ && p.row_major) ? t / p.num_n_blks : t % p.num_m_blks;
+      const int n_blk = (QZ && p.row_major) ? t % p.num_n_blks : t / p.num_m_blks;
 #pragma unroll
       for (int u = 0; u < WC / 32; ++u) {
         wsc[lane + 32 * u] = pf_n[u];
