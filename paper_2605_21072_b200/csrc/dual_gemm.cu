@@ -152,6 +152,7 @@ struct GemmParams {
   // order): the bf16 output is quantized per token in the epilogue instead of being stored.
   // qz_rowmax [m]: (launch epoch << 16) | row |y| max as sign-cleared bf16 bits; qz_count
   // [num_m_blks]: arrivals per row block, growing across launches (zero-filled once).
+  unsigned long long* cta_times;  // QARVD_GEMM_DEBUG=128: per-CTA start / end globaltimer
   int row_major;  // tile order: all N tiles of a row block consecutive (the per-token fused quantizer)
   int qz;
   int qz_qmax;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ long long s_trace[6][32];  // QARVD_GEMM_TRACE: per-tile clocks of CTA 0
   __shared__ long long s_clk0;
   __shared__ unsigned long long s_g0;
-  if (p.trace && threadIdx.x == 0) {
+  if ((p.trace || (p.debug & 128)) && threadIdx.x == 0) {
     s_clk0 = clock64();
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_g0));
   }
@@ -1457,6 +1458,13 @@ __global__ void __launch_bounds__(kThreads, 1)
              s_trace[0][i] - t0, s_trace[1][i] - t0, s_trace[2][i] - t0, s_trace[3][i] - t0,
              s_trace[5][i] - t0, s_trace[4][i] - t0);
   }
+  if ((p.debug & 128) && threadIdx.x == 0 && p.cta_times) {
+    // diagnostic (QARVD_GEMM_DEBUG=128): per-CTA start / end globaltimer (ns)
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    p.cta_times[2 * blockIdx.x] = s_g0;
+    p.cta_times[2 * blockIdx.x + 1] = g1;
+  }
   if (CG == 2) ptx::cluster_sync();  // the leader's MMAs wrote this CTA's TMEM / read its smem
   if (warp == 2) {
     ptx::tc_fence_after();
@@ -1528,6 +1536,16 @@ int make_q_tmap(CUtensorMap* map, void* q, int64_t m, int64_t n, int64_t ld) {
   if (r != CUDA_SUCCESS)
     QARVD_FAIL(QARVD_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed with CUresult " + std::to_string(r));
   return QARVD_OK;
+}
+
+// QARVD_GEMM_DEBUG=128 diagnostic buffer (2 x 1024 globaltimer stamps), read by qarvd_debug_cta_times
+unsigned long long* debug_cta_times() {
+  static unsigned long long* buf = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&buf, 2 * 1024 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+  });
+  return buf;
 }
 
 int sm_count() {
@@ -1753,6 +1771,7 @@ int dual_gemm_launch(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ld
   p.acc_n_dbg = acc_n;
   p.debug = getenv("QARVD_GEMM_DEBUG") ? atoi(getenv("QARVD_GEMM_DEBUG")) : 0;
   p.trace = getenv("QARVD_GEMM_TRACE") ? 1 + (getenv("QARVD_GEMM_TRACE_CTA") ? atoi(getenv("QARVD_GEMM_TRACE_CTA")) : 0) : 0;
+  if (p.debug & 128) p.cta_times = debug_cta_times();
   p.epilogue = epilogue;
   p.out_dtype = out_dtype;
   TileCfg c = choose_cfg(m, n, k);
@@ -2045,4 +2064,13 @@ extern "C" int qarvd_dual_gemm_quant(const int8_t* xq, int64_t ldq, const int8_t
   // the fused epilogue is built for the deployed tile (256 x 256 pair tiles, one TMEM stage,
   // the register-held accumulator path)
   return launch_gemm<256, 2, 2>(xq, ldq, wq, ldw, p, s);
+}
+
+// diagnostic (not part of the ABI header): the per-CTA start / end globaltimer stamps of the last
+// K2 launch made with QARVD_GEMM_DEBUG=128, n CTAs -> host[2n]
+extern "C" int qarvd_debug_cta_times(unsigned long long* host, int n) {
+  unsigned long long* d = qarvd_b200::debug_cta_times();
+  if (!d || n <= 0 || n > 1024) return QARVD_ERR_INVALID_ARGUMENT;
+  return cudaMemcpy(host, d, 2 * n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? QARVD_OK
+                                                                                                      : QARVD_ERR_CUDA;
 }
