@@ -253,8 +253,9 @@ int qarvd_dual_gemm_pmax(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_
  * same non-finite reporting (flat index row * ldq_out + c).  The consumer's input channels must
  * be in this layer's output order (no gather; pipeline.fold_output_permutation does that).
  * n % 256 == 0; q rows 16-byte aligned.  workspace: device, 16-byte aligned, ZERO-FILLED once
- * before first use (it resets itself), >= qarvd_dual_gemm_quant_workspace_size(m) bytes, one
- * per concurrently running call.  QARVD_ERR_UNSUPPORTED when the persistent grid cannot be
+ * before first use, >= qarvd_dual_gemm_quant_workspace_size(m) bytes, one per concurrently
+ * running call; it needs no reset between calls (per-launch epochs, counters only grow), but a
+ * launch that fails midway leaves it invalid (zero it again).  QARVD_ERR_UNSUPPORTED when the persistent grid cannot be
  * co-resident on this device (the caller then runs qarvd_dual_gemm + qarvd_quantize_act). */
 int64_t qarvd_dual_gemm_quant_workspace_size(int64_t m);
 int qarvd_dual_gemm_quant(const int8_t* xq, int64_t ldq, const int8_t* wq, int64_t ldw, int64_t m,
