@@ -569,9 +569,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        const long long tr0 = clock64();
+        // trace clocks go straight to shared memory: a clock held in registers across the tile
+        // costs the epilogue warps two spilled 64-bit values per tile
+        const bool trc_mma = p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && item < 32 && lane == 0;
+        if (trc_mma) s_trace[0][item] = clock64();
         if (C::kAccStages == 2) ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-        const long long tr1 = clock64();
         ptx::tc_fence_after();
         const uint32_t d_o = tmem_base + static_cast<uint32_t>(acc * 2 * BN);
         const uint32_t d_n = d_o + BN;
@@ -646,10 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (CG == 1) ptx::mma_commit(&tfull[acc]);
           else ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
           const int ti = item;
-          if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && ti < 32) {
-            s_trace[0][ti] = tr0;
-            s_trace[1][ti] = clock64();
-          }
+          if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && ti < 32) s_trace[1][ti] = clock64();
         }
         ++item;
         __syncwarp();
@@ -911,9 +910,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < p.m;
       tile_mx = 0;
       __syncwarp();  // this warp's scales visible to its lanes
-      const long long te0 = clock64();
+      const bool trc_epi = p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4 &&
+                           item < 32;
+      if (trc_epi) s_trace[2][item] = clock64();
       ptx::mbar_wait(&tfull[acc], acc_phase);
-      const long long te1 = clock64();
+      if (trc_epi) s_trace[3][item] = clock64();
       ptx::tc_fence_after();
       const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
       const uint32_t t_o = tmem_base + t_lane + static_cast<uint32_t>(acc * 2 * BN);
@@ -1415,11 +1416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.row_pmax[row * p.pm_count + n_blk * kSubs + half] = max(tile_mx & 0xffffu, tile_mx >> 16);
       {
         const int ti = item;
-        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4 && ti < 32) {
-          s_trace[2][ti] = te0;
-          s_trace[3][ti] = te1;
+        if (p.trace && blockIdx.x == static_cast<unsigned>(p.trace - 1) && lane == 0 && warp == 4 && ti < 32)
           s_trace[4][ti] = clock64();
-        }
       }
       if (++acc == C::kAccStages) {
         acc = 0;
