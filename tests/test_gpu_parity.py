@@ -1466,3 +1466,46 @@ def test_chain_fused_quant_bitexact(cuda, static):
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
     assert torch.equal(outs[0][2].view(torch.int16), outs[1][2].view(torch.int16))
+
+
+@pytest.mark.parametrize("m", [1, 255, 256, 257, 511])
+def test_k2_fused_quant_row_block_edges(cuda, m):
+    """Row counts at the 256-row block edges (a single row, one short / exact / one over a block):
+    the per-token fused quantizer's row-block counting and the partial last block stay exact."""
+    n, k, ko = 512, 128, 32
+    g = torch.Generator(device="cpu").manual_seed(m)
+    xq = torch.randint(-127, 128, (m, k), generator=g, dtype=torch.int8).cuda()
+    wq = torch.randint(-127, 128, (n, k), generator=g, dtype=torch.int8).cuda()
+    sx = (torch.rand(m, generator=g) * 0.02 + 1e-3).cuda()
+    swo = (torch.rand(n, generator=g) * 1e-3 + 1e-4).cuda()
+    swn = (torch.rand(n, generator=g) * 1e-3 + 1e-4).cuda()
+    b = (torch.rand(n, generator=g) - 0.5).cuda()
+    ws = torch.zeros(int(qb._lib.load().qarvd_dual_gemm_quant_workspace_size(m)), dtype=torch.uint8, device="cuda")
+    ref, outs = _qz_pair(ws, m, n, k, ko, True, xq, wq, sx, swo, swn, b, reps=3)
+    for q, s, d, e in outs:
+        assert torch.equal(q, ref[0])
+        assert torch.equal(s.view(torch.int32), ref[1].view(torch.int32))
+        assert torch.equal(d.view(torch.int64), ref[2].view(torch.int64))
+
+
+def test_k2_fused_quant_rejects_bad_arguments(cuda):
+    """The fused entry validates like the reference: n not a multiple of 256 is outside this
+    build's envelope, a missing workspace and a bad static scale are invalid arguments."""
+    lib = qb._lib
+    m, n, k = 64, 384, 64
+    xq = torch.zeros((m, k), dtype=torch.int8, device="cuda")
+    wq = torch.zeros((n, k), dtype=torch.int8, device="cuda")
+    sx = torch.ones(m, device="cuda")
+    sw = torch.ones(n, device="cuda")
+    q = torch.empty((m, 512), dtype=torch.int8, device="cuda")
+    s = torch.empty(m, device="cuda")
+    ws = torch.zeros(int(lib.load().qarvd_dual_gemm_quant_workspace_size(m)), dtype=torch.uint8, device="cuda")
+    args = lambda nn, gran, sst, w: (xq.data_ptr(), k, wq.data_ptr(), k, m, nn, k, 0, sx.data_ptr(), sw.data_ptr(),
+                                      sw.data_ptr(), None, qb.EPI_NONE, gran, sst, 8, q.data_ptr(), 512, s.data_ptr(),
+                                      None, None, w, ws.numel(), None)
+    with pytest.raises(qb._lib.Unsupported):
+        lib.call("qarvd_dual_gemm_quant", *args(n, qb.ACT_PER_TOKEN, 0.0, ws.data_ptr()))
+    with pytest.raises(qb._lib.InvalidArgument):
+        lib.call("qarvd_dual_gemm_quant", *args(256, qb.ACT_PER_TOKEN, 0.0, None))
+    with pytest.raises(qb._lib.InvalidArgument):
+        lib.call("qarvd_dual_gemm_quant", *args(256, qb.ACT_PER_TENSOR, -1.0, ws.data_ptr()))
