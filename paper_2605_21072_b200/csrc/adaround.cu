@@ -388,8 +388,12 @@ __global__ void __launch_bounds__(256) act_codes_group_kernel(const double* __re
                                                                int8_t* __restrict__ cx, int8_t* __restrict__ bt,
                                                                int* bad) {
   __shared__ int8_t tile[64][64 + 4];
-  const double s = libm::exp(*log_sa);
-  const double rinv = 1.0 / s;
+  __shared__ double s_sr[2];  // s = exp(log s_a) and 1 / s, once per CTA (glibc exp restated)
+  if (threadIdx.x == 64) {
+    const double sv = libm::exp(*log_sa);
+    s_sr[0] = sv;
+    s_sr[1] = 1.0 / sv;
+  }
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   __shared__ const double* rowp[64];  // source row of each tile row (NULL past the group)
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(256) act_codes_group_kernel(const double* __re
     rowp[threadIdx.x] = p;
   }
   __syncthreads();
+  const double s = s_sr[0], rinv = s_sr[1];
   const double lim = static_cast<double>(qmax) + 1.0;
   const int64_t c = c0 + tx;
   const bool col_ok = c < k;
