@@ -7,13 +7,15 @@
 // already permuted [outlier | normal] along K (calibrate.cpp:474-480 for the
 // weights, K1 for the activations); TMA streams 128-byte K-slices of both into
 // a 128B-swizzled shared-memory ring, a single elected thread issues
-// tcgen05.mma.kind::i8 (M=128, N=BN, K=32) and routes every K=32 step to one of
-// two int32 tensor-memory accumulators: acc_o for k < k_outlier, acc_n after.
-// int32 is exact because |code| <= 127 and k <= 132104 (D4 in SURVEY.md).
-// Four epilogue warps read both accumulators with tcgen05.ld and apply
-//   y = s_x[i] * (s_wo[j]*acc_o + s_wn[j]*acc_n) (+ bias[j]) -> bf16.
-// Persistent, warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer,
-// warp 2 = TMEM allocator, warps 4..7 = epilogue.
+// tcgen05.mma.kind::i8 (M=128 per CTA, 256 over an SM pair with cta_group::2, N=BN, K=32) and
+// routes every K=32 step to one of two int32 tensor-memory accumulators: acc_o for
+// k < k_outlier, acc_n after.  int32 is exact because |code| <= 127 and k <= 132104 (D4 in
+// SURVEY.md).  Sixteen epilogue warps (four per TMEM lane quadrant) read both accumulators
+// with tcgen05.ld and apply
+//   y = s_x[i] * (s_wo[j]*acc_o + s_wn[j]*acc_n) (+ bias[j]) [gelu] -> bf16
+// (or f32, the reference's exact f64 epilogue, K7's slice recombination, or the next layer's
+// int8 codes: qarvd_dual_gemm_quant).  Persistent, warp-specialised: warp 0 = TMA producer,
+// warp 1 = MMA issuer, warp 2 = TMEM allocator, warps 4..19 = epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
