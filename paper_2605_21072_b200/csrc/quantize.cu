@@ -1418,12 +1418,25 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
   // the plan's gather as an int16 table, staged once per CTA (pad -> k: the zero sentinel of
   // every row copy); read through L1 per row it cost more bytes than the row itself
   int16_t* gidx = reinterpret_cast<int16_t*>(k1r_smem + kTeams * row_stride);
+  // runs[j]: the first source column of output chunk j (8 columns) when the chunk copies 8
+  // consecutive source columns (a plan keeps the normal columns in order, so almost every chunk
+  // does), else -1.  Such a chunk is gathered by two funnel shifts of three aligned words.
+  int16_t* runs = gidx + ((k_out + 7) & ~7);
   if (kGather) {
-    for (int c4 = threadIdx.x; c4 < (k_out >> 2); c4 += blockDim.x) {
-      const int4 g = __ldg(reinterpret_cast<const int4*>(gather) + c4);
-      reinterpret_cast<uint2*>(gidx)[c4] =
-          make_uint2(static_cast<uint16_t>(g.x < 0 ? k : g.x) | (static_cast<uint32_t>(g.y < 0 ? k : g.y) << 16),
-                     static_cast<uint16_t>(g.z < 0 ? k : g.z) | (static_cast<uint32_t>(g.w < 0 ? k : g.w) << 16));
+    for (int c8 = threadIdx.x; c8 < (k_out >> 3); c8 += blockDim.x) {
+      const int4 ga = __ldg(reinterpret_cast<const int4*>(gather) + 2 * c8);
+      const int4 gb = __ldg(reinterpret_cast<const int4*>(gather) + 2 * c8 + 1);
+      const int g[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+      uint32_t w[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        w[h] = static_cast<uint16_t>(g[2 * h] < 0 ? k : g[2 * h]) |
+               (static_cast<uint32_t>(g[2 * h + 1] < 0 ? k : g[2 * h + 1]) << 16);
+      reinterpret_cast<uint4*>(gidx)[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+      bool run = g[0] >= 0 && g[0] + 7 < k;
+#pragma unroll
+      for (int h = 1; h < 8; ++h) run = run && g[h] == g[0] + h;
+      runs[c8] = static_cast<int16_t>(run ? g[0] : -1);
     }
   }
   __shared__ unsigned int s_nfix;
@@ -1534,12 +1547,23 @@ __global__ void __launch_bounds__(W == 1 ? 256 : 32 * W, W == 1 ? 4 : (1152 / (3
   if (kGather) {
     __syncthreads();  // the slots hold the final codes
     if (live && !slow) {
-      // the plan's gather on the codes, 4 per lane per step
-#pragma unroll 4
-      for (int c0 = tt * 4; c0 < k_out; c0 += T * 4) {
-        const uint2 gp = *reinterpret_cast<const uint2*>(gidx + c0);
-        *reinterpret_cast<uint32_t*>(qr + c0) =
-            pack4(crow[gp.x & 0xffffu], crow[gp.x >> 16], crow[gp.y & 0xffffu], crow[gp.y >> 16]);
+      // the plan's gather on the codes, 8 per lane per step: a run chunk by two funnel shifts of
+      // three aligned words (the slot holds k + 8 bytes), the others byte by byte
+      const uint32_t* crow32 = reinterpret_cast<const uint32_t*>(crow);
+#pragma unroll 2
+      for (int c0 = tt * 8; c0 < k_out; c0 += T * 8) {
+        const int r = runs[c0 >> 3];
+        uint2 out;
+        if (r >= 0) {
+          const uint32_t w0 = crow32[r >> 2], w1 = crow32[(r >> 2) + 1], w2 = crow32[(r >> 2) + 2];
+          const uint32_t sh = static_cast<uint32_t>(r & 3) * 8u;
+          out = make_uint2(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh));
+        } else {
+          const uint4 gp = *reinterpret_cast<const uint4*>(gidx + c0);
+          out = make_uint2(pack4(crow[gp.x & 0xffffu], crow[gp.x >> 16], crow[gp.y & 0xffffu], crow[gp.y >> 16]),
+                           pack4(crow[gp.z & 0xffffu], crow[gp.z >> 16], crow[gp.w & 0xffffu], crow[gp.w >> 16]));
+        }
+        *reinterpret_cast<uint2*>(qr + c0) = out;
       }
     }
   }
@@ -1587,7 +1611,9 @@ int launch_act_reg_t(const uint16_t* x, int64_t m, int k, int64_t ldx, const int
   constexpr int kThreads = W == 1 ? 256 : 32 * W;
   auto kern = quant_act_reg_kernel<V, W, kStatic, kGather>;
   const size_t smem =
-      kGather ? static_cast<size_t>(kTeams) * ((k + 8 + 63) & ~63) * 2 + static_cast<size_t>((k_out + 7) & ~7) * 2 : 0;
+      kGather ? static_cast<size_t>(kTeams) * ((k + 8 + 63) & ~63) * 2 + static_cast<size_t>((k_out + 7) & ~7) * 2 +
+                    static_cast<size_t>((k_out + 7) / 8) * 2
+              : 0;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [&] { attr = set_smem_attrs(kern, 64 * 1024); });
@@ -1868,7 +1894,7 @@ int launch_act_rows(bool gathered, const uint16_t* x, int64_t m, int k, int64_t 
                     : launch_act_bulk<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax, q, ldq, s32,
                                                       s64, err, stream);
   static const int reg = getenv("QARVD_K1_REG") ? atoi(getenv("QARVD_K1_REG")) : 2;
-  if (reg > 0 && (!gathered || (reg == 2 && k_out % 4 == 0))) {
+  if (reg > 0 && (!gathered || (reg == 2 && k_out % 8 == 0 && ldq % 8 == 0))) {
     const int st = gathered ? launch_act_reg<kStatic, true>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
                                                             ldq, s32, s64, err, stream)
                             : launch_act_reg<kStatic, false>(x, m, k, ldx, gather, k_out, static_scale, qmax, q,
